@@ -1,0 +1,200 @@
+/*
+ * mfbake.h — C ABI of the B200 normal-bake library (libmfbake.so).
+ *
+ * This is the drop-in boundary for the reference's bake hot path
+ * (meshforge, /root/reference/proj). Every entry point below replaces one
+ * reference interface; the file:line it replaces is cited next to it. The
+ * C++ API in include/meshforge/ (source-compatible with the reference's
+ * proj/include/meshforge) is implemented on top of these calls, and the
+ * Python bindings (paper_2605_26137_b200/capi.py) bind them with ctypes.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no C++ or torch types cross the ABI, and
+ *     no exception ever does.
+ *   - Return value: 0 on success; 1 + (meshforge ErrorCode) for the
+ *     reference's own errors (proj/include/meshforge/core/error.h:8-21), so
+ *     MF_ERR(EmptyMesh) == 1 ...; negative values for device/runtime failures.
+ *     mf_last_error() returns a thread-local message for the last failure.
+ *   - Host buffers are caller-owned and laid out exactly as the reference's
+ *     std::vector<Eigen::...>::data(): Vector3d = 3 x f64, Vector3f = 3 x f32,
+ *     Vector3i = 3 x i32, Vector2d = 2 x f64, ImageU8 = row-major interleaved.
+ *   - Device memory is owned by an mf_ctx (one CUDA stream) or by handles
+ *     created from it. One context is single-threaded; distinct contexts may
+ *     be driven from distinct threads concurrently.
+ *   - "_dev" entry points take device pointers (inputs already resident in
+ *     HBM); everything else takes host pointers and performs the copies.
+ */
+#ifndef MFBAKE_H_
+#define MFBAKE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MF_ABI_VERSION 1
+
+/* ---- status codes ------------------------------------------------------- */
+/* Reference error codes, offset by one (error.h:8-21 enum order). */
+enum {
+  MF_OK = 0,
+  MF_ERR_EMPTY_MESH = 1,        /* ErrorCode::EmptyMesh */
+  MF_ERR_INVALID_GEOMETRY = 2,  /* ErrorCode::InvalidGeometry */
+  MF_ERR_OUT_OF_BOUNDS = 3,
+  MF_ERR_EMPTY_SURFACE = 4,
+  MF_ERR_ALL_HIDDEN = 5,
+  MF_ERR_CHART_FAILURE = 6,
+  MF_ERR_PACK_OVERFLOW = 7,
+  MF_ERR_ATLAS_OVERLAP = 8,     /* ErrorCode::AtlasOverlap */
+  MF_ERR_SHAPE_MISMATCH = 9,    /* ErrorCode::ShapeMismatch */
+  MF_ERR_NOTHING_TO_INPAINT = 10,
+  MF_ERR_EXPORT_MISMATCH = 11,
+  MF_ERR_INVALID_CONFIG = 12,   /* ErrorCode::InvalidConfig */
+  MF_ERR_IO = 13,               /* ErrorCode::IoError */
+  /* Runtime failures (no reference equivalent; the C++ wrapper maps them to
+   * Error(IoError, ...), a non-validation error, CLI exit code 3). */
+  MF_ERR_CUDA = -1,
+  MF_ERR_OUT_OF_MEMORY = -2,
+  MF_ERR_BAD_ARGUMENT = -3,
+  MF_ERR_NO_DEVICE = -4
+};
+
+/* ---- mesh view ---------------------------------------------------------- */
+/* Non-owning view of meshforge::TriangleMesh (core/mesh.h:15-26).
+ * hasNormals() == (normals != NULL && n_vertices > 0);
+ * hasUvs()     == (face_uvs != NULL && n_uvs > 0). */
+typedef struct mf_mesh_view {
+  const double* positions;  /* n_vertices x 3 */
+  int32_t n_vertices;
+  const int32_t* faces;     /* n_faces x 3 */
+  int32_t n_faces;
+  const double* normals;    /* nullable, n_vertices x 3 */
+  const double* uvs;        /* nullable, n_uvs x 2 */
+  int32_t n_uvs;
+  const int32_t* face_uvs;  /* nullable, n_faces x 3 */
+} mf_mesh_view;
+
+/* Per-call measurements filled by the bake entry points (all optional). */
+typedef struct mf_bake_stats {
+  int64_t valid_texels;   /* N_v: texels whose centre lies in a UV triangle */
+  int64_t queries;        /* N_q: valid and reliable texels (closest-point queries) */
+  int64_t hits;           /* queries that found a surface within maxDist */
+  int32_t bvh_nodes;      /* LBVH node count (2F - 1) */
+  int32_t bvh_depth;      /* deepest leaf */
+  /* device time per stage in milliseconds (CUDA events on the ctx stream);
+   * only filled when mf_ctx_set_timing(ctx, 1) was called. */
+  float ms_upload;        /* H2D of the meshes (host entry points only) */
+  float ms_prepare;       /* normals, wedge tangents, reliability, setup */
+  float ms_bvh;           /* LBVH build (Morton, sort, emit, refit, repack) */
+  float ms_raster;        /* G-buffer rasterisation */
+  float ms_transfer;      /* closest-point transfer + RGB8 encode */
+  float ms_dilate;        /* seam dilation */
+  float ms_download;      /* D2H of the result (host entry points only) */
+  float ms_total;
+} mf_bake_stats;
+
+typedef struct mf_ctx mf_ctx;    /* device context: device + stream + scratch */
+typedef struct mf_mesh mf_mesh;  /* device-resident mesh (+ cached derived data) */
+typedef struct mf_bvh mf_bvh;    /* device-resident LBVH over an mf_mesh */
+
+/* ---- library / context -------------------------------------------------- */
+const char* mf_version(void);
+int mf_abi_version(void);
+const char* mf_last_error(void);
+/* stream: a cudaStream_t (nullable: the context creates its own). */
+int mf_ctx_create(int device, void* stream, mf_ctx** out);
+void mf_ctx_destroy(mf_ctx* ctx);
+int mf_ctx_synchronize(mf_ctx* ctx);
+int mf_ctx_set_timing(mf_ctx* ctx, int enabled);
+/* Number of kernels this context has launched since creation. */
+int64_t mf_ctx_launch_count(const mf_ctx* ctx);
+
+/* ---- device-resident meshes -------------------------------------------- */
+/* Validates (validateMesh, core/mesh.cpp:37-48) and uploads. */
+int mf_mesh_upload(mf_ctx* ctx, const mf_mesh_view* mesh, mf_mesh** out);
+void mf_mesh_destroy(mf_mesh* mesh);
+
+/* ---- reference-shaped entry points (host buffers) ----------------------- */
+/* rasterizeGBuffer (bake/gbuffer.h:65, gbuffer.cpp:92-191).
+ * Outputs: pos/nrm/tan/bit res*res*3 f32, valid/reliable res*res u8. */
+int mf_raster_gbuffer(mf_ctx* ctx, const mf_mesh_view* lowpoly, int resolution, float* position,
+                      float* normal, float* tangent, float* bitangent, uint8_t* valid,
+                      uint8_t* reliable);
+
+/* transferNormals (bake/gbuffer.h:72-73, gbuffer.cpp:193-252).
+ * valid == NULL or resolution < 1 means an empty G-buffer (InvalidConfig). */
+int mf_transfer_normals(mf_ctx* ctx, int resolution, const float* position, const float* normal,
+                        const float* tangent, const float* bitangent, const uint8_t* valid,
+                        const uint8_t* reliable, const mf_mesh_view* highpoly,
+                        double bbox_diagonal, double max_distance_fraction, uint8_t* rgb_out);
+
+/* dilateSeams (bake/gbuffer.h:79, gbuffer.cpp:254-322). The map is
+ * width x height x channels; the G-buffer mask is gbuffer_res^2. */
+int mf_dilate_seams(mf_ctx* ctx, int width, int height, int channels, const uint8_t* map_in,
+                    int gbuffer_res, const uint8_t* valid, int radius, uint8_t* map_out);
+
+/* The fused bake: dilateSeams(transferNormals(rasterizeGBuffer(lo,res), hi,
+ * diag, frac), g, radius) (test_bake.cpp:205-206) with the G-buffer kept in
+ * HBM. rgb_out res*res*3 host. dbg_face (nullable, res*res i32): -1 invalid,
+ * -2 unreliable, -3 miss, >=0 hit face. dbg_ts (nullable, res*res*3 f64): the
+ * normalised tangent-space vector before encoding (0 where not encoded). */
+int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_view* highpoly,
+                       int resolution, double bbox_diagonal, double max_distance_fraction,
+                       int radius, uint8_t* rgb_out, int32_t* dbg_face, double* dbg_ts,
+                       mf_bake_stats* stats);
+
+/* Same bake over device-resident meshes into a device buffer, for rows
+ * [row_begin, row_end) of the atlas (0, res for the whole map). rgb_dev holds
+ * (row_end - row_begin) * res * 3 bytes. Rows outside the range are still
+ * rasterised/transferred within the dilation halo so the slab is exact. */
+int mf_bake_normal_map_dev(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int resolution,
+                           double bbox_diagonal, double max_distance_fraction, int radius,
+                           int row_begin, int row_end, uint8_t* rgb_dev, mf_bake_stats* stats);
+
+/* Per-row valid-texel counts (res int64 on the host) from a coverage
+ * pre-pass; used to balance row shards by N_v. */
+int mf_coverage_rows(mf_ctx* ctx, mf_mesh* lowpoly, int resolution, int64_t* row_counts);
+
+/* ---- BVH (spatial/bvh.h:30-69) ----------------------------------------- */
+/* Bvh::Bvh (bvh.cpp:48-61): validates and builds an LBVH on the device.
+ * The mesh must outlive the tree, as in the reference (bvh.h:27). */
+int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out);
+void mf_bvh_destroy(mf_bvh* bvh);
+/* Node count, leaf count, max depth. */
+int mf_bvh_info(const mf_bvh* bvh, int32_t* nodes, int32_t* leaves, int32_t* depth);
+/* Export in the reference's Node layout (bvh.h:32-39): per node
+ * box min/max (6 f64), left, right, first, count (4 i32); plus faceOrder. */
+int mf_bvh_export(mf_bvh* bvh, double* boxes, int32_t* links, int32_t* face_order);
+
+/* Bvh::closestPointWithin (bvh.cpp:151-176); max_distance = +inf gives
+ * closestPoint (bvh.cpp:147-149). Host arrays of n queries. Outputs:
+ * face (-1 = none), dist_sq (+inf when none), point[3], bary[3]. */
+int mf_bvh_closest_within(mf_bvh* bvh, const double* queries, int64_t n, double max_distance,
+                          int32_t* face, double* dist_sq, double* point, double* bary);
+/* Device-pointer variant of the above. */
+int mf_bvh_closest_within_dev(mf_bvh* bvh, const double* queries_dev, int64_t n,
+                              double max_distance, int32_t* face_dev, double* dist_sq_dev,
+                              double* point_dev, double* bary_dev);
+
+/* Bvh::raycastFirst (bvh.cpp:100-140): nearest hit with tmin <= t <= tmax,
+ * ties to the lower face. face -1 = miss (t = +inf). */
+int mf_bvh_raycast_first(mf_bvh* bvh, const double* origins, const double* dirs, int64_t n,
+                         double tmin, double tmax, int32_t* face, double* t, double* u, double* v);
+int mf_bvh_raycast_first_dev(mf_bvh* bvh, const double* origins_dev, const double* dirs_dev,
+                             int64_t n, double tmin, double tmax, int32_t* face_dev,
+                             double* t_dev, double* u_dev, double* v_dev);
+
+/* ---- lowpoly helpers ----------------------------------------------------- */
+/* computeWedgeTangents (bake/tangent.cpp:22-82): frames n_faces x 3 corners x
+ * {tangent, bitangent, normal} x 3 f64 (= std::array<TangentFrame,3>). */
+int mf_wedge_tangents(mf_ctx* ctx, const mf_mesh_view* mesh, double* frames);
+/* computeVertexNormals (core/mesh.cpp:24-35): n_vertices x 3 f64. */
+int mf_vertex_normals(mf_ctx* ctx, const mf_mesh_view* mesh, double* normals);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* MFBAKE_H_ */
