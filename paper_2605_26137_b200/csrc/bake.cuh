@@ -1,0 +1,186 @@
+// bake.cuh — internal interfaces between the libmfbake translation units.
+//
+// HBM layout:
+//   DevMesh   : the reference's arrays verbatim (f64 positions AoS, i32 faces,
+//               optional f64 normals, f64 uv pool, i32 face_uvs).
+//   GBufDev   : the reference G-buffer layout (gbuffer.h:17-30): four f32x3
+//               AoS planes + two u8 planes, row-major, v down; a row slab
+//               [row0, row0 + rows) of the full res x res atlas.
+//   Lbvh      : 64-byte binary nodes with both child boxes stored in the
+//               parent (fp32, rounded outward), child refs >= 0 = node,
+//               < 0 = leaf range of <= kLeafMax Morton-ordered triangles;
+//               80-byte triangle records (f64 vertices + face id) in leaf order.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+struct mf_ctx;
+
+namespace mfb {
+
+// ---------------------------------------------------------------- context
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t side = nullptr;      // second stream: dense-mesh work overlaps the lowpoly work
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool timing = false;
+  int64_t launches = 0;
+  struct Buf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+  };
+  std::unordered_map<std::string, Buf> scratch;
+  std::unordered_map<std::string, Buf> pinned;
+  void* cub_tmp = nullptr;
+  size_t cub_tmp_bytes = 0;
+  void* cub_tmp_side = nullptr;
+  size_t cub_tmp_side_bytes = 0;
+  int64_t bin_capacity = 0;         // raster tile-bin capacity hint (grows on overflow)
+
+  // Grow-only named device scratch (never shrinks; freed with the context).
+  void* buf(const std::string& name, size_t bytes);
+  template <typename T>
+  T* buf(const std::string& name, size_t count) {
+    return static_cast<T*>(buf(name, count * sizeof(T) + 16));
+  }
+  void* host_buf(const std::string& name, size_t bytes);
+  void* cub_temp(size_t bytes, bool side_stream = false);
+  void count_launch(int n = 1) { launches += n; }
+  ~Ctx();
+};
+
+// ---------------------------------------------------------------- meshes
+struct DevMesh {
+  const double* pos = nullptr;   // V x 3
+  const int32_t* faces = nullptr;  // F x 3
+  const double* nrm = nullptr;   // V x 3 or null
+  const double* uvs = nullptr;   // U x 2 or null
+  const int32_t* fuv = nullptr;  // F x 3 or null
+  int nv = 0, nf = 0, nu = 0;
+  bool has_normals() const { return nrm != nullptr && nv > 0; }
+  bool has_uvs() const { return fuv != nullptr && uvs != nullptr && nu > 0; }
+};
+
+// ---------------------------------------------------------------- G-buffer
+struct GBufDev {
+  int res = 0;
+  int row0 = 0, rows = 0;  // stored slab of atlas rows
+  float* pos = nullptr;    // rows*res*3
+  float* nrm = nullptr;
+  float* tan = nullptr;
+  float* bit = nullptr;
+  uint8_t* valid = nullptr;  // rows*res
+  uint8_t* rel = nullptr;
+  int64_t texels() const { return static_cast<int64_t>(rows) * res; }
+};
+
+// ---------------------------------------------------------------- LBVH
+constexpr int kLeafMax = 4;     // reference leaf size (bvh.cpp:13)
+constexpr int kStackMax = 96;   // > max Karras depth over 63-bit Morton + 32-bit index keys
+
+struct alignas(16) BNode {
+  float4 a;  // L.min.x L.min.y L.min.z L.max.x
+  float4 b;  // L.max.y L.max.z R.min.x R.min.y
+  float4 c;  // R.min.z R.max.x R.max.y R.max.z
+  int4 d;    // left ref, right ref, range first, range count
+};
+static_assert(sizeof(BNode) == 64, "node must be one 64-byte line segment");
+
+struct alignas(16) BTri {
+  double v[9];  // the reference's f64 vertices, gathered in leaf order
+  int32_t face;
+  int32_t pad;
+};
+static_assert(sizeof(BTri) == 80, "triangle record is 5 x 16 B");
+
+__host__ __device__ __forceinline__ int32_t leaf_ref(int first, int count) {
+  return ~((first << 3) | count);
+}
+__host__ __device__ __forceinline__ void leaf_decode(int32_t ref, int& first, int& count) {
+  const int32_t r = ~ref;
+  first = r >> 3;
+  count = r & 7;
+}
+
+struct Lbvh {
+  int n_tris = 0;
+  int n_nodes = 0;          // internal nodes (n_tris - 1), root = node 0 when n_tris > 1
+  BNode* nodes = nullptr;   // device
+  BTri* tris = nullptr;     // device, leaf order
+  int32_t root_ref = 0;     // 0 (internal root) or a leaf ref when n_tris <= kLeafMax... see build
+  float root_box[6];        // host copy not needed for traversal; kept for export
+  float* root_box_dev = nullptr;
+  // [min c, max c, max |coord|] as ordered-int doubles (device); the
+  // traversal derives its f64 error slack from max |coord|.
+  const unsigned long long* scene_acc = nullptr;
+};
+
+// Build into buffers owned by `owner` scratch names prefixed with `tag`.
+void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag);
+
+// ---------------------------------------------------------------- lowpoly prep + raster
+// computeVertexNormals (mesh.cpp:24-35) followed, when `renorm`, by the
+// 1e-20 re-normalisation of tangent.cpp:26-31 / gbuffer.cpp:201-206. If the
+// mesh carries normals, they are copied and re-normalised instead.
+void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, bool renorm,
+                    const std::string& tag);
+
+// Everything rasterizeGBuffer needs before the texel loop: wedge frames
+// (tangent.cpp:22-82), reliable flags (gbuffer.cpp:31-83) and per-face
+// raster setup. Returns the device pointer of the face-setup array.
+struct RasterPlan {
+  void* faces = nullptr;   // RasterFace[nf]
+  void* attrs = nullptr;   // AttrFace[nf]
+  int nf = 0;
+  int res = 0;
+};
+void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterPlan& plan);
+// Frames only (for mf_wedge_tangents): F x 3 x {T, B, N} x 3 doubles.
+void wedge_frames(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames_out);
+
+// Tile-binned rasteriser over rows [g.row0, g.row0 + g.rows). Device flags:
+// flags[0] = 1 when a texel is claimed twice (AtlasOverlap); flags[1] = 1
+// when the tile bins overflowed (re-run after setting ctx.bin_capacity to
+// flags[2], the exact bin total). Never synchronises.
+void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPlan& plan,
+                    GBufDev& g, int* flags_dev, int64_t* row_counts_dev);
+
+// ---------------------------------------------------------------- queries
+struct TransferArgs {
+  const GBufDev* g = nullptr;
+  int row_begin = 0, row_end = 0;   // rows to transfer (absolute), within the slab
+  const double* hi_normals = nullptr;
+  const int32_t* hi_faces = nullptr;
+  double max_dist = 0.0;
+  uint8_t* rgb = nullptr;           // raw map rows [row_begin,row_end) x res x 3 (slab-relative to g)
+  int32_t* dbg_face = nullptr;
+  double* dbg_ts = nullptr;
+  unsigned long long* counters = nullptr;  // [valid, queries, hits]
+};
+void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferArgs& a);
+
+void closest_within(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* q, int64_t n,
+                    double max_dist, int32_t* face, double* dist_sq, double* point, double* bary);
+void raycast_first(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* o, const double* d,
+                   int64_t n, double tmin, double tmax, int32_t* face, double* t, double* u,
+                   double* v);
+
+// ---------------------------------------------------------------- dilation
+// dilateSeams over a slab: input map rows [in_row0, in_row0 + in_rows) of a
+// width x height x channels image with the matching valid slab; outputs rows
+// [out_row0, out_row0 + out_rows) (which must lie `radius` rows inside the
+// input slab unless at the image border).
+void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
+                  const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
+                  int radius, uint8_t* map_out, int out_row0, int out_rows);
+
+}  // namespace mfb

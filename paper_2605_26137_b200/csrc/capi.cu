@@ -1,0 +1,874 @@
+// capi.cu — the extern "C" boundary of libmfbake (include/mfbake.h).
+//
+// Orchestration of the fused bake (mf_bake_normal_map[_dev]):
+//   main stream : prepare_lowpoly (normals, wedge frames, reliability, face
+//                 setup) -> raster G-buffer slab            [rasterizeGBuffer]
+//   side stream : dense vertex normals -> LBVH build        [transferNormals
+//                                                            :201-208]
+//   join        : transfer (closest point + encode)         [:215-250]
+//                 -> dilation                               [dilateSeams]
+// Meshes are validated on the device at upload (validateMesh,
+// core/mesh.cpp:37-48, plus face_uvs range); errors are reported in the
+// reference's throw order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "bake.cuh"
+
+namespace mfb {
+
+thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+void* Ctx::buf(const std::string& name, size_t bytes) {
+  Buf& b = scratch[name];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      // the stream may still use the old buffer; free after it drains
+      MFB_CUDA_TRY(cudaStreamSynchronize(stream));
+      if (side) MFB_CUDA_TRY(cudaStreamSynchronize(side));
+      MFB_CUDA_TRY(cudaFree(b.ptr));
+      b.ptr = nullptr;
+    }
+    const size_t want = std::max(bytes, b.bytes + b.bytes / 4);
+    cudaError_t e = cudaMalloc(&b.ptr, want);
+    if (e == cudaErrorMemoryAllocation) {
+      (void)cudaGetLastError();
+      throw std::bad_alloc();
+    }
+    MFB_CUDA_TRY(e);
+    b.bytes = want;
+  }
+  return b.ptr;
+}
+void* Ctx::host_buf(const std::string& name, size_t bytes) {
+  Buf& b = pinned[name];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      MFB_CUDA_TRY(cudaStreamSynchronize(stream));
+      MFB_CUDA_TRY(cudaFreeHost(b.ptr));
+    }
+    MFB_CUDA_TRY(cudaMallocHost(&b.ptr, bytes));
+    b.bytes = bytes;
+  }
+  return b.ptr;
+}
+void* Ctx::cub_temp(size_t bytes, bool side_stream) {
+  void*& p = side_stream ? cub_tmp_side : cub_tmp;
+  size_t& n = side_stream ? cub_tmp_side_bytes : cub_tmp_bytes;
+  if (n < bytes) {
+    if (p) {
+      MFB_CUDA_TRY(cudaStreamSynchronize(stream));
+      if (side) MFB_CUDA_TRY(cudaStreamSynchronize(side));
+      MFB_CUDA_TRY(cudaFree(p));
+    }
+    const size_t want = std::max<size_t>(bytes, 1 << 20);
+    MFB_CUDA_TRY(cudaMalloc(&p, want));
+    n = want;
+  }
+  return p;
+}
+Ctx::~Ctx() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  if (side) cudaStreamSynchronize(side);
+  for (auto& kv : scratch) cudaFree(kv.second.ptr);
+  for (auto& kv : pinned) cudaFreeHost(kv.second.ptr);
+  if (cub_tmp) cudaFree(cub_tmp);
+  if (cub_tmp_side) cudaFree(cub_tmp_side);
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
+  if (side) cudaStreamDestroy(side);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+namespace {
+
+// ---------------------------------------------------------------- validation
+// flags: 1 = non-finite position, 2 = face index out of range,
+//        4 = face_uv index out of range (superset of the reference)
+__global__ void k_validate(const double* __restrict__ pos, int nv, const int32_t* __restrict__ faces, int nf,
+                           const int32_t* __restrict__ fuv, int nu, int* flags) {
+  int f = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < 3ll * nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (!isfinite(pos[i])) f |= 1;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < 3ll * nf;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int v = faces[i];
+    if (v < 0 || v >= nv) f |= 2;
+    if (fuv) {
+      const int u = fuv[i];
+      if (u < 0 || u >= nu) f |= 4;
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flags, f);
+}
+
+}  // namespace
+}  // namespace mfb
+
+using namespace mfb;
+
+struct mf_ctx {
+  Ctx c;
+};
+
+struct mf_mesh {
+  mf_ctx* ctx = nullptr;
+  DevMesh m;
+  void* mem = nullptr;
+  int status = MF_OK;  // validateMesh outcome (reference order)
+  std::string status_msg;
+  bool uv_index_ok = true;
+  bool owns_mem = true;  // false when the arrays live in context scratch
+  ~mf_mesh() {
+    if (mem && owns_mem) cudaFree(mem);
+  }
+};
+
+struct mf_bvh {
+  mf_ctx* ctx = nullptr;
+  mf_mesh* mesh = nullptr;
+  Ctx store;  // owns the tree's device arrays
+  Lbvh bvh;
+  // host export cache
+  bool exported = false;
+  std::vector<double> boxes;
+  std::vector<int32_t> links, order;
+  int32_t leaves = 0, depth = 0;
+};
+
+namespace {
+
+int fail(int code, const std::string& msg) {
+  set_last_error(msg);
+  return code;
+}
+
+template <typename F>
+int guarded(mf_ctx* ctx, F&& fn) {
+  try {
+    if (ctx) MFB_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    return fn();
+  } catch (const ApiError& e) {
+    return fail(e.code, e.msg);
+  } catch (const CudaFailure& e) {
+    return fail(MF_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e.err) + " at " + e.file + ":" +
+                                 std::to_string(e.line) + " (" + e.expr + ")");
+  } catch (const std::bad_alloc&) {
+    return fail(MF_ERR_OUT_OF_MEMORY, "device or host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(MF_ERR_CUDA, e.what());
+  }
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+bool view_has_uvs(const mf_mesh_view* v) { return v->face_uvs && v->uvs && v->n_uvs > 0; }
+
+// Upload + device validation into `mesh`. With a scratch tag the arrays live
+// in the context's grow-only scratch (host-buffer entry points: no
+// cudaMalloc per call); otherwise the mesh owns a fresh allocation.
+void upload_mesh(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* mesh,
+                 const char* scratch_tag = nullptr) {
+  if (!v) throw ApiError(MF_ERR_BAD_ARGUMENT, "mesh view is null");
+  if (v->n_vertices < 0 || v->n_faces < 0 || v->n_uvs < 0) throw ApiError(MF_ERR_BAD_ARGUMENT, "negative size");
+  if ((v->n_vertices > 0 && !v->positions) || (v->n_faces > 0 && !v->faces))
+    throw ApiError(MF_ERR_BAD_ARGUMENT, "null positions/faces with non-zero size");
+  const bool has_n = v->normals && v->n_vertices > 0;
+  const bool has_uv = view_has_uvs(v);
+  const size_t bp = align_up(sizeof(double) * 3 * v->n_vertices, 256);
+  const size_t bf = align_up(sizeof(int32_t) * 3 * v->n_faces, 256);
+  const size_t bn = has_n ? bp : 0;
+  const size_t bu = has_uv ? align_up(sizeof(double) * 2 * v->n_uvs, 256) : 0;
+  const size_t bfu = has_uv ? bf : 0;
+  const size_t total = bp + bf + bn + bu + bfu + 256;
+  if (mesh->mem && mesh->owns_mem) cudaFree(mesh->mem);
+  mesh->mem = nullptr;
+  if (scratch_tag) {
+    mesh->mem = c.buf(scratch_tag, total);
+    mesh->owns_mem = false;
+  } else {
+    cudaError_t e = cudaMalloc(&mesh->mem, total);
+    if (e == cudaErrorMemoryAllocation) {
+      (void)cudaGetLastError();
+      throw std::bad_alloc();
+    }
+    MFB_CUDA_TRY(e);
+    mesh->owns_mem = true;
+  }
+  char* p = static_cast<char*>(mesh->mem);
+  DevMesh m;
+  m.nv = v->n_vertices;
+  m.nf = v->n_faces;
+  m.nu = has_uv ? v->n_uvs : 0;
+  double* dpos = reinterpret_cast<double*>(p);
+  int32_t* dfac = reinterpret_cast<int32_t*>(p + bp);
+  double* dnrm = has_n ? reinterpret_cast<double*>(p + bp + bf) : nullptr;
+  double* duv = has_uv ? reinterpret_cast<double*>(p + bp + bf + bn) : nullptr;
+  int32_t* dfuv = has_uv ? reinterpret_cast<int32_t*>(p + bp + bf + bn + bu) : nullptr;
+  int* flags = reinterpret_cast<int*>(p + total - 256);
+  if (m.nv) MFB_CUDA_TRY(cudaMemcpyAsync(dpos, v->positions, sizeof(double) * 3 * m.nv, cudaMemcpyHostToDevice, s));
+  if (m.nf) MFB_CUDA_TRY(cudaMemcpyAsync(dfac, v->faces, sizeof(int32_t) * 3 * m.nf, cudaMemcpyHostToDevice, s));
+  if (has_n) MFB_CUDA_TRY(cudaMemcpyAsync(dnrm, v->normals, sizeof(double) * 3 * m.nv, cudaMemcpyHostToDevice, s));
+  if (has_uv) {
+    MFB_CUDA_TRY(cudaMemcpyAsync(duv, v->uvs, sizeof(double) * 2 * m.nu, cudaMemcpyHostToDevice, s));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dfuv, v->face_uvs, sizeof(int32_t) * 3 * m.nf, cudaMemcpyHostToDevice, s));
+  }
+  MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int), s));
+  const int64_t work = std::max<int64_t>(3ll * m.nv, 3ll * m.nf);
+  if (work > 0) {
+    const int grid = static_cast<int>(std::min<int64_t>(div_up(work, 256), kNumSMs * 16));
+    k_validate<<<grid, 256, 0, s>>>(dpos, m.nv, dfac, m.nf, dfuv, m.nu, flags);
+    c.count_launch();
+    MFB_CUDA_TRY(cudaGetLastError());
+  }
+  int hf = 0;
+  MFB_CUDA_TRY(cudaMemcpyAsync(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+  MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  m.pos = dpos;
+  m.faces = dfac;
+  m.nrm = dnrm;
+  m.uvs = duv;
+  m.fuv = dfuv;
+  mesh->m = m;
+  mesh->status = MF_OK;
+  mesh->status_msg.clear();
+  if (m.nf == 0) {
+    mesh->status = MF_ERR_EMPTY_MESH;
+    mesh->status_msg = "EmptyMesh: mesh has no faces";
+  } else if (hf & 1) {
+    mesh->status = MF_ERR_INVALID_GEOMETRY;
+    mesh->status_msg = "InvalidGeometry: non-finite vertex coordinate";
+  } else if (hf & 2) {
+    mesh->status = MF_ERR_INVALID_GEOMETRY;
+    mesh->status_msg = "InvalidGeometry: face index out of range";
+  }
+  mesh->uv_index_ok = !(hf & 4);
+}
+
+void check_mesh(const mf_mesh* mesh) {
+  if (mesh->status != MF_OK) throw ApiError(mesh->status, mesh->status_msg);
+}
+
+// rasterizeGBuffer's precondition order (gbuffer.cpp:93-97).
+void check_lowpoly(const mf_mesh* lo, int res) {
+  check_mesh(lo);
+  if (!lo->m.has_uvs()) throw ApiError(MF_ERR_INVALID_GEOMETRY, "InvalidGeometry: atlas rasterization needs a UV-mapped mesh");
+  if (res < 1) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: resolution must be >= 1");
+  if (!lo->uv_index_ok) throw ApiError(MF_ERR_INVALID_GEOMETRY, "InvalidGeometry: face uv index out of range");
+}
+void check_transfer_cfg(double diag, double frac) {
+  if (!(diag > 0.0) || !(frac > 0.0))
+    throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: distance filter must be positive");
+}
+
+struct Timer {
+  Ctx& c;
+  std::vector<cudaEvent_t> ev;
+  explicit Timer(Ctx& cc) : c(cc) {}
+  cudaEvent_t mark(cudaStream_t s) {
+    if (!c.timing) return nullptr;
+    cudaEvent_t e;
+    MFB_CUDA_TRY(cudaEventCreate(&e));
+    MFB_CUDA_TRY(cudaEventRecord(e, s));
+    ev.push_back(e);
+    return e;
+  }
+  static float ms(cudaEvent_t a, cudaEvent_t b) {
+    if (!a || !b) return 0.f;
+    float v = 0.f;
+    cudaEventElapsedTime(&v, a, b);
+    return v;
+  }
+  ~Timer() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+GBufDev gbuf_slab(Ctx& c, int res, int row0, int rows) {
+  GBufDev g;
+  g.res = res;
+  g.row0 = row0;
+  g.rows = rows;
+  const int64_t n = g.texels();
+  g.pos = c.buf<float>("g.pos", 3 * n);
+  g.nrm = c.buf<float>("g.nrm", 3 * n);
+  g.tan = c.buf<float>("g.tan", 3 * n);
+  g.bit = c.buf<float>("g.bit", 3 * n);
+  g.valid = c.buf<uint8_t>("g.valid", n);
+  g.rel = c.buf<uint8_t>("g.rel", n);
+  return g;
+}
+
+// The fused bake over validated device meshes; rows [rb, re) into rgb_out (device).
+void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
+              int rb, int re, uint8_t* rgb_out, int32_t* dbg_face, double* dbg_ts, mf_bake_stats* st,
+              Timer& tm, cudaEvent_t t_begin) {
+  check_lowpoly(lo, res);
+  check_mesh(hi);
+  check_transfer_cfg(diag, frac);
+  if (radius < 0) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilation radius must be >= 0");
+  if (rb < 0 || re > res || rb >= re) throw ApiError(MF_ERR_BAD_ARGUMENT, "row range outside the atlas");
+  cudaStream_t s = c.stream, side = c.side;
+  const int r = radius;
+  const int s0 = std::max(0, rb - r), s1 = std::min(res, re + r);  // raster/transfer slab with dilation halo
+  GBufDev g = gbuf_slab(c, res, s0, s1 - s0);
+  int* flags = c.buf<int>("bake.flags", 4);
+  unsigned long long* counters = c.buf<unsigned long long>("bake.counters", 4);
+  MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
+
+  // fork: dense-mesh work on the side stream
+  MFB_CUDA_TRY(cudaEventRecord(c.fork, s));
+  MFB_CUDA_TRY(cudaStreamWaitEvent(side, c.fork, 0));
+  cudaEvent_t e_side0 = tm.mark(side);
+  double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
+  vertex_normals(c, side, hi->m, hiN, true, "hi");
+  Lbvh bvh;
+  lbvh_build(c, side, hi->m, bvh, "hi.bvh");
+  cudaEvent_t e_side1 = tm.mark(side);
+  MFB_CUDA_TRY(cudaEventRecord(c.join, side));
+
+  // main: lowpoly prep + raster
+  cudaEvent_t e0 = tm.mark(s);
+  RasterPlan plan;
+  prepare_lowpoly(c, s, lo->m, res, plan);
+  cudaEvent_t e1 = tm.mark(s);
+  raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr);
+  cudaEvent_t e2 = tm.mark(s);
+
+  // join, transfer, dilate
+  MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
+  cudaEvent_t e3 = tm.mark(s);
+  uint8_t* raw = c.buf<uint8_t>("bake.raw", 3 * g.texels());
+  TransferArgs ta;
+  ta.g = &g;
+  ta.row_begin = s0;
+  ta.row_end = s1;
+  ta.hi_normals = hiN;
+  ta.hi_faces = hi->m.faces;
+  ta.max_dist = frac * diag;
+  ta.rgb = raw;
+  ta.counters = counters;
+  int32_t* dface = nullptr;
+  double* dts = nullptr;
+  if (dbg_face || dbg_ts) {
+    dface = c.buf<int32_t>("bake.dface", g.texels());
+    dts = c.buf<double>("bake.dts", 3 * g.texels());
+    ta.dbg_face = dface;
+    ta.dbg_ts = dts;
+  }
+  transfer_normals(c, s, bvh, ta);
+  cudaEvent_t e4 = tm.mark(s);
+  dilate_seams(c, s, res, res, 3, raw, g.valid, s0, s1 - s0, r, rgb_out, rb, re - rb);
+  cudaEvent_t e5 = tm.mark(s);
+
+  if (dbg_face)
+    MFB_CUDA_TRY(cudaMemcpyAsync(dbg_face, dface + static_cast<int64_t>(rb - s0) * res,
+                                 sizeof(int32_t) * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
+  if (dbg_ts)
+    MFB_CUDA_TRY(cudaMemcpyAsync(dbg_ts, dts + 3 * static_cast<int64_t>(rb - s0) * res,
+                                 sizeof(double) * 3 * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
+  int hflags[4] = {0, 0, 0, 0};
+  unsigned long long hcnt[4] = {0, 0, 0, 0};
+  MFB_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s));
+  MFB_CUDA_TRY(cudaMemcpyAsync(hcnt, counters, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
+  MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hflags[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+  if (st) {
+    st->valid_texels = static_cast<int64_t>(hcnt[0]);
+    st->queries = static_cast<int64_t>(hcnt[1]);
+    st->hits = static_cast<int64_t>(hcnt[2]);
+    st->bvh_nodes = bvh.n_nodes;
+    st->bvh_depth = 0;
+    if (c.timing) {
+      st->ms_prepare = Timer::ms(e0, e1);
+      st->ms_raster = Timer::ms(e1, e2);
+      st->ms_bvh = Timer::ms(e_side0, e_side1);
+      st->ms_transfer = Timer::ms(e3, e4);
+      st->ms_dilate = Timer::ms(e4, e5);
+      st->ms_total = Timer::ms(t_begin ? t_begin : e0, e5);
+    }
+  }
+}
+
+thread_local std::vector<std::unique_ptr<mf_mesh>> g_tmp_meshes;
+
+}  // namespace
+
+extern "C" {
+
+const char* mf_version(void) { return "mfbake-b200 0.1.0 (sm_100a)"; }
+int mf_abi_version(void) { return MF_ABI_VERSION; }
+const char* mf_last_error(void) { return g_last_error.c_str(); }
+
+int mf_ctx_create(int device, void* stream, mf_ctx** out) {
+  if (!out) return fail(MF_ERR_BAD_ARGUMENT, "out is null");
+  *out = nullptr;
+  return guarded(nullptr, [&]() -> int {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+      (void)cudaGetLastError();
+      return fail(MF_ERR_NO_DEVICE, "no CUDA device available");
+    }
+    if (device < 0 || device >= n) return fail(MF_ERR_NO_DEVICE, "device ordinal out of range");
+    MFB_CUDA_TRY(cudaSetDevice(device));
+    auto ctx = std::make_unique<mf_ctx>();
+    ctx->c.device = device;
+    if (stream) {
+      ctx->c.stream = static_cast<cudaStream_t>(stream);
+    } else {
+      MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+      ctx->c.own_stream = true;
+    }
+    MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
+    MFB_CUDA_TRY(cudaEventCreateWithFlags(&ctx->c.fork, cudaEventDisableTiming));
+    MFB_CUDA_TRY(cudaEventCreateWithFlags(&ctx->c.join, cudaEventDisableTiming));
+    *out = ctx.release();
+    return MF_OK;
+  });
+}
+
+void mf_ctx_destroy(mf_ctx* ctx) { delete ctx; }
+
+int mf_ctx_synchronize(mf_ctx* ctx) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    MFB_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(ctx->c.side));
+    return MF_OK;
+  });
+}
+
+int mf_ctx_set_timing(mf_ctx* ctx, int enabled) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  ctx->c.timing = enabled != 0;
+  return MF_OK;
+}
+
+int64_t mf_ctx_launch_count(const mf_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int mf_mesh_upload(mf_ctx* ctx, const mf_mesh_view* view, mf_mesh** out) {
+  if (!ctx || !out) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded(ctx, [&]() -> int {
+    auto mesh = std::make_unique<mf_mesh>();
+    mesh->ctx = ctx;
+    upload_mesh(ctx->c, ctx->c.stream, view, mesh.get());
+    *out = mesh.release();
+    return MF_OK;
+  });
+}
+
+void mf_mesh_destroy(mf_mesh* mesh) {
+  if (mesh && mesh->ctx) cudaSetDevice(mesh->ctx->c.device);
+  delete mesh;
+}
+
+int mf_raster_gbuffer(mf_ctx* ctx, const mf_mesh_view* lowpoly, int res, float* position, float* normal,
+                      float* tangent, float* bitangent, uint8_t* valid, uint8_t* reliable) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    mf_mesh lo;
+    lo.ctx = ctx;
+    upload_mesh(c, c.stream, lowpoly, &lo, "up.lo");
+    check_lowpoly(&lo, res);
+    if (!position || !normal || !tangent || !bitangent || !valid || !reliable)
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "null G-buffer output");
+    GBufDev g = gbuf_slab(c, res, 0, res);
+    int* flags = c.buf<int>("bake.flags", 4);
+    MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), c.stream));
+    RasterPlan plan;
+    prepare_lowpoly(c, c.stream, lo.m, res, plan);
+    raster_gbuffer(c, c.stream, lo.m, plan, g, flags, nullptr);
+    int hf = 0;
+    MFB_CUDA_TRY(cudaMemcpyAsync(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (hf) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+    const int64_t n = g.texels();
+    MFB_CUDA_TRY(cudaMemcpyAsync(position, g.pos, 12 * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(normal, g.nrm, 12 * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(tangent, g.tan, 12 * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(bitangent, g.bit, 12 * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(valid, g.valid, n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(reliable, g.rel, n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_transfer_normals(mf_ctx* ctx, int res, const float* position, const float* normal, const float* tangent,
+                        const float* bitangent, const uint8_t* valid, const uint8_t* reliable,
+                        const mf_mesh_view* highpoly, double bbox_diagonal, double max_distance_fraction,
+                        uint8_t* rgb_out) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    if (res < 1 || !valid) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: g-buffer is empty");
+    mf_mesh hi;
+    hi.ctx = ctx;
+    upload_mesh(c, c.stream, highpoly, &hi, "up.hi");
+    check_mesh(&hi);
+    check_transfer_cfg(bbox_diagonal, max_distance_fraction);
+    if (!position || !normal || !tangent || !bitangent || !reliable || !rgb_out)
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "null G-buffer input or output");
+    GBufDev g = gbuf_slab(c, res, 0, res);
+    const int64_t n = g.texels();
+    MFB_CUDA_TRY(cudaMemcpyAsync(g.pos, position, 12 * n, cudaMemcpyHostToDevice, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(g.nrm, normal, 12 * n, cudaMemcpyHostToDevice, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(g.tan, tangent, 12 * n, cudaMemcpyHostToDevice, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(g.bit, bitangent, 12 * n, cudaMemcpyHostToDevice, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(g.valid, valid, n, cudaMemcpyHostToDevice, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(g.rel, reliable, n, cudaMemcpyHostToDevice, c.stream));
+    double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi.m.nv));
+    vertex_normals(c, c.stream, hi.m, hiN, true, "hi");
+    Lbvh bvh;
+    lbvh_build(c, c.stream, hi.m, bvh, "hi.bvh");
+    uint8_t* raw = c.buf<uint8_t>("bake.raw", 3 * n);
+    TransferArgs ta;
+    ta.g = &g;
+    ta.row_begin = 0;
+    ta.row_end = res;
+    ta.hi_normals = hiN;
+    ta.hi_faces = hi.m.faces;
+    ta.max_dist = max_distance_fraction * bbox_diagonal;
+    ta.rgb = raw;
+    transfer_normals(c, c.stream, bvh, ta);
+    MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, raw, 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_dilate_seams(mf_ctx* ctx, int width, int height, int channels, const uint8_t* map_in, int gres,
+                    const uint8_t* valid, int radius, uint8_t* map_out) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    if (radius < 0) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilation radius must be >= 0");
+    if (width != gres || height != gres)
+      throw ApiError(MF_ERR_SHAPE_MISMATCH, "ShapeMismatch: map and g-buffer resolutions differ");
+    if (channels < 1 || !map_in || !map_out || (gres > 0 && !valid))
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "bad map arguments");
+    const int64_t n = static_cast<int64_t>(width) * height;
+    if (n == 0) return MF_OK;
+    uint8_t* din = c.buf<uint8_t>("dil.in", n * channels);
+    uint8_t* dout = c.buf<uint8_t>("dil.out", n * channels);
+    uint8_t* dval = c.buf<uint8_t>("dil.valid", n);
+    MFB_CUDA_TRY(cudaMemcpyAsync(din, map_in, n * channels, cudaMemcpyHostToDevice, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dval, valid, n, cudaMemcpyHostToDevice, c.stream));
+    dilate_seams(c, c.stream, width, height, channels, din, dval, 0, height, radius, dout, 0, height);
+    MFB_CUDA_TRY(cudaMemcpyAsync(map_out, dout, n * channels, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_view* highpoly, int res,
+                       double bbox_diagonal, double max_distance_fraction, int radius, uint8_t* rgb_out,
+                       int32_t* dbg_face, double* dbg_ts, mf_bake_stats* stats) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    Timer tm(c);
+    cudaEvent_t t0 = tm.mark(c.stream);
+    mf_mesh lo, hi;
+    lo.ctx = hi.ctx = ctx;
+    upload_mesh(c, c.stream, lowpoly, &lo, "up.lo");
+    // reference order: lowpoly checks precede the highpoly's (gbuffer.cpp:93-97 then :195-199)
+    check_lowpoly(&lo, res);
+    upload_mesh(c, c.stream, highpoly, &hi, "up.hi");
+    cudaEvent_t t1 = tm.mark(c.stream);
+    if (!rgb_out) throw ApiError(MF_ERR_BAD_ARGUMENT, "rgb_out is null");
+    uint8_t* drgb = c.buf<uint8_t>("bake.rgb", 3 * static_cast<int64_t>(res) * res);
+    mf_bake_stats local{};
+    bake_dev(c, &lo, &hi, res, bbox_diagonal, max_distance_fraction, radius, 0, res, drgb, dbg_face, dbg_ts,
+             &local, tm, t1);
+    cudaEvent_t t2 = tm.mark(c.stream);
+    MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, c.stream));
+    cudaEvent_t t3 = tm.mark(c.stream);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (stats) {
+      *stats = local;
+      if (c.timing) {
+        stats->ms_upload = Timer::ms(t0, t1);
+        stats->ms_download = Timer::ms(t2, t3);
+        stats->ms_total = Timer::ms(t0, t3);
+      }
+    }
+    return MF_OK;
+  });
+}
+
+int mf_bake_normal_map_dev(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int res, double bbox_diagonal,
+                           double max_distance_fraction, int radius, int row_begin, int row_end, uint8_t* rgb_dev,
+                           mf_bake_stats* stats) {
+  if (!ctx || !lowpoly || !highpoly || !rgb_dev) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Timer tm(ctx->c);
+    mf_bake_stats local{};
+    bake_dev(ctx->c, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius, row_begin, row_end,
+             rgb_dev, nullptr, nullptr, &local, tm, nullptr);
+    if (stats) *stats = local;
+    return MF_OK;
+  });
+}
+
+int mf_coverage_rows(mf_ctx* ctx, mf_mesh* lowpoly, int res, int64_t* row_counts) {
+  if (!ctx || !lowpoly || !row_counts) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    check_lowpoly(lowpoly, res);
+    GBufDev g = gbuf_slab(c, res, 0, res);
+    int* flags = c.buf<int>("bake.flags", 4);
+    int64_t* rows = c.buf<int64_t>("cov.rows", res);
+    MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), c.stream));
+    RasterPlan plan;
+    prepare_lowpoly(c, c.stream, lowpoly->m, res, plan);
+    raster_gbuffer(c, c.stream, lowpoly->m, plan, g, flags, rows);
+    MFB_CUDA_TRY(cudaMemcpyAsync(row_counts, rows, sizeof(int64_t) * res, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+// ---------------------------------------------------------------- BVH API
+int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
+  if (!ctx || !mesh || !out) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded(ctx, [&]() -> int {
+    check_mesh(mesh);  // Bvh::Bvh calls validateMesh (bvh.cpp:49)
+    auto b = std::make_unique<mf_bvh>();
+    b->ctx = ctx;
+    b->mesh = mesh;
+    b->store.device = ctx->c.device;
+    b->store.stream = ctx->c.stream;  // only used to order frees
+    lbvh_build(ctx->c, ctx->c.stream, mesh->m, b->bvh, "bvh");
+    // move the persistent arrays out of the context scratch into the handle
+    const int nn = std::max(b->bvh.n_nodes, 1);
+    BNode* nodes = b->store.buf<BNode>("nodes", nn);
+    BTri* tris = b->store.buf<BTri>("tris", b->bvh.n_tris);
+    auto* acc = b->store.buf<unsigned long long>("acc", 8);
+    MFB_CUDA_TRY(cudaMemcpyAsync(nodes, b->bvh.nodes, sizeof(BNode) * nn, cudaMemcpyDeviceToDevice, ctx->c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(tris, b->bvh.tris, sizeof(BTri) * b->bvh.n_tris, cudaMemcpyDeviceToDevice, ctx->c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(acc, b->bvh.scene_acc, sizeof(unsigned long long) * 8, cudaMemcpyDeviceToDevice,
+                                 ctx->c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(b->bvh.root_box, b->bvh.root_box_dev, sizeof(float) * 6, cudaMemcpyDeviceToHost,
+                                 ctx->c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
+    b->bvh.nodes = nodes;
+    b->bvh.tris = tris;
+    b->bvh.scene_acc = acc;
+    b->bvh.root_box_dev = nullptr;
+    b->store.own_stream = false;
+    *out = b.release();
+    return MF_OK;
+  });
+}
+
+void mf_bvh_destroy(mf_bvh* bvh) {
+  if (bvh && bvh->ctx) cudaSetDevice(bvh->ctx->c.device);
+  if (bvh) bvh->store.stream = nullptr;
+  delete bvh;
+}
+
+namespace {
+void export_bvh(mf_bvh* b) {
+  if (b->exported) return;
+  const Lbvh& t = b->bvh;
+  std::vector<BNode> nodes(std::max(t.n_nodes, 1));
+  std::vector<BTri> tris(t.n_tris);
+  if (t.n_nodes > 0)
+    MFB_CUDA_TRY(cudaMemcpy(nodes.data(), t.nodes, sizeof(BNode) * t.n_nodes, cudaMemcpyDeviceToHost));
+  MFB_CUDA_TRY(cudaMemcpy(tris.data(), t.tris, sizeof(BTri) * t.n_tris, cudaMemcpyDeviceToHost));
+  b->order.resize(t.n_tris);
+  for (int i = 0; i < t.n_tris; ++i) b->order[i] = tris[i].face;
+  // DFS pre-order (root = 0), mirroring the reference's node numbering (bvh.cpp:65-66)
+  struct Item {
+    int32_t ref;
+    float box[6];
+    int parent, side, depth;
+  };
+  std::vector<Item> stack;
+  Item root{t.root_ref, {t.root_box[0], t.root_box[1], t.root_box[2], t.root_box[3], t.root_box[4], t.root_box[5]},
+            -1, 0, 0};
+  stack.push_back(root);
+  b->boxes.clear();
+  b->links.clear();
+  b->leaves = 0;
+  b->depth = 0;
+  while (!stack.empty()) {
+    Item it = stack.back();
+    stack.pop_back();
+    const int idx = static_cast<int>(b->links.size() / 4);
+    for (int k = 0; k < 6; ++k) b->boxes.push_back(it.box[k]);
+    b->links.insert(b->links.end(), {-1, -1, 0, 0});
+    if (it.parent >= 0) b->links[4 * it.parent + it.side] = idx;
+    b->depth = std::max(b->depth, it.depth);
+    if (it.ref < 0) {
+      int first, count;
+      leaf_decode(it.ref, first, count);
+      b->links[4 * idx + 2] = first;
+      b->links[4 * idx + 3] = count;
+      ++b->leaves;
+      continue;
+    }
+    const BNode& n = nodes[it.ref];
+    const float* f = reinterpret_cast<const float*>(&n);
+    Item l{n.d.x, {f[0], f[1], f[2], f[3], f[4], f[5]}, idx, 0, it.depth + 1};
+    Item r{n.d.y, {f[6], f[7], f[8], f[9], f[10], f[11]}, idx, 1, it.depth + 1};
+    stack.push_back(r);  // left is visited (and numbered) first
+    stack.push_back(l);
+  }
+  b->exported = true;
+}
+}  // namespace
+
+int mf_bvh_info(const mf_bvh* bvh, int32_t* nodes, int32_t* leaves, int32_t* depth) {
+  if (!bvh) return fail(MF_ERR_BAD_ARGUMENT, "bvh is null");
+  mf_bvh* b = const_cast<mf_bvh*>(bvh);
+  return guarded(b->ctx, [&]() -> int {
+    export_bvh(b);
+    if (nodes) *nodes = static_cast<int32_t>(b->links.size() / 4);
+    if (leaves) *leaves = b->leaves;
+    if (depth) *depth = b->depth;
+    return MF_OK;
+  });
+}
+
+int mf_bvh_export(mf_bvh* bvh, double* boxes, int32_t* links, int32_t* face_order) {
+  if (!bvh) return fail(MF_ERR_BAD_ARGUMENT, "bvh is null");
+  return guarded(bvh->ctx, [&]() -> int {
+    export_bvh(bvh);
+    if (boxes) std::memcpy(boxes, bvh->boxes.data(), sizeof(double) * bvh->boxes.size());
+    if (links) std::memcpy(links, bvh->links.data(), sizeof(int32_t) * bvh->links.size());
+    if (face_order) std::memcpy(face_order, bvh->order.data(), sizeof(int32_t) * bvh->order.size());
+    return MF_OK;
+  });
+}
+
+int mf_bvh_closest_within_dev(mf_bvh* bvh, const double* q, int64_t n, double max_distance, int32_t* face,
+                              double* dist_sq, double* point, double* bary) {
+  if (!bvh || (n > 0 && (!q || !face || !dist_sq))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(bvh->ctx, [&]() -> int {
+    Ctx& c = bvh->ctx->c;
+    closest_within(c, c.stream, bvh->bvh, q, n, max_distance, face, dist_sq, point, bary);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_bvh_closest_within(mf_bvh* bvh, const double* q, int64_t n, double max_distance, int32_t* face,
+                          double* dist_sq, double* point, double* bary) {
+  if (!bvh || (n > 0 && (!q || !face || !dist_sq))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(bvh->ctx, [&]() -> int {
+    if (n <= 0) return MF_OK;
+    Ctx& c = bvh->ctx->c;
+    double* dq = c.buf<double>("cp.q", 3 * n);
+    int32_t* df = c.buf<int32_t>("cp.f", n);
+    double* dd = c.buf<double>("cp.d", n);
+    double* dp = c.buf<double>("cp.p", 3 * n);
+    double* db = c.buf<double>("cp.b", 3 * n);
+    MFB_CUDA_TRY(cudaMemcpyAsync(dq, q, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    closest_within(c, c.stream, bvh->bvh, dq, n, max_distance, df, dd, dp, db);
+    MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dist_sq, dd, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    if (point) MFB_CUDA_TRY(cudaMemcpyAsync(point, dp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    if (bary) MFB_CUDA_TRY(cudaMemcpyAsync(bary, db, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_bvh_raycast_first_dev(mf_bvh* bvh, const double* o, const double* d, int64_t n, double tmin, double tmax,
+                             int32_t* face, double* t, double* u, double* v) {
+  if (!bvh || (n > 0 && (!o || !d || !face || !t || !u || !v))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(bvh->ctx, [&]() -> int {
+    Ctx& c = bvh->ctx->c;
+    raycast_first(c, c.stream, bvh->bvh, o, d, n, tmin, tmax, face, t, u, v);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_bvh_raycast_first(mf_bvh* bvh, const double* o, const double* d, int64_t n, double tmin, double tmax,
+                         int32_t* face, double* t, double* u, double* v) {
+  if (!bvh || (n > 0 && (!o || !d || !face || !t || !u || !v))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(bvh->ctx, [&]() -> int {
+    if (n <= 0) return MF_OK;
+    Ctx& c = bvh->ctx->c;
+    double* dO = c.buf<double>("rc.o", 3 * n);
+    double* dD = c.buf<double>("rc.d", 3 * n);
+    int32_t* df = c.buf<int32_t>("rc.f", n);
+    double* dt = c.buf<double>("rc.t", n);
+    double* du = c.buf<double>("rc.u", n);
+    double* dv = c.buf<double>("rc.v", n);
+    MFB_CUDA_TRY(cudaMemcpyAsync(dO, o, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dD, d, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    raycast_first(c, c.stream, bvh->bvh, dO, dD, n, tmin, tmax, df, dt, du, dv);
+    MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(t, dt, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(u, du, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(v, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_wedge_tangents(mf_ctx* ctx, const mf_mesh_view* mesh, double* frames) {
+  if (!ctx || !frames) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    mf_mesh m;
+    m.ctx = ctx;
+    upload_mesh(c, c.stream, mesh, &m, "up.m");
+    // computeWedgeTangents only requires UVs (tangent.cpp:23-24); indices are
+    // used as given, so a bad mesh is reported as the reference would crash on it.
+    if (!m.m.has_uvs()) throw ApiError(MF_ERR_INVALID_GEOMETRY, "InvalidGeometry: tangent frames require a UV-mapped mesh");
+    check_mesh(&m);
+    if (!m.uv_index_ok) throw ApiError(MF_ERR_INVALID_GEOMETRY, "InvalidGeometry: face uv index out of range");
+    double* d = c.buf<double>("wt.frames", 27 * static_cast<size_t>(m.m.nf));
+    wedge_frames(c, c.stream, m.m, d);
+    MFB_CUDA_TRY(cudaMemcpyAsync(frames, d, sizeof(double) * 27 * m.m.nf, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_vertex_normals(mf_ctx* ctx, const mf_mesh_view* mesh, double* normals) {
+  if (!ctx || !normals) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    mf_mesh m;
+    m.ctx = ctx;
+    upload_mesh(c, c.stream, mesh, &m, "up.m");
+    if (m.m.nf > 0) check_mesh(&m);
+    DevMesh dm = m.m;
+    dm.nrm = nullptr;  // computeVertexNormals ignores stored normals
+    double* d = c.buf<double>("vn.out", 3 * static_cast<size_t>(std::max(dm.nv, 1)));
+    if (dm.nv > 0) {
+      if (dm.nf > 0) {
+        vertex_normals(c, c.stream, dm, d, false, "vn");
+      } else {
+        MFB_CUDA_TRY(cudaMemsetAsync(d, 0, sizeof(double) * 3 * dm.nv, c.stream));
+      }
+      MFB_CUDA_TRY(cudaMemcpyAsync(normals, d, sizeof(double) * 3 * dm.nv, cudaMemcpyDeviceToHost, c.stream));
+    }
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+// dilate.cu — dilateSeams (bake/gbuffer.cpp:254-322) on the device.
+//
+// The reference runs `radius` double-buffered 8-neighbour chamfer passes over
+// the whole atlas, each texel keeping (source, dist2) with dist2 ==
+// |texel - source|^2 exactly, and finally copies the input map at the source.
+// Bit-exact restatement:
+//   * state is the source offset (dx, dy) relative to the texel; dist2 is
+//     recomputed exactly from it (int32 suffices while |offset| <= radius);
+//   * neighbours are scanned in the reference's (dy, dx) raster order and a
+//     candidate wins only if strictly nearer, so ties keep the current source,
+//     then the first neighbour in scan order (gbuffer.cpp:288-303).
+// k_dilate_fused runs all passes for one 32x8 tile inside shared memory over
+// a (32+2r) x (8+2r) halo region (one launch, ~1.6x halo read overhead at
+// r = 4); k_dilate_pass is the multi-launch global fallback for large radii.
+#include "bake.cuh"
+
+namespace mfb {
+namespace {
+
+constexpr int kTW = 32, kTH = 8;
+constexpr int16_t kNone = -32768;  // "no source" marker in the x offset
+
+__device__ __forceinline__ int sq(int v) { return v * v; }
+
+// One chamfer step for a texel at region coords (cx, cy) of a rw x rh region.
+// ox/oy hold source offsets; ox == kNone means no source. Region cells
+// outside the image are never sources; region cells outside the region are
+// unknown and simply skipped (only affects cells within `pass` of the edge).
+__device__ __forceinline__ void chamfer_step(const int16_t* __restrict__ ox, const int16_t* __restrict__ oy,
+                                             int rw, int rh, int cx, int cy, int gx, int gy, int width,
+                                             int height, int16_t& nox, int16_t& noy) {
+  const int self = cy * rw + cx;
+  const int16_t sx = ox[self], sy = oy[self];
+  nox = sx;
+  noy = sy;
+  if (sx != kNone && sx == 0 && sy == 0) return;  // valid texel: dist2 == 0, skipped
+  long long best = sx == kNone ? 0x7fffffffffffffffll : static_cast<long long>(sq(sx) + sq(sy));
+#pragma unroll
+  for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
+    for (int dx = -1; dx <= 1; ++dx) {
+      if (dx == 0 && dy == 0) continue;
+      const int nx = gx + dx, ny = gy + dy;
+      if (nx < 0 || nx >= width || ny < 0 || ny >= height) continue;
+      const int rx = cx + dx, ry = cy + dy;
+      if (rx < 0 || rx >= rw || ry < 0 || ry >= rh) continue;
+      const int n = ry * rw + rx;
+      const int16_t nsx = ox[n];
+      if (nsx == kNone) continue;
+      // candidate source = neighbour + its offset; offset from this texel:
+      const int cxo = dx + nsx, cyo = dy + oy[n];
+      const long long d = static_cast<long long>(sq(cxo) + sq(cyo));
+      if (d < best) {
+        best = d;
+        nox = static_cast<int16_t>(cxo);
+        noy = static_cast<int16_t>(cyo);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int channels,
+                                                      const uint8_t* __restrict__ map_in,
+                                                      const uint8_t* __restrict__ valid, int in_row0,
+                                                      int in_rows, int radius,
+                                                      uint8_t* __restrict__ map_out, int out_row0,
+                                                      int out_rows) {
+  extern __shared__ int16_t sm[];
+  const int rw = kTW + 2 * radius, rh = kTH + 2 * radius, cells = rw * rh;
+  int16_t* ox0 = sm;
+  int16_t* oy0 = sm + cells;
+  int16_t* ox1 = sm + 2 * cells;
+  int16_t* oy1 = sm + 3 * cells;
+  const int tiles_x = (width + kTW - 1) / kTW;
+  const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+  const int x0 = tx * kTW - radius;            // region origin (absolute)
+  const int y0 = out_row0 + ty * kTH - radius;
+  const int in_end = in_row0 + in_rows;
+  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+    const int gx = x0 + c % rw, gy = y0 + c / rw;
+    int16_t v = kNone;
+    if (gx >= 0 && gx < width && gy >= in_row0 && gy < in_end && gy < height &&
+        valid[static_cast<int64_t>(gy - in_row0) * width + gx])
+      v = 0;
+    ox0[c] = v;
+    oy0[c] = 0;
+  }
+  __syncthreads();
+  for (int pass = 0; pass < radius; ++pass) {
+    for (int c = threadIdx.x; c < cells; c += blockDim.x) {
+      const int cx = c % rw, cy = c / rw;
+      int16_t a, b;
+      chamfer_step(ox0, oy0, rw, rh, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
+      ox1[c] = a;
+      oy1[c] = b;
+    }
+    __syncthreads();
+    int16_t* t = ox0;
+    ox0 = ox1;
+    ox1 = t;
+    t = oy0;
+    oy0 = oy1;
+    oy1 = t;
+  }
+  // output: tile interior
+  for (int c = threadIdx.x; c < kTW * kTH; c += blockDim.x) {
+    const int lx = c % kTW, ly = c / kTW;
+    const int gx = tx * kTW + lx, gy = out_row0 + ty * kTH + ly;
+    if (gx >= width || gy >= out_row0 + out_rows) continue;
+    const int rc = (ly + radius) * rw + (lx + radius);
+    const int16_t sx = ox0[rc], sy = oy0[rc];
+    int srcx = gx, srcy = gy;
+    const bool is_valid = sx == 0 && sy == 0;
+    if (sx != kNone && !is_valid) {
+      srcx = gx + sx;
+      srcy = gy + sy;
+    }
+    const uint8_t* src = map_in + (static_cast<int64_t>(srcy - in_row0) * width + srcx) * channels;
+    uint8_t* dst = map_out + (static_cast<int64_t>(gy - out_row0) * width + gx) * channels;
+    for (int ch = 0; ch < channels; ++ch) dst[ch] = src[ch];
+  }
+}
+
+// ---- global multi-pass fallback (large radius) ----------------------------
+__global__ void k_dilate_init(int width, int rows, const uint8_t* __restrict__ valid,
+                              int32_t* __restrict__ sx, int32_t* __restrict__ sy,
+                              long long* __restrict__ d2, int in_row0) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(width) * rows) return;
+  const bool v = valid[i] != 0;
+  sx[i] = v ? static_cast<int32_t>(i % width) : 0;
+  sy[i] = v ? static_cast<int32_t>(i / width) + in_row0 : 0;
+  d2[i] = v ? 0 : 0x7fffffffffffffffll;
+}
+
+__global__ void k_dilate_pass(int width, int height, int rows, int in_row0,
+                              const int32_t* __restrict__ sx, const int32_t* __restrict__ sy,
+                              const long long* __restrict__ d2, int32_t* __restrict__ nsx,
+                              int32_t* __restrict__ nsy, long long* __restrict__ nd2) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(width) * rows) return;
+  const int x = static_cast<int>(i % width), ly = static_cast<int>(i / width), y = ly + in_row0;
+  long long best = d2[i];
+  int32_t bx = sx[i], by = sy[i];
+  if (best != 0) {
+    for (int dy = -1; dy <= 1; ++dy)
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (dx == 0 && dy == 0) continue;
+        const int nx = x + dx, ny = y + dy;
+        if (nx < 0 || nx >= width || ny < 0 || ny >= height) continue;
+        if (ny < in_row0 || ny >= in_row0 + rows) continue;
+        const int64_t n = static_cast<int64_t>(ny - in_row0) * width + nx;
+        if (d2[n] == 0x7fffffffffffffffll) continue;
+        const long long ddx = x - sx[n], ddy = y - sy[n];
+        const long long d = ddx * ddx + ddy * ddy;
+        if (d < best) {
+          best = d;
+          bx = sx[n];
+          by = sy[n];
+        }
+      }
+  }
+  nd2[i] = best;
+  nsx[i] = bx;
+  nsy[i] = by;
+}
+
+__global__ void k_dilate_copy(int width, int channels, const uint8_t* __restrict__ map_in,
+                              const uint8_t* __restrict__ valid, int in_row0,
+                              const int32_t* __restrict__ sx, const int32_t* __restrict__ sy,
+                              const long long* __restrict__ d2, uint8_t* __restrict__ map_out,
+                              int out_row0, int out_rows) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<int64_t>(width) * out_rows) return;
+  const int x = static_cast<int>(i % width), y = static_cast<int>(i / width) + out_row0;
+  const int64_t si = static_cast<int64_t>(y - in_row0) * width + x;
+  int64_t src = si;
+  if (!valid[si] && d2[si] != 0x7fffffffffffffffll)
+    src = static_cast<int64_t>(sy[si] - in_row0) * width + sx[si];
+  for (int c = 0; c < channels; ++c) map_out[i * channels + c] = map_in[src * channels + c];
+}
+
+}  // namespace
+
+void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
+                  const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
+                  int radius, uint8_t* map_out, int out_row0, int out_rows) {
+  if (out_rows <= 0 || width <= 0) return;
+  const int64_t out_bytes = static_cast<int64_t>(width) * out_rows * channels;
+  if (radius == 0) {
+    MFB_CUDA_TRY(cudaMemcpyAsync(map_out,
+                                 map_in + static_cast<int64_t>(out_row0 - in_row0) * width * channels,
+                                 out_bytes, cudaMemcpyDeviceToDevice, s));
+    return;
+  }
+  const size_t smem = static_cast<size_t>(4) * (kTW + 2 * radius) * (kTH + 2 * radius) * sizeof(int16_t);
+  if (radius <= 32 && smem <= 200 * 1024) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      MFB_CUDA_TRY(cudaFuncSetAttribute(k_dilate_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024));
+      attr_set = true;
+    }
+    const int tiles = ((width + kTW - 1) / kTW) * ((out_rows + kTH - 1) / kTH);
+    k_dilate_fused<<<tiles, 256, smem, s>>>(width, height, channels, map_in, valid, in_row0, in_rows,
+                                            radius, map_out, out_row0, out_rows);
+    ctx.count_launch();
+    MFB_CUDA_TRY(cudaGetLastError());
+    return;
+  }
+  const int64_t n = static_cast<int64_t>(width) * in_rows;
+  auto* sx = ctx.buf<int32_t>("dil.sx", n);
+  auto* sy = ctx.buf<int32_t>("dil.sy", n);
+  auto* d2 = ctx.buf<long long>("dil.d2", n);
+  auto* nsx = ctx.buf<int32_t>("dil.nsx", n);
+  auto* nsy = ctx.buf<int32_t>("dil.nsy", n);
+  auto* nd2 = ctx.buf<long long>("dil.nd2", n);
+  const int T = 256;
+  k_dilate_init<<<div_up(n, T), T, 0, s>>>(width, in_rows, valid, sx, sy, d2, in_row0);
+  for (int p = 0; p < radius; ++p) {
+    k_dilate_pass<<<div_up(n, T), T, 0, s>>>(width, height, in_rows, in_row0, sx, sy, d2, nsx, nsy, nd2);
+    std::swap(sx, nsx);
+    std::swap(sy, nsy);
+    std::swap(d2, nd2);
+  }
+  k_dilate_copy<<<div_up(static_cast<int64_t>(width) * out_rows, T), T, 0, s>>>(
+      width, channels, map_in, valid, in_row0, sx, sy, d2, map_out, out_row0, out_rows);
+  ctx.count_launch(radius + 2);
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+}  // namespace mfb

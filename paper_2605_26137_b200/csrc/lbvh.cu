@@ -1,0 +1,292 @@
+// lbvh.cu — GPU LBVH over the dense mesh (replaces Bvh::Bvh/build,
+// spatial/bvh.cpp:48-98).
+//
+// Pipeline (one stream, 5 launches + one CUB radix sort):
+//   1. bounds      : centroid bounds + max |coordinate| (ordered-int atomics)
+//   2. morton      : 63-bit Morton key of each face centroid
+//   3. sort        : CUB onesweep radix sort of (key, face) pairs
+//   4. emit        : Karras 2012 hierarchy emission; subtrees covering
+//                    <= kLeafMax primitives become leaf ranges (the
+//                    reference's leaf size, bvh.cpp:13)
+//   5. repack+refit: gather each primitive's f64 vertices into Morton order
+//                    (BTri) and propagate fp32 boxes, rounded outward, up the
+//                    tree; each parent stores both child boxes (64-B nodes).
+// Query results do not depend on the tree shape: the reference
+// answer is argmin over faces of (distSq, face), which any conservative tree
+// reproduces exactly.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "bake.cuh"
+
+namespace mfb {
+namespace {
+
+__device__ __forceinline__ unsigned long long ordered_bits(double v) {
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ __forceinline__ double from_ordered(unsigned long long b) {
+  b = (b & 0x8000000000000000ull) ? (b & ~0x8000000000000000ull) : ~b;
+#ifdef __CUDA_ARCH__
+  return __longlong_as_double(static_cast<long long>(b));
+#else
+  double d;
+  memcpy(&d, &b, 8);
+  return d;
+#endif
+}
+
+// acc[0..2] = min centroid, acc[3..5] = max centroid, acc[6] = max |vertex coord|
+__global__ void k_bounds(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
+                         int nv, unsigned long long* acc) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  double amax = 0.0;
+  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
+    const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double ck = ((pos[3 * a + k] + pos[3 * b + k]) + pos[3 * c + k]) / 3.0;
+      mn[k] = fmin(mn[k], ck);
+      mx[k] = fmax(mx[k], ck);
+    }
+  }
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    amax = fmax(amax, fmax(fabs(pos[3 * v]), fmax(fabs(pos[3 * v + 1]), fabs(pos[3 * v + 2]))));
+  }
+  // warp reduce then one atomic per warp
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      mn[k] = fmin(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+      mx[k] = fmax(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], off));
+    }
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      atomicMin(&acc[k], ordered_bits(mn[k]));
+      atomicMax(&acc[3 + k], ordered_bits(mx[k]));
+    }
+    atomicMax(&acc[6], ordered_bits(amax));
+  }
+}
+
+__device__ __forceinline__ uint64_t spread21(uint32_t v) {
+  uint64_t x = v & 0x1fffffull;
+  x = (x | (x << 32)) & 0x1f00000000ffffull;
+  x = (x | (x << 16)) & 0x1f0000ff0000ffull;
+  x = (x | (x << 8)) & 0x100f00f00f00f00full;
+  x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+  x = (x | (x << 2)) & 0x1249249249249249ull;
+  return x;
+}
+
+__global__ void k_morton(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
+                         const unsigned long long* __restrict__ acc, uint64_t* __restrict__ keys,
+                         uint32_t* __restrict__ vals) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  double lo[3], inv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    lo[k] = from_ordered(acc[k]);
+    const double ext = from_ordered(acc[3 + k]) - lo[k];
+    inv[k] = ext > 0.0 ? 2097151.0 / ext : 0.0;
+  }
+  const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+  uint32_t q[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double ck = ((pos[3 * a + k] + pos[3 * b + k]) + pos[3 * c + k]) / 3.0;
+    double t = (ck - lo[k]) * inv[k];
+    t = fmin(fmax(t, 0.0), 2097151.0);
+    q[k] = static_cast<uint32_t>(t);
+  }
+  keys[f] = (spread21(q[0]) << 2) | (spread21(q[1]) << 1) | spread21(q[2]);
+  vals[f] = static_cast<uint32_t>(f);
+}
+
+// Karras delta over augmented keys (key, index): -1 outside [0, n).
+__device__ __forceinline__ int kdelta(const uint64_t* __restrict__ k, int n, int i, int j) {
+  if (j < 0 || j >= n) return -1;
+  const uint64_t a = k[i], b = k[j];
+  if (a == b) return 64 + __clz(static_cast<uint32_t>(i ^ j));
+  return __clzll(static_cast<long long>(a ^ b));
+}
+
+// parent links: (parent << 1) | side; prim_parent for primitives, node_parent for internals.
+__global__ void k_emit(const uint64_t* __restrict__ keys, int n, BNode* __restrict__ nodes,
+                       int32_t* __restrict__ prim_parent, int32_t* __restrict__ node_parent) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  const int d = (kdelta(keys, n, i, i + 1) - kdelta(keys, n, i, i - 1)) > 0 ? 1 : -1;
+  const int dmin = kdelta(keys, n, i, i - d);
+  int lmax = 2;
+  while (kdelta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
+  int l = 0;
+  for (int t = lmax >> 1; t >= 1; t >>= 1)
+    if (kdelta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+  const int j = i + l * d;
+  const int dnode = kdelta(keys, n, i, j);
+  int s = 0, t = l;
+  do {
+    t = (t + 1) >> 1;
+    if (kdelta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+  } while (t > 1);
+  const int gamma = i + s * d + min(d, 0);
+  const int first = min(i, j), last = max(i, j);
+  const int cl = gamma - first + 1, cr = last - gamma;
+  int4 dd;
+  dd.x = cl <= kLeafMax ? leaf_ref(first, cl) : gamma;
+  dd.y = cr <= kLeafMax ? leaf_ref(gamma + 1, cr) : gamma + 1;
+  dd.z = first;
+  dd.w = last - first + 1;
+  nodes[i].d = dd;
+  if (first == gamma) prim_parent[gamma] = (i << 1) | 0;
+  else node_parent[gamma] = (i << 1) | 0;
+  if (last == gamma + 1) prim_parent[gamma + 1] = (i << 1) | 1;
+  else node_parent[gamma + 1] = (i << 1) | 1;
+}
+
+struct FBox {
+  float mn[3], mx[3];
+};
+
+__device__ __forceinline__ void store_child_box(BNode* nd, int side, const FBox& b) {
+  float* f = reinterpret_cast<float*>(nd);
+  const int o = side ? 6 : 0;
+  f[o + 0] = b.mn[0];
+  f[o + 1] = b.mn[1];
+  f[o + 2] = b.mn[2];
+  f[o + 3] = b.mx[0];
+  f[o + 4] = b.mx[1];
+  f[o + 5] = b.mx[2];
+}
+__device__ __forceinline__ FBox load_child_box_cg(const BNode* nd, int side) {
+  const float* f = reinterpret_cast<const float*>(nd);
+  const int o = side ? 6 : 0;
+  FBox b;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    b.mn[k] = __ldcg(f + o + k);
+    b.mx[k] = __ldcg(f + o + 3 + k);
+  }
+  return b;
+}
+
+__global__ void k_repack_refit(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                               const uint32_t* __restrict__ order, int n, BNode* nodes, BTri* __restrict__ tris,
+                               const int32_t* __restrict__ prim_parent,
+                               const int32_t* __restrict__ node_parent, int* __restrict__ flags,
+                               float* __restrict__ root_box) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int f = static_cast<int>(order[p]);
+  const int vi[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
+  BTri t;
+  FBox box;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    box.mn[k] = INFINITY;
+    box.mx[k] = -INFINITY;
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double x = pos[3 * vi[c] + k];
+      t.v[3 * c + k] = x;
+      box.mn[k] = fminf(box.mn[k], __double2float_rd(x));
+      box.mx[k] = fmaxf(box.mx[k], __double2float_ru(x));
+    }
+  }
+  t.face = f;
+  t.pad = 0;
+  {
+    const double2* src = reinterpret_cast<const double2*>(&t);
+    double2* dst = reinterpret_cast<double2*>(&tris[p]);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) dst[q] = src[q];
+  }
+  if (n == 1) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      root_box[k] = box.mn[k];
+      root_box[3 + k] = box.mx[k];
+    }
+    return;
+  }
+  int link = prim_parent[p];
+  for (;;) {
+    const int par = link >> 1, side = link & 1;
+    store_child_box(&nodes[par], side, box);
+    __threadfence();
+    const int old = atomicAdd(&flags[par], 1);
+    if (old == 0) return;  // sibling not done yet; it will carry the union upward
+    __threadfence();
+    const FBox other = load_child_box_cg(&nodes[par], side ^ 1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      box.mn[k] = fminf(box.mn[k], other.mn[k]);
+      box.mx[k] = fmaxf(box.mx[k], other.mx[k]);
+    }
+    if (par == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        root_box[k] = box.mn[k];
+        root_box[3 + k] = box.mx[k];
+      }
+      return;
+    }
+    link = node_parent[par];
+  }
+}
+
+}  // namespace
+
+void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag) {
+  const int n = m.nf;
+  out.n_tris = n;
+  out.n_nodes = n > 1 ? n - 1 : 0;
+  auto* acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
+  auto* keys = ctx.buf<uint64_t>(tag + ".keys", n);
+  auto* keys2 = ctx.buf<uint64_t>(tag + ".keys2", n);
+  auto* vals = ctx.buf<uint32_t>(tag + ".vals", n);
+  auto* vals2 = ctx.buf<uint32_t>(tag + ".vals2", n);
+  out.nodes = ctx.buf<BNode>(tag + ".nodes", out.n_nodes > 0 ? out.n_nodes : 1);
+  out.tris = ctx.buf<BTri>(tag + ".tris", n);
+  out.root_box_dev = ctx.buf<float>(tag + ".rootbox", 8);
+  auto* prim_parent = ctx.buf<int32_t>(tag + ".pparent", n);
+  auto* node_parent = ctx.buf<int32_t>(tag + ".nparent", n);
+  auto* flags = ctx.buf<int>(tag + ".flags", n);
+
+  MFB_CUDA_TRY(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(acc + 3, 0x00, 5 * sizeof(unsigned long long), s));
+  if (out.n_nodes > 0) MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * out.n_nodes, s));
+
+  const int T = 256;
+  const int grid_b = std::min(div_up(std::max(n, m.nv), T), kNumSMs * 8);
+  k_bounds<<<grid_b, T, 0, s>>>(m.pos, m.faces, n, m.nv, acc);
+  k_morton<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, n, acc, keys, vals);
+  ctx.count_launch(2);
+
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, vals, vals2, n, 0, 63, s);
+  void* tptr = ctx.cub_temp(tmp, s != ctx.stream);
+  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 63, s));
+
+  if (n > 1) {
+    k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, out.nodes, prim_parent, node_parent);
+    ctx.count_launch();
+  }
+  k_repack_refit<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.nodes, out.tris, prim_parent,
+                                            node_parent, flags, out.root_box_dev);
+  ctx.count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
+  out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
+  out.scene_acc = acc;
+}
+
+}  // namespace mfb

@@ -1,0 +1,633 @@
+// raster.cu — rasterizeGBuffer (bake/gbuffer.cpp:92-191) and the per-mesh
+// pre-passes it depends on, all on the device:
+//   vertex_normals  computeVertexNormals (core/mesh.cpp:24-35): per-vertex
+//                   CSR of incident corners, summed in face order
+//                   (deterministic, no float atomics);
+//   wedge frames    computeWedgeTangents (bake/tangent.cpp:22-82): corner
+//                   contributions keyed by (vertex, uv), stable radix sort,
+//                   in-order segmented sums;
+//   reliable faces  reliableFaces (gbuffer.cpp:31-83): lock-free union-find
+//                   whose roots are island minima, (island, ratio) sort,
+//                   median = element size/2;
+//   face setup      canonical edge functions + texel bbox per face;
+//   binning         counting sort of faces into 16x16 texel tiles
+//                   (conservative: every tile the face's texel bbox touches);
+//   raster          one tile per 256-thread CTA, one texel per thread: exact
+//                   reference coverage predicate (tie rule ownsBoundary,
+//                   gbuffer.cpp:21-27,146-154), AtlasOverlap detection,
+//                   f64 attribute interpolation, coalesced G-buffer stores.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "bake.cuh"
+
+namespace mfb {
+namespace {
+
+constexpr int kTile = 16;
+
+struct alignas(16) RasterFace {
+  double px[3], py[3];
+  double doubled;
+  double ox[3], oy[3], dx[3], dy[3], sg[3];
+  int x0, y0, x1, y1;  // clamped texel bbox; x0 > x1 when the face is skipped
+};
+static_assert(sizeof(RasterFace) % 16 == 0, "RasterFace must stay 16-B aligned");
+
+struct alignas(16) AttrFace {
+  double P[9];  // corner positions
+  double N[9];  // corner frame normals
+  double T[9];  // corner frame tangents
+  int reliable;
+  int pad;
+};
+
+// ------------------------------------------------------------ vertex normals
+__global__ void k_corner_count(const int32_t* __restrict__ faces, int nc, int* __restrict__ cnt) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nc) atomicAdd(&cnt[faces[c]], 1);
+}
+__global__ void k_corner_fill(const int32_t* __restrict__ faces, int nc, const int* __restrict__ start,
+                              int* __restrict__ cursor, int* __restrict__ list) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const int v = faces[c];
+  list[start[v] + atomicAdd(&cursor[v], 1)] = c;
+}
+__global__ void k_face_area_vec(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
+                                double* __restrict__ av) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const d3 p0 = ld3(pos + 3 * faces[3 * f]), p1 = ld3(pos + 3 * faces[3 * f + 1]),
+           p2 = ld3(pos + 3 * faces[3 * f + 2]);
+  st3(av + 3 * f, 0.5 * cross(p1 - p0, p2 - p0));  // faceAreaVector, mesh.h:28-31
+}
+__global__ void k_vertex_sum(int nv, const int* __restrict__ start, int* __restrict__ list,
+                             const double* __restrict__ av, double* __restrict__ out, int renorm) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int b = start[v], e = start[v + 1];
+  for (int i = b + 1; i < e; ++i) {  // insertion sort: face order (valence is small)
+    const int key = list[i];
+    int j = i - 1;
+    while (j >= b && list[j] > key) {
+      list[j + 1] = list[j];
+      --j;
+    }
+    list[j + 1] = key;
+  }
+  d3 n = mk3(0.0, 0.0, 0.0);
+  for (int i = b; i < e; ++i) n = n + ld3(av + 3 * (list[i] / 3));
+  const double len = norm(n);
+  if (len > 0) n = n / len;
+  if (renorm) {
+    const double l2 = norm(n);
+    if (l2 > 1e-20) n = n / l2;
+  }
+  st3(out + 3 * v, n);
+}
+__global__ void k_renorm(int nv, const double* __restrict__ in, double* __restrict__ out) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  d3 n = ld3(in + 3 * v);
+  const double len = norm(n);
+  if (len > 1e-20) n = n / len;
+  st3(out + 3 * v, n);
+}
+
+// ------------------------------------------------------------ wedge frames
+__global__ void k_wedge_contrib(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
+                                int nu, double* __restrict__ contrib, uint8_t* __restrict__ present,
+                                uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int t[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
+  const int u[3] = {fuv[3 * f], fuv[3 * f + 1], fuv[3 * f + 2]};
+  const d3 p0 = ld3(pos + 3 * t[0]), p1 = ld3(pos + 3 * t[1]), p2 = ld3(pos + 3 * t[2]);
+  const double d1x = uvs[2 * u[1]] - uvs[2 * u[0]], d1y = uvs[2 * u[1] + 1] - uvs[2 * u[0] + 1];
+  const double d2x = uvs[2 * u[2]] - uvs[2 * u[0]], d2y = uvs[2 * u[2] + 1] - uvs[2 * u[0] + 1];
+  const double det = d1x * d2y - d2x * d1y;
+  const bool face_ok = !(fabs(det) < 1e-20);
+  d3 ft = mk3(0.0, 0.0, 0.0);
+  if (face_ok) ft = ((p1 - p0) * d2y - (p2 - p0) * d1y) / det;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int c = 3 * f + k;
+    keys[c] = static_cast<uint64_t>(t[k]) * static_cast<uint64_t>(nu) + static_cast<uint64_t>(u[k]);
+    idx[c] = static_cast<uint32_t>(c);
+    bool ok = face_ok;
+    d3 w = mk3(0.0, 0.0, 0.0);
+    if (ok) {
+      const d3 self = ld3(pos + 3 * t[k]);
+      const d3 ea = ld3(pos + 3 * t[(k + 1) % 3]) - self;
+      const d3 eb = ld3(pos + 3 * t[(k + 2) % 3]) - self;
+      const double la = norm(ea), lb = norm(eb);
+      if (la < 1e-20 || lb < 1e-20) {
+        ok = false;
+      } else {
+        double cs = dot(ea, eb) / (la * lb);
+        cs = cs < -1.0 ? -1.0 : (cs > 1.0 ? 1.0 : cs);
+        w = acos(cs) * ft;
+      }
+    }
+    present[c] = ok ? 1 : 0;
+    st3(contrib + 3 * c, w);
+  }
+}
+__global__ void k_wedge_segsum(int nc, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
+                               const double* __restrict__ contrib, const uint8_t* __restrict__ present,
+                               double* __restrict__ acc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nc) return;
+  if (i > 0 && keys[i] == keys[i - 1]) return;  // not a segment head
+  d3 s = mk3(0.0, 0.0, 0.0);
+  int j = i;
+  for (; j < nc && keys[j] == keys[i]; ++j) {
+    const int c = idx[j];
+    if (present[c]) s = s + ld3(contrib + 3 * c);
+  }
+  for (int k = i; k < j; ++k) st3(acc + 3 * idx[k], s);
+}
+// frames[c] = {T, B, N}; also fills the raster attribute block when attrs != null.
+__global__ void k_wedge_frames(const int32_t* __restrict__ faces, int nf, const double* __restrict__ unitN,
+                               const double* __restrict__ acc, double* __restrict__ frames,
+                               AttrFace* __restrict__ attrs, const double* __restrict__ pos) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 3 * nf) return;
+  const int v = faces[c];
+  d3 N = ld3(unitN + 3 * v);
+  if (norm(N) < 1e-20) N = mk3(0.0, 0.0, 1.0);
+  d3 t = ld3(acc + 3 * c);
+  t = t - N * dot(N, t);
+  const double len = norm(t);
+  const d3 T = len > 1e-12 ? t / len : any_perpendicular(N);
+  if (frames) {
+    st3(frames + 9 * c, T);
+    st3(frames + 9 * c + 3, cross(N, T));
+    st3(frames + 9 * c + 6, N);
+  }
+  if (attrs) {
+    const int f = c / 3, k = c % 3;
+    st3(attrs[f].P + 3 * k, ld3(pos + 3 * v));
+    st3(attrs[f].N + 3 * k, N);
+    st3(attrs[f].T + 3 * k, T);
+  }
+}
+
+// ------------------------------------------------------------ reliable faces
+__global__ void k_iota(int n, int* __restrict__ a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+__device__ __forceinline__ int uf_find(int* parent, int x) {
+  int p = __ldcg(&parent[x]);
+  while (p != x) {
+    x = p;
+    p = __ldcg(&parent[x]);
+  }
+  return x;
+}
+// Hook the larger root under the smaller one, so every root is its island's
+// minimum UV index — exactly the reference's parent[max] = min (gbuffer.cpp:41-45).
+__global__ void k_uf_unite(const int32_t* __restrict__ fuv, int nf, int* parent) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  for (int e = 1; e <= 2; ++e) {
+    int a = fuv[3 * f], b = fuv[3 * f + e];
+    for (;;) {
+      a = uf_find(parent, a);
+      b = uf_find(parent, b);
+      if (a == b) break;
+      const int hi = a > b ? a : b, lo = a > b ? b : a;
+      if (atomicCAS(&parent[hi], hi, lo) == hi) break;
+      a = hi;
+      b = lo;
+    }
+  }
+}
+__global__ void k_uf_flatten(int n, int* parent) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) parent[i] = uf_find(parent, i);
+}
+__global__ void k_face_ratio(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                             const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
+                             int nu, const int* __restrict__ parent, double* __restrict__ uv_area,
+                             double* __restrict__ ratio, int* __restrict__ island, int* __restrict__ count,
+                             uint64_t* __restrict__ rkey, uint32_t* __restrict__ ikey,
+                             uint32_t* __restrict__ fidx) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  const int u0 = fuv[3 * f], u1 = fuv[3 * f + 1], u2 = fuv[3 * f + 2];
+  const double a = 0.5 * fabs(cross2(uvs[2 * u1] - uvs[2 * u0], uvs[2 * u1 + 1] - uvs[2 * u0 + 1],
+                                     uvs[2 * u2] - uvs[2 * u0], uvs[2 * u2 + 1] - uvs[2 * u0 + 1]));
+  const d3 p0 = ld3(pos + 3 * faces[3 * f]), p1 = ld3(pos + 3 * faces[3 * f + 1]),
+           p2 = ld3(pos + 3 * faces[3 * f + 2]);
+  const double surf = norm(0.5 * cross(p1 - p0, p2 - p0));  // faceArea, mesh.h:33
+  const int isl = parent[u0];
+  double r = -1.0;
+  const bool has = surf > 1e-20;
+  if (has) {
+    r = a / surf;
+    atomicAdd(&count[isl], 1);
+  }
+  uv_area[f] = a;
+  ratio[f] = r;
+  island[f] = isl;
+  rkey[f] = has ? static_cast<uint64_t>(__double_as_longlong(r)) : 0ull;
+  ikey[f] = has ? static_cast<uint32_t>(isl) : static_cast<uint32_t>(nu);
+  fidx[f] = static_cast<uint32_t>(f);
+}
+__global__ void k_island_median(int nu, const int* __restrict__ count, const int* __restrict__ start,
+                                const uint32_t* __restrict__ sorted_face, const double* __restrict__ ratio,
+                                double* __restrict__ median) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nu) return;
+  const int n = count[i];
+  median[i] = n > 0 ? ratio[sorted_face[start[i] + n / 2]] : 0.0;
+}
+
+// ------------------------------------------------------------ face setup
+__global__ void k_face_setup(const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
+                             int res, const double* __restrict__ uv_area, const double* __restrict__ ratio,
+                             const int* __restrict__ island, const double* __restrict__ median,
+                             RasterFace* __restrict__ rf, AttrFace* __restrict__ attrs) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  // reliable (gbuffer.cpp:74-81)
+  int rel = 0;
+  if (!(uv_area[f] < 1e-8) && !(ratio[f] < 0.0)) {
+    const double m = median[island[f]];
+    if (!(ratio[f] > 100.0 * m || 100.0 * ratio[f] < m)) rel = 1;
+  }
+  attrs[f].reliable = rel;
+  attrs[f].pad = 0;
+
+  RasterFace s;
+  const double R = static_cast<double>(res);
+  const int u[3] = {fuv[3 * f], fuv[3 * f + 1], fuv[3 * f + 2]};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    s.px[k] = uvs[2 * u[k]] * R;
+    s.py[k] = uvs[2 * u[k] + 1] * R;
+  }
+  s.doubled = cross2(s.px[1] - s.px[0], s.py[1] - s.py[0], s.px[2] - s.px[0], s.py[2] - s.py[0]);
+  bool skip = s.doubled == 0.0;
+  const double orient = s.doubled > 0.0 ? 1.0 : -1.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int i0 = u[k], i1 = u[(k + 1) % 3];
+    const int lo = i0 < i1 ? i0 : i1, hi = i0 < i1 ? i1 : i0;
+    if (lo == hi) {
+      skip = true;
+      s.ox[k] = s.oy[k] = s.dx[k] = s.dy[k] = s.sg[k] = 0.0;
+      continue;
+    }
+    s.ox[k] = uvs[2 * lo] * R;
+    s.oy[k] = uvs[2 * lo + 1] * R;
+    s.dx[k] = uvs[2 * hi] * R - s.ox[k];
+    s.dy[k] = uvs[2 * hi + 1] * R - s.oy[k];
+    s.sg[k] = (i0 == lo ? 1.0 : -1.0) * orient;
+  }
+  // Eigen cwiseMin/Max: b < a ? b : a / a < b ? b : a (shim, include/Eigen/Core)
+  double lx = s.px[0], ly = s.py[0], hx = s.px[0], hy = s.py[0];
+#pragma unroll
+  for (int k = 1; k < 3; ++k) {
+    lx = s.px[k] < lx ? s.px[k] : lx;
+    ly = s.py[k] < ly ? s.py[k] : ly;
+    hx = hx < s.px[k] ? s.px[k] : hx;
+    hy = hy < s.py[k] ? s.py[k] : hy;
+  }
+  s.x0 = max(0, static_cast<int>(floor(lx - 0.5)));
+  s.y0 = max(0, static_cast<int>(floor(ly - 0.5)));
+  s.x1 = min(res - 1, static_cast<int>(ceil(hx - 0.5)));
+  s.y1 = min(res - 1, static_cast<int>(ceil(hy - 0.5)));
+  if (skip) {
+    s.x0 = 1;
+    s.x1 = 0;
+  }
+  rf[f] = s;
+}
+
+// ------------------------------------------------------------ binning
+__device__ __forceinline__ bool face_tiles(const RasterFace& s, int row_begin, int row_end, int& tx0,
+                                           int& tx1, int& ty0, int& ty1) {
+  const int y0 = max(s.y0, row_begin), y1 = min(s.y1, row_end - 1);
+  if (s.x0 > s.x1 || y0 > y1) return false;
+  tx0 = s.x0 / kTile;
+  tx1 = s.x1 / kTile;
+  ty0 = (y0 - row_begin) / kTile;
+  ty1 = (y1 - row_begin) / kTile;
+  return true;
+}
+__global__ void k_bin_count(const RasterFace* __restrict__ rf, int nf, int row_begin, int row_end,
+                            int tiles_x, int* __restrict__ tile_cnt) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  int tx0, tx1, ty0, ty1;
+  if (!face_tiles(rf[f], row_begin, row_end, tx0, tx1, ty0, ty1)) return;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&tile_cnt[ty * tiles_x + tx], 1);
+}
+__global__ void k_bin_fill(const RasterFace* __restrict__ rf, int nf, int row_begin, int row_end,
+                           int tiles_x, const int* __restrict__ tile_start, int* __restrict__ cursor,
+                           int* __restrict__ bins, int capacity, int* __restrict__ overflow) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  int tx0, tx1, ty0, ty1;
+  if (!face_tiles(rf[f], row_begin, row_end, tx0, tx1, ty0, ty1)) return;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) {
+      const int t = ty * tiles_x + tx;
+      const int p = tile_start[t] + atomicAdd(&cursor[t], 1);
+      if (p < capacity) bins[p] = f;
+      else *overflow = 1;
+    }
+}
+
+// ------------------------------------------------------------ raster
+__device__ __forceinline__ bool owns_boundary(double dx, double dy) {
+  if (dy != 0.0) return dy > 0.0;
+  return dx < 0.0;
+}
+
+constexpr int kChunk = 32;
+
+__global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ rf,
+                                                const AttrFace* __restrict__ attrs,
+                                                const int* __restrict__ tile_start,
+                                                const int* __restrict__ bins, int capacity, int res,
+                                                int row_begin, int row_end, int g_row0,
+                                                float* __restrict__ gpos, float* __restrict__ gnrm,
+                                                float* __restrict__ gtan, float* __restrict__ gbit,
+                                                uint8_t* __restrict__ gvalid, uint8_t* __restrict__ grel,
+                                                int* __restrict__ overlap,
+                                                unsigned long long* __restrict__ row_counts) {
+  __shared__ RasterFace sf[kChunk];
+  __shared__ int sfid[kChunk];
+  const int tiles_x = (res + kTile - 1) / kTile;
+  const int t = blockIdx.x;
+  const int tx = t % tiles_x, ty = t / tiles_x;
+  const int x = tx * kTile + (threadIdx.x & 15);
+  const int y = row_begin + ty * kTile + (threadIdx.x >> 4);
+  const bool in = x < res && y < row_end;
+  const double cx = x + 0.5, cy = y + 0.5;
+  const int b = tile_start[t], e = min(tile_start[t + 1], capacity);
+  int cover = -1, hits = 0;
+  for (int base = b; base < e; base += kChunk) {
+    const int n = min(kChunk, e - base);
+    __syncthreads();
+    {
+      // cooperative 16-B copies of n RasterFace records
+      const int words = n * static_cast<int>(sizeof(RasterFace) / 16);
+      for (int w = threadIdx.x; w < words; w += blockDim.x) {
+        const int i = w / static_cast<int>(sizeof(RasterFace) / 16);
+        const int o = w % static_cast<int>(sizeof(RasterFace) / 16);
+        const int f = bins[base + i];
+        reinterpret_cast<float4*>(&sf[i])[o] = __ldg(reinterpret_cast<const float4*>(&rf[f]) + o);
+        if (o == 0) sfid[i] = f;
+      }
+    }
+    __syncthreads();
+    if (in) {
+      for (int i = 0; i < n; ++i) {
+        const RasterFace& s = sf[i];
+        if (x < s.x0 || x > s.x1 || y < s.y0 || y > s.y1) continue;
+        bool inside = true;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const double ev = s.sg[k] * cross2(s.dx[k], s.dy[k], cx - s.ox[k], cy - s.oy[k]);
+          if (ev < 0.0 || (ev == 0.0 && !owns_boundary(s.sg[k] * s.dx[k], s.sg[k] * s.dy[k]))) {
+            inside = false;
+            break;
+          }
+        }
+        if (!inside) continue;
+        ++hits;
+        if (cover < 0 || sfid[i] < cover) cover = sfid[i];
+      }
+    }
+  }
+  if (hits > 1) atomicExch(overlap, 1);
+  if (!in) return;
+  const int64_t gi = static_cast<int64_t>(y - g_row0) * res + x;
+  float P[3] = {0.f, 0.f, 0.f}, Nf[3] = {0.f, 0.f, 0.f}, Tf[3] = {0.f, 0.f, 0.f}, Bf[3] = {0.f, 0.f, 0.f};
+  uint8_t valid = 0, rel = 0;
+  if (cover >= 0) {
+    const RasterFace& s = rf[cover];
+    const AttrFace& a = attrs[cover];
+    const double px0 = s.px[0], py0 = s.py[0], px1 = s.px[1], py1 = s.py[1], px2 = s.px[2], py2 = s.py[2];
+    const double w0 = cross2(px2 - px1, py2 - py1, cx - px1, cy - py1) / s.doubled;
+    const double w1 = cross2(px0 - px2, py0 - py2, cx - px2, cy - py2) / s.doubled;
+    const double w2 = cross2(px1 - px0, py1 - py0, cx - px0, cy - py0) / s.doubled;
+    const d3 pos = (w0 * ld3(a.P) + w1 * ld3(a.P + 3)) + w2 * ld3(a.P + 6);
+    d3 n = (w0 * ld3(a.N) + w1 * ld3(a.N + 3)) + w2 * ld3(a.N + 6);
+    const double nl = norm(n);
+    n = nl > 1e-12 ? n / nl : ld3(a.N);
+    d3 tg = (w0 * ld3(a.T) + w1 * ld3(a.T + 3)) + w2 * ld3(a.T + 6);
+    tg = tg - n * dot(n, tg);
+    const double tl = norm(tg);
+    tg = tl > 1e-12 ? tg / tl : any_perpendicular(n);
+    const d3 bt = cross(n, tg);
+    P[0] = __double2float_rn(pos.x);
+    P[1] = __double2float_rn(pos.y);
+    P[2] = __double2float_rn(pos.z);
+    Nf[0] = __double2float_rn(n.x);
+    Nf[1] = __double2float_rn(n.y);
+    Nf[2] = __double2float_rn(n.z);
+    Tf[0] = __double2float_rn(tg.x);
+    Tf[1] = __double2float_rn(tg.y);
+    Tf[2] = __double2float_rn(tg.z);
+    Bf[0] = __double2float_rn(bt.x);
+    Bf[1] = __double2float_rn(bt.y);
+    Bf[2] = __double2float_rn(bt.z);
+    valid = 1;
+    rel = static_cast<uint8_t>(a.reliable);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    gpos[3 * gi + k] = P[k];
+    gnrm[3 * gi + k] = Nf[k];
+    gtan[3 * gi + k] = Tf[k];
+    gbit[3 * gi + k] = Bf[k];
+  }
+  gvalid[gi] = valid;
+  grel[gi] = rel;
+  if (row_counts) {
+    // 16 lanes of a half-warp share one row
+    const unsigned m = __ballot_sync(__activemask(), valid != 0);
+    const int lane = threadIdx.x & 31;
+    const unsigned half = (lane < 16) ? (m & 0xffffu) : (m >> 16);
+    if ((lane & 15) == 0 && half) atomicAdd(&row_counts[y - row_begin], static_cast<unsigned long long>(__popc(half)));
+  }
+}
+
+__global__ void k_gather_u32(int n, const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm,
+                             uint32_t* __restrict__ dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[perm[i]];
+}
+
+int bits_for(uint64_t n) {
+  int b = 1;
+  while (b < 64 && (uint64_t(1) << b) < n) ++b;
+  return b;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, bool renorm,
+                    const std::string& tag) {
+  const int T = 256;
+  if (m.has_normals()) {
+    if (renorm) {
+      k_renorm<<<div_up(m.nv, T), T, 0, s>>>(m.nv, m.nrm, out);
+      ctx.count_launch();
+    } else {
+      MFB_CUDA_TRY(cudaMemcpyAsync(out, m.nrm, sizeof(double) * 3 * m.nv, cudaMemcpyDeviceToDevice, s));
+    }
+    return;
+  }
+  const int nc = 3 * m.nf;
+  int* cnt = ctx.buf<int>(tag + ".vn.cnt", m.nv + 1);
+  int* start = ctx.buf<int>(tag + ".vn.start", m.nv + 1);
+  int* cursor = ctx.buf<int>(tag + ".vn.cursor", m.nv + 1);
+  int* list = ctx.buf<int>(tag + ".vn.list", nc);
+  double* av = ctx.buf<double>(tag + ".vn.av", 3 * static_cast<size_t>(m.nf));
+  MFB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (m.nv + 1), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (m.nv + 1), s));
+  k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, cnt, start, m.nv + 1, s));
+  k_corner_fill<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, start, cursor, list);
+  k_face_area_vec<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, av);
+  k_vertex_sum<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list, av, out, renorm ? 1 : 0);
+  ctx.count_launch(4);
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+namespace {
+// Shared by prepare_lowpoly and wedge_frames.
+void wedge_pipeline(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames, AttrFace* attrs) {
+  const int T = 256;
+  const int nf = lo.nf, nc = 3 * nf;
+  double* unitN = ctx.buf<double>("lo.unitN", 3 * static_cast<size_t>(lo.nv));
+  vertex_normals(ctx, s, lo, unitN, true, "lo");
+  double* contrib = ctx.buf<double>("lo.wt.contrib", 3 * static_cast<size_t>(nc));
+  uint8_t* present = ctx.buf<uint8_t>("lo.wt.present", nc);
+  uint64_t* keys = ctx.buf<uint64_t>("lo.wt.keys", nc);
+  uint64_t* keys2 = ctx.buf<uint64_t>("lo.wt.keys2", nc);
+  uint32_t* idx = ctx.buf<uint32_t>("lo.wt.idx", nc);
+  uint32_t* idx2 = ctx.buf<uint32_t>("lo.wt.idx2", nc);
+  double* acc = ctx.buf<double>("lo.wt.acc", 3 * static_cast<size_t>(nc));
+  k_wedge_contrib<<<div_up(nf, T), T, 0, s>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, lo.nu, contrib, present,
+                                              keys, idx);
+  const int kb = bits_for(static_cast<uint64_t>(lo.nv) * static_cast<uint64_t>(lo.nu) + 1);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, idx, idx2, nc, 0, kb, s);
+  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx.cub_temp(tmp, s != ctx.stream), tmp, keys, keys2, idx,
+                                               idx2, nc, 0, kb, s));
+  k_wedge_segsum<<<div_up(nc, T), T, 0, s>>>(nc, keys2, idx2, contrib, present, acc);
+  k_wedge_frames<<<div_up(nc, T), T, 0, s>>>(lo.faces, nf, unitN, acc, frames, attrs, lo.pos);
+  ctx.count_launch(3);
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+}  // namespace
+
+void wedge_frames(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames_out) {
+  wedge_pipeline(ctx, s, lo, frames_out, nullptr);
+}
+
+void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterPlan& plan) {
+  const int T = 256;
+  const int nf = lo.nf, nu = lo.nu;
+  auto* rf = ctx.buf<RasterFace>("lo.rf", nf);
+  auto* attrs = ctx.buf<AttrFace>("lo.attrs", nf);
+  wedge_pipeline(ctx, s, lo, nullptr, attrs);
+
+  // reliableFaces
+  int* parent = ctx.buf<int>("lo.rel.parent", nu);
+  double* uv_area = ctx.buf<double>("lo.rel.uvarea", nf);
+  double* ratio = ctx.buf<double>("lo.rel.ratio", nf);
+  int* island = ctx.buf<int>("lo.rel.island", nf);
+  int* count = ctx.buf<int>("lo.rel.count", nu + 1);
+  int* start = ctx.buf<int>("lo.rel.start", nu + 1);
+  uint64_t* rkey = ctx.buf<uint64_t>("lo.rel.rkey", nf);
+  uint64_t* rkey2 = ctx.buf<uint64_t>("lo.rel.rkey2", nf);
+  uint32_t* ikey = ctx.buf<uint32_t>("lo.rel.ikey", nf);
+  uint32_t* ikey2 = ctx.buf<uint32_t>("lo.rel.ikey2", nf);
+  uint32_t* fidx = ctx.buf<uint32_t>("lo.rel.fidx", nf);
+  uint32_t* fidx2 = ctx.buf<uint32_t>("lo.rel.fidx2", nf);
+  double* median = ctx.buf<double>("lo.rel.median", nu);
+  MFB_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int) * (nu + 1), s));
+  k_iota<<<div_up(nu, T), T, 0, s>>>(nu, parent);
+  k_uf_unite<<<div_up(nf, T), T, 0, s>>>(lo.fuv, nf, parent);
+  k_uf_flatten<<<div_up(nu, T), T, 0, s>>>(nu, parent);
+  k_face_ratio<<<div_up(nf, T), T, 0, s>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, nu, parent, uv_area, ratio,
+                                           island, count, rkey, ikey, fidx);
+  ctx.count_launch(4);
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, rkey, rkey2, fidx, fidx2, nf, 0, 64, s);
+  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx.cub_temp(tmp, s != ctx.stream), tmp, rkey, rkey2, fidx,
+                                               fidx2, nf, 0, 64, s));
+  // gather island keys in ratio order, then stable sort by island
+  // (reuse rkey as a u32 scratch via ikey/ikey2)
+  k_gather_u32<<<div_up(nf, T), T, 0, s>>>(nf, ikey, fidx2, ikey2);  // island keys in ratio order
+  ctx.count_launch();
+  const int ib = bits_for(static_cast<uint64_t>(nu) + 1);
+  tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, ikey2, ikey, fidx2, fidx, nf, 0, ib, s);
+  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx.cub_temp(tmp, s != ctx.stream), tmp, ikey2, ikey, fidx2,
+                                               fidx, nf, 0, ib, s));
+  tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, start, nu + 1, s);
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, count, start, nu + 1, s));
+  k_island_median<<<div_up(nu, T), T, 0, s>>>(nu, count, start, fidx, ratio, median);
+  k_face_setup<<<div_up(nf, T), T, 0, s>>>(lo.uvs, lo.fuv, nf, res, uv_area, ratio, island, median, rf, attrs);
+  ctx.count_launch(2);
+  MFB_CUDA_TRY(cudaGetLastError());
+  plan.faces = rf;
+  plan.attrs = attrs;
+  plan.nf = nf;
+  plan.res = res;
+}
+
+void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPlan& plan, GBufDev& g,
+                    int* flags_dev, int64_t* row_counts_dev) {
+  (void)lo;
+  const int T = 256;
+  const int res = plan.res;
+  const int row_begin = g.row0, row_end = g.row0 + g.rows;
+  const int tiles_x = (res + kTile - 1) / kTile;
+  const int tiles_y = (g.rows + kTile - 1) / kTile;
+  const int ntiles = tiles_x * tiles_y;
+  auto* rf = static_cast<const RasterFace*>(plan.faces);
+  auto* attrs = static_cast<const AttrFace*>(plan.attrs);
+  int* cnt = ctx.buf<int>("ras.cnt", ntiles + 1);
+  int* start = ctx.buf<int>("ras.start", ntiles + 1);
+  int* cursor = ctx.buf<int>("ras.cursor", ntiles + 1);
+  // Bin capacity: a bound that holds for ordinary atlases; the bake driver
+  // re-runs with the exact total (flags[1] set, total in flags[2]) otherwise.
+  const int64_t cap64 = std::max<int64_t>(ctx.bin_capacity, 8ll * plan.nf + 4ll * ntiles + 1024);
+  const int capacity = static_cast<int>(std::min<int64_t>(cap64, 0x7fffffff));
+  int* bins = ctx.buf<int>("ras.bins", capacity);
+  MFB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (ntiles + 1), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (ntiles + 1), s));
+  k_bin_count<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, cnt);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, ntiles + 1, s);
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, cnt, start, ntiles + 1, s));
+  k_bin_fill<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, start, cursor, bins,
+                                              capacity, flags_dev + 1);
+  MFB_CUDA_TRY(cudaMemcpyAsync(flags_dev + 2, start + ntiles, sizeof(int), cudaMemcpyDeviceToDevice, s));
+  if (row_counts_dev) MFB_CUDA_TRY(cudaMemsetAsync(row_counts_dev, 0, sizeof(int64_t) * g.rows, s));
+  k_raster<<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos, g.nrm,
+                                  g.tan, g.bit, g.valid, g.rel, flags_dev,
+                                  reinterpret_cast<unsigned long long*>(row_counts_dev));
+  ctx.count_launch(3);
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+}  // namespace mfb
