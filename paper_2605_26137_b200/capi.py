@@ -14,7 +14,7 @@ import numpy as np
 from .mesh import MfMeshView, TriangleMesh
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmfbake.so")
+LIB_PATH = os.environ.get("MFB_LIB") or os.path.join(HERE, "libmfbake.so")
 
 # include/mfbake.h status codes (1 + meshforge::ErrorCode, error.h:8-21)
 ERROR_NAMES = {

@@ -102,6 +102,11 @@ struct alignas(16) BTri {
 };
 static_assert(sizeof(BTri) == 80, "triangle record is 5 x 16 B");
 
+// Per-triangle fp32 box (rounded outward), leaf order: mn.xyz mx.x | mx.yz pad pad.
+struct alignas(16) TBox {
+  float4 a, b;
+};
+
 __host__ __device__ __forceinline__ int32_t leaf_ref(int first, int count) {
   return ~((first << 3) | count);
 }
@@ -116,6 +121,7 @@ struct Lbvh {
   int n_nodes = 0;          // internal nodes (n_tris - 1), root = node 0 when n_tris > 1
   BNode* nodes = nullptr;   // device
   BTri* tris = nullptr;     // device, leaf order
+  TBox* tbox = nullptr;     // device, leaf order
   int32_t root_ref = 0;     // 0 (internal root) or a leaf ref when n_tris <= kLeafMax... see build
   float root_box[6];        // host copy not needed for traversal; kept for export
   float* root_box_dev = nullptr;
@@ -147,24 +153,64 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
 // Frames only (for mf_wedge_tangents): F x 3 x {T, B, N} x 3 doubles.
 void wedge_frames(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames_out);
 
+// Compacted closest-point queries (valid and reliable texels), in 8x4 texel
+// blocks so each warp's 32 queries are spatial neighbours. Two passes share
+// one buffer: pass A (texels with even x and even y, one per 2x2 quad) fills
+// slots from the front, pass B (the other three texels of each quad) from the
+// back, so pass B can seed its bound with the face pass A found for the quad
+// corner (result-neutral: it only tests that face first).
+// Measured on config B (r01 profiles): the quad split lowers per-warp
+// coherence more than the seeded bound saves, so it is off; every query is
+// in pass A and pass B is empty.
+constexpr bool kSeedPasses = false;
+
+struct QueryList {
+  float4* qpos = nullptr;  // x, y, z (the G-buffer's f32 position), w = slab texel index (int bits)
+  float* qtbn = nullptr;   // 9 floats per query: tangent, bitangent, normal (f32, as stored)
+  int* count = nullptr;    // device counters: [0] pass A, [1] pass B (reset by the producer)
+  int capacity = 0;
+};
+
+// Fused-bake raster outputs: instead of the full G-buffer, the raster writes
+// the valid mask (g.valid), the raw map for every non-query texel
+// (background (128,128,128) / unreliable (128,128,255), gbuffer.cpp:212-227)
+// and the query records; debug planes get -1/-2 for invalid/unreliable.
+struct RasterFused {
+  uint8_t* rgb = nullptr;
+  QueryList q;
+  int32_t* dbg_face = nullptr;
+  double* dbg_ts = nullptr;
+  unsigned long long* valid_count = nullptr;  // N_v accumulator (optional)
+};
+
 // Tile-binned rasteriser over rows [g.row0, g.row0 + g.rows). Device flags:
 // flags[0] = 1 when a texel is claimed twice (AtlasOverlap); flags[1] = 1
 // when the tile bins overflowed (re-run after setting ctx.bin_capacity to
-// flags[2], the exact bin total). Never synchronises.
+// flags[2], the exact bin total). Never synchronises. With `fused` the
+// G-buffer planes other than `valid` are not written (see RasterFused).
 void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPlan& plan,
-                    GBufDev& g, int* flags_dev, int64_t* row_counts_dev);
+                    GBufDev& g, int* flags_dev, int64_t* row_counts_dev,
+                    const RasterFused* fused = nullptr);
+
+// Builds the query list (and the raw map / debug codes of non-query texels)
+// from a full G-buffer slab (the mf_transfer_normals entry point).
+void gbuffer_queries(Ctx& ctx, cudaStream_t s, const GBufDev& g, const RasterFused& out);
 
 // ---------------------------------------------------------------- queries
 struct TransferArgs {
-  const GBufDev* g = nullptr;
-  int row_begin = 0, row_end = 0;   // rows to transfer (absolute), within the slab
+  QueryList q;
+  int res = 0;
+  int slab_row0 = 0;                // absolute atlas row of slab row 0
+  int* face_map = nullptr;          // slab-sized: pass-A winning face per texel (-1 elsewhere)
+  int64_t face_map_size = 0;
+  const double* hi_positions = nullptr;
   const double* hi_normals = nullptr;
   const int32_t* hi_faces = nullptr;
   double max_dist = 0.0;
-  uint8_t* rgb = nullptr;           // raw map rows [row_begin,row_end) x res x 3 (slab-relative to g)
+  uint8_t* rgb = nullptr;           // raw map slab (indexed by the query's slab texel)
   int32_t* dbg_face = nullptr;
   double* dbg_ts = nullptr;
-  unsigned long long* counters = nullptr;  // [valid, queries, hits]
+  unsigned long long* counters = nullptr;  // [queries, hits]
 };
 void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferArgs& a);
 

@@ -13,7 +13,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -148,6 +151,24 @@ struct mf_bvh {
 };
 
 namespace {
+
+// MFB_TRACE=1 prints host-side phase timestamps of the entry points (stderr).
+struct HostTrace {
+  bool on;
+  std::chrono::steady_clock::time_point t0, last;
+  const char* what;
+  explicit HostTrace(const char* w) : on(std::getenv("MFB_TRACE") != nullptr), what(w) {
+    t0 = last = std::chrono::steady_clock::now();
+  }
+  void mark(const char* phase) {
+    if (!on) return;
+    auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[mfb] %s %-14s +%8.3f ms (t=%8.3f)\n", what, phase,
+                 std::chrono::duration<double, std::milli>(now - last).count(),
+                 std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
 
 int fail(int code, const std::string& msg) {
   set_last_error(msg);
@@ -310,6 +331,15 @@ GBufDev gbuf_slab(Ctx& c, int res, int row0, int rows) {
   return g;
 }
 
+QueryList query_list(Ctx& c, int64_t capacity) {
+  QueryList q;
+  q.capacity = static_cast<int>(capacity);
+  q.qpos = c.buf<float4>("q.pos", capacity);
+  q.qtbn = c.buf<float>("q.tbn", 9 * capacity);
+  q.count = c.buf<int>("q.count", 4);  // [0] pass A, [1] pass B
+  return q;
+}
+
 // The fused bake over validated device meshes; rows [rb, re) into rgb_out (device).
 void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
               int rb, int re, uint8_t* rgb_out, int32_t* dbg_face, double* dbg_ts, mf_bake_stats* st,
@@ -322,83 +352,100 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
   cudaStream_t s = c.stream, side = c.side;
   const int r = radius;
   const int s0 = std::max(0, rb - r), s1 = std::min(res, re + r);  // raster/transfer slab with dilation halo
-  GBufDev g = gbuf_slab(c, res, s0, s1 - s0);
+  GBufDev g;
+  g.res = res;
+  g.row0 = s0;
+  g.rows = s1 - s0;
+  g.valid = c.buf<uint8_t>("g.valid", g.texels());
+  // flags: [0] AtlasOverlap, [1] bin overflow, [2] bin total, [3] query overflow
   int* flags = c.buf<int>("bake.flags", 4);
   unsigned long long* counters = c.buf<unsigned long long>("bake.counters", 4);
-  MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
-
-  // fork: dense-mesh work on the side stream
-  MFB_CUDA_TRY(cudaEventRecord(c.fork, s));
-  MFB_CUDA_TRY(cudaStreamWaitEvent(side, c.fork, 0));
-  cudaEvent_t e_side0 = tm.mark(side);
-  double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
-  vertex_normals(c, side, hi->m, hiN, true, "hi");
-  Lbvh bvh;
-  lbvh_build(c, side, hi->m, bvh, "hi.bvh");
-  cudaEvent_t e_side1 = tm.mark(side);
-  MFB_CUDA_TRY(cudaEventRecord(c.join, side));
-
-  // main: lowpoly prep + raster
-  cudaEvent_t e0 = tm.mark(s);
-  RasterPlan plan;
-  prepare_lowpoly(c, s, lo->m, res, plan);
-  cudaEvent_t e1 = tm.mark(s);
-  raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr);
-  cudaEvent_t e2 = tm.mark(s);
-
-  // join, transfer, dilate
-  MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
-  cudaEvent_t e3 = tm.mark(s);
-  uint8_t* raw = c.buf<uint8_t>("bake.raw", 3 * g.texels());
-  TransferArgs ta;
-  ta.g = &g;
-  ta.row_begin = s0;
-  ta.row_end = s1;
-  ta.hi_normals = hiN;
-  ta.hi_faces = hi->m.faces;
-  ta.max_dist = frac * diag;
-  ta.rgb = raw;
-  ta.counters = counters;
-  int32_t* dface = nullptr;
-  double* dts = nullptr;
+  RasterFused fo;
+  fo.rgb = c.buf<uint8_t>("bake.raw", 3 * g.texels());
+  fo.q = query_list(c, g.texels());
+  fo.valid_count = counters + 2;
   if (dbg_face || dbg_ts) {
-    dface = c.buf<int32_t>("bake.dface", g.texels());
-    dts = c.buf<double>("bake.dts", 3 * g.texels());
-    ta.dbg_face = dface;
-    ta.dbg_ts = dts;
+    fo.dbg_face = c.buf<int32_t>("bake.dface", g.texels());
+    fo.dbg_ts = c.buf<double>("bake.dts", 3 * g.texels());
   }
-  transfer_normals(c, s, bvh, ta);
-  cudaEvent_t e4 = tm.mark(s);
-  dilate_seams(c, s, res, res, 3, raw, g.valid, s0, s1 - s0, r, rgb_out, rb, re - rb);
-  cudaEvent_t e5 = tm.mark(s);
+  for (int attempt = 0;; ++attempt) {
+    MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
+    MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
 
-  if (dbg_face)
-    MFB_CUDA_TRY(cudaMemcpyAsync(dbg_face, dface + static_cast<int64_t>(rb - s0) * res,
-                                 sizeof(int32_t) * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
-  if (dbg_ts)
-    MFB_CUDA_TRY(cudaMemcpyAsync(dbg_ts, dts + 3 * static_cast<int64_t>(rb - s0) * res,
-                                 sizeof(double) * 3 * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
-  int hflags[4] = {0, 0, 0, 0};
-  unsigned long long hcnt[4] = {0, 0, 0, 0};
-  MFB_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s));
-  MFB_CUDA_TRY(cudaMemcpyAsync(hcnt, counters, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
-  MFB_CUDA_TRY(cudaStreamSynchronize(s));
-  if (hflags[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
-  if (st) {
-    st->valid_texels = static_cast<int64_t>(hcnt[0]);
-    st->queries = static_cast<int64_t>(hcnt[1]);
-    st->hits = static_cast<int64_t>(hcnt[2]);
-    st->bvh_nodes = bvh.n_nodes;
-    st->bvh_depth = 0;
-    if (c.timing) {
-      st->ms_prepare = Timer::ms(e0, e1);
-      st->ms_raster = Timer::ms(e1, e2);
-      st->ms_bvh = Timer::ms(e_side0, e_side1);
-      st->ms_transfer = Timer::ms(e3, e4);
-      st->ms_dilate = Timer::ms(e4, e5);
-      st->ms_total = Timer::ms(t_begin ? t_begin : e0, e5);
+    // fork: dense-mesh work on the side stream
+    MFB_CUDA_TRY(cudaEventRecord(c.fork, s));
+    MFB_CUDA_TRY(cudaStreamWaitEvent(side, c.fork, 0));
+    cudaEvent_t e_side0 = tm.mark(side);
+    double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
+    vertex_normals(c, side, hi->m, hiN, true, "hi");
+    Lbvh bvh;
+    lbvh_build(c, side, hi->m, bvh, "hi.bvh");
+    cudaEvent_t e_side1 = tm.mark(side);
+    MFB_CUDA_TRY(cudaEventRecord(c.join, side));
+
+    // main: lowpoly prep + raster (fused: valid mask, raw map, query list)
+    cudaEvent_t e0 = tm.mark(s);
+    RasterPlan plan;
+    prepare_lowpoly(c, s, lo->m, res, plan);
+    cudaEvent_t e1 = tm.mark(s);
+    raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
+    cudaEvent_t e2 = tm.mark(s);
+
+    // join, transfer, dilate
+    MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
+    cudaEvent_t e3 = tm.mark(s);
+    TransferArgs ta;
+    ta.q = fo.q;
+    ta.res = res;
+    ta.slab_row0 = s0;
+    ta.face_map = c.buf<int>("bake.facemap", g.texels());
+    ta.face_map_size = g.texels();
+    ta.hi_positions = hi->m.pos;
+    ta.hi_normals = hiN;
+    ta.hi_faces = hi->m.faces;
+    ta.max_dist = frac * diag;
+    ta.rgb = fo.rgb;
+    ta.dbg_face = fo.dbg_face;
+    ta.dbg_ts = fo.dbg_ts;
+    ta.counters = counters;
+    transfer_normals(c, s, bvh, ta);
+    cudaEvent_t e4 = tm.mark(s);
+    dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, r, rgb_out, rb, re - rb);
+    cudaEvent_t e5 = tm.mark(s);
+
+    if (dbg_face)
+      MFB_CUDA_TRY(cudaMemcpyAsync(dbg_face, fo.dbg_face + static_cast<int64_t>(rb - s0) * res,
+                                   sizeof(int32_t) * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
+    if (dbg_ts)
+      MFB_CUDA_TRY(cudaMemcpyAsync(dbg_ts, fo.dbg_ts + 3 * static_cast<int64_t>(rb - s0) * res,
+                                   sizeof(double) * 3 * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
+    int hflags[4] = {0, 0, 0, 0};
+    unsigned long long hcnt[4] = {0, 0, 0, 0};
+    MFB_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s));
+    MFB_CUDA_TRY(cudaMemcpyAsync(hcnt, counters, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
+    MFB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (hflags[1] && attempt == 0) {  // tile bins overflowed: rerun with the exact capacity
+      c.bin_capacity = static_cast<int64_t>(hflags[2]) + 1;
+      continue;
     }
+    if (hflags[1] || hflags[3]) throw ApiError(MF_ERR_CUDA, "internal capacity overflow");
+    if (hflags[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+    if (st) {
+      st->queries = static_cast<int64_t>(hcnt[0]);
+      st->hits = static_cast<int64_t>(hcnt[1]);
+      st->valid_texels = static_cast<int64_t>(hcnt[2]);
+      st->bvh_nodes = bvh.n_nodes;
+      st->bvh_depth = 0;
+      if (c.timing) {
+        st->ms_prepare = Timer::ms(e0, e1);
+        st->ms_raster = Timer::ms(e1, e2);
+        st->ms_bvh = Timer::ms(e_side0, e_side1);
+        st->ms_transfer = Timer::ms(e3, e4);
+        st->ms_dilate = Timer::ms(e4, e5);
+        st->ms_total = Timer::ms(t_begin ? t_begin : e0, e5);
+      }
+    }
+    return;
   }
 }
 
@@ -489,14 +536,22 @@ int mf_raster_gbuffer(mf_ctx* ctx, const mf_mesh_view* lowpoly, int res, float* 
       throw ApiError(MF_ERR_BAD_ARGUMENT, "null G-buffer output");
     GBufDev g = gbuf_slab(c, res, 0, res);
     int* flags = c.buf<int>("bake.flags", 4);
-    MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), c.stream));
-    RasterPlan plan;
-    prepare_lowpoly(c, c.stream, lo.m, res, plan);
-    raster_gbuffer(c, c.stream, lo.m, plan, g, flags, nullptr);
-    int hf = 0;
-    MFB_CUDA_TRY(cudaMemcpyAsync(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
-    if (hf) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+    for (int attempt = 0;; ++attempt) {
+      MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), c.stream));
+      RasterPlan plan;
+      prepare_lowpoly(c, c.stream, lo.m, res, plan);
+      raster_gbuffer(c, c.stream, lo.m, plan, g, flags, nullptr);
+      int hf[4] = {0, 0, 0, 0};
+      MFB_CUDA_TRY(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, c.stream));
+      MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+      if (hf[1] && attempt == 0) {
+        c.bin_capacity = static_cast<int64_t>(hf[2]) + 1;
+        continue;
+      }
+      if (hf[1]) throw ApiError(MF_ERR_CUDA, "internal capacity overflow");
+      if (hf[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+      break;
+    }
     const int64_t n = g.texels();
     MFB_CUDA_TRY(cudaMemcpyAsync(position, g.pos, 12 * n, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaMemcpyAsync(normal, g.nrm, 12 * n, cudaMemcpyDeviceToHost, c.stream));
@@ -536,16 +591,23 @@ int mf_transfer_normals(mf_ctx* ctx, int res, const float* position, const float
     vertex_normals(c, c.stream, hi.m, hiN, true, "hi");
     Lbvh bvh;
     lbvh_build(c, c.stream, hi.m, bvh, "hi.bvh");
-    uint8_t* raw = c.buf<uint8_t>("bake.raw", 3 * n);
+    RasterFused fo;
+    fo.rgb = c.buf<uint8_t>("bake.raw", 3 * n);
+    fo.q = query_list(c, n);
+    gbuffer_queries(c, c.stream, g, fo);
     TransferArgs ta;
-    ta.g = &g;
-    ta.row_begin = 0;
-    ta.row_end = res;
+    ta.q = fo.q;
+    ta.res = res;
+    ta.slab_row0 = 0;
+    ta.face_map = c.buf<int>("bake.facemap", n);
+    ta.face_map_size = n;
+    ta.hi_positions = hi.m.pos;
     ta.hi_normals = hiN;
     ta.hi_faces = hi.m.faces;
     ta.max_dist = max_distance_fraction * bbox_diagonal;
-    ta.rgb = raw;
+    ta.rgb = fo.rgb;
     transfer_normals(c, c.stream, bvh, ta);
+    uint8_t* raw = fo.rgb;
     MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, raw, 3 * n, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
     return MF_OK;
@@ -582,24 +644,29 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
   if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
   return guarded(ctx, [&]() -> int {
     Ctx& c = ctx->c;
+    HostTrace ht("bake_host");
     Timer tm(c);
     cudaEvent_t t0 = tm.mark(c.stream);
     mf_mesh lo, hi;
     lo.ctx = hi.ctx = ctx;
     upload_mesh(c, c.stream, lowpoly, &lo, "up.lo");
+    ht.mark("upload lo");
     // reference order: lowpoly checks precede the highpoly's (gbuffer.cpp:93-97 then :195-199)
     check_lowpoly(&lo, res);
     upload_mesh(c, c.stream, highpoly, &hi, "up.hi");
+    ht.mark("upload hi");
     cudaEvent_t t1 = tm.mark(c.stream);
     if (!rgb_out) throw ApiError(MF_ERR_BAD_ARGUMENT, "rgb_out is null");
     uint8_t* drgb = c.buf<uint8_t>("bake.rgb", 3 * static_cast<int64_t>(res) * res);
     mf_bake_stats local{};
     bake_dev(c, &lo, &hi, res, bbox_diagonal, max_distance_fraction, radius, 0, res, drgb, dbg_face, dbg_ts,
              &local, tm, t1);
+    ht.mark("bake_dev");
     cudaEvent_t t2 = tm.mark(c.stream);
     MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, c.stream));
     cudaEvent_t t3 = tm.mark(c.stream);
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    ht.mark("download+sync");
     if (stats) {
       *stats = local;
       if (c.timing) {
@@ -608,6 +675,7 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
         stats->ms_total = Timer::ms(t0, t3);
       }
     }
+    ht.mark("stats");
     return MF_OK;
   });
 }
@@ -660,6 +728,8 @@ int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
     const int nn = std::max(b->bvh.n_nodes, 1);
     BNode* nodes = b->store.buf<BNode>("nodes", nn);
     BTri* tris = b->store.buf<BTri>("tris", b->bvh.n_tris);
+    TBox* tbox = b->store.buf<TBox>("tbox", b->bvh.n_tris);
+    MFB_CUDA_TRY(cudaMemcpyAsync(tbox, b->bvh.tbox, sizeof(TBox) * b->bvh.n_tris, cudaMemcpyDeviceToDevice, ctx->c.stream));
     auto* acc = b->store.buf<unsigned long long>("acc", 8);
     MFB_CUDA_TRY(cudaMemcpyAsync(nodes, b->bvh.nodes, sizeof(BNode) * nn, cudaMemcpyDeviceToDevice, ctx->c.stream));
     MFB_CUDA_TRY(cudaMemcpyAsync(tris, b->bvh.tris, sizeof(BTri) * b->bvh.n_tris, cudaMemcpyDeviceToDevice, ctx->c.stream));
@@ -670,6 +740,7 @@ int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
     MFB_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
     b->bvh.nodes = nodes;
     b->bvh.tris = tris;
+    b->bvh.tbox = tbox;
     b->bvh.scene_acc = acc;
     b->bvh.root_box_dev = nullptr;
     b->store.own_stream = false;

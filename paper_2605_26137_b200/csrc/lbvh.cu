@@ -16,6 +16,8 @@
 // reproduces exactly.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <cstdlib>
+
 #include "bake.cuh"
 
 namespace mfb {
@@ -117,7 +119,7 @@ __device__ __forceinline__ int kdelta(const uint64_t* __restrict__ k, int n, int
 }
 
 // parent links: (parent << 1) | side; prim_parent for primitives, node_parent for internals.
-__global__ void k_emit(const uint64_t* __restrict__ keys, int n, BNode* __restrict__ nodes,
+__global__ void k_emit(const uint64_t* __restrict__ keys, int n, int leaf_max, BNode* __restrict__ nodes,
                        int32_t* __restrict__ prim_parent, int32_t* __restrict__ node_parent) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n - 1) return;
@@ -139,8 +141,8 @@ __global__ void k_emit(const uint64_t* __restrict__ keys, int n, BNode* __restri
   const int first = min(i, j), last = max(i, j);
   const int cl = gamma - first + 1, cr = last - gamma;
   int4 dd;
-  dd.x = cl <= kLeafMax ? leaf_ref(first, cl) : gamma;
-  dd.y = cr <= kLeafMax ? leaf_ref(gamma + 1, cr) : gamma + 1;
+  dd.x = cl <= leaf_max ? leaf_ref(first, cl) : gamma;
+  dd.y = cr <= leaf_max ? leaf_ref(gamma + 1, cr) : gamma + 1;
   dd.z = first;
   dd.w = last - first + 1;
   nodes[i].d = dd;
@@ -178,6 +180,7 @@ __device__ __forceinline__ FBox load_child_box_cg(const BNode* nd, int side) {
 
 __global__ void k_repack_refit(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                                const uint32_t* __restrict__ order, int n, BNode* nodes, BTri* __restrict__ tris,
+                               TBox* __restrict__ tbox,
                                const int32_t* __restrict__ prim_parent,
                                const int32_t* __restrict__ node_parent, int* __restrict__ flags,
                                float* __restrict__ root_box) {
@@ -204,6 +207,8 @@ __global__ void k_repack_refit(const double* __restrict__ pos, const int32_t* __
   }
   t.face = f;
   t.pad = 0;
+  tbox[p].a = make_float4(box.mn[0], box.mn[1], box.mn[2], box.mx[0]);
+  tbox[p].b = make_float4(box.mx[1], box.mx[2], 0.f, 0.f);
   {
     const double2* src = reinterpret_cast<const double2*>(&t);
     double2* dst = reinterpret_cast<double2*>(&tris[p]);
@@ -257,6 +262,7 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   auto* vals2 = ctx.buf<uint32_t>(tag + ".vals2", n);
   out.nodes = ctx.buf<BNode>(tag + ".nodes", out.n_nodes > 0 ? out.n_nodes : 1);
   out.tris = ctx.buf<BTri>(tag + ".tris", n);
+  out.tbox = ctx.buf<TBox>(tag + ".tbox", n);
   out.root_box_dev = ctx.buf<float>(tag + ".rootbox", 8);
   auto* prim_parent = ctx.buf<int32_t>(tag + ".pparent", n);
   auto* node_parent = ctx.buf<int32_t>(tag + ".nparent", n);
@@ -278,10 +284,16 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 63, s));
 
   if (n > 1) {
-    k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, out.nodes, prim_parent, node_parent);
+    // Leaf size: the reference's 4 (bvh.cpp:13) unless MFB_LEAF_MAX (1..7) overrides it.
+    static int leaf_max = [] {
+      const char* e = std::getenv("MFB_LEAF_MAX");
+      const int v = e ? std::atoi(e) : kLeafMax;
+      return v >= 1 && v <= 7 ? v : kLeafMax;
+    }();
+    k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent);
     ctx.count_launch();
   }
-  k_repack_refit<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.nodes, out.tris, prim_parent,
+  k_repack_refit<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.nodes, out.tris, out.tbox, prim_parent,
                                             node_parent, flags, out.root_box_dev);
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());

@@ -11,6 +11,11 @@
 // conservative: fp32 child boxes rounded outward, fp32 lower bounds computed
 // with round-down intrinsics, compared against an upper bound of the current
 // best inflated by the scene-scale f64 error slack.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
 #include "bake.cuh"
 
 namespace mfb {
@@ -81,6 +86,61 @@ __device__ __forceinline__ d3 closest_point_triangle(d3 p, d3 a, d3 b, d3 c, d3&
   const double wb = vb * denom, wc = vc * denom;
   bary = mk3((1.0 - wb) - wc, wb, wc);
   return (a + ab * wb) + ac * wc;
+}
+
+// Branch-free form of closestPointTriangle for the SIMT pair rounds: every
+// lane evaluates all Voronoi-region predicates in the reference's order and
+// then the one formula of its region, with a single shared f64 division
+// (num / den selected per region: edge weight, or 1 / (va + vb + vc) for the
+// interior). Each region's outputs are computed with exactly the expressions
+// of tri_geom.h:37-95 (selects, never "+ 0"), so results are bit-identical to
+// closest_point_triangle; only the control flow differs.
+__device__ __forceinline__ d3 closest_point_triangle_sel(d3 p, d3 a, d3 b, d3 c, d3& bary) {
+  const d3 ab = b - a, ac = c - a, ap = p - a;
+  const double d1 = dot(ab, ap), d2 = dot(ac, ap);
+  const d3 bp = p - b;
+  const double d3_ = dot(ab, bp), d4 = dot(ac, bp);
+  const d3 cp = p - c;
+  const double d5 = dot(ab, cp), d6 = dot(ac, cp);
+  const double vc = d1 * d4 - d3_ * d2;
+  const double vb = d5 * d2 - d1 * d6;
+  const double va = d3_ * d6 - d5 * d4;
+  const double e43 = d4 - d3_, e56 = d5 - d6;
+  // region: 0 A, 1 B, 2 AB, 3 C, 4 AC, 5 BC, 6 interior (reference test order)
+  int r;
+  if (d1 <= 0.0 && d2 <= 0.0) r = 0;
+  else if (d3_ >= 0.0 && d4 <= d3_) r = 1;
+  else if (vc <= 0.0 && d1 >= 0.0 && d3_ <= 0.0) r = 2;
+  else if (d6 >= 0.0 && d5 <= d6) r = 3;
+  else if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) r = 4;
+  else if (va <= 0.0 && e43 >= 0.0 && e56 >= 0.0) r = 5;
+  else r = 6;
+  const double num = r == 2 ? d1 : (r == 4 ? d2 : (r == 5 ? e43 : 1.0));
+  const double den = r == 2 ? (d1 - d3_) : (r == 4 ? (d2 - d6) : (r == 5 ? (e43 + e56) : ((va + vb) + vc)));
+  const double w = (r == 0 || r == 1 || r == 3) ? 0.0 : num / den;
+  const double wb = vb * w, wc = vc * w;  // interior weights (only used when r == 6)
+  // edge / interior first step: base + dir * s
+  const d3 cb = c - b;
+  const d3 base = r == 5 ? b : a;
+  const d3 dir = r == 4 ? ac : (r == 5 ? cb : ab);
+  const double sc = r == 6 ? wb : w;
+  d3 pt;
+  if (r == 6) {
+    pt = (base + dir * sc) + ac * wc;  // (a + ab*wb) + ac*wc
+  } else {
+    // a + w*ab, a + w*ac, b + w*(c-b): scalar*vector, same rounding as dir*w
+    pt = base + sc * dir;
+  }
+  pt = r == 0 ? a : (r == 1 ? b : (r == 3 ? c : pt));
+  const double om = 1.0 - w;
+  bary = r == 0 ? mk3(1.0, 0.0, 0.0)
+       : r == 1 ? mk3(0.0, 1.0, 0.0)
+       : r == 3 ? mk3(0.0, 0.0, 1.0)
+       : r == 2 ? mk3(om, w, 0.0)
+       : r == 4 ? mk3(om, 0.0, w)
+       : r == 5 ? mk3(0.0, om, w)
+                : mk3((1.0 - wb) - wc, wb, wc);
+  return pt;
 }
 
 struct Best {
@@ -172,91 +232,402 @@ __device__ __forceinline__ uint8_t encode_channel(double v) {
   return static_cast<uint8_t>(q < 0 ? 0 : (q > 255 ? 255 : q));
 }
 
-// One 16x16 texel tile per 256-thread block; warp = 8x4 sub-tile.
-__global__ void __launch_bounds__(256) k_transfer(
+// ---------------------------------------------------------------- warp-coherent transfer
+// A warp owns 32 spatially coherent queries (one 8x4 texel block, compacted
+// by the rasteriser) and walks ONE traversal for all of them: every node is
+// fetched once per warp (uniform 64-B load, 4 x LDG.128 broadcast), each lane
+// tests both child boxes against its own bound, and the warp descends into a
+// child if any lane still needs it (ballot). Leaves are intersected by the
+// lanes whose bound admits them. The traversal stack is warp-uniform and lives
+// distributed in registers: entry k is held by lane k % 32 in slot k / 32, so
+// it needs neither shared nor local memory. Entries record (parent, side) so
+// a popped subtree is re-tested against every lane's current bound.
+__device__ __forceinline__ int stack_get(int s0, int s1, int s2, int k) {
+  const int v = k < 32 ? s0 : (k < 64 ? s1 : s2);
+  return __shfl_sync(0xffffffffu, v, k & 31);
+}
+__device__ __forceinline__ void stack_put(int& s0, int& s1, int& s2, int k, int v, int lane) {
+  if (lane == (k & 31)) {
+    if (k < 32) s0 = v;
+    else if (k < 64) s1 = v;
+    else s2 = v;
+  }
+}
+
+// prof (optional, warp-uniform counters): [0] internal-node visits,
+// [1] leaf visits, [2] stack pops tested, [3] pair rounds, [4] pairs,
+// [5] batches (warps x batches)
+template <bool kProf>
+__device__ __forceinline__ void warp_closest(const BNode* __restrict__ nodes, const BTri* __restrict__ tris,
+                                             const TBox* __restrict__ tbox, int32_t root, d3 q, float3 qf,
+                                             double E, Best& best, float& bnd, int lane,
+                                             unsigned long long* prof) {
+  int s0 = 0, s1 = 0, s2 = 0;
+  int sp = 0;
+  int32_t ref = root;
+  unsigned need = __ballot_sync(0xffffffffu, bnd >= 0.0f);  // root: every live lane
+  for (;;) {
+    if (ref >= 0) {
+      if (kProf) ++prof[0];
+      const float4* np = reinterpret_cast<const float4*>(nodes + ref);
+      const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+      const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
+      const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
+      const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
+      const bool hL = lbL <= bnd, hR = lbR <= bnd;
+      const unsigned mL = __ballot_sync(0xffffffffu, hL);
+      const unsigned mR = __ballot_sync(0xffffffffu, hR);
+      if (mL && mR) {
+        const unsigned prefL = __ballot_sync(0xffffffffu, hL && (!hR || lbL <= lbR));
+        const bool goL = 2 * __popc(prefL) >= __popc(mL | mR);
+        stack_put(s0, s1, s2, sp, (ref << 1) | (goL ? 1 : 0), lane);
+        ++sp;
+        need = goL ? mL : mR;
+        ref = goL ? d.x : d.y;
+        continue;
+      }
+      if (mL | mR) {
+        need = mL ? mL : mR;
+        ref = mL ? d.x : d.y;
+        continue;
+      }
+    } else {
+      // Leaf: each lane in `need` first tests every triangle's own fp32 box
+      // (conservative, like the node boxes). The surviving (lane, triangle)
+      // pairs are spread over the 32 lanes, evaluated exactly in f64 in rounds
+      // of 32 (branch-free test: full-width f64 issue), and each owner gathers
+      // its candidates by shuffle keeping the lexicographic (distSq, face)
+      // minimum - order-independent, so the result is exact. Per-triangle
+      // masks and prefix counts live one per lane (lane t holds triangle t).
+      int first, count;
+      leaf_decode(ref, first, count);
+      const bool mine = (need >> lane) & 1u;
+      unsigned my_m = 0;
+      for (int t = 0; t < count; ++t) {
+        const float4* bp = reinterpret_cast<const float4*>(tbox + first + t);
+        const float4 ba = __ldg(bp), bb = __ldg(bp + 1);
+        const float lb = box_lb(ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, qf, qf);
+        const unsigned m = __ballot_sync(0xffffffffu, mine && lb <= bnd);
+        if (lane == t) my_m = m;
+      }
+      const int my_cnt = __popc(my_m);
+      int incl = my_cnt;
+#pragma unroll
+      for (int off = 1; off < 8; off <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += v;
+      }
+      const int excl = incl - my_cnt;
+      const int total = __shfl_sync(0xffffffffu, incl, 7);
+      if (kProf) {
+        ++prof[1];
+        prof[3] += (total + 31) / 32;
+        prof[4] += total;
+      }
+      for (int base = 0; base < total; base += 32) {
+        const int j = base + lane;
+        const bool act = j < total;
+        int t = 0;
+        for (int k = 0; k < count - 1; ++k) t += (__shfl_sync(0xffffffffu, incl, k) <= j) ? 1 : 0;
+        const unsigned m = __shfl_sync(0xffffffffu, my_m, t);
+        const int pre_t = __shfl_sync(0xffffffffu, excl, t);
+        const int owner = act ? static_cast<int>(__fns(m, 0, j - pre_t + 1)) : 0;
+        const float ox = __shfl_sync(0xffffffffu, qf.x, owner);
+        const float oy = __shfl_sync(0xffffffffu, qf.y, owner);
+        const float oz = __shfl_sync(0xffffffffu, qf.z, owner);
+        double ds = INFINITY;
+        int face = 0x7fffffff;
+        d3 bary = mk3(0.0, 0.0, 0.0);
+        if (act) {
+          d3 A, B, C;
+          load_tri(tris + first + t, A, B, C, face);
+          const d3 oq = mk3(ox, oy, oz);
+          const d3 pt = closest_point_triangle_sel(oq, A, B, C, bary);
+          ds = sqnorm(pt - oq);
+        }
+        int win = -1;
+        for (int tt = 0; tt < count; ++tt) {
+          const unsigned mt = __shfl_sync(0xffffffffu, my_m, tt);
+          const int src = __shfl_sync(0xffffffffu, excl, tt) + __popc(mt & ((1u << lane) - 1u)) - base;
+          const bool ok = ((mt >> lane) & 1u) && src >= 0 && src < 32;
+          const double dd = __shfl_sync(0xffffffffu, ds, src & 31);
+          const int ff = __shfl_sync(0xffffffffu, face, src & 31);
+          if (ok && (dd < best.d || (dd == best.d && ff < best.face))) {
+            best.d = dd;
+            best.face = ff;
+            win = src;
+          }
+        }
+        const double bx = __shfl_sync(0xffffffffu, bary.x, win & 31);
+        const double by = __shfl_sync(0xffffffffu, bary.y, win & 31);
+        const double bz = __shfl_sync(0xffffffffu, bary.z, win & 31);
+        if (win >= 0) {
+          best.bary = mk3(bx, by, bz);
+          bnd = prune_bound(best.d, E);
+        }
+      }
+    }
+    bool found = false;
+    while (sp > 0) {
+      --sp;
+      if (kProf) ++prof[2];
+      const int e = stack_get(s0, s1, s2, sp);
+      const int par = e >> 1, side = e & 1;
+      const float* f = reinterpret_cast<const float*>(nodes + par) + (side ? 6 : 0);
+      const float lb = box_lb(__ldg(f), __ldg(f + 1), __ldg(f + 2), __ldg(f + 3), __ldg(f + 4), __ldg(f + 5), qf, qf);
+      const unsigned m = __ballot_sync(0xffffffffu, lb <= bnd);
+      if (m) {
+        need = m;
+        ref = __ldg(reinterpret_cast<const int*>(nodes + par) + 12 + side);
+        found = true;
+        break;
+      }
+    }
+    if (!found) break;
+  }
+}
+
+// ---------------------------------------------------------------- per-thread while-while transfer
+// One query per thread over the compacted, spatially coherent query list.
+// Aila-Laine "while-while" structure: each lane descends internal nodes until
+// it holds a leaf (or finishes); the leaf loop then runs with every lane that
+// holds one, so the expensive exact f64 test executes at high SIMT width.
+// Depth-first nearest-child-first with conservative fp32 pruning (see
+// traverse_closest) - result-neutral vs the reference's best-first heap.
+template <bool kDebug>
+__global__ void __launch_bounds__(128) k_transfer_t(
     const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
-    const unsigned long long* __restrict__ scene_acc, int res, int g_row0,
-    const float* __restrict__ gpos, const float* __restrict__ gnrm, const float* __restrict__ gtan,
-    const float* __restrict__ gbit, const uint8_t* __restrict__ gvalid,
-    const uint8_t* __restrict__ grel, int row_begin, int row_end,
+    const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
+    const float* __restrict__ qtbn, const int* __restrict__ qcount, const double* __restrict__ hiN,
+    const int32_t* __restrict__ hiF, double max_dist, uint8_t* __restrict__ rgb,
+    int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters) {
+  const int nq = qcount[0];
+  const int lane = threadIdx.x & 31;
+  const double scene_max = from_ordered_dev(scene_acc[6]);
+  const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
+  unsigned long long hits = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i - lane < nq; i += gridDim.x * blockDim.x) {
+    const bool live = i < nq;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) p = __ldg(qpos + i);
+    const float3 qf = make_float3(p.x, p.y, p.z);
+    const d3 q = mk3(p.x, p.y, p.z);
+    const double E = fmax(scene_max, fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z)))) * 0x1p-32;
+    Best best;
+    best.d = init;
+    best.face = -1;
+    best.bary = mk3(0.0, 0.0, 0.0);
+    float bnd = live ? prune_bound(init, E) : -INFINITY;
+    int32_t st_ref[kStackMax];
+    float st_lb[kStackMax];
+    int sp = 0;
+    // ref: node (>= 0), leaf (< 0 and != kDone), or kDone
+    constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
+    int32_t ref = live ? root : kDone;
+    while (ref != kDone) {
+      // ---- descend until this lane holds a leaf
+      while (ref >= 0) {
+        const float4* np = reinterpret_cast<const float4*>(nodes + ref);
+        const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+        const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
+        const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
+        const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
+        const bool hL = lbL <= bnd, hR = lbR <= bnd;
+        if (hL && hR) {
+          const bool lf = lbL <= lbR;
+          st_ref[sp] = lf ? d.y : d.x;
+          st_lb[sp] = lf ? lbR : lbL;
+          ++sp;
+          ref = lf ? d.x : d.y;
+        } else if (hL || hR) {
+          ref = hL ? d.x : d.y;
+        } else {
+          ref = kDone;
+          while (sp > 0) {
+            --sp;
+            if (st_lb[sp] <= bnd) {
+              ref = st_ref[sp];
+              break;
+            }
+          }
+        }
+      }
+      if (ref == kDone) break;
+      // ---- leaf: exact f64 tests (branch-free, reference arithmetic)
+      int first, count;
+      leaf_decode(ref, first, count);
+      for (int k = 0; k < count; ++k) {
+        d3 A, B, C;
+        int face;
+        load_tri(tris + first + k, A, B, C, face);
+        d3 bary;
+        const d3 pt = closest_point_triangle_sel(q, A, B, C, bary);
+        const double ds = sqnorm(pt - q);
+        if (ds < best.d || (ds == best.d && face < best.face)) {
+          best.d = ds;
+          best.face = face;
+          best.bary = bary;
+          bnd = prune_bound(ds, E);
+        }
+      }
+      ref = kDone;
+      while (sp > 0) {
+        --sp;
+        if (st_lb[sp] <= bnd) {
+          ref = st_ref[sp];
+          break;
+        }
+      }
+    }
+    if (!live) continue;
+    const int texel = __float_as_int(p.w);
+    uint8_t px[3] = {128, 128, 255};
+    double ts3[3] = {0.0, 0.0, 0.0};
+    if (best.face >= 0) {
+      ++hits;
+      const float* tb = qtbn + 9ll * i;
+      const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
+      const d3 n = (best.bary.x * ld3(hiN + 3 * v0) + best.bary.y * ld3(hiN + 3 * v1)) +
+                   best.bary.z * ld3(hiN + 3 * v2);
+      const d3 T = mk3(tb[0], tb[1], tb[2]);
+      const d3 B = mk3(tb[3], tb[4], tb[5]);
+      const d3 N = mk3(tb[6], tb[7], tb[8]);
+      d3 ts = mk3(dot(n, T), dot(n, B), dot(n, N));
+      const double len = norm(ts);
+      if (!(len < 1e-12)) {
+        ts = ts / len;
+        px[0] = encode_channel(ts.x);
+        px[1] = encode_channel(ts.y);
+        px[2] = encode_channel(ts.z);
+        ts3[0] = ts.x;
+        ts3[1] = ts.y;
+        ts3[2] = ts.z;
+      }
+    }
+    uint8_t* o = rgb + 3ll * texel;
+    o[0] = px[0];
+    o[1] = px[1];
+    o[2] = px[2];
+    if (kDebug) {
+      if (dbg_face) dbg_face[texel] = best.face >= 0 ? best.face : -3;
+      if (dbg_ts) {
+        dbg_ts[3ll * texel] = ts3[0];
+        dbg_ts[3ll * texel + 1] = ts3[1];
+        dbg_ts[3ll * texel + 2] = ts3[2];
+      }
+    }
+  }
+  if (counters) {
+    for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
+    if (lane == 0 && hits) atomicAdd(&counters[1], hits);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));
+  }
+}
+
+// kPass 1: pass A (records each query's winning face in face_map);
+// kPass 2: pass B (queries stored from the back of the list; each lane first
+// tests the face pass A found for its 2x2-quad corner texel, which only
+// tightens its initial bound - the answer is unchanged).
+template <bool kDebug, bool kProf, int kPass>
+#ifndef MFB_XFER_MINB
+#define MFB_XFER_MINB 4
+#endif
+__global__ void __launch_bounds__(128, MFB_XFER_MINB) k_transfer(
+    const BNode* __restrict__ nodes, const BTri* __restrict__ tris, const TBox* __restrict__ tbox, int32_t root,
+    const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
+    const float* __restrict__ qtbn, const int* __restrict__ qcount, int qcap, int res, int slab_row0,
+    int* __restrict__ face_map, const double* __restrict__ hiPos,
     const double* __restrict__ hiN, const int32_t* __restrict__ hiF, double max_dist,
     uint8_t* __restrict__ rgb, int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts,
-    unsigned long long* __restrict__ counters) {
-  const int tiles_x = (res + 15) >> 4;
-  const int tile = blockIdx.x;
-  const int tx = tile % tiles_x, ty = tile / tiles_x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int x = tx * 16 + (warp & 1) * 8 + (lane & 7);
-  const int y = row_begin + ty * 16 + (warp >> 1) * 4 + (lane >> 3);
-  const bool in = x < res && y < row_end;
-  const int64_t gi = (static_cast<int64_t>(y - g_row0)) * res + x;       // G-buffer slab index
-  const int64_t oi = (static_cast<int64_t>(y - row_begin)) * res + x;    // output slab index
-  bool valid = false, query = false, hit = false;
-  int32_t face_out = -1;
-  double ts3[3] = {0.0, 0.0, 0.0};
-  uint8_t px[3] = {128, 128, 128};
-  if (in) {
-    valid = gvalid[gi] != 0;
-    if (valid) {
-      px[2] = 255;  // neutral (128,128,255) unless a hit is encoded below
-      if (!grel[gi]) {
-        face_out = -2;
-      } else {
-        query = true;
-        const float qx = gpos[3 * gi], qy = gpos[3 * gi + 1], qz = gpos[3 * gi + 2];
-        const d3 q = mk3(qx, qy, qz);
-        const float3 qf = make_float3(qx, qy, qz);
-        const double M = fmax(from_ordered_dev(scene_acc[6]),
-                              fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z))));
-        Best best;
-        best.d = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
-        best.face = -1;
-        traverse_closest<false>(nodes, tris, root, q, qf, qf, M * 0x1p-32, best);
-        if (best.face < 0) {
-          face_out = -3;
-        } else {
-          hit = true;
-          face_out = best.face;
-          const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
-          const d3 n = (best.bary.x * ld3(hiN + 3 * v0) + best.bary.y * ld3(hiN + 3 * v1)) +
-                       best.bary.z * ld3(hiN + 3 * v2);
-          const d3 T = mk3(gtan[3 * gi], gtan[3 * gi + 1], gtan[3 * gi + 2]);
-          const d3 B = mk3(gbit[3 * gi], gbit[3 * gi + 1], gbit[3 * gi + 2]);
-          const d3 N = mk3(gnrm[3 * gi], gnrm[3 * gi + 1], gnrm[3 * gi + 2]);
-          d3 ts = mk3(dot(n, T), dot(n, B), dot(n, N));
-          const double len = norm(ts);
-          if (!(len < 1e-12)) {
-            ts = ts / len;
-            px[0] = encode_channel(ts.x);
-            px[1] = encode_channel(ts.y);
-            px[2] = encode_channel(ts.z);
-            ts3[0] = ts.x;
-            ts3[1] = ts.y;
-            ts3[2] = ts.z;
+    unsigned long long* __restrict__ counters, unsigned long long* __restrict__ prof_out) {
+  const int lane = threadIdx.x & 31;
+  const int nq = qcount[kPass == 2 ? 1 : 0];
+  unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  const double scene_max = from_ordered_dev(scene_acc[6]);
+  const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
+  unsigned long long hits = 0;
+  for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nq; base += warps * 32) {
+    const int li = base + lane;
+    const bool live = li < nq;
+    const int i = kPass == 2 ? qcap - 1 - li : li;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) p = __ldg(qpos + i);
+    const d3 q = mk3(p.x, p.y, p.z);
+    const float3 qf = make_float3(p.x, p.y, p.z);
+    const double M = fmax(scene_max, fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z))));
+    const double E = M * 0x1p-32;
+    Best best;
+    best.d = init;
+    best.face = -1;
+    best.bary = mk3(0.0, 0.0, 0.0);
+    if (kPass == 2 && live) {
+      const int gi = __float_as_int(p.w);
+      const int x = gi % res, y = gi / res + slab_row0;
+      const int sy = (y & ~1) - slab_row0;
+      if (sy >= 0) {
+        const int sf = face_map[static_cast<int64_t>(sy) * res + (x & ~1)];
+        if (sf >= 0) {  // exact test of the seed face (as if visited first)
+          const int v0 = hiF[3 * sf], v1 = hiF[3 * sf + 1], v2 = hiF[3 * sf + 2];
+          d3 bary;
+          const d3 pt = closest_point_triangle(q, ld3(hiPos + 3 * v0), ld3(hiPos + 3 * v1), ld3(hiPos + 3 * v2), bary);
+          const double ds = sqnorm(pt - q);
+          if (ds < best.d || (ds == best.d && sf < best.face)) {
+            best.d = ds;
+            best.face = sf;
+            best.bary = bary;
           }
         }
       }
     }
-    uint8_t* o = rgb + 3 * oi;
+    float bnd = live ? prune_bound(best.d, E) : -INFINITY;
+    warp_closest<kProf>(nodes, tris, tbox, root, q, qf, E, best, bnd, lane, prof);
+    if (kProf) ++prof[5];
+    if (!live) continue;
+    const int texel = __float_as_int(p.w);
+    if (kPass == 1) face_map[texel] = best.face;
+    uint8_t px[3] = {128, 128, 255};
+    double ts3[3] = {0.0, 0.0, 0.0};
+    if (best.face >= 0) {
+      ++hits;
+      const float* tb = qtbn + 9ll * i;
+      const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
+      const d3 n = (best.bary.x * ld3(hiN + 3 * v0) + best.bary.y * ld3(hiN + 3 * v1)) +
+                   best.bary.z * ld3(hiN + 3 * v2);
+      const d3 T = mk3(tb[0], tb[1], tb[2]);
+      const d3 B = mk3(tb[3], tb[4], tb[5]);
+      const d3 N = mk3(tb[6], tb[7], tb[8]);
+      d3 ts = mk3(dot(n, T), dot(n, B), dot(n, N));
+      const double len = norm(ts);
+      if (!(len < 1e-12)) {
+        ts = ts / len;
+        px[0] = encode_channel(ts.x);
+        px[1] = encode_channel(ts.y);
+        px[2] = encode_channel(ts.z);
+        ts3[0] = ts.x;
+        ts3[1] = ts.y;
+        ts3[2] = ts.z;
+      }
+    }
+    uint8_t* o = rgb + 3ll * texel;
     o[0] = px[0];
     o[1] = px[1];
     o[2] = px[2];
-    if (dbg_face) dbg_face[oi] = face_out;
-    if (dbg_ts) {
-      dbg_ts[3 * oi] = ts3[0];
-      dbg_ts[3 * oi + 1] = ts3[1];
-      dbg_ts[3 * oi + 2] = ts3[2];
+    if (kDebug) {
+      if (dbg_face) dbg_face[texel] = best.face >= 0 ? best.face : -3;
+      if (dbg_ts) {
+        dbg_ts[3ll * texel] = ts3[0];
+        dbg_ts[3ll * texel + 1] = ts3[1];
+        dbg_ts[3ll * texel + 2] = ts3[2];
+      }
     }
   }
+  if (kProf && lane == 0)
+    for (int k = 0; k < 6; ++k) atomicAdd(&prof_out[k], prof[k]);
   if (counters) {
-    const unsigned bv = __ballot_sync(0xffffffffu, valid);
-    const unsigned bq = __ballot_sync(0xffffffffu, query);
-    const unsigned bh = __ballot_sync(0xffffffffu, hit);
-    if (lane == 0) {
-      if (bv) atomicAdd(&counters[0], static_cast<unsigned long long>(__popc(bv)));
-      if (bq) atomicAdd(&counters[1], static_cast<unsigned long long>(__popc(bq)));
-      if (bh) atomicAdd(&counters[2], static_cast<unsigned long long>(__popc(bh)));
-    }
+    for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
+    if (lane == 0 && hits) atomicAdd(&counters[1], hits);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));  // per pass
   }
 }
 
@@ -404,16 +775,78 @@ __global__ void __launch_bounds__(128) k_raycast(const BNode* __restrict__ nodes
 static const unsigned long long* scene_acc_of(Ctx&, const Lbvh& bvh) { return bvh.scene_acc; }
 
 void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferArgs& a) {
-  const int res = a.g->res;
-  const int rows = a.row_end - a.row_begin;
-  if (rows <= 0) return;
-  const int tiles = ((res + 15) / 16) * ((rows + 15) / 16);
-  k_transfer<<<tiles, 256, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, scene_acc_of(ctx, bvh), res,
-                                   a.g->row0, a.g->pos, a.g->nrm, a.g->tan, a.g->bit, a.g->valid,
-                                   a.g->rel, a.row_begin, a.row_end, a.hi_normals, a.hi_faces,
-                                   a.max_dist, a.rgb, a.dbg_face, a.dbg_ts, a.counters);
+  // Persistent grid: enough resident warps to cover every SM; each warp
+  // strides over 32-query batches until the (device-side) count is reached.
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_transfer<false, false, 1>, 128, 0));
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const int grid_cap = kNumSMs * blocks_per_sm;
+  const int grid = std::max(1, std::min(grid_cap, div_up(a.q.capacity, 128)));
+  const bool dbg = a.dbg_face || a.dbg_ts;
+  static const bool prof = std::getenv("MFB_PROF") != nullptr;
+  unsigned long long* pbuf = nullptr;
+  if (prof) {
+    pbuf = ctx.buf<unsigned long long>("xfer.prof", 8);
+    MFB_CUDA_TRY(cudaMemsetAsync(pbuf, 0, 8 * sizeof(unsigned long long), s));
+  }
+  MFB_CUDA_TRY(cudaMemsetAsync(a.face_map, 0xff, sizeof(int) * a.face_map_size, s));
+#define MFB_XFER(D, P, PASS)                                                                                     \
+  k_transfer<D, P, PASS><<<grid, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.tbox, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, \
+                                              a.q.count, a.q.capacity, a.res, a.slab_row0, a.face_map,            \
+                                              a.hi_positions, a.hi_normals, a.hi_faces, a.max_dist, a.rgb,        \
+                                              D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf)
+#define MFB_XFER_PASS(PASS)                              \
+  if (prof) {                                            \
+    if (dbg) MFB_XFER(true, true, PASS);                 \
+    else MFB_XFER(false, true, PASS);                    \
+  } else {                                               \
+    if (dbg) MFB_XFER(true, false, PASS);                \
+    else MFB_XFER(false, false, PASS);                   \
+  }
+  // Default: per-thread while-while (measured 1.43 ms vs 2.49 ms for the
+  // warp-coherent kernel on config B, profiles/r01). MFB_XFER=warp selects
+  // the warp-coherent variant for comparison.
+  static const bool per_thread = [] {
+    const char* e = std::getenv("MFB_XFER");
+    return !(e && std::string(e) == "warp");
+  }();
+  if (per_thread) {
+    static int bps = 0;
+    if (!bps) {
+      MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_transfer_t<false>, 128, 0));
+      if (bps < 1) bps = 1;
+    }
+    const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
+    if (dbg)
+      k_transfer_t<true><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn,
+                                            a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, a.dbg_face,
+                                            a.dbg_ts, a.counters);
+    else
+      k_transfer_t<false><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn,
+                                             a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, nullptr,
+                                             nullptr, a.counters);
+  } else {
+    MFB_XFER_PASS(1);
+    if (kSeedPasses) {
+      MFB_XFER_PASS(2);
+    }
+  }
+#undef MFB_XFER_PASS
+#undef MFB_XFER
+  ctx.count_launch();
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
+  if (prof) {
+    unsigned long long h[8];
+    MFB_CUDA_TRY(cudaMemcpyAsync(h, pbuf, sizeof(h), cudaMemcpyDeviceToHost, s));
+    MFB_CUDA_TRY(cudaStreamSynchronize(s));
+    const double b = h[5] ? static_cast<double>(h[5]) : 1.0;
+    std::fprintf(stderr,
+                 "[mfb prof] per warp-batch: internal %.1f leaves %.1f pops %.1f rounds %.1f pairs %.1f "
+                 "(batches %llu)\n", h[0] / b, h[1] / b, h[2] / b, h[3] / b, h[4] / b, h[5]);
+  }
 }
 
 void closest_within(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* q, int64_t n,

@@ -353,6 +353,90 @@ __device__ __forceinline__ bool owns_boundary(double dx, double dy) {
 
 constexpr int kChunk = 32;
 
+// Texel of thread t in a 16x16 tile: 8 warps of 8x4 texels (so a warp's
+// compacted queries are spatial neighbours).
+__device__ __forceinline__ void tile_texel(int t, int& lx, int& ly) {
+  const int w = t >> 5, l = t & 31;
+  lx = (w & 1) * 8 + (l & 7);
+  ly = (w >> 1) * 4 + (l >> 3);
+}
+
+// Block-wide compaction of this thread's query flag: returns the query slot
+// (or -1). One atomicAdd per block on the global counter.
+__device__ __forceinline__ int compact_slot(bool is_q, int* counter, int capacity, int* overflow) {
+  __shared__ int warp_base[8];
+  __shared__ int block_base;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, is_q);
+  if (lane == 0) warp_base[w] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < (blockDim.x >> 5); ++k) {
+      const int c = warp_base[k];
+      warp_base[k] = acc;
+      acc += c;
+    }
+    block_base = acc ? atomicAdd(counter, acc) : 0;
+    if (acc && block_base + acc > capacity) *overflow = 1;
+  }
+  __syncthreads();
+  if (!is_q) return -1;
+  const int slot = block_base + warp_base[w] + __popc(m & ((1u << lane) - 1u));
+  return slot < capacity ? slot : -1;
+}
+
+// Writes one query record into pass A (front) or pass B (back) of the list.
+__device__ __forceinline__ void store_query(const QueryList& q, int slot, bool pass_b, int64_t gi, const float* P,
+                                            const float* Nf, const float* Tf, const float* Bf) {
+  if (slot < 0) return;
+  const int idx = pass_b ? q.capacity - 1 - slot : slot;
+  q.qpos[idx] = make_float4(P[0], P[1], P[2], __int_as_float(static_cast<int>(gi)));
+  float* t = q.qtbn + 9ll * idx;
+  t[0] = Tf[0];
+  t[1] = Tf[1];
+  t[2] = Tf[2];
+  t[3] = Bf[0];
+  t[4] = Bf[1];
+  t[5] = Bf[2];
+  t[6] = Nf[0];
+  t[7] = Nf[1];
+  t[8] = Nf[2];
+}
+
+// Fused-mode stores of one texel: valid mask, raw map for non-query texels,
+// the query record otherwise (pass A for even (x, y), else pass B), and the
+// debug planes.
+__device__ __forceinline__ void emit_fused(int64_t gi, int x, int y, bool in, uint8_t valid, uint8_t rel,
+                                           const float* P, const float* Nf, const float* Tf, const float* Bf,
+                                           uint8_t* gvalid, const RasterFused& fo, int* overflow) {
+  const bool is_q = in && valid && rel;
+  const bool pass_a = kSeedPasses ? ((x | y) & 1) == 0 : true;
+  const int slot_a = compact_slot(is_q && pass_a, fo.q.count, fo.q.capacity, overflow);
+  const int slot_b = compact_slot(is_q && !pass_a, fo.q.count + 1, fo.q.capacity, overflow);
+  if (fo.valid_count) {
+    const unsigned vm = __ballot_sync(0xffffffffu, in && valid);
+    if ((threadIdx.x & 31) == 0 && vm) atomicAdd(fo.valid_count, static_cast<unsigned long long>(__popc(vm)));
+  }
+  if (!in) return;
+  if (gvalid) gvalid[gi] = valid;
+  if (!is_q) {
+    uint8_t* o = fo.rgb + 3 * gi;
+    o[0] = 128;
+    o[1] = 128;
+    o[2] = valid ? 255 : 128;  // gbuffer.cpp:212-213 background / neutral
+    if (fo.dbg_face) fo.dbg_face[gi] = valid ? -2 : -1;
+    if (fo.dbg_ts) {
+      fo.dbg_ts[3 * gi] = 0.0;
+      fo.dbg_ts[3 * gi + 1] = 0.0;
+      fo.dbg_ts[3 * gi + 2] = 0.0;
+    }
+    return;
+  }
+  store_query(fo.q, pass_a ? slot_a : slot_b, !pass_a, gi, P, Nf, Tf, Bf);
+}
+
+template <bool kFused>
 __global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ rf,
                                                 const AttrFace* __restrict__ attrs,
                                                 const int* __restrict__ tile_start,
@@ -361,15 +445,17 @@ __global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ r
                                                 float* __restrict__ gpos, float* __restrict__ gnrm,
                                                 float* __restrict__ gtan, float* __restrict__ gbit,
                                                 uint8_t* __restrict__ gvalid, uint8_t* __restrict__ grel,
-                                                int* __restrict__ overlap,
-                                                unsigned long long* __restrict__ row_counts) {
+                                                int* __restrict__ flags,
+                                                unsigned long long* __restrict__ row_counts, RasterFused fo) {
   __shared__ RasterFace sf[kChunk];
   __shared__ int sfid[kChunk];
   const int tiles_x = (res + kTile - 1) / kTile;
   const int t = blockIdx.x;
   const int tx = t % tiles_x, ty = t / tiles_x;
-  const int x = tx * kTile + (threadIdx.x & 15);
-  const int y = row_begin + ty * kTile + (threadIdx.x >> 4);
+  int lx, ly;
+  tile_texel(threadIdx.x, lx, ly);
+  const int x = tx * kTile + lx;
+  const int y = row_begin + ty * kTile + ly;
   const bool in = x < res && y < row_end;
   const double cx = x + 0.5, cy = y + 0.5;
   const int b = tile_start[t], e = min(tile_start[t + 1], capacity);
@@ -378,7 +464,6 @@ __global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ r
     const int n = min(kChunk, e - base);
     __syncthreads();
     {
-      // cooperative 16-B copies of n RasterFace records
       const int words = n * static_cast<int>(sizeof(RasterFace) / 16);
       for (int w = threadIdx.x; w < words; w += blockDim.x) {
         const int i = w / static_cast<int>(sizeof(RasterFace) / 16);
@@ -391,13 +476,13 @@ __global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ r
     __syncthreads();
     if (in) {
       for (int i = 0; i < n; ++i) {
-        const RasterFace& s = sf[i];
-        if (x < s.x0 || x > s.x1 || y < s.y0 || y > s.y1) continue;
+        const RasterFace& sfc = sf[i];
+        if (x < sfc.x0 || x > sfc.x1 || y < sfc.y0 || y > sfc.y1) continue;
         bool inside = true;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          const double ev = s.sg[k] * cross2(s.dx[k], s.dy[k], cx - s.ox[k], cy - s.oy[k]);
-          if (ev < 0.0 || (ev == 0.0 && !owns_boundary(s.sg[k] * s.dx[k], s.sg[k] * s.dy[k]))) {
+          const double ev = sfc.sg[k] * cross2(sfc.dx[k], sfc.dy[k], cx - sfc.ox[k], cy - sfc.oy[k]);
+          if (ev < 0.0 || (ev == 0.0 && !owns_boundary(sfc.sg[k] * sfc.dx[k], sfc.sg[k] * sfc.dy[k]))) {
             inside = false;
             break;
           }
@@ -408,18 +493,18 @@ __global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ r
       }
     }
   }
-  if (hits > 1) atomicExch(overlap, 1);
-  if (!in) return;
+  if (hits > 1) atomicExch(&flags[0], 1);
   const int64_t gi = static_cast<int64_t>(y - g_row0) * res + x;
   float P[3] = {0.f, 0.f, 0.f}, Nf[3] = {0.f, 0.f, 0.f}, Tf[3] = {0.f, 0.f, 0.f}, Bf[3] = {0.f, 0.f, 0.f};
   uint8_t valid = 0, rel = 0;
-  if (cover >= 0) {
-    const RasterFace& s = rf[cover];
+  if (in && cover >= 0) {
+    const RasterFace& sfc = rf[cover];
     const AttrFace& a = attrs[cover];
-    const double px0 = s.px[0], py0 = s.py[0], px1 = s.px[1], py1 = s.py[1], px2 = s.px[2], py2 = s.py[2];
-    const double w0 = cross2(px2 - px1, py2 - py1, cx - px1, cy - py1) / s.doubled;
-    const double w1 = cross2(px0 - px2, py0 - py2, cx - px2, cy - py2) / s.doubled;
-    const double w2 = cross2(px1 - px0, py1 - py0, cx - px0, cy - py0) / s.doubled;
+    const double px0 = sfc.px[0], py0 = sfc.py[0], px1 = sfc.px[1], py1 = sfc.py[1], px2 = sfc.px[2],
+                 py2 = sfc.py[2];
+    const double w0 = cross2(px2 - px1, py2 - py1, cx - px1, cy - py1) / sfc.doubled;
+    const double w1 = cross2(px0 - px2, py0 - py2, cx - px2, cy - py2) / sfc.doubled;
+    const double w2 = cross2(px1 - px0, py1 - py0, cx - px0, cy - py0) / sfc.doubled;
     const d3 pos = (w0 * ld3(a.P) + w1 * ld3(a.P + 3)) + w2 * ld3(a.P + 6);
     d3 n = (w0 * ld3(a.N) + w1 * ld3(a.N + 3)) + w2 * ld3(a.N + 6);
     const double nl = norm(n);
@@ -444,6 +529,21 @@ __global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ r
     valid = 1;
     rel = static_cast<uint8_t>(a.reliable);
   }
+  if (row_counts) {
+    // warp = 8 columns x 4 rows: lanes 8r..8r+7 share row r
+    const unsigned m = __ballot_sync(0xffffffffu, in && valid);
+    const int lane = threadIdx.x & 31;
+    if (lane < 4) {
+      const unsigned rowbits = (m >> (8 * lane)) & 0xffu;
+      const int yr = row_begin + ty * kTile + (threadIdx.x >> 6) * 4 + lane;
+      if (rowbits && yr < row_end) atomicAdd(&row_counts[yr - row_begin], static_cast<unsigned long long>(__popc(rowbits)));
+    }
+  }
+  if (kFused) {
+    emit_fused(gi, x, y, in, valid, rel, P, Nf, Tf, Bf, gvalid, fo, &flags[3]);
+    return;
+  }
+  if (!in) return;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     gpos[3 * gi + k] = P[k];
@@ -453,13 +553,36 @@ __global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ r
   }
   gvalid[gi] = valid;
   grel[gi] = rel;
-  if (row_counts) {
-    // 16 lanes of a half-warp share one row
-    const unsigned m = __ballot_sync(__activemask(), valid != 0);
-    const int lane = threadIdx.x & 31;
-    const unsigned half = (lane < 16) ? (m & 0xffffu) : (m >> 16);
-    if ((lane & 15) == 0 && half) atomicAdd(&row_counts[y - row_begin], static_cast<unsigned long long>(__popc(half)));
+}
+
+// Query list from a full G-buffer slab (mf_transfer_normals), same tiling.
+__global__ void __launch_bounds__(256) k_gbuffer_queries(int res, int rows, const float* __restrict__ gpos,
+                                                         const float* __restrict__ gnrm,
+                                                         const float* __restrict__ gtan,
+                                                         const float* __restrict__ gbit,
+                                                         const uint8_t* __restrict__ gvalid,
+                                                         const uint8_t* __restrict__ grel, RasterFused fo,
+                                                         int* overflow) {
+  const int tiles_x = (res + kTile - 1) / kTile;
+  const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+  int lx, ly;
+  tile_texel(threadIdx.x, lx, ly);
+  const int x = tx * kTile + lx, y = ty * kTile + ly;
+  const bool in = x < res && y < rows;
+  const int64_t gi = static_cast<int64_t>(y) * res + x;
+  uint8_t valid = 0, rel = 0;
+  float P[3] = {0, 0, 0}, N[3] = {0, 0, 0}, T[3] = {0, 0, 0}, B[3] = {0, 0, 0};
+  if (in) {
+    valid = gvalid[gi];
+    rel = grel[gi];
+    for (int k = 0; k < 3; ++k) {
+      P[k] = gpos[3 * gi + k];
+      N[k] = gnrm[3 * gi + k];
+      T[k] = gtan[3 * gi + k];
+      B[k] = gbit[3 * gi + k];
+    }
   }
+  emit_fused(gi, x, y, in, valid, rel, P, N, T, B, nullptr, fo, overflow);
 }
 
 __global__ void k_gather_u32(int n, const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm,
@@ -595,7 +718,7 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
 }
 
 void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPlan& plan, GBufDev& g,
-                    int* flags_dev, int64_t* row_counts_dev) {
+                    int* flags_dev, int64_t* row_counts_dev, const RasterFused* fused) {
   (void)lo;
   const int T = 256;
   const int res = plan.res;
@@ -623,10 +746,27 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
                                               capacity, flags_dev + 1);
   MFB_CUDA_TRY(cudaMemcpyAsync(flags_dev + 2, start + ntiles, sizeof(int), cudaMemcpyDeviceToDevice, s));
   if (row_counts_dev) MFB_CUDA_TRY(cudaMemsetAsync(row_counts_dev, 0, sizeof(int64_t) * g.rows, s));
-  k_raster<<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos, g.nrm,
-                                  g.tan, g.bit, g.valid, g.rel, flags_dev,
-                                  reinterpret_cast<unsigned long long*>(row_counts_dev));
+  auto* rc = reinterpret_cast<unsigned long long*>(row_counts_dev);
+  if (fused) {
+    MFB_CUDA_TRY(cudaMemsetAsync(fused->q.count, 0, 2 * sizeof(int), s));
+    k_raster<true><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
+                                          g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, *fused);
+  } else {
+    k_raster<false><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0,
+                                           g.pos, g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc,
+                                           RasterFused{});
+  }
   ctx.count_launch(3);
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+void gbuffer_queries(Ctx& ctx, cudaStream_t s, const GBufDev& g, const RasterFused& out) {
+  const int tiles = ((g.res + kTile - 1) / kTile) * ((g.rows + kTile - 1) / kTile);
+  int* overflow = ctx.buf<int>("gq.overflow", 1);
+  MFB_CUDA_TRY(cudaMemsetAsync(out.q.count, 0, 2 * sizeof(int), s));
+  k_gbuffer_queries<<<tiles, 256, 0, s>>>(g.res, g.rows, g.pos, g.nrm, g.tan, g.bit, g.valid, g.rel, out,
+                                          overflow);
+  ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
 }
 

@@ -411,9 +411,14 @@ class BakePair:
     max_distance_fraction: float
     radius: int = 4
 
+    _diag: float = -1.0
+
     @property
     def bbox_diagonal(self) -> float:
-        return self.dense.bbox_diagonal()
+        """bounds(dense).diagonal() (test_bake.cpp:206), computed once."""
+        if self._diag < 0:
+            self._diag = self.dense.bbox_diagonal()
+        return self._diag
 
 
 # BASELINE.json configs (SURVEY §8 sizes table / BASELINE.md §2 inputs)
