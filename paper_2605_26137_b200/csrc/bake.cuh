@@ -85,7 +85,7 @@ struct GBufDev {
 
 // ---------------------------------------------------------------- LBVH
 constexpr int kLeafMax = 4;     // reference leaf size (bvh.cpp:13)
-constexpr int kStackMax = 96;   // > max Karras depth over 63-bit Morton + 32-bit index keys
+constexpr int kStackMax = 64;   // >= max Karras depth over 30-bit Morton + 32-bit index keys (62)
 
 struct alignas(16) BNode {
   float4 a;  // L.min.x L.min.y L.min.z L.max.x

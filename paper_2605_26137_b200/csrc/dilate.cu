@@ -9,31 +9,33 @@
 //   * neighbours are scanned in the reference's (dy, dx) raster order and a
 //     candidate wins only if strictly nearer, so ties keep the current source,
 //     then the first neighbour in scan order (gbuffer.cpp:288-303).
-// k_dilate_fused runs all passes for one 32x8 tile inside shared memory over
-// a (32+2r) x (8+2r) halo region (one launch, ~1.6x halo read overhead at
-// r = 4); k_dilate_pass is the multi-launch global fallback for large radii.
+// k_dilate_fused runs all passes for one 64x16 tile inside shared memory over
+// a (64+2r) x (16+2r) halo region (one launch, ~1.7x halo read of the 1-byte
+// mask at r = 4); k_dilate_pass is the multi-launch global fallback for radii
+// whose halo does not fit in shared memory.
 #include "bake.cuh"
 
 namespace mfb {
 namespace {
 
-constexpr int kTW = 32, kTH = 8;
+constexpr int kTW = 64, kTH = 16;
 constexpr int16_t kNone = -32768;  // "no source" marker in the x offset
 
 __device__ __forceinline__ int sq(int v) { return v * v; }
 
-// One chamfer step for a texel at region coords (cx, cy) of a rw x rh region.
-// ox/oy hold source offsets; ox == kNone means no source. Region cells
-// outside the image are never sources; region cells outside the region are
-// unknown and simply skipped (only affects cells within `pass` of the edge).
+// One chamfer step (gbuffer.cpp:284-305) for the texel at region coords
+// (cx, cy) of a rw x rh region whose origin is (x0, y0) in the image. ox/oy
+// hold source offsets; ox == kNone means no source. Neighbours outside the
+// image are skipped exactly as in the reference; cells outside the region are
+// never read (the caller only updates cells at least one step inside).
 __device__ __forceinline__ void chamfer_step(const int16_t* __restrict__ ox, const int16_t* __restrict__ oy,
-                                             int rw, int rh, int cx, int cy, int gx, int gy, int width,
-                                             int height, int16_t& nox, int16_t& noy) {
+                                             int rw, int cx, int cy, int gx, int gy, int width, int height,
+                                             int16_t& nox, int16_t& noy) {
   const int self = cy * rw + cx;
   const int16_t sx = ox[self], sy = oy[self];
   nox = sx;
   noy = sy;
-  if (sx != kNone && sx == 0 && sy == 0) return;  // valid texel: dist2 == 0, skipped
+  if (sx == 0 && sy == 0) return;  // valid texel: dist2 == 0, skipped
   long long best = sx == kNone ? 0x7fffffffffffffffll : static_cast<long long>(sq(sx) + sq(sy));
 #pragma unroll
   for (int dy = -1; dy <= 1; ++dy) {
@@ -42,12 +44,9 @@ __device__ __forceinline__ void chamfer_step(const int16_t* __restrict__ ox, con
       if (dx == 0 && dy == 0) continue;
       const int nx = gx + dx, ny = gy + dy;
       if (nx < 0 || nx >= width || ny < 0 || ny >= height) continue;
-      const int rx = cx + dx, ry = cy + dy;
-      if (rx < 0 || rx >= rw || ry < 0 || ry >= rh) continue;
-      const int n = ry * rw + rx;
+      const int n = self + dy * rw + dx;
       const int16_t nsx = ox[n];
       if (nsx == kNone) continue;
-      // candidate source = neighbour + its offset; offset from this texel:
       const int cxo = dx + nsx, cyo = dy + oy[n];
       const long long d = static_cast<long long>(sq(cxo) + sq(cyo));
       if (d < best) {
@@ -59,6 +58,11 @@ __device__ __forceinline__ void chamfer_step(const int16_t* __restrict__ ox, con
   }
 }
 
+// One 64x16 output tile per 256-thread CTA over a (64+2r) x (16+2r) halo
+// region in shared memory. Tiles whose output texels are all valid, or whose
+// region holds no valid texel, are plain copies. Pass k (1-based) updates only
+// cells at least k steps inside the region: exactly the cells the output
+// depends on, so the region shrinks by one ring per pass.
 __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int channels,
                                                       const uint8_t* __restrict__ map_in,
                                                       const uint8_t* __restrict__ valid, int in_row0,
@@ -76,44 +80,57 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
   const int x0 = tx * kTW - radius;            // region origin (absolute)
   const int y0 = out_row0 + ty * kTH - radius;
   const int in_end = in_row0 + in_rows;
+  const int out_end = out_row0 + out_rows;
+  int any_valid = 0, any_hole = 0;
   for (int c = threadIdx.x; c < cells; c += blockDim.x) {
-    const int gx = x0 + c % rw, gy = y0 + c / rw;
+    const int lx = c % rw, ly = c / rw;
+    const int gx = x0 + lx, gy = y0 + ly;
     int16_t v = kNone;
-    if (gx >= 0 && gx < width && gy >= in_row0 && gy < in_end && gy < height &&
-        valid[static_cast<int64_t>(gy - in_row0) * width + gx])
-      v = 0;
+    const bool inimg = gx >= 0 && gx < width && gy >= in_row0 && gy < in_end && gy < height;
+    if (inimg && valid[static_cast<int64_t>(gy - in_row0) * width + gx]) v = 0;
     ox0[c] = v;
     oy0[c] = 0;
+    any_valid |= v == 0;
+    const bool out_cell = lx >= radius && lx < radius + kTW && ly >= radius && ly < radius + kTH &&
+                          gx < width && gy < out_end;
+    any_hole |= out_cell && v != 0;
   }
-  __syncthreads();
-  for (int pass = 0; pass < radius; ++pass) {
-    for (int c = threadIdx.x; c < cells; c += blockDim.x) {
-      const int cx = c % rw, cy = c / rw;
-      int16_t a, b;
-      chamfer_step(ox0, oy0, rw, rh, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
-      ox1[c] = a;
-      oy1[c] = b;
+  const bool work = __syncthreads_or(any_valid) && __syncthreads_or(any_hole);
+  if (work) {
+    for (int pass = 1; pass <= radius; ++pass) {
+      const int iw = rw - 2 * pass, ih = rh - 2 * pass;
+      for (int c = threadIdx.x; c < iw * ih; c += blockDim.x) {
+        const int cx = pass + c % iw, cy = pass + c / iw;
+        const int i = cy * rw + cx;
+        int16_t a, b;
+        chamfer_step(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
+        ox1[i] = a;
+        oy1[i] = b;
+      }
+      __syncthreads();
+      int16_t* t = ox0;
+      ox0 = ox1;
+      ox1 = t;
+      t = oy0;
+      oy0 = oy1;
+      oy1 = t;
+      // (pass k + 1 reads only cells in [k, rw - k) x [k, rh - k), all
+      // written by pass k, so the stale outer ring is never read)
     }
-    __syncthreads();
-    int16_t* t = ox0;
-    ox0 = ox1;
-    ox1 = t;
-    t = oy0;
-    oy0 = oy1;
-    oy1 = t;
   }
-  // output: tile interior
+  // output: tile interior (4 texels per thread, row-contiguous)
   for (int c = threadIdx.x; c < kTW * kTH; c += blockDim.x) {
     const int lx = c % kTW, ly = c / kTW;
     const int gx = tx * kTW + lx, gy = out_row0 + ty * kTH + ly;
-    if (gx >= width || gy >= out_row0 + out_rows) continue;
-    const int rc = (ly + radius) * rw + (lx + radius);
-    const int16_t sx = ox0[rc], sy = oy0[rc];
+    if (gx >= width || gy >= out_end) continue;
     int srcx = gx, srcy = gy;
-    const bool is_valid = sx == 0 && sy == 0;
-    if (sx != kNone && !is_valid) {
-      srcx = gx + sx;
-      srcy = gy + sy;
+    if (work) {
+      const int rc = (ly + radius) * rw + (lx + radius);
+      const int16_t sx = ox0[rc], sy = oy0[rc];
+      if (sx != kNone && !(sx == 0 && sy == 0)) {
+        srcx = gx + sx;
+        srcy = gy + sy;
+      }
     }
     const uint8_t* src = map_in + (static_cast<int64_t>(srcy - in_row0) * width + srcx) * channels;
     uint8_t* dst = map_out + (static_cast<int64_t>(gy - out_row0) * width + gx) * channels;
@@ -194,7 +211,7 @@ void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
     return;
   }
   const size_t smem = static_cast<size_t>(4) * (kTW + 2 * radius) * (kTH + 2 * radius) * sizeof(int16_t);
-  if (radius <= 32 && smem <= 200 * 1024) {
+  if (radius <= 64 && smem <= 200 * 1024) {
     static bool attr_set = false;
     if (!attr_set) {
       MFB_CUDA_TRY(cudaFuncSetAttribute(k_dilate_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,

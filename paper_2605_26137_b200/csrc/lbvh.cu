@@ -3,18 +3,20 @@
 //
 // Pipeline (one stream, 5 launches + one CUB radix sort):
 //   1. bounds      : centroid bounds + max |coordinate| (ordered-int atomics)
-//   2. morton      : 63-bit Morton key of each face centroid
+//   2. morton      : 30-bit Morton key of each face centroid
 //   3. sort        : CUB onesweep radix sort of (key, face) pairs
 //   4. emit        : Karras 2012 hierarchy emission; subtrees covering
 //                    <= kLeafMax primitives become leaf ranges (the
 //                    reference's leaf size, bvh.cpp:13)
-//   5. repack+refit: gather each primitive's f64 vertices into Morton order
-//                    (BTri) and propagate fp32 boxes, rounded outward, up the
-//                    tree; each parent stores both child boxes (64-B nodes).
+//   5. repack      : gather each primitive's f64 vertices into Morton order
+//                    (BTri) plus its outward-rounded fp32 box (TBox)
+//   6. refit       : propagate the fp32 boxes up the tree; each parent stores
+//                    both child boxes (64-B nodes).
 // Query results do not depend on the tree shape: the reference
 // answer is argmin over faces of (distSq, face), which any conservative tree
 // reproduces exactly.
 #include <cub/device/device_radix_sort.cuh>
+#include <cuda/atomic>
 
 #include <cstdlib>
 
@@ -55,7 +57,7 @@ __global__ void k_bounds(const double* __restrict__ pos, const int32_t* __restri
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
     amax = fmax(amax, fmax(fabs(pos[3 * v]), fmax(fabs(pos[3 * v + 1]), fabs(pos[3 * v + 2]))));
   }
-  // warp reduce then one atomic per warp
+  // warp reduce, then block reduce in shared memory, one atomic per block
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
@@ -65,28 +67,40 @@ __global__ void k_bounds(const double* __restrict__ pos, const int32_t* __restri
     }
     amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, off));
   }
+  __shared__ double red[7][32];
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((threadIdx.x & 31) == 0) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      atomicMin(&acc[k], ordered_bits(mn[k]));
-      atomicMax(&acc[3 + k], ordered_bits(mx[k]));
+      red[k][w] = mn[k];
+      red[3 + k][w] = mx[k];
     }
-    atomicMax(&acc[6], ordered_bits(amax));
+    red[6][w] = amax;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    const int k = threadIdx.x;
+    double v = red[k][0];
+    for (int i = 1; i < nw; ++i) v = k < 3 ? fmin(v, red[k][i]) : fmax(v, red[k][i]);
+    if (k < 3) atomicMin(&acc[k], ordered_bits(v));
+    else atomicMax(&acc[k], ordered_bits(v));
   }
 }
 
-__device__ __forceinline__ uint64_t spread21(uint32_t v) {
-  uint64_t x = v & 0x1fffffull;
-  x = (x | (x << 32)) & 0x1f00000000ffffull;
-  x = (x | (x << 16)) & 0x1f0000ff0000ffull;
-  x = (x | (x << 8)) & 0x100f00f00f00f00full;
-  x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
-  x = (x | (x << 2)) & 0x1249249249249249ull;
-  return x;
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+  v &= 0x3ffu;
+  v = (v | (v << 16)) & 0x030000ffu;
+  v = (v | (v << 8)) & 0x0300f00fu;
+  v = (v | (v << 4)) & 0x030c30c3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
 }
 
+// 30-bit Morton keys (10 bits per axis over the centroid bounds): 4 radix
+// passes instead of 8. Duplicate keys are fine - Karras' emission breaks
+// ties with the primitive index.
 __global__ void k_morton(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
-                         const unsigned long long* __restrict__ acc, uint64_t* __restrict__ keys,
+                         const unsigned long long* __restrict__ acc, uint32_t* __restrict__ keys,
                          uint32_t* __restrict__ vals) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
@@ -95,7 +109,7 @@ __global__ void k_morton(const double* __restrict__ pos, const int32_t* __restri
   for (int k = 0; k < 3; ++k) {
     lo[k] = from_ordered(acc[k]);
     const double ext = from_ordered(acc[3 + k]) - lo[k];
-    inv[k] = ext > 0.0 ? 2097151.0 / ext : 0.0;
+    inv[k] = ext > 0.0 ? 1023.0 / ext : 0.0;
   }
   const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
   uint32_t q[3];
@@ -103,23 +117,23 @@ __global__ void k_morton(const double* __restrict__ pos, const int32_t* __restri
   for (int k = 0; k < 3; ++k) {
     const double ck = ((pos[3 * a + k] + pos[3 * b + k]) + pos[3 * c + k]) / 3.0;
     double t = (ck - lo[k]) * inv[k];
-    t = fmin(fmax(t, 0.0), 2097151.0);
+    t = fmin(fmax(t, 0.0), 1023.0);
     q[k] = static_cast<uint32_t>(t);
   }
-  keys[f] = (spread21(q[0]) << 2) | (spread21(q[1]) << 1) | spread21(q[2]);
+  keys[f] = (spread10(q[0]) << 2) | (spread10(q[1]) << 1) | spread10(q[2]);
   vals[f] = static_cast<uint32_t>(f);
 }
 
 // Karras delta over augmented keys (key, index): -1 outside [0, n).
-__device__ __forceinline__ int kdelta(const uint64_t* __restrict__ k, int n, int i, int j) {
+__device__ __forceinline__ int kdelta(const uint32_t* __restrict__ k, int n, int i, int j) {
   if (j < 0 || j >= n) return -1;
-  const uint64_t a = k[i], b = k[j];
-  if (a == b) return 64 + __clz(static_cast<uint32_t>(i ^ j));
-  return __clzll(static_cast<long long>(a ^ b));
+  const uint32_t a = __ldg(k + i), b = __ldg(k + j);
+  if (a == b) return 32 + __clz(static_cast<uint32_t>(i ^ j));
+  return __clz(a ^ b);
 }
 
 // parent links: (parent << 1) | side; prim_parent for primitives, node_parent for internals.
-__global__ void k_emit(const uint64_t* __restrict__ keys, int n, int leaf_max, BNode* __restrict__ nodes,
+__global__ void k_emit(const uint32_t* __restrict__ keys, int n, int leaf_max, BNode* __restrict__ nodes,
                        int32_t* __restrict__ prim_parent, int32_t* __restrict__ node_parent) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n - 1) return;
@@ -178,12 +192,11 @@ __device__ __forceinline__ FBox load_child_box_cg(const BNode* nd, int side) {
   return b;
 }
 
-__global__ void k_repack_refit(const double* __restrict__ pos, const int32_t* __restrict__ faces,
-                               const uint32_t* __restrict__ order, int n, BNode* nodes, BTri* __restrict__ tris,
-                               TBox* __restrict__ tbox,
-                               const int32_t* __restrict__ prim_parent,
-                               const int32_t* __restrict__ node_parent, int* __restrict__ flags,
-                               float* __restrict__ root_box) {
+// Gathers each primitive's f64 vertices into leaf order and its outward-
+// rounded fp32 box (fully parallel; random reads, coalesced writes).
+__global__ void k_repack(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                         const uint32_t* __restrict__ order, int n, BTri* __restrict__ tris,
+                         TBox* __restrict__ tbox) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int f = static_cast<int>(order[p]);
@@ -207,14 +220,30 @@ __global__ void k_repack_refit(const double* __restrict__ pos, const int32_t* __
   }
   t.face = f;
   t.pad = 0;
+  const double2* src = reinterpret_cast<const double2*>(&t);
+  double2* dst = reinterpret_cast<double2*>(&tris[p]);
+#pragma unroll
+  for (int q = 0; q < 5; ++q) dst[q] = src[q];
   tbox[p].a = make_float4(box.mn[0], box.mn[1], box.mn[2], box.mx[0]);
   tbox[p].b = make_float4(box.mx[1], box.mx[2], 0.f, 0.f);
-  {
-    const double2* src = reinterpret_cast<const double2*>(&t);
-    double2* dst = reinterpret_cast<double2*>(&tris[p]);
-#pragma unroll
-    for (int q = 0; q < 5; ++q) dst[q] = src[q];
-  }
+}
+
+// Bottom-up refit: each primitive's thread climbs while it is the second
+// child to arrive (acquire/release counter per node), storing the child box
+// into its parent's slot.
+__global__ void k_refit(const TBox* __restrict__ tbox, int n, BNode* nodes, const int32_t* __restrict__ prim_parent,
+                        const int32_t* __restrict__ node_parent, int* __restrict__ flags,
+                        float* __restrict__ root_box) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const float4 ba = tbox[p].a, bb = tbox[p].b;
+  FBox box;
+  box.mn[0] = ba.x;
+  box.mn[1] = ba.y;
+  box.mn[2] = ba.z;
+  box.mx[0] = ba.w;
+  box.mx[1] = bb.x;
+  box.mx[2] = bb.y;
   if (n == 1) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -227,10 +256,8 @@ __global__ void k_repack_refit(const double* __restrict__ pos, const int32_t* __
   for (;;) {
     const int par = link >> 1, side = link & 1;
     store_child_box(&nodes[par], side, box);
-    __threadfence();
-    const int old = atomicAdd(&flags[par], 1);
-    if (old == 0) return;  // sibling not done yet; it will carry the union upward
-    __threadfence();
+    cuda::atomic_ref<int, cuda::thread_scope_device> flag(flags[par]);
+    if (flag.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;  // sibling carries on
     const FBox other = load_child_box_cg(&nodes[par], side ^ 1);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -256,8 +283,8 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   out.n_tris = n;
   out.n_nodes = n > 1 ? n - 1 : 0;
   auto* acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
-  auto* keys = ctx.buf<uint64_t>(tag + ".keys", n);
-  auto* keys2 = ctx.buf<uint64_t>(tag + ".keys2", n);
+  auto* keys = ctx.buf<uint32_t>(tag + ".keys", n);
+  auto* keys2 = ctx.buf<uint32_t>(tag + ".keys2", n);
   auto* vals = ctx.buf<uint32_t>(tag + ".vals", n);
   auto* vals2 = ctx.buf<uint32_t>(tag + ".vals2", n);
   out.nodes = ctx.buf<BNode>(tag + ".nodes", out.n_nodes > 0 ? out.n_nodes : 1);
@@ -279,9 +306,9 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   ctx.count_launch(2);
 
   size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, vals, vals2, n, 0, 63, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, vals, vals2, n, 0, 30, s);
   void* tptr = ctx.cub_temp(tmp, s != ctx.stream);
-  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 63, s));
+  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 30, s));
 
   if (n > 1) {
     // Leaf size: the reference's 4 (bvh.cpp:13) unless MFB_LEAF_MAX (1..7) overrides it.
@@ -293,9 +320,9 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
     k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent);
     ctx.count_launch();
   }
-  k_repack_refit<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.nodes, out.tris, out.tbox, prim_parent,
-                                            node_parent, flags, out.root_box_dev);
-  ctx.count_launch();
+  k_repack<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
+  k_refit<<<div_up(n, T), T, 0, s>>>(out.tbox, n, out.nodes, prim_parent, node_parent, flags, out.root_box_dev);
+  ctx.count_launch(2);
   MFB_CUDA_TRY(cudaGetLastError());
   out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
   out.scene_acc = acc;

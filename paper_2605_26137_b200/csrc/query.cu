@@ -394,15 +394,17 @@ __device__ __forceinline__ void warp_closest(const BNode* __restrict__ nodes, co
 // holds one, so the expensive exact f64 test executes at high SIMT width.
 // Depth-first nearest-child-first with conservative fp32 pruning (see
 // traverse_closest) - result-neutral vs the reference's best-first heap.
-template <bool kDebug>
+template <bool kDebug, bool kProf>
 __global__ void __launch_bounds__(128) k_transfer_t(
     const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
     const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
     const float* __restrict__ qtbn, const int* __restrict__ qcount, const double* __restrict__ hiN,
     const int32_t* __restrict__ hiF, double max_dist, uint8_t* __restrict__ rgb,
-    int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters) {
+    int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters,
+    unsigned long long* __restrict__ prof_out) {
   const int nq = qcount[0];
   const int lane = threadIdx.x & 31;
+  unsigned long long pv[4] = {0, 0, 0, 0};  // internal visits, leaf visits, triangle tests, queries
   const double scene_max = from_ordered_dev(scene_acc[6]);
   const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
   unsigned long long hits = 0;
@@ -427,6 +429,7 @@ __global__ void __launch_bounds__(128) k_transfer_t(
     while (ref != kDone) {
       // ---- descend until this lane holds a leaf
       while (ref >= 0) {
+        if (kProf) ++pv[0];
         const float4* np = reinterpret_cast<const float4*>(nodes + ref);
         const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
         const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
@@ -456,6 +459,10 @@ __global__ void __launch_bounds__(128) k_transfer_t(
       // ---- leaf: exact f64 tests (branch-free, reference arithmetic)
       int first, count;
       leaf_decode(ref, first, count);
+      if (kProf) {
+        ++pv[1];
+        pv[2] += count;
+      }
       for (int k = 0; k < count; ++k) {
         d3 A, B, C;
         int face;
@@ -480,6 +487,7 @@ __global__ void __launch_bounds__(128) k_transfer_t(
       }
     }
     if (!live) continue;
+    if (kProf) ++pv[3];
     const int texel = __float_as_int(p.w);
     uint8_t px[3] = {128, 128, 255};
     double ts3[3] = {0.0, 0.0, 0.0};
@@ -515,6 +523,188 @@ __global__ void __launch_bounds__(128) k_transfer_t(
         dbg_ts[3ll * texel + 1] = ts3[1];
         dbg_ts[3ll * texel + 2] = ts3[2];
       }
+    }
+  }
+  if (kProf)
+    for (int k = 0; k < 4; ++k) {
+      unsigned long long v = pv[k];
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) atomicAdd(&prof_out[k], v);
+    }
+  if (counters) {
+    for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
+    if (lane == 0 && hits) atomicAdd(&counters[1], hits);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));
+  }
+}
+
+// ---------------------------------------------------------------- persistent refill transfer
+// Same per-thread while-while traversal, but lanes are persistent: a lane that
+// finishes its query writes the texel and, once at least kRefill lanes of the
+// warp are idle, the idle lanes grab new queries from a global cursor with
+// one warp-aggregated atomic. Warps therefore stay (nearly) full instead of
+// running at the width of their slowest query.
+__device__ __forceinline__ void encode_texel(const Best& best, const float* __restrict__ tb,
+                                             const double* __restrict__ hiN, const int32_t* __restrict__ hiF,
+                                             uint8_t* __restrict__ rgb, int texel, int32_t* dbg_face,
+                                             double* dbg_ts) {
+  uint8_t px[3] = {128, 128, 255};
+  double ts3[3] = {0.0, 0.0, 0.0};
+  if (best.face >= 0) {
+    const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
+    const d3 n = (best.bary.x * ld3(hiN + 3 * v0) + best.bary.y * ld3(hiN + 3 * v1)) + best.bary.z * ld3(hiN + 3 * v2);
+    const d3 T = mk3(tb[0], tb[1], tb[2]);
+    const d3 B = mk3(tb[3], tb[4], tb[5]);
+    const d3 N = mk3(tb[6], tb[7], tb[8]);
+    d3 ts = mk3(dot(n, T), dot(n, B), dot(n, N));
+    const double len = norm(ts);
+    if (!(len < 1e-12)) {
+      ts = ts / len;
+      px[0] = encode_channel(ts.x);
+      px[1] = encode_channel(ts.y);
+      px[2] = encode_channel(ts.z);
+      ts3[0] = ts.x;
+      ts3[1] = ts.y;
+      ts3[2] = ts.z;
+    }
+  }
+  uint8_t* o = rgb + 3ll * texel;
+  o[0] = px[0];
+  o[1] = px[1];
+  o[2] = px[2];
+  if (dbg_face) dbg_face[texel] = best.face >= 0 ? best.face : -3;
+  if (dbg_ts) {
+    dbg_ts[3ll * texel] = ts3[0];
+    dbg_ts[3ll * texel + 1] = ts3[1];
+    dbg_ts[3ll * texel + 2] = ts3[2];
+  }
+}
+
+template <bool kDebug, int kRefill, int kChunkQ>
+__global__ void __launch_bounds__(128) k_transfer_p(
+    const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
+    const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
+    const float* __restrict__ qtbn, int* __restrict__ qcount, const double* __restrict__ hiN,
+    const int32_t* __restrict__ hiF, double max_dist, uint8_t* __restrict__ rgb,
+    int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters) {
+  constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
+  const int nq = qcount[0];
+  const int lane = threadIdx.x & 31;
+  const double scene_max = from_ordered_dev(scene_acc[6]);
+  const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
+  unsigned long long hits = 0;
+  int32_t st_ref[kStackMax];
+  float st_lb[kStackMax];
+  int sp = 0;
+  int32_t ref = kDone;
+  bool live = false;
+  int qi = 0;
+  float3 qf = make_float3(0.f, 0.f, 0.f);
+  double E = 0.0;
+  Best best;
+  best.d = init;
+  best.face = -1;
+  best.bary = mk3(0.0, 0.0, 0.0);
+  float bnd = -INFINITY;
+  // Work distribution: warp w owns chunks w, w + W, w + 2W, ... of kChunkQ
+  // consecutive queries (one raster tile's worth: spatial neighbours); idle
+  // lanes refill from the warp's current chunk through a warp-uniform cursor.
+  const int warp_id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int chunk = warp_id;
+  int cur = chunk * kChunkQ;                      // next unassigned query of the chunk
+  int chunk_end = min(cur + kChunkQ, nq);
+  for (;;) {
+    const unsigned idle = __ballot_sync(0xffffffffu, !live);
+    if (cur >= chunk_end && idle == 0xffffffffu) {  // chunk drained: move the whole warp on
+      chunk += nwarps;
+      cur = chunk * kChunkQ;
+      if (cur >= nq) break;
+      chunk_end = min(cur + kChunkQ, nq);
+    }
+    if (cur < chunk_end && __popc(idle) >= (idle == 0xffffffffu ? 1 : kRefill)) {
+      if (!live) {
+        const int i = cur + __popc(idle & ((1u << lane) - 1u));
+        if (i < chunk_end) {
+          qi = i;
+          const float4 p = __ldg(qpos + i);
+          qf = make_float3(p.x, p.y, p.z);
+          E = fmax(scene_max, fmax(fabs(static_cast<double>(p.x)), fmax(fabs(static_cast<double>(p.y)),
+                                                                          fabs(static_cast<double>(p.z))))) * 0x1p-32;
+          best.d = init;
+          best.face = -1;
+          best.bary = mk3(0.0, 0.0, 0.0);
+          bnd = prune_bound(init, E);
+          sp = 0;
+          ref = root;
+          live = true;
+        }
+      }
+      cur = min(cur + __popc(idle), chunk_end);
+    }
+    if (!__any_sync(0xffffffffu, live)) break;
+    // ---- descend until this lane holds a leaf (or finishes)
+    while (live && ref >= 0) {
+      const float4* np = reinterpret_cast<const float4*>(nodes + ref);
+      const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+      const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
+      const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
+      const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
+      const bool hL = lbL <= bnd, hR = lbR <= bnd;
+      if (hL && hR) {
+        const bool lf = lbL <= lbR;
+        st_ref[sp] = lf ? d.y : d.x;
+        st_lb[sp] = lf ? lbR : lbL;
+        ++sp;
+        ref = lf ? d.x : d.y;
+      } else if (hL || hR) {
+        ref = hL ? d.x : d.y;
+      } else {
+        ref = kDone;
+        while (sp > 0) {
+          --sp;
+          if (st_lb[sp] <= bnd) {
+            ref = st_ref[sp];
+            break;
+          }
+        }
+      }
+    }
+    // ---- leaf phase
+    if (live && ref != kDone) {
+      const d3 q = mk3(qf.x, qf.y, qf.z);
+      int first, count;
+      leaf_decode(ref, first, count);
+      for (int k = 0; k < count; ++k) {
+        d3 A, B, C;
+        int face;
+        load_tri(tris + first + k, A, B, C, face);
+        d3 bary;
+        const d3 pt = closest_point_triangle_sel(q, A, B, C, bary);
+        const double ds = sqnorm(pt - q);
+        if (ds < best.d || (ds == best.d && face < best.face)) {
+          best.d = ds;
+          best.face = face;
+          best.bary = bary;
+          bnd = prune_bound(ds, E);
+        }
+      }
+      ref = kDone;
+      while (sp > 0) {
+        --sp;
+        if (st_lb[sp] <= bnd) {
+          ref = st_ref[sp];
+          break;
+        }
+      }
+    }
+    // ---- finished queries: encode and free the lane
+    if (live && ref == kDone) {
+      const int texel = __float_as_int(__ldg(qpos + qi).w);
+      if (best.face >= 0) ++hits;
+      encode_texel(best, qtbn + 9ll * qi, hiN, hiF, rgb, texel, kDebug ? dbg_face : nullptr,
+                   kDebug ? dbg_ts : nullptr);
+      live = false;
     }
   }
   if (counters) {
@@ -812,21 +1002,59 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     const char* e = std::getenv("MFB_XFER");
     return !(e && std::string(e) == "warp");
   }();
-  if (per_thread) {
+  // Persistent lanes with refill measured slower than plain while-while on
+  // config B (1.85 vs 1.42 ms): lanes at different depths lose the broadcast
+  // node loads. Off by default; MFB_REFILL=k enables it for experiments.
+  static const int refill = [] {
+    const char* e = std::getenv("MFB_REFILL");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (per_thread && refill > 0) {
+    static int bpp = 0;
+    if (!bpp) {
+      MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpp, k_transfer_p<false, 8, 256>, 128, 0));
+      if (bpp < 1) bpp = 1;
+    }
+    const int g3 = std::max(1, std::min(kNumSMs * bpp, div_up(a.q.capacity, 128)));
+    MFB_CUDA_TRY(cudaMemsetAsync(a.q.count + 2, 0, sizeof(int), s));
+#define MFB_XFER_P(D, R, C)                                                                                 \
+  k_transfer_p<D, R, C><<<g3, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos,        \
+                                           a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, \
+                                           D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters)
+    static const int chunkq = [] {
+      const char* e = std::getenv("MFB_CHUNKQ");
+      return e ? std::atoi(e) : 256;
+    }();
+#define MFB_XFER_PC(D, R) \
+  if (chunkq >= 1024) MFB_XFER_P(D, R, 1024); else if (chunkq >= 256) MFB_XFER_P(D, R, 256); else MFB_XFER_P(D, R, 64)
+    if (refill >= 16) {
+      if (dbg) { MFB_XFER_PC(true, 16); } else { MFB_XFER_PC(false, 16); }
+    } else if (refill >= 8) {
+      if (dbg) { MFB_XFER_PC(true, 8); } else { MFB_XFER_PC(false, 8); }
+    } else if (refill >= 4) {
+      if (dbg) { MFB_XFER_PC(true, 4); } else { MFB_XFER_PC(false, 4); }
+    } else {
+      if (dbg) { MFB_XFER_PC(true, 1); } else { MFB_XFER_PC(false, 1); }
+    }
+#undef MFB_XFER_PC
+#undef MFB_XFER_P
+  } else if (per_thread) {
     static int bps = 0;
     if (!bps) {
-      MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_transfer_t<false>, 128, 0));
+      MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_transfer_t<false, false>, 128, 0));
       if (bps < 1) bps = 1;
     }
     const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
-    if (dbg)
-      k_transfer_t<true><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn,
-                                            a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, a.dbg_face,
-                                            a.dbg_ts, a.counters);
-    else
-      k_transfer_t<false><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn,
-                                             a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, nullptr,
-                                             nullptr, a.counters);
+#define MFB_XFER_T(D, P)                                                                                    \
+  k_transfer_t<D, P><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, \
+                                        a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb,              \
+                                        D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf)
+    if (prof) {
+      if (dbg) MFB_XFER_T(true, true); else MFB_XFER_T(false, true);
+    } else {
+      if (dbg) MFB_XFER_T(true, false); else MFB_XFER_T(false, false);
+    }
+#undef MFB_XFER_T
   } else {
     MFB_XFER_PASS(1);
     if (kSeedPasses) {
@@ -842,6 +1070,12 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     unsigned long long h[8];
     MFB_CUDA_TRY(cudaMemcpyAsync(h, pbuf, sizeof(h), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
+    if (per_thread) {
+      const double nqd = h[3] ? static_cast<double>(h[3]) : 1.0;
+      std::fprintf(stderr, "[mfb prof] per query: internal %.2f leaves %.2f triangles %.2f (queries %llu)\n",
+                   h[0] / nqd, h[1] / nqd, h[2] / nqd, h[3]);
+      return;
+    }
     const double b = h[5] ? static_cast<double>(h[5]) : 1.0;
     std::fprintf(stderr,
                  "[mfb prof] per warp-batch: internal %.1f leaves %.1f pops %.1f rounds %.1f pairs %.1f "

@@ -4,11 +4,11 @@
 //                   CSR of incident corners, summed in face order
 //                   (deterministic, no float atomics);
 //   wedge frames    computeWedgeTangents (bake/tangent.cpp:22-82): corner
-//                   contributions keyed by (vertex, uv), stable radix sort,
-//                   in-order segmented sums;
+//                   contributions summed per (vertex, uv) wedge in face order
+//                   over the vertex's sorted incident-corner list;
 //   reliable faces  reliableFaces (gbuffer.cpp:31-83): lock-free union-find
-//                   whose roots are island minima, (island, ratio) sort,
-//                   median = element size/2;
+//                   whose roots are island minima, ratios grouped per island,
+//                   median = element size/2 by an exact per-island radix select;
 //   face setup      canonical edge functions + texel bbox per face;
 //   binning         counting sort of faces into 16x16 texel tiles
 //                   (conservative: every tile the face's texel bbox touches);
@@ -16,7 +16,6 @@
 //                   reference coverage predicate (tie rule ownsBoundary,
 //                   gbuffer.cpp:21-27,146-154), AtlasOverlap detection,
 //                   f64 attribute interpolation, coalesced G-buffer stores.
-#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "bake.cuh"
@@ -62,12 +61,12 @@ __global__ void k_face_area_vec(const double* __restrict__ pos, const int32_t* _
            p2 = ld3(pos + 3 * faces[3 * f + 2]);
   st3(av + 3 * f, 0.5 * cross(p1 - p0, p2 - p0));  // faceAreaVector, mesh.h:28-31
 }
-__global__ void k_vertex_sum(int nv, const int* __restrict__ start, int* __restrict__ list,
-                             const double* __restrict__ av, double* __restrict__ out, int renorm) {
+// Sorts each vertex's incident-corner list into face order (valence is small).
+__global__ void k_csr_sort(int nv, const int* __restrict__ start, int* __restrict__ list) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
   const int b = start[v], e = start[v + 1];
-  for (int i = b + 1; i < e; ++i) {  // insertion sort: face order (valence is small)
+  for (int i = b + 1; i < e; ++i) {
     const int key = list[i];
     int j = i - 1;
     while (j >= b && list[j] > key) {
@@ -76,6 +75,13 @@ __global__ void k_vertex_sum(int nv, const int* __restrict__ start, int* __restr
     }
     list[j + 1] = key;
   }
+}
+// computeVertexNormals (mesh.cpp:24-35): area vectors summed in face order.
+__global__ void k_vertex_sum(int nv, const int* __restrict__ start, const int* __restrict__ list,
+                             const double* __restrict__ av, double* __restrict__ out, int renorm) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int b = start[v], e = start[v + 1];
   d3 n = mk3(0.0, 0.0, 0.0);
   for (int i = b; i < e; ++i) n = n + ld3(av + 3 * (list[i] / 3));
   const double len = norm(n);
@@ -98,8 +104,7 @@ __global__ void k_renorm(int nv, const double* __restrict__ in, double* __restri
 // ------------------------------------------------------------ wedge frames
 __global__ void k_wedge_contrib(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                                 const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
-                                int nu, double* __restrict__ contrib, uint8_t* __restrict__ present,
-                                uint64_t* __restrict__ keys, uint32_t* __restrict__ idx) {
+                                double* __restrict__ contrib, uint8_t* __restrict__ present) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   const int t[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
@@ -114,8 +119,6 @@ __global__ void k_wedge_contrib(const double* __restrict__ pos, const int32_t* _
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     const int c = 3 * f + k;
-    keys[c] = static_cast<uint64_t>(t[k]) * static_cast<uint64_t>(nu) + static_cast<uint64_t>(u[k]);
-    idx[c] = static_cast<uint32_t>(c);
     bool ok = face_ok;
     d3 w = mk3(0.0, 0.0, 0.0);
     if (ok) {
@@ -135,19 +138,31 @@ __global__ void k_wedge_contrib(const double* __restrict__ pos, const int32_t* _
     st3(contrib + 3 * c, w);
   }
 }
-__global__ void k_wedge_segsum(int nc, const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
-                               const double* __restrict__ contrib, const uint8_t* __restrict__ present,
-                               double* __restrict__ acc) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nc) return;
-  if (i > 0 && keys[i] == keys[i - 1]) return;  // not a segment head
-  d3 s = mk3(0.0, 0.0, 0.0);
-  int j = i;
-  for (; j < nc && keys[j] == keys[i]; ++j) {
-    const int c = idx[j];
-    if (present[c]) s = s + ld3(contrib + 3 * c);
+// Per vertex: each wedge (vertex, uv index) sums its corners' contributions
+// in face order (the vertex's corner list is sorted by corner id) - exactly
+// the unordered_map accumulation of tangent.cpp:40-63 - and every corner
+// receives its wedge's sum.
+__global__ void k_wedge_acc(int nv, const int* __restrict__ start, const int* __restrict__ list,
+                            const int32_t* __restrict__ fuv, const double* __restrict__ contrib,
+                            const uint8_t* __restrict__ present, double* __restrict__ acc) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int b = start[v], e = start[v + 1];
+  for (int i = b; i < e; ++i) {
+    const int ui = fuv[list[i]];
+    bool seen = false;
+    for (int j = b; j < i && !seen; ++j) seen = fuv[list[j]] == ui;
+    if (seen) continue;
+    d3 sum = mk3(0.0, 0.0, 0.0);
+    for (int j = i; j < e; ++j) {
+      const int cj = list[j];
+      if (fuv[cj] == ui && present[cj]) sum = sum + ld3(contrib + 3 * cj);
+    }
+    for (int j = i; j < e; ++j) {
+      const int cj = list[j];
+      if (fuv[cj] == ui) st3(acc + 3 * cj, sum);
+    }
   }
-  for (int k = i; k < j; ++k) st3(acc + 3 * idx[k], s);
 }
 // frames[c] = {T, B, N}; also fills the raster attribute block when attrs != null.
 __global__ void k_wedge_frames(const int32_t* __restrict__ faces, int nf, const double* __restrict__ unitN,
@@ -180,11 +195,15 @@ __global__ void k_iota(int n, int* __restrict__ a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) a[i] = i;
 }
+// find with path halving: parent[x] <- parent[parent[x]] (a benign race:
+// any ancestor is a valid parent, and roots never change except by the CAS).
 __device__ __forceinline__ int uf_find(int* parent, int x) {
   int p = __ldcg(&parent[x]);
   while (p != x) {
+    const int gp = __ldcg(&parent[p]);
+    if (gp != p) atomicCAS(&parent[x], p, gp);
     x = p;
-    p = __ldcg(&parent[x]);
+    p = gp;
   }
   return x;
 }
@@ -212,10 +231,8 @@ __global__ void k_uf_flatten(int n, int* parent) {
 }
 __global__ void k_face_ratio(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                              const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
-                             int nu, const int* __restrict__ parent, double* __restrict__ uv_area,
-                             double* __restrict__ ratio, int* __restrict__ island, int* __restrict__ count,
-                             uint64_t* __restrict__ rkey, uint32_t* __restrict__ ikey,
-                             uint32_t* __restrict__ fidx) {
+                             const int* __restrict__ parent, double* __restrict__ uv_area,
+                             double* __restrict__ ratio, int* __restrict__ island, int* __restrict__ count) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   const int u0 = fuv[3 * f], u1 = fuv[3 * f + 1], u2 = fuv[3 * f + 2];
@@ -226,25 +243,70 @@ __global__ void k_face_ratio(const double* __restrict__ pos, const int32_t* __re
   const double surf = norm(0.5 * cross(p1 - p0, p2 - p0));  // faceArea, mesh.h:33
   const int isl = parent[u0];
   double r = -1.0;
-  const bool has = surf > 1e-20;
-  if (has) {
+  if (surf > 1e-20) {
     r = a / surf;
     atomicAdd(&count[isl], 1);
   }
   uv_area[f] = a;
   ratio[f] = r;
   island[f] = isl;
-  rkey[f] = has ? static_cast<uint64_t>(__double_as_longlong(r)) : 0ull;
-  ikey[f] = has ? static_cast<uint32_t>(isl) : static_cast<uint32_t>(nu);
-  fidx[f] = static_cast<uint32_t>(f);
 }
-__global__ void k_island_median(int nu, const int* __restrict__ count, const int* __restrict__ start,
-                                const uint32_t* __restrict__ sorted_face, const double* __restrict__ ratio,
-                                double* __restrict__ median) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nu) return;
-  const int n = count[i];
-  median[i] = n > 0 ? ratio[sorted_face[start[i] + n / 2]] : 0.0;
+// Groups the sampled ratios by island (order within an island is irrelevant
+// to its median).
+__global__ void k_island_fill(int nf, const double* __restrict__ ratio, const int* __restrict__ island,
+                              const int* __restrict__ start, int* __restrict__ cursor,
+                              unsigned long long* __restrict__ items) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf || ratio[f] < 0.0) return;
+  const int isl = island[f];
+  // ratio >= 0, so its IEEE bit pattern orders like its value
+  items[start[isl] + atomicAdd(&cursor[isl], 1)] = static_cast<unsigned long long>(__double_as_longlong(ratio[f]));
+}
+// Island median = element size/2 of the island's sorted ratios (the
+// std::nth_element of gbuffer.cpp:69-71), by an exact 8-pass radix select
+// over the 64-bit patterns; one CTA per island.
+__global__ void __launch_bounds__(256) k_island_select(int nu, const int* __restrict__ count,
+                                                       const int* __restrict__ start,
+                                                       const unsigned long long* __restrict__ items,
+                                                       double* __restrict__ median) {
+  const int isl = blockIdx.x;
+  if (isl >= nu) return;
+  const int n = count[isl];
+  if (n == 0) {
+    if (threadIdx.x == 0) median[isl] = 0.0;
+    return;
+  }
+  const unsigned long long* it = items + start[isl];
+  __shared__ int hist[256];
+  __shared__ unsigned long long s_prefix;
+  __shared__ int s_k;
+  if (threadIdx.x == 0) {
+    s_prefix = 0;
+    s_k = n / 2;
+  }
+  for (int pass = 7; pass >= 0; --pass) {
+    const int shift = pass * 8;
+    const unsigned long long hi_mask = pass == 7 ? 0ull : (~0ull << (shift + 8));
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = s_prefix;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const unsigned long long v = it[i];
+      if ((v & hi_mask) == prefix) atomicAdd(&hist[(v >> shift) & 0xff], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int k = s_k, b = 0;
+      while (k >= hist[b]) {
+        k -= hist[b];
+        ++b;
+      }
+      s_k = k;
+      s_prefix = prefix | (static_cast<unsigned long long>(b) << shift);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) median[isl] = __longlong_as_double(static_cast<long long>(s_prefix));
 }
 
 // ------------------------------------------------------------ face setup
@@ -585,21 +647,45 @@ __global__ void __launch_bounds__(256) k_gbuffer_queries(int res, int rows, cons
   emit_fused(gi, x, y, in, valid, rel, P, N, T, B, nullptr, fo, overflow);
 }
 
-__global__ void k_gather_u32(int n, const uint32_t* __restrict__ src, const uint32_t* __restrict__ perm,
-                             uint32_t* __restrict__ dst) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) dst[i] = src[perm[i]];
-}
 
-int bits_for(uint64_t n) {
-  int b = 1;
-  while (b < 64 && (uint64_t(1) << b) < n) ++b;
-  return b;
-}
 
 }  // namespace
 
 // ---------------------------------------------------------------- host side
+namespace {
+// Incident-corner CSR of a mesh: start[v]..start[v+1] lists the corners 3f+k
+// of vertex v in face order.
+void corner_csr(Ctx& ctx, cudaStream_t s, const DevMesh& m, const std::string& tag, int** start_out,
+                int** list_out) {
+  const int T = 256;
+  const int nc = 3 * m.nf;
+  int* cnt = ctx.buf<int>(tag + ".csr.cnt", m.nv + 1);
+  int* start = ctx.buf<int>(tag + ".csr.start", m.nv + 1);
+  int* cursor = ctx.buf<int>(tag + ".csr.cursor", m.nv + 1);
+  int* list = ctx.buf<int>(tag + ".csr.list", nc);
+  MFB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (m.nv + 1), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (m.nv + 1), s));
+  k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, cnt, start, m.nv + 1, s));
+  k_corner_fill<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, start, cursor, list);
+  k_csr_sort<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list);
+  ctx.count_launch(3);
+  *start_out = start;
+  *list_out = list;
+}
+
+void normals_from_csr(Ctx& ctx, cudaStream_t s, const DevMesh& m, const int* start, const int* list,
+                      double* out, bool renorm, const std::string& tag) {
+  const int T = 256;
+  double* av = ctx.buf<double>(tag + ".vn.av", 3 * static_cast<size_t>(m.nf));
+  k_face_area_vec<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, av);
+  k_vertex_sum<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list, av, out, renorm ? 1 : 0);
+  ctx.count_launch(2);
+}
+}  // namespace
+
 void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, bool renorm,
                     const std::string& tag) {
   const int T = 256;
@@ -612,47 +698,31 @@ void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, boo
     }
     return;
   }
-  const int nc = 3 * m.nf;
-  int* cnt = ctx.buf<int>(tag + ".vn.cnt", m.nv + 1);
-  int* start = ctx.buf<int>(tag + ".vn.start", m.nv + 1);
-  int* cursor = ctx.buf<int>(tag + ".vn.cursor", m.nv + 1);
-  int* list = ctx.buf<int>(tag + ".vn.list", nc);
-  double* av = ctx.buf<double>(tag + ".vn.av", 3 * static_cast<size_t>(m.nf));
-  MFB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (m.nv + 1), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (m.nv + 1), s));
-  k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, cnt, start, m.nv + 1, s));
-  k_corner_fill<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, start, cursor, list);
-  k_face_area_vec<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, av);
-  k_vertex_sum<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list, av, out, renorm ? 1 : 0);
-  ctx.count_launch(4);
+  int *start, *list;
+  corner_csr(ctx, s, m, tag, &start, &list);
+  normals_from_csr(ctx, s, m, start, list, out, renorm, tag);
   MFB_CUDA_TRY(cudaGetLastError());
 }
 
 namespace {
-// Shared by prepare_lowpoly and wedge_frames.
+// computeWedgeTangents (tangent.cpp:22-82); shared by prepare_lowpoly and wedge_frames.
 void wedge_pipeline(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames, AttrFace* attrs) {
   const int T = 256;
   const int nf = lo.nf, nc = 3 * nf;
+  int *start, *list;
+  corner_csr(ctx, s, lo, "lo", &start, &list);
   double* unitN = ctx.buf<double>("lo.unitN", 3 * static_cast<size_t>(lo.nv));
-  vertex_normals(ctx, s, lo, unitN, true, "lo");
+  if (lo.has_normals()) {
+    k_renorm<<<div_up(lo.nv, T), T, 0, s>>>(lo.nv, lo.nrm, unitN);
+    ctx.count_launch();
+  } else {
+    normals_from_csr(ctx, s, lo, start, list, unitN, true, "lo");
+  }
   double* contrib = ctx.buf<double>("lo.wt.contrib", 3 * static_cast<size_t>(nc));
   uint8_t* present = ctx.buf<uint8_t>("lo.wt.present", nc);
-  uint64_t* keys = ctx.buf<uint64_t>("lo.wt.keys", nc);
-  uint64_t* keys2 = ctx.buf<uint64_t>("lo.wt.keys2", nc);
-  uint32_t* idx = ctx.buf<uint32_t>("lo.wt.idx", nc);
-  uint32_t* idx2 = ctx.buf<uint32_t>("lo.wt.idx2", nc);
   double* acc = ctx.buf<double>("lo.wt.acc", 3 * static_cast<size_t>(nc));
-  k_wedge_contrib<<<div_up(nf, T), T, 0, s>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, lo.nu, contrib, present,
-                                              keys, idx);
-  const int kb = bits_for(static_cast<uint64_t>(lo.nv) * static_cast<uint64_t>(lo.nu) + 1);
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, idx, idx2, nc, 0, kb, s);
-  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx.cub_temp(tmp, s != ctx.stream), tmp, keys, keys2, idx,
-                                               idx2, nc, 0, kb, s));
-  k_wedge_segsum<<<div_up(nc, T), T, 0, s>>>(nc, keys2, idx2, contrib, present, acc);
+  k_wedge_contrib<<<div_up(nf, T), T, 0, s>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, contrib, present);
+  k_wedge_acc<<<div_up(lo.nv, T), T, 0, s>>>(lo.nv, start, list, lo.fuv, contrib, present, acc);
   k_wedge_frames<<<div_up(nc, T), T, 0, s>>>(lo.faces, nf, unitN, acc, frames, attrs, lo.pos);
   ctx.count_launch(3);
   MFB_CUDA_TRY(cudaGetLastError());
@@ -670,46 +740,30 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
   auto* attrs = ctx.buf<AttrFace>("lo.attrs", nf);
   wedge_pipeline(ctx, s, lo, nullptr, attrs);
 
-  // reliableFaces
+  // reliableFaces (gbuffer.cpp:31-83)
   int* parent = ctx.buf<int>("lo.rel.parent", nu);
   double* uv_area = ctx.buf<double>("lo.rel.uvarea", nf);
   double* ratio = ctx.buf<double>("lo.rel.ratio", nf);
   int* island = ctx.buf<int>("lo.rel.island", nf);
   int* count = ctx.buf<int>("lo.rel.count", nu + 1);
   int* start = ctx.buf<int>("lo.rel.start", nu + 1);
-  uint64_t* rkey = ctx.buf<uint64_t>("lo.rel.rkey", nf);
-  uint64_t* rkey2 = ctx.buf<uint64_t>("lo.rel.rkey2", nf);
-  uint32_t* ikey = ctx.buf<uint32_t>("lo.rel.ikey", nf);
-  uint32_t* ikey2 = ctx.buf<uint32_t>("lo.rel.ikey2", nf);
-  uint32_t* fidx = ctx.buf<uint32_t>("lo.rel.fidx", nf);
-  uint32_t* fidx2 = ctx.buf<uint32_t>("lo.rel.fidx2", nf);
+  int* cursor = ctx.buf<int>("lo.rel.cursor", nu + 1);
+  auto* items = ctx.buf<unsigned long long>("lo.rel.items", nf);
   double* median = ctx.buf<double>("lo.rel.median", nu);
   MFB_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int) * (nu + 1), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (nu + 1), s));
   k_iota<<<div_up(nu, T), T, 0, s>>>(nu, parent);
   k_uf_unite<<<div_up(nf, T), T, 0, s>>>(lo.fuv, nf, parent);
   k_uf_flatten<<<div_up(nu, T), T, 0, s>>>(nu, parent);
-  k_face_ratio<<<div_up(nf, T), T, 0, s>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, nu, parent, uv_area, ratio,
-                                           island, count, rkey, ikey, fidx);
-  ctx.count_launch(4);
+  k_face_ratio<<<div_up(nf, T), T, 0, s>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, parent, uv_area, ratio, island,
+                                           count);
   size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, rkey, rkey2, fidx, fidx2, nf, 0, 64, s);
-  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx.cub_temp(tmp, s != ctx.stream), tmp, rkey, rkey2, fidx,
-                                               fidx2, nf, 0, 64, s));
-  // gather island keys in ratio order, then stable sort by island
-  // (reuse rkey as a u32 scratch via ikey/ikey2)
-  k_gather_u32<<<div_up(nf, T), T, 0, s>>>(nf, ikey, fidx2, ikey2);  // island keys in ratio order
-  ctx.count_launch();
-  const int ib = bits_for(static_cast<uint64_t>(nu) + 1);
-  tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, ikey2, ikey, fidx2, fidx, nf, 0, ib, s);
-  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(ctx.cub_temp(tmp, s != ctx.stream), tmp, ikey2, ikey, fidx2,
-                                               fidx, nf, 0, ib, s));
-  tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, start, nu + 1, s);
   MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, count, start, nu + 1, s));
-  k_island_median<<<div_up(nu, T), T, 0, s>>>(nu, count, start, fidx, ratio, median);
+  k_island_fill<<<div_up(nf, T), T, 0, s>>>(nf, ratio, island, start, cursor, items);
+  k_island_select<<<nu, 256, 0, s>>>(nu, count, start, items, median);
   k_face_setup<<<div_up(nf, T), T, 0, s>>>(lo.uvs, lo.fuv, nf, res, uv_area, ratio, island, median, rf, attrs);
-  ctx.count_launch(2);
+  ctx.count_launch(7);
   MFB_CUDA_TRY(cudaGetLastError());
   plan.faces = rf;
   plan.attrs = attrs;
