@@ -369,6 +369,7 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
     fo.dbg_ts = c.buf<double>("bake.dts", 3 * g.texels());
   }
   for (int attempt = 0;; ++attempt) {
+    HostTrace ht("bake_dev");
     MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
     MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
 
@@ -421,9 +422,11 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
                                    sizeof(double) * 3 * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
     int hflags[4] = {0, 0, 0, 0};
     unsigned long long hcnt[4] = {0, 0, 0, 0};
+    ht.mark("enqueued");
     MFB_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(cudaMemcpyAsync(hcnt, counters, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
+    ht.mark("synced");
     if (hflags[1] && attempt == 0) {  // tile bins overflowed: rerun with the exact capacity
       c.bin_capacity = static_cast<int64_t>(hflags[2]) + 1;
       continue;
@@ -729,6 +732,8 @@ int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
     BNode* nodes = b->store.buf<BNode>("nodes", nn);
     BTri* tris = b->store.buf<BTri>("tris", b->bvh.n_tris);
     TBox* tbox = b->store.buf<TBox>("tbox", b->bvh.n_tris);
+    WNode* wn = b->store.buf<WNode>("wnodes", nn);
+    MFB_CUDA_TRY(cudaMemcpyAsync(wn, b->bvh.wnodes, sizeof(WNode) * nn, cudaMemcpyDeviceToDevice, ctx->c.stream));
     MFB_CUDA_TRY(cudaMemcpyAsync(tbox, b->bvh.tbox, sizeof(TBox) * b->bvh.n_tris, cudaMemcpyDeviceToDevice, ctx->c.stream));
     auto* acc = b->store.buf<unsigned long long>("acc", 8);
     MFB_CUDA_TRY(cudaMemcpyAsync(nodes, b->bvh.nodes, sizeof(BNode) * nn, cudaMemcpyDeviceToDevice, ctx->c.stream));
@@ -741,6 +746,7 @@ int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
     b->bvh.nodes = nodes;
     b->bvh.tris = tris;
     b->bvh.tbox = tbox;
+    b->bvh.wnodes = wn;
     b->bvh.scene_acc = acc;
     b->bvh.root_box_dev = nullptr;
     b->store.own_stream = false;

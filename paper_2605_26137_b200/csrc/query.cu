@@ -714,6 +714,148 @@ __global__ void __launch_bounds__(128) k_transfer_p(
   }
 }
 
+// ---------------------------------------------------------------- 4-wide while-while transfer
+// Per-thread while-while over the 4-wide collapse (WNode): each visit loads
+// one 128-B node (7 x LDG.128), tests four fp32 child boxes, continues into the
+// nearest admissible child and pushes the others far-to-near, halving the
+// dependent node-to-node chain of the binary walk.
+__device__ __forceinline__ void cswap(float& la, int& ra, float& lb, int& rb) {
+  if (lb < la) {
+    const float tl = la;
+    la = lb;
+    lb = tl;
+    const int tr = ra;
+    ra = rb;
+    rb = tr;
+  }
+}
+
+template <bool kDebug, bool kProf>
+__global__ void __launch_bounds__(128) k_transfer_w(
+    const WNode* __restrict__ wnodes, const BTri* __restrict__ tris, int32_t root,
+    const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
+    const float* __restrict__ qtbn, const int* __restrict__ qcount, const double* __restrict__ hiN,
+    const int32_t* __restrict__ hiF, double max_dist, uint8_t* __restrict__ rgb,
+    int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters,
+    unsigned long long* __restrict__ prof_out) {
+  const int nq = qcount[0];
+  const int lane = threadIdx.x & 31;
+  unsigned long long pv[4] = {0, 0, 0, 0};  // wide visits, leaf visits, triangle tests, queries
+  const double scene_max = from_ordered_dev(scene_acc[6]);
+  const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
+  unsigned long long hits = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i - lane < nq; i += gridDim.x * blockDim.x) {
+    const bool live = i < nq;
+    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) p = __ldg(qpos + i);
+    const float3 qf = make_float3(p.x, p.y, p.z);
+    const d3 q = mk3(p.x, p.y, p.z);
+    const double E = fmax(scene_max, fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z)))) * 0x1p-32;
+    Best best;
+    best.d = init;
+    best.face = -1;
+    best.bary = mk3(0.0, 0.0, 0.0);
+    float bnd = live ? prune_bound(init, E) : -INFINITY;
+    int32_t st_ref[kStackMax];
+    float st_lb[kStackMax];
+    int sp = 0;
+    constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
+    int32_t ref = live ? root : kDone;
+    while (ref != kDone) {
+      while (ref >= 0) {
+        if (kProf) ++pv[0];
+        const float4* np = reinterpret_cast<const float4*>(wnodes + ref);
+        const float4 lx = __ldg(np), ly = __ldg(np + 1), lz = __ldg(np + 2);
+        const float4 hx = __ldg(np + 3), hy = __ldg(np + 4), hz = __ldg(np + 5);
+        const int4 rr = __ldg(reinterpret_cast<const int4*>(np + 6));
+        float l0 = box_lb(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, qf, qf);
+        float l1 = box_lb(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, qf, qf);
+        float l2 = box_lb(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, qf, qf);
+        float l3 = box_lb(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, qf, qf);
+        int r0 = rr.x, r1 = rr.y, r2 = rr.z, r3 = rr.w;
+        // sort the four (lb, ref) pairs ascending (5-comparator network)
+        cswap(l0, r0, l1, r1);
+        cswap(l2, r2, l3, r3);
+        cswap(l0, r0, l2, r2);
+        cswap(l1, r1, l3, r3);
+        cswap(l1, r1, l2, r2);
+        if (l3 <= bnd) {
+          st_ref[sp] = r3;
+          st_lb[sp] = l3;
+          ++sp;
+        }
+        if (l2 <= bnd) {
+          st_ref[sp] = r2;
+          st_lb[sp] = l2;
+          ++sp;
+        }
+        if (l1 <= bnd) {
+          st_ref[sp] = r1;
+          st_lb[sp] = l1;
+          ++sp;
+        }
+        if (l0 <= bnd) {
+          ref = r0;
+        } else {
+          ref = kDone;
+          while (sp > 0) {
+            --sp;
+            if (st_lb[sp] <= bnd) {
+              ref = st_ref[sp];
+              break;
+            }
+          }
+        }
+      }
+      if (ref == kDone) break;
+      int first, count;
+      leaf_decode(ref, first, count);
+      if (kProf) {
+        ++pv[1];
+        pv[2] += count;
+      }
+      for (int k = 0; k < count; ++k) {
+        d3 A, B, C;
+        int face;
+        load_tri(tris + first + k, A, B, C, face);
+        d3 bary;
+        const d3 pt = closest_point_triangle_sel(q, A, B, C, bary);
+        const double ds = sqnorm(pt - q);
+        if (ds < best.d || (ds == best.d && face < best.face)) {
+          best.d = ds;
+          best.face = face;
+          best.bary = bary;
+          bnd = prune_bound(ds, E);
+        }
+      }
+      ref = kDone;
+      while (sp > 0) {
+        --sp;
+        if (st_lb[sp] <= bnd) {
+          ref = st_ref[sp];
+          break;
+        }
+      }
+    }
+    if (!live) continue;
+    if (kProf) ++pv[3];
+    if (best.face >= 0) ++hits;
+    encode_texel(best, qtbn + 9ll * i, hiN, hiF, rgb, __float_as_int(p.w), kDebug ? dbg_face : nullptr,
+                 kDebug ? dbg_ts : nullptr);
+  }
+  if (kProf)
+    for (int k = 0; k < 4; ++k) {
+      unsigned long long v = pv[k];
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0) atomicAdd(&prof_out[k], v);
+    }
+  if (counters) {
+    for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
+    if (lane == 0 && hits) atomicAdd(&counters[1], hits);
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));
+  }
+}
+
 // kPass 1: pass A (records each query's winning face in face_map);
 // kPass 2: pass B (queries stored from the back of the list; each lane first
 // tests the face pass A found for its 2x2-quad corner texel, which only
@@ -1009,7 +1151,31 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     const char* e = std::getenv("MFB_REFILL");
     return e ? std::atoi(e) : 0;
   }();
-  if (per_thread && refill > 0) {
+  // 4-wide walk (MFB_BVH4=1): 13.8 wide visits vs 27.1 binary visits per
+  // query on config B but the same time (1.45 vs 1.43 ms, r01 profiles) - the
+  // kernel is issue-bound, not chain-latency-bound - so binary stays default.
+  static const bool wide = [] {
+    const char* e = std::getenv("MFB_BVH4");
+    return e && std::string(e) == "1";
+  }();
+  if (per_thread && wide && refill == 0) {
+    static int bpw = 0;
+    if (!bpw) {
+      MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpw, k_transfer_w<false, false>, 128, 0));
+      if (bpw < 1) bpw = 1;
+    }
+    const int gw = std::max(1, std::min(kNumSMs * bpw, div_up(a.q.capacity, 128)));
+#define MFB_XFER_W(D, P)                                                                                      \
+  k_transfer_w<D, P><<<gw, 128, 0, s>>>(bvh.wnodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn,  \
+                                        a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb,               \
+                                        D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf)
+    if (prof) {
+      if (dbg) MFB_XFER_W(true, true); else MFB_XFER_W(false, true);
+    } else {
+      if (dbg) MFB_XFER_W(true, false); else MFB_XFER_W(false, false);
+    }
+#undef MFB_XFER_W
+  } else if (per_thread && refill > 0) {
     static int bpp = 0;
     if (!bpp) {
       MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpp, k_transfer_p<false, 8, 256>, 128, 0));
@@ -1072,6 +1238,9 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
     if (per_thread) {
       const double nqd = h[3] ? static_cast<double>(h[3]) : 1.0;
+      if (wide && refill == 0)
+        std::fprintf(stderr, "[mfb prof] (4-wide) per query: wide visits %.2f leaves %.2f triangles %.2f\n",
+                     h[0] / nqd, h[1] / nqd, h[2] / nqd);
       std::fprintf(stderr, "[mfb prof] per query: internal %.2f leaves %.2f triangles %.2f (queries %llu)\n",
                    h[0] / nqd, h[1] / nqd, h[2] / nqd, h[3]);
       return;

@@ -475,7 +475,7 @@ __device__ __forceinline__ void emit_fused(int64_t gi, int x, int y, bool in, ui
   const bool is_q = in && valid && rel;
   const bool pass_a = kSeedPasses ? ((x | y) & 1) == 0 : true;
   const int slot_a = compact_slot(is_q && pass_a, fo.q.count, fo.q.capacity, overflow);
-  const int slot_b = compact_slot(is_q && !pass_a, fo.q.count + 1, fo.q.capacity, overflow);
+  const int slot_b = kSeedPasses ? compact_slot(is_q && !pass_a, fo.q.count + 1, fo.q.capacity, overflow) : -1;
   if (fo.valid_count) {
     const unsigned vm = __ballot_sync(0xffffffffu, in && valid);
     if ((threadIdx.x & 31) == 0 && vm) atomicAdd(fo.valid_count, static_cast<unsigned long long>(__popc(vm)));
