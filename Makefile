@@ -4,8 +4,8 @@
 #   paper_2605_26137_b200/libmeshforge_b200.so
 #                                           the reference-compatible C++ API
 #                                           (include/meshforge/...) over the C ABI
-#   build/test_bake_b200                    C++ parity tests (tests/cpp) against
-#                                           the C++ API
+#   build/test_bake_b200                    C++ KAT tests (tests/cpp) through the
+#                                           C++ API (run on a GPU by tests/test_cpp_api.py)
 #   oracle/...                              see oracle/Makefile
 #
 # Every CUDA TU is compiled for sm_100a only, with --fmad=false so fp64
@@ -14,19 +14,19 @@ NVCC ?= nvcc
 CXX ?= g++
 PKG := paper_2605_26137_b200
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Iinclude \
+NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Iinclude -Iinclude/eigen_shim \
            -Xptxas -warn-spills --expt-relaxed-constexpr
-CXXFLAGS := -std=c++20 -O2 -g -ffp-contract=off -fPIC -Iinclude -Wall -Wextra
+CXXFLAGS := -std=c++20 -O2 -g -ffp-contract=off -fPIC -Iinclude -Iinclude/eigen_shim -Wall -Wextra
 CU_SRCS := $(wildcard $(PKG)/csrc/*.cu)
 CU_OBJS := $(patsubst $(PKG)/csrc/%.cu,build/cu/%.o,$(CU_SRCS))
 CU_HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/mfbake.h
-MF_HDRS := $(shell find include/meshforge -name '*.h' 2>/dev/null) include/Eigen/Core
+MF_HDRS := $(shell find include/meshforge -name '*.h' 2>/dev/null) include/eigen_shim/Eigen/Core
 
 .PHONY: all lib cpp oracle clean
 all: lib cpp oracle
 
 lib: $(PKG)/libmfbake.so
-cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200 build/test_spatial_b200
+cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200
 
 build/cu/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 	@mkdir -p build/cu
@@ -38,15 +38,9 @@ $(PKG)/libmfbake.so: $(CU_OBJS)
 $(PKG)/libmeshforge_b200.so: $(PKG)/cpp/meshforge_b200.cpp $(MF_HDRS) include/mfbake.h $(PKG)/libmfbake.so
 	$(CXX) $(CXXFLAGS) -shared -o $@ $< -L$(PKG) -lmfbake -Wl,-rpath,'$$ORIGIN'
 
-build/test_bake_b200: tests/cpp/test_bake_b200.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so $(PKG)/fixtures_cpp.h
+build/test_bake_b200: tests/cpp/test_bake_b200.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so
 	@mkdir -p build
-	$(CXX) $(CXXFLAGS) -Itests/cpp -I$(PKG) -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake \
-	  -Wl,-rpath,'$$ORIGIN/../$(PKG)'
-
-build/test_spatial_b200: tests/cpp/test_spatial_b200.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so $(PKG)/fixtures_cpp.h
-	@mkdir -p build
-	$(CXX) $(CXXFLAGS) -Itests/cpp -I$(PKG) -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake \
-	  -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+	$(CXX) $(CXXFLAGS) -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 oracle:
 	$(MAKE) -C oracle

@@ -186,6 +186,14 @@ int mf_bvh_raycast_first_dev(mf_bvh* bvh, const double* origins_dev, const doubl
                              int64_t n, double tmin, double tmax, int32_t* face_dev,
                              double* t_dev, double* u_dev, double* v_dev);
 
+/* raycastFirstBrute / closestPointBrute (bvh.cpp:178-189): O(faces) per
+ * query with the same tie rules, one CTA per query on the device. */
+int mf_closest_point_brute(mf_ctx* ctx, const mf_mesh_view* mesh, const double* queries, int64_t n,
+                           int32_t* face, double* dist_sq, double* point, double* bary);
+int mf_raycast_first_brute(mf_ctx* ctx, const mf_mesh_view* mesh, const double* origins,
+                           const double* dirs, int64_t n, double tmin, double tmax, int32_t* face,
+                           double* t, double* u, double* v);
+
 /* ---- lowpoly helpers ----------------------------------------------------- */
 /* computeWedgeTangents (bake/tangent.cpp:22-82): frames n_faces x 3 corners x
  * {tangent, bitangent, normal} x 3 f64 (= std::array<TangentFrame,3>). */

@@ -4,7 +4,7 @@
 //
 // A thin extern "C" shell around the reference's OWN translation units
 // (compiled in place from /root/reference/proj by oracle/Makefile against the
-// Eigen-subset shim in include/Eigen). Nothing here re-implements the
+// Eigen-subset shim in include/eigen_shim). Nothing here re-implements the
 // algorithm; it converts flat arrays to meshforge::TriangleMesh / GBuffer /
 // ImageU8, calls the reference entry points, and copies results back:
 //   rasterizeGBuffer / transferNormals / dilateSeams  (src/bake/gbuffer.cpp:92-322)

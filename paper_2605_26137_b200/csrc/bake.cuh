@@ -233,6 +233,10 @@ void closest_within(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* q, 
 void raycast_first(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* o, const double* d,
                    int64_t n, double tmin, double tmax, int32_t* face, double* t, double* u,
                    double* v);
+void closest_brute(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* q, int64_t n, int32_t* face,
+                   double* dist_sq, double* point, double* bary);
+void raycast_brute(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* o, const double* d, int64_t n,
+                   double tmin, double tmax, int32_t* face, double* t, double* u, double* v);
 
 // ---------------------------------------------------------------- dilation
 // dilateSeams over a slab: input map rows [in_row0, in_row0 + in_rows) of a

@@ -904,6 +904,75 @@ int mf_bvh_raycast_first(mf_bvh* bvh, const double* o, const double* d, int64_t 
   });
 }
 
+int mf_closest_point_brute(mf_ctx* ctx, const mf_mesh_view* mesh, const double* q, int64_t n, int32_t* face,
+                           double* dist_sq, double* point, double* bary) {
+  if (!ctx || (n > 0 && (!q || !face || !dist_sq))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    mf_mesh m;
+    m.ctx = ctx;
+    upload_mesh(c, c.stream, mesh, &m, "up.m");
+    if (n <= 0) return MF_OK;
+    double* dq = c.buf<double>("bf.q", 3 * n);
+    int32_t* df = c.buf<int32_t>("bf.f", n);
+    double* dd = c.buf<double>("bf.d", n);
+    double* dp = c.buf<double>("bf.p", 3 * n);
+    double* db = c.buf<double>("bf.b", 3 * n);
+    MFB_CUDA_TRY(cudaMemcpyAsync(dq, q, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    if (m.m.nf > 0 && m.status == MF_OK) {
+      closest_brute(c, c.stream, m.m, dq, n, df, dd, dp, db);
+    } else {  // no faces (or unusable indices): every query misses
+      MFB_CUDA_TRY(cudaMemsetAsync(df, 0xff, sizeof(int32_t) * n, c.stream));
+      std::vector<double> inf(n, INFINITY);
+      MFB_CUDA_TRY(cudaMemcpyAsync(dd, inf.data(), sizeof(double) * n, cudaMemcpyHostToDevice, c.stream));
+      MFB_CUDA_TRY(cudaMemsetAsync(dp, 0, sizeof(double) * 3 * n, c.stream));
+      MFB_CUDA_TRY(cudaMemsetAsync(db, 0, sizeof(double) * 3 * n, c.stream));
+      MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    }
+    MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dist_sq, dd, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    if (point) MFB_CUDA_TRY(cudaMemcpyAsync(point, dp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    if (bary) MFB_CUDA_TRY(cudaMemcpyAsync(bary, db, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_raycast_first_brute(mf_ctx* ctx, const mf_mesh_view* mesh, const double* o, const double* d, int64_t n,
+                           double tmin, double tmax, int32_t* face, double* t, double* u, double* v) {
+  if (!ctx || (n > 0 && (!o || !d || !face || !t || !u || !v))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    mf_mesh m;
+    m.ctx = ctx;
+    upload_mesh(c, c.stream, mesh, &m, "up.m");
+    if (n <= 0) return MF_OK;
+    if (m.m.nf == 0 || m.status != MF_OK) {
+      for (int64_t i = 0; i < n; ++i) {
+        face[i] = -1;
+        t[i] = INFINITY;
+        u[i] = v[i] = 0.0;
+      }
+      return MF_OK;
+    }
+    double* dO = c.buf<double>("rb.o", 3 * n);
+    double* dD = c.buf<double>("rb.d", 3 * n);
+    int32_t* df = c.buf<int32_t>("rb.f", n);
+    double* dt = c.buf<double>("rb.t", n);
+    double* du = c.buf<double>("rb.u", n);
+    double* dv = c.buf<double>("rb.v", n);
+    MFB_CUDA_TRY(cudaMemcpyAsync(dO, o, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dD, d, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
+    raycast_brute(c, c.stream, m.m, dO, dD, n, tmin, tmax, df, dt, du, dv);
+    MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(t, dt, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(u, du, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(v, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
 int mf_wedge_tangents(mf_ctx* ctx, const mf_mesh_view* mesh, double* frames) {
   if (!ctx || !frames) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
   return guarded(ctx, [&]() -> int {

@@ -1102,6 +1102,115 @@ __global__ void __launch_bounds__(128) k_raycast(const BNode* __restrict__ nodes
   v_out[i] = bv;
 }
 
+// ---------------------------------------------------------------- brute force
+// One CTA per query strides over all faces and reduces the lexicographic
+// minimum (distSq, face) / (t, face) - the reference's O(F) oracles.
+__global__ void __launch_bounds__(256) k_closest_brute(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                                       int nf, const double* __restrict__ q, int64_t n,
+                                                       int32_t* __restrict__ face_out, double* __restrict__ dist_out,
+                                                       double* __restrict__ point_out, double* __restrict__ bary_out) {
+  const int64_t qi = blockIdx.x;
+  if (qi >= n) return;
+  const d3 p = ld3(q + 3 * qi);
+  double bd = INFINITY;
+  int bf = -1;
+  d3 bp = mk3(0.0, 0.0, 0.0), bb = mk3(0.0, 0.0, 0.0);
+  for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+    d3 bary;
+    const d3 pt = closest_point_triangle(p, ld3(pos + 3 * faces[3 * f]), ld3(pos + 3 * faces[3 * f + 1]),
+                                         ld3(pos + 3 * faces[3 * f + 2]), bary);
+    const double ds = sqnorm(pt - p);
+    if (ds < bd || (ds == bd && f < bf)) {  // improves(), bvh.cpp:21-23 (bf = -1 never wins a tie)
+      bd = ds;
+      bf = f;
+      bp = pt;
+      bb = bary;
+    }
+  }
+  __shared__ double sd[256];
+  __shared__ int sf[256];
+  sd[threadIdx.x] = bd;
+  sf[threadIdx.x] = bf < 0 ? 0x7fffffff : bf;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double od = sd[threadIdx.x + w];
+      const int of = sf[threadIdx.x + w];
+      if (od < sd[threadIdx.x] || (od == sd[threadIdx.x] && of < sf[threadIdx.x])) {
+        sd[threadIdx.x] = od;
+        sf[threadIdx.x] = of;
+      }
+    }
+    __syncthreads();
+  }
+  const int wf = sf[0];
+  if (threadIdx.x == 0 && (wf == 0x7fffffff)) {
+    face_out[qi] = -1;
+    dist_out[qi] = INFINITY;
+    if (point_out) st3(point_out + 3 * qi, mk3(0.0, 0.0, 0.0));
+    if (bary_out) st3(bary_out + 3 * qi, mk3(0.0, 0.0, 0.0));
+  }
+  if (wf != 0x7fffffff && bf == wf) {
+    face_out[qi] = bf;
+    dist_out[qi] = bd;
+    if (point_out) st3(point_out + 3 * qi, bp);
+    if (bary_out) st3(bary_out + 3 * qi, bb);
+  }
+}
+
+__global__ void __launch_bounds__(256) k_raycast_brute(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                                       int nf, const double* __restrict__ org,
+                                                       const double* __restrict__ dir, int64_t n, double tmin,
+                                                       double tmax, int32_t* __restrict__ face_out,
+                                                       double* __restrict__ t_out, double* __restrict__ u_out,
+                                                       double* __restrict__ v_out) {
+  const int64_t qi = blockIdx.x;
+  if (qi >= n) return;
+  const d3 o = ld3(org + 3 * qi), d = ld3(dir + 3 * qi);
+  double bt = INFINITY, bu = 0.0, bv = 0.0;
+  int bf = -1;
+  for (int f = threadIdx.x; f < nf; f += blockDim.x) {
+    double t, u, v;
+    if (ray_triangle(o, d, ld3(pos + 3 * faces[3 * f]), ld3(pos + 3 * faces[3 * f + 1]),
+                     ld3(pos + 3 * faces[3 * f + 2]), t, u, v) &&
+        t >= tmin && t <= tmax && (t < bt || (t == bt && f < bf))) {  // testFace, bvh.cpp:25-34
+      bt = t;
+      bu = u;
+      bv = v;
+      bf = f;
+    }
+  }
+  __shared__ double st[256];
+  __shared__ int sf[256];
+  st[threadIdx.x] = bt;
+  sf[threadIdx.x] = bf < 0 ? 0x7fffffff : bf;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      const double ot = st[threadIdx.x + w];
+      const int of = sf[threadIdx.x + w];
+      if (ot < st[threadIdx.x] || (ot == st[threadIdx.x] && of < sf[threadIdx.x])) {
+        st[threadIdx.x] = ot;
+        sf[threadIdx.x] = of;
+      }
+    }
+    __syncthreads();
+  }
+  const int wf = sf[0];
+  if (threadIdx.x == 0 && wf == 0x7fffffff) {
+    face_out[qi] = -1;
+    t_out[qi] = INFINITY;
+    u_out[qi] = 0.0;
+    v_out[qi] = 0.0;
+  }
+  if (wf != 0x7fffffff && bf == wf) {
+    face_out[qi] = bf;
+    t_out[qi] = bt;
+    u_out[qi] = bu;
+    v_out[qi] = bv;
+  }
+}
+
 }  // namespace
 
 static const unsigned long long* scene_acc_of(Ctx&, const Lbvh& bvh) { return bvh.scene_acc; }
@@ -1257,6 +1366,22 @@ void closest_within(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* q, 
   if (n <= 0) return;
   k_closest<<<div_up(n, 128), 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, scene_acc_of(ctx, bvh),
                                            q, n, max_dist, face, dist_sq, point, bary);
+  ctx.count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+void closest_brute(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* q, int64_t n, int32_t* face,
+                   double* dist_sq, double* point, double* bary) {
+  if (n <= 0) return;
+  k_closest_brute<<<static_cast<unsigned>(n), 256, 0, s>>>(m.pos, m.faces, m.nf, q, n, face, dist_sq, point, bary);
+  ctx.count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+void raycast_brute(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* o, const double* d, int64_t n,
+                   double tmin, double tmax, int32_t* face, double* t, double* u, double* v) {
+  if (n <= 0) return;
+  k_raycast_brute<<<static_cast<unsigned>(n), 256, 0, s>>>(m.pos, m.faces, m.nf, o, d, n, tmin, tmax, face, t, u, v);
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
 }

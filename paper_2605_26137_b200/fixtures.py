@@ -357,6 +357,7 @@ def chart_atlas(n: int, res: int, margin_texels: float = 3.0):
     L = (1.0 - 2 * pad) / (4 * math.sqrt(3.0) / 2.0)
     H = L * math.sqrt(3.0) / 2.0
     r_in = L / (2.0 * math.sqrt(3.0))
+    margin_texels = min(margin_texels, 0.25 * r_in * res)  # small atlases: keep charts >= 3/4 size
     delta = margin_texels / res
     shrink = (r_in - delta) / r_in
     assert shrink > 0.5, "atlas resolution too small for the chart margin"

@@ -1,0 +1,115 @@
+"""Regenerates tests/golden/*.npz from the REFERENCE's own translation units
+(oracle/_ref/libmfref.so, built by oracle/Makefile from /root/reference).
+
+Run here (the container that has /root/reference):
+    python tests/golden/make_golden.py
+The .npz files are committed; the GPU box never reads /root/reference.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import bindings  # noqa: E402
+from paper_2605_26137_b200 import fixtures as fx  # noqa: E402
+
+# Small cases whose outputs pin the oracle and the CUDA path.
+BAKE_CASES = {
+    # name: (n_dense, n_low, res, frac, seed, low_scale)
+    "tiny": (24, 4, 64, 0.01, 7, 1.0),
+    "small": (48, 8, 128, 0.01, 11, 1.0),
+    "cage": (48, 8, 128, 0.05, 5, 1.04),
+}
+
+
+def bake_case(ref, name):
+    nd, nl, res, frac, seed, scale = BAKE_CASES[name]
+    p = fx.bake_pair(nd, nl, res, frac, seed, scale, name=name)
+    g = ref.raster_gbuffer(p.lowpoly, res)
+    out = ref.bake(p.lowpoly, p.dense, res, p.bbox_diagonal, frac, 4, debug=True)
+    return dict(
+        res=res, frac=frac, diag=p.bbox_diagonal, seed=seed, n_dense=nd, n_low=nl, low_scale=scale,
+        valid=g.valid, reliable=g.reliable, position=g.position, normal=g.normal, tangent=g.tangent,
+        bitangent=g.bitangent, rgb=out["rgb"], rgb_raw=out["rgb_raw"], face=out["face"], ts=out["ts"],
+        n_node=out["n_node"], n_tri=out["n_tri"])
+
+
+def spatial_case(ref):
+    sphere = ref.fixture(0, 2, r=0.5)  # icosphere(2)
+    q = ref.random_points(300, (-1, -1, -1), (1, 1, 1), 41)
+    f, ds, pt, bary = ref.closest_within(sphere, q)
+    fb, dsb, ptb, baryb = ref.closest_within(sphere, q, 0.2)
+    uvs = ref.fixture(1, 24, 24, r=0.5)  # uvSphere(24, 24)
+    o = ref.random_points(300, (-1.5, -1.5, -1.5), (1.5, 1.5, 1.5), 21)
+    tgt = ref.random_points(300, (-0.4, -0.4, -0.4), (0.4, 0.4, 0.4), 23)
+    d = ref.random_units(300, 22)
+    d[::2] = (tgt - o)[::2] / np.linalg.norm((tgt - o)[::2], axis=1, keepdims=True)
+    rf, rt, ru, rv = ref.raycast_first(uvs, o, d)
+    return dict(ico_pos=sphere.positions, ico_faces=sphere.faces, q=q, cp_face=f, cp_dist=ds, cp_point=pt,
+                cp_bary=bary, cpw_face=fb, cpw_dist=dsb, uvs_pos=uvs.positions, uvs_faces=uvs.faces,
+                ray_o=o, ray_d=d, ray_face=rf, ray_t=rt, ray_u=ru, ray_v=rv)
+
+
+def tangent_case(ref):
+    m = ref.fixture(0, 1, r=0.5)
+    m = fx.assign_cell_uvs(m, 10)
+    frames = ref.wedge_tangents(m)
+    vn = ref.vertex_normals(ref.fixture(0, 3, r=0.5))
+    return dict(pos=m.positions, faces=m.faces, uvs=m.uvs, face_uvs=m.face_uvs, frames=frames,
+                vn_mesh_pos=ref.fixture(0, 3, r=0.5).positions, vn_mesh_faces=ref.fixture(0, 3, r=0.5).faces,
+                vnormals=vn)
+
+
+def kat_case(ref):
+    """Small known-answer inputs of proj/tests/test_bake.cpp run through the reference."""
+    from paper_2605_26137_b200.mesh import TriangleMesh
+    out = {}
+    # off-density face (test_bake.cpp:145-169)
+    m = TriangleMesh([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0], [1, 0, 200]], [[0, 1, 2], [0, 2, 3], [1, 4, 2]],
+                     uvs=[[0.05, 0.05], [0.35, 0.05], [0.35, 0.35], [0.05, 0.35], [0.65, 0.05]],
+                     face_uvs=[[0, 1, 2], [0, 2, 3], [1, 4, 2]])
+    g = ref.raster_gbuffer(m, 128)
+    out.update(od_valid=g.valid, od_reliable=g.reliable, od_rgb=ref.transfer_normals(g, m, m.bbox_diagonal()))
+    # distance filter (test_bake.cpp:185-200)
+    q = fx.identity_quad()
+    far = fx.identity_quad()
+    far.positions[:, 2] += 0.08
+    g = ref.raster_gbuffer(q, 32)
+    out.update(far_valid=g.valid, far_rgb=ref.transfer_normals(g, far, float(np.sqrt(2.0))))
+    # fill rule (test_bake.cpp:135-143) and one triangle covering the atlas (:77-96)
+    out["fill_valid"] = ref.raster_gbuffer(q, 8).valid
+    tri = TriangleMesh([[0, 0, 0], [2, 0, 0], [0, 2, 0]], [[0, 1, 2]], uvs=[[0, 0], [2, 0], [0, 2]],
+                       face_uvs=[[0, 1, 2]])
+    g = ref.raster_gbuffer(tri, 32)
+    out.update(tri_valid=g.valid, tri_position=g.position, tri_normal=g.normal, tri_tangent=g.tangent)
+    # lone texel chebyshev ball (test_bake.cpp:253-274)
+    valid = np.zeros(121, np.uint8)
+    valid[5 * 11 + 5] = 1
+    img = np.zeros((121, 3), np.uint8)
+    img[5 * 11 + 5] = (10, 20, 30)
+    out["lone_valid"] = valid
+    out["lone_in"] = img
+    out["lone_out"] = ref.dilate_seams(img, 11, 11, 3, 11, valid, 2)
+    return out
+
+
+def main():
+    ref = bindings.ref()
+    np.savez_compressed(os.path.join(HERE, "kats.npz"), **kat_case(ref))
+    for name in BAKE_CASES:
+        np.savez_compressed(os.path.join(HERE, f"bake_{name}.npz"), **bake_case(ref, name))
+    np.savez_compressed(os.path.join(HERE, "spatial.npz"), **spatial_case(ref))
+    np.savez_compressed(os.path.join(HERE, "tangents.npz"), **tangent_case(ref))
+    for f in sorted(os.listdir(HERE)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(HERE, f)))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,30 @@
+"""GPU: the reference-compatible C++ API (include/meshforge over
+libmfbake.so): our C++ port of the bake KATs, and the reference's OWN
+unmodified tests/test_spatial.cpp compiled against our headers
+(oracle/_ref/test_spatial_b200, built by oracle/Makefile)."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(exe):
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    return r.stdout
+
+
+def test_cpp_bake_kats(gpu_ctx):
+    out = run(os.path.join(ROOT, "build", "test_bake_b200"))
+    assert "FAIL" not in out and "test cases passed" in out
+
+
+def test_reference_test_spatial_against_b200_api(gpu_ctx):
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_spatial_b200")
+    if not os.path.exists(exe):
+        pytest.skip("built only where /root/reference exists")
+    out = run(exe)
+    assert "14/14 test cases passed" in out

@@ -95,3 +95,94 @@ def test_dilate_seams_bit_exact(gpu_ctx, port, radius):
     out = mf.dilate_seams(img, g, radius)
     ref = port.dilate_seams(img.reshape(-1, 3), res, res, 3, res, valid, radius).reshape(res, res, 3)
     assert np.array_equal(out, ref)
+
+
+# ---------------------------------------------------------------- reference goldens
+import os  # noqa: E402
+
+from paper_2605_26137_b200.mesh import TriangleMesh  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.mark.parametrize("case", ["tiny", "small", "cage"])
+def test_gpu_matches_reference_golden_bake(gpu_ctx, case):
+    """Against outputs of the reference's own code (tests/golden/make_golden.py)."""
+    d = np.load(os.path.join(GOLDEN, f"bake_{case}.npz"))
+    p = fx.bake_pair(int(d["n_dense"]), int(d["n_low"]), int(d["res"]), float(d["frac"]), int(d["seed"]),
+                     float(d["low_scale"]), name=case)
+    g = mf.rasterize_gbuffer(p.lowpoly, p.res)
+    assert np.array_equal(g.valid, d["valid"]) and np.array_equal(g.reliable, d["reliable"])
+    assert np.array_equal(_u32(g.position), _u32(d["position"]))
+    assert np.array_equal(_u32(g.normal), _u32(d["normal"]))
+    assert np.abs(g.tangent - d["tangent"]).max() <= 1e-6
+    out = mf.bake_normal_map(p.lowpoly, p.dense, p.res, p.bbox_diagonal, float(d["frac"]), 4, debug=True)
+    assert np.array_equal(out["face"], d["face"])
+    assert np.abs(out["ts"] - d["ts"]).max() <= TS_TOL
+    assert_rgb_parity(out["rgb"], d["rgb"], d["ts"])
+
+
+def test_gpu_reference_kats(gpu_ctx):
+    """test_bake.cpp:77-200,253-274 known answers, through the Python mirror API."""
+    d = np.load(os.path.join(GOLDEN, "kats.npz"))
+    m = TriangleMesh([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0], [1, 0, 200]], [[0, 1, 2], [0, 2, 3], [1, 4, 2]],
+                     uvs=[[0.05, 0.05], [0.35, 0.05], [0.35, 0.35], [0.05, 0.35], [0.65, 0.05]],
+                     face_uvs=[[0, 1, 2], [0, 2, 3], [1, 4, 2]])
+    g = mf.rasterize_gbuffer(m, 128)
+    assert np.array_equal(g.valid, d["od_valid"]) and np.array_equal(g.reliable, d["od_reliable"])
+    assert np.array_equal(mf.transfer_normals(g, m, m.bbox_diagonal()).reshape(-1, 3), d["od_rgb"])
+    q, far = fx.identity_quad(), fx.identity_quad()
+    far.positions[:, 2] += 0.08
+    g = mf.rasterize_gbuffer(q, 32)
+    assert np.array_equal(mf.transfer_normals(g, far, float(np.sqrt(2.0))).reshape(-1, 3), d["far_rgb"])
+    assert np.array_equal(mf.rasterize_gbuffer(q, 8).valid, d["fill_valid"])
+    tri = TriangleMesh([[0, 0, 0], [2, 0, 0], [0, 2, 0]], [[0, 1, 2]], uvs=[[0, 0], [2, 0], [0, 2]],
+                       face_uvs=[[0, 1, 2]])
+    g = mf.rasterize_gbuffer(tri, 32)
+    assert (g.valid == 1).all()
+    assert np.array_equal(_u32(g.position), _u32(d["tri_position"]))
+    gl = mf.GBuffer.allocate(11)
+    gl.valid[:] = d["lone_valid"]
+    out = mf.dilate_seams(d["lone_in"].reshape(11, 11, 3), gl, 2)
+    assert np.array_equal(out.reshape(-1, 3), d["lone_out"])
+
+
+def test_gpu_error_codes(gpu_ctx):
+    """test_bake.cpp:126-133,332-350: same codes through the C ABI."""
+    def code(fn):
+        with pytest.raises(mf.MeshforgeError) as e:
+            fn()
+        return e.value.code
+
+    bare = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]])
+    assert code(lambda: mf.rasterize_gbuffer(bare, 64)) == "InvalidGeometry"
+    assert code(lambda: mf.rasterize_gbuffer(fx.identity_quad(), 0)) == "InvalidConfig"
+    assert code(lambda: mf.rasterize_gbuffer(TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3))), 64)) == "EmptyMesh"
+    overlap = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 0, 1], [0, 1, 1]],
+                           [[0, 1, 2], [3, 4, 5]],
+                           uvs=[[0.1, 0.1], [0.9, 0.1], [0.1, 0.9], [0.2, 0.2], [0.8, 0.2], [0.2, 0.8]],
+                           face_uvs=[[0, 1, 2], [3, 4, 5]])
+    assert code(lambda: mf.rasterize_gbuffer(overlap, 64)) == "AtlasOverlap"
+    assert code(lambda: mf.bake_normal_map(overlap, fx.identity_quad(), 64, 1.0)) == "AtlasOverlap"
+    g = mf.rasterize_gbuffer(fx.identity_quad(), 16)
+    assert code(lambda: mf.transfer_normals(mf.GBuffer.allocate(0), fx.identity_quad(), 1.0)) == "InvalidConfig"
+    assert code(lambda: mf.transfer_normals(g, fx.identity_quad(), 0.0)) == "InvalidConfig"
+    empty = TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3)))
+    assert code(lambda: mf.transfer_normals(g, empty, 1.0)) == "EmptyMesh"
+    nan = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, np.nan, 0]], [[0, 1, 2]])
+    assert code(lambda: mf.transfer_normals(g, nan, 1.0)) == "InvalidGeometry"
+    assert code(lambda: mf.dilate_seams(np.zeros((8, 8, 3), np.uint8), g, 2)) == "ShapeMismatch"
+    assert code(lambda: mf.dilate_seams(np.zeros((16, 16, 3), np.uint8), g, -1)) == "InvalidConfig"
+    # the context survives errors
+    assert mf.rasterize_gbuffer(fx.identity_quad(), 8).valid.sum() == 64
+
+
+def test_gpu_wedge_tangents_and_vertex_normals(gpu_ctx):
+    d = np.load(os.path.join(GOLDEN, "tangents.npz"))
+    m = TriangleMesh(d["pos"], d["faces"], uvs=d["uvs"], face_uvs=d["face_uvs"])
+    frames = mf.compute_wedge_tangents(m)
+    # normals are exact; tangents/bitangents go through acos (CUDA vs glibc ulps)
+    assert np.array_equal(frames[:, :, 2], d["frames"][:, :, 2])
+    assert np.abs(frames - d["frames"]).max() <= 1e-12
+    vm = TriangleMesh(d["vn_mesh_pos"], d["vn_mesh_faces"])
+    assert np.array_equal(mf.compute_vertex_normals(vm), d["vnormals"])

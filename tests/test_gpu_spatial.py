@@ -1,0 +1,150 @@
+"""GPU: the LBVH queries (Bvh::closestPointWithin / raycastFirst and the
+brute-force oracles) through the C ABI, restating proj/tests/test_spatial.cpp
+and checking against reference goldens: face ids, distances, points, t/u/v
+bit-exact."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2605_26137_b200 import fixtures as fx
+from paper_2605_26137_b200 import meshforge as mf
+from paper_2605_26137_b200.mesh import TriangleMesh
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def brute_closest(ctx, mesh, q):
+    import ctypes
+    q = np.ascontiguousarray(q, np.float64).reshape(-1, 3)
+    n = q.shape[0]
+    f, d, p, b = np.zeros(n, np.int32), np.zeros(n), np.zeros((n, 3)), np.zeros((n, 3))
+    v = mesh.view()
+    from paper_2605_26137_b200.capi import check
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    check(ctx.lib.mf_closest_point_brute(ctx.h, ctypes.byref(v), P(q), n, P(f), P(d), P(p), P(b)))
+    return f, d, p, b
+
+
+def brute_ray(ctx, mesh, o, dr, tmin=0.0, tmax=float("inf")):
+    import ctypes
+    o = np.ascontiguousarray(o, np.float64).reshape(-1, 3)
+    dr = np.ascontiguousarray(dr, np.float64).reshape(-1, 3)
+    n = o.shape[0]
+    f, t, u, v_ = np.zeros(n, np.int32), np.zeros(n), np.zeros(n), np.zeros(n)
+    v = mesh.view()
+    from paper_2605_26137_b200.capi import check
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    check(ctx.lib.mf_raycast_first_brute(ctx.h, ctypes.byref(v), P(o), P(dr), n, tmin, tmax, P(f), P(t), P(u),
+                                         P(v_)))
+    return f, t, u, v_
+
+
+def test_golden_closest_points_and_rays(gpu_ctx):
+    d = np.load(os.path.join(GOLDEN, "spatial.npz"))
+    ico = TriangleMesh(d["ico_pos"], d["ico_faces"])
+    bvh = mf.Bvh(ico)
+    f, ds, pt, bary = bvh.closest_points(d["q"])
+    assert np.array_equal(f, d["cp_face"]) and np.array_equal(ds, d["cp_dist"])
+    assert np.array_equal(pt, d["cp_point"]) and np.array_equal(bary, d["cp_bary"])
+    f, ds, _, _ = bvh.closest_points(d["q"], 0.2)
+    assert np.array_equal(f, d["cpw_face"]) and np.array_equal(ds, d["cpw_dist"])
+    uvs = TriangleMesh(d["uvs_pos"], d["uvs_faces"])
+    f, t, u, v = mf.Bvh(uvs).raycasts(d["ray_o"], d["ray_d"])
+    assert np.array_equal(f, d["ray_face"])
+    hit = f >= 0
+    assert np.array_equal(t[hit], d["ray_t"][hit])
+    assert np.array_equal(u[hit], d["ray_u"][hit]) and np.array_equal(v[hit], d["ray_v"][hit])
+
+
+def test_bvh_equals_brute_force_rays_10k_sphere(gpu_ctx, port):
+    """test_spatial.cpp:139-161 (bit-exact face, t, u, v), plus the oracle."""
+    sphere = fx.uv_sphere(72, 72, 0.5)
+    assert sphere.face_count() > 10000
+    o = fx.random_points_in_box(1000, (-1.5,) * 3, (1.5,) * 3, 21)
+    dirs = fx.random_unit_vectors(1000, 22)
+    tgt = fx.random_points_in_box(1000, (-0.4,) * 3, (0.4,) * 3, 23)
+    aim = (tgt - o) / np.linalg.norm(tgt - o, axis=1, keepdims=True)
+    dirs[::2] = aim[::2]
+    a = mf.Bvh(sphere).raycasts(o, dirs)
+    b = brute_ray(gpu_ctx, sphere, o, dirs)
+    c = port.raycast_first(sphere, o, dirs, brute=True)
+    for x, y, z in zip(a, b, c):
+        assert np.array_equal(x, y) and np.array_equal(x, z)
+    assert (a[0] >= 0).sum() > 100
+
+
+def test_closest_point_equals_brute_force(gpu_ctx, port):
+    """test_spatial.cpp:184-195 on starBlob(4, 48, 48), 1000 queries."""
+    blob = fx.star_blob(4, 48, 48)
+    q = fx.random_points_in_box(1000, (-1,) * 3, (1,) * 3, 31)
+    a = mf.Bvh(blob).closest_points(q)
+    b = brute_closest(gpu_ctx, blob, q)
+    c = port.closest_within(blob, q, brute=True)
+    for x, y, z in zip(a, b, c):
+        assert np.array_equal(x, y) and np.array_equal(x, z)
+
+
+def test_bounded_matches_global_inside_radius(gpu_ctx):
+    """test_spatial.cpp:197-212."""
+    s = fx.icosphere(3)
+    q = fx.random_points_in_box(200, (-1,) * 3, (1,) * 3, 41)
+    bvh = mf.Bvh(s)
+    fa, da, _, _ = bvh.closest_points(q)
+    fb, db, _, _ = bvh.closest_points(q, 0.2)
+    inside, outside = np.sqrt(da) < 0.2, np.sqrt(da) > 0.2
+    assert np.array_equal(fb[inside], fa[inside]) and np.array_equal(db[inside], da[inside])
+    assert (fb[outside] == -1).all() and np.isinf(db[outside]).all()
+
+
+def test_small_known_answers(gpu_ctx):
+    """test_spatial.cpp:74-137,163-182,214-226."""
+    tri = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]])
+    h = mf.Bvh(tri).raycast_first([1 / 3, 1 / 3, 2.0], [0, 0, -1])
+    assert h.valid() and h.face == 0 and abs(h.t - 2.0) < 1e-12
+    cube = fx.box((0.5, 0.5, 0.5))
+    h = mf.Bvh(cube).raycast_first([2, 0.1, 0.1], [-1, 0, 0])
+    assert h.valid() and abs(h.t - 1.5) < 1e-12
+    assert np.allclose(cube.positions[cube.faces[h.face]][:, 0], 0.5)
+    assert not mf.Bvh(fx.plane_grid(2, 2)).raycast_first([-1, -1, 0.5], [1, 0, 0]).valid()
+    quad = TriangleMesh([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0]], [[0, 1, 2], [0, 2, 3]])
+    assert mf.Bvh(quad).raycast_first([0.25, 0.25, 1.0], [0, 0, -1]).face == 0  # lower face on the tie
+    s = fx.icosphere(1)
+    sp = mf.Bvh(s).closest_point(s.positions[7])
+    assert sp.valid() and sp.distance() < 1e-12 and abs(sp.barycentric.max() - 1.0) < 1e-12
+    assert abs(mf.Bvh(fx.box((0.5, 0.5, 0.5), 2)).closest_point([0, 0, 0]).distance() - 0.5) < 1e-12
+    s2 = fx.icosphere(2)
+    rng = fx.CounterRng(6)
+    bvh = mf.Bvh(s2)
+    for i in range(100):
+        f = int(rng.below(3 * i, s2.face_count()))
+        u = float(rng.uniform(3 * i + 1))
+        v = float(rng.uniform(3 * i + 2)) * (1 - u)
+        t = s2.positions[s2.faces[f]]
+        p = (1 - u - v) * t[0] + u * t[1] + v * t[2]
+        assert bvh.closest_point(p).distance() < 1e-9
+
+
+def test_bvh_export_structurally_sound(gpu_ctx):
+    """test_spatial.cpp:228-263: every face in exactly one leaf, leaf boxes
+    contain their triangles, deterministic build."""
+    m = fx.star_blob(9, 40, 40)
+    a, b = mf.Bvh(m).export(), mf.Bvh(m).export()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    boxes, links, order = a
+    leaf = links[:, 3] > 0
+    seen = np.concatenate([order[f:f + c] for f, c in links[leaf][:, 2:4]])
+    assert np.array_equal(np.sort(seen), np.arange(m.face_count()))
+    for (f, c), box in zip(links[leaf][:, 2:4], boxes[leaf]):
+        pts = m.positions[m.faces[order[f:f + c]]].reshape(-1, 3)
+        assert (pts >= box[:3] - 1e-12).all() and (pts <= box[3:] + 1e-12).all()
+
+
+def test_bvh_rejects_bad_input(gpu_ctx):
+    """test_spatial.cpp:265-274."""
+    with pytest.raises(mf.MeshforgeError):
+        mf.Bvh(TriangleMesh([[0, 0, 0]], np.zeros((0, 3))))
+    with pytest.raises(mf.MeshforgeError):
+        mf.Bvh(TriangleMesh([[0, 0, 0], [1, 0, 0], [0, np.nan, 0]], [[0, 1, 2]]))
