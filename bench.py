@@ -38,8 +38,16 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "baked texels/sec (2048^2 atlas, 1M-face dense source, config B)"
+METRICS = {
+    "A": "baked texels/sec (512^2 atlas, 200k-face dense source, config A)",
+    "B": METRIC,
+    "C": "baked texels/sec (4096^2 atlas, 1M-face dense source, config C)",
+    "D": "baked texels/sec (1024^2 atlas, 500k-face dense source, config D asset)",
+    "E": "baked texels/sec (4096^2 atlas, 4M-face dense source, large cage offset, config E)",
+}
 UNIT = "texels/s"
 CONSTANTS = os.path.join(ROOT, "bench_data", "reference_counters.json")
+TRAFFIC = os.path.join(ROOT, "profiles", "k_transfer_ncu.json")  # one `ncu --set full` capture
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
@@ -54,6 +62,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: row-shard ONE atlas across ranks + NCCL all-gather (strong scaling) "
+                         "instead of one asset per rank")
     return ap.parse_args()
 
 
@@ -134,6 +145,18 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
+def transfer_traffic():
+    """dram__bytes_read + dram__bytes_write of the transfer kernel from the
+    committed `ncu --set full` capture summary (profiles/k_transfer_ncu.json)."""
+    try:
+        with open(TRAFFIC) as f:
+            d = json.load(f)
+        launch = next(x for x in d["launches"] if "k_transfer" in x["kernel"])
+        return float(launch["dram_bytes"]), d.get("source")
+    except (OSError, KeyError, StopIteration, ValueError):
+        return None, None
+
+
 def transfer_algorithmic_bytes(name, n_queries, n_valid, res):
     """transfer bytes per query W_q = 50 (G-buffer read) + 3 (RGB8
     write) + 64*N_node + 84*N_tri + 72 (winner's vertex normals), N_node/N_tri =
@@ -162,7 +185,7 @@ def run_ours(args):
     from paper_2605_26137_b200 import capi, fixtures as fx
 
     name = args.config
-    pair = fx.config_pair(name, seed=fx.CONFIGS[name]["seed"] + rank)
+    pair = fx.config_pair(name, seed=fx.CONFIGS[name]["seed"] + (0 if args.shard else rank))
     res = pair.res
     stream = torch.cuda.current_stream()
     ctx = capi.Context(local_rank, stream.cuda_stream)
@@ -175,9 +198,29 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")  # > 126 MB L2
     st = capi.MfBakeStats()
 
+    row_b, row_e = 0, res
+    shard_ranges = None
+    if args.shard and world > 1:
+        # one atlas, rows balanced by valid texels, all-gathered
+        import ctypes
+        from paper_2605_26137_b200 import sharding
+        counts = np.zeros(res, np.int64)
+        capi.check(lib.mf_coverage_rows(ctx.h, lo.h, res, ctypes.c_void_p(counts.ctypes.data)))
+        shard_ranges = sharding.balanced_row_ranges(counts, world)
+        row_b, row_e = shard_ranges[rank]
+        rows_max = max(e - b for b, e in shard_ranges)
+        slab = torch.empty((rows_max, res, 3), dtype=torch.uint8, device="cuda")
+        gathered = [torch.empty_like(slab) for _ in range(world)]
+
     def step(stats=None):
-        capi.check(lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, diag, frac, 4, 0, res,
-                                              rgb.data_ptr(), stats))
+        if shard_ranges is None:
+            capi.check(lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, diag, frac, 4, 0, res,
+                                                  rgb.data_ptr(), stats))
+            return
+        capi.check(lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, diag, frac, 4, row_b, row_e,
+                                              slab.data_ptr(), stats))
+        torch.distributed.all_gather(gathered, slab)
+        rgb.copy_(sharding.assemble(gathered, shard_ranges))
 
     for _ in range(max(args.warmup, 3)):
         step()
@@ -226,6 +269,8 @@ def run_ours(args):
         dist.all_reduce(nn, op=dist.ReduceOp.SUM)
         t_max, t_xfer_max = tt.tolist()
         agg_nv, agg_nq = nn.tolist()
+        if shard_ranges is not None:  # slabs overlap by the dilation halo: count each texel once
+            agg_nv, agg_nq = float(_n_valid(pair)), float(n_queries_full(name, pair))
 
     # end-to-end through the host-buffer C ABI call (pinned host inputs/outputs)
     e2e = None
@@ -242,9 +287,11 @@ def run_ours(args):
     roofline = None
     if alg_bytes is not None:
         achieved = alg_bytes / (ms_transfer * 1e-3) / 1e9
-        roofline = {"bound": "hbm", "kernel": "k_transfer (closest-point traversal + encode)",
+        traffic, traffic_src = transfer_traffic()
+        roofline = {"bound": "hbm", "kernel": "k_transfer_t (closest-point traversal + encode)",
                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                    "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                    "peak_source": peak_src,
                     "algorithmic_bytes_per_launch": alg_bytes, "ms_per_launch": round(ms_transfer, 4),
                     "per_query": counters}
     cpu = None
@@ -252,12 +299,15 @@ def run_ours(args):
         cpu = cpu_baseline(pair, name)
     clocks = clk.summary()
     line = {
-        "metric": METRIC, "value": agg_nv / (t_max * 1e-3), "unit": UNIT, "n_gpus": world,
+        "metric": METRICS.get(name, METRIC), "value": agg_nv / (t_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_max,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if shard_ranges else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (deterministic geodesic blob pair, Appendix B of SURVEY.md)",
-        "config": {"workload": workload_desc(name, pair), "global_batch": world, "seq_len": None,
-                   "parallelism": f"assets x{world} (one asset per GPU, no collective)",
+        "config": {"workload": workload_desc(name, pair), "global_batch": 1 if shard_ranges else world,
+                   "seq_len": None,
+                   "parallelism": (f"rows x{world} (one atlas, valid-balanced row slabs, NCCL all-gather)"
+                                   if shard_ranges else f"assets x{world} (one asset per GPU, no collective)"),
                    "l2": "flushed between timed steps (256 MiB write, outside the per-step events)",
                    "seed": fx.CONFIGS[name]["seed"]},
         "rays_per_s": agg_nq / (t_xfer_max * 1e-3),
@@ -367,6 +417,14 @@ def cpu_baseline(pair, name):
 _NV_CACHE = {}
 
 
+def n_queries_full(name, pair):
+    try:
+        with open(CONSTANTS) as f:
+            return int(json.load(f)[name]["n_queries"])
+    except (OSError, KeyError):
+        return _n_valid(pair)
+
+
 def _n_valid(pair):
     key = id(pair)
     if key not in _NV_CACHE:
@@ -400,7 +458,7 @@ def run_reference(args):
     t = statistics.mean(ts)
     value = n_valid / t
     return {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRICS.get(name, METRIC), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (same pair as --impl ours)",
         "config": {"workload": workload_desc(name, pair), "global_batch": 1, "seq_len": None,
