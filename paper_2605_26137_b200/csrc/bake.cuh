@@ -55,6 +55,17 @@ struct Ctx {
   void* host_buf(const std::string& name, size_t bytes);
   void* cub_temp(size_t bytes, bool side_stream = false);
   void count_launch(int n = 1) { launches += n; }
+
+  // Every scratch (re)allocation bumps the generation: a captured CUDA graph
+  // is replayed only while the buffers it references are unchanged.
+  uint64_t alloc_gen = 0;
+  // Persistent timing events (graph-capturable: never destroyed mid-flight).
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t pool_event(int i);
+  // Captured fused bake (see capi.cu bake_dev).
+  cudaGraphExec_t bake_exec = nullptr;
+  std::vector<char> bake_key, bake_prev_key;
+  uint64_t bake_gen = 0, bake_prev_gen = ~0ull;
   ~Ctx();
 };
 
@@ -176,7 +187,10 @@ void wedge_frames(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames_ou
 // Measured on config B (r01 profiles): the quad split lowers per-warp
 // coherence more than the seeded bound saves, so it is off; every query is
 // in pass A and pass B is empty.
-constexpr bool kSeedPasses = false;
+#ifndef MFB_SEED_PASSES
+#define MFB_SEED_PASSES 0
+#endif
+constexpr bool kSeedPasses = MFB_SEED_PASSES != 0;
 
 struct QueryList {
   float4* qpos = nullptr;  // x, y, z (the G-buffer's f32 position), w = slab texel index (int bits)

@@ -41,6 +41,7 @@ void* Ctx::buf(const std::string& name, size_t bytes) {
       b.ptr = nullptr;
     }
     const size_t want = std::max(bytes, b.bytes + b.bytes / 4);
+    ++alloc_gen;
     cudaError_t e = cudaMalloc(&b.ptr, want);
     if (e == cudaErrorMemoryAllocation) {
       (void)cudaGetLastError();
@@ -58,6 +59,7 @@ void* Ctx::host_buf(const std::string& name, size_t bytes) {
       MFB_CUDA_TRY(cudaStreamSynchronize(stream));
       MFB_CUDA_TRY(cudaFreeHost(b.ptr));
     }
+    ++alloc_gen;
     MFB_CUDA_TRY(cudaMallocHost(&b.ptr, bytes));
     b.bytes = bytes;
   }
@@ -73,13 +75,25 @@ void* Ctx::cub_temp(size_t bytes, bool side_stream) {
       MFB_CUDA_TRY(cudaFree(p));
     }
     const size_t want = std::max<size_t>(bytes, 1 << 20);
+    ++alloc_gen;
     MFB_CUDA_TRY(cudaMalloc(&p, want));
     n = want;
   }
   return p;
 }
+cudaEvent_t Ctx::pool_event(int i) {
+  while (static_cast<int>(ev_pool.size()) <= i) {
+    cudaEvent_t e;
+    MFB_CUDA_TRY(cudaEventCreate(&e));
+    ev_pool.push_back(e);
+  }
+  return ev_pool[i];
+}
+
 Ctx::~Ctx() {
   cudaSetDevice(device);
+  if (bake_exec) cudaGraphExecDestroy(bake_exec);
+  for (auto e : ev_pool) cudaEventDestroy(e);
   if (stream) cudaStreamSynchronize(stream);
   if (side) cudaStreamSynchronize(side);
   for (auto& kv : scratch) cudaFree(kv.second.ptr);
@@ -293,26 +307,26 @@ void check_transfer_cfg(double diag, double frac) {
     throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: distance filter must be positive");
 }
 
+// Stage timing on the context's persistent event pool: mark k records pool
+// event base + k (so the marks survive inside a captured graph).
 struct Timer {
   Ctx& c;
-  std::vector<cudaEvent_t> ev;
-  explicit Timer(Ctx& cc) : c(cc) {}
+  int next;
+  explicit Timer(Ctx& cc, int base = 0) : c(cc), next(base) {}
   cudaEvent_t mark(cudaStream_t s) {
     if (!c.timing) return nullptr;
-    cudaEvent_t e;
-    MFB_CUDA_TRY(cudaEventCreate(&e));
+    cudaEvent_t e = c.pool_event(next++);
     MFB_CUDA_TRY(cudaEventRecord(e, s));
-    ev.push_back(e);
     return e;
   }
   static float ms(cudaEvent_t a, cudaEvent_t b) {
     if (!a || !b) return 0.f;
     float v = 0.f;
-    cudaEventElapsedTime(&v, a, b);
+    if (cudaEventElapsedTime(&v, a, b) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return 0.f;
+    }
     return v;
-  }
-  ~Timer() {
-    for (auto e : ev) cudaEventDestroy(e);
   }
 };
 
@@ -340,15 +354,16 @@ QueryList query_list(Ctx& c, int64_t capacity) {
   return q;
 }
 
-// The fused bake over validated device meshes; rows [rb, re) into rgb_out (device).
-void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
-              int rb, int re, uint8_t* rgb_out, int32_t* dbg_face, double* dbg_ts, mf_bake_stats* st,
-              Timer& tm, cudaEvent_t t_begin) {
-  check_lowpoly(lo, res);
-  check_mesh(hi);
-  check_transfer_cfg(diag, frac);
-  if (radius < 0) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilation radius must be >= 0");
-  if (rb < 0 || re > res || rb >= re) throw ApiError(MF_ERR_BAD_ARGUMENT, "row range outside the atlas");
+// Everything the fused bake enqueues; no host synchronisation inside, so
+// the same sequence can be captured into a CUDA graph.
+struct BakeMarks {
+  cudaEvent_t side0 = nullptr, side1 = nullptr, e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr,
+              e4 = nullptr, e5 = nullptr;
+};
+
+void enqueue_bake(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
+                  int rb, int re, uint8_t* rgb_out, bool debug, Timer& tm, BakeMarks& mk, int* hflags_pinned,
+                  unsigned long long* hcnt_pinned) {
   cudaStream_t s = c.stream, side = c.side;
   const int r = radius;
   const int s0 = std::max(0, rb - r), s1 = std::min(res, re + r);  // raster/transfer slab with dilation halo
@@ -364,71 +379,152 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
   fo.rgb = c.buf<uint8_t>("bake.raw", 3 * g.texels());
   fo.q = query_list(c, g.texels());
   fo.valid_count = counters + 2;
-  if (dbg_face || dbg_ts) {
+  if (debug) {
     fo.dbg_face = c.buf<int32_t>("bake.dface", g.texels());
     fo.dbg_ts = c.buf<double>("bake.dts", 3 * g.texels());
   }
+  MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
+
+  // fork: dense-mesh work on the side stream
+  MFB_CUDA_TRY(cudaEventRecord(c.fork, s));
+  MFB_CUDA_TRY(cudaStreamWaitEvent(side, c.fork, 0));
+  mk.side0 = tm.mark(side);
+  double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
+  vertex_normals(c, side, hi->m, hiN, true, "hi");
+  Lbvh bvh;
+  lbvh_build(c, side, hi->m, bvh, "hi.bvh");
+  mk.side1 = tm.mark(side);
+  MFB_CUDA_TRY(cudaEventRecord(c.join, side));
+
+  // main: lowpoly prep + raster (fused: valid mask, raw map, query list)
+  mk.e0 = tm.mark(s);
+  RasterPlan plan;
+  prepare_lowpoly(c, s, lo->m, res, plan);
+  mk.e1 = tm.mark(s);
+  raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
+  mk.e2 = tm.mark(s);
+
+  // join, transfer, dilate
+  MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
+  mk.e3 = tm.mark(s);
+  TransferArgs ta;
+  ta.q = fo.q;
+  ta.res = res;
+  ta.slab_row0 = s0;
+  ta.face_map = c.buf<int>("bake.facemap", g.texels());
+  ta.face_map_size = g.texels();
+  ta.hi_positions = hi->m.pos;
+  ta.hi_normals = hiN;
+  ta.hi_faces = hi->m.faces;
+  ta.max_dist = frac * diag;
+  ta.rgb = fo.rgb;
+  ta.dbg_face = fo.dbg_face;
+  ta.dbg_ts = fo.dbg_ts;
+  ta.counters = counters;
+  transfer_normals(c, s, bvh, ta);
+  mk.e4 = tm.mark(s);
+  dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, r, rgb_out, rb, re - rb);
+  mk.e5 = tm.mark(s);
+  MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  MFB_CUDA_TRY(cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+}
+
+// The fused bake over validated device meshes; rows [rb, re) into rgb_out
+// (device). The first call with a given shape runs eagerly (allocating
+// scratch), the second identical call captures the whole two-stream sequence
+// into a CUDA graph, later ones replay it (MFB_GRAPH=0 disables). Debug
+// outputs always run eagerly.
+void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
+              int rb, int re, uint8_t* rgb_out, int32_t* dbg_face, double* dbg_ts, mf_bake_stats* st,
+              Timer& tm, cudaEvent_t t_begin) {
+  check_lowpoly(lo, res);
+  check_mesh(hi);
+  check_transfer_cfg(diag, frac);
+  if (radius < 0) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilation radius must be >= 0");
+  if (rb < 0 || re > res || rb >= re) throw ApiError(MF_ERR_BAD_ARGUMENT, "row range outside the atlas");
+  cudaStream_t s = c.stream;
+  // debug outputs and stage timing always run eagerly (events inside a graph
+  // are not meaningful)
+  const bool debug = dbg_face || dbg_ts || c.timing;
+  static const bool graphs = [] {
+    const char* e = std::getenv("MFB_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  int* hflags = static_cast<int*>(c.host_buf("bake.hflags", 4 * sizeof(int)));
+  auto* hcnt = static_cast<unsigned long long*>(c.host_buf("bake.hcnt", 4 * sizeof(unsigned long long)));
+  // graph key: everything baked into the captured sequence
+  struct Key {
+    const void *lo, *hi, *out, *lo_mem, *hi_mem;
+    int lo_nf, lo_nv, lo_nu, hi_nf, hi_nv, res, radius, rb, re, timing;
+    double diag, frac;
+  } key{lo, hi, rgb_out, lo->mem, hi->mem, lo->m.nf, lo->m.nv, lo->m.nu, hi->m.nf, hi->m.nv, res, radius, rb, re,
+        c.timing ? 1 : 0, diag, frac};
+  std::vector<char> kb(reinterpret_cast<const char*>(&key), reinterpret_cast<const char*>(&key) + sizeof(key));
+  const int s0 = std::max(0, rb - radius);
   for (int attempt = 0;; ++attempt) {
     HostTrace ht("bake_dev");
-    MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
-    MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
-
-    // fork: dense-mesh work on the side stream
-    MFB_CUDA_TRY(cudaEventRecord(c.fork, s));
-    MFB_CUDA_TRY(cudaStreamWaitEvent(side, c.fork, 0));
-    cudaEvent_t e_side0 = tm.mark(side);
-    double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
-    vertex_normals(c, side, hi->m, hiN, true, "hi");
-    Lbvh bvh;
-    lbvh_build(c, side, hi->m, bvh, "hi.bvh");
-    cudaEvent_t e_side1 = tm.mark(side);
-    MFB_CUDA_TRY(cudaEventRecord(c.join, side));
-
-    // main: lowpoly prep + raster (fused: valid mask, raw map, query list)
-    cudaEvent_t e0 = tm.mark(s);
-    RasterPlan plan;
-    prepare_lowpoly(c, s, lo->m, res, plan);
-    cudaEvent_t e1 = tm.mark(s);
-    raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
-    cudaEvent_t e2 = tm.mark(s);
-
-    // join, transfer, dilate
-    MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
-    cudaEvent_t e3 = tm.mark(s);
-    TransferArgs ta;
-    ta.q = fo.q;
-    ta.res = res;
-    ta.slab_row0 = s0;
-    ta.face_map = c.buf<int>("bake.facemap", g.texels());
-    ta.face_map_size = g.texels();
-    ta.hi_positions = hi->m.pos;
-    ta.hi_normals = hiN;
-    ta.hi_faces = hi->m.faces;
-    ta.max_dist = frac * diag;
-    ta.rgb = fo.rgb;
-    ta.dbg_face = fo.dbg_face;
-    ta.dbg_ts = fo.dbg_ts;
-    ta.counters = counters;
-    transfer_normals(c, s, bvh, ta);
-    cudaEvent_t e4 = tm.mark(s);
-    dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, r, rgb_out, rb, re - rb);
-    cudaEvent_t e5 = tm.mark(s);
-
-    if (dbg_face)
-      MFB_CUDA_TRY(cudaMemcpyAsync(dbg_face, fo.dbg_face + static_cast<int64_t>(rb - s0) * res,
-                                   sizeof(int32_t) * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
-    if (dbg_ts)
-      MFB_CUDA_TRY(cudaMemcpyAsync(dbg_ts, fo.dbg_ts + 3 * static_cast<int64_t>(rb - s0) * res,
-                                   sizeof(double) * 3 * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
-    int hflags[4] = {0, 0, 0, 0};
-    unsigned long long hcnt[4] = {0, 0, 0, 0};
+    BakeMarks mk;
+    Timer t2(c, tm.next);
+    if (graphs && !debug && c.bake_exec && kb == c.bake_key && c.alloc_gen == c.bake_gen) {
+      MFB_CUDA_TRY(cudaGraphLaunch(c.bake_exec, s));
+      // the graph recorded its marks on pool events tm.next .. tm.next + 7 in this order
+      if (c.timing) {
+        int i = tm.next;
+        mk.side0 = c.pool_event(i++);
+        mk.side1 = c.pool_event(i++);
+        mk.e0 = c.pool_event(i++);
+        mk.e1 = c.pool_event(i++);
+        mk.e2 = c.pool_event(i++);
+        mk.e3 = c.pool_event(i++);
+        mk.e4 = c.pool_event(i++);
+        mk.e5 = c.pool_event(i++);
+      }
+    } else if (graphs && !debug && kb == c.bake_prev_key && c.alloc_gen == c.bake_prev_gen) {
+      // same shape as the previous eager run: every buffer exists -> capture
+      cudaGraph_t graph = nullptr;
+      MFB_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      try {
+        enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, false, t2, mk, hflags, hcnt);
+      } catch (...) {
+        cudaStreamEndCapture(s, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      MFB_CUDA_TRY(cudaStreamEndCapture(s, &graph));
+      if (c.alloc_gen != c.bake_prev_gen) {  // something allocated during capture: do not keep it
+        cudaGraphDestroy(graph);
+        c.bake_prev_gen = c.alloc_gen;
+        enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, false, t2, mk, hflags, hcnt);
+      } else {
+        if (c.bake_exec) cudaGraphExecDestroy(c.bake_exec);
+        c.bake_exec = nullptr;
+        MFB_CUDA_TRY(cudaGraphInstantiate(&c.bake_exec, graph, 0));
+        cudaGraphDestroy(graph);
+        c.bake_key = kb;
+        c.bake_gen = c.alloc_gen;
+        MFB_CUDA_TRY(cudaGraphLaunch(c.bake_exec, s));
+        }
+    } else {
+      enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, dbg_face || dbg_ts, t2, mk, hflags, hcnt);
+      c.bake_prev_key = kb;
+      c.bake_prev_gen = c.alloc_gen;
+    }
     ht.mark("enqueued");
-    MFB_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, s));
-    MFB_CUDA_TRY(cudaMemcpyAsync(hcnt, counters, sizeof(hcnt), cudaMemcpyDeviceToHost, s));
+    if (dbg_face || dbg_ts) {
+      if (dbg_face)
+        MFB_CUDA_TRY(cudaMemcpyAsync(dbg_face, c.buf<int32_t>("bake.dface", 1) + static_cast<int64_t>(rb - s0) * res,
+                                     sizeof(int32_t) * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost, s));
+      if (dbg_ts)
+        MFB_CUDA_TRY(cudaMemcpyAsync(dbg_ts, c.buf<double>("bake.dts", 1) + 3 * static_cast<int64_t>(rb - s0) * res,
+                                     sizeof(double) * 3 * static_cast<int64_t>(re - rb) * res, cudaMemcpyDeviceToHost,
+                                     s));
+    }
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
     ht.mark("synced");
-    if (hflags[1] && attempt == 0) {  // tile bins overflowed: rerun with the exact capacity
+    if (hflags[1] && attempt == 0) {  // tile bins overflowed: rerun eagerly with the exact capacity
       c.bin_capacity = static_cast<int64_t>(hflags[2]) + 1;
+      c.bake_prev_key.clear();
       continue;
     }
     if (hflags[1] || hflags[3]) throw ApiError(MF_ERR_CUDA, "internal capacity overflow");
@@ -437,15 +533,15 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
       st->queries = static_cast<int64_t>(hcnt[0]);
       st->hits = static_cast<int64_t>(hcnt[1]);
       st->valid_texels = static_cast<int64_t>(hcnt[2]);
-      st->bvh_nodes = bvh.n_nodes;
+      st->bvh_nodes = hi->m.nf > 1 ? hi->m.nf - 1 : 0;
       st->bvh_depth = 0;
       if (c.timing) {
-        st->ms_prepare = Timer::ms(e0, e1);
-        st->ms_raster = Timer::ms(e1, e2);
-        st->ms_bvh = Timer::ms(e_side0, e_side1);
-        st->ms_transfer = Timer::ms(e3, e4);
-        st->ms_dilate = Timer::ms(e4, e5);
-        st->ms_total = Timer::ms(t_begin ? t_begin : e0, e5);
+        st->ms_prepare = Timer::ms(mk.e0, mk.e1);
+        st->ms_raster = Timer::ms(mk.e1, mk.e2);
+        st->ms_bvh = Timer::ms(mk.side0, mk.side1);
+        st->ms_transfer = Timer::ms(mk.e3, mk.e4);
+        st->ms_dilate = Timer::ms(mk.e4, mk.e5);
+        st->ms_total = Timer::ms(t_begin ? t_begin : mk.e0, mk.e5);
       }
     }
     return;
@@ -648,7 +744,8 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
   return guarded(ctx, [&]() -> int {
     Ctx& c = ctx->c;
     HostTrace ht("bake_host");
-    Timer tm(c);
+    Timer tm(c, 0);  // host marks use pool events 0..3; bake_dev's start at 8
+    Timer tmb(c, 8);
     cudaEvent_t t0 = tm.mark(c.stream);
     mf_mesh lo, hi;
     lo.ctx = hi.ctx = ctx;
@@ -663,7 +760,7 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
     uint8_t* drgb = c.buf<uint8_t>("bake.rgb", 3 * static_cast<int64_t>(res) * res);
     mf_bake_stats local{};
     bake_dev(c, &lo, &hi, res, bbox_diagonal, max_distance_fraction, radius, 0, res, drgb, dbg_face, dbg_ts,
-             &local, tm, t1);
+             &local, tmb, t1);
     ht.mark("bake_dev");
     cudaEvent_t t2 = tm.mark(c.stream);
     MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, c.stream));
@@ -688,7 +785,7 @@ int mf_bake_normal_map_dev(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int
                            mf_bake_stats* stats) {
   if (!ctx || !lowpoly || !highpoly || !rgb_dev) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
   return guarded(ctx, [&]() -> int {
-    Timer tm(ctx->c);
+    Timer tm(ctx->c, 8);
     mf_bake_stats local{};
     bake_dev(ctx->c, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius, row_begin, row_end,
              rgb_dev, nullptr, nullptr, &local, tm, nullptr);

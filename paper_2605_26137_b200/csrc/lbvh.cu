@@ -373,7 +373,12 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   k_repack<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
   k_refit<<<div_up(n, T), T, 0, s>>>(out.tbox, n, out.nodes, prim_parent, node_parent, flags, out.root_box_dev);
   ctx.count_launch(2);
-  if (out.n_nodes > 0) {
+  // 4-wide collapse only when the wide traversal is selected (MFB_BVH4=1)
+  static const bool wide = [] {
+    const char* e = std::getenv("MFB_BVH4");
+    return e && e[0] == '1';
+  }();
+  if (wide && out.n_nodes > 0) {
     k_collapse4<<<div_up(out.n_nodes, T), T, 0, s>>>(out.nodes, out.n_nodes, out.wnodes);
     ctx.count_launch();
   }

@@ -394,22 +394,39 @@ __device__ __forceinline__ void warp_closest(const BNode* __restrict__ nodes, co
 // holds one, so the expensive exact f64 test executes at high SIMT width.
 // Depth-first nearest-child-first with conservative fp32 pruning (see
 // traverse_closest) - result-neutral vs the reference's best-first heap.
-template <bool kDebug, bool kProf>
+// kPass 0: single pass over all queries. kPass 1/2: the quad-seeded passes
+// (kSeedPasses): pass 1 (one texel per 2x2 quad, list front) records its
+// winning faces in face_map; pass 2 (the other texels, list back) first tests
+// the face its quad corner won - result-neutral, it only tightens the
+// initial bound.
+#ifndef MFB_TRI_BOX
+#define MFB_TRI_BOX 0
+#endif
+#ifndef MFB_TRI_SEL
+#define MFB_TRI_SEL 0  // branchy form measured 2% faster in the per-thread walk
+#endif
+#ifndef MFB_SPEC
+#define MFB_SPEC 0
+#endif
+template <bool kDebug, bool kProf, int kPass = 0>
 __global__ void __launch_bounds__(128) k_transfer_t(
     const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
     const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
     const float* __restrict__ qtbn, const int* __restrict__ qcount, const double* __restrict__ hiN,
     const int32_t* __restrict__ hiF, double max_dist, uint8_t* __restrict__ rgb,
     int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters,
-    unsigned long long* __restrict__ prof_out) {
-  const int nq = qcount[0];
+    unsigned long long* __restrict__ prof_out, int qcap = 0, int res = 0, int slab_row0 = 0,
+    int* __restrict__ face_map = nullptr, const double* __restrict__ hiPos = nullptr,
+    const TBox* __restrict__ tbox = nullptr) {
+  const int nq = qcount[kPass == 2 ? 1 : 0];
   const int lane = threadIdx.x & 31;
   unsigned long long pv[4] = {0, 0, 0, 0};  // internal visits, leaf visits, triangle tests, queries
   const double scene_max = from_ordered_dev(scene_acc[6]);
   const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
   unsigned long long hits = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i - lane < nq; i += gridDim.x * blockDim.x) {
-    const bool live = i < nq;
+  for (int li = blockIdx.x * blockDim.x + threadIdx.x; li - lane < nq; li += gridDim.x * blockDim.x) {
+    const bool live = li < nq;
+    const int i = kPass == 2 ? qcap - 1 - li : li;
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
     if (live) p = __ldg(qpos + i);
     const float3 qf = make_float3(p.x, p.y, p.z);
@@ -419,13 +436,113 @@ __global__ void __launch_bounds__(128) k_transfer_t(
     best.d = init;
     best.face = -1;
     best.bary = mk3(0.0, 0.0, 0.0);
-    float bnd = live ? prune_bound(init, E) : -INFINITY;
+    if (kPass == 2 && live) {
+      const int gi = __float_as_int(p.w);
+      const int x = gi % res, y = gi / res + slab_row0;
+      const int sy = (y & ~1) - slab_row0;
+      if (sy >= 0) {
+        const int sf = face_map[static_cast<int64_t>(sy) * res + (x & ~1)];
+        if (sf >= 0) {  // exact test of the seed face (as if visited first)
+          d3 bary;
+          const d3 pt = closest_point_triangle_sel(q, ld3(hiPos + 3 * hiF[3 * sf]), ld3(hiPos + 3 * hiF[3 * sf + 1]),
+                                                   ld3(hiPos + 3 * hiF[3 * sf + 2]), bary);
+          const double ds = sqnorm(pt - q);
+          if (ds < best.d || (ds == best.d && sf < best.face)) {
+            best.d = ds;
+            best.face = sf;
+            best.bary = bary;
+          }
+        }
+      }
+    }
+    float bnd = live ? prune_bound(best.d, E) : -INFINITY;
     int32_t st_ref[kStackMax];
     float st_lb[kStackMax];
     int sp = 0;
     // ref: node (>= 0), leaf (< 0 and != kDone), or kDone
     constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
     int32_t ref = live ? root : kDone;
+#if MFB_SPEC
+    // Speculative while-while (Aila & Laine 2009): a lane that reaches a leaf
+    // parks it and keeps walking while any lane of the warp still needs
+    // internal nodes; the leaf phase then intersects every parked leaf.
+    const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+    (void)live_mask;
+    int32_t park0 = kDone, park1 = kDone;
+    // all loop conditions are warp-uniform (ballots over every lane)
+    while (__any_sync(0xffffffffu, ref != kDone || park0 != kDone)) {
+      for (;;) {
+        if (ref < 0 && ref != kDone) {  // reached a leaf: park it
+          if (park0 == kDone) park0 = ref;
+          else park1 = ref;
+          ref = kDone;
+          while (sp > 0) {
+            --sp;
+            if (st_lb[sp] <= bnd) {
+              ref = st_ref[sp];
+              break;
+            }
+          }
+        }
+        const bool want = ref >= 0 && park1 == kDone;   // can still walk
+        const bool needy = ref >= 0 && park0 == kDone;  // has no leaf yet
+        if (!__any_sync(0xffffffffu, needy)) break;     // uniform exit
+        if (!want) continue;                            // parked-full lanes idle this step
+        if (kProf) ++pv[0];
+        const float4* np = reinterpret_cast<const float4*>(nodes + ref);
+        const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+        const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
+        const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
+        const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
+        const bool hL = lbL <= bnd, hR = lbR <= bnd;
+        if (hL && hR) {
+          const bool lf = lbL <= lbR;
+          st_ref[sp] = lf ? d.y : d.x;
+          st_lb[sp] = lf ? lbR : lbL;
+          ++sp;
+          ref = lf ? d.x : d.y;
+        } else if (hL || hR) {
+          ref = hL ? d.x : d.y;
+        } else {
+          ref = kDone;
+          while (sp > 0) {
+            --sp;
+            if (st_lb[sp] <= bnd) {
+              ref = st_ref[sp];
+              break;
+            }
+          }
+        }
+      }
+      // ---- leaf phase: every parked leaf
+      for (int slot = 0; slot < 2; ++slot) {
+        const int32_t leaf = slot ? park1 : park0;
+        if (leaf == kDone) continue;
+        int first, count;
+        leaf_decode(leaf, first, count);
+        if (kProf) {
+          ++pv[1];
+          pv[2] += count;
+        }
+        for (int k = 0; k < count; ++k) {
+          d3 A, B, C;
+          int face;
+          load_tri(tris + first + k, A, B, C, face);
+          d3 bary;
+          const d3 pt = closest_point_triangle(q, A, B, C, bary);
+          const double ds = sqnorm(pt - q);
+          if (ds < best.d || (ds == best.d && face < best.face)) {
+            best.d = ds;
+            best.face = face;
+            best.bary = bary;
+            bnd = prune_bound(ds, E);
+          }
+        }
+      }
+      park0 = park1 = kDone;
+      // the node a lane stopped on may now be prunable; it is re-tested on visit
+    }
+#else
     while (ref != kDone) {
       // ---- descend until this lane holds a leaf
       while (ref >= 0) {
@@ -464,11 +581,22 @@ __global__ void __launch_bounds__(128) k_transfer_t(
         pv[2] += count;
       }
       for (int k = 0; k < count; ++k) {
+#if MFB_TRI_BOX
+        {  // conservative per-triangle fp32 box check before the exact f64 test
+          const float4* bp = reinterpret_cast<const float4*>(tbox + first + k);
+          const float4 ba = __ldg(bp), bb = __ldg(bp + 1);
+          if (box_lb(ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, qf, qf) > bnd) continue;
+        }
+#endif
         d3 A, B, C;
         int face;
         load_tri(tris + first + k, A, B, C, face);
         d3 bary;
+#if MFB_TRI_SEL
         const d3 pt = closest_point_triangle_sel(q, A, B, C, bary);
+#else
+        const d3 pt = closest_point_triangle(q, A, B, C, bary);
+#endif
         const double ds = sqnorm(pt - q);
         if (ds < best.d || (ds == best.d && face < best.face)) {
           best.d = ds;
@@ -486,9 +614,11 @@ __global__ void __launch_bounds__(128) k_transfer_t(
         }
       }
     }
+#endif
     if (!live) continue;
     if (kProf) ++pv[3];
     const int texel = __float_as_int(p.w);
+    if (kPass == 1) face_map[texel] = best.face;
     uint8_t px[3] = {128, 128, 255};
     double ts3[3] = {0.0, 0.0, 0.0};
     if (best.face >= 0) {
@@ -1232,7 +1362,7 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     pbuf = ctx.buf<unsigned long long>("xfer.prof", 8);
     MFB_CUDA_TRY(cudaMemsetAsync(pbuf, 0, 8 * sizeof(unsigned long long), s));
   }
-  MFB_CUDA_TRY(cudaMemsetAsync(a.face_map, 0xff, sizeof(int) * a.face_map_size, s));
+  if (kSeedPasses) MFB_CUDA_TRY(cudaMemsetAsync(a.face_map, 0xff, sizeof(int) * a.face_map_size, s));
 #define MFB_XFER(D, P, PASS)                                                                                     \
   k_transfer<D, P, PASS><<<grid, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.tbox, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, \
                                               a.q.count, a.q.capacity, a.res, a.slab_row0, a.face_map,            \
@@ -1320,15 +1450,25 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
       if (bps < 1) bps = 1;
     }
     const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
-#define MFB_XFER_T(D, P)                                                                                    \
-  k_transfer_t<D, P><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, \
-                                        a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb,              \
-                                        D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf)
-    if (prof) {
-      if (dbg) MFB_XFER_T(true, true); else MFB_XFER_T(false, true);
-    } else {
-      if (dbg) MFB_XFER_T(true, false); else MFB_XFER_T(false, false);
+#define MFB_XFER_T(D, P, PASS)                                                                                \
+  k_transfer_t<D, P, PASS><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos,        \
+                                              a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, \
+                                              D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf, \
+                                              a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions,  \
+                                              bvh.tbox)
+#define MFB_XFER_TP(PASS)                                               \
+    if (prof) {                                                          \
+      if (dbg) MFB_XFER_T(true, true, PASS); else MFB_XFER_T(false, true, PASS); \
+    } else {                                                             \
+      if (dbg) MFB_XFER_T(true, false, PASS); else MFB_XFER_T(false, false, PASS); \
     }
+    if (kSeedPasses) {
+      MFB_XFER_TP(1);
+      MFB_XFER_TP(2);
+    } else {
+      MFB_XFER_TP(0);
+    }
+#undef MFB_XFER_TP
 #undef MFB_XFER_T
   } else {
     MFB_XFER_PASS(1);

@@ -425,22 +425,30 @@ __device__ __forceinline__ void tile_texel(int t, int& lx, int& ly) {
 
 // Block-wide compaction of this thread's query flag: returns the query slot
 // (or -1). One atomicAdd per block on the global counter.
-__device__ __forceinline__ int compact_slot(bool is_q, int* counter, int capacity, int* overflow) {
+__device__ __forceinline__ int compact_slot(bool is_q, int* counter, int capacity, int* overflow,
+                                            bool extra = false, unsigned long long* extra_count = nullptr) {
   __shared__ int warp_base[8];
+  __shared__ int warp_extra[8];
   __shared__ int block_base;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned m = __ballot_sync(0xffffffffu, is_q);
-  if (lane == 0) warp_base[w] = __popc(m);
+  const unsigned me = __ballot_sync(0xffffffffu, extra);
+  if (lane == 0) {
+    warp_base[w] = __popc(m);
+    warp_extra[w] = __popc(me);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int acc = 0;
+    int acc = 0, ex = 0;
     for (int k = 0; k < (blockDim.x >> 5); ++k) {
       const int c = warp_base[k];
       warp_base[k] = acc;
       acc += c;
+      ex += warp_extra[k];
     }
     block_base = acc ? atomicAdd(counter, acc) : 0;
     if (acc && block_base + acc > capacity) *overflow = 1;
+    if (extra_count && ex) atomicAdd(extra_count, static_cast<unsigned long long>(ex));
   }
   __syncthreads();
   if (!is_q) return -1;
@@ -474,12 +482,10 @@ __device__ __forceinline__ void emit_fused(int64_t gi, int x, int y, bool in, ui
                                            uint8_t* gvalid, const RasterFused& fo, int* overflow) {
   const bool is_q = in && valid && rel;
   const bool pass_a = kSeedPasses ? ((x | y) & 1) == 0 : true;
-  const int slot_a = compact_slot(is_q && pass_a, fo.q.count, fo.q.capacity, overflow);
+  // one block-level compaction per pass; the valid-texel count rides along
+  const int slot_a = compact_slot(is_q && pass_a, fo.q.count, fo.q.capacity, overflow, in && valid != 0,
+                                  fo.valid_count);
   const int slot_b = kSeedPasses ? compact_slot(is_q && !pass_a, fo.q.count + 1, fo.q.capacity, overflow) : -1;
-  if (fo.valid_count) {
-    const unsigned vm = __ballot_sync(0xffffffffu, in && valid);
-    if ((threadIdx.x & 31) == 0 && vm) atomicAdd(fo.valid_count, static_cast<unsigned long long>(__popc(vm)));
-  }
   if (!in) return;
   if (gvalid) gvalid[gi] = valid;
   if (!is_q) {
