@@ -276,6 +276,94 @@ __global__ void k_refit(const TBox* __restrict__ tbox, int n, BNode* nodes, cons
   }
 }
 
+// Refit from the leaf ranges. Internal nodes whose range holds <= leaf_max
+// primitives are never visited (their parent references them as a leaf
+// range), so the climb starts at the reachable nodes that have leaf-range
+// children: such a node unions its leaf ranges' triangle boxes into its child
+// slots and counts them as arrivals; a node is complete after two arrivals,
+// and the thread that completes it carries its box up to the parent's slot
+// (acquire/release counter per node).
+__global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __restrict__ nodes_in, int n_nodes,
+                               int leaf_max, BNode* nodes, const int32_t* __restrict__ node_parent,
+                               int* __restrict__ flags, float* __restrict__ root_box) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_nodes) return;
+  const int4 d = nodes_in[i].d;
+  if (i != 0 && d.w <= leaf_max) return;       // unreachable: inside a leaf range
+  const int refs[2] = {d.x, d.y};
+  FBox box;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    box.mn[k] = INFINITY;
+    box.mx[k] = -INFINITY;
+  }
+  int leaves = 0;
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    if (refs[side] >= 0) continue;
+    int first, count;
+    leaf_decode(refs[side], first, count);
+    FBox lb;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      lb.mn[k] = INFINITY;
+      lb.mx[k] = -INFINITY;
+    }
+    for (int t = 0; t < count; ++t) {
+      const float4 a = tbox[first + t].a, b = tbox[first + t].b;
+      lb.mn[0] = fminf(lb.mn[0], a.x);
+      lb.mn[1] = fminf(lb.mn[1], a.y);
+      lb.mn[2] = fminf(lb.mn[2], a.z);
+      lb.mx[0] = fmaxf(lb.mx[0], a.w);
+      lb.mx[1] = fmaxf(lb.mx[1], b.x);
+      lb.mx[2] = fmaxf(lb.mx[2], b.y);
+    }
+    store_child_box(&nodes[i], side, lb);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      box.mn[k] = fminf(box.mn[k], lb.mn[k]);
+      box.mx[k] = fmaxf(box.mx[k], lb.mx[k]);
+    }
+    ++leaves;
+  }
+  if (leaves == 0) return;  // both children internal: climbers arrive from below
+  int node = i;
+  if (leaves == 1) {
+    cuda::atomic_ref<int, cuda::thread_scope_device> flag(flags[node]);
+    if (flag.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;  // internal sibling still climbing
+    const int internal_side = refs[0] >= 0 ? 0 : 1;
+    const FBox other = load_child_box_cg(&nodes[node], internal_side);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      box.mn[k] = fminf(box.mn[k], other.mn[k]);
+      box.mx[k] = fmaxf(box.mx[k], other.mx[k]);
+    }
+  }
+  // `node` is complete with `box`: climb
+  for (;;) {
+    if (node == 0) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        root_box[k] = box.mn[k];
+        root_box[3 + k] = box.mx[k];
+      }
+      return;
+    }
+    const int link = node_parent[node];
+    const int par = link >> 1, side = link & 1;
+    store_child_box(&nodes[par], side, box);
+    cuda::atomic_ref<int, cuda::thread_scope_device> flag(flags[par]);
+    if (flag.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;
+    const FBox other = load_child_box_cg(&nodes[par], side ^ 1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      box.mn[k] = fminf(box.mn[k], other.mn[k]);
+      box.mx[k] = fmaxf(box.mx[k], other.mx[k]);
+    }
+    node = par;
+  }
+}
+
 // Collapses the binary tree into 4-wide nodes: wide node i lists binary
 // node i's grandchildren (an internal child contributes its two children, a
 // leaf child itself). Fully parallel over binary nodes; uses the refit boxes.
@@ -360,18 +448,23 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   void* tptr = ctx.cub_temp(tmp, s != ctx.stream);
   MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 30, s));
 
+  // Leaf size: the reference's 4 (bvh.cpp:13) unless MFB_LEAF_MAX (1..7) overrides it.
+  static const int leaf_max = [] {
+    const char* e = std::getenv("MFB_LEAF_MAX");
+    const int v = e ? std::atoi(e) : kLeafMax;
+    return v >= 1 && v <= 7 ? v : kLeafMax;
+  }();
   if (n > 1) {
-    // Leaf size: the reference's 4 (bvh.cpp:13) unless MFB_LEAF_MAX (1..7) overrides it.
-    static int leaf_max = [] {
-      const char* e = std::getenv("MFB_LEAF_MAX");
-      const int v = e ? std::atoi(e) : kLeafMax;
-      return v >= 1 && v <= 7 ? v : kLeafMax;
-    }();
     k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent);
     ctx.count_launch();
   }
   k_repack<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
-  k_refit<<<div_up(n, T), T, 0, s>>>(out.tbox, n, out.nodes, prim_parent, node_parent, flags, out.root_box_dev);
+  if (n > 1) {
+    k_refit_ranges<<<div_up(out.n_nodes, T), T, 0, s>>>(out.tbox, out.nodes, out.n_nodes, leaf_max, out.nodes,
+                                                         node_parent, flags, out.root_box_dev);
+  } else {
+    k_refit<<<1, 32, 0, s>>>(out.tbox, n, out.nodes, prim_parent, node_parent, flags, out.root_box_dev);
+  }
   ctx.count_launch(2);
   // 4-wide collapse only when the wide traversal is selected (MFB_BVH4=1)
   static const bool wide = [] {

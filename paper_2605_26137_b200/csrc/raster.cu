@@ -92,6 +92,51 @@ __global__ void k_vertex_sum(int nv, const int* __restrict__ start, const int* _
   }
   st3(out + 3 * v, n);
 }
+// Same sum for an UNSORTED incident-corner list: lists of up to 16 corners
+// (any regular mesh) are ordered in registers, longer ones in place; the sum
+// then runs in face order exactly as k_vertex_sum.
+__global__ void k_vertex_sum_unsorted(int nv, const int* __restrict__ start, int* __restrict__ list,
+                                      const double* __restrict__ av, double* __restrict__ out, int renorm) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= nv) return;
+  const int b = start[v], e = start[v + 1], k = e - b;
+  d3 n = mk3(0.0, 0.0, 0.0);
+  if (k <= 16) {
+    int c[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) c[i] = i < k ? list[b + i] : 0x7fffffff;
+#pragma unroll
+    for (int i = 1; i < 16; ++i) {  // insertion sort, fully unrolled (register resident)
+#pragma unroll
+      for (int j = i; j > 0; --j) {
+        const int lo = min(c[j - 1], c[j]), hi = max(c[j - 1], c[j]);
+        c[j - 1] = lo;
+        c[j] = hi;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < k) n = n + ld3(av + 3 * (c[i] / 3));
+  } else {
+    for (int i = b + 1; i < e; ++i) {
+      const int key = list[i];
+      int j = i - 1;
+      while (j >= b && list[j] > key) {
+        list[j + 1] = list[j];
+        --j;
+      }
+      list[j + 1] = key;
+    }
+    for (int i = b; i < e; ++i) n = n + ld3(av + 3 * (list[i] / 3));
+  }
+  const double len = norm(n);
+  if (len > 0) n = n / len;
+  if (renorm) {
+    const double l2 = norm(n);
+    if (l2 > 1e-20) n = n / l2;
+  }
+  st3(out + 3 * v, n);
+}
 __global__ void k_renorm(int nv, const double* __restrict__ in, double* __restrict__ out) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
@@ -704,9 +749,23 @@ void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, boo
     }
     return;
   }
-  int *start, *list;
-  corner_csr(ctx, s, m, tag, &start, &list);
-  normals_from_csr(ctx, s, m, start, list, out, renorm, tag);
+  // unsorted CSR + in-register ordering inside the summation kernel
+  const int nc = 3 * m.nf;
+  int* cnt = ctx.buf<int>(tag + ".csr.cnt", m.nv + 1);
+  int* start = ctx.buf<int>(tag + ".csr.start", m.nv + 1);
+  int* cursor = ctx.buf<int>(tag + ".csr.cursor", m.nv + 1);
+  int* list = ctx.buf<int>(tag + ".csr.list", nc);
+  double* av = ctx.buf<double>(tag + ".vn.av", 3 * static_cast<size_t>(m.nf));
+  MFB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (m.nv + 1), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (m.nv + 1), s));
+  k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, cnt, start, m.nv + 1, s));
+  k_corner_fill<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, start, cursor, list);
+  k_face_area_vec<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, av);
+  k_vertex_sum_unsorted<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list, av, out, renorm ? 1 : 0);
+  ctx.count_launch(4);
   MFB_CUDA_TRY(cudaGetLastError());
 }
 
