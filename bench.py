@@ -80,33 +80,61 @@ def workload_desc(name, pair):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled DURING the timed region with NVML
+    (every 2 ms; nvidia-smi's 100 ms floor would miss a ~20 ms region),
+    falling back to `nvidia-smi -lms 100`."""
 
     def __init__(self, index: int):
         self.index = index
+        self.samples = []  # (sm_mhz, max_mhz, reasons bitmask)
+        self.stop = threading.Event()
         self.proc = None
         self.lines = []
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:  # no NVML: nvidia-smi
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                     "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                     "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except OSError:
+                self.proc = None
         return self
+
+    def _poll(self):
+        n = self.nvml
+        while not self.stop.is_set():
+            try:
+                sm = n.nvmlDeviceGetClockInfo(self.h, n.NVML_CLOCK_SM)
+                try:
+                    rs = n.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    rs = n.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.samples.append((float(sm), float(self.max_mhz), int(rs)))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             time.sleep(0.15)
             self.proc.terminate()
@@ -114,27 +142,37 @@ class ClockSampler:
                 self.proc.wait(timeout=2)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        elif getattr(self, "t", None):
+            self.t.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x4: "sw_power_cap"}
+        reasons = set()
+        sm, mx = [], None
+        for v, m, rs in self.samples:
+            sm.append(v)
+            mx = m
+            for bit, nm in names.items():
+                if rs & bit:
+                    reasons.add(nm)
         for ln in self.lines:
             parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 6:
                 continue
             try:
                 sm.append(float(parts[0]))
                 mx = float(parts[1])
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[3:7]):
+            for nm, val in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"],
+                               parts[2:6]):
                 if val.lower().startswith("active"):
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
-        busy = [v for v in sm if mx is None or v > 0.5 * mx] or sm
-        return {"sm_mhz": statistics.median(busy), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def hbm_peak():
@@ -179,7 +217,8 @@ def run_ours(args):
 
     rank, local_rank, world = dist_env()
     torch.cuda.set_device(local_rank)
-    if world > 1:
+    distributed = "RANK" in os.environ  # launched by torchrun (any world size)
+    if distributed:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2605_26137_b200 import capi, fixtures as fx
@@ -200,7 +239,7 @@ def run_ours(args):
 
     row_b, row_e = 0, res
     shard_ranges = None
-    if args.shard and world > 1:
+    if args.shard and distributed:
         # one atlas, rows balanced by valid texels, all-gathered
         import ctypes
         from paper_2605_26137_b200 import sharding
@@ -233,7 +272,7 @@ def run_ours(args):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = ctx.launches
     n_valid = n_queries = hits = 0
-    if world > 1:
+    if distributed:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
@@ -244,7 +283,7 @@ def run_ours(args):
             ends[i].record(stream)
             n_valid, n_queries, hits = st.valid_texels, st.queries, st.hits
         torch.cuda.synchronize()
-    if world > 1:
+    if distributed:
         torch.distributed.barrier()
     launches = ctx.launches - launches0
     if launches == 0:  # graph replays do not pass through the host launch counter
@@ -269,7 +308,7 @@ def run_ours(args):
     agg_nq = n_queries
     t_max = ms_step
     t_xfer_max = ms_transfer
-    if world > 1:
+    if distributed:
         import torch.distributed as dist
         tt = torch.tensor([ms_step, ms_transfer], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -283,10 +322,10 @@ def run_ours(args):
     # end-to-end through the host-buffer C ABI call (pinned host inputs/outputs)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, ctx, pair, world)
+        e2e = run_e2e(args, ctx, pair, world, distributed)
 
     if rank != 0:
-        if world > 1:
+        if distributed:
             torch.distributed.destroy_process_group()
         return None
 
@@ -324,7 +363,7 @@ def run_ours(args):
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks,
     }
-    if world > 1:
+    if distributed:
         torch.distributed.destroy_process_group()
     return line
 
@@ -338,7 +377,7 @@ def launches_per_bake(ctx, step):
     return ctx.launches - before
 
 
-def run_e2e(args, ctx, pair, world):
+def run_e2e(args, ctx, pair, world, distributed=False):
     import ctypes
     import torch
 
@@ -380,7 +419,7 @@ def run_e2e(args, ctx, pair, world):
         times.append(s.elapsed_time(e))
     ms = statistics.mean(times)
     nv = st.valid_texels
-    if world > 1:
+    if distributed:
         import torch.distributed as dist
         tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

@@ -40,6 +40,15 @@ METRICS = {
 }
 
 
+def _kname(n: str) -> str:
+    """Short kernel name: drop `void`, namespaces (ncu prints the anonymous one
+    as `<unnamed>`) and the argument list; keep template arguments."""
+    n = n.replace("(anonymous namespace)", "<unnamed>").replace("void ", "").split("(")[0]
+    if n.startswith(("mfb::", "unnamed>::")):
+        n = n.rsplit("::", 1)[-1]
+    return n
+
+
 def _num(v: str) -> float:
     try:
         return float(v.replace(",", ""))
@@ -59,7 +68,7 @@ def launches(path: str) -> str:
         v = _num(r[vi])
         unit = r[ui]
         us = v / 1000.0 if unit in ("ns", "nsecond") else (v * 1000.0 if unit in ("ms", "msecond") else v)
-        name = r[ki].split("(")[0].replace("void ", "")
+        name = _kname(r[ki])
         agg.setdefault(name, []).append(us)
     ref = [k for k in agg if "k_transfer" in k]
     bakes = len(agg[ref[0]]) if ref else 1
@@ -85,7 +94,7 @@ def full(path: str) -> dict:
     unit_of = dict(zip(header, units))
     for r in rows[2:]:
         d = dict(zip(header, r))
-        res = {"kernel": d.get("Kernel Name", "").split("(")[0]}
+        res = {"kernel": _kname(d.get("Kernel Name", ""))}
         for m, key in METRICS.items():
             if m in d:
                 res[key] = _num(d[m]) * scale.get(unit_of.get(m, ""), 1.0)

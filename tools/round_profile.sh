@@ -1,0 +1,22 @@
+#!/bin/bash
+# Round evidence: parity tests, smoke, bench line, launch list and full ncu
+# captures of the main kernels. Raw artefacts -> gpurun_out/, summaries are
+# produced here afterwards with tools/ncu_summary.py into profiles/.
+set -u
+TAG=${TAG:-r01}
+OUT=gpurun_out
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw,driver_version --format=csv > $OUT/${TAG}_smi.txt
+lscpu | grep -E "Model name|^CPU\(s\)" > $OUT/${TAG}_host.txt
+timeout 900 python -m pytest tests -q -m gpu > $OUT/${TAG}_pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $OUT/${TAG}_pytest_gpu.txt
+tail -2 $OUT/${TAG}_pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/${TAG}_smoke.txt
+timeout 600 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err; echo "bench rc=$?"
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/${TAG}_bench_reference.json 2>> $OUT/${TAG}_bench.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
+  --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
+  > $OUT/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
+timeout 1200 ncu --set full --clock-control none --import-source on \
+  -k 'regex:k_transfer_t|k_raster|k_refit_ranges|k_dilate_fused' -c 4 \
+  -o $OUT/${TAG}_prof -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
+  > $OUT/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
