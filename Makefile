@@ -4,6 +4,7 @@
 #   paper_2605_26137_b200/libmeshforge_b200.so
 #                                           the reference-compatible C++ API
 #                                           (include/meshforge/...) over the C ABI
+#   build/libmfpeaks.so                     L2-read / FP64 microbenchmarks (tools/peaks.cu)
 #   build/test_bake_b200                    C++ KAT tests (tests/cpp) through the
 #                                           C++ API (run on a GPU by tests/test_cpp_api.py)
 #   oracle/...                              see oracle/Makefile
@@ -22,11 +23,12 @@ CU_OBJS := $(patsubst $(PKG)/csrc/%.cu,build/cu/%.o,$(CU_SRCS))
 CU_HDRS := $(wildcard $(PKG)/csrc/*.cuh) include/mfbake.h
 MF_HDRS := $(shell find include/meshforge -name '*.h' 2>/dev/null) include/eigen_shim/Eigen/Core
 
-.PHONY: all lib cpp oracle clean
-all: lib cpp oracle
+.PHONY: all lib cpp peaks oracle clean
+all: lib cpp peaks oracle
 
 lib: $(PKG)/libmfbake.so
 cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200
+peaks: build/libmfpeaks.so
 
 build/cu/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 	@mkdir -p build/cu
@@ -41,6 +43,11 @@ $(PKG)/libmeshforge_b200.so: $(PKG)/cpp/meshforge_b200.cpp $(MF_HDRS) include/mf
 build/test_bake_b200: tests/cpp/test_bake_b200.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+# L2 / FP64 microbenchmarks (tools/peaks.cu) used by bench.py for the roofline peaks
+build/libmfpeaks.so: tools/peaks.cu
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -o $@ $<
 
 oracle:
 	$(MAKE) -C oracle

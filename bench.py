@@ -49,6 +49,8 @@ UNIT = "texels/s"
 CONSTANTS = os.path.join(ROOT, "bench_data", "reference_counters.json")
 TRAFFIC = os.path.join(ROOT, "profiles", "k_transfer_ncu.json")  # one `ncu --set full` capture
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+PEAKS_LIB = os.path.join(ROOT, "build", "libmfpeaks.so")  # tools/peaks.cu
+N_RAYS = 1_000_000  # SURVEY §8(d) secondary metric: raycastFirst on 10^6 random rays
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
 
 
@@ -61,7 +63,11 @@ def parse():
     ap.add_argument("--config", default="B")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rays", action="store_true", help="skip the secondary BVH rays/s metrics")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--assets", type=int, default=1,
+                    help="independent assets baked concurrently per GPU (config D: 8), one context + stream + "
+                         "host thread each")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: row-shard ONE atlas across ranks + NCCL all-gather (strong scaling) "
                          "instead of one asset per rank")
@@ -181,6 +187,111 @@ def hbm_peak():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except (OSError, KeyError, ValueError):
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def live_peaks(device):
+    """L2 read bandwidth and FP64 FMA throughput measured live on this box
+    (tools/peaks.cu; MEASURED_PEAKS.json has only HBM and bf16)."""
+    import ctypes
+    try:
+        lib = ctypes.CDLL(PEAKS_LIB)
+    except OSError as e:
+        return {"error": f"{PEAKS_LIB}: {e}"}
+    lib.mfp_l2_read_gbs.argtypes = [ctypes.c_int, ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    lib.mfp_fp64_tflops.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    out = {"source": "live, tools/peaks.cu: 64 MiB L2-resident buffer streamed with ld.global.cg by 4 CTAs/SM "
+                     "(best of 5); 8 independent DFMA chains per thread, 8 CTAs/SM (best of 5)"}
+    v = ctypes.c_double()
+    if lib.mfp_l2_read_gbs(device, 64 << 20, 20, ctypes.byref(v)) == 0:
+        out["l2_read_gbs"] = round(v.value, 1)
+    if lib.mfp_fp64_tflops(device, ctypes.byref(v)) == 0:
+        out["fp64_tflops"] = round(v.value, 2)
+    return out
+
+
+def stage_rooflines(pair, stage, n_queries, counters, hbm, peaks):
+    """SURVEY §8(d) per-stage roofline fractions: streaming stages against HBM,
+    the traversal against the measured L2 read bandwidth and the FP64 pipe.
+    Times are the eager per-stage CUDA-event times (all kernels of the stage)."""
+    res = pair.res
+    f, v = pair.dense.face_count(), pair.dense.vertex_count()
+
+    def row(bytes_, ms, peak, unit="GB/s", scale=1e9, note=""):
+        if not ms or not peak:
+            return None
+        a = bytes_ / (ms * 1e-3) / scale
+        r = {"algorithmic": bytes_, "ms": round(ms, 4), "achieved": round(a, 1), "peak": peak, "unit": unit,
+             "frac": round(a / peak, 4)}
+        if note:
+            r["note"] = note
+        return r
+
+    out = {
+        "raster": row(50 * res * res, stage["ms_raster"], hbm,
+                      note="50 B x res^2 (G-buffer as the API output); fused path writes only query records"),
+        "lbvh": row(148 * f + 24 * v, stage["ms_bvh"], hbm,
+                    note="148 F + 24 V; stage also builds the dense vertex normals, side stream, overlapped"),
+        "dilate": row(7 * res * res, stage["ms_dilate"], hbm, note="7 B x res^2"),
+    }
+    if counters:
+        out["transfer_l2"] = row(counters["bytes_per_query"] * n_queries, stage["ms_transfer"],
+                                 peaks.get("l2_read_gbs"), note="W_q x N_q against the measured L2 read bandwidth")
+        flops = (22 * counters["n_node"] + 80 * counters["n_tri"]) * n_queries
+        out["transfer_fp64"] = row(flops, stage["ms_transfer"], peaks.get("fp64_tflops"), unit="TFLOP/s",
+                                   scale=1e12, note="(22 N_node + 80 N_tri) x N_q")
+    return out
+
+
+def bvh_rays(ctx, hi, pair, steps):
+    """Secondary metrics (SURVEY §8d): Bvh::raycastFirst over 10^6 random rays
+    (origins uniform in the dense mesh's box, directions uniform on the sphere)
+    and closestPointWithin over 10^6 random points at the bake's search radius,
+    both against the dense LBVH, device-resident inputs, CUDA events."""
+    import ctypes
+    import torch
+
+    from paper_2605_26137_b200 import capi
+    lib = ctx.lib
+    h = ctypes.c_void_p()
+    capi.check(lib.mf_bvh_build(ctx.h, hi.h, ctypes.byref(h)))
+    g = torch.Generator(device="cuda").manual_seed(11)
+    lo_b = torch.tensor(pair.dense.positions.min(0), device="cuda")
+    hi_b = torch.tensor(pair.dense.positions.max(0), device="cuda")
+    o = lo_b + (hi_b - lo_b) * torch.rand((N_RAYS, 3), generator=g, device="cuda", dtype=torch.float64)
+    d = torch.randn((N_RAYS, 3), generator=g, device="cuda", dtype=torch.float64)
+    d /= d.norm(dim=1, keepdim=True)
+    face = torch.empty(N_RAYS, dtype=torch.int32, device="cuda")
+    t, u, w = (torch.empty(N_RAYS, dtype=torch.float64, device="cuda") for _ in range(3))
+    pt = torch.empty((N_RAYS, 3), dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(3, min(steps, 10))):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    ms_ray = timed(lambda: capi.check(lib.mf_bvh_raycast_first_dev(
+        h, o.data_ptr(), d.data_ptr(), N_RAYS, 0.0, float("inf"), face.data_ptr(), t.data_ptr(), u.data_ptr(),
+        w.data_ptr())))
+    ray_hits = int((face >= 0).sum())
+    max_d = pair.max_distance_fraction * pair.bbox_diagonal
+    ms_cp = timed(lambda: capi.check(lib.mf_bvh_closest_within_dev(
+        h, o.data_ptr(), N_RAYS, max_d, face.data_ptr(), t.data_ptr(), pt.data_ptr(), None)))
+    cp_hits = int((face >= 0).sum())
+    lib.mf_bvh_destroy(h)
+    return {"raycast_rays_per_s": N_RAYS / (ms_ray * 1e-3), "raycast_ms": round(ms_ray, 4), "raycast_hits": ray_hits,
+            "closest_within_per_s": N_RAYS / (ms_cp * 1e-3), "closest_within_ms": round(ms_cp, 4),
+            "closest_within_hits": cp_hits, "n": N_RAYS,
+            "inputs": "uniform origins in the dense bbox, uniform unit directions (seed 11); "
+                      "closest-point radius = maxDistFrac x diag"}
 
 
 def transfer_traffic():
@@ -319,6 +430,10 @@ def run_ours(args):
         if shard_ranges is not None:  # slabs overlap by the dilation halo: count each texel once
             agg_nv, agg_nq = float(_n_valid(pair)), float(n_queries_full(name, pair))
 
+    # secondary BVH metrics and the live L2 / FP64 peaks (rank 0)
+    rays = bvh_rays(ctx, hi, pair, args.steps) if rank == 0 and not args.no_rays else None
+    peaks = live_peaks(local_rank) if rank == 0 else {}
+
     # end-to-end through the host-buffer C ABI call (pinned host inputs/outputs)
     e2e = None
     if not args.no_e2e:
@@ -331,14 +446,21 @@ def run_ours(args):
 
     peak, peak_src = hbm_peak()
     alg_bytes, counters = transfer_algorithmic_bytes(name, n_queries, n_valid, res)
+    stage_mean = {k: statistics.mean(v) for k, v in stage.items()}
+    stages_rl = stage_rooflines(pair, stage_mean, n_queries, counters, peak, peaks)
     roofline = None
     if alg_bytes is not None:
+        # the traversal's node/triangle bytes are served from L2
+        # (its DRAM traffic, `traffic`, is ~5% of them), so its roofline is the
+        # measured L2 read bandwidth; the HBM-relative figure is kept beside it.
         achieved = alg_bytes / (ms_transfer * 1e-3) / 1e9
         traffic, traffic_src = transfer_traffic()
-        roofline = {"bound": "hbm", "kernel": "k_transfer_t (closest-point traversal + encode)",
-                    "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                    "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
-                    "peak_source": peak_src,
+        l2 = peaks.get("l2_read_gbs")
+        roofline = {"bound": "l2" if l2 else "hbm", "kernel": "k_transfer_t (closest-point traversal + encode)",
+                    "achieved": round(achieved, 1), "peak": l2 or peak, "unit": "GB/s",
+                    "frac": round(achieved / (l2 or peak), 4), "traffic": traffic, "traffic_source": traffic_src,
+                    "peak_source": ("measured live: L2 read bandwidth, tools/peaks.cu" if l2 else peak_src),
+                    "hbm_peak": peak, "hbm_peak_source": peak_src, "frac_of_hbm": round(achieved / peak, 4),
                     "algorithmic_bytes_per_launch": alg_bytes, "ms_per_launch": round(ms_transfer, 4),
                     "per_query": counters}
     cpu = None
@@ -360,8 +482,107 @@ def run_ours(args):
         "rays_per_s": agg_nq / (t_xfer_max * 1e-3),
         "n_valid_texels": n_valid, "n_queries": n_queries, "hits": hits,
         "stage_ms": {k: round(statistics.mean(v), 4) for k, v in stage.items()},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "roofline": roofline, "stage_rooflines": stages_rl, "peaks": peaks, "bvh": rays,
+        "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks,
+    }
+    if distributed:
+        torch.distributed.destroy_process_group()
+    return line
+
+
+def run_batch(args):
+    """K independent assets per GPU, each on its own
+    context (own stream + side stream, own captured graph), driven by K host
+    threads (ctypes drops the GIL in the call). One step = all K bakes;
+    value = sum of valid texels over all assets of all ranks / max-rank time.
+    Device time: one event on the launch stream that every asset stream waits
+    on, and one after the launch stream joins every asset stream."""
+    import concurrent.futures as cf
+
+    import torch
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    distributed = "RANK" in os.environ
+    if distributed:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2605_26137_b200 import capi, fixtures as fx
+
+    name, k = args.config, args.assets
+    base = fx.CONFIGS[name]["seed"] + rank * k
+    pairs = [fx.config_pair(name, seed=base + i) for i in range(k)]
+    streams = [torch.cuda.Stream() for _ in range(k)]
+    ctxs = [capi.Context(local_rank, st.cuda_stream) for st in streams]
+    meshes = [(capi.DeviceMesh(c, p.lowpoly), capi.DeviceMesh(c, p.dense)) for c, p in zip(ctxs, pairs)]
+    outs = [torch.empty((p.res, p.res, 3), dtype=torch.uint8, device="cuda") for p in pairs]
+    stats = [capi.MfBakeStats() for _ in range(k)]
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+    main = torch.cuda.current_stream()
+    pool = cf.ThreadPoolExecutor(max_workers=k)
+
+    def one(i):
+        c, (lo, hi), p = ctxs[i], meshes[i], pairs[i]
+        capi.check(c.lib.mf_bake_normal_map_dev(c.h, lo.h, hi.h, p.res, p.bbox_diagonal, p.max_distance_fraction,
+                                                4, 0, p.res, outs[i].data_ptr(), stats[i]))
+
+    def batch():
+        ev = torch.cuda.Event()
+        ev.record(main)
+        for st in streams:
+            st.wait_event(ev)
+        list(pool.map(one, range(k)))
+        for st in streams:
+            main.wait_stream(st)
+
+    for _ in range(max(args.warmup, 3)):
+        batch()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if distributed:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    launches0 = sum(c.launches for c in ctxs)
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record(main)
+            batch()
+            ends[i].record(main)
+        torch.cuda.synchronize()
+    if distributed:
+        torch.distributed.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / args.steps
+    nv = sum(s.valid_texels for s in stats)
+    launches = sum(c.launches for c in ctxs) - launches0
+    if launches == 0:
+        launches = args.steps * k * launches_per_bake(ctxs[0], lambda: one(0))
+    if distributed:
+        import torch.distributed as dist
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        nn = torch.tensor([nv], dtype=torch.float64, device="cuda")
+        dist.all_reduce(nn, op=dist.ReduceOp.SUM)
+        ms, nv = tt.item(), nn.item()
+    pool.shutdown()
+    if rank != 0:
+        if distributed:
+            torch.distributed.destroy_process_group()
+        return None
+    line = {
+        "metric": METRICS.get(name, METRIC), "value": nv / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (deterministic geodesic blob pairs, one seed per asset)",
+        "config": {"workload": workload_desc(name, pairs[0]) + f"; {k} assets per GPU (seeds {base}..{base + k - 1} "
+                                                               f"on rank {rank})",
+                   "global_batch": k * world, "seq_len": None,
+                   "parallelism": f"assets x{k * world} ({k} per GPU on {k} streams, no collective)",
+                   "l2": "flushed between timed steps (256 MiB write, outside the per-step events)"},
+        "assets_per_gpu": k, "ms_per_asset": ms / k,
+        "gpu_launches": launches, "clocks": clk.summary(),
     }
     if distributed:
         torch.distributed.destroy_process_group()
@@ -440,10 +661,11 @@ def _reference_lib():
     return bindings.port(), "port"
 
 
-def cpu_reference_bake(pair):
+def cpu_reference_bake(pair, time_bvh=False):
     lib, kind = _reference_lib()
     t0 = time.perf_counter()
-    r = lib.bake(pair.lowpoly, pair.dense, pair.res, pair.bbox_diagonal, pair.max_distance_fraction, 4)
+    r = lib.bake(pair.lowpoly, pair.dense, pair.res, pair.bbox_diagonal, pair.max_distance_fraction, 4,
+                 time_bvh=time_bvh)
     wall = time.perf_counter() - t0
     return r, wall, kind, r.get("n_valid")
 
@@ -455,17 +677,27 @@ def cores():
     return os.cpu_count() or 1
 
 
-def cpu_baseline(pair, name):
+def cpu_baseline(pair, name, runs=5):
     """The reference's CPU bake (rasterizeGBuffer + transferNormals + dilateSeams,
-    as test_bake.cpp:205-206 composes it) on the box's host cores: one full
-    config bake is the bounded sample (~5-20 s)."""
-    r, wall, kind, _ = cpu_reference_bake(pair)
-    times = r.get("times") or {}
-    t = times.get("total", wall) or wall
+    as test_bake.cpp:205-206 composes it) on the box's host cores, median of
+    `runs` full bakes (~8 s at B), with a standalone Bvh(hi) build
+    timed beside it (not part of the total: transferNormals builds its own)."""
+    runs_t = []
+    for i in range(runs):
+        r, wall, kind, _ = cpu_reference_bake(pair, time_bvh=(i == 0))
+        times = r.get("times") or {}
+        if i == 0:
+            bvh_s = times.get("bvh", 0.0)
+        runs_t.append((times.get("total", wall) or wall, times))
+    runs_t.sort(key=lambda x: x[0])
+    t, times = runs_t[len(runs_t) // 2]
+    times = dict(times, bvh=bvh_s)
     n_valid = _n_valid(pair)
     return {"value": n_valid / t, "unit": UNIT, "cores": cores(), "kind": kind,
-            "sample": f"one full {name} bake (raster + transfer incl. its BVH build + dilate r=4), "
-                      f"{t:.2f} s; stages s: " + ", ".join(f"{k} {v:.3f}" for k, v in times.items()),
+            "sample": f"median of {runs} full {name} bakes (raster + transfer incl. its normals and BVH build + "
+                      f"dilate r=4), {t:.3f} s; median run's stages s: "
+                      + ", ".join(f"{k} {v:.3f}" for k, v in times.items() if k != "bvh")
+                      + f"; standalone Bvh(hi) build {bvh_s:.3f} s (outside the total)",
             "threads_note": "std::thread::hardware_concurrency() threads in the transfer loop only, "
                             "raster/BVH/dilate single-threaded, exactly as shipped (core/parallel.h)"}
 
@@ -528,7 +760,12 @@ def run_reference(args):
 
 def main():
     args = parse()
-    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if args.impl == "reference":
+        line = run_reference(args)
+    elif args.assets > 1:
+        line = run_batch(args)
+    else:
+        line = run_ours(args)
     if line is not None:
         s = json.dumps(line)
         print(s, flush=True)

@@ -13,6 +13,7 @@
 // a (64+2r) x (16+2r) halo region (one launch, ~1.7x halo read of the 1-byte
 // mask at r = 4); k_dilate_pass is the multi-launch global fallback for radii
 // whose halo does not fit in shared memory.
+#include <atomic>
 #include "bake.cuh"
 
 namespace mfb {
@@ -212,11 +213,14 @@ void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
   }
   const size_t smem = static_cast<size_t>(4) * (kTW + 2 * radius) * (kTH + 2 * radius) * sizeof(int16_t);
   if (radius <= 64 && smem <= 200 * 1024) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    // the attribute is per device: one bit per device, set once each
+    static std::atomic<unsigned long long> attr_set{0};
+    int dev = 0;
+    MFB_CUDA_TRY(cudaGetDevice(&dev));
+    if (!((attr_set.load(std::memory_order_acquire) >> (dev & 63)) & 1ull)) {
       MFB_CUDA_TRY(cudaFuncSetAttribute(k_dilate_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         200 * 1024));
-      attr_set = true;
+      attr_set.fetch_or(1ull << (dev & 63), std::memory_order_acq_rel);
     }
     const int tiles = ((width + kTW - 1) / kTW) * ((out_rows + kTH - 1) / kTH);
     k_dilate_fused<<<tiles, 256, smem, s>>>(width, height, channels, map_in, valid, in_row0, in_rows,

@@ -408,8 +408,49 @@ __device__ __forceinline__ void warp_closest(const BNode* __restrict__ nodes, co
 #ifndef MFB_SPEC
 #define MFB_SPEC 0
 #endif
+// L1 prefetch hints for the traversal (bit mask, compile-time):
+//   1 = a leaf's triangle lines when the leaf is entered (its 2-4 triangles
+//       are otherwise fetched one dependent L2 round trip after another),
+//   2 = the far child when it is pushed (node record or leaf triangle lines),
+//   4 = both internal children's node records as soon as a node is loaded.
+#ifndef MFB_PF
+#define MFB_PF 0
+#endif
+// Lean traversal state: the incumbent's barycentrics are not carried through
+// the walk (recomputed for the winner at the end), the slack E is one fp32.
+#ifndef MFB_LEAN
+#define MFB_LEAN 1
+#endif
+__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void pf_leaf(const BTri* __restrict__ tris, int32_t ref) {
+  int first, count;
+  leaf_decode(ref, first, count);
+  const uintptr_t b = reinterpret_cast<uintptr_t>(tris + first) & ~static_cast<uintptr_t>(127);
+  const uintptr_t e = reinterpret_cast<uintptr_t>(tris + first + count);
+  for (uintptr_t a = b; a < e; a += 128) pf_l1(reinterpret_cast<const void*>(a));
+}
+__device__ __forceinline__ void pf_ref(const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t ref) {
+  if (ref >= 0)
+    pf_l1(nodes + ref);  // 64-B record inside one 128-B line (256-B aligned array)
+  else
+    pf_leaf(tris, ref);
+}
+
+// Occupancy over registers: the walk is bound by dependent L1/L2 latency
+// (node record -> box test -> child record), so resident warps matter more
+// than the spills a 64-register cap costs. Measured at config B (transfer
+// ms): no cap (92 regs, 5 blocks/SM) 1.34, 6 blocks 1.24, 7 blocks 1.19,
+// 8 blocks (64 regs) 1.15, 9 blocks 1.23, 10 blocks 1.50.
+#ifndef MFB_XFER_T_MINB
+#define MFB_XFER_T_MINB 8
+#endif
+#if MFB_XFER_T_MINB > 0
+#define MFB_XFER_T_BOUNDS __launch_bounds__(128, MFB_XFER_T_MINB)
+#else
+#define MFB_XFER_T_BOUNDS __launch_bounds__(128)
+#endif
 template <bool kDebug, bool kProf, int kPass = 0>
-__global__ void __launch_bounds__(128) k_transfer_t(
+__global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
     const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
     const float* __restrict__ qtbn, const int* __restrict__ qcount, const double* __restrict__ hiN,
@@ -423,7 +464,7 @@ __global__ void __launch_bounds__(128) k_transfer_t(
   unsigned long long pv[4] = {0, 0, 0, 0};  // internal visits, leaf visits, triangle tests, queries
   const double scene_max = from_ordered_dev(scene_acc[6]);
   const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
-  unsigned long long hits = 0;
+  unsigned hits = 0;
   for (int li = blockIdx.x * blockDim.x + threadIdx.x; li - lane < nq; li += gridDim.x * blockDim.x) {
     const bool live = li < nq;
     const int i = kPass == 2 ? qcap - 1 - li : li;
@@ -431,7 +472,8 @@ __global__ void __launch_bounds__(128) k_transfer_t(
     if (live) p = __ldg(qpos + i);
     const float3 qf = make_float3(p.x, p.y, p.z);
     const d3 q = mk3(p.x, p.y, p.z);
-    const double E = fmax(scene_max, fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z)))) * 0x1p-32;
+    // pruning slack, rounded up to fp32 (conservative; one register)
+    const float E = __double2float_ru(fmax(scene_max, fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z)))) * 0x1p-32);
     Best best;
     best.d = init;
     best.face = -1;
@@ -550,6 +592,10 @@ __global__ void __launch_bounds__(128) k_transfer_t(
         const float4* np = reinterpret_cast<const float4*>(nodes + ref);
         const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
         const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
+        if (MFB_PF & 4) {
+          if (d.x >= 0) pf_l1(nodes + d.x);
+          if (d.y >= 0) pf_l1(nodes + d.y);
+        }
         const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
         const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
         const bool hL = lbL <= bnd, hR = lbR <= bnd;
@@ -559,6 +605,7 @@ __global__ void __launch_bounds__(128) k_transfer_t(
           st_lb[sp] = lf ? lbR : lbL;
           ++sp;
           ref = lf ? d.x : d.y;
+          if (MFB_PF & 2) pf_ref(nodes, tris, lf ? d.y : d.x);
         } else if (hL || hR) {
           ref = hL ? d.x : d.y;
         } else {
@@ -576,6 +623,7 @@ __global__ void __launch_bounds__(128) k_transfer_t(
       // ---- leaf: exact f64 tests (branch-free, reference arithmetic)
       int first, count;
       leaf_decode(ref, first, count);
+      if (MFB_PF & 1) pf_leaf(tris, ref);
       if (kProf) {
         ++pv[1];
         pv[2] += count;
@@ -592,16 +640,19 @@ __global__ void __launch_bounds__(128) k_transfer_t(
         int face;
         load_tri(tris + first + k, A, B, C, face);
         d3 bary;
+        const d3 ql = q;
 #if MFB_TRI_SEL
-        const d3 pt = closest_point_triangle_sel(q, A, B, C, bary);
+        const d3 pt = closest_point_triangle_sel(ql, A, B, C, bary);
 #else
-        const d3 pt = closest_point_triangle(q, A, B, C, bary);
+        const d3 pt = closest_point_triangle(ql, A, B, C, bary);
 #endif
-        const double ds = sqnorm(pt - q);
+        const double ds = sqnorm(pt - ql);
         if (ds < best.d || (ds == best.d && face < best.face)) {
           best.d = ds;
           best.face = face;
+#if !MFB_LEAN
           best.bary = bary;
+#endif
           bnd = prune_bound(ds, E);
         }
       }
@@ -618,6 +669,7 @@ __global__ void __launch_bounds__(128) k_transfer_t(
     if (!live) continue;
     if (kProf) ++pv[3];
     const int texel = __float_as_int(p.w);
+    const d3 qe = q;
     if (kPass == 1) face_map[texel] = best.face;
     uint8_t px[3] = {128, 128, 255};
     double ts3[3] = {0.0, 0.0, 0.0};
@@ -625,6 +677,11 @@ __global__ void __launch_bounds__(128) k_transfer_t(
       ++hits;
       const float* tb = qtbn + 9ll * i;
       const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
+#if MFB_LEAN && !MFB_SPEC
+      // the winner's barycentrics, recomputed: same inputs (BTri holds copies
+      // of these positions) and the same function give the same bits
+      closest_point_triangle(qe, ld3(hiPos + 3 * v0), ld3(hiPos + 3 * v1), ld3(hiPos + 3 * v2), best.bary);
+#endif
       const d3 n = (best.bary.x * ld3(hiN + 3 * v0) + best.bary.y * ld3(hiN + 3 * v1)) +
                    best.bary.z * ld3(hiN + 3 * v2);
       const d3 T = mk3(tb[0], tb[1], tb[2]);
@@ -663,7 +720,7 @@ __global__ void __launch_bounds__(128) k_transfer_t(
     }
   if (counters) {
     for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
-    if (lane == 0 && hits) atomicAdd(&counters[1], hits);
+    if (lane == 0 && hits) atomicAdd(&counters[1], static_cast<unsigned long long>(hits));
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));
   }
 }
@@ -1343,16 +1400,21 @@ __global__ void __launch_bounds__(256) k_raycast_brute(const double* __restrict_
 
 }  // namespace
 
+// Resident 128-thread blocks per SM of `kern` (>= 1); callers cache it in a
+// function-local static (thread-safe initialisation).
+template <class K>
+int occupancy(K kern) {
+  int v = 0;
+  MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, 128, 0));
+  return v < 1 ? 1 : v;
+}
+
 static const unsigned long long* scene_acc_of(Ctx&, const Lbvh& bvh) { return bvh.scene_acc; }
 
 void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferArgs& a) {
   // Persistent grid: enough resident warps to cover every SM; each warp
   // strides over 32-query batches until the (device-side) count is reached.
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_transfer<false, false, 1>, 128, 0));
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
+  static const int blocks_per_sm = occupancy(k_transfer<false, false, 1>);
   const int grid_cap = kNumSMs * blocks_per_sm;
   const int grid = std::max(1, std::min(grid_cap, div_up(a.q.capacity, 128)));
   const bool dbg = a.dbg_face || a.dbg_ts;
@@ -1398,11 +1460,7 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     return e && std::string(e) == "1";
   }();
   if (per_thread && wide && refill == 0) {
-    static int bpw = 0;
-    if (!bpw) {
-      MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpw, k_transfer_w<false, false>, 128, 0));
-      if (bpw < 1) bpw = 1;
-    }
+    static const int bpw = occupancy(k_transfer_w<false, false>);
     const int gw = std::max(1, std::min(kNumSMs * bpw, div_up(a.q.capacity, 128)));
 #define MFB_XFER_W(D, P)                                                                                      \
   k_transfer_w<D, P><<<gw, 128, 0, s>>>(bvh.wnodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn,  \
@@ -1415,11 +1473,7 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     }
 #undef MFB_XFER_W
   } else if (per_thread && refill > 0) {
-    static int bpp = 0;
-    if (!bpp) {
-      MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpp, k_transfer_p<false, 8, 256>, 128, 0));
-      if (bpp < 1) bpp = 1;
-    }
+    static const int bpp = occupancy(k_transfer_p<false, 8, 256>);
     const int g3 = std::max(1, std::min(kNumSMs * bpp, div_up(a.q.capacity, 128)));
     MFB_CUDA_TRY(cudaMemsetAsync(a.q.count + 2, 0, sizeof(int), s));
 #define MFB_XFER_P(D, R, C)                                                                                 \
@@ -1444,11 +1498,7 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
 #undef MFB_XFER_PC
 #undef MFB_XFER_P
   } else if (per_thread) {
-    static int bps = 0;
-    if (!bps) {
-      MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_transfer_t<false, false>, 128, 0));
-      if (bps < 1) bps = 1;
-    }
+    static const int bps = occupancy(k_transfer_t<false, false>);
     const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
 #define MFB_XFER_T(D, P, PASS)                                                                                \
   k_transfer_t<D, P, PASS><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos,        \

@@ -14,9 +14,9 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/${TAG}_smo
 timeout 600 python bench.py > $OUT/${TAG}_bench.json 2> $OUT/${TAG}_bench.err; echo "bench rc=$?"
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $OUT/${TAG}_bench_reference.json 2>> $OUT/${TAG}_bench.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
-  --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline \
+  --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-rays \
   > $OUT/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on \
   -k 'regex:k_transfer_t|k_raster|k_refit_ranges|k_dilate_fused' -c 4 \
-  -o $OUT/${TAG}_prof -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
+  -o $OUT/${TAG}_prof -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-rays \
   > $OUT/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
