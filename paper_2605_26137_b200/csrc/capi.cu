@@ -34,9 +34,8 @@ void* Ctx::buf(const std::string& name, size_t bytes) {
   Buf& b = scratch[name];
   if (b.bytes < bytes) {
     if (b.ptr) {
-      // the stream may still use the old buffer; free after it drains
-      MFB_CUDA_TRY(cudaStreamSynchronize(stream));
-      if (side) MFB_CUDA_TRY(cudaStreamSynchronize(side));
+      // the streams may still use the old buffer; free after they drain
+      sync_all();
       MFB_CUDA_TRY(cudaFree(b.ptr));
       b.ptr = nullptr;
     }
@@ -65,13 +64,18 @@ void* Ctx::host_buf(const std::string& name, size_t bytes) {
   }
   return b.ptr;
 }
-void* Ctx::cub_temp(size_t bytes, bool side_stream) {
-  void*& p = side_stream ? cub_tmp_side : cub_tmp;
-  size_t& n = side_stream ? cub_tmp_side_bytes : cub_tmp_bytes;
+void Ctx::sync_all() {
+  MFB_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (side) MFB_CUDA_TRY(cudaStreamSynchronize(side));
+  if (aux) MFB_CUDA_TRY(cudaStreamSynchronize(aux));
+}
+void* Ctx::cub_temp(size_t bytes, cudaStream_t s) {
+  const int slot = s == side ? 1 : (s == aux ? 2 : 0);
+  void*& p = cub_tmp[slot];
+  size_t& n = cub_tmp_bytes[slot];
   if (n < bytes) {
     if (p) {
-      MFB_CUDA_TRY(cudaStreamSynchronize(stream));
-      if (side) MFB_CUDA_TRY(cudaStreamSynchronize(side));
+      sync_all();
       MFB_CUDA_TRY(cudaFree(p));
     }
     const size_t want = std::max<size_t>(bytes, 1 << 20);
@@ -96,13 +100,15 @@ Ctx::~Ctx() {
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (stream) cudaStreamSynchronize(stream);
   if (side) cudaStreamSynchronize(side);
+  if (aux) cudaStreamSynchronize(aux);
   for (auto& kv : scratch) cudaFree(kv.second.ptr);
   for (auto& kv : pinned) cudaFreeHost(kv.second.ptr);
-  if (cub_tmp) cudaFree(cub_tmp);
-  if (cub_tmp_side) cudaFree(cub_tmp_side);
-  if (fork) cudaEventDestroy(fork);
-  if (join) cudaEventDestroy(join);
+  for (void* p : cub_tmp)
+    if (p) cudaFree(p);
+  for (cudaEvent_t e : {fork, join, fork2, join2, join3})
+    if (e) cudaEventDestroy(e);
   if (side) cudaStreamDestroy(side);
+  if (aux) cudaStreamDestroy(aux);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -390,23 +396,29 @@ void enqueue_bake(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double 
   MFB_CUDA_TRY(cudaEventRecord(c.fork, s));
   MFB_CUDA_TRY(cudaStreamWaitEvent(side, c.fork, 0));
   mk.side0 = tm.mark(side);
-  double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
-  vertex_normals(c, side, hi->m, hiN, true, "hi");
   Lbvh bvh;
   lbvh_build(c, side, hi->m, bvh, "hi.bvh");
   mk.side1 = tm.mark(side);
   MFB_CUDA_TRY(cudaEventRecord(c.join, side));
 
-  // main: lowpoly prep + raster (fused: valid mask, raw map, query list)
+  // main: lowpoly prep (its wedge frames on the aux stream) + raster (fused:
+  // valid mask, raw map, query list)
   mk.e0 = tm.mark(s);
   RasterPlan plan;
   prepare_lowpoly(c, s, lo->m, res, plan);
   mk.e1 = tm.mark(s);
+  // aux, after the lowpoly wedge frames: the dense vertex normals, needed
+  // only by the transfer's encode — off the LBVH's critical path
+  double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
+  cudaStream_t ns = c.aux ? c.aux : side;
+  vertex_normals(c, ns, hi->m, hiN, true, "hi");
+  MFB_CUDA_TRY(cudaEventRecord(c.join3, ns));
   raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
   mk.e2 = tm.mark(s);
 
   // join, transfer, dilate
   MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
+  MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join3, 0));
   mk.e3 = tm.mark(s);
   TransferArgs ta;
   ta.q = fo.q;
@@ -579,8 +591,9 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
       ctx->c.own_stream = true;
     }
     MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
-    MFB_CUDA_TRY(cudaEventCreateWithFlags(&ctx->c.fork, cudaEventDisableTiming));
-    MFB_CUDA_TRY(cudaEventCreateWithFlags(&ctx->c.join, cudaEventDisableTiming));
+    MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.aux, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3})
+      MFB_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     *out = ctx.release();
     return MF_OK;
   });
@@ -591,8 +604,7 @@ void mf_ctx_destroy(mf_ctx* ctx) { delete ctx; }
 int mf_ctx_synchronize(mf_ctx* ctx) {
   if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
   return guarded(ctx, [&]() -> int {
-    MFB_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
-    MFB_CUDA_TRY(cudaStreamSynchronize(ctx->c.side));
+    ctx->c.sync_all();
     return MF_OK;
   });
 }

@@ -445,14 +445,15 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
 
   size_t tmp = 0;
   cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, vals, vals2, n, 0, 30, s);
-  void* tptr = ctx.cub_temp(tmp, s != ctx.stream);
+  void* tptr = ctx.cub_temp(tmp, s);
   MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 30, s));
 
-  // Leaf size: the reference's 4 (bvh.cpp:13) unless MFB_LEAF_MAX (1..7) overrides it.
+  // Leaf size: kLeafMaxDefault (the reference uses 4, bvh.cpp:13; the
+  // results are tree-independent) unless MFB_LEAF_MAX (1..7) overrides it.
   static const int leaf_max = [] {
     const char* e = std::getenv("MFB_LEAF_MAX");
-    const int v = e ? std::atoi(e) : kLeafMax;
-    return v >= 1 && v <= 7 ? v : kLeafMax;
+    const int v = e ? std::atoi(e) : kLeafMaxDefault;
+    return v >= 1 && v <= 7 ? v : kLeafMaxDefault;
   }();
   if (n > 1) {
     k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent);

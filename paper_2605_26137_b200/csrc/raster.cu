@@ -340,14 +340,36 @@ __global__ void __launch_bounds__(256) k_island_select(int nu, const int* __rest
       if ((v & hi_mask) == prefix) atomicAdd(&hist[(v >> shift) & 0xff], 1);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      int k = s_k, b = 0;
-      while (k >= hist[b]) {
-        k -= hist[b];
-        ++b;
+    if (threadIdx.x < 32) {
+      // warp 0: bucket holding rank k. Lane l owns buckets 8l..8l+7; an
+      // inclusive scan of the lane sums finds the lane, then its 8 buckets.
+      const int lane = threadIdx.x;
+      int c[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        c[j] = hist[8 * lane + j];
+        sum += c[j];
       }
-      s_k = k;
-      s_prefix = prefix | (static_cast<unsigned long long>(b) << shift);
+      int incl = sum;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      const int k = s_k;
+      const unsigned owner = __ballot_sync(0xffffffffu, incl > k);  // k < n: some lane holds it
+      const int ol = __ffs(owner) - 1;
+      if (lane == ol) {
+        int kk = k - (incl - sum), b = 8 * lane;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (kk < c[j]) break;
+          kk -= c[j];
+          ++b;
+        }
+        s_k = kk;
+        s_prefix = prefix | (static_cast<unsigned long long>(b) << shift);
+      }
     }
     __syncthreads();
   }
@@ -719,7 +741,7 @@ void corner_csr(Ctx& ctx, cudaStream_t s, const DevMesh& m, const std::string& t
   k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, cnt, start, m.nv + 1, s));
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, start, m.nv + 1, s));
   k_corner_fill<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, start, cursor, list);
   k_csr_sort<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list);
   ctx.count_launch(3);
@@ -761,7 +783,7 @@ void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, boo
   k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, cnt, start, m.nv + 1, s));
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, start, m.nv + 1, s));
   k_corner_fill<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, start, cursor, list);
   k_face_area_vec<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, av);
   k_vertex_sum_unsorted<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list, av, out, renorm ? 1 : 0);
@@ -803,7 +825,16 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
   const int nf = lo.nf, nu = lo.nu;
   auto* rf = ctx.buf<RasterFace>("lo.rf", nf);
   auto* attrs = ctx.buf<AttrFace>("lo.attrs", nf);
-  wedge_pipeline(ctx, s, lo, nullptr, attrs);
+  // fork: the wedge frames (computeWedgeTangents) on the aux stream overlap
+  // the reliability pass below; they write disjoint AttrFace fields
+  // (P/N/T vs reliable/pad). Joined before returning.
+  cudaStream_t ws = ctx.aux ? ctx.aux : s;
+  if (ws != s) {
+    MFB_CUDA_TRY(cudaEventRecord(ctx.fork2, s));
+    MFB_CUDA_TRY(cudaStreamWaitEvent(ws, ctx.fork2, 0));
+  }
+  wedge_pipeline(ctx, ws, lo, nullptr, attrs);
+  if (ws != s) MFB_CUDA_TRY(cudaEventRecord(ctx.join2, ws));
 
   // reliableFaces (gbuffer.cpp:31-83)
   int* parent = ctx.buf<int>("lo.rel.parent", nu);
@@ -824,12 +855,13 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
                                            count);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, start, nu + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, count, start, nu + 1, s));
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, count, start, nu + 1, s));
   k_island_fill<<<div_up(nf, T), T, 0, s>>>(nf, ratio, island, start, cursor, items);
   k_island_select<<<nu, 256, 0, s>>>(nu, count, start, items, median);
   k_face_setup<<<div_up(nf, T), T, 0, s>>>(lo.uvs, lo.fuv, nf, res, uv_area, ratio, island, median, rf, attrs);
   ctx.count_launch(7);
   MFB_CUDA_TRY(cudaGetLastError());
+  if (ws != s) MFB_CUDA_TRY(cudaStreamWaitEvent(s, ctx.join2, 0));
   plan.faces = rf;
   plan.attrs = attrs;
   plan.nf = nf;
@@ -860,7 +892,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
   k_bin_count<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, cnt);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, ntiles + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s != ctx.stream), tmp, cnt, start, ntiles + 1, s));
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, start, ntiles + 1, s));
   k_bin_fill<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, start, cursor, bins,
                                               capacity, flags_dev + 1);
   MFB_CUDA_TRY(cudaMemcpyAsync(flags_dev + 2, start + ntiles, sizeof(int), cudaMemcpyDeviceToDevice, s));

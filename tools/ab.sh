@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 for rep in 1 2; do
 for v in ${VARIANTS:-base}; do
-  e=$v; [ "$v" = base ] && e="MFB_NOOP=1"
+  e=${v//+/ }; [ "$v" = base ] && e="MFB_NOOP=1"
   env $e timeout 300 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-rays ${BENCH_ARGS} 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read()); print('$v'.replace('/libmfbake.so','').replace('MFB_LIB=build/var/',''), round(d['ms_per_step'],4), 'ms', {k:round(v,3) for k,v in d['stage_ms'].items()})"

@@ -16,4 +16,5 @@ for f in paper_2605_26137_b200/csrc/*.cu; do
 done
 wait
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/libmfbake.so $objs -Xlinker -soname=libmfbake.so
+rm -f $objs
 echo "$out/libmfbake.so ($*)"
