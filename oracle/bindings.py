@@ -221,6 +221,17 @@ class Ref(_Lib):
                        n_tri=float(counters[3]))
         return out
 
+    def sampled_counters(self, lo: TriangleMesh, hi: TriangleMesh, res: int, diag: float, frac: float,
+                         stride: int):
+        """Best-first traversal counters on every `stride`-th query (ref_harness.cpp)."""
+        c = np.zeros(5)
+        lv, hv = lo.view(), hi.view()
+        self._check(self.fn("sampled_counters")(ctypes.byref(lv), ctypes.byref(hv), ctypes.c_int(res),
+                                                ctypes.c_double(diag), ctypes.c_double(frac),
+                                                ctypes.c_int(stride), _ptr(c)))
+        return dict(n_valid=int(c[0]), n_queries=int(c[1]), sampled=int(c[2]), n_node=float(c[3]),
+                    n_tri=float(c[4]), stride=stride)
+
     def bvh_build_time(self, m: TriangleMesh):
         s, nodes = ctypes.c_double(0), ctypes.c_int(0)
         v = m.view()

@@ -297,6 +297,46 @@ int ref_bake(const mf_mesh_view* lo, const mf_mesh_view* hi, int res, double dia
   });
 }
 
+// Traversal counters of the reference's best-first loop on every `stride`-th
+// texel only (configs whose full bake is too slow to instrument, e.g. E):
+// counters = [valid, queries (full), sampled queries, mean pops, mean tests].
+int ref_sampled_counters(const mf_mesh_view* lo, const mf_mesh_view* hi, int res, double diag, double frac,
+                         int stride, double* counters) {
+  return guarded([&] {
+    const TriangleMesh low = toMesh(lo);
+    const TriangleMesh high = toMesh(hi);
+    const GBuffer g = rasterizeGBuffer(low, res);
+    const Bvh bvh(high);
+    const double maxDist = frac * diag;
+    const int64_t texels = static_cast<int64_t>(res) * res;
+    std::vector<int64_t> idx;
+    int64_t nv = 0, nq = 0;
+    for (int64_t t = 0; t < texels; ++t) {
+      nv += g.valid[t];
+      if (g.valid[t] && g.reliable[t]) {
+        if (nq % stride == 0) idx.push_back(t);
+        ++nq;
+      }
+    }
+    std::vector<int64_t> pops(idx.size(), 0), tris(idx.size(), 0);
+    parallelFor(
+        0, static_cast<int64_t>(idx.size()),
+        [&](int64_t k) { countedClosestWithin(bvh, g.position[idx[k]].cast<double>(), maxDist, pops[k], tris[k]); },
+        256);
+    int64_t sp = 0, st = 0;
+    for (size_t k = 0; k < idx.size(); ++k) {
+      sp += pops[k];
+      st += tris[k];
+    }
+    const double ns = idx.empty() ? 1.0 : static_cast<double>(idx.size());
+    counters[0] = static_cast<double>(nv);
+    counters[1] = static_cast<double>(nq);
+    counters[2] = static_cast<double>(idx.size());
+    counters[3] = sp / ns;
+    counters[4] = st / ns;
+  });
+}
+
 int ref_bvh_build_time(const mf_mesh_view* mesh, double* seconds, int* nodes) {
   return guarded([&] {
     const TriangleMesh m = toMesh(mesh);

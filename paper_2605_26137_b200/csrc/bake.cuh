@@ -33,6 +33,8 @@ struct Ctx {
   cudaStream_t side = nullptr;      // second stream: dense-mesh work overlaps the lowpoly work
   cudaStream_t aux = nullptr;       // third stream: lowpoly wedge frames overlap its reliability pass
   cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr, join3 = nullptr;
+  cudaEvent_t hi_ready = nullptr;   // host entry point: dense mesh uploaded and validated
+  cudaEvent_t dfork = nullptr, djoin = nullptr;  // host entry point: dense phase side -> aux -> side
   bool timing = false;
   int64_t launches = 0;
   struct Buf {
@@ -68,6 +70,15 @@ struct Ctx {
   cudaGraphExec_t bake_exec = nullptr;
   std::vector<char> bake_key, bake_prev_key;
   uint64_t bake_gen = 0, bake_prev_gen = ~0ull;
+  // Captured phases of the host-buffer bake (capi.cu bake_host_overlapped):
+  // the first call with a key runs eagerly, the second captures, later ones
+  // replay while no scratch buffer was reallocated.
+  struct GraphSlot {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<char> key, prev_key;
+    uint64_t gen = 0, prev_gen = ~0ull;
+  };
+  GraphSlot g_low, g_dense;
   ~Ctx();
 };
 
@@ -162,6 +173,9 @@ struct Lbvh {
 
 // Build into buffers owned by `owner` scratch names prefixed with `tag`.
 void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag);
+// The descriptor lbvh_build fills (device buffers by scratch name), without
+// launching anything: used when a captured build is replayed.
+void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag);
 
 // ---------------------------------------------------------------- lowpoly prep + raster
 // computeVertexNormals (mesh.cpp:24-35) followed, when `renorm`, by the

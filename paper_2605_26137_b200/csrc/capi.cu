@@ -97,6 +97,8 @@ cudaEvent_t Ctx::pool_event(int i) {
 Ctx::~Ctx() {
   cudaSetDevice(device);
   if (bake_exec) cudaGraphExecDestroy(bake_exec);
+  for (GraphSlot* g : {&g_low, &g_dense})
+    if (g->exec) cudaGraphExecDestroy(g->exec);
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (stream) cudaStreamSynchronize(stream);
   if (side) cudaStreamSynchronize(side);
@@ -105,7 +107,7 @@ Ctx::~Ctx() {
   for (auto& kv : pinned) cudaFreeHost(kv.second.ptr);
   for (void* p : cub_tmp)
     if (p) cudaFree(p);
-  for (cudaEvent_t e : {fork, join, fork2, join2, join3})
+  for (cudaEvent_t e : {fork, join, fork2, join2, join3, hi_ready, dfork, djoin})
     if (e) cudaEventDestroy(e);
   if (side) cudaStreamDestroy(side);
   if (aux) cudaStreamDestroy(aux);
@@ -216,11 +218,12 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 bool view_has_uvs(const mf_mesh_view* v) { return v->face_uvs && v->uvs && v->n_uvs > 0; }
 
-// Upload + device validation into `mesh`. With a scratch tag the arrays live
-// in the context's grow-only scratch (host-buffer entry points: no
-// cudaMalloc per call); otherwise the mesh owns a fresh allocation.
-void upload_mesh(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* mesh,
-                 const char* scratch_tag = nullptr) {
+// Enqueues the H2D copies and the device validation of `v` on `s`; the
+// validation flags land in `*hflag` (pinned host memory) when `s` reaches
+// them. finish_upload() turns them into the mesh status after the caller has
+// synchronised.
+void upload_mesh_async(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* mesh, const char* scratch_tag,
+                       int* hflag) {
   if (!v) throw ApiError(MF_ERR_BAD_ARGUMENT, "mesh view is null");
   if (v->n_vertices < 0 || v->n_faces < 0 || v->n_uvs < 0) throw ApiError(MF_ERR_BAD_ARGUMENT, "negative size");
   if ((v->n_vertices > 0 && !v->positions) || (v->n_faces > 0 && !v->faces))
@@ -273,18 +276,20 @@ void upload_mesh(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* mesh,
     c.count_launch();
     MFB_CUDA_TRY(cudaGetLastError());
   }
-  int hf = 0;
-  MFB_CUDA_TRY(cudaMemcpyAsync(&hf, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
-  MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  MFB_CUDA_TRY(cudaMemcpyAsync(hflag, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
   m.pos = dpos;
   m.faces = dfac;
   m.nrm = dnrm;
   m.uvs = duv;
   m.fuv = dfuv;
   mesh->m = m;
+}
+
+// validateMesh (core/mesh.cpp:37-48) outcome from the device flags.
+void finish_upload(mf_mesh* mesh, int hf) {
   mesh->status = MF_OK;
   mesh->status_msg.clear();
-  if (m.nf == 0) {
+  if (mesh->m.nf == 0) {
     mesh->status = MF_ERR_EMPTY_MESH;
     mesh->status_msg = "EmptyMesh: mesh has no faces";
   } else if (hf & 1) {
@@ -295,6 +300,17 @@ void upload_mesh(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* mesh,
     mesh->status_msg = "InvalidGeometry: face index out of range";
   }
   mesh->uv_index_ok = !(hf & 4);
+}
+
+// Upload + device validation into `mesh`, synchronously. With a scratch tag
+// the arrays live in the context's grow-only scratch (host-buffer entry
+// points: no cudaMalloc per call); otherwise the mesh owns a fresh allocation.
+void upload_mesh(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* mesh,
+                 const char* scratch_tag = nullptr) {
+  int* hf = static_cast<int*>(c.host_buf(std::string("upflag.") + (scratch_tag ? scratch_tag : "own"), sizeof(int)));
+  upload_mesh_async(c, s, v, mesh, scratch_tag, hf);
+  MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  finish_upload(mesh, *hf);
 }
 
 void check_mesh(const mf_mesh* mesh) {
@@ -367,79 +383,194 @@ struct BakeMarks {
               e4 = nullptr, e5 = nullptr;
 };
 
+// Runs `body` (work enqueued on `s`, possibly forking/joining other streams)
+// through `slot`: eagerly the first time a key is seen, captured into a graph
+// on the second identical call, replayed afterwards. A capture during which
+// scratch was (re)allocated is discarded (its pointers are stale).
+template <class F>
+void run_graphed(Ctx& c, Ctx::GraphSlot& slot, cudaStream_t s, const std::vector<char>& key, bool allow, F&& body) {
+  if (allow && slot.exec && key == slot.key && c.alloc_gen == slot.gen) {
+    MFB_CUDA_TRY(cudaGraphLaunch(slot.exec, s));
+    return;
+  }
+  if (allow && key == slot.prev_key && c.alloc_gen == slot.prev_gen) {
+    cudaGraph_t graph = nullptr;
+    MFB_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+      body();
+    } catch (...) {
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    MFB_CUDA_TRY(cudaStreamEndCapture(s, &graph));
+    if (c.alloc_gen != slot.prev_gen) {
+      cudaGraphDestroy(graph);
+      slot.prev_gen = c.alloc_gen;
+      body();
+      return;
+    }
+    if (slot.exec) cudaGraphExecDestroy(slot.exec);
+    slot.exec = nullptr;
+    MFB_CUDA_TRY(cudaGraphInstantiate(&slot.exec, graph, 0));
+    cudaGraphDestroy(graph);
+    slot.key = key;
+    slot.gen = c.alloc_gen;
+    MFB_CUDA_TRY(cudaGraphLaunch(slot.exec, s));
+    return;
+  }
+  body();
+  slot.prev_key = key;
+  slot.prev_gen = c.alloc_gen;
+}
+
+template <class T>
+std::vector<char> key_bytes(const T& k) {
+  return std::vector<char>(reinterpret_cast<const char*>(&k), reinterpret_cast<const char*>(&k) + sizeof(k));
+}
+
+// The bake's three phases. enqueue_bake() chains them with a fork/join (the
+// captured graph); the host-buffer entry point interleaves its own upload and
+// validation wait between them (bake_host_overlapped).
+struct BakeEnq {
+  Ctx& c;
+  const mf_mesh *lo, *hi;
+  int res, radius, rb, re, s0, s1;
+  double diag, frac;
+  uint8_t* rgb_out;
+  bool debug;
+  Timer& tm;
+  BakeMarks& mk;
+  GBufDev g;
+  int* flags = nullptr;
+  unsigned long long* counters = nullptr;
+  RasterFused fo;
+  Lbvh bvh;
+  double* hiN = nullptr;
+
+  BakeEnq(Ctx& cc, const mf_mesh* l, const mf_mesh* h, int rs, double dg, double fr, int rad, int b0, int b1,
+          uint8_t* out, bool dbg, Timer& t, BakeMarks& m)
+      : c(cc), lo(l), hi(h), res(rs), radius(rad), rb(b0), re(b1), diag(dg), frac(fr), rgb_out(out), debug(dbg),
+        tm(t), mk(m) {
+    s0 = std::max(0, rb - radius);  // raster/transfer slab with the dilation halo
+    s1 = std::min(res, re + radius);
+    g.res = res;
+    g.row0 = s0;
+    g.rows = s1 - s0;
+    g.valid = c.buf<uint8_t>("g.valid", g.texels());
+    // flags: [0] AtlasOverlap, [1] bin overflow, [2] bin total, [3] query overflow
+    flags = c.buf<int>("bake.flags", 4);
+    counters = c.buf<unsigned long long>("bake.counters", 4);
+    fo.rgb = c.buf<uint8_t>("bake.raw", 3 * g.texels());
+    fo.q = query_list(c, g.texels());
+    fo.valid_count = counters + 2;
+    if (debug) {
+      fo.dbg_face = c.buf<int32_t>("bake.dface", g.texels());
+      fo.dbg_ts = c.buf<double>("bake.dts", 3 * g.texels());
+    }
+  }
+
+  // main stream: lowpoly prep (its wedge frames on the aux stream) + fused
+  // raster (valid mask, raw map, query list)
+  void low() {
+    cudaStream_t s = c.stream;
+    MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
+    MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
+    mk.e0 = tm.mark(s);
+    RasterPlan plan;
+    prepare_lowpoly(c, s, lo->m, res, plan);
+    mk.e1 = tm.mark(s);
+    raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
+    mk.e2 = tm.mark(s);
+  }
+
+  // dense mesh: LBVH on the side stream; unit vertex normals (needed only by
+  // the transfer's encode) on the aux stream, enqueued after low() so they
+  // queue behind the lowpoly wedge frames. Both wait for `ready`.
+  void dense_bvh(cudaEvent_t ready) {
+    cudaStream_t side = c.side;
+    MFB_CUDA_TRY(cudaStreamWaitEvent(side, ready, 0));
+    mk.side0 = tm.mark(side);
+    lbvh_build(c, side, hi->m, bvh, "hi.bvh");
+    mk.side1 = tm.mark(side);
+    MFB_CUDA_TRY(cudaEventRecord(c.join, side));
+  }
+  void dense_normals(cudaEvent_t ready) {
+    cudaStream_t ns = c.aux ? c.aux : c.side;
+    hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
+    if (ns != c.side) MFB_CUDA_TRY(cudaStreamWaitEvent(ns, ready, 0));
+    vertex_normals(c, ns, hi->m, hiN, true, "hi");
+    MFB_CUDA_TRY(cudaEventRecord(c.join3, ns));
+  }
+
+  // host-buffer path: the whole dense phase on the side stream (normals on
+  // aux, forked and joined back), so it can be captured from `side` alone;
+  // then c.join / c.join3 mark its end for tail().
+  void dense_side(bool graphs) {
+    cudaStream_t side = c.side, ns = c.aux ? c.aux : c.side;
+    lbvh_layout(c, hi->m, bvh, "hi.bvh");
+    hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
+    const int64_t k[] = {reinterpret_cast<int64_t>(hi->m.pos), reinterpret_cast<int64_t>(hi->m.faces),
+                         reinterpret_cast<int64_t>(hi->m.nrm), hi->m.nf, hi->m.nv};
+    run_graphed(c, c.g_dense, side, key_bytes(k), graphs, [&] {
+      MFB_CUDA_TRY(cudaEventRecord(c.dfork, side));
+      mk.side0 = tm.mark(side);
+      lbvh_build(c, side, hi->m, bvh, "hi.bvh");
+      mk.side1 = tm.mark(side);
+      if (ns != side) {
+        MFB_CUDA_TRY(cudaStreamWaitEvent(ns, c.dfork, 0));
+        vertex_normals(c, ns, hi->m, hiN, true, "hi");
+        MFB_CUDA_TRY(cudaEventRecord(c.djoin, ns));
+        MFB_CUDA_TRY(cudaStreamWaitEvent(side, c.djoin, 0));
+      } else {
+        vertex_normals(c, side, hi->m, hiN, true, "hi");
+      }
+    });
+    MFB_CUDA_TRY(cudaEventRecord(c.join, side));
+    MFB_CUDA_TRY(cudaEventRecord(c.join3, side));
+  }
+
+  // main stream, after both dense branches: transfer + dilation + flags
+  void tail(int* hflags_pinned, unsigned long long* hcnt_pinned) {
+    cudaStream_t s = c.stream;
+    MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
+    MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join3, 0));
+    mk.e3 = tm.mark(s);
+    TransferArgs ta;
+    ta.q = fo.q;
+    ta.res = res;
+    ta.slab_row0 = s0;
+    ta.face_map = c.buf<int>("bake.facemap", g.texels());
+    ta.face_map_size = g.texels();
+    ta.hi_positions = hi->m.pos;
+    ta.hi_normals = hiN;
+    ta.hi_faces = hi->m.faces;
+    ta.max_dist = frac * diag;
+    ta.rgb = fo.rgb;
+    ta.dbg_face = fo.dbg_face;
+    ta.dbg_ts = fo.dbg_ts;
+    ta.counters = counters;
+    transfer_normals(c, s, bvh, ta);
+    mk.e4 = tm.mark(s);
+    dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out, rb, re - rb);
+    mk.e5 = tm.mark(s);
+    MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    MFB_CUDA_TRY(
+        cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  }
+};
+
+// Everything the fused bake enqueues; no host synchronisation inside, so
+// the same sequence can be captured into a CUDA graph.
 void enqueue_bake(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
                   int rb, int re, uint8_t* rgb_out, bool debug, Timer& tm, BakeMarks& mk, int* hflags_pinned,
                   unsigned long long* hcnt_pinned) {
-  cudaStream_t s = c.stream, side = c.side;
-  const int r = radius;
-  const int s0 = std::max(0, rb - r), s1 = std::min(res, re + r);  // raster/transfer slab with dilation halo
-  GBufDev g;
-  g.res = res;
-  g.row0 = s0;
-  g.rows = s1 - s0;
-  g.valid = c.buf<uint8_t>("g.valid", g.texels());
-  // flags: [0] AtlasOverlap, [1] bin overflow, [2] bin total, [3] query overflow
-  int* flags = c.buf<int>("bake.flags", 4);
-  unsigned long long* counters = c.buf<unsigned long long>("bake.counters", 4);
-  RasterFused fo;
-  fo.rgb = c.buf<uint8_t>("bake.raw", 3 * g.texels());
-  fo.q = query_list(c, g.texels());
-  fo.valid_count = counters + 2;
-  if (debug) {
-    fo.dbg_face = c.buf<int32_t>("bake.dface", g.texels());
-    fo.dbg_ts = c.buf<double>("bake.dts", 3 * g.texels());
-  }
-  MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), s));
-
-  // fork: dense-mesh work on the side stream
-  MFB_CUDA_TRY(cudaEventRecord(c.fork, s));
-  MFB_CUDA_TRY(cudaStreamWaitEvent(side, c.fork, 0));
-  mk.side0 = tm.mark(side);
-  Lbvh bvh;
-  lbvh_build(c, side, hi->m, bvh, "hi.bvh");
-  mk.side1 = tm.mark(side);
-  MFB_CUDA_TRY(cudaEventRecord(c.join, side));
-
-  // main: lowpoly prep (its wedge frames on the aux stream) + raster (fused:
-  // valid mask, raw map, query list)
-  mk.e0 = tm.mark(s);
-  RasterPlan plan;
-  prepare_lowpoly(c, s, lo->m, res, plan);
-  mk.e1 = tm.mark(s);
-  // aux, after the lowpoly wedge frames: the dense vertex normals, needed
-  // only by the transfer's encode — off the LBVH's critical path
-  double* hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
-  cudaStream_t ns = c.aux ? c.aux : side;
-  vertex_normals(c, ns, hi->m, hiN, true, "hi");
-  MFB_CUDA_TRY(cudaEventRecord(c.join3, ns));
-  raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
-  mk.e2 = tm.mark(s);
-
-  // join, transfer, dilate
-  MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
-  MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join3, 0));
-  mk.e3 = tm.mark(s);
-  TransferArgs ta;
-  ta.q = fo.q;
-  ta.res = res;
-  ta.slab_row0 = s0;
-  ta.face_map = c.buf<int>("bake.facemap", g.texels());
-  ta.face_map_size = g.texels();
-  ta.hi_positions = hi->m.pos;
-  ta.hi_normals = hiN;
-  ta.hi_faces = hi->m.faces;
-  ta.max_dist = frac * diag;
-  ta.rgb = fo.rgb;
-  ta.dbg_face = fo.dbg_face;
-  ta.dbg_ts = fo.dbg_ts;
-  ta.counters = counters;
-  transfer_normals(c, s, bvh, ta);
-  mk.e4 = tm.mark(s);
-  dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, r, rgb_out, rb, re - rb);
-  mk.e5 = tm.mark(s);
-  MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-  MFB_CUDA_TRY(cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  BakeEnq q(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, debug, tm, mk);
+  MFB_CUDA_TRY(cudaEventRecord(c.fork, c.stream));
+  q.dense_bvh(c.fork);
+  q.low();
+  q.dense_normals(c.fork);
+  q.tail(hflags_pinned, hcnt_pinned);
 }
 
 // The fused bake over validated device meshes; rows [rb, re) into rgb_out
@@ -560,6 +691,126 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
   }
 }
 
+// True when [p, p + bytes) is page-locked host memory (its H2D copy is a
+// truly asynchronous DMA; a pageable source blocks the calling thread).
+bool host_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// mf_bake_normal_map without debug outputs. The dense mesh's H2D copy and
+// device validation run on the side stream while the lowpoly is uploaded,
+// validated, prepared and rasterised on the main stream; the host waits for
+// the dense validation flag only after the lowpoly work is queued, then
+// queues the LBVH / dense normals and the transfer. Errors keep the
+// reference's order: lowpoly checks (gbuffer.cpp:93-97), AtlasOverlap
+// (:157-159), then transferNormals' checks (:195-199), then dilateSeams' (:255).
+void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const mf_mesh_view* hv, int res,
+                          double diag, double frac, int radius, uint8_t* rgb_out, mf_bake_stats* st) {
+  cudaStream_t s = c.stream;
+  mf_mesh lo, hi;
+  lo.ctx = hi.ctx = owner;
+  int* hup = static_cast<int*>(c.host_buf("bake.upflags", 2 * sizeof(int)));
+  int* hflags = static_cast<int*>(c.host_buf("bake.hflags", 4 * sizeof(int)));
+  auto* hcnt = static_cast<unsigned long long*>(c.host_buf("bake.hcnt", 4 * sizeof(unsigned long long)));
+  Timer tm(c, 0);
+  cudaEvent_t t0 = tm.mark(s);
+  if (!hv) throw ApiError(MF_ERR_BAD_ARGUMENT, "mesh view is null");
+  // The lowpoly's copy goes first: H2D copies share one copy engine in
+  // submission order, so the (small) lowpoly must not queue behind the
+  // dense mesh. Pinned dense arrays are then submitted before the host waits
+  // for the lowpoly flags; pageable ones would block this thread, so they go
+  // after the lowpoly work is queued.
+  const bool early = host_pinned(hv->positions) && host_pinned(hv->faces) && host_pinned(hv->normals);
+  MFB_CUDA_TRY(cudaEventRecord(c.fork, s));  // the caller's earlier work on the ctx stream
+  auto upload_hi = [&] {
+    MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.fork, 0));
+    upload_mesh_async(c, c.side, hv, &hi, "up.hi", hup + 1);
+    MFB_CUDA_TRY(cudaEventRecord(c.hi_ready, c.side));
+  };
+  auto drain = [&] {
+    cudaStreamSynchronize(c.side);
+    cudaStreamSynchronize(s);
+  };
+  try {
+    upload_mesh_async(c, s, lv, &lo, "up.lo", hup);
+    if (early) upload_hi();
+    MFB_CUDA_TRY(cudaStreamSynchronize(s));
+    finish_upload(&lo, hup[0]);
+    check_lowpoly(&lo, res);
+    if (!rgb_out) throw ApiError(MF_ERR_BAD_ARGUMENT, "rgb_out is null");
+  } catch (...) {
+    drain();
+    throw;
+  }
+  uint8_t* drgb = c.buf<uint8_t>("bake.rgb", 3 * static_cast<int64_t>(res) * res);
+  BakeMarks mk;
+  Timer tmb(c, 8);
+  BakeEnq q(c, &lo, &hi, res, diag, frac, radius, 0, res, drgb, false, tmb, mk);
+  static const bool graphs = [] {
+    const char* e = std::getenv("MFB_GRAPH");
+    return !(e && e[0] == '0');
+  }();
+  const bool use_graphs = graphs && !c.timing;
+  {
+    const int64_t k[] = {reinterpret_cast<int64_t>(lo.m.pos), reinterpret_cast<int64_t>(lo.m.faces),
+                         reinterpret_cast<int64_t>(lo.m.nrm), reinterpret_cast<int64_t>(lo.m.uvs),
+                         reinterpret_cast<int64_t>(lo.m.fuv), lo.m.nf, lo.m.nv, lo.m.nu, res, c.bin_capacity};
+    run_graphed(c, c.g_low, s, key_bytes(k), use_graphs, [&] { q.low(); });
+  }
+  if (!early) upload_hi();
+  MFB_CUDA_TRY(cudaEventSynchronize(c.hi_ready));
+  finish_upload(&hi, hup[1]);
+  if (hi.status != MF_OK || !(diag > 0.0) || !(frac > 0.0) || radius < 0) {
+    // raster errors precede transferNormals' checks: finish the raster first
+    MFB_CUDA_TRY(cudaMemcpyAsync(hflags, q.flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    drain();
+    if (hflags[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+    check_mesh(&hi);
+    check_transfer_cfg(diag, frac);
+    throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilation radius must be >= 0");
+  }
+  q.dense_side(use_graphs);
+  q.tail(hflags, hcnt);
+  cudaEvent_t t2 = tm.mark(s);
+  MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, s));
+  cudaEvent_t t3 = tm.mark(s);
+  MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (hflags[1] || hflags[3]) {
+    // tile bins overflowed on this shape: the device-mesh path re-runs with
+    // the exact capacity (and keeps it for later calls)
+    if (hflags[1]) c.bin_capacity = static_cast<int64_t>(hflags[2]) + 1;
+    Timer tr(c, 8);
+    bake_dev(c, &lo, &hi, res, diag, frac, radius, 0, res, drgb, nullptr, nullptr, st, tr, nullptr);
+    MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, s));
+    MFB_CUDA_TRY(cudaStreamSynchronize(s));
+    return;
+  }
+  if (hflags[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+  if (st) {
+    st->queries = static_cast<int64_t>(hcnt[0]);
+    st->hits = static_cast<int64_t>(hcnt[1]);
+    st->valid_texels = static_cast<int64_t>(hcnt[2]);
+    st->bvh_nodes = hi.m.nf > 1 ? hi.m.nf - 1 : 0;
+    st->bvh_depth = 0;
+    if (c.timing) {
+      st->ms_upload = Timer::ms(t0, mk.e0);
+      st->ms_prepare = Timer::ms(mk.e0, mk.e1);
+      st->ms_raster = Timer::ms(mk.e1, mk.e2);
+      st->ms_bvh = Timer::ms(mk.side0, mk.side1);
+      st->ms_transfer = Timer::ms(mk.e3, mk.e4);
+      st->ms_dilate = Timer::ms(mk.e4, mk.e5);
+      st->ms_download = Timer::ms(t2, t3);
+      st->ms_total = Timer::ms(t0, t3);
+    }
+  }
+}
+
 thread_local std::vector<std::unique_ptr<mf_mesh>> g_tmp_meshes;
 
 }  // namespace
@@ -592,7 +843,8 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     }
     MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
     MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.aux, cudaStreamNonBlocking));
-    for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3})
+    for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3, &ctx->c.hi_ready,
+                            &ctx->c.dfork, &ctx->c.djoin})
       MFB_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     *out = ctx.release();
     return MF_OK;
@@ -755,6 +1007,18 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
   if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
   return guarded(ctx, [&]() -> int {
     Ctx& c = ctx->c;
+    // MFB_E2E_OVERLAP=0: the sequential upload -> bake -> download path (A/B)
+    static const bool overlap = [] {
+      const char* e = std::getenv("MFB_E2E_OVERLAP");
+      return !(e && e[0] == '0');
+    }();
+    if (overlap && !dbg_face && !dbg_ts) {
+      mf_bake_stats local{};
+      bake_host_overlapped(c, ctx, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius, rgb_out,
+                           &local);
+      if (stats) *stats = local;
+      return MF_OK;
+    }
     HostTrace ht("bake_host");
     Timer tm(c, 0);  // host marks use pool events 0..3; bake_dev's start at 8
     Timer tmb(c, 8);

@@ -415,20 +415,27 @@ __global__ void k_collapse4(const BNode* __restrict__ nodes, int n_nodes, WNode*
 
 }  // namespace
 
-void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag) {
+void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag) {
   const int n = m.nf;
   out.n_tris = n;
   out.n_nodes = n > 1 ? n - 1 : 0;
-  auto* acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
-  auto* keys = ctx.buf<uint32_t>(tag + ".keys", n);
-  auto* keys2 = ctx.buf<uint32_t>(tag + ".keys2", n);
-  auto* vals = ctx.buf<uint32_t>(tag + ".vals", n);
-  auto* vals2 = ctx.buf<uint32_t>(tag + ".vals2", n);
   out.nodes = ctx.buf<BNode>(tag + ".nodes", out.n_nodes > 0 ? out.n_nodes : 1);
   out.tris = ctx.buf<BTri>(tag + ".tris", n);
   out.tbox = ctx.buf<TBox>(tag + ".tbox", n);
   out.wnodes = ctx.buf<WNode>(tag + ".wnodes", out.n_nodes > 0 ? out.n_nodes : 1);
   out.root_box_dev = ctx.buf<float>(tag + ".rootbox", 8);
+  out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
+  out.scene_acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
+}
+
+void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag) {
+  const int n = m.nf;
+  lbvh_layout(ctx, m, out, tag);
+  auto* acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
+  auto* keys = ctx.buf<uint32_t>(tag + ".keys", n);
+  auto* keys2 = ctx.buf<uint32_t>(tag + ".keys2", n);
+  auto* vals = ctx.buf<uint32_t>(tag + ".vals", n);
+  auto* vals2 = ctx.buf<uint32_t>(tag + ".vals2", n);
   auto* prim_parent = ctx.buf<int32_t>(tag + ".pparent", n);
   auto* node_parent = ctx.buf<int32_t>(tag + ".nparent", n);
   auto* flags = ctx.buf<int>(tag + ".flags", n);
