@@ -15,7 +15,7 @@ NVCC ?= nvcc
 CXX ?= g++
 PKG := paper_2605_26137_b200
 ARCH := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Iinclude -Iinclude/eigen_shim \
+NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcompiler -ffp-contract=off -Iinclude -Iinclude/eigen_shim \
            -Xptxas -warn-spills --expt-relaxed-constexpr
 CXXFLAGS := -std=c++20 -O2 -g -ffp-contract=off -fPIC -Iinclude -Iinclude/eigen_shim -Wall -Wextra
 CU_SRCS := $(wildcard $(PKG)/csrc/*.cu)

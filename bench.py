@@ -286,8 +286,19 @@ def bvh_rays(ctx, hi, pair, steps):
     ms_cp = timed(lambda: capi.check(lib.mf_bvh_closest_within_dev(
         h, o.data_ptr(), N_RAYS, max_d, face.data_ptr(), t.data_ptr(), pt.data_ptr(), None)))
     cp_hits = int((face >= 0).sum())
+    # markSurfaceBand's voxel sweep: 256^3 voxel-centre
+    # queries at the sign field's truncation radius, device outputs
+    band_res = 256
+    nb = band_res ** 3
+    labels = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    bdist = torch.empty(nb, dtype=torch.float32, device="cuda")
+    ms_band = timed(lambda: capi.check(lib.mf_surface_band_dev(
+        h, band_res, 1.0, 2, None, labels.data_ptr(), bdist.data_ptr(), None)))
+    band_voxels = int(labels.sum())
     lib.mf_bvh_destroy(h)
-    return {"raycast_rays_per_s": N_RAYS / (ms_ray * 1e-3), "raycast_ms": round(ms_ray, 4), "raycast_hits": ray_hits,
+    return {"surface_band_voxels_per_s": nb / (ms_band * 1e-3), "surface_band_ms": round(ms_band, 4),
+            "surface_band_res": band_res, "surface_band_marked": band_voxels,
+            "raycast_rays_per_s": N_RAYS / (ms_ray * 1e-3), "raycast_ms": round(ms_ray, 4), "raycast_hits": ray_hits,
             "closest_within_per_s": N_RAYS / (ms_cp * 1e-3), "closest_within_ms": round(ms_cp, 4),
             "closest_within_hits": cp_hits, "n": N_RAYS,
             "inputs": "uniform origins in the dense bbox, uniform unit directions (seed 11); "

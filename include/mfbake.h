@@ -186,6 +186,23 @@ int mf_bvh_raycast_first_dev(mf_bvh* bvh, const double* origins_dev, const doubl
                              int64_t n, double tmin, double tmax, int32_t* face_dev,
                              double* t_dev, double* u_dev, double* v_dev);
 
+/* ---- bulk closest-point callers ------------------------ */
+/* markSurfaceBand (signfield/sign_grid.cpp:23-69, sign_grid.h:14-50) over the
+ * mesh `bvh` was built on: grid parameters exactly as the reference derives
+ * them (auto-fit cube with dilate_radius + 3 voxels of margin, or the cube
+ * `domain` = min xyz, max xyz when non-null), then one bounded closest-point
+ * query per voxel centre. Outputs (x fastest, res^3 each): labels 0 = Unknown,
+ * 1 = SurfaceBand (VoxelLabel); distance f32 (truncation where no surface is
+ * within it). grid_out (nullable, 5 f64): origin xyz, voxelSize, truncation.
+ * Errors as the reference: InvalidConfig (resolution < 8, dilate_radius < 0,
+ * resolution too small for the margin), OutOfBounds (mesh not inside the grid
+ * with 2 voxels of margin). */
+int mf_surface_band(mf_bvh* bvh, int resolution, double band_voxels, int dilate_radius, const double* domain,
+                    uint8_t* labels, float* distance, double* grid_out);
+/* Device-pointer outputs (labels_dev, distance_dev). */
+int mf_surface_band_dev(mf_bvh* bvh, int resolution, double band_voxels, int dilate_radius, const double* domain,
+                        uint8_t* labels_dev, float* distance_dev, double* grid_out);
+
 /* raycastFirstBrute / closestPointBrute (bvh.cpp:178-189): O(faces) per
  * query with the same tie rules, one CTA per query on the device. */
 int mf_closest_point_brute(mf_ctx* ctx, const mf_mesh_view* mesh, const double* queries, int64_t n,

@@ -154,6 +154,17 @@ class Port(_Lib):
                                               _ptr(bary)))
         return face, ds, pt, bary
 
+    def surface_band(self, m: TriangleMesh, res: int, band_voxels: float = 1.0, dilate: int = 2,
+                     domain=None, threads: int = 0):
+        n = res ** 3
+        labels, dist, grid = np.zeros(n, np.uint8), np.zeros(n, np.float32), np.zeros(5)
+        dom = None if domain is None else np.ascontiguousarray(domain, dtype=np.float64).reshape(6)
+        v = m.view()
+        self._check(self.fn("surface_band")(ctypes.byref(v), ctypes.c_int(res), ctypes.c_double(band_voxels),
+                                            ctypes.c_int(dilate), _ptr(dom), ctypes.c_int(threads),
+                                            _ptr(labels), _ptr(dist), _ptr(grid)))
+        return labels, dist, grid
+
     def raycast_first(self, m: TriangleMesh, o: np.ndarray, d: np.ndarray, tmin: float = 0.0,
                       tmax: float = float("inf"), brute: bool = False, threads: int = 0):
         o = np.ascontiguousarray(o, dtype=np.float64).reshape(-1, 3)
@@ -247,6 +258,15 @@ class Ref(_Lib):
                                               ctypes.c_double(max_dist), ctypes.c_int(int(brute)),
                                               _ptr(face), _ptr(ds), _ptr(pt), _ptr(bary)))
         return face, ds, pt, bary
+
+    def surface_band(self, m: TriangleMesh, res: int, band_voxels: float = 1.0, dilate: int = 2, domain=None):
+        n = res ** 3
+        labels, dist, grid = np.zeros(n, np.uint8), np.zeros(n, np.float32), np.zeros(5)
+        dom = None if domain is None else np.ascontiguousarray(domain, dtype=np.float64).reshape(6)
+        v = m.view()
+        self._check(self.fn("surface_band")(ctypes.byref(v), ctypes.c_int(res), ctypes.c_double(band_voxels),
+                                            ctypes.c_int(dilate), _ptr(dom), _ptr(labels), _ptr(dist), _ptr(grid)))
+        return labels, dist, grid
 
     def raycast_first(self, m: TriangleMesh, o, d, tmin=0.0, tmax=float("inf"), brute=False):
         o = np.ascontiguousarray(o, dtype=np.float64).reshape(-1, 3)

@@ -1051,3 +1051,90 @@ int orc_raycast_first(const mf_mesh_view* m, const double* o, const double* d, i
   bvh_free(&bvh);
   return 0;
 }
+
+/* ---------------------------------------------------------------- surface band
+ * signfield/sign_grid.cpp:23-69 markSurfaceBand: grid parameters (:24-52),
+ * then closestPointWithin(voxelCenter, truncation) per voxel (:56-66);
+ * voxelCenter = origin + voxelSize * (x + 0.5, y + 0.5, z + 0.5)
+ * (sign_grid.h:30-32); index x-fastest (:27-29). */
+typedef struct {
+  const bvh_t* bvh;
+  int res;
+  double o[3], h, trunc, band;
+  uint8_t* labels;
+  float* dist;
+} band_ctx;
+static void band_range(void* vctx, int64_t lo, int64_t hi) {
+  band_ctx* c = (band_ctx*)vctx;
+  int cap = 256;
+  heap_e* heap = (heap_e*)malloc(sizeof(heap_e) * (size_t)cap);
+  const int64_t r = c->res;
+  for (int64_t i = lo; i < hi; ++i) {
+    const int x = (int)(i % r), y = (int)((i / r) % r), z = (int)(i / (r * r));
+    d3 q = mk3(c->o[0] + c->h * (x + 0.5), c->o[1] + c->h * (y + 0.5), c->o[2] + c->h * (z + 0.5));
+    surf_pt sp = bvh_closest_within(c->bvh, q, c->trunc, &heap, &cap);
+    c->labels[i] = 0;
+    c->dist[i] = (float)c->trunc;
+    if (sp.face >= 0) {
+      const double d = sqrt(sp.dist_sq);
+      c->dist[i] = (float)d;
+      if (d < c->band) c->labels[i] = 1;
+    }
+  }
+  free(heap);
+}
+int orc_surface_band(const mf_mesh_view* m, int res, double band_voxels, int dilate, const double* domain,
+                     int threads, uint8_t* labels, float* dist, double* grid_out) {
+  int rc = validate_mesh(m); /* Bvh(mesh) validates (bvh.cpp:48-50) */
+  if (rc) return rc;
+  if (res < 8) return fail(MF_ERR_INVALID_CONFIG, "InvalidConfig: grid resolution must be >= 8");
+  if (dilate < 0) return fail(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilate radius must be >= 0");
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int v = 0; v < m->n_vertices; ++v)
+    for (int k = 0; k < 3; ++k) {
+      const double p = m->positions[3 * v + k];
+      mn[k] = p < mn[k] ? p : mn[k];
+      mx[k] = mx[k] < p ? p : mx[k];
+    }
+  const int margin = dilate + 3;
+  if (res - 2 * margin < 4)
+    return fail(MF_ERR_INVALID_CONFIG, "InvalidConfig: grid resolution too small for the dilation margin");
+  band_ctx c;
+  double ext[3];
+  if (domain) {
+    for (int k = 0; k < 3; ++k) ext[k] = domain[3 + k] - domain[k];
+  } else {
+    for (int k = 0; k < 3; ++k) ext[k] = mx[k] - mn[k];
+  }
+  double e = ext[0];
+  for (int k = 1; k < 3; ++k)
+    if (ext[k] > e) e = ext[k];
+  if (domain) {
+    c.h = e / res;
+    for (int k = 0; k < 3; ++k) c.o[k] = domain[k];
+  } else {
+    const double usable = res - 2.0 * margin;
+    c.h = e / usable;
+    const double half = 0.5 * res * c.h;
+    for (int k = 0; k < 3; ++k) c.o[k] = (mn[k] + mx[k]) * 0.5 - half;
+  }
+  for (int k = 0; k < 3; ++k)
+    if (mn[k] < c.o[k] + 2 * c.h || mx[k] > c.o[k] + (res - 2.0) * c.h)
+      return fail(MF_ERR_OUT_OF_BOUNDS, "OutOfBounds: mesh does not fit in the grid with 2 voxels of margin");
+  c.trunc = (band_voxels + dilate * sqrt(3.0) + 2.0) * c.h;
+  c.band = band_voxels * c.h;
+  c.res = res;
+  c.labels = labels;
+  c.dist = dist;
+  bvh_t bvh;
+  bvh_build(&bvh, m);
+  c.bvh = &bvh;
+  parallel_for((int64_t)res * res * res, 4096, threads, band_range, &c);
+  bvh_free(&bvh);
+  if (grid_out) {
+    for (int k = 0; k < 3; ++k) grid_out[k] = c.o[k];
+    grid_out[3] = c.h;
+    grid_out[4] = c.trunc;
+  }
+  return 0;
+}

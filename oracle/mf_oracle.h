@@ -58,6 +58,11 @@ int orc_raycast_first(const mf_mesh_view* m, const double* o, const double* d, i
                       double tmin, double tmax, int brute, int threads, int32_t* face, double* t,
                       double* u, double* v);
 
+/* signfield/sign_grid.cpp:23-69 markSurfaceBand: labels (0 Unknown, 1 SurfaceBand) and
+ * f32 distances, res^3 x-fastest; grid_out = origin xyz, voxelSize, truncation. */
+int orc_surface_band(const mf_mesh_view* m, int res, double band_voxels, int dilate, const double* domain,
+                     int threads, uint8_t* labels, float* dist, double* grid_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,7 @@
 #include "meshforge/core/mesh.h"
 #include "meshforge/core/parallel.h"
 #include "meshforge/metrics/metrics.h"
+#include "meshforge/signfield/sign_grid.h"
 #include "meshforge/spatial/bvh.h"
 #include "meshforge/spatial/tri_geom.h"
 #include "mfbake.h"
@@ -334,6 +335,30 @@ int ref_sampled_counters(const mf_mesh_view* lo, const mf_mesh_view* hi, int res
     counters[2] = static_cast<double>(idx.size());
     counters[3] = sp / ns;
     counters[4] = st / ns;
+  });
+}
+
+// markSurfaceBand (src/signfield/sign_grid.cpp:23-69), as the reference runs it.
+int ref_surface_band(const mf_mesh_view* mesh, int res, double band_voxels, int dilate, const double* domain,
+                     uint8_t* labels, float* dist, double* grid_out) {
+  return guarded([&] {
+    const TriangleMesh m = toMesh(mesh);
+    const Bvh bvh(m);
+    GridParams p;
+    p.resolution = res;
+    p.bandVoxels = band_voxels;
+    p.dilateRadius = dilate;
+    if (domain) p.domain = Aabb3d{{domain[0], domain[1], domain[2]}, {domain[3], domain[4], domain[5]}};
+    const SignGrid g = markSurfaceBand(m, bvh, p);
+    for (size_t i = 0; i < g.cells(); ++i) {
+      labels[i] = static_cast<uint8_t>(g.labels[i]);
+      dist[i] = g.distance[i];
+    }
+    if (grid_out) {
+      for (int k = 0; k < 3; ++k) grid_out[k] = g.origin[k];
+      grid_out[3] = g.voxelSize;
+      grid_out[4] = g.truncation;
+    }
   });
 }
 

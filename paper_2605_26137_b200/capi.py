@@ -87,6 +87,8 @@ SIGNATURES = [
     ("mf_bvh_closest_within_dev", _I, [_VP, _VP, _I64, _D, _VP, _VP, _VP, _VP]),
     ("mf_bvh_raycast_first", _I, [_VP, _VP, _VP, _I64, _D, _D, _VP, _VP, _VP, _VP]),
     ("mf_bvh_raycast_first_dev", _I, [_VP, _VP, _VP, _I64, _D, _D, _VP, _VP, _VP, _VP]),
+    ("mf_surface_band", _I, [_VP, _I, _D, _I, _VP, _VP, _VP, _VP]),
+    ("mf_surface_band_dev", _I, [_VP, _I, _D, _I, _VP, _VP, _VP, _VP]),
     ("mf_closest_point_brute", _I, [_VP, _MV, _VP, _I64, _VP, _VP, _VP, _VP]),
     ("mf_raycast_first_brute", _I, [_VP, _MV, _VP, _VP, _I64, _D, _D, _VP, _VP, _VP, _VP]),
     ("mf_wedge_tangents", _I, [_VP, _MV, _VP]),

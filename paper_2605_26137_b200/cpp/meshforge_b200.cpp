@@ -17,6 +17,7 @@
 #include "meshforge/bake/tangent.h"
 #include "meshforge/core/error.h"
 #include "meshforge/core/mesh.h"
+#include "meshforge/signfield/sign_grid.h"
 #include "meshforge/spatial/bvh.h"
 #include "mfbake.h"
 
@@ -281,6 +282,36 @@ SurfacePoint closestPointBrute(const TriangleMesh& mesh, const Eigen::Vector3d& 
   check(mf_closest_point_brute(context(), &v, query.data(), 1, &sp.face, &sp.distanceSquared, sp.point.data(),
                                sp.barycentric.data()));
   return sp;
+}
+
+// ------------------------------------------------------------------ sign grid
+SignGrid markSurfaceBand(const TriangleMesh& mesh, const Bvh& bvh, const GridParams& params) {
+  (void)mesh;  // the device derives bounds(mesh) from the tree's own copy of it
+  SignGrid g;
+  const int res = params.resolution;
+  double dom[6];
+  if (params.domain) {
+    for (int k = 0; k < 3; ++k) {
+      dom[k] = params.domain->min[k];
+      dom[3 + k] = params.domain->max[k];
+    }
+  }
+  std::vector<std::uint8_t> labels;
+  double grid[5];
+  // (invalid resolutions get 1-element buffers so the ABI reports the
+  // reference's InvalidConfig rather than a null-argument error)
+  const std::size_t cells = res >= 8 ? static_cast<std::size_t>(res) * res * res : 1;
+  labels.resize(cells);
+  g.distance.resize(cells);
+  check(mf_surface_band(bvh.handle()->bvh, res, params.bandVoxels, params.dilateRadius,
+                        params.domain ? dom : nullptr, labels.data(), g.distance.data(), grid));
+  g.res = res;
+  g.origin = Eigen::Vector3d(grid[0], grid[1], grid[2]);
+  g.voxelSize = grid[3];
+  g.truncation = grid[4];
+  g.labels.resize(labels.size());
+  for (std::size_t i = 0; i < labels.size(); ++i) g.labels[i] = static_cast<VoxelLabel>(labels[i]);
+  return g;
 }
 
 }  // namespace meshforge

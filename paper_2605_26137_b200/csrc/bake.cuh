@@ -263,6 +263,11 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
 
 void closest_within(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* q, int64_t n,
                     double max_dist, int32_t* face, double* dist_sq, double* point, double* bary);
+// bounds(mesh) (core/mesh.cpp:12-16) into out6 = min xyz, max xyz (synchronises).
+void vertex_bounds(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out6);
+// markSurfaceBand's voxel sweep (signfield/sign_grid.cpp:56-66) over a res^3 grid.
+void surface_band(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, int res, const double origin[3], double h,
+                  double truncation, double band_world, uint8_t* labels, float* dist);
 void raycast_first(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* o, const double* d,
                    int64_t n, double tmin, double tmax, int32_t* face, double* t, double* u,
                    double* v);

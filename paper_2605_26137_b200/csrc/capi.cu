@@ -1391,3 +1391,99 @@ int mf_vertex_normals(mf_ctx* ctx, const mf_mesh_view* mesh, double* normals) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- surface band
+namespace {
+// sign_grid.cpp:23-54 — the grid parameters, in the reference's expression
+// order (host f64, no contraction: -ffp-contract is irrelevant here, nvcc's
+// host compiler sees plain mul/add statements).
+struct BandGrid {
+  double origin[3], h, truncation, band_world;
+};
+BandGrid band_grid(Ctx& c, const mf_bvh* bvh, int res, double band_voxels, int dilate, const double* domain) {
+  if (res < 8) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: grid resolution must be >= 8");
+  if (dilate < 0) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilate radius must be >= 0");
+  double box[6];
+  vertex_bounds(c, c.stream, bvh->mesh->m, box);  // bounds(mesh), mesh.cpp:12-16
+  const int margin = dilate + 3;
+  if (res - 2 * margin < 4)
+    throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: grid resolution too small for the dilation margin");
+  BandGrid g;
+  auto max_coeff = [](const double e[3]) {  // Eigen maxCoeff: first maximum
+    double m = e[0];
+    for (int k = 1; k < 3; ++k)
+      if (e[k] > m) m = e[k];
+    return m;
+  };
+  if (domain) {
+    const double ext[3] = {domain[3] - domain[0], domain[4] - domain[1], domain[5] - domain[2]};
+    g.h = max_coeff(ext) / res;
+    for (int k = 0; k < 3; ++k) g.origin[k] = domain[k];
+  } else {
+    const double usable = res - 2.0 * margin;
+    const double ext[3] = {box[3] - box[0], box[4] - box[1], box[5] - box[2]};
+    g.h = max_coeff(ext) / usable;
+    const double half = 0.5 * res * g.h;
+    for (int k = 0; k < 3; ++k) {
+      const double center = (box[k] + box[3 + k]) * 0.5;  // aabb.h:25
+      g.origin[k] = center - half;
+    }
+  }
+  bool out = false;
+  for (int k = 0; k < 3; ++k) {
+    const double gmin = g.origin[k] + 2 * g.h;
+    const double gmax = g.origin[k] + (res - 2.0) * g.h;
+    if (box[k] < gmin || box[3 + k] > gmax) out = true;
+  }
+  if (out) throw ApiError(MF_ERR_OUT_OF_BOUNDS, "OutOfBounds: mesh does not fit in the grid with 2 voxels of margin");
+  g.truncation = (band_voxels + dilate * std::sqrt(3.0) + 2.0) * g.h;
+  g.band_world = band_voxels * g.h;
+  return g;
+}
+}  // namespace
+
+extern "C" {
+int mf_surface_band_dev(mf_bvh* bvh, int resolution, double band_voxels, int dilate_radius, const double* domain,
+                        uint8_t* labels_dev, float* distance_dev, double* grid_out) {
+  if (!bvh || !labels_dev || !distance_dev) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(bvh->ctx, [&]() -> int {
+    Ctx& c = bvh->ctx->c;
+    const BandGrid g = band_grid(c, bvh, resolution, band_voxels, dilate_radius, domain);
+    surface_band(c, c.stream, bvh->bvh, resolution, g.origin, g.h, g.truncation, g.band_world, labels_dev,
+                 distance_dev);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (grid_out) {
+      grid_out[0] = g.origin[0];
+      grid_out[1] = g.origin[1];
+      grid_out[2] = g.origin[2];
+      grid_out[3] = g.h;
+      grid_out[4] = g.truncation;
+    }
+    return MF_OK;
+  });
+}
+
+int mf_surface_band(mf_bvh* bvh, int resolution, double band_voxels, int dilate_radius, const double* domain,
+                    uint8_t* labels, float* distance, double* grid_out) {
+  if (!bvh || !labels || !distance) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(bvh->ctx, [&]() -> int {
+    Ctx& c = bvh->ctx->c;
+    const BandGrid g = band_grid(c, bvh, resolution, band_voxels, dilate_radius, domain);
+    const int64_t n = static_cast<int64_t>(resolution) * resolution * resolution;
+    uint8_t* dl = c.buf<uint8_t>("band.labels", n);
+    float* dd = c.buf<float>("band.dist", n);
+    surface_band(c, c.stream, bvh->bvh, resolution, g.origin, g.h, g.truncation, g.band_world, dl, dd);
+    MFB_CUDA_TRY(cudaMemcpyAsync(labels, dl, n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(distance, dd, sizeof(float) * n, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (grid_out) {
+      grid_out[0] = g.origin[0];
+      grid_out[1] = g.origin[1];
+      grid_out[2] = g.origin[2];
+      grid_out[3] = g.h;
+      grid_out[4] = g.truncation;
+    }
+    return MF_OK;
+  });
+}
+}  // extern "C"

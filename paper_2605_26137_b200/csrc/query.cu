@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "bake.cuh"
@@ -24,6 +25,10 @@ namespace {
 __device__ __forceinline__ double from_ordered_dev(unsigned long long b) {
   b = (b & 0x8000000000000000ull) ? (b & ~0x8000000000000000ull) : ~b;
   return __longlong_as_double(static_cast<long long>(b));
+}
+__device__ __forceinline__ unsigned long long ordered_bits_dev(double v) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
 }
 
 // Upper bound (as float) on the squared distance any face that can still win
@@ -1455,6 +1460,125 @@ __global__ void __launch_bounds__(256) k_raycast_brute(const double* __restrict_
   }
 }
 
+
+
+// True when some leaf (range) box of the tree has a fp32 lower-bound distance
+// to the query box [qlo, qhi] of at most `bnd` (depth-first, stops at the
+// first such leaf).
+__device__ __forceinline__ bool any_leaf_within(const BNode* __restrict__ nodes, int32_t root, float3 qlo,
+                                                float3 qhi, float bnd) {
+  if (root < 0) return true;
+  int32_t st[kStackMax];
+  int sp = 0;
+  int32_t ref = root;
+  for (;;) {
+    const float4* np = reinterpret_cast<const float4*>(nodes + ref);
+    const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
+    const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
+    const bool hL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qlo, qhi) <= bnd;
+    const bool hR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qlo, qhi) <= bnd;
+    if ((hL && d.x < 0) || (hR && d.y < 0)) return true;
+    if (hL && hR) {
+      st[sp++] = d.y;
+      ref = d.x;
+    } else if (hL || hR) {
+      ref = hL ? d.x : d.y;
+    } else {
+      if (sp == 0) return false;
+      ref = st[--sp];
+    }
+  }
+}
+// ---------------------------------------------------------------- surface band
+// markSurfaceBand's voxel sweep (signfield/sign_grid.cpp:56-66): per voxel,
+// Bvh::closestPointWithin(voxelCenter, truncation); distance = sqrt(distSq)
+// stored as f32 and SurfaceBand (1) where it is below bandWorld, else the
+// voxel keeps (Unknown, f32(truncation)). voxelCenter (sign_grid.h:30-32) is
+// origin + voxelSize * (x + 0.5, ...), component by component, no FMA.
+// Threads are mapped to 4x4x2 voxel bricks (one brick per warp) so a warp's
+// queries are spatial neighbours; storage stays x-fastest.
+__global__ void __launch_bounds__(128) k_surface_band(const BNode* __restrict__ nodes, const BTri* __restrict__ tris,
+                                                      int32_t root, const unsigned long long* __restrict__ scene_acc,
+                                                      int res, double ox, double oy, double oz, double h,
+                                                      double truncation, double band_world,
+                                                      uint8_t* __restrict__ labels, float* __restrict__ dist) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int bx = (res + 3) >> 2, by = (res + 3) >> 2, bz = (res + 1) >> 1;
+  const int64_t brick = t >> 5;
+  const int lane = static_cast<int>(t & 31);
+  if (brick >= static_cast<int64_t>(bx) * by * bz) return;
+  const int kx = static_cast<int>(brick % bx);
+  const int ky = static_cast<int>((brick / bx) % by);
+  const int kz = static_cast<int>(brick / (static_cast<int64_t>(bx) * by));
+  const int x = kx * 4 + (lane & 3), y = ky * 4 + ((lane >> 2) & 3), z = kz * 2 + (lane >> 4);
+  // Brick cull (warp-uniform): if no leaf box of the tree lies within the
+  // truncation of the box spanning the brick's voxel centres, no voxel of
+  // the brick can find a surface point (a leaf box's distance bounds its
+  // triangles' from below), so every voxel keeps (Unknown, truncation).
+  const double M0 = from_ordered_dev(scene_acc[6]);
+  {
+    const int x1 = min(kx * 4 + 3, res - 1), y1 = min(ky * 4 + 3, res - 1), z1 = min(kz * 2 + 1, res - 1);
+    const double cx0 = ox + h * (kx * 4 + 0.5), cy0 = oy + h * (ky * 4 + 0.5), cz0 = oz + h * (kz * 2 + 0.5);
+    const double cx1 = ox + h * (x1 + 0.5), cy1 = oy + h * (y1 + 0.5), cz1 = oz + h * (z1 + 0.5);
+    const float3 blo = make_float3(__double2float_rd(cx0), __double2float_rd(cy0), __double2float_rd(cz0));
+    const float3 bhi = make_float3(__double2float_ru(cx1), __double2float_ru(cy1), __double2float_ru(cz1));
+    const double Mb = fmax(M0, fmax(fmax(fabs(cx0), fabs(cx1)), fmax(fmax(fabs(cy0), fabs(cy1)),
+                                                                     fmax(fabs(cz0), fabs(cz1)))));
+    const double t2 = isinf(truncation) ? truncation : truncation * truncation;
+    if (!any_leaf_within(nodes, root, blo, bhi, prune_bound(t2, Mb * 0x1p-32))) {
+      if (x < res && y < res && z < res) {
+        const int64_t i = x + static_cast<int64_t>(res) * (y + static_cast<int64_t>(res) * z);
+        labels[i] = 0;
+        dist[i] = static_cast<float>(truncation);
+      }
+      return;
+    }
+  }
+  if (x >= res || y >= res || z >= res) return;
+  const d3 p = mk3(ox + h * (x + 0.5), oy + h * (y + 0.5), oz + h * (z + 0.5));
+  const float3 lo = make_float3(__double2float_rd(p.x), __double2float_rd(p.y), __double2float_rd(p.z));
+  const float3 hi = make_float3(__double2float_ru(p.x), __double2float_ru(p.y), __double2float_ru(p.z));
+  const double M = fmax(M0, fmax(fabs(p.x), fmax(fabs(p.y), fabs(p.z))));
+  Best best;
+  best.d = isinf(truncation) ? truncation : truncation * truncation;  // bvh.cpp:153-154
+  best.face = -1;
+  best.bary = mk3(0.0, 0.0, 0.0);
+  traverse_closest<false>(nodes, tris, root, p, lo, hi, M * 0x1p-32, best);
+  const int64_t i = x + static_cast<int64_t>(res) * (y + static_cast<int64_t>(res) * z);  // sign_grid.h:27-29
+  uint8_t lab = 0;
+  float dv = static_cast<float>(truncation);
+  if (best.face >= 0) {
+    const double d = sqrt(best.d);  // SurfacePoint::distance (bvh.h:24)
+    dv = static_cast<float>(d);
+    if (d < band_world) lab = 1;
+  }
+  labels[i] = lab;
+  dist[i] = dv;
+}
+
+// Exact vertex bounds of a mesh (core/mesh.cpp:12-16): acc[0..2] min, acc[3..5] max (ordered bits).
+__global__ void k_vertex_bounds(const double* __restrict__ pos, int nv, unsigned long long* acc) {
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double c = pos[3 * v + k];
+      mn[k] = c < mn[k] ? c : mn[k];
+      mx[k] = mx[k] < c ? c : mx[k];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    for (int off = 16; off > 0; off >>= 1) {
+      mn[k] = fmin(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], off));
+      mx[k] = fmax(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], off));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(&acc[k], ordered_bits_dev(mn[k]));
+      atomicMax(&acc[3 + k], ordered_bits_dev(mx[k]));
+    }
+  }
+}
 }  // namespace
 
 // Resident 128-thread blocks per SM of `kern` (>= 1); callers cache it in a
@@ -1630,6 +1754,43 @@ void raycast_brute(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* o, 
                    double tmin, double tmax, int32_t* face, double* t, double* u, double* v) {
   if (n <= 0) return;
   k_raycast_brute<<<static_cast<unsigned>(n), 256, 0, s>>>(m.pos, m.faces, m.nf, o, d, n, tmin, tmax, face, t, u, v);
+  ctx.count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+
+void vertex_bounds(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out6) {
+  auto* acc = ctx.buf<unsigned long long>("vb.acc", 6);
+  MFB_CUDA_TRY(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(acc + 3, 0x00, 3 * sizeof(unsigned long long), s));
+  if (m.nv > 0) {
+    k_vertex_bounds<<<std::min(div_up(m.nv, 256), kNumSMs * 4), 256, 0, s>>>(m.pos, m.nv, acc);
+    ctx.count_launch();
+    MFB_CUDA_TRY(cudaGetLastError());
+  }
+  unsigned long long h[6];
+  MFB_CUDA_TRY(cudaMemcpyAsync(h, acc, sizeof(h), cudaMemcpyDeviceToHost, s));
+  MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int k = 0; k < 6; ++k) {
+    unsigned long long b = h[k];
+    b = (b & 0x8000000000000000ull) ? (b & ~0x8000000000000000ull) : ~b;
+    std::memcpy(&out6[k], &b, 8);
+  }
+  if (m.nv == 0) {
+    for (int k = 0; k < 3; ++k) {
+      out6[k] = INFINITY;
+      out6[3 + k] = -INFINITY;
+    }
+  }
+}
+
+void surface_band(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, int res, const double origin[3], double h,
+                  double truncation, double band_world, uint8_t* labels, float* dist) {
+  const int64_t bricks = static_cast<int64_t>((res + 3) / 4) * ((res + 3) / 4) * ((res + 1) / 2);
+  const int64_t threads = bricks * 32;
+  k_surface_band<<<static_cast<unsigned>(div_up(threads, 128)), 128, 0, s>>>(
+      bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, res, origin[0], origin[1], origin[2], h, truncation,
+      band_world, labels, dist);
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
 }

@@ -193,6 +193,20 @@ class Bvh:
                                    t_min, t_max)
         return RayHit(int(f[0]), float(t[0]), float(u[0]), float(v[0]))
 
+    def surface_band(self, resolution: int = 128, band_voxels: float = 1.0, dilate_radius: int = 2,
+                     domain=None):
+        """markSurfaceBand (signfield/sign_grid.cpp:23-69) on this tree's mesh:
+        (labels u8 res^3 with 0 = Unknown / 1 = SurfaceBand, distance f32 res^3,
+        grid dict), x fastest as SignGrid::index (sign_grid.h:27-29)."""
+        n = resolution ** 3
+        labels = np.zeros(n, np.uint8)
+        dist = np.zeros(n, np.float32)
+        grid = np.zeros(5)
+        dom = None if domain is None else np.ascontiguousarray(domain, dtype=np.float64).reshape(6)
+        check(self.ctx.lib.mf_surface_band(self.h, int(resolution), float(band_voxels), int(dilate_radius),
+                                           _p(dom), _p(labels), _p(dist), _p(grid)))
+        return labels, dist, dict(origin=grid[:3].copy(), voxel_size=float(grid[3]), truncation=float(grid[4]))
+
     def info(self):
         nodes, leaves, depth = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         check(self.ctx.lib.mf_bvh_info(self.h, ctypes.byref(nodes), ctypes.byref(leaves), ctypes.byref(depth)))

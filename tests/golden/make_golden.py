@@ -99,8 +99,30 @@ def kat_case(ref):
     return out
 
 
+# markSurfaceBand cases (signfield/sign_grid.cpp:23-69): (fixture args, res, bandVoxels, dilateRadius, domain)
+BAND_CASES = {
+    "ico4": ((0, 4, 0, 0, 0.5), 64, 1.0, 2, None),
+    "plane": ((4, 8, 8, 0, 0.5), 48, 1.0, 2, None),
+    "torus": ((5, 24, 12, 0, 0.5), 40, 1.5, 1, None),
+    "domain": ((0, 3, 0, 0, 0.4), 32, 1.0, 2, (-0.6, -0.6, -0.6, 0.6, 0.6, 0.6)),
+}
+
+
+def band_case(ref):
+    out = {}
+    for name, (fa, res, band, dil, dom) in BAND_CASES.items():
+        m = ref.fixture(*fa)
+        labels, dist, grid = ref.surface_band(m, res, band, dil, dom)
+        out.update({f"{name}_pos": m.positions, f"{name}_faces": m.faces, f"{name}_labels": labels,
+                    f"{name}_dist": dist, f"{name}_grid": grid,
+                    f"{name}_params": np.array([res, band, dil], np.float64),
+                    f"{name}_domain": np.array(dom if dom else [np.nan] * 6, np.float64)})
+    return out
+
+
 def main():
     ref = bindings.ref()
+    np.savez_compressed(os.path.join(HERE, "band.npz"), **band_case(ref))
     np.savez_compressed(os.path.join(HERE, "kats.npz"), **kat_case(ref))
     for name in BAKE_CASES:
         np.savez_compressed(os.path.join(HERE, f"bake_{name}.npz"), **bake_case(ref, name))

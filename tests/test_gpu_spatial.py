@@ -148,3 +148,40 @@ def test_bvh_rejects_bad_input(gpu_ctx):
         mf.Bvh(TriangleMesh([[0, 0, 0]], np.zeros((0, 3))))
     with pytest.raises(mf.MeshforgeError):
         mf.Bvh(TriangleMesh([[0, 0, 0], [1, 0, 0], [0, np.nan, 0]], [[0, 1, 2]]))
+
+
+@pytest.mark.parametrize("case", ["ico4", "plane", "torus", "domain"])
+def test_surface_band_matches_reference_golden(gpu_ctx, case):
+    """markSurfaceBand's voxel sweep on the device (mf_surface_band): labels,
+    f32 distances and the grid parameters bit-exact vs the reference build."""
+    d = np.load(os.path.join(GOLDEN, "band.npz"))
+    mesh = TriangleMesh(d[f"{case}_pos"], d[f"{case}_faces"])
+    res, band, dil = d[f"{case}_params"]
+    dom = d[f"{case}_domain"]
+    labels, dist, grid = mf.Bvh(mesh).surface_band(int(res), float(band), int(dil),
+                                                   None if np.isnan(dom).any() else dom)
+    assert np.array_equal(labels, d[f"{case}_labels"])
+    assert np.array_equal(dist.view(np.uint32), d[f"{case}_dist"].view(np.uint32))
+    assert np.array_equal(np.r_[grid["origin"], grid["voxel_size"], grid["truncation"]], d[f"{case}_grid"])
+
+
+def test_surface_band_dense_blob_matches_port(gpu_ctx, port):
+    """A config-A-sized dense mesh (200k faces) on a 96^3 grid vs the oracle."""
+    pair = fx.config_pair("A")
+    m = pair.dense
+    labels, dist, grid = mf.Bvh(m).surface_band(96, 1.0, 2)
+    pl, pd, pg = port.surface_band(m, 96, 1.0, 2)
+    assert np.array_equal(labels, pl)
+    assert np.array_equal(dist.view(np.uint32), pd.view(np.uint32))
+    assert labels.sum() > 1000
+
+
+def test_surface_band_errors(gpu_ctx):
+    from paper_2605_26137_b200.capi import MeshforgeError
+    d = np.load(os.path.join(GOLDEN, "band.npz"))
+    bvh = mf.Bvh(TriangleMesh(d["domain_pos"], d["domain_faces"]))
+    for args, code in [((7, 1.0, 2, None), 12), ((32, 1.0, -1, None), 12), ((12, 1.0, 2, None), 12),
+                       ((32, 1.0, 2, (0, 0, 0, 1, 1, 1)), 3)]:
+        with pytest.raises(MeshforgeError) as e:
+            bvh.surface_band(*args)
+        assert e.value.status == code

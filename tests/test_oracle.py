@@ -178,3 +178,35 @@ def test_reference_spatial_suite_passes_on_its_own_build(ref):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "14/14 test cases passed" in r.stdout
+
+
+BAND_CASES = ("ico4", "plane", "torus", "domain")
+
+
+def band_inputs(d, name):
+    mesh = TriangleMesh(d[f"{name}_pos"], d[f"{name}_faces"])
+    res, band, dil = d[f"{name}_params"]
+    dom = d[f"{name}_domain"]
+    return mesh, int(res), float(band), int(dil), (None if np.isnan(dom).any() else dom)
+
+
+@pytest.mark.parametrize("case", BAND_CASES)
+def test_port_matches_reference_golden_surface_band(port, case):
+    """markSurfaceBand (signfield/sign_grid.cpp:23-69): labels, f32 distances
+    and grid parameters bit-for-bit against the reference's own build."""
+    d = load("band.npz")
+    mesh, res, band, dil, dom = band_inputs(d, case)
+    labels, dist, grid = port.surface_band(mesh, res, band, dil, dom)
+    assert np.array_equal(labels, d[f"{case}_labels"])
+    assert np.array_equal(u32(dist), u32(d[f"{case}_dist"]))
+    assert np.array_equal(grid, d[f"{case}_grid"])
+
+
+def test_port_surface_band_errors(port):
+    from oracle.bindings import OracleError
+    ico = TriangleMesh(load("band.npz")["domain_pos"], load("band.npz")["domain_faces"])
+    for args, code in [((7, 1.0, 2, None), 12), ((32, 1.0, -1, None), 12), ((12, 1.0, 2, None), 12),
+                       ((32, 1.0, 2, (0, 0, 0, 1, 1, 1)), 3)]:
+        with pytest.raises(OracleError) as e:
+            port.surface_band(ico, *args)
+        assert e.value.code == code
