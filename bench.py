@@ -296,7 +296,19 @@ def bvh_rays(ctx, hi, pair, steps):
         h, band_res, 1.0, 2, None, labels.data_ptr(), bdist.data_ptr(), None)))
     band_voxels = int(labels.sum())
     lib.mf_bvh_destroy(h)
-    return {"surface_band_voxels_per_s": nb / (ms_band * 1e-3), "surface_band_ms": round(ms_band, 4),
+    # castVisibility at the paper's setting (PAPER "BVH ... 512
+    # viewpoints"): 512 fibonacci ortho views x 1024^2 pixel rays against the
+    # dense mesh, whole host call (upload, centring, LBVH, rays, hit counts)
+    vis_views, vis_res = 512, 1024
+    hits = np.zeros(pair.dense.face_count(), np.int64)
+    mv = pair.dense.view()
+    ms_vis = timed(lambda: capi.check(lib.mf_cast_visibility(ctx.h, ctypes.byref(mv), vis_views, vis_res,
+                                                             hits.ctypes.data_as(ctypes.c_void_p), None)))
+    vis_rays = vis_views * vis_res * vis_res
+    return {"visibility_rays_per_s": vis_rays / (ms_vis * 1e-3), "visibility_ms": round(ms_vis, 3),
+            "visibility_views": vis_views, "visibility_res": vis_res,
+            "visibility_visible_faces": int((hits > 0).sum()),
+            "surface_band_voxels_per_s": nb / (ms_band * 1e-3), "surface_band_ms": round(ms_band, 4),
             "surface_band_res": band_res, "surface_band_marked": band_voxels,
             "raycast_rays_per_s": N_RAYS / (ms_ray * 1e-3), "raycast_ms": round(ms_ray, 4), "raycast_hits": ray_hits,
             "closest_within_per_s": N_RAYS / (ms_cp * 1e-3), "closest_within_ms": round(ms_cp, 4),

@@ -203,6 +203,26 @@ int mf_surface_band(mf_bvh* bvh, int resolution, double band_voxels, int dilate_
 int mf_surface_band_dev(mf_bvh* bvh, int resolution, double band_voxels, int dilate_radius, const double* domain,
                         uint8_t* labels_dev, float* distance_dev, double* grid_out);
 
+/* ---- ortho ray-cast views ------------------------------ */
+/* fibonacciCameras (render/camera.cpp:38-55): count x 7 f64 per camera =
+ * direction xyz, up xyz, halfExtent. Host-only helper (no device). */
+int mf_fibonacci_cameras(int count, double half_extent, double* cameras);
+/* renderView (render/raster.cpp:12-102) for n_views cameras (n x 7 as above)
+ * at resolution^2 pixels each, one pixel ray per thread through the LBVH of
+ * `mesh` (built per call). Per view, row-major: face i32 (-1 background),
+ * depth f32 (+inf background), position f32x3, normal f32x3 (interpolated
+ * `vertex_normals`, V x 3 f64; zero when null). Any output may be null. */
+int mf_render_views(mf_ctx* ctx, const mf_mesh_view* mesh, const double* cameras, int n_views, int resolution,
+                    const double* vertex_normals, int32_t* face, float* depth, float* position, float* normal);
+/* castVisibility (visibility/visibility.cpp:13-59): the mesh centred on its
+ * bounds, `viewpoints` fibonacci cameras of half extent 1.04 x its bounding
+ * radius, resolution^2 pixel rays each; hits[f] = pixels face f won over all
+ * views, state[f] = FaceVisibility (0 Hidden, 1 Visible). state may be null.
+ * Errors: EmptyMesh / InvalidGeometry (validateMesh), InvalidConfig
+ * (viewpoints or resolution <= 0). */
+int mf_cast_visibility(mf_ctx* ctx, const mf_mesh_view* mesh, int viewpoints, int resolution, int64_t* hits,
+                       uint8_t* state);
+
 /* raycastFirstBrute / closestPointBrute (bvh.cpp:178-189): O(faces) per
  * query with the same tie rules, one CTA per query on the device. */
 int mf_closest_point_brute(mf_ctx* ctx, const mf_mesh_view* mesh, const double* queries, int64_t n,

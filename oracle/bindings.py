@@ -154,6 +154,31 @@ class Port(_Lib):
                                               _ptr(bary)))
         return face, ds, pt, bary
 
+    def fibonacci_cameras(self, count: int, half_extent: float, res: int = 0) -> np.ndarray:
+        cams = np.zeros((count, 7))
+        self.fn("fibonacci_cameras")(ctypes.c_int(count), ctypes.c_double(half_extent), _ptr(cams))
+        return cams
+
+    def render_views(self, m: TriangleMesh, cams: np.ndarray, res: int, vn=None):
+        cams = np.ascontiguousarray(cams, dtype=np.float64).reshape(-1, 7)
+        nvw = cams.shape[0]
+        face = np.zeros((nvw, res, res), np.int32)
+        depth = np.zeros((nvw, res, res), np.float32)
+        pos = np.zeros((nvw, res, res, 3), np.float32)
+        nrm = np.zeros((nvw, res, res, 3), np.float32)
+        vn = None if vn is None else np.ascontiguousarray(vn, dtype=np.float64)
+        v = m.view()
+        self._check(self.fn("render_views")(ctypes.byref(v), _ptr(cams), ctypes.c_int(nvw), ctypes.c_int(res),
+                                            _ptr(vn), _ptr(face), _ptr(depth), _ptr(pos), _ptr(nrm)))
+        return face, depth, pos, nrm
+
+    def cast_visibility(self, m: TriangleMesh, viewpoints: int, res: int) -> np.ndarray:
+        hits = np.zeros(m.face_count(), np.int64)
+        v = m.view()
+        self._check(self.fn("cast_visibility")(ctypes.byref(v), ctypes.c_int(viewpoints), ctypes.c_int(res),
+                                               _ptr(hits)))
+        return hits
+
     def surface_band(self, m: TriangleMesh, res: int, band_voxels: float = 1.0, dilate: int = 2,
                      domain=None, threads: int = 0):
         n = res ** 3
@@ -258,6 +283,32 @@ class Ref(_Lib):
                                               ctypes.c_double(max_dist), ctypes.c_int(int(brute)),
                                               _ptr(face), _ptr(ds), _ptr(pt), _ptr(bary)))
         return face, ds, pt, bary
+
+    def fibonacci_cameras(self, count: int, half_extent: float, res: int = 0) -> np.ndarray:
+        cams = np.zeros((count, 7))
+        self.fn("fibonacci_cameras")(ctypes.c_int(count), ctypes.c_int(res), ctypes.c_double(half_extent),
+                                     _ptr(cams))
+        return cams
+
+    def render_views(self, m: TriangleMesh, cams: np.ndarray, res: int, vn=None):
+        cams = np.ascontiguousarray(cams, dtype=np.float64).reshape(-1, 7)
+        nvw = cams.shape[0]
+        face = np.zeros((nvw, res, res), np.int32)
+        depth = np.zeros((nvw, res, res), np.float32)
+        pos = np.zeros((nvw, res, res, 3), np.float32)
+        nrm = np.zeros((nvw, res, res, 3), np.float32)
+        vn = None if vn is None else np.ascontiguousarray(vn, dtype=np.float64)
+        v = m.view()
+        self._check(self.fn("render_views")(ctypes.byref(v), _ptr(cams), ctypes.c_int(nvw), ctypes.c_int(res),
+                                            _ptr(vn), _ptr(face), _ptr(depth), _ptr(pos), _ptr(nrm)))
+        return face, depth, pos, nrm
+
+    def cast_visibility(self, m: TriangleMesh, viewpoints: int, res: int) -> np.ndarray:
+        hits = np.zeros(m.face_count(), np.int64)
+        v = m.view()
+        self._check(self.fn("cast_visibility")(ctypes.byref(v), ctypes.c_int(viewpoints), ctypes.c_int(res),
+                                               _ptr(hits)))
+        return hits
 
     def surface_band(self, m: TriangleMesh, res: int, band_voxels: float = 1.0, dilate: int = 2, domain=None):
         n = res ** 3

@@ -1138,3 +1138,157 @@ int orc_surface_band(const mf_mesh_view* m, int res, double band_voxels, int dil
   }
   return 0;
 }
+
+/* ---------------------------------------------------------------- ortho views
+ * render/camera.cpp:38-55 fibonacciCameras -> cams7 (direction, up, halfExtent). */
+void orc_fibonacci_cameras(int count, double half_extent, double* cams7) {
+  const double golden = M_PI * (3.0 - sqrt(5.0));
+  for (int i = 0; i < count; ++i) {
+    const double z = 1.0 - 2.0 * (i + 0.5) / count;
+    const double r = sqrt(fmax(0.0, 1.0 - z * z));
+    const double a = golden * i;
+    const d3 dir = mk3(-(r * cos(a)), -(r * sin(a)), -z);
+    const d3 ref = fabs(z) < 0.9 ? mk3(0, 0, 1) : mk3(0, 1, 0);
+    d3 up = cross3(dir, ref);
+    const double z2 = sqn3(up);
+    if (z2 > 0.0) up = div3(up, sqrt(z2));
+    double* c = cams7 + 7 * i;
+    for (int k = 0; k < 3; ++k) {
+      c[k] = dir.v[k];
+      c[3 + k] = up.v[k];
+    }
+    c[6] = half_extent;
+  }
+}
+
+/* render/raster.cpp:12-102 renderView, face by face in index order over the
+ * padded pixel box, Moller-Trumbore with the hoisted per-face factors, z-test
+ * "replace iff depth > stored" (ties keep the lower face). Outputs nullable
+ * except face/depth scratch. */
+static void render_view(const mf_mesh_view* m, const double* vn, const double* cam7, int res, int32_t* face,
+                        float* depth, float* pos, float* nrm) {
+  const d3 dir = ld3(cam7), up = ld3(cam7 + 3);
+  const d3 right = cross3(dir, up);
+  const double he = cam7[6];
+  const double step = 2.0 * he / res;
+  const size_t n = (size_t)res * res;
+  for (size_t i = 0; i < n; ++i) {
+    face[i] = -1;
+    depth[i] = INFINITY;
+    if (pos) pos[3 * i] = pos[3 * i + 1] = pos[3 * i + 2] = 0.f;
+    if (nrm) nrm[3 * i] = nrm[3 * i + 1] = nrm[3 * i + 2] = 0.f;
+  }
+  d3* colU = (d3*)malloc(sizeof(d3) * (size_t)res);
+  d3* rowV = (d3*)malloc(sizeof(d3) * (size_t)res);
+  for (int p = 0; p < res; ++p) {
+    const double pu = -he + (p + 0.5) * (2.0 * he / res); /* camera.h:22-27 */
+    const double pv = he - (p + 0.5) * (2.0 * he / res);
+    colU[p] = scl3(pu, right);
+    rowV[p] = scl3(pv, up);
+  }
+  for (int f = 0; f < m->n_faces; ++f) {
+    const int* tri = m->faces + 3 * (size_t)f;
+    const d3 a = P(m, tri[0]), b = P(m, tri[1]), c = P(m, tri[2]);
+    const double u0 = dot3(a, right), u1 = dot3(b, right), u2 = dot3(c, right);
+    const double v0 = dot3(a, up), v1 = dot3(b, up), v2 = dot3(c, up);
+    const double umin = fmin(u0, fmin(u1, u2)), umax = fmax(u0, fmax(u1, u2));
+    const double vmin = fmin(v0, fmin(v1, v2)), vmax = fmax(v0, fmax(v1, v2));
+    int pxLo = (int)floor((umin + he) / step - 0.5) - 1;
+    int pxHi = (int)ceil((umax + he) / step - 0.5) + 1;
+    int pyLo = (int)floor((he - vmax) / step - 0.5) - 1;
+    int pyHi = (int)ceil((he - vmin) / step - 0.5) + 1;
+    if (pxLo < 0) pxLo = 0;
+    if (pyLo < 0) pyLo = 0;
+    if (pxHi > res - 1) pxHi = res - 1;
+    if (pyHi > res - 1) pyHi = res - 1;
+    if (pxLo > pxHi || pyLo > pyHi) continue;
+    const d3 e1 = sub3(b, a), e2 = sub3(c, a);
+    const d3 pvec = cross3(dir, e2);
+    const double det = dot3(e1, pvec);
+    if (fabs(det) < 1e-9) continue;
+    const double invDet = 1.0 / det;
+    for (int py = pyLo; py <= pyHi; ++py)
+      for (int px = pxLo; px <= pxHi; ++px) {
+        const d3 origin = add3(colU[px], rowV[py]);
+        const d3 svec = sub3(origin, a);
+        const double bu = dot3(svec, pvec) * invDet;
+        if (bu < 0.0 || bu > 1.0) continue;
+        const d3 qvec = cross3(svec, e1);
+        const double bv = dot3(dir, qvec) * invDet;
+        if (bv < 0.0 || bu + bv > 1.0) continue;
+        const double t = dot3(e2, qvec) * invDet;
+        const float dp = (float)(-t);
+        const size_t idx = (size_t)py * res + px;
+        if (face[idx] >= 0 && !(dp > depth[idx])) continue;
+        face[idx] = f;
+        depth[idx] = dp;
+        if (pos) {
+          const d3 hit = add3(origin, scl3(t, dir));
+          for (int k = 0; k < 3; ++k) pos[3 * idx + k] = (float)hit.v[k];
+        }
+        if (nrm && vn) {
+          d3 nn = add3(add3(scl3(1.0 - bu - bv, ld3(vn + 3 * (size_t)tri[0])), scl3(bu, ld3(vn + 3 * (size_t)tri[1]))),
+                       scl3(bv, ld3(vn + 3 * (size_t)tri[2])));
+          const double len = nrm3(nn);
+          if (len > 0) nn = div3(nn, len);
+          for (int k = 0; k < 3; ++k) nrm[3 * idx + k] = (float)nn.v[k];
+        }
+      }
+  }
+  free(colU);
+  free(rowV);
+}
+
+int orc_render_views(const mf_mesh_view* m, const double* cams7, int n_views, int res, const double* vn,
+                     int32_t* face, float* depth, float* pos, float* nrm) {
+  const size_t n = (size_t)res * res;
+  for (int v = 0; v < n_views; ++v)
+    render_view(m, vn, cams7 + 7 * v, res, face + v * n, depth + v * n, pos ? pos + 3 * v * n : NULL,
+                nrm ? nrm + 3 * v * n : NULL);
+  return 0;
+}
+
+/* visibility/visibility.cpp:13-59 castVisibility: validate, centre on the
+ * bounds, radius = max |p - centre| (1 if 0), fibonacci cameras of half
+ * extent radius * 1.04, per view renderView, won pixels per face. */
+int orc_cast_visibility(const mf_mesh_view* m, int viewpoints, int res, int64_t* hits) {
+  int rc = validate_mesh(m);
+  if (rc) return rc;
+  if (viewpoints <= 0 || res <= 0)
+    return fail(MF_ERR_INVALID_CONFIG, "InvalidConfig: viewpoints and resolution must be positive");
+  double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int v = 0; v < m->n_vertices; ++v)
+    for (int k = 0; k < 3; ++k) {
+      const double p = m->positions[3 * v + k];
+      mn[k] = p < mn[k] ? p : mn[k];
+      mx[k] = mx[k] < p ? p : mx[k];
+    }
+  const d3 center = mk3((mn[0] + mx[0]) * 0.5, (mn[1] + mx[1]) * 0.5, (mn[2] + mx[2]) * 0.5);
+  double* cpos = (double*)malloc(sizeof(double) * 3 * (size_t)m->n_vertices);
+  double radius = 0.0;
+  for (int v = 0; v < m->n_vertices; ++v) {
+    const d3 p = sub3(P(m, v), center);
+    memcpy(cpos + 3 * (size_t)v, p.v, 24);
+    const double nn = nrm3(p);
+    radius = radius < nn ? nn : radius;
+  }
+  if (radius <= 0.0) radius = 1.0;
+  mf_mesh_view cm = *m;
+  cm.positions = cpos;
+  double* cams = (double*)malloc(sizeof(double) * 7 * (size_t)viewpoints);
+  orc_fibonacci_cameras(viewpoints, radius * 1.04, cams);
+  const size_t n = (size_t)res * res;
+  int32_t* face = (int32_t*)malloc(sizeof(int32_t) * n);
+  float* depth = (float*)malloc(sizeof(float) * n);
+  memset(hits, 0, sizeof(int64_t) * (size_t)m->n_faces);
+  for (int v = 0; v < viewpoints; ++v) {
+    render_view(&cm, NULL, cams + 7 * v, res, face, depth, NULL, NULL);
+    for (size_t i = 0; i < n; ++i)
+      if (face[i] >= 0) ++hits[face[i]];
+  }
+  free(face);
+  free(depth);
+  free(cams);
+  free(cpos);
+  return 0;
+}

@@ -63,6 +63,12 @@ int orc_raycast_first(const mf_mesh_view* m, const double* o, const double* d, i
 int orc_surface_band(const mf_mesh_view* m, int res, double band_voxels, int dilate, const double* domain,
                      int threads, uint8_t* labels, float* dist, double* grid_out);
 
+/* render/camera.cpp:38-55, render/raster.cpp:12-102, visibility/visibility.cpp:13-59 */
+void orc_fibonacci_cameras(int count, double half_extent, double* cams7);
+int orc_render_views(const mf_mesh_view* m, const double* cams7, int n_views, int res, const double* vn,
+                     int32_t* face, float* depth, float* pos, float* nrm);
+int orc_cast_visibility(const mf_mesh_view* m, int viewpoints, int res, int64_t* hits);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,7 +30,10 @@
 #include "meshforge/core/mesh.h"
 #include "meshforge/core/parallel.h"
 #include "meshforge/metrics/metrics.h"
+#include "meshforge/render/camera.h"
+#include "meshforge/render/raster.h"
 #include "meshforge/signfield/sign_grid.h"
+#include "meshforge/visibility/visibility.h"
 #include "meshforge/spatial/bvh.h"
 #include "meshforge/spatial/tri_geom.h"
 #include "mfbake.h"
@@ -359,6 +362,50 @@ int ref_surface_band(const mf_mesh_view* mesh, int res, double band_voxels, int 
       grid_out[3] = g.voxelSize;
       grid_out[4] = g.truncation;
     }
+  });
+}
+
+// fibonacciCameras (src/render/camera.cpp:38-55) -> direction, up, halfExtent.
+void ref_fibonacci_cameras(int count, int res, double half_extent, double* cams7) {
+  const auto cams = fibonacciCameras(count, res, half_extent);
+  for (int i = 0; i < count; ++i) {
+    for (int k = 0; k < 3; ++k) {
+      cams7[7 * i + k] = cams[i].direction[k];
+      cams7[7 * i + 3 + k] = cams[i].up[k];
+    }
+    cams7[7 * i + 6] = cams[i].halfExtent;
+  }
+}
+
+// renderView (src/render/raster.cpp:12-102) per camera.
+int ref_render_views(const mf_mesh_view* mesh, const double* cams7, int n_views, int res, const double* vn,
+                     int32_t* face, float* depth, float* pos, float* nrm) {
+  return guarded([&] {
+    const TriangleMesh m = toMesh(mesh);
+    std::vector<Eigen::Vector3d> normals(m.positions.size(), Eigen::Vector3d::Zero());
+    if (vn)
+      for (size_t i = 0; i < normals.size(); ++i) normals[i] = {vn[3 * i], vn[3 * i + 1], vn[3 * i + 2]};
+    const size_t n = static_cast<size_t>(res) * res;
+    for (int v = 0; v < n_views; ++v) {
+      OrthoCamera cam;
+      cam.direction = {cams7[7 * v], cams7[7 * v + 1], cams7[7 * v + 2]};
+      cam.up = {cams7[7 * v + 3], cams7[7 * v + 4], cams7[7 * v + 5]};
+      cam.halfExtent = cams7[7 * v + 6];
+      cam.resolution = res;
+      const RenderedView r = renderView(m, normals, cam, {});
+      std::memcpy(face + v * n, r.face.data.data(), n * sizeof(int32_t));
+      std::memcpy(depth + v * n, r.depth.data.data(), n * sizeof(float));
+      if (pos) std::memcpy(pos + 3 * v * n, r.position.data.data(), 3 * n * sizeof(float));
+      if (nrm) std::memcpy(nrm + 3 * v * n, r.normal.data.data(), 3 * n * sizeof(float));
+    }
+  });
+}
+
+// castVisibility (src/visibility/visibility.cpp:13-59).
+int ref_cast_visibility(const mf_mesh_view* mesh, int viewpoints, int res, int64_t* hits) {
+  return guarded([&] {
+    const VisibilityMask mask = castVisibility(toMesh(mesh), viewpoints, res);
+    std::memcpy(hits, mask.hits.data(), mask.hits.size() * sizeof(int64_t));
   });
 }
 

@@ -268,6 +268,16 @@ void vertex_bounds(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out6);
 // markSurfaceBand's voxel sweep (signfield/sign_grid.cpp:56-66) over a res^3 grid.
 void surface_band(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, int res, const double origin[3], double h,
                   double truncation, double band_world, uint8_t* labels, float* dist);
+// Ortho pixel-ray views (renderView, render/raster.cpp:12-102): cams7 = per
+// view direction xyz, up xyz, halfExtent. Optional outputs: per-face won-pixel
+// counters (castVisibility), per-view face / depth / position / normal images.
+void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7, int nviews, int res,
+                  unsigned long long* hits, int32_t* face_img, float* depth_img, float* pos_img, float* nrm_img,
+                  const int32_t* faces, const double* vnormals);
+// fibonacciCameras (render/camera.cpp:38-55) into cams7 (host).
+void fibonacci_cameras(int count, double half_extent, double* cams7);
+// out = positions - center; returns max |out| (synchronises).
+double center_mesh(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double center[3], double* out);
 void raycast_first(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* o, const double* d,
                    int64_t n, double tmin, double tmax, int32_t* face, double* t, double* u,
                    double* v);

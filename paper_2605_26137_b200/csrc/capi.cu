@@ -1487,3 +1487,83 @@ int mf_surface_band(mf_bvh* bvh, int resolution, double band_voxels, int dilate_
   });
 }
 }  // extern "C"
+
+// ---------------------------------------------------------------- ortho views
+extern "C" {
+int mf_fibonacci_cameras(int count, double half_extent, double* cameras) {
+  if (count < 0 || (count > 0 && !cameras)) return fail(MF_ERR_BAD_ARGUMENT, "bad camera buffer");
+  fibonacci_cameras(count, half_extent, cameras);
+  return MF_OK;
+}
+
+int mf_render_views(mf_ctx* ctx, const mf_mesh_view* mesh, const double* cameras, int n_views, int resolution,
+                    const double* vertex_normals, int32_t* face, float* depth, float* position, float* normal) {
+  if (!ctx || !mesh || (n_views > 0 && !cameras)) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    if (n_views < 0 || resolution < 0) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: negative view count");
+    mf_mesh m;
+    m.ctx = ctx;
+    upload_mesh(c, c.stream, mesh, &m, "rv.mesh");
+    check_mesh(&m);
+    Lbvh bvh;
+    lbvh_build(c, c.stream, m.m, bvh, "rv.bvh");
+    const int64_t px = static_cast<int64_t>(n_views) * resolution * resolution;
+    double* dvn = nullptr;
+    if (vertex_normals && normal) {
+      dvn = c.buf<double>("rv.vn", 3 * static_cast<size_t>(m.m.nv));
+      MFB_CUDA_TRY(cudaMemcpyAsync(dvn, vertex_normals, sizeof(double) * 3 * m.m.nv, cudaMemcpyHostToDevice,
+                                   c.stream));
+    }
+    int32_t* df = c.buf<int32_t>("rv.face", px);
+    float* dd = depth ? c.buf<float>("rv.depth", px) : nullptr;
+    float* dp = position ? c.buf<float>("rv.pos", 3 * px) : nullptr;
+    float* dn = normal ? c.buf<float>("rv.nrm", 3 * px) : nullptr;
+    render_views(c, c.stream, bvh, cameras, n_views, resolution, nullptr, df, dd, dp, dn, m.m.faces, dvn);
+    if (face) MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * px, cudaMemcpyDeviceToHost, c.stream));
+    if (depth) MFB_CUDA_TRY(cudaMemcpyAsync(depth, dd, sizeof(float) * px, cudaMemcpyDeviceToHost, c.stream));
+    if (position) MFB_CUDA_TRY(cudaMemcpyAsync(position, dp, sizeof(float) * 3 * px, cudaMemcpyDeviceToHost, c.stream));
+    if (normal) MFB_CUDA_TRY(cudaMemcpyAsync(normal, dn, sizeof(float) * 3 * px, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_cast_visibility(mf_ctx* ctx, const mf_mesh_view* mesh, int viewpoints, int resolution, int64_t* hits,
+                       uint8_t* state) {
+  if (!ctx || !mesh || !hits) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    mf_mesh m;
+    m.ctx = ctx;
+    upload_mesh(c, c.stream, mesh, &m, "vis.mesh");
+    check_mesh(&m);  // validateMesh (visibility.cpp:14)
+    if (viewpoints <= 0 || resolution <= 0)
+      throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: viewpoints and resolution must be positive");
+    const int nf = m.m.nf;
+    // centred copy (visibility.cpp:20-30): bounds centre, max |p - centre|
+    double box[6];
+    vertex_bounds(c, c.stream, m.m, box);
+    double center[3];
+    for (int k = 0; k < 3; ++k) center[k] = (box[k] + box[3 + k]) * 0.5;  // aabb.h:25
+    DevMesh cm = m.m;
+    double* cpos = c.buf<double>("vis.cpos", 3 * static_cast<size_t>(m.m.nv));
+    double radius = center_mesh(c, c.stream, m.m, center, cpos);
+    cm.pos = cpos;
+    if (radius <= 0.0) radius = 1.0;
+    std::vector<double> cams(7 * static_cast<size_t>(viewpoints));
+    fibonacci_cameras(viewpoints, radius * 1.04, cams.data());
+    Lbvh bvh;
+    lbvh_build(c, c.stream, cm, bvh, "vis.bvh");
+    auto* dh = c.buf<unsigned long long>("vis.hits", nf);
+    MFB_CUDA_TRY(cudaMemsetAsync(dh, 0, sizeof(unsigned long long) * nf, c.stream));
+    render_views(c, c.stream, bvh, cams.data(), viewpoints, resolution, dh, nullptr, nullptr, nullptr, nullptr,
+                 nullptr, nullptr);
+    MFB_CUDA_TRY(cudaMemcpyAsync(hits, dh, sizeof(int64_t) * nf, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (state)
+      for (int f = 0; f < nf; ++f) state[f] = hits[f] > 0 ? 1 : 0;  // visibility.cpp:53-56
+    return MF_OK;
+  });
+}
+}  // extern "C"

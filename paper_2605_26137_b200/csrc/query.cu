@@ -12,6 +12,8 @@
 // with round-down intrinsics, compared against an upper bound of the current
 // best inflated by the scene-scale f64 error slack.
 #include <algorithm>
+#include <cmath>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1579,6 +1581,148 @@ __global__ void k_vertex_bounds(const double* __restrict__ pos, int nv, unsigned
     }
   }
 }
+
+// ---------------------------------------------------------------- ortho views
+// renderView (render/raster.cpp:12-102) as one pixel ray per thread through
+// the LBVH. Per pixel the reference keeps, over faces in index order, the
+// first face whose depth f32(-t) is strictly larger than the stored one: the
+// winner is argmax f32(-t), ties to the lowest face, among faces whose
+// Moller-Trumbore test (same expressions as rayTriangle, tri_geom.h:14-33)
+// passes and whose padded pixel box (raster.cpp:53-61) holds the pixel. The
+// ray is the full line (no t range). The walk prunes a box only when its
+// slab entry exceeds -prev_f32(best depth): such faces cannot reach the
+// stored depth, so the result is the reference's for any tree.
+// castVisibility (visibility/visibility.cpp:13-59) adds one hit per won pixel
+// to the winner's counter over all views.
+struct ViewCam {
+  double dir[3], up[3], right[3];
+  double he, step;  // halfExtent, 2 * halfExtent / resolution
+};
+
+__global__ void __launch_bounds__(128) k_render_views(
+    const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root, const ViewCam* __restrict__ cams,
+    int nviews, int res, unsigned long long* __restrict__ hits, int32_t* __restrict__ face_img,
+    float* __restrict__ depth_img, float* __restrict__ pos_img, float* __restrict__ nrm_img,
+    const int32_t* __restrict__ faces, const double* __restrict__ vnormals) {
+  const int tiles_x = (res + 7) >> 3, tiles_y = (res + 3) >> 2;
+  const int64_t per_view = static_cast<int64_t>(tiles_x) * tiles_y * 32;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int view = static_cast<int>(t / per_view);
+  if (view >= nviews) return;
+  const int64_t r = t - view * per_view;
+  const int tile = static_cast<int>(r >> 5), lane = static_cast<int>(r & 31);
+  const int px = (tile % tiles_x) * 8 + (lane & 7), py = (tile / tiles_x) * 4 + (lane >> 3);
+  if (px >= res || py >= res) return;
+  const ViewCam& c = cams[view];
+  const d3 dir = mk3(c.dir[0], c.dir[1], c.dir[2]);
+  const d3 up = mk3(c.up[0], c.up[1], c.up[2]);
+  const d3 right = mk3(c.right[0], c.right[1], c.right[2]);
+  // camera.h:22-33: pixelU/V, origin = colU[px] + rowV[py] (raster.cpp:31-35, :70)
+  const double pu = -c.he + (px + 0.5) * c.step;
+  const double pv = c.he - (py + 0.5) * c.step;
+  const d3 o = pu * right + pv * up;
+  const d3 inv = mk3(1.0 / dir.x, 1.0 / dir.y, 1.0 / dir.z);
+  const double slack = 0x1p-24;
+  int bf = -1;
+  float bd = -INFINITY;
+  double bt = 0.0, bu = 0.0, bv = 0.0;
+  double limit = INFINITY;
+  int32_t st[kStackMax];
+  int sp = 0;
+  int32_t ref = root;
+  for (;;) {
+    if (ref >= 0) {
+      const float4* np = reinterpret_cast<const float4*>(nodes + ref);
+      const float4 a = __ldg(np), b = __ldg(np + 1), cc = __ldg(np + 2);
+      const int4 dd = __ldg(reinterpret_cast<const int4*>(np + 3));
+      double tl = 0.0, tr = 0.0;
+      const bool hl = slab(a.x, a.y, a.z, a.w, b.x, b.y, o, inv, -INFINITY, limit, slack, tl);
+      const bool hr = slab(b.z, b.w, cc.x, cc.y, cc.z, cc.w, o, inv, -INFINITY, limit, slack, tr);
+      if (hl && hr) {
+        const bool lf = tl <= tr;
+        st[sp++] = lf ? dd.y : dd.x;
+        ref = lf ? dd.x : dd.y;
+        continue;
+      }
+      if (hl || hr) {
+        ref = hl ? dd.x : dd.y;
+        continue;
+      }
+    } else {
+      int first, count;
+      leaf_decode(ref, first, count);
+      for (int k = 0; k < count; ++k) {
+        d3 A, B, C;
+        int f;
+        load_tri(tris + first + k, A, B, C, f);
+        double tt, u, v;
+        if (!ray_triangle(o, dir, A, B, C, tt, u, v)) continue;
+        const float depth = __double2float_rn(-tt);
+        if (!(bf < 0 || depth > bd || (depth == bd && f < bf))) continue;
+        // candidate pixel box of the face (raster.cpp:46-61)
+        const double u0 = dot(A, right), u1 = dot(B, right), u2 = dot(C, right);
+        const double v0 = dot(A, up), v1 = dot(B, up), v2 = dot(C, up);
+        const double umin = fmin(u0, fmin(u1, u2)), umax = fmax(u0, fmax(u1, u2));
+        const double vmin = fmin(v0, fmin(v1, v2)), vmax = fmax(v0, fmax(v1, v2));
+        const int pxLo = max(0, static_cast<int>(floor((umin + c.he) / c.step - 0.5)) - 1);
+        const int pxHi = min(res - 1, static_cast<int>(ceil((umax + c.he) / c.step - 0.5)) + 1);
+        const int pyLo = max(0, static_cast<int>(floor((c.he - vmax) / c.step - 0.5)) - 1);
+        const int pyHi = min(res - 1, static_cast<int>(ceil((c.he - vmin) / c.step - 0.5)) + 1);
+        if (px < pxLo || px > pxHi || py < pyLo || py > pyHi) continue;
+        bf = f;
+        bd = depth;
+        bt = tt;
+        bu = u;
+        bv = v;
+        limit = -static_cast<double>(nextafterf(bd, -INFINITY));
+      }
+    }
+    if (sp == 0) break;
+    ref = st[--sp];
+  }
+  if (hits && bf >= 0) atomicAdd(&hits[bf], 1ull);
+  if (!face_img) return;
+  const int64_t pi = static_cast<int64_t>(view) * res * res + static_cast<int64_t>(py) * res + px;
+  face_img[pi] = bf;
+  if (depth_img) depth_img[pi] = bf >= 0 ? bd : INFINITY;
+  if (pos_img) {
+    const d3 hit = o + bt * dir;  // raster.cpp:88
+    pos_img[3 * pi] = bf >= 0 ? __double2float_rn(hit.x) : 0.f;
+    pos_img[3 * pi + 1] = bf >= 0 ? __double2float_rn(hit.y) : 0.f;
+    pos_img[3 * pi + 2] = bf >= 0 ? __double2float_rn(hit.z) : 0.f;
+  }
+  if (nrm_img) {
+    float nf[3] = {0.f, 0.f, 0.f};
+    if (bf >= 0 && vnormals) {  // raster.cpp:89-92
+      const d3 n0 = ld3(vnormals + 3 * faces[3 * bf]), n1 = ld3(vnormals + 3 * faces[3 * bf + 1]),
+               n2 = ld3(vnormals + 3 * faces[3 * bf + 2]);
+      d3 n = ((1.0 - bu - bv) * n0 + bu * n1) + bv * n2;
+      const double len = norm(n);
+      if (len > 0) n = n / len;
+      nf[0] = __double2float_rn(n.x);
+      nf[1] = __double2float_rn(n.y);
+      nf[2] = __double2float_rn(n.z);
+    }
+    nrm_img[3 * pi] = nf[0];
+    nrm_img[3 * pi + 1] = nf[1];
+    nrm_img[3 * pi + 2] = nf[2];
+  }
+}
+
+// castVisibility's centring (visibility.cpp:20-30): out = p - center, and the
+// largest |out| (ordered bits, max) into acc.
+__global__ void k_center_mesh(const double* __restrict__ pos, int nv, double cx, double cy, double cz,
+                              double* __restrict__ out, unsigned long long* acc) {
+  double m = 0.0;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+    const d3 p = mk3(pos[3 * v] - cx, pos[3 * v + 1] - cy, pos[3 * v + 2] - cz);
+    st3(out + 3 * v, p);
+    const double n = norm(p);
+    m = m < n ? n : m;
+  }
+  for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(acc, ordered_bits_dev(m));
+}
 }  // namespace
 
 // Resident 128-thread blocks per SM of `kern` (>= 1); callers cache it in a
@@ -1793,6 +1937,85 @@ void surface_band(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, int res, const doub
       band_world, labels, dist);
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
+}
+
+
+// fibonacciCameras (render/camera.cpp:38-55) + right() (camera.h:19), host f64.
+static std::vector<ViewCam> view_cams(const double* cams7, int nviews, int res) {
+  std::vector<ViewCam> v(nviews);
+  for (int i = 0; i < nviews; ++i) {
+    const double* c = cams7 + 7 * i;
+    const d3 dir = mk3(c[0], c[1], c[2]), up = mk3(c[3], c[4], c[5]);
+    const d3 right = cross(dir, up);
+    for (int k = 0; k < 3; ++k) {
+      v[i].dir[k] = (&dir.x)[k];
+      v[i].up[k] = (&up.x)[k];
+      v[i].right[k] = (&right.x)[k];
+    }
+    v[i].he = c[6];
+    v[i].step = 2.0 * c[6] / res;
+  }
+  return v;
+}
+
+void fibonacci_cameras(int count, double half_extent, double* cams7) {
+  const double golden = M_PI * (3.0 - std::sqrt(5.0));
+  for (int i = 0; i < count; ++i) {
+    const double z = 1.0 - 2.0 * (i + 0.5) / count;
+    const double r = std::sqrt(std::max(0.0, 1.0 - z * z));
+    const double a = golden * i;
+    const d3 viewpoint = mk3(r * std::cos(a), r * std::sin(a), z);
+    const d3 dir = mk3(-viewpoint.x, -viewpoint.y, -viewpoint.z);
+    const d3 refv = std::abs(z) < 0.9 ? mk3(0, 0, 1) : mk3(0, 1, 0);
+    d3 up = cross(dir, refv);
+    const double z2 = dot(up, up);
+    if (z2 > 0.0) up = up / std::sqrt(z2);  // Eigen normalized() (shim order)
+    double* c = cams7 + 7 * i;
+    c[0] = dir.x, c[1] = dir.y, c[2] = dir.z;
+    c[3] = up.x, c[4] = up.y, c[5] = up.z;
+    c[6] = half_extent;
+  }
+}
+
+void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7, int nviews, int res,
+                  unsigned long long* hits, int32_t* face_img, float* depth_img, float* pos_img, float* nrm_img,
+                  const int32_t* faces, const double* vnormals) {
+  if (nviews <= 0 || res <= 0) return;
+  const std::vector<ViewCam> hv = view_cams(cams7, nviews, res);
+  auto* dc = ctx.buf<ViewCam>("view.cams", nviews);
+  MFB_CUDA_TRY(cudaMemcpyAsync(dc, hv.data(), sizeof(ViewCam) * nviews, cudaMemcpyHostToDevice, s));
+  const int64_t per_view = static_cast<int64_t>((res + 7) / 8) * ((res + 3) / 4) * 32;
+  // views in launch-sized groups (grid.x stays well inside 2^31 blocks)
+  const int group = static_cast<int>(std::max<int64_t>(1, (int64_t{1} << 30) / per_view));
+  for (int v0 = 0; v0 < nviews; v0 += group) {
+    const int nv = std::min(group, nviews - v0);
+    const int64_t threads = per_view * nv;
+    const int64_t img_off = static_cast<int64_t>(v0) * res * res;
+    k_render_views<<<static_cast<unsigned>(div_up(threads, 128)), 128, 0, s>>>(
+        bvh.nodes, bvh.tris, bvh.root_ref, dc + v0, nv, res, hits, face_img ? face_img + img_off : nullptr,
+        depth_img ? depth_img + img_off : nullptr, pos_img ? pos_img + 3 * img_off : nullptr,
+        nrm_img ? nrm_img + 3 * img_off : nullptr, faces, vnormals);
+    ctx.count_launch();
+  }
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+double center_mesh(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double center[3], double* out) {
+  auto* acc = ctx.buf<unsigned long long>("ctr.acc", 1);
+  MFB_CUDA_TRY(cudaMemsetAsync(acc, 0, sizeof(unsigned long long), s));
+  if (m.nv > 0) {
+    k_center_mesh<<<std::min(div_up(m.nv, 256), kNumSMs * 4), 256, 0, s>>>(m.pos, m.nv, center[0], center[1],
+                                                                            center[2], out, acc);
+    ctx.count_launch();
+    MFB_CUDA_TRY(cudaGetLastError());
+  }
+  unsigned long long h = 0;
+  MFB_CUDA_TRY(cudaMemcpyAsync(&h, acc, sizeof(h), cudaMemcpyDeviceToHost, s));
+  MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  h = (h & 0x8000000000000000ull) ? (h & ~0x8000000000000000ull) : ~h;
+  double r;
+  std::memcpy(&r, &h, 8);
+  return m.nv > 0 ? r : 0.0;
 }
 
 void raycast_first(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* o, const double* d,

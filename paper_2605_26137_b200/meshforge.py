@@ -246,3 +246,39 @@ class RayHit:
 
     def valid(self) -> bool:
         return self.face >= 0
+
+
+# ---------------------------------------------------------------- ortho views
+def fibonacci_cameras(count: int, half_extent: float = 0.52, ctx=None) -> np.ndarray:
+    """fibonacciCameras (render/camera.cpp:38-55): count x 7 = direction xyz, up xyz, halfExtent."""
+    ctx = ctx or default_context()
+    cams = np.zeros((count, 7))
+    check(ctx.lib.mf_fibonacci_cameras(int(count), float(half_extent), _p(cams)))
+    return cams
+
+
+def render_views(mesh: TriangleMesh, cameras: np.ndarray, resolution: int, vertex_normals=None, ctx=None):
+    """renderView (render/raster.cpp:12-102) for each camera row: (face i32, depth f32,
+    position f32x3, normal f32x3) per view, one pixel ray per thread through the LBVH."""
+    ctx = ctx or default_context()
+    cams = np.ascontiguousarray(cameras, dtype=np.float64).reshape(-1, 7)
+    n = cams.shape[0]
+    face = np.zeros((n, resolution, resolution), np.int32)
+    depth = np.zeros((n, resolution, resolution), np.float32)
+    pos = np.zeros((n, resolution, resolution, 3), np.float32)
+    nrm = np.zeros((n, resolution, resolution, 3), np.float32)
+    vn = None if vertex_normals is None else np.ascontiguousarray(vertex_normals, dtype=np.float64)
+    v = mesh.view()
+    check(ctx.lib.mf_render_views(ctx.h, ctypes.byref(v), _p(cams), n, int(resolution), _p(vn), _p(face), _p(depth),
+                                  _p(pos), _p(nrm)))
+    return face, depth, pos, nrm
+
+
+def cast_visibility(mesh: TriangleMesh, viewpoints: int = 512, resolution: int = 1024, ctx=None):
+    """castVisibility (visibility/visibility.cpp:13-59): (hits i64 per face, state u8 0 Hidden / 1 Visible)."""
+    ctx = ctx or default_context()
+    hits = np.zeros(mesh.face_count(), np.int64)
+    state = np.zeros(mesh.face_count(), np.uint8)
+    v = mesh.view()
+    check(ctx.lib.mf_cast_visibility(ctx.h, ctypes.byref(v), int(viewpoints), int(resolution), _p(hits), _p(state)))
+    return hits, state

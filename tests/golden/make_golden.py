@@ -120,8 +120,34 @@ def band_case(ref):
     return out
 
 
+def concat(a, b):
+    from paper_2605_26137_b200.mesh import TriangleMesh
+    return TriangleMesh(np.vstack([a.positions, b.positions]),
+                        np.vstack([a.faces, b.faces + a.vertex_count()]).astype(np.int32))
+
+
+def views_case(ref):
+    """renderView / castVisibility (render/raster.cpp:12-102, visibility.cpp:13-59)
+    through the reference: nested spheres (sealed inner shell: zero hits), a
+    duplicated mesh (depth ties keep the lower face) and a star blob."""
+    nested = concat(ref.fixture(0, 3, r=0.5), ref.fixture(0, 2, r=0.2))
+    blob = ref.fixture(2, 24, 32, 11, 0.5)
+    dup = concat(ref.fixture(0, 1, r=0.5), ref.fixture(0, 1, r=0.5))
+    cams = ref.fibonacci_cameras(8, 0.55, 96)
+    out = dict(cams=cams)
+    for name, m in (("nested", nested), ("blob", blob), ("dup", dup)):
+        vn = ref.vertex_normals(m)
+        face, depth, pos, nrm = ref.render_views(m, cams, 96, vn)
+        out.update({f"{name}_pos_in": m.positions, f"{name}_faces": m.faces, f"{name}_vn": vn,
+                    f"{name}_face": face, f"{name}_depth": depth, f"{name}_hits": ref.cast_visibility(m, 32, 96)})
+        if name == "blob":  # position / normal images of two views
+            out.update(blob_position=pos[:2], blob_normal=nrm[:2])
+    return out
+
+
 def main():
     ref = bindings.ref()
+    np.savez_compressed(os.path.join(HERE, "views.npz"), **views_case(ref))
     np.savez_compressed(os.path.join(HERE, "band.npz"), **band_case(ref))
     np.savez_compressed(os.path.join(HERE, "kats.npz"), **kat_case(ref))
     for name in BAKE_CASES:

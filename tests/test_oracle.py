@@ -210,3 +210,26 @@ def test_port_surface_band_errors(port):
         with pytest.raises(OracleError) as e:
             port.surface_band(ico, *args)
         assert e.value.code == code
+
+
+VIEW_CASES = ("nested", "blob", "dup")
+
+
+def f32bits(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("case", VIEW_CASES)
+def test_port_matches_reference_golden_views(port, case):
+    """renderView face/depth images and castVisibility hit histograms
+    (render/raster.cpp:12-102, visibility/visibility.cpp:13-59) bit-for-bit."""
+    d = load("views.npz")
+    assert np.array_equal(port.fibonacci_cameras(8, 0.55), d["cams"])
+    m = TriangleMesh(d[f"{case}_pos_in"], d[f"{case}_faces"])
+    face, depth, pos, nrm = port.render_views(m, d["cams"], 96, d[f"{case}_vn"])
+    assert np.array_equal(face, d[f"{case}_face"])
+    assert np.array_equal(f32bits(depth), f32bits(d[f"{case}_depth"]))
+    if case == "blob":
+        assert np.array_equal(f32bits(pos[:2]), f32bits(d["blob_position"]))
+        assert np.array_equal(f32bits(nrm[:2]), f32bits(d["blob_normal"]))
+    assert np.array_equal(port.cast_visibility(m, 32, 96), d[f"{case}_hits"])
