@@ -486,6 +486,42 @@ __device__ __forceinline__ int32_t warp_root(const BNode* __restrict__ nodes, in
   return ref;
 }
 
+// Pop of the per-thread stack that skips entries whose lower bound no longer
+// passes `bnd` four at a time: one aligned 16-byte local load covers the top
+// (up to) four lower bounds, so a run of pruned entries costs one dependent
+// L1 round trip per four entries instead of one per entry. Returns the
+// topmost surviving entry's ref (sp = its slot) or kDoneRef (sp = 0).
+#ifndef MFB_POP4
+#define MFB_POP4 1
+#endif
+#ifndef MFB_LEAF_UNROLL
+#define MFB_LEAF_UNROLL 0
+#endif
+constexpr int32_t kDoneRef = static_cast<int32_t>(0x80000000);
+__device__ __forceinline__ int32_t pop_within(const int32_t* st_ref, const float* st_lb, int& sp, float bnd) {
+#if MFB_POP4
+  while (sp > 0) {
+    const int base = (sp - 1) & ~3;
+    const float4 v = *reinterpret_cast<const float4*>(st_lb + base);
+    unsigned m = (v.x <= bnd ? 1u : 0u) | (v.y <= bnd ? 2u : 0u) | (v.z <= bnd ? 4u : 0u) | (v.w <= bnd ? 8u : 0u);
+    m &= (1u << (sp - base)) - 1u;
+    if (m) {
+      const int top = base + 31 - __clz(m);
+      sp = top;
+      return st_ref[top];
+    }
+    sp = base;
+  }
+  return kDoneRef;
+#else
+  while (sp > 0) {
+    --sp;
+    if (st_lb[sp] <= bnd) return st_ref[sp];
+  }
+  return kDoneRef;
+#endif
+}
+
 // Occupancy over registers: the walk is bound by dependent L1/L2 latency
 // (node record -> box test -> child record), so resident warps matter more
 // than the spills a 64-register cap costs. Measured at config B (transfer
@@ -549,7 +585,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     }
     float bnd = live ? prune_bound(best.d, E) : -INFINITY;
     int32_t st_ref[kStackMax];
-    float st_lb[kStackMax];
+    alignas(16) float st_lb[kStackMax];
     int sp = 0;
     // ref: node (>= 0), leaf (< 0 and != kDone), or kDone
     constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
@@ -665,14 +701,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         } else if (hL || hR) {
           ref = hL ? d.x : d.y;
         } else {
-          ref = kDone;
-          while (sp > 0) {
-            --sp;
-            if (st_lb[sp] <= bnd) {
-              ref = st_ref[sp];
-              break;
-            }
-          }
+          ref = pop_within(st_ref, st_lb, sp, bnd);
         }
       }
       if (ref == kDone) break;
@@ -684,17 +713,23 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         ++pv[1];
         pv[2] += count;
       }
-      for (int k = 0; k < count; ++k) {
+      // (iterate [first, end): two live loop values instead of three, so the
+      // loop state stays in registers under the 64-register cap)
+      const int end = first + count;
+#if MFB_LEAF_UNROLL
+#pragma unroll 3
+#endif
+      for (int k = first; k < end; ++k) {
 #if MFB_TRI_BOX
         {  // conservative per-triangle fp32 box check before the exact f64 test
-          const float4* bp = reinterpret_cast<const float4*>(tbox + first + k);
+          const float4* bp = reinterpret_cast<const float4*>(tbox + k);
           const float4 ba = __ldg(bp), bb = __ldg(bp + 1);
           if (box_lb(ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, qf, qf) > bnd) continue;
         }
 #endif
         d3 A, B, C;
         int face;
-        load_tri(tris + first + k, A, B, C, face);
+        load_tri(tris + k, A, B, C, face);
         d3 bary;
         const d3 ql = q;
 #if MFB_TRI_SEL
@@ -712,14 +747,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
           bnd = prune_bound(ds, E);
         }
       }
-      ref = kDone;
-      while (sp > 0) {
-        --sp;
-        if (st_lb[sp] <= bnd) {
-          ref = st_ref[sp];
-          break;
-        }
-      }
+      ref = pop_within(st_ref, st_lb, sp, bnd);
     }
 #endif
     if (!live) continue;
