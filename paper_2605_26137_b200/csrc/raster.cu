@@ -572,7 +572,15 @@ __device__ __forceinline__ void emit_fused(int64_t gi, int x, int y, bool in, ui
 }
 
 template <bool kFused>
-__global__ void __launch_bounds__(256) k_raster(const RasterFace* __restrict__ rf,
+#ifndef MFB_RASTER_MINB
+#define MFB_RASTER_MINB 6  // 40 registers: 6 CTAs per SM (measured 1.676 -> 1.652 ms per bake at config B; 5: 1.660)
+#endif
+#if MFB_RASTER_MINB > 0
+#define MFB_RASTER_BOUNDS __launch_bounds__(256, MFB_RASTER_MINB)
+#else
+#define MFB_RASTER_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
                                                 const AttrFace* __restrict__ attrs,
                                                 const int* __restrict__ tile_start,
                                                 const int* __restrict__ bins, int capacity, int res,
@@ -899,7 +907,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
   if (row_counts_dev) MFB_CUDA_TRY(cudaMemsetAsync(row_counts_dev, 0, sizeof(int64_t) * g.rows, s));
   auto* rc = reinterpret_cast<unsigned long long*>(row_counts_dev);
   if (fused) {
-    MFB_CUDA_TRY(cudaMemsetAsync(fused->q.count, 0, 2 * sizeof(int), s));
+    MFB_CUDA_TRY(cudaMemsetAsync(fused->q.count, 0, 4 * sizeof(int), s));  // [3]: transfer batch cursor
     k_raster<true><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
                                           g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, *fused);
   } else {
@@ -914,7 +922,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
 void gbuffer_queries(Ctx& ctx, cudaStream_t s, const GBufDev& g, const RasterFused& out) {
   const int tiles = ((g.res + kTile - 1) / kTile) * ((g.rows + kTile - 1) / kTile);
   int* overflow = ctx.buf<int>("gq.overflow", 1);
-  MFB_CUDA_TRY(cudaMemsetAsync(out.q.count, 0, 2 * sizeof(int), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(out.q.count, 0, 4 * sizeof(int), s));  // [3]: transfer batch cursor
   k_gbuffer_queries<<<tiles, 256, 0, s>>>(g.res, g.rows, g.pos, g.nrm, g.tan, g.bit, g.valid, g.rel, out,
                                           overflow);
   ctx.count_launch();
