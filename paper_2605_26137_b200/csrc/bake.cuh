@@ -228,6 +228,7 @@ struct RasterFused {
   int32_t* dbg_face = nullptr;
   double* dbg_ts = nullptr;
   unsigned long long* valid_count = nullptr;  // N_v accumulator (optional)
+  int2* pend = nullptr;  // split raster: (slab texel, face) per query, interpolated by k_interp
 };
 
 // Tile-binned rasteriser over rows [g.row0, g.row0 + g.rows). Device flags:

@@ -18,6 +18,8 @@
 //                   f64 attribute interpolation, coalesced G-buffer stores.
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "bake.cuh"
 
 namespace mfb {
@@ -30,6 +32,7 @@ struct alignas(16) RasterFace {
   double doubled;
   double ox[3], oy[3], dx[3], dy[3], sg[3];
   int x0, y0, x1, y1;  // clamped texel bbox; x0 > x1 when the face is skipped
+  int rel, pad[3];     // reliableFaces flag (gbuffer.cpp:74-81), carried for the split raster
 };
 static_assert(sizeof(RasterFace) % 16 == 0, "RasterFace must stay 16-B aligned");
 
@@ -393,6 +396,8 @@ __global__ void k_face_setup(const double* __restrict__ uvs, const int32_t* __re
   attrs[f].pad = 0;
 
   RasterFace s;
+  s.rel = rel;
+  s.pad[0] = s.pad[1] = s.pad[2] = 0;
   const double R = static_cast<double>(res);
   const int u[3] = {fuv[3 * f], fuv[3 * f + 1], fuv[3 * f + 2]};
 #pragma unroll
@@ -571,7 +576,57 @@ __device__ __forceinline__ void emit_fused(int64_t gi, int x, int y, bool in, ui
   store_query(fo.q, pass_a ? slot_a : slot_b, !pass_a, gi, P, Nf, Tf, Bf);
 }
 
-template <bool kFused>
+// gbuffer.cpp:162-186 for texel centre (cx, cy) inside face `sfc`: f64
+// barycentrics, position, renormalised normal, Gram-Schmidt tangent,
+// bitangent = N x T, stored as f32 (the G-buffer's types).
+__device__ __forceinline__ void interp_texel(const RasterFace& sfc, const AttrFace& a, double cx, double cy,
+                                             float* P, float* Nf, float* Tf, float* Bf) {
+  const double px0 = sfc.px[0], py0 = sfc.py[0], px1 = sfc.px[1], py1 = sfc.py[1], px2 = sfc.px[2],
+               py2 = sfc.py[2];
+  const double w0 = cross2(px2 - px1, py2 - py1, cx - px1, cy - py1) / sfc.doubled;
+  const double w1 = cross2(px0 - px2, py0 - py2, cx - px2, cy - py2) / sfc.doubled;
+  const double w2 = cross2(px1 - px0, py1 - py0, cx - px0, cy - py0) / sfc.doubled;
+  const d3 pos = (w0 * ld3(a.P) + w1 * ld3(a.P + 3)) + w2 * ld3(a.P + 6);
+  d3 n = (w0 * ld3(a.N) + w1 * ld3(a.N + 3)) + w2 * ld3(a.N + 6);
+  const double nl = norm(n);
+  n = nl > 1e-12 ? n / nl : ld3(a.N);
+  d3 tg = (w0 * ld3(a.T) + w1 * ld3(a.T + 3)) + w2 * ld3(a.T + 6);
+  tg = tg - n * dot(n, tg);
+  const double tl = norm(tg);
+  tg = tl > 1e-12 ? tg / tl : any_perpendicular(n);
+  const d3 bt = cross(n, tg);
+  P[0] = __double2float_rn(pos.x);
+  P[1] = __double2float_rn(pos.y);
+  P[2] = __double2float_rn(pos.z);
+  Nf[0] = __double2float_rn(n.x);
+  Nf[1] = __double2float_rn(n.y);
+  Nf[2] = __double2float_rn(n.z);
+  Tf[0] = __double2float_rn(tg.x);
+  Tf[1] = __double2float_rn(tg.y);
+  Tf[2] = __double2float_rn(tg.z);
+  Bf[0] = __double2float_rn(bt.x);
+  Bf[1] = __double2float_rn(bt.y);
+  Bf[2] = __double2float_rn(bt.z);
+}
+
+// Split raster, second kernel: one thread per compacted query (texel, face)
+// written by k_raster<2>; interpolates exactly as the fused path and writes
+// the same query record. No barriers, full SIMT width for the f64 chain.
+__global__ void __launch_bounds__(256) k_interp(const RasterFace* __restrict__ rf,
+                                                const AttrFace* __restrict__ attrs,
+                                                const int2* __restrict__ pend, const int* __restrict__ count,
+                                                int res, int g_row0, QueryList q) {
+  const int n = *count;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int2 tf = pend[i];
+    const int yr = tf.x / res, x = tf.x - yr * res;
+    const double cx = x + 0.5, cy = (yr + g_row0) + 0.5;
+    float P[3], Nf[3], Tf[3], Bf[3];
+    interp_texel(rf[tf.y], attrs[tf.y], cx, cy, P, Nf, Tf, Bf);
+    store_query(q, i, false, tf.x, P, Nf, Tf, Bf);
+  }
+}
+
 #ifndef MFB_RASTER_MINB
 #define MFB_RASTER_MINB 6  // 40 registers: 6 CTAs per SM (measured 1.676 -> 1.652 ms per bake at config B; 5: 1.660)
 #endif
@@ -580,6 +635,10 @@ template <bool kFused>
 #else
 #define MFB_RASTER_BOUNDS __launch_bounds__(256)
 #endif
+// kMode 0: full G-buffer planes (mf_raster_gbuffer); 1: fused bake, query
+// records interpolated in-kernel; 2: fused bake, split: coverage and
+// compaction here, (texel, face) pairs to fo.pend, k_interp interpolates.
+template <int kMode>
 __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
                                                 const AttrFace* __restrict__ attrs,
                                                 const int* __restrict__ tile_start,
@@ -602,7 +661,7 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
   const bool in = x < res && y < row_end;
   const double cx = x + 0.5, cy = y + 0.5;
   const int b = tile_start[t], e = min(tile_start[t + 1], capacity);
-  int cover = -1, hits = 0;
+  int cover = -1, hits = 0, crel = 0;
   for (int base = b; base < e; base += kChunk) {
     const int n = min(kChunk, e - base);
     __syncthreads();
@@ -632,7 +691,10 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
         }
         if (!inside) continue;
         ++hits;
-        if (cover < 0 || sfid[i] < cover) cover = sfid[i];
+        if (cover < 0 || sfid[i] < cover) {
+          cover = sfid[i];
+          crel = sfc.rel;
+        }
       }
     }
   }
@@ -640,37 +702,14 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
   const int64_t gi = static_cast<int64_t>(y - g_row0) * res + x;
   float P[3] = {0.f, 0.f, 0.f}, Nf[3] = {0.f, 0.f, 0.f}, Tf[3] = {0.f, 0.f, 0.f}, Bf[3] = {0.f, 0.f, 0.f};
   uint8_t valid = 0, rel = 0;
-  if (in && cover >= 0) {
-    const RasterFace& sfc = rf[cover];
-    const AttrFace& a = attrs[cover];
-    const double px0 = sfc.px[0], py0 = sfc.py[0], px1 = sfc.px[1], py1 = sfc.py[1], px2 = sfc.px[2],
-                 py2 = sfc.py[2];
-    const double w0 = cross2(px2 - px1, py2 - py1, cx - px1, cy - py1) / sfc.doubled;
-    const double w1 = cross2(px0 - px2, py0 - py2, cx - px2, cy - py2) / sfc.doubled;
-    const double w2 = cross2(px1 - px0, py1 - py0, cx - px0, cy - py0) / sfc.doubled;
-    const d3 pos = (w0 * ld3(a.P) + w1 * ld3(a.P + 3)) + w2 * ld3(a.P + 6);
-    d3 n = (w0 * ld3(a.N) + w1 * ld3(a.N + 3)) + w2 * ld3(a.N + 6);
-    const double nl = norm(n);
-    n = nl > 1e-12 ? n / nl : ld3(a.N);
-    d3 tg = (w0 * ld3(a.T) + w1 * ld3(a.T + 3)) + w2 * ld3(a.T + 6);
-    tg = tg - n * dot(n, tg);
-    const double tl = norm(tg);
-    tg = tl > 1e-12 ? tg / tl : any_perpendicular(n);
-    const d3 bt = cross(n, tg);
-    P[0] = __double2float_rn(pos.x);
-    P[1] = __double2float_rn(pos.y);
-    P[2] = __double2float_rn(pos.z);
-    Nf[0] = __double2float_rn(n.x);
-    Nf[1] = __double2float_rn(n.y);
-    Nf[2] = __double2float_rn(n.z);
-    Tf[0] = __double2float_rn(tg.x);
-    Tf[1] = __double2float_rn(tg.y);
-    Tf[2] = __double2float_rn(tg.z);
-    Bf[0] = __double2float_rn(bt.x);
-    Bf[1] = __double2float_rn(bt.y);
-    Bf[2] = __double2float_rn(bt.z);
+  if (kMode != 2 && in && cover >= 0) {
+    interp_texel(rf[cover], attrs[cover], cx, cy, P, Nf, Tf, Bf);
     valid = 1;
-    rel = static_cast<uint8_t>(a.reliable);
+    rel = static_cast<uint8_t>(attrs[cover].reliable);
+  }
+  if (kMode == 2 && in && cover >= 0) {
+    valid = 1;
+    rel = static_cast<uint8_t>(crel);
   }
   if (row_counts) {
     // warp = 8 columns x 4 rows: lanes 8r..8r+7 share row r
@@ -682,8 +721,29 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
       if (rowbits && yr < row_end) atomicAdd(&row_counts[yr - row_begin], static_cast<unsigned long long>(__popc(rowbits)));
     }
   }
-  if (kFused) {
+  if (kMode == 1) {
     emit_fused(gi, x, y, in, valid, rel, P, Nf, Tf, Bf, gvalid, fo, &flags[3]);
+    return;
+  }
+  if (kMode == 2) {
+    const bool is_q = in && valid && rel;
+    const int slot = compact_slot(is_q, fo.q.count, fo.q.capacity, &flags[3], in && valid != 0, fo.valid_count);
+    if (!in) return;
+    if (gvalid) gvalid[gi] = valid;
+    if (is_q) {
+      if (slot >= 0) fo.pend[slot] = make_int2(static_cast<int>(gi), cover);
+      return;
+    }
+    uint8_t* o = fo.rgb + 3 * gi;
+    o[0] = 128;
+    o[1] = 128;
+    o[2] = valid ? 255 : 128;  // gbuffer.cpp:212-213 background / neutral
+    if (fo.dbg_face) fo.dbg_face[gi] = valid ? -2 : -1;
+    if (fo.dbg_ts) {
+      fo.dbg_ts[3 * gi] = 0.0;
+      fo.dbg_ts[3 * gi + 1] = 0.0;
+      fo.dbg_ts[3 * gi + 2] = 0.0;
+    }
     return;
   }
   if (!in) return;
@@ -906,14 +966,28 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
   MFB_CUDA_TRY(cudaMemcpyAsync(flags_dev + 2, start + ntiles, sizeof(int), cudaMemcpyDeviceToDevice, s));
   if (row_counts_dev) MFB_CUDA_TRY(cudaMemsetAsync(row_counts_dev, 0, sizeof(int64_t) * g.rows, s));
   auto* rc = reinterpret_cast<unsigned long long*>(row_counts_dev);
-  if (fused) {
+  // Split raster (default): coverage + compaction, then a barrier-free
+  // interpolation kernel over the compacted queries. MFB_RASTER_SPLIT=0
+  // selects the single fused kernel (A/B).
+  static const bool split = [] {
+    const char* e = std::getenv("MFB_RASTER_SPLIT");
+    return !(e && e[0] == '0') && !kSeedPasses;
+  }();
+  if (fused && split) {
     MFB_CUDA_TRY(cudaMemsetAsync(fused->q.count, 0, 4 * sizeof(int), s));  // [3]: transfer batch cursor
-    k_raster<true><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
-                                          g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, *fused);
+    RasterFused f2 = *fused;
+    f2.pend = ctx.buf<int2>("ras.pend", g.texels());
+    k_raster<2><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
+                                       g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, f2);
+    k_interp<<<kNumSMs * 8, 256, 0, s>>>(rf, attrs, f2.pend, fused->q.count, res, g.row0, fused->q);
+    ctx.count_launch();
+  } else if (fused) {
+    MFB_CUDA_TRY(cudaMemsetAsync(fused->q.count, 0, 4 * sizeof(int), s));  // [3]: transfer batch cursor
+    k_raster<1><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
+                                       g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, *fused);
   } else {
-    k_raster<false><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0,
-                                           g.pos, g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc,
-                                           RasterFused{});
+    k_raster<0><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0,
+                                       g.pos, g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, RasterFused{});
   }
   ctx.count_launch(3);
   MFB_CUDA_TRY(cudaGetLastError());
