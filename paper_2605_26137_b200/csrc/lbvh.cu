@@ -101,7 +101,8 @@ __device__ __forceinline__ uint32_t spread10(uint32_t v) {
 // ties with the primitive index.
 __global__ void k_morton(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
                          const unsigned long long* __restrict__ acc, uint32_t* __restrict__ keys,
-                         uint32_t* __restrict__ vals) {
+                         uint32_t* __restrict__ vals, int axis_bits) {
+  const double cells = static_cast<double>((1 << axis_bits) - 1);
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
   double lo[3], inv[3];
@@ -109,7 +110,7 @@ __global__ void k_morton(const double* __restrict__ pos, const int32_t* __restri
   for (int k = 0; k < 3; ++k) {
     lo[k] = from_ordered(acc[k]);
     const double ext = from_ordered(acc[3 + k]) - lo[k];
-    inv[k] = ext > 0.0 ? 1023.0 / ext : 0.0;
+    inv[k] = ext > 0.0 ? cells / ext : 0.0;
   }
   const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
   uint32_t q[3];
@@ -117,7 +118,7 @@ __global__ void k_morton(const double* __restrict__ pos, const int32_t* __restri
   for (int k = 0; k < 3; ++k) {
     const double ck = ((pos[3 * a + k] + pos[3 * b + k]) + pos[3 * c + k]) / 3.0;
     double t = (ck - lo[k]) * inv[k];
-    t = fmin(fmax(t, 0.0), 1023.0);
+    t = fmin(fmax(t, 0.0), cells);
     q[k] = static_cast<uint32_t>(t);
   }
   keys[f] = (spread10(q[0]) << 2) | (spread10(q[1]) << 1) | spread10(q[2]);
@@ -133,37 +134,53 @@ __device__ __forceinline__ int kdelta(const uint32_t* __restrict__ k, int n, int
 }
 
 // parent links: (parent << 1) | side; prim_parent for primitives, node_parent for internals.
+// Also appends every reachable node with a leaf-range child to `starts`
+// (count in starts_n): the refit climbs start there, so it never reads the
+// nodes buried inside leaf ranges.
 __global__ void k_emit(const uint32_t* __restrict__ keys, int n, int leaf_max, BNode* __restrict__ nodes,
-                       int32_t* __restrict__ prim_parent, int32_t* __restrict__ node_parent) {
+                       int32_t* __restrict__ prim_parent, int32_t* __restrict__ node_parent,
+                       int32_t* __restrict__ starts, int* __restrict__ starts_n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n - 1) return;
-  const int d = (kdelta(keys, n, i, i + 1) - kdelta(keys, n, i, i - 1)) > 0 ? 1 : -1;
-  const int dmin = kdelta(keys, n, i, i - d);
-  int lmax = 2;
-  while (kdelta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
-  int l = 0;
-  for (int t = lmax >> 1; t >= 1; t >>= 1)
-    if (kdelta(keys, n, i, i + (l + t) * d) > dmin) l += t;
-  const int j = i + l * d;
-  const int dnode = kdelta(keys, n, i, j);
-  int s = 0, t = l;
-  do {
-    t = (t + 1) >> 1;
-    if (kdelta(keys, n, i, i + (s + t) * d) > dnode) s += t;
-  } while (t > 1);
-  const int gamma = i + s * d + min(d, 0);
-  const int first = min(i, j), last = max(i, j);
-  const int cl = gamma - first + 1, cr = last - gamma;
-  int4 dd;
-  dd.x = cl <= leaf_max ? leaf_ref(first, cl) : gamma;
-  dd.y = cr <= leaf_max ? leaf_ref(gamma + 1, cr) : gamma + 1;
-  dd.z = first;
-  dd.w = last - first + 1;
-  nodes[i].d = dd;
-  if (first == gamma) prim_parent[gamma] = (i << 1) | 0;
-  else node_parent[gamma] = (i << 1) | 0;
-  if (last == gamma + 1) prim_parent[gamma + 1] = (i << 1) | 1;
-  else node_parent[gamma + 1] = (i << 1) | 1;
+  const bool active = i < n - 1;
+  bool start = false;
+  if (active) {
+    const int d = (kdelta(keys, n, i, i + 1) - kdelta(keys, n, i, i - 1)) > 0 ? 1 : -1;
+    const int dmin = kdelta(keys, n, i, i - d);
+    int lmax = 2;
+    while (kdelta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
+    int l = 0;
+    for (int t = lmax >> 1; t >= 1; t >>= 1)
+      if (kdelta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+    const int j = i + l * d;
+    const int dnode = kdelta(keys, n, i, j);
+    int s = 0, t = l;
+    do {
+      t = (t + 1) >> 1;
+      if (kdelta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+    } while (t > 1);
+    const int gamma = i + s * d + min(d, 0);
+    const int first = min(i, j), last = max(i, j);
+    const int cl = gamma - first + 1, cr = last - gamma;
+    int4 dd;
+    dd.x = cl <= leaf_max ? leaf_ref(first, cl) : gamma;
+    dd.y = cr <= leaf_max ? leaf_ref(gamma + 1, cr) : gamma + 1;
+    dd.z = first;
+    dd.w = last - first + 1;
+    nodes[i].d = dd;
+    if (first == gamma) prim_parent[gamma] = (i << 1) | 0;
+    else node_parent[gamma] = (i << 1) | 0;
+    if (last == gamma + 1) prim_parent[gamma + 1] = (i << 1) | 1;
+    else node_parent[gamma + 1] = (i << 1) | 1;
+    start = (i == 0 || dd.w > leaf_max) && (dd.x < 0 || dd.y < 0);
+  }
+  // warp-aggregated append
+  const unsigned m = __ballot_sync(0xffffffffu, start);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(starts_n, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (start) starts[base + __popc(m & ((1u << lane) - 1u))] = i;
 }
 
 struct FBox {
@@ -283,13 +300,14 @@ __global__ void k_refit(const TBox* __restrict__ tbox, int n, BNode* nodes, cons
 // slots and counts them as arrivals; a node is complete after two arrivals,
 // and the thread that completes it carries its box up to the parent's slot
 // (acquire/release counter per node).
-__global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __restrict__ nodes_in, int n_nodes,
-                               int leaf_max, BNode* nodes, const int32_t* __restrict__ node_parent,
+__global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __restrict__ nodes_in,
+                               const int32_t* __restrict__ starts, const int* __restrict__ starts_n,
+                               BNode* nodes, const int32_t* __restrict__ node_parent,
                                int* __restrict__ flags, float* __restrict__ root_box) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_nodes) return;
+  const int si = blockIdx.x * blockDim.x + threadIdx.x;
+  if (si >= *starts_n) return;
+  const int i = starts[si];
   const int4 d = nodes_in[i].d;
-  if (i != 0 && d.w <= leaf_max) return;       // unreachable: inside a leaf range
   const int refs[2] = {d.x, d.y};
   FBox box;
 #pragma unroll
@@ -439,6 +457,8 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   auto* prim_parent = ctx.buf<int32_t>(tag + ".pparent", n);
   auto* node_parent = ctx.buf<int32_t>(tag + ".nparent", n);
   auto* flags = ctx.buf<int>(tag + ".flags", n);
+  auto* starts = ctx.buf<int32_t>(tag + ".starts", n);
+  auto* starts_n = ctx.buf<int>(tag + ".starts_n", 1);
 
   MFB_CUDA_TRY(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
   MFB_CUDA_TRY(cudaMemsetAsync(acc + 3, 0x00, 5 * sizeof(unsigned long long), s));
@@ -447,13 +467,20 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   const int T = 256;
   const int grid_b = std::min(div_up(std::max(n, m.nv), T), kNumSMs * 8);
   k_bounds<<<grid_b, T, 0, s>>>(m.pos, m.faces, n, m.nv, acc);
-  k_morton<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, n, acc, keys, vals);
+  // Morton bits per axis: 10 (30-bit keys, 4 radix passes) unless
+  // MFB_MORTON_BITS (6..10) overrides it; fewer bits = fewer sort passes.
+  static const int axis_bits = [] {
+    const char* e = std::getenv("MFB_MORTON_BITS");
+    const int v = e ? std::atoi(e) : 10;
+    return v >= 6 && v <= 10 ? v : 10;
+  }();
+  k_morton<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, n, acc, keys, vals, axis_bits);
   ctx.count_launch(2);
 
   size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, vals, vals2, n, 0, 30, s);
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, vals, vals2, n, 0, 3 * axis_bits, s);
   void* tptr = ctx.cub_temp(tmp, s);
-  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 30, s));
+  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 3 * axis_bits, s));
 
   // Leaf size: kLeafMaxDefault (the reference uses 4, bvh.cpp:13; the
   // results are tree-independent) unless MFB_LEAF_MAX (1..7) overrides it.
@@ -463,13 +490,16 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
     return v >= 1 && v <= 7 ? v : kLeafMaxDefault;
   }();
   if (n > 1) {
-    k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent);
+    MFB_CUDA_TRY(cudaMemsetAsync(starts_n, 0, sizeof(int), s));
+    k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent, starts,
+                                          starts_n);
     ctx.count_launch();
   }
   k_repack<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
   if (n > 1) {
-    k_refit_ranges<<<div_up(out.n_nodes, T), T, 0, s>>>(out.tbox, out.nodes, out.n_nodes, leaf_max, out.nodes,
-                                                         node_parent, flags, out.root_box_dev);
+    // starts <= leaf ranges <= n; threads past the device count exit at once
+    k_refit_ranges<<<div_up(n, T), T, 0, s>>>(out.tbox, out.nodes, starts, starts_n, out.nodes,
+                                                       node_parent, flags, out.root_box_dev);
   } else {
     k_refit<<<1, 32, 0, s>>>(out.tbox, n, out.nodes, prim_parent, node_parent, flags, out.root_box_dev);
   }
