@@ -612,7 +612,15 @@ __device__ __forceinline__ void interp_texel(const RasterFace& sfc, const AttrFa
 // Split raster, second kernel: one thread per compacted query (texel, face)
 // written by k_raster<2>; interpolates exactly as the fused path and writes
 // the same query record. No barriers, full SIMT width for the f64 chain.
-__global__ void __launch_bounds__(256) k_interp(const RasterFace* __restrict__ rf,
+#ifndef MFB_INTERP_MINB
+#define MFB_INTERP_MINB 0
+#endif
+#if MFB_INTERP_MINB > 0
+#define MFB_INTERP_BOUNDS __launch_bounds__(256, MFB_INTERP_MINB)
+#else
+#define MFB_INTERP_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void MFB_INTERP_BOUNDS k_interp(const RasterFace* __restrict__ rf,
                                                 const AttrFace* __restrict__ attrs,
                                                 const int2* __restrict__ pend, const int* __restrict__ count,
                                                 int res, int g_row0, QueryList q) {
