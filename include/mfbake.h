@@ -211,9 +211,11 @@ int mf_fibonacci_cameras(int count, double half_extent, double* cameras);
  * at resolution^2 pixels each, one pixel ray per thread through the LBVH of
  * `mesh` (built per call). Per view, row-major: face i32 (-1 background),
  * depth f32 (+inf background), position f32x3, normal f32x3 (interpolated
- * `vertex_normals`, V x 3 f64; zero when null). Any output may be null. */
+ * `vertex_normals`, V x 3 f64; zero when null). backface_cull != 0 is
+ * RasterOptions::backfaceCull (raster.h:29-33). Any output may be null. */
 int mf_render_views(mf_ctx* ctx, const mf_mesh_view* mesh, const double* cameras, int n_views, int resolution,
-                    const double* vertex_normals, int32_t* face, float* depth, float* position, float* normal);
+                    const double* vertex_normals, int backface_cull, int32_t* face, float* depth, float* position,
+                    float* normal);
 /* castVisibility (visibility/visibility.cpp:13-59): the mesh centred on its
  * bounds, `viewpoints` fibonacci cameras of half extent 1.04 x its bounding
  * radius, resolution^2 pixel rays each; hits[f] = pixels face f won over all

@@ -159,7 +159,7 @@ class Port(_Lib):
         self.fn("fibonacci_cameras")(ctypes.c_int(count), ctypes.c_double(half_extent), _ptr(cams))
         return cams
 
-    def render_views(self, m: TriangleMesh, cams: np.ndarray, res: int, vn=None):
+    def render_views(self, m: TriangleMesh, cams: np.ndarray, res: int, vn=None, cull: bool = False):
         cams = np.ascontiguousarray(cams, dtype=np.float64).reshape(-1, 7)
         nvw = cams.shape[0]
         face = np.zeros((nvw, res, res), np.int32)
@@ -169,7 +169,8 @@ class Port(_Lib):
         vn = None if vn is None else np.ascontiguousarray(vn, dtype=np.float64)
         v = m.view()
         self._check(self.fn("render_views")(ctypes.byref(v), _ptr(cams), ctypes.c_int(nvw), ctypes.c_int(res),
-                                            _ptr(vn), _ptr(face), _ptr(depth), _ptr(pos), _ptr(nrm)))
+                                            _ptr(vn), ctypes.c_int(int(cull)), _ptr(face), _ptr(depth), _ptr(pos),
+                                            _ptr(nrm)))
         return face, depth, pos, nrm
 
     def cast_visibility(self, m: TriangleMesh, viewpoints: int, res: int) -> np.ndarray:
@@ -290,7 +291,7 @@ class Ref(_Lib):
                                      _ptr(cams))
         return cams
 
-    def render_views(self, m: TriangleMesh, cams: np.ndarray, res: int, vn=None):
+    def render_views(self, m: TriangleMesh, cams: np.ndarray, res: int, vn=None, cull: bool = False):
         cams = np.ascontiguousarray(cams, dtype=np.float64).reshape(-1, 7)
         nvw = cams.shape[0]
         face = np.zeros((nvw, res, res), np.int32)
@@ -300,7 +301,8 @@ class Ref(_Lib):
         vn = None if vn is None else np.ascontiguousarray(vn, dtype=np.float64)
         v = m.view()
         self._check(self.fn("render_views")(ctypes.byref(v), _ptr(cams), ctypes.c_int(nvw), ctypes.c_int(res),
-                                            _ptr(vn), _ptr(face), _ptr(depth), _ptr(pos), _ptr(nrm)))
+                                            _ptr(vn), ctypes.c_int(int(cull)), _ptr(face), _ptr(depth), _ptr(pos),
+                                            _ptr(nrm)))
         return face, depth, pos, nrm
 
     def cast_visibility(self, m: TriangleMesh, viewpoints: int, res: int) -> np.ndarray:

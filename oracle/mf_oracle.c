@@ -1165,8 +1165,8 @@ void orc_fibonacci_cameras(int count, double half_extent, double* cams7) {
  * padded pixel box, Moller-Trumbore with the hoisted per-face factors, z-test
  * "replace iff depth > stored" (ties keep the lower face). Outputs nullable
  * except face/depth scratch. */
-static void render_view(const mf_mesh_view* m, const double* vn, const double* cam7, int res, int32_t* face,
-                        float* depth, float* pos, float* nrm) {
+static void render_view(const mf_mesh_view* m, const double* vn, const double* cam7, int res, int cull,
+                        int32_t* face, float* depth, float* pos, float* nrm) {
   const d3 dir = ld3(cam7), up = ld3(cam7 + 3);
   const d3 right = cross3(dir, up);
   const double he = cam7[6];
@@ -1189,6 +1189,7 @@ static void render_view(const mf_mesh_view* m, const double* vn, const double* c
   for (int f = 0; f < m->n_faces; ++f) {
     const int* tri = m->faces + 3 * (size_t)f;
     const d3 a = P(m, tri[0]), b = P(m, tri[1]), c = P(m, tri[2]);
+    if (cull && dot3(cross3(sub3(b, a), sub3(c, a)), dir) > 0.0) continue; /* raster.cpp:44 */
     const double u0 = dot3(a, right), u1 = dot3(b, right), u2 = dot3(c, right);
     const double v0 = dot3(a, up), v1 = dot3(b, up), v2 = dot3(c, up);
     const double umin = fmin(u0, fmin(u1, u2)), umax = fmax(u0, fmax(u1, u2));
@@ -1239,11 +1240,11 @@ static void render_view(const mf_mesh_view* m, const double* vn, const double* c
   free(rowV);
 }
 
-int orc_render_views(const mf_mesh_view* m, const double* cams7, int n_views, int res, const double* vn,
+int orc_render_views(const mf_mesh_view* m, const double* cams7, int n_views, int res, const double* vn, int cull,
                      int32_t* face, float* depth, float* pos, float* nrm) {
   const size_t n = (size_t)res * res;
   for (int v = 0; v < n_views; ++v)
-    render_view(m, vn, cams7 + 7 * v, res, face + v * n, depth + v * n, pos ? pos + 3 * v * n : NULL,
+    render_view(m, vn, cams7 + 7 * v, res, cull, face + v * n, depth + v * n, pos ? pos + 3 * v * n : NULL,
                 nrm ? nrm + 3 * v * n : NULL);
   return 0;
 }
@@ -1282,7 +1283,7 @@ int orc_cast_visibility(const mf_mesh_view* m, int viewpoints, int res, int64_t*
   float* depth = (float*)malloc(sizeof(float) * n);
   memset(hits, 0, sizeof(int64_t) * (size_t)m->n_faces);
   for (int v = 0; v < viewpoints; ++v) {
-    render_view(&cm, NULL, cams + 7 * v, res, face, depth, NULL, NULL);
+    render_view(&cm, NULL, cams + 7 * v, res, 0, face, depth, NULL, NULL);
     for (size_t i = 0; i < n; ++i)
       if (face[i] >= 0) ++hits[face[i]];
   }

@@ -65,7 +65,7 @@ int orc_surface_band(const mf_mesh_view* m, int res, double band_voxels, int dil
 
 /* render/camera.cpp:38-55, render/raster.cpp:12-102, visibility/visibility.cpp:13-59 */
 void orc_fibonacci_cameras(int count, double half_extent, double* cams7);
-int orc_render_views(const mf_mesh_view* m, const double* cams7, int n_views, int res, const double* vn,
+int orc_render_views(const mf_mesh_view* m, const double* cams7, int n_views, int res, const double* vn, int cull,
                      int32_t* face, float* depth, float* pos, float* nrm);
 int orc_cast_visibility(const mf_mesh_view* m, int viewpoints, int res, int64_t* hits);
 

@@ -379,7 +379,7 @@ void ref_fibonacci_cameras(int count, int res, double half_extent, double* cams7
 
 // renderView (src/render/raster.cpp:12-102) per camera.
 int ref_render_views(const mf_mesh_view* mesh, const double* cams7, int n_views, int res, const double* vn,
-                     int32_t* face, float* depth, float* pos, float* nrm) {
+                     int cull, int32_t* face, float* depth, float* pos, float* nrm) {
   return guarded([&] {
     const TriangleMesh m = toMesh(mesh);
     std::vector<Eigen::Vector3d> normals(m.positions.size(), Eigen::Vector3d::Zero());
@@ -392,7 +392,9 @@ int ref_render_views(const mf_mesh_view* mesh, const double* cams7, int n_views,
       cam.up = {cams7[7 * v + 3], cams7[7 * v + 4], cams7[7 * v + 5]};
       cam.halfExtent = cams7[7 * v + 6];
       cam.resolution = res;
-      const RenderedView r = renderView(m, normals, cam, {});
+      RasterOptions opt;
+      opt.backfaceCull = cull != 0;
+      const RenderedView r = renderView(m, normals, cam, opt);
       std::memcpy(face + v * n, r.face.data.data(), n * sizeof(int32_t));
       std::memcpy(depth + v * n, r.depth.data.data(), n * sizeof(float));
       if (pos) std::memcpy(pos + 3 * v * n, r.position.data.data(), 3 * n * sizeof(float));

@@ -90,7 +90,7 @@ SIGNATURES = [
     ("mf_surface_band", _I, [_VP, _I, _D, _I, _VP, _VP, _VP, _VP]),
     ("mf_surface_band_dev", _I, [_VP, _I, _D, _I, _VP, _VP, _VP, _VP]),
     ("mf_fibonacci_cameras", _I, [_I, _D, _VP]),
-    ("mf_render_views", _I, [_VP, _MV, _VP, _I, _I, _VP, _VP, _VP, _VP, _VP]),
+    ("mf_render_views", _I, [_VP, _MV, _VP, _I, _I, _VP, _I, _VP, _VP, _VP, _VP]),
     ("mf_cast_visibility", _I, [_VP, _MV, _I, _I, _VP, _VP]),
     ("mf_closest_point_brute", _I, [_VP, _MV, _VP, _I64, _VP, _VP, _VP, _VP]),
     ("mf_raycast_first_brute", _I, [_VP, _MV, _VP, _VP, _I64, _D, _D, _VP, _VP, _VP, _VP]),

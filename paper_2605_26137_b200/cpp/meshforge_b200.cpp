@@ -17,7 +17,10 @@
 #include "meshforge/bake/tangent.h"
 #include "meshforge/core/error.h"
 #include "meshforge/core/mesh.h"
+#include "meshforge/render/camera.h"
+#include "meshforge/render/raster.h"
 #include "meshforge/signfield/sign_grid.h"
+#include "meshforge/visibility/visibility.h"
 #include "meshforge/spatial/bvh.h"
 #include "mfbake.h"
 
@@ -312,6 +315,114 @@ SignGrid markSurfaceBand(const TriangleMesh& mesh, const Bvh& bvh, const GridPar
   g.labels.resize(labels.size());
   for (std::size_t i = 0; i < labels.size(); ++i) g.labels[i] = static_cast<VoxelLabel>(labels[i]);
   return g;
+}
+
+// ------------------------------------------------------------------ cameras, views, visibility
+std::vector<OrthoCamera> standardCameras(int resolution, double halfExtent) {  // render/camera.cpp:7-31
+  const double s2 = std::sqrt(0.5);
+  const double cosA[8] = {1, s2, 0, -s2, -1, -s2, 0, s2};
+  const double sinA[8] = {0, s2, 1, s2, 0, -s2, -1, -s2};
+  std::vector<OrthoCamera> cams(10);
+  for (int k = 0; k < 8; ++k) {
+    cams[k].direction = Eigen::Vector3d(-cosA[k], -sinA[k], 0.0);
+    cams[k].up = Eigen::Vector3d(0, 0, 1);
+  }
+  cams[8].direction = Eigen::Vector3d(0, 0, -1);
+  cams[8].up = Eigen::Vector3d(0, 1, 0);
+  cams[9].direction = Eigen::Vector3d(0, 0, 1);
+  cams[9].up = Eigen::Vector3d(0, 1, 0);
+  for (auto& cam : cams) {
+    cam.halfExtent = halfExtent;
+    cam.resolution = resolution;
+  }
+  return cams;
+}
+
+std::vector<OrthoCamera> fibonacciCameras(int count, int resolution, double halfExtent) {
+  std::vector<double> raw(7 * static_cast<size_t>(std::max(count, 0)));
+  check(mf_fibonacci_cameras(count, halfExtent, raw.data()));
+  std::vector<OrthoCamera> cams(std::max(count, 0));
+  for (int i = 0; i < count; ++i) {
+    const double* c = raw.data() + 7 * i;
+    cams[i].direction = Eigen::Vector3d(c[0], c[1], c[2]);
+    cams[i].up = Eigen::Vector3d(c[3], c[4], c[5]);
+    cams[i].halfExtent = c[6];
+    cams[i].resolution = resolution;
+  }
+  return cams;
+}
+
+namespace {
+// One mf_render_views call for cameras sharing a resolution.
+std::vector<RenderedView> renderSameRes(const TriangleMesh& mesh, const std::vector<Eigen::Vector3d>& vn,
+                                        const std::vector<OrthoCamera>& cams, const RasterOptions& options) {
+  std::vector<RenderedView> out;
+  if (cams.empty()) return out;
+  const int res = cams[0].resolution;
+  const size_t px = static_cast<size_t>(res) * res;
+  std::vector<double> raw(7 * cams.size());
+  for (size_t i = 0; i < cams.size(); ++i) {
+    for (int k = 0; k < 3; ++k) {
+      raw[7 * i + k] = cams[i].direction[k];
+      raw[7 * i + 3 + k] = cams[i].up[k];
+    }
+    raw[7 * i + 6] = cams[i].halfExtent;
+  }
+  std::vector<std::int32_t> face(px * cams.size());
+  std::vector<float> depth(px * cams.size()), pos(3 * px * cams.size()), nrm(3 * px * cams.size());
+  const mf_mesh_view v = viewOf(mesh);
+  check(mf_render_views(context(), &v, raw.data(), static_cast<int>(cams.size()), res,
+                        vn.empty() ? nullptr : vn.data()->data(), options.backfaceCull ? 1 : 0, face.data(),
+                        depth.data(), pos.data(), nrm.data()));
+  out.resize(cams.size());
+  for (size_t i = 0; i < cams.size(); ++i) {
+    RenderedView& r = out[i];
+    r.face = Image<std::int32_t>(res, res, 1);
+    r.depth = ImageF(res, res, 1);
+    r.position = ImageF(res, res, 3);
+    r.normal = ImageF(res, res, 3);
+    std::memcpy(r.face.data.data(), face.data() + i * px, px * sizeof(std::int32_t));
+    std::memcpy(r.depth.data.data(), depth.data() + i * px, px * sizeof(float));
+    std::memcpy(r.position.data.data(), pos.data() + 3 * i * px, 3 * px * sizeof(float));
+    std::memcpy(r.normal.data.data(), nrm.data() + 3 * i * px, 3 * px * sizeof(float));
+  }
+  return out;
+}
+}  // namespace
+
+RenderedView renderView(const TriangleMesh& mesh, const std::vector<Eigen::Vector3d>& vertexNormals,
+                        const OrthoCamera& camera, const RasterOptions& options) {
+  return renderSameRes(mesh, vertexNormals, {camera}, options)[0];
+}
+
+ViewSet renderGeometry(const TriangleMesh& mesh, const std::vector<OrthoCamera>& cameras,
+                       const RasterOptions& options) {  // render/raster.cpp:104-115
+  ViewSet set;
+  set.cameras = cameras;
+  set.views.resize(cameras.size());
+  const std::vector<Eigen::Vector3d> normals = mesh.hasNormals() ? mesh.normals : computeVertexNormals(mesh);
+  for (size_t i = 0; i < cameras.size();) {  // batch consecutive cameras of one resolution
+    size_t j = i + 1;
+    while (j < cameras.size() && cameras[j].resolution == cameras[i].resolution) ++j;
+    std::vector<OrthoCamera> batch(cameras.begin() + i, cameras.begin() + j);
+    std::vector<RenderedView> views = renderSameRes(mesh, normals, batch, options);
+    for (size_t k = i; k < j; ++k) set.views[k] = std::move(views[k - i]);
+    i = j;
+  }
+  return set;
+}
+
+VisibilityMask castVisibility(const TriangleMesh& mesh, int viewpoints, int resolution) {
+  VisibilityMask mask;
+  mask.hits.assign(mesh.faceCount(), 0);
+  std::vector<std::uint8_t> state(mesh.faceCount() > 0 ? mesh.faceCount() : 1);
+  const mf_mesh_view v = viewOf(mesh);
+  std::int64_t dummy = 0;
+  check(mf_cast_visibility(context(), &v, viewpoints, resolution, mesh.faceCount() > 0 ? mask.hits.data() : &dummy,
+                           state.data()));
+  mask.state.resize(mesh.faceCount());
+  for (int f = 0; f < mesh.faceCount(); ++f) mask.state[f] = static_cast<FaceVisibility>(state[f]);
+  return mask;
 }
 
 }  // namespace meshforge

@@ -272,7 +272,7 @@ void surface_band(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, int res, const doub
 // Ortho pixel-ray views (renderView, render/raster.cpp:12-102): cams7 = per
 // view direction xyz, up xyz, halfExtent. Optional outputs: per-face won-pixel
 // counters (castVisibility), per-view face / depth / position / normal images.
-void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7, int nviews, int res,
+void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7, int nviews, int res, int cull,
                   unsigned long long* hits, int32_t* face_img, float* depth_img, float* pos_img, float* nrm_img,
                   const int32_t* faces, const double* vnormals);
 // fibonacciCameras (render/camera.cpp:38-55) into cams7 (host).

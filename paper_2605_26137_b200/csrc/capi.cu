@@ -1497,7 +1497,8 @@ int mf_fibonacci_cameras(int count, double half_extent, double* cameras) {
 }
 
 int mf_render_views(mf_ctx* ctx, const mf_mesh_view* mesh, const double* cameras, int n_views, int resolution,
-                    const double* vertex_normals, int32_t* face, float* depth, float* position, float* normal) {
+                    const double* vertex_normals, int backface_cull, int32_t* face, float* depth, float* position,
+                    float* normal) {
   if (!ctx || !mesh || (n_views > 0 && !cameras)) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
   return guarded(ctx, [&]() -> int {
     Ctx& c = ctx->c;
@@ -1519,7 +1520,8 @@ int mf_render_views(mf_ctx* ctx, const mf_mesh_view* mesh, const double* cameras
     float* dd = depth ? c.buf<float>("rv.depth", px) : nullptr;
     float* dp = position ? c.buf<float>("rv.pos", 3 * px) : nullptr;
     float* dn = normal ? c.buf<float>("rv.nrm", 3 * px) : nullptr;
-    render_views(c, c.stream, bvh, cameras, n_views, resolution, nullptr, df, dd, dp, dn, m.m.faces, dvn);
+    render_views(c, c.stream, bvh, cameras, n_views, resolution, backface_cull, nullptr, df, dd, dp, dn, m.m.faces,
+                 dvn);
     if (face) MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * px, cudaMemcpyDeviceToHost, c.stream));
     if (depth) MFB_CUDA_TRY(cudaMemcpyAsync(depth, dd, sizeof(float) * px, cudaMemcpyDeviceToHost, c.stream));
     if (position) MFB_CUDA_TRY(cudaMemcpyAsync(position, dp, sizeof(float) * 3 * px, cudaMemcpyDeviceToHost, c.stream));
@@ -1557,7 +1559,7 @@ int mf_cast_visibility(mf_ctx* ctx, const mf_mesh_view* mesh, int viewpoints, in
     lbvh_build(c, c.stream, cm, bvh, "vis.bvh");
     auto* dh = c.buf<unsigned long long>("vis.hits", nf);
     MFB_CUDA_TRY(cudaMemsetAsync(dh, 0, sizeof(unsigned long long) * nf, c.stream));
-    render_views(c, c.stream, bvh, cams.data(), viewpoints, resolution, dh, nullptr, nullptr, nullptr, nullptr,
+    render_views(c, c.stream, bvh, cams.data(), viewpoints, resolution, 0, dh, nullptr, nullptr, nullptr, nullptr,
                  nullptr, nullptr);
     MFB_CUDA_TRY(cudaMemcpyAsync(hits, dh, sizeof(int64_t) * nf, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));

@@ -1658,7 +1658,7 @@ struct ViewCam {
 
 __global__ void __launch_bounds__(128) k_render_views(
     const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root, const ViewCam* __restrict__ cams,
-    int nviews, int res, unsigned long long* __restrict__ hits, int32_t* __restrict__ face_img,
+    int nviews, int res, int cull, unsigned long long* __restrict__ hits, int32_t* __restrict__ face_img,
     float* __restrict__ depth_img, float* __restrict__ pos_img, float* __restrict__ nrm_img,
     const int32_t* __restrict__ faces, const double* __restrict__ vnormals) {
   const int tiles_x = (res + 7) >> 3, tiles_y = (res + 3) >> 2;
@@ -1712,6 +1712,9 @@ __global__ void __launch_bounds__(128) k_render_views(
         d3 A, B, C;
         int f;
         load_tri(tris + first + k, A, B, C, f);
+        // RasterOptions::backfaceCull (raster.cpp:44): faces whose geometric
+        // normal points along the view direction are skipped
+        if (cull && dot(cross(B - A, C - A), dir) > 0.0) continue;
         double tt, u, v;
         if (!ray_triangle(o, dir, A, B, C, tt, u, v)) continue;
         const float depth = __double2float_rn(-tt);
@@ -2034,7 +2037,7 @@ void fibonacci_cameras(int count, double half_extent, double* cams7) {
   }
 }
 
-void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7, int nviews, int res,
+void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7, int nviews, int res, int cull,
                   unsigned long long* hits, int32_t* face_img, float* depth_img, float* pos_img, float* nrm_img,
                   const int32_t* faces, const double* vnormals) {
   if (nviews <= 0 || res <= 0) return;
@@ -2049,7 +2052,7 @@ void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7
     const int64_t threads = per_view * nv;
     const int64_t img_off = static_cast<int64_t>(v0) * res * res;
     k_render_views<<<static_cast<unsigned>(div_up(threads, 128)), 128, 0, s>>>(
-        bvh.nodes, bvh.tris, bvh.root_ref, dc + v0, nv, res, hits, face_img ? face_img + img_off : nullptr,
+        bvh.nodes, bvh.tris, bvh.root_ref, dc + v0, nv, res, cull, hits, face_img ? face_img + img_off : nullptr,
         depth_img ? depth_img + img_off : nullptr, pos_img ? pos_img + 3 * img_off : nullptr,
         nrm_img ? nrm_img + 3 * img_off : nullptr, faces, vnormals);
     ctx.count_launch();

@@ -257,7 +257,8 @@ def fibonacci_cameras(count: int, half_extent: float = 0.52, ctx=None) -> np.nda
     return cams
 
 
-def render_views(mesh: TriangleMesh, cameras: np.ndarray, resolution: int, vertex_normals=None, ctx=None):
+def render_views(mesh: TriangleMesh, cameras: np.ndarray, resolution: int, vertex_normals=None,
+                 backface_cull: bool = False, ctx=None):
     """renderView (render/raster.cpp:12-102) for each camera row: (face i32, depth f32,
     position f32x3, normal f32x3) per view, one pixel ray per thread through the LBVH."""
     ctx = ctx or default_context()
@@ -269,8 +270,8 @@ def render_views(mesh: TriangleMesh, cameras: np.ndarray, resolution: int, verte
     nrm = np.zeros((n, resolution, resolution, 3), np.float32)
     vn = None if vertex_normals is None else np.ascontiguousarray(vertex_normals, dtype=np.float64)
     v = mesh.view()
-    check(ctx.lib.mf_render_views(ctx.h, ctypes.byref(v), _p(cams), n, int(resolution), _p(vn), _p(face), _p(depth),
-                                  _p(pos), _p(nrm)))
+    check(ctx.lib.mf_render_views(ctx.h, ctypes.byref(v), _p(cams), n, int(resolution), _p(vn), int(backface_cull),
+                                  _p(face), _p(depth), _p(pos), _p(nrm)))
     return face, depth, pos, nrm
 
 

@@ -140,8 +140,13 @@ def views_case(ref):
         face, depth, pos, nrm = ref.render_views(m, cams, 96, vn)
         out.update({f"{name}_pos_in": m.positions, f"{name}_faces": m.faces, f"{name}_vn": vn,
                     f"{name}_face": face, f"{name}_depth": depth, f"{name}_hits": ref.cast_visibility(m, 32, 96)})
-        if name == "blob":  # position / normal images of two views
+        if name == "blob":  # position / normal images of two views; RasterOptions::backfaceCull
             out.update(blob_position=pos[:2], blob_normal=nrm[:2])
+            # reversed winding: culling drops the near shell, the far one shows
+            from paper_2605_26137_b200.mesh import TriangleMesh
+            rev = TriangleMesh(m.positions, np.ascontiguousarray(m.faces[:, ::-1]))
+            cf, cd, _, _ = ref.render_views(rev, cams[:2], 96, vn, cull=True)
+            out.update(blob_cull_face=cf, blob_cull_depth=cd)
     return out
 
 

@@ -28,3 +28,13 @@ def test_reference_test_spatial_against_b200_api(gpu_ctx):
         pytest.skip("built only where /root/reference exists")
     out = run(exe)
     assert "14/14 test cases passed" in out
+
+
+def test_reference_test_render_against_b200_api(gpu_ctx):
+    """The reference's own tests/test_render.cpp (renderView, renderGeometry,
+    standardCameras) compiled against include/meshforge and run on the B200."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_render_b200")
+    if not os.path.exists(exe):
+        pytest.skip("built only where /root/reference exists")
+    out = run(exe)
+    assert "FAIL" not in out and "test cases passed" in out

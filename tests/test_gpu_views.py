@@ -34,6 +34,10 @@ def test_render_views_match_reference_golden(gpu_ctx, case):
     if case == "blob":
         assert np.array_equal(f32bits(pos[:2]), f32bits(d["blob_position"]))
         assert np.array_equal(f32bits(nrm[:2]), f32bits(d["blob_normal"]))
+        cf, cd, _, _ = mf.render_views(TriangleMesh(m.positions, np.ascontiguousarray(m.faces[:, ::-1])), d["cams"][:2], 96,
+                                     d["blob_vn"], backface_cull=True)
+        assert np.array_equal(cf, d["blob_cull_face"])
+        assert np.array_equal(f32bits(cd), f32bits(d["blob_cull_depth"]))
 
 
 @pytest.mark.parametrize("case", ["nested", "blob", "dup"])

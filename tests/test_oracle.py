@@ -232,4 +232,8 @@ def test_port_matches_reference_golden_views(port, case):
     if case == "blob":
         assert np.array_equal(f32bits(pos[:2]), f32bits(d["blob_position"]))
         assert np.array_equal(f32bits(nrm[:2]), f32bits(d["blob_normal"]))
+        cf, cd, _, _ = port.render_views(TriangleMesh(m.positions, np.ascontiguousarray(m.faces[:, ::-1])), d["cams"][:2], 96,
+                                       d["blob_vn"], cull=True)
+        assert np.array_equal(cf, d["blob_cull_face"])
+        assert np.array_equal(f32bits(cd), f32bits(d["blob_cull_depth"]))
     assert np.array_equal(port.cast_visibility(m, 32, 96), d[f"{case}_hits"])
