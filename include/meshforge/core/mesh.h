@@ -6,6 +6,7 @@
 
 #include <Eigen/Core>
 #include <Eigen/Geometry>
+#include <array>
 #include <cstdint>
 #include <utility>
 #include <vector>
@@ -47,6 +48,14 @@ std::vector<Eigen::Vector3d> computeVertexNormals(const TriangleMesh& m);
 // EmptyMesh when there are no faces; InvalidGeometry on a non-finite
 // coordinate or an out-of-range face index.
 void validateMesh(const TriangleMesh& m);
+
+// Per-face edge-adjacent neighbour faces (-1 where none). Incidences of one
+// edge pair up in face (then corner) order, first with second, third with
+// fourth, as core/mesh.cpp:114-133 does.
+std::vector<std::array<int, 3>> faceAdjacency(const TriangleMesh& m);
+// Keeps the flagged faces in order and the vertices (and uv corners) they
+// reference, renumbered in first-use order (core/mesh.cpp:154-186).
+TriangleMesh extractFaces(const TriangleMesh& m, const std::vector<std::uint8_t>& keep);
 
 // Order-independent 64-bit key of an undirected edge.
 inline std::uint64_t edgeKey(int a, int b) {

@@ -2,9 +2,8 @@
 // mf_cast_visibility): source-compatible subset of
 // proj/include/meshforge/visibility/visibility.h:10-35 — FaceVisibility,
 // VisibilityMask and castVisibility (one pixel ray per thread over all views,
-// per-face won-pixel counts identical to the reference). The edge-flood
-// passes that follow it (promoteExterior, removeHidden) are host graph
-// algorithms outside the bake hot path and are not provided here.
+// per-face won-pixel counts identical to the reference), plus the host-side
+// edge flood and compaction that complete the cull stage.
 #pragma once
 
 #include <cstdint>
@@ -30,5 +29,18 @@ struct VisibilityMask {
 };
 
 VisibilityMask castVisibility(const TriangleMesh& mesh, int viewpoints = 512, int resolution = 1024);
+
+// Closure of Visible faces over edges whose unit face normals agree with the
+// reached face's (dot >= cosThreshold): newly reached faces become
+// PromotedExterior (visibility.cpp:60-93). ShapeMismatch on a foreign mask.
+VisibilityMask promoteExterior(const TriangleMesh& mesh, const VisibilityMask& mask, double cosThreshold = 0.5);
+
+// Keeps the Visible and PromotedExterior faces (extractFaces order); AllHidden
+// when none survive; the mesh is returned untouched when all do (:95-113).
+TriangleMesh removeHidden(const TriangleMesh& mesh, const VisibilityMask& mask);
+
+// castVisibility -> promoteExterior -> removeHidden (:115-120).
+TriangleMesh cullHiddenFaces(const TriangleMesh& mesh, int viewpoints = 512, int resolution = 1024,
+                             double cosThreshold = 0.5);
 
 }  // namespace meshforge

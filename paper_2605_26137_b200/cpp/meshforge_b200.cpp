@@ -6,6 +6,7 @@
 // own scalar utilities, not a fallback for any device path. Errors map back
 // to meshforge::Error with the reference's codes; runtime failures become
 // Error(IoError, "cuda: ...").
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -423,6 +424,105 @@ VisibilityMask castVisibility(const TriangleMesh& mesh, int viewpoints, int reso
   mask.state.resize(mesh.faceCount());
   for (int f = 0; f < mesh.faceCount(); ++f) mask.state[f] = static_cast<FaceVisibility>(state[f]);
   return mask;
+}
+
+// ------------------------------------------------------------------ mesh topology + cull stage (host)
+std::vector<std::array<int, 3>> faceAdjacency(const TriangleMesh& m) {
+  // every (edge, face, corner) incidence, ordered by edge then face then
+  // corner; consecutive incidences of an edge pair up two by two
+  struct Inc {
+    std::uint64_t key;
+    int face, corner;
+  };
+  std::vector<Inc> inc;
+  inc.reserve(3 * m.faces.size());
+  for (int f = 0; f < m.faceCount(); ++f)
+    for (int k = 0; k < 3; ++k) inc.push_back({edgeKey(m.faces[f][k], m.faces[f][(k + 1) % 3]), f, k});
+  std::stable_sort(inc.begin(), inc.end(), [](const Inc& a, const Inc& b) { return a.key < b.key; });
+  std::vector<std::array<int, 3>> adj(m.faces.size(), {-1, -1, -1});
+  for (size_t i = 0; i + 1 < inc.size();) {
+    if (inc[i].key == inc[i + 1].key) {
+      adj[inc[i].face][inc[i].corner] = inc[i + 1].face;
+      adj[inc[i + 1].face][inc[i + 1].corner] = inc[i].face;
+      i += 2;
+    } else {
+      ++i;
+    }
+  }
+  return adj;
+}
+
+TriangleMesh extractFaces(const TriangleMesh& m, const std::vector<std::uint8_t>& keep) {
+  TriangleMesh out;
+  std::vector<int> vmap(m.positions.size(), -1);
+  const bool uv = m.hasUvs();
+  std::vector<int> tmap(uv ? m.uvs.size() : 0, -1);
+  for (int f = 0; f < m.faceCount(); ++f) {
+    if (!keep[f]) continue;
+    Eigen::Vector3i tri, tuv;
+    for (int k = 0; k < 3; ++k) {
+      int& slot = vmap[m.faces[f][k]];
+      if (slot < 0) {
+        slot = static_cast<int>(out.positions.size());
+        out.positions.push_back(m.positions[m.faces[f][k]]);
+        if (m.hasNormals()) out.normals.push_back(m.normals[m.faces[f][k]]);
+      }
+      tri[k] = slot;
+      if (uv) {
+        int& ts = tmap[m.faceUvs[f][k]];
+        if (ts < 0) {
+          ts = static_cast<int>(out.uvs.size());
+          out.uvs.push_back(m.uvs[m.faceUvs[f][k]]);
+        }
+        tuv[k] = ts;
+      }
+    }
+    out.faces.push_back(tri);
+    if (uv) out.faceUvs.push_back(tuv);
+  }
+  return out;
+}
+
+VisibilityMask promoteExterior(const TriangleMesh& mesh, const VisibilityMask& mask, double cosThreshold) {
+  if (static_cast<int>(mask.state.size()) != mesh.faceCount() || mask.hits.size() != mask.state.size())
+    throw Error(ErrorCode::ShapeMismatch, "visibility mask does not match the mesh");
+  const int nf = mesh.faceCount();
+  std::vector<Eigen::Vector3d> n(nf);
+  for (int f = 0; f < nf; ++f) n[f] = faceNormal(mesh, f);
+  const auto adj = faceAdjacency(mesh);
+  VisibilityMask out = mask;
+  // the result is the closure under accepting edges, so any visiting order
+  // gives it; a work stack of reached faces
+  std::vector<int> work;
+  for (int f = 0; f < nf; ++f)
+    if (out.state[f] == FaceVisibility::Visible) work.push_back(f);
+  while (!work.empty()) {
+    const int f = work.back();
+    work.pop_back();
+    for (int g : adj[f]) {
+      if (g < 0 || out.state[g] != FaceVisibility::Hidden) continue;
+      if (n[g].dot(n[f]) >= cosThreshold) {
+        out.state[g] = FaceVisibility::PromotedExterior;
+        work.push_back(g);
+      }
+    }
+  }
+  return out;
+}
+
+TriangleMesh removeHidden(const TriangleMesh& mesh, const VisibilityMask& mask) {
+  if (static_cast<int>(mask.state.size()) != mesh.faceCount())
+    throw Error(ErrorCode::ShapeMismatch, "visibility mask does not match the mesh");
+  std::vector<std::uint8_t> keep(mesh.faceCount());
+  int kept = 0;
+  for (int f = 0; f < mesh.faceCount(); ++f) kept += (keep[f] = mask.keep(f) ? 1 : 0);
+  if (kept == 0) throw Error(ErrorCode::AllHidden, "every face is occluded from all viewpoints");
+  if (kept == mesh.faceCount()) return mesh;
+  return extractFaces(mesh, keep);
+}
+
+TriangleMesh cullHiddenFaces(const TriangleMesh& mesh, int viewpoints, int resolution, double cosThreshold) {
+  return removeHidden(mesh, promoteExterior(mesh, castVisibility(mesh, viewpoints, resolution), cosThreshold));
 }
 
 }  // namespace meshforge

@@ -38,3 +38,14 @@ def test_reference_test_render_against_b200_api(gpu_ctx):
         pytest.skip("built only where /root/reference exists")
     out = run(exe)
     assert "FAIL" not in out and "test cases passed" in out
+
+
+def test_reference_test_visibility_against_b200_api(gpu_ctx):
+    """The reference's own tests/test_visibility.cpp (castVisibility vs its
+    brute-force ray caster, sealed shells, promotion, culling) against the
+    B200 C++ API."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_visibility_b200")
+    if not os.path.exists(exe):
+        pytest.skip("built only where /root/reference exists")
+    out = run(exe)
+    assert "FAIL" not in out and "test cases passed" in out
