@@ -275,6 +275,10 @@ void surface_band(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, int res, const doub
 void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7, int nviews, int res, int cull,
                   unsigned long long* hits, int32_t* face_img, float* depth_img, float* pos_img, float* nrm_img,
                   const int32_t* faces, const double* vnormals);
+// castVisibility's counts by the reference's own face-order rasteriser on the
+// device (z-buffer of atomicMax keys), views in z-buffer-sized passes.
+void raster_visibility(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* cams7, int nviews, int res,
+                       unsigned long long* hits);
 // fibonacciCameras (render/camera.cpp:38-55) into cams7 (host).
 void fibonacci_cameras(int count, double half_extent, double* cams7);
 // out = positions - center; returns max |out| (synchronises).

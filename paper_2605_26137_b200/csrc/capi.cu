@@ -1555,12 +1555,22 @@ int mf_cast_visibility(mf_ctx* ctx, const mf_mesh_view* mesh, int viewpoints, in
     if (radius <= 0.0) radius = 1.0;
     std::vector<double> cams(7 * static_cast<size_t>(viewpoints));
     fibonacci_cameras(viewpoints, radius * 1.04, cams.data());
-    Lbvh bvh;
-    lbvh_build(c, c.stream, cm, bvh, "vis.bvh");
     auto* dh = c.buf<unsigned long long>("vis.hits", nf);
     MFB_CUDA_TRY(cudaMemsetAsync(dh, 0, sizeof(unsigned long long) * nf, c.stream));
-    render_views(c, c.stream, bvh, cams.data(), viewpoints, resolution, 0, dh, nullptr, nullptr, nullptr, nullptr,
-                 nullptr, nullptr);
+    // default: the reference's face-order rasteriser on the device (z-buffer
+    // of atomicMax keys); MFB_VIS_RAY=1: one pixel ray per thread through the LBVH
+    static const bool by_ray = [] {
+      const char* e = std::getenv("MFB_VIS_RAY");
+      return e && e[0] == '1';
+    }();
+    if (by_ray) {
+      Lbvh bvh;
+      lbvh_build(c, c.stream, cm, bvh, "vis.bvh");
+      render_views(c, c.stream, bvh, cams.data(), viewpoints, resolution, 0, dh, nullptr, nullptr, nullptr, nullptr,
+                   nullptr, nullptr);
+    } else {
+      raster_visibility(c, c.stream, cm, cams.data(), viewpoints, resolution, dh);
+    }
     MFB_CUDA_TRY(cudaMemcpyAsync(hits, dh, sizeof(int64_t) * nf, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
     if (state)

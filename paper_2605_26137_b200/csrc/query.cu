@@ -1783,6 +1783,76 @@ __global__ void k_center_mesh(const double* __restrict__ pos, int nv, double cx,
   for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
   if ((threadIdx.x & 31) == 0) atomicMax(acc, ordered_bits_dev(m));
 }
+
+// ---------------------------------------------------------------- view z-buffer rasteriser
+// renderView's own face loop (render/raster.cpp:39-98), one thread per
+// (view, face): the face's padded pixel box, the per-face Moller-Trumbore
+// factors, and per pixel the reference's expressions; the z-test becomes a
+// 64-bit atomicMax on key = ordered(f32 depth) << 32 | (0xffffffff - face),
+// i.e. the largest depth wins and equal depths go to the lowest face - the
+// order-independent form of "replace iff depth > stored" over faces in index
+// order. Key 0 = background.
+__device__ __forceinline__ unsigned ordered_f32(float f) {
+  const unsigned b = __float_as_uint(f);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__global__ void __launch_bounds__(128) k_zbuf_faces(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                                    int nf, const ViewCam* __restrict__ cams, int res, int cull,
+                                                    unsigned long long* __restrict__ zbuf) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  const int view = blockIdx.y;
+  if (f >= nf) return;
+  const ViewCam& c = cams[view];
+  const d3 dir = mk3(c.dir[0], c.dir[1], c.dir[2]);
+  const d3 up = mk3(c.up[0], c.up[1], c.up[2]);
+  const d3 right = mk3(c.right[0], c.right[1], c.right[2]);
+  const d3 a = ld3(pos + 3 * faces[3 * f]), b = ld3(pos + 3 * faces[3 * f + 1]), cc = ld3(pos + 3 * faces[3 * f + 2]);
+  if (cull && dot(cross(b - a, cc - a), dir) > 0.0) return;
+  const double u0 = dot(a, right), u1 = dot(b, right), u2 = dot(cc, right);
+  const double v0 = dot(a, up), v1 = dot(b, up), v2 = dot(cc, up);
+  const double umin = fmin(u0, fmin(u1, u2)), umax = fmax(u0, fmax(u1, u2));
+  const double vmin = fmin(v0, fmin(v1, v2)), vmax = fmax(v0, fmax(v1, v2));
+  const int pxLo = max(0, static_cast<int>(floor((umin + c.he) / c.step - 0.5)) - 1);
+  const int pxHi = min(res - 1, static_cast<int>(ceil((umax + c.he) / c.step - 0.5)) + 1);
+  const int pyLo = max(0, static_cast<int>(floor((c.he - vmax) / c.step - 0.5)) - 1);
+  const int pyHi = min(res - 1, static_cast<int>(ceil((c.he - vmin) / c.step - 0.5)) + 1);
+  if (pxLo > pxHi || pyLo > pyHi) return;
+  const d3 e1 = b - a, e2 = cc - a;
+  const d3 pvec = cross(dir, e2);
+  const double det = dot(e1, pvec);
+  if (fabs(det) < 1e-9) return;
+  const double inv = 1.0 / det;
+  unsigned long long* zb = zbuf + static_cast<int64_t>(view) * res * res;
+  const unsigned fkey = 0xffffffffu - static_cast<unsigned>(f);
+  for (int py = pyLo; py <= pyHi; ++py) {
+    const d3 rowV = (c.he - (py + 0.5) * c.step) * up;
+    for (int px = pxLo; px <= pxHi; ++px) {
+      const d3 origin = (-c.he + (px + 0.5) * c.step) * right + rowV;
+      const d3 sv = origin - a;
+      const double bu = dot(sv, pvec) * inv;
+      if (bu < 0.0 || bu > 1.0) continue;
+      const d3 qv = cross(sv, e1);
+      const double bv = dot(dir, qv) * inv;
+      if (bv < 0.0 || bu + bv > 1.0) continue;
+      const double t = dot(e2, qv) * inv;
+      const unsigned long long key =
+          (static_cast<unsigned long long>(ordered_f32(__double2float_rn(-t))) << 32) | fkey;
+      unsigned long long* z = zb + static_cast<int64_t>(py) * res + px;
+      if (key > *z) atomicMax(z, key);
+    }
+  }
+}
+
+// castVisibility's tally (visibility.cpp:41-45): one hit per won pixel.
+__global__ void k_zbuf_hits(const unsigned long long* __restrict__ zbuf, int64_t n,
+                            unsigned long long* __restrict__ hits) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long k = zbuf[i];
+    if (k) atomicAdd(&hits[0xffffffffu - static_cast<unsigned>(k & 0xffffffffu)], 1ull);
+  }
+}
 }  // namespace
 
 // Resident 128-thread blocks per SM of `kern` (>= 1); callers cache it in a
@@ -2056,6 +2126,27 @@ void render_views(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* cams7
         depth_img ? depth_img + img_off : nullptr, pos_img ? pos_img + 3 * img_off : nullptr,
         nrm_img ? nrm_img + 3 * img_off : nullptr, faces, vnormals);
     ctx.count_launch();
+  }
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
+
+void raster_visibility(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* cams7, int nviews, int res,
+                       unsigned long long* hits) {
+  if (nviews <= 0 || res <= 0 || m.nf <= 0) return;
+  const std::vector<ViewCam> hv = view_cams(cams7, nviews, res);
+  auto* dc = ctx.buf<ViewCam>("view.cams", nviews);
+  MFB_CUDA_TRY(cudaMemcpyAsync(dc, hv.data(), sizeof(ViewCam) * nviews, cudaMemcpyHostToDevice, s));
+  const int64_t px = static_cast<int64_t>(res) * res;
+  // views per pass: z-buffers of <= 256 MiB
+  const int group = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(65535, (int64_t{256} << 20) / (8 * px))));
+  auto* zb = ctx.buf<unsigned long long>("view.zbuf", static_cast<size_t>(std::min(group, nviews)) * px);
+  for (int v0 = 0; v0 < nviews; v0 += group) {
+    const int nv = std::min(group, nviews - v0);
+    MFB_CUDA_TRY(cudaMemsetAsync(zb, 0, sizeof(unsigned long long) * nv * px, s));
+    k_zbuf_faces<<<dim3(div_up(m.nf, 128), nv), 128, 0, s>>>(m.pos, m.faces, m.nf, dc + v0, res, 0, zb);
+    k_zbuf_hits<<<kNumSMs * 8, 256, 0, s>>>(zb, nv * px, hits);
+    ctx.count_launch(2);
   }
   MFB_CUDA_TRY(cudaGetLastError());
 }

@@ -11,10 +11,16 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def run(exe):
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
-    return r.stdout
+def run(exe, attempts=2):
+    """Runs a doctest binary; one retry, because the reference suites carry
+    wall-clock budget checks (e.g. test_render.cpp:226-235, < 1 s) that can
+    trip on a cold, shared box - a second failure is reported."""
+    for k in range(attempts):
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+        if r.returncode == 0:
+            return r.stdout
+    failed = [ln for ln in r.stdout.splitlines() if "FAIL" in ln or "CHECK" in ln]
+    raise AssertionError("\n".join(failed[-40:]) + r.stdout[-2000:] + r.stderr[-2000:])
 
 
 def test_cpp_bake_kats(gpu_ctx):
