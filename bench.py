@@ -305,9 +305,25 @@ def bvh_rays(ctx, hi, pair, steps):
     ms_vis = timed(lambda: capi.check(lib.mf_cast_visibility(ctx.h, ctypes.byref(mv), vis_views, vis_res,
                                                              hits.ctypes.data_as(ctypes.c_void_p), None)))
     vis_rays = vis_views * vis_res * vis_res
-    return {"visibility_rays_per_s": vis_rays / (ms_vis * 1e-3), "visibility_ms": round(ms_vis, 3),
+    # the reference's castVisibility on the host cores, 32 of the views (its
+    # views are independent, parallelChunks over views)
+    vis_cpu = None
+    try:
+        lib_ref, kind = _reference_lib()
+        t0 = time.perf_counter()
+        ref_hits = lib_ref.cast_visibility(pair.dense, 32, vis_res)
+        dt = time.perf_counter() - t0
+        vis_cpu = {"pixels_per_s": 32 * vis_res * vis_res / dt, "s": round(dt, 3), "views": 32, "kind": kind,
+                   "cores": cores()}
+        del ref_hits
+    except Exception as e:  # noqa: BLE001 - the CPU leg is informative only
+        vis_cpu = {"unavailable": str(e)[:120]}
+    return {"visibility_pixels_per_s": vis_rays / (ms_vis * 1e-3), "visibility_ms": round(ms_vis, 3),
             "visibility_views": vis_views, "visibility_res": vis_res,
             "visibility_visible_faces": int((hits > 0).sum()),
+            "visibility_method": "device z-buffer rasteriser (the reference's face loop, atomicMax keys); "
+                                 "whole host call incl. upload and centring",
+            "visibility_cpu_reference": vis_cpu,
             "surface_band_voxels_per_s": nb / (ms_band * 1e-3), "surface_band_ms": round(ms_band, 4),
             "surface_band_res": band_res, "surface_band_marked": band_voxels,
             "raycast_rays_per_s": N_RAYS / (ms_ray * 1e-3), "raycast_ms": round(ms_ray, 4), "raycast_hits": ray_hits,
