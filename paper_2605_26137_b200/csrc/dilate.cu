@@ -29,6 +29,10 @@ __device__ __forceinline__ int sq(int v) { return v * v; }
 // hold source offsets; ox == kNone means no source. Neighbours outside the
 // image are skipped exactly as in the reference; cells outside the region are
 // never read (the caller only updates cells at least one step inside).
+// Distances are exact in int32: |offset| <= radius <= 64 keeps them below
+// 2^14 (the reference's int64 values are the same integers). kBorder = false
+// for tiles whose region lies inside the image (no neighbour bounds checks).
+template <bool kBorder>
 __device__ __forceinline__ void chamfer_step(const int16_t* __restrict__ ox, const int16_t* __restrict__ oy,
                                              int rw, int cx, int cy, int gx, int gy, int width, int height,
                                              int16_t& nox, int16_t& noy) {
@@ -37,19 +41,21 @@ __device__ __forceinline__ void chamfer_step(const int16_t* __restrict__ ox, con
   nox = sx;
   noy = sy;
   if (sx == 0 && sy == 0) return;  // valid texel: dist2 == 0, skipped
-  long long best = sx == kNone ? 0x7fffffffffffffffll : static_cast<long long>(sq(sx) + sq(sy));
+  int best = sx == kNone ? 0x7fffffff : sq(sx) + sq(sy);
 #pragma unroll
   for (int dy = -1; dy <= 1; ++dy) {
 #pragma unroll
     for (int dx = -1; dx <= 1; ++dx) {
       if (dx == 0 && dy == 0) continue;
-      const int nx = gx + dx, ny = gy + dy;
-      if (nx < 0 || nx >= width || ny < 0 || ny >= height) continue;
+      if (kBorder) {
+        const int nx = gx + dx, ny = gy + dy;
+        if (nx < 0 || nx >= width || ny < 0 || ny >= height) continue;
+      }
       const int n = self + dy * rw + dx;
       const int16_t nsx = ox[n];
       if (nsx == kNone) continue;
       const int cxo = dx + nsx, cyo = dy + oy[n];
-      const long long d = static_cast<long long>(sq(cxo) + sq(cyo));
+      const int d = sq(cxo) + sq(cyo);
       if (d < best) {
         best = d;
         nox = static_cast<int16_t>(cxo);
@@ -97,6 +103,8 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
     any_hole |= out_cell && v != 0;
   }
   const bool work = __syncthreads_or(any_valid) && __syncthreads_or(any_hole);
+  // the region (and so every neighbour read) lies inside the image
+  const bool interior = x0 >= 0 && x0 + rw <= width && y0 >= 0 && y0 + rh <= height;
   if (work) {
     for (int pass = 1; pass <= radius; ++pass) {
       const int iw = rw - 2 * pass, ih = rh - 2 * pass;
@@ -104,7 +112,8 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
         const int cx = pass + c % iw, cy = pass + c / iw;
         const int i = cy * rw + cx;
         int16_t a, b;
-        chamfer_step(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
+        if (interior) chamfer_step<false>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
+        else chamfer_step<true>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
         ox1[i] = a;
         oy1[i] = b;
       }
@@ -117,6 +126,22 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
       oy1 = t;
       // (pass k + 1 reads only cells in [k, rw - k) x [k, rh - k), all
       // written by pass k, so the stale outer ring is never read)
+    }
+  }
+  // copy-only tile, full width, 16-byte aligned rows: 16-byte moves
+  const int gx0 = tx * kTW, gy0 = out_row0 + ty * kTH;
+  if (!work && gx0 + kTW <= width && gy0 + kTH <= out_end) {
+    const int64_t row_bytes = static_cast<int64_t>(width) * channels;
+    const uint8_t* src0 = map_in + (static_cast<int64_t>(gy0 - in_row0) * width + gx0) * channels;
+    uint8_t* dst0 = map_out + (static_cast<int64_t>(gy0 - out_row0) * width + gx0) * channels;
+    const int vec_per_row = kTW * channels / 16;
+    if (kTW * channels % 16 == 0 && row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(src0) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(dst0) & 15) == 0) {
+      for (int c = threadIdx.x; c < vec_per_row * kTH; c += blockDim.x) {
+        const int r = c / vec_per_row, k = c % vec_per_row;
+        reinterpret_cast<uint4*>(dst0 + r * row_bytes)[k] = __ldg(reinterpret_cast<const uint4*>(src0 + r * row_bytes) + k);
+      }
+      return;
     }
   }
   // output: tile interior (4 texels per thread, row-contiguous)
