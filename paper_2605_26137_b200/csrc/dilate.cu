@@ -89,34 +89,36 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
   const int in_end = in_row0 + in_rows;
   const int out_end = out_row0 + out_rows;
   int any_valid = 0, any_hole = 0;
-  for (int c = threadIdx.x; c < cells; c += blockDim.x) {
-    const int lx = c % rw, ly = c / rw;
-    const int gx = x0 + lx, gy = y0 + ly;
-    int16_t v = kNone;
-    const bool inimg = gx >= 0 && gx < width && gy >= in_row0 && gy < in_end && gy < height;
-    if (inimg && valid[static_cast<int64_t>(gy - in_row0) * width + gx]) v = 0;
-    ox0[c] = v;
-    oy0[c] = 0;
-    any_valid |= v == 0;
-    const bool out_cell = lx >= radius && lx < radius + kTW && ly >= radius && ly < radius + kTH &&
-                          gx < width && gy < out_end;
-    any_hole |= out_cell && v != 0;
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  // (row per warp, lanes along the row: no integer division per cell)
+  for (int ly = warp; ly < rh; ly += nwarps)
+    for (int lx = lane; lx < rw; lx += 32) {
+      const int c = ly * rw + lx;
+      const int gx = x0 + lx, gy = y0 + ly;
+      int16_t v = kNone;
+      const bool inimg = gx >= 0 && gx < width && gy >= in_row0 && gy < in_end && gy < height;
+      if (inimg && valid[static_cast<int64_t>(gy - in_row0) * width + gx]) v = 0;
+      ox0[c] = v;
+      oy0[c] = 0;
+      any_valid |= v == 0;
+      const bool out_cell = lx >= radius && lx < radius + kTW && ly >= radius && ly < radius + kTH &&
+                            gx < width && gy < out_end;
+      any_hole |= out_cell && v != 0;
+    }
   const bool work = __syncthreads_or(any_valid) && __syncthreads_or(any_hole);
   // the region (and so every neighbour read) lies inside the image
   const bool interior = x0 >= 0 && x0 + rw <= width && y0 >= 0 && y0 + rh <= height;
   if (work) {
     for (int pass = 1; pass <= radius; ++pass) {
-      const int iw = rw - 2 * pass, ih = rh - 2 * pass;
-      for (int c = threadIdx.x; c < iw * ih; c += blockDim.x) {
-        const int cx = pass + c % iw, cy = pass + c / iw;
-        const int i = cy * rw + cx;
-        int16_t a, b;
-        if (interior) chamfer_step<false>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
-        else chamfer_step<true>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
-        ox1[i] = a;
-        oy1[i] = b;
-      }
+      for (int cy = pass + warp; cy < rh - pass; cy += nwarps)
+        for (int cx = pass + lane; cx < rw - pass; cx += 32) {
+          const int i = cy * rw + cx;
+          int16_t a, b;
+          if (interior) chamfer_step<false>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
+          else chamfer_step<true>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
+          ox1[i] = a;
+          oy1[i] = b;
+        }
       __syncthreads();
       int16_t* t = ox0;
       ox0 = ox1;
