@@ -338,7 +338,12 @@ struct Timer {
   cudaEvent_t mark(cudaStream_t s) {
     if (!c.timing) return nullptr;
     cudaEvent_t e = c.pool_event(next++);
-    MFB_CUDA_TRY(cudaEventRecord(e, s));
+    // inside a stream capture a plain record is only a dependency marker; an
+    // external record becomes an event-record node that timestamps on replay
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    MFB_CUDA_TRY(cudaStreamIsCapturing(s, &cs));
+    if (cs == cudaStreamCaptureStatusActive) MFB_CUDA_TRY(cudaEventRecordWithFlags(e, s, cudaEventRecordExternal));
+    else MFB_CUDA_TRY(cudaEventRecord(e, s));
     return e;
   }
   static float ms(cudaEvent_t a, cudaEvent_t b) {
@@ -566,10 +571,32 @@ void enqueue_bake(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double 
                   int rb, int re, uint8_t* rgb_out, bool debug, Timer& tm, BakeMarks& mk, int* hflags_pinned,
                   unsigned long long* hcnt_pinned) {
   BakeEnq q(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, debug, tm, mk);
+  // MFB_DIAG_SKIP=bvh|low|normals: DIAGNOSTIC ONLY (critical-path analysis):
+  // reuse that phase's buffers from the previous (eager) call instead of
+  // recomputing them. Never set in a measured run.
+  static const std::string skip = [] {
+    const char* e = std::getenv("MFB_DIAG_SKIP");
+    return std::string(e ? e : "");
+  }();
+  static int calls = 0;
+  const bool reuse = !debug && ++calls > 2;  // the first calls build every buffer
   MFB_CUDA_TRY(cudaEventRecord(c.fork, c.stream));
-  q.dense_bvh(c.fork);
-  q.low();
-  q.dense_normals(c.fork);
+  if (skip == "bvh" && reuse) {
+    lbvh_layout(c, hi->m, q.bvh, "hi.bvh");
+    MFB_CUDA_TRY(cudaEventRecord(c.join, c.stream));
+  } else {
+    q.dense_bvh(c.fork);
+  }
+  if (!(skip == "low" && reuse)) q.low();
+  if (skip == "low" && reuse) {  // the transfer's batch cursor is reset by the raster
+    MFB_CUDA_TRY(cudaMemsetAsync(q.fo.q.count + 3, 0, sizeof(int), c.stream));
+  }
+  if (skip == "normals" && reuse) {
+    q.hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
+    MFB_CUDA_TRY(cudaEventRecord(c.join3, c.stream));
+  } else {
+    q.dense_normals(c.fork);
+  }
   q.tail(hflags_pinned, hcnt_pinned);
 }
 
@@ -589,7 +616,13 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
   cudaStream_t s = c.stream;
   // debug outputs and stage timing always run eagerly (events inside a graph
   // are not meaningful)
-  const bool debug = dbg_face || dbg_ts || c.timing;
+  // MFB_GRAPH_TIMING=1: keep the captured graph when stage timing is on (its
+  // marks are event-record nodes), to time the stages as the graph runs them
+  static const bool graph_timing = [] {
+    const char* e = std::getenv("MFB_GRAPH_TIMING");
+    return e && e[0] == '1';
+  }();
+  const bool debug = dbg_face || dbg_ts || (c.timing && !graph_timing);
   static const bool graphs = [] {
     const char* e = std::getenv("MFB_GRAPH");
     return !(e && e[0] == '0');
@@ -678,6 +711,13 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
       st->valid_texels = static_cast<int64_t>(hcnt[2]);
       st->bvh_nodes = hi->m.nf > 1 ? hi->m.nf - 1 : 0;
       st->bvh_depth = 0;
+      if (c.timing && std::getenv("MFB_TRACE_MARKS")) {  // diagnostic: mark offsets from the bake start
+        const cudaEvent_t t0e = t_begin ? t_begin : mk.e0;
+        std::fprintf(stderr, "[mfb marks] side0 %.3f side1 %.3f e0 %.3f e1 %.3f e2 %.3f e3 %.3f e4 %.3f e5 %.3f\n",
+                     Timer::ms(t0e, mk.side0), Timer::ms(t0e, mk.side1), Timer::ms(t0e, mk.e0),
+                     Timer::ms(t0e, mk.e1), Timer::ms(t0e, mk.e2), Timer::ms(t0e, mk.e3), Timer::ms(t0e, mk.e4),
+                     Timer::ms(t0e, mk.e5));
+      }
       if (c.timing) {
         st->ms_prepare = Timer::ms(mk.e0, mk.e1);
         st->ms_raster = Timer::ms(mk.e1, mk.e2);
