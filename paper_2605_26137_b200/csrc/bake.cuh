@@ -35,6 +35,7 @@ struct Ctx {
   cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr, join3 = nullptr;
   cudaEvent_t hi_ready = nullptr;   // host entry point: dense mesh uploaded and validated
   cudaEvent_t dfork = nullptr, djoin = nullptr;  // host entry point: dense phase side -> aux -> side
+  cudaEvent_t up_fork = nullptr, up_join = nullptr;  // split H2D of one mesh over two streams
   bool timing = false;
   int64_t launches = 0;
   struct Buf {
