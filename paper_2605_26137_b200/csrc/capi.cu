@@ -811,7 +811,11 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     const char* e = std::getenv("MFB_GRAPH");
     return !(e && e[0] == '0');
   }();
-  const bool use_graphs = graphs && !c.timing;
+  static const bool graph_timing = [] {
+    const char* e = std::getenv("MFB_GRAPH_TIMING");
+    return e && e[0] == '1';
+  }();
+  const bool use_graphs = graphs && (!c.timing || graph_timing);
   {
     const int64_t k[] = {reinterpret_cast<int64_t>(lo.m.pos), reinterpret_cast<int64_t>(lo.m.faces),
                          reinterpret_cast<int64_t>(lo.m.nrm), reinterpret_cast<int64_t>(lo.m.uvs),
@@ -853,6 +857,14 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     st->valid_texels = static_cast<int64_t>(hcnt[2]);
     st->bvh_nodes = hi.m.nf > 1 ? hi.m.nf - 1 : 0;
     st->bvh_depth = 0;
+    if (c.timing && std::getenv("MFB_TRACE_MARKS")) {
+      std::fprintf(stderr,
+                   "[mfb host marks] e0 %.3f e1 %.3f e2 %.3f side0 %.3f side1 %.3f e3 %.3f e4 %.3f e5 %.3f "
+                   "dl0 %.3f dl1 %.3f\n",
+                   Timer::ms(t0, mk.e0), Timer::ms(t0, mk.e1), Timer::ms(t0, mk.e2), Timer::ms(t0, mk.side0),
+                   Timer::ms(t0, mk.side1), Timer::ms(t0, mk.e3), Timer::ms(t0, mk.e4), Timer::ms(t0, mk.e5),
+                   Timer::ms(t0, t2), Timer::ms(t0, t3));
+    }
     if (c.timing) {
       st->ms_upload = Timer::ms(t0, mk.e0);
       st->ms_prepare = Timer::ms(mk.e0, mk.e1);
