@@ -186,3 +186,37 @@ def test_gpu_wedge_tangents_and_vertex_normals(gpu_ctx):
     assert np.abs(frames - d["frames"]).max() <= 1e-12
     vm = TriangleMesh(d["vn_mesh_pos"], d["vn_mesh_faces"])
     assert np.array_equal(mf.compute_vertex_normals(vm), d["vnormals"])
+
+
+def test_host_bake_error_order(gpu_ctx):
+    """mf_bake_normal_map overlaps the dense upload with the lowpoly raster;
+    its errors keep the reference composition's order (test_bake.cpp:205-206):
+    lowpoly checks (gbuffer.cpp:93-97) -> AtlasOverlap (:157-159) ->
+    transferNormals' checks (:195-199) -> dilateSeams' radius (:255)."""
+    def code(fn):
+        with pytest.raises(mf.MeshforgeError) as e:
+            fn()
+        return e.value.code
+
+    quad = fx.identity_quad()
+    bare = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 2]])
+    nan = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, np.nan, 0]], [[0, 1, 2]])
+    oob = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0]], [[0, 1, 7]])
+    empty = TriangleMesh(np.zeros((0, 3)), np.zeros((0, 3)))
+    overlap = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1], [1, 0, 1], [0, 1, 1]],
+                           [[0, 1, 2], [3, 4, 5]],
+                           uvs=[[0.1, 0.1], [0.9, 0.1], [0.1, 0.9], [0.2, 0.2], [0.8, 0.2], [0.2, 0.8]],
+                           face_uvs=[[0, 1, 2], [3, 4, 5]])
+    assert code(lambda: mf.bake_normal_map(bare, nan, 32, 1.0)) == "InvalidGeometry"  # lowpoly first
+    assert code(lambda: mf.bake_normal_map(quad, nan, 0, 1.0)) == "InvalidConfig"  # res before the dense mesh
+    assert code(lambda: mf.bake_normal_map(overlap, nan, 32, 1.0)) == "AtlasOverlap"
+    assert code(lambda: mf.bake_normal_map(overlap, quad, 32, 0.0)) == "AtlasOverlap"
+    assert code(lambda: mf.bake_normal_map(quad, nan, 32, 1.0)) == "InvalidGeometry"
+    assert code(lambda: mf.bake_normal_map(quad, oob, 32, 1.0)) == "InvalidGeometry"
+    assert code(lambda: mf.bake_normal_map(quad, empty, 32, 1.0)) == "EmptyMesh"
+    assert code(lambda: mf.bake_normal_map(quad, nan, 32, 0.0)) == "InvalidGeometry"  # mesh before config
+    assert code(lambda: mf.bake_normal_map(quad, quad, 32, 0.0)) == "InvalidConfig"
+    assert code(lambda: mf.bake_normal_map(quad, quad, 32, 1.0, radius=-1)) == "InvalidConfig"
+    # and the context still bakes afterwards
+    out = mf.bake_normal_map(quad, quad, 32, float(np.sqrt(2.0)))
+    assert out.shape[:2] == (32, 32) or out.size == 32 * 32 * 3
