@@ -55,3 +55,14 @@ def test_reference_test_visibility_against_b200_api(gpu_ctx):
         pytest.skip("built only where /root/reference exists")
     out = run(exe)
     assert "FAIL" not in out and "test cases passed" in out
+
+
+def test_reference_test_io_against_b200_api(gpu_ctx):
+    """The reference's own tests/test_io.cpp (OBJ, PNG, raw f32 files) against
+    the B200 library's host I/O (its OBJ round trip computes vertex normals on
+    the device, hence the GPU mark)."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_io_b200")
+    if not os.path.exists(exe):
+        pytest.skip("built only where /root/reference exists")
+    out = run(exe)
+    assert "FAIL" not in out and "test cases passed" in out
