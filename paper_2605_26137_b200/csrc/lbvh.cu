@@ -183,6 +183,18 @@ __global__ void k_emit(const uint32_t* __restrict__ keys, int n, int leaf_max, B
   if (start) starts[base + __popc(m & ((1u << lane) - 1u))] = i;
 }
 
+// Arrival counter of a refit node: release (our child box store is made
+// visible at L2 before the count moves; MEMBAR.GPU) but no acquire fence -
+// the second arriver reads its sibling's box with ld.cg from L2, the point of
+// coherence, after (control-dependent on) the atomic's result, so the L1-wide
+// CCTL.IVALL an acq_rel atomic adds on every level is avoided (the
+// threadFenceReduction pattern). Returns the previous count.
+__device__ __forceinline__ int arrive(int* f) {
+  int old;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(f) : "memory");
+  return old;
+}
+
 struct FBox {
   float mn[3], mx[3];
 };
@@ -273,8 +285,7 @@ __global__ void k_refit(const TBox* __restrict__ tbox, int n, BNode* nodes, cons
   for (;;) {
     const int par = link >> 1, side = link & 1;
     store_child_box(&nodes[par], side, box);
-    cuda::atomic_ref<int, cuda::thread_scope_device> flag(flags[par]);
-    if (flag.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;  // sibling carries on
+    if (arrive(&flags[par]) == 0) return;  // sibling carries on
     const FBox other = load_child_box_cg(&nodes[par], side ^ 1);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -347,8 +358,7 @@ __global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __res
   if (leaves == 0) return;  // both children internal: climbers arrive from below
   int node = i;
   if (leaves == 1) {
-    cuda::atomic_ref<int, cuda::thread_scope_device> flag(flags[node]);
-    if (flag.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;  // internal sibling still climbing
+    if (arrive(&flags[node]) == 0) return;  // internal sibling still climbing
     const int internal_side = refs[0] >= 0 ? 0 : 1;
     const FBox other = load_child_box_cg(&nodes[node], internal_side);
 #pragma unroll
@@ -370,8 +380,7 @@ __global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __res
     const int link = node_parent[node];
     const int par = link >> 1, side = link & 1;
     store_child_box(&nodes[par], side, box);
-    cuda::atomic_ref<int, cuda::thread_scope_device> flag(flags[par]);
-    if (flag.fetch_add(1, cuda::memory_order_acq_rel) == 0) return;
+    if (arrive(&flags[par]) == 0) return;
     const FBox other = load_child_box_cg(&nodes[par], side ^ 1);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
