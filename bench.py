@@ -68,6 +68,9 @@ def parse():
     ap.add_argument("--assets", type=int, default=1,
                     help="independent assets baked concurrently per GPU (config D: 8), one context + stream + "
                          "host thread each")
+    ap.add_argument("--gather", choices=["nccl", "peer"], default="peer",
+                    help="--shard: atlas gather by NCCL all-gather, or by the dilation kernel storing its rows "
+                         "into every rank's atlas over CUDA IPC peer memory (mf_bake_normal_map_dev_publish)")
     ap.add_argument("--shard", action="store_true",
                     help="N>1: row-shard ONE atlas across ranks + NCCL all-gather (strong scaling) "
                          "instead of one asset per rank")
@@ -389,6 +392,7 @@ def run_ours(args):
 
     row_b, row_e = 0, res
     shard_ranges = None
+    peer = None
     if args.shard and distributed:
         # one atlas, rows balanced by valid texels, all-gathered
         import ctypes
@@ -400,11 +404,17 @@ def run_ours(args):
         rows_max = max(e - b for b, e in shard_ranges)
         slab = torch.empty((rows_max, res, 3), dtype=torch.uint8, device="cuda")
         gathered = [torch.empty_like(slab) for _ in range(world)]
+        peer = sharding.PeerAtlas(ctx, res) if args.gather == "peer" else None
 
     def step(stats=None):
         if shard_ranges is None:
             capi.check(lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, diag, frac, 4, 0, res,
                                                   rgb.data_ptr(), stats))
+            return
+        if peer is not None:  # rows stored into every rank's atlas by the dilation kernel
+            capi.check(lib.mf_bake_normal_map_dev_publish(ctx.h, lo.h, hi.h, res, diag, frac, 4, row_b, row_e,
+                                                          peer.dst, peer.n, stats))
+            torch.distributed.barrier()
             return
         capi.check(lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, diag, frac, 4, row_b, row_e,
                                               slab.data_ptr(), stats))
@@ -514,7 +524,8 @@ def run_ours(args):
         "data": "synthetic (deterministic geodesic blob pair, Appendix B of SURVEY.md)",
         "config": {"workload": workload_desc(name, pair), "global_batch": 1 if shard_ranges else world,
                    "seq_len": None,
-                   "parallelism": (f"rows x{world} (one atlas, valid-balanced row slabs, NCCL all-gather)"
+                   "parallelism": (f"rows x{world} (one atlas, valid-balanced row slabs, "
+                                   f"{'peer-memory gather in the dilation kernel' if args.gather == 'peer' else 'NCCL all-gather'})"
                                    if shard_ranges else f"assets x{world} (one asset per GPU, no collective)"),
                    "l2": "flushed between timed steps (256 MiB write, outside the per-step events)",
                    "seed": fx.CONFIGS[name]["seed"]},

@@ -186,6 +186,27 @@ int mf_bvh_raycast_first_dev(mf_bvh* bvh, const double* origins_dev, const doubl
                              int64_t n, double tmin, double tmax, int32_t* face_dev,
                              double* t_dev, double* u_dev, double* v_dev);
 
+/* ---- multi-GPU: the sharded atlas gathered by the producing kernel ------ */
+/* CUDA IPC export of the device allocation that holds dev_ptr: a 64-byte
+ * handle plus dev_ptr's byte offset inside it (caching allocators hand out
+ * interior pointers). */
+int mf_ipc_export(const void* dev_ptr, uint8_t* handle64, uint64_t* offset);
+/* Opens a handle exported by another process on this node (peer GPU over
+ * NVLink, or the same GPU) into a device pointer usable by this context's
+ * kernels; closed by mf_ipc_close or with the context. */
+int mf_ipc_open(mf_ctx* ctx, const uint8_t* handle64, uint64_t offset, void** dev_ptr);
+int mf_ipc_close(mf_ctx* ctx, void* dev_ptr);
+/* mf_bake_normal_map_dev for rows [row_begin, row_end) whose dilation kernel
+ * stores every output row straight into each of the n_dst (1..8) full
+ * res x res x 3 atlases - this rank's own and its peers' (mf_ipc_open) - at
+ * its row index: the atlas all-gather of the row-sharded bake
+ * happens inside the producing kernel over peer memory instead of a separate
+ * collective. The caller synchronises ranks (a host barrier after this call
+ * returns) before reading its atlas. */
+int mf_bake_normal_map_dev_publish(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int resolution,
+                                   double bbox_diagonal, double max_distance_fraction, int radius, int row_begin,
+                                   int row_end, void* const* dst_atlases, int n_dst, mf_bake_stats* stats);
+
 /* ---- bulk closest-point callers ------------------------ */
 /* markSurfaceBand (signfield/sign_grid.cpp:23-69, sign_grid.h:14-50) over the
  * mesh `bvh` was built on: grid parameters exactly as the reference derives

@@ -87,6 +87,11 @@ SIGNATURES = [
     ("mf_bvh_closest_within_dev", _I, [_VP, _VP, _I64, _D, _VP, _VP, _VP, _VP]),
     ("mf_bvh_raycast_first", _I, [_VP, _VP, _VP, _I64, _D, _D, _VP, _VP, _VP, _VP]),
     ("mf_bvh_raycast_first_dev", _I, [_VP, _VP, _VP, _I64, _D, _D, _VP, _VP, _VP, _VP]),
+    ("mf_ipc_export", _I, [_VP, _VP, ctypes.POINTER(ctypes.c_uint64)]),
+    ("mf_ipc_open", _I, [_VP, _VP, ctypes.c_uint64, ctypes.POINTER(_VP)]),
+    ("mf_ipc_close", _I, [_VP, _VP]),
+    ("mf_bake_normal_map_dev_publish", _I, [_VP, _VP, _VP, _I, _D, _D, _I, _I, _I, _VP, _I,
+                                            ctypes.POINTER(MfBakeStats)]),
     ("mf_surface_band", _I, [_VP, _I, _D, _I, _VP, _VP, _VP, _VP]),
     ("mf_surface_band_dev", _I, [_VP, _I, _D, _I, _VP, _VP, _VP, _VP]),
     ("mf_fibonacci_cameras", _I, [_I, _D, _VP]),

@@ -293,6 +293,19 @@ void raycast_brute(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* o, 
                    double tmin, double tmax, int32_t* face, double* t, double* u, double* v);
 
 // ---------------------------------------------------------------- dilation
+// Destinations of the dilation's output rows: buffer k holds image rows from
+// row0 on. With several buffers every output row is stored into each - the
+// sharded bake's atlas all-gather done by the producing kernel itself over
+// peer (NVLink) memory (mf_bake_normal_map_dev_publish).
+constexpr int kMaxPublish = 8;
+struct OutSet {
+  uint8_t* p[kMaxPublish] = {};
+  int n = 0;
+  int row0 = 0;
+};
+void dilate_seams_to(Ctx& ctx, cudaStream_t s, int width, int height, int channels, const uint8_t* map_in,
+                     const uint8_t* valid, int in_row0, int in_rows, int radius, const OutSet& outs, int out_row0,
+                     int out_rows);
 // dilateSeams over a slab: input map rows [in_row0, in_row0 + in_rows) of a
 // width x height x channels image with the matching valid slab; outputs rows
 // [out_row0, out_row0 + out_rows) (which must lie `radius` rows inside the

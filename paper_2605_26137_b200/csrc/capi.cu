@@ -10,6 +10,7 @@
 // Meshes are validated on the device at upload (validateMesh,
 // core/mesh.cpp:37-48, plus face_uvs range); errors are reported in the
 // reference's throw order.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -145,6 +146,10 @@ using namespace mfb;
 
 struct mf_ctx {
   Ctx c;
+  std::vector<std::pair<void*, void*>> ipc_bases;  // (user pointer, opened base) of mf_ipc_open
+  ~mf_ctx() {
+    for (auto& b : ipc_bases) cudaIpcCloseMemHandle(b.second);
+  }
 };
 
 struct mf_mesh {
@@ -455,6 +460,7 @@ struct BakeEnq {
   double diag, frac;
   uint8_t* rgb_out;
   bool debug;
+  const OutSet* pub = nullptr;  // set: the dilation stores every output row into each buffer
   Timer& tm;
   BakeMarks& mk;
   GBufDev g;
@@ -568,7 +574,8 @@ struct BakeEnq {
     ta.counters = counters;
     transfer_normals(c, s, bvh, ta);
     mk.e4 = tm.mark(s);
-    dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out, rb, re - rb);
+    if (pub) dilate_seams_to(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, *pub, rb, re - rb);
+    else dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out, rb, re - rb);
     mk.e5 = tm.mark(s);
     MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(
@@ -580,8 +587,9 @@ struct BakeEnq {
 // the same sequence can be captured into a CUDA graph.
 void enqueue_bake(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
                   int rb, int re, uint8_t* rgb_out, bool debug, Timer& tm, BakeMarks& mk, int* hflags_pinned,
-                  unsigned long long* hcnt_pinned) {
+                  unsigned long long* hcnt_pinned, const OutSet* pub = nullptr) {
   BakeEnq q(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, debug, tm, mk);
+  q.pub = pub;
   // MFB_DIAG_SKIP=bvh|low|normals: DIAGNOSTIC ONLY (critical-path analysis):
   // reuse that phase's buffers from the previous (eager) call instead of
   // recomputing them. Never set in a measured run.
@@ -618,7 +626,7 @@ void enqueue_bake(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double 
 // outputs always run eagerly.
 void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
               int rb, int re, uint8_t* rgb_out, int32_t* dbg_face, double* dbg_ts, mf_bake_stats* st,
-              Timer& tm, cudaEvent_t t_begin) {
+              Timer& tm, cudaEvent_t t_begin, const OutSet* pub = nullptr) {
   check_lowpoly(lo, res);
   check_mesh(hi);
   check_transfer_cfg(diag, frac);
@@ -648,6 +656,10 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
   } key{lo, hi, rgb_out, lo->mem, hi->mem, lo->m.nf, lo->m.nv, lo->m.nu, hi->m.nf, hi->m.nv, res, radius, rb, re,
         c.timing ? 1 : 0, diag, frac};
   std::vector<char> kb(reinterpret_cast<const char*>(&key), reinterpret_cast<const char*>(&key) + sizeof(key));
+  if (pub) {  // published bakes are keyed on their destination buffers too
+    const char* pb = reinterpret_cast<const char*>(pub);
+    kb.insert(kb.end(), pb, pb + sizeof(OutSet));
+  }
   const int s0 = std::max(0, rb - radius);
   for (int attempt = 0;; ++attempt) {
     HostTrace ht("bake_dev");
@@ -672,7 +684,7 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
       cudaGraph_t graph = nullptr;
       MFB_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
       try {
-        enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, false, t2, mk, hflags, hcnt);
+        enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, false, t2, mk, hflags, hcnt, pub);
       } catch (...) {
         cudaStreamEndCapture(s, &graph);
         if (graph) cudaGraphDestroy(graph);
@@ -682,7 +694,7 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
       if (c.alloc_gen != c.bake_prev_gen) {  // something allocated during capture: do not keep it
         cudaGraphDestroy(graph);
         c.bake_prev_gen = c.alloc_gen;
-        enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, false, t2, mk, hflags, hcnt);
+        enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, false, t2, mk, hflags, hcnt, pub);
       } else {
         if (c.bake_exec) cudaGraphExecDestroy(c.bake_exec);
         c.bake_exec = nullptr;
@@ -693,7 +705,8 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
         MFB_CUDA_TRY(cudaGraphLaunch(c.bake_exec, s));
         }
     } else {
-      enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, dbg_face || dbg_ts, t2, mk, hflags, hcnt);
+      enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, dbg_face || dbg_ts, t2, mk, hflags, hcnt,
+                   pub);
       c.bake_prev_key = kb;
       c.bake_prev_gen = c.alloc_gen;
     }
@@ -1642,6 +1655,89 @@ int mf_cast_visibility(mf_ctx* ctx, const mf_mesh_view* mesh, int viewpoints, in
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
     if (state)
       for (int f = 0; f < nf; ++f) state[f] = hits[f] > 0 ? 1 : 0;  // visibility.cpp:53-56
+    return MF_OK;
+  });
+}
+}  // extern "C"
+
+// ---------------------------------------------------------------- peer-memory publish (multi-GPU)
+extern "C" {
+int mf_ipc_export(const void* dev_ptr, uint8_t* handle, uint64_t* offset) {
+  if (!dev_ptr || !handle || !offset) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(nullptr, [&]() -> int {
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    cudaIpcMemHandle_t h;
+    {
+      cudaPointerAttributes a{};
+      MFB_CUDA_TRY(cudaPointerGetAttributes(&a, dev_ptr));
+      if (a.type != cudaMemoryTypeDevice) throw ApiError(MF_ERR_BAD_ARGUMENT, "not device memory");
+    }
+    // the caller's pointer may sit inside a larger (caching-allocator) block:
+    // find its base with the driver entry point (no link-time libcuda)
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q{};
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return reinterpret_cast<RangeFn>(fn);
+    }();
+    if (!range || range(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS)
+      throw ApiError(MF_ERR_CUDA, "cuMemGetAddressRange failed");
+    void* b = reinterpret_cast<void*>(base);
+    MFB_CUDA_TRY(cudaIpcGetMemHandle(&h, b));
+    std::memcpy(handle, &h, sizeof(h));
+    *offset = static_cast<uint64_t>(reinterpret_cast<uintptr_t>(dev_ptr) - static_cast<uintptr_t>(base));
+    return MF_OK;
+  });
+}
+
+int mf_ipc_open(mf_ctx* ctx, const uint8_t* handle, uint64_t offset, void** dev_ptr) {
+  if (!ctx || !handle || !dev_ptr) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    MFB_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dev_ptr = static_cast<char*>(base) + offset;
+    ctx->ipc_bases.push_back({*dev_ptr, base});
+    return MF_OK;
+  });
+}
+
+int mf_ipc_close(mf_ctx* ctx, void* dev_ptr) {
+  if (!ctx || !dev_ptr) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    for (auto it = ctx->ipc_bases.begin(); it != ctx->ipc_bases.end(); ++it)
+      if (it->first == dev_ptr) {
+        MFB_CUDA_TRY(cudaIpcCloseMemHandle(it->second));
+        ctx->ipc_bases.erase(it);
+        return MF_OK;
+      }
+    throw ApiError(MF_ERR_BAD_ARGUMENT, "pointer was not opened with mf_ipc_open");
+  });
+}
+
+int mf_bake_normal_map_dev_publish(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int res, double bbox_diagonal,
+                                   double max_distance_fraction, int radius, int row_begin, int row_end,
+                                   void* const* dst_atlases, int n_dst, mf_bake_stats* stats) {
+  if (!ctx || !lowpoly || !highpoly || !dst_atlases) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  if (n_dst < 1 || n_dst > kMaxPublish) return fail(MF_ERR_BAD_ARGUMENT, "n_dst must be 1..8");
+  return guarded(ctx, [&]() -> int {
+    OutSet outs;
+    for (int k = 0; k < n_dst; ++k) {
+      if (!dst_atlases[k]) throw ApiError(MF_ERR_BAD_ARGUMENT, "null destination atlas");
+      outs.p[k] = static_cast<uint8_t*>(dst_atlases[k]);
+    }
+    outs.n = n_dst;
+    outs.row0 = 0;  // full res x res x 3 atlases: rows land at their own index
+    Timer tm(ctx->c, 8);
+    mf_bake_stats local{};
+    bake_dev(ctx->c, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius, row_begin, row_end,
+             outs.p[0] + 3ll * row_begin * res, nullptr, nullptr, &local, tm, nullptr, &outs);
+    if (stats) *stats = local;
     return MF_OK;
   });
 }

@@ -73,9 +73,8 @@ __device__ __forceinline__ void chamfer_step(const int16_t* __restrict__ ox, con
 __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int channels,
                                                       const uint8_t* __restrict__ map_in,
                                                       const uint8_t* __restrict__ valid, int in_row0,
-                                                      int in_rows, int radius,
-                                                      uint8_t* __restrict__ map_out, int out_row0,
-                                                      int out_rows) {
+                                                      int in_rows, int radius, OutSet outs,
+                                                      int out_row0, int out_rows) {
   extern __shared__ int16_t sm[];
   const int rw = kTW + 2 * radius, rh = kTH + 2 * radius, cells = rw * rh;
   int16_t* ox0 = sm;
@@ -135,13 +134,15 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
   if (!work && gx0 + kTW <= width && gy0 + kTH <= out_end) {
     const int64_t row_bytes = static_cast<int64_t>(width) * channels;
     const uint8_t* src0 = map_in + (static_cast<int64_t>(gy0 - in_row0) * width + gx0) * channels;
-    uint8_t* dst0 = map_out + (static_cast<int64_t>(gy0 - out_row0) * width + gx0) * channels;
+    const int64_t dst_off = (static_cast<int64_t>(gy0 - outs.row0) * width + gx0) * channels;
     const int vec_per_row = kTW * channels / 16;
-    if (kTW * channels % 16 == 0 && row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(src0) & 15) == 0 &&
-        (reinterpret_cast<uintptr_t>(dst0) & 15) == 0) {
+    bool aligned = kTW * channels % 16 == 0 && row_bytes % 16 == 0 && (reinterpret_cast<uintptr_t>(src0) & 15) == 0;
+    for (int k = 0; k < outs.n; ++k) aligned = aligned && (reinterpret_cast<uintptr_t>(outs.p[k] + dst_off) & 15) == 0;
+    if (aligned) {
       for (int c = threadIdx.x; c < vec_per_row * kTH; c += blockDim.x) {
         const int r = c / vec_per_row, k = c % vec_per_row;
-        reinterpret_cast<uint4*>(dst0 + r * row_bytes)[k] = __ldg(reinterpret_cast<const uint4*>(src0 + r * row_bytes) + k);
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src0 + r * row_bytes) + k);
+        for (int o = 0; o < outs.n; ++o) reinterpret_cast<uint4*>(outs.p[o] + dst_off + r * row_bytes)[k] = v;
       }
       return;
     }
@@ -161,8 +162,9 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
       }
     }
     const uint8_t* src = map_in + (static_cast<int64_t>(srcy - in_row0) * width + srcx) * channels;
-    uint8_t* dst = map_out + (static_cast<int64_t>(gy - out_row0) * width + gx) * channels;
-    for (int ch = 0; ch < channels; ++ch) dst[ch] = src[ch];
+    const int64_t doff = (static_cast<int64_t>(gy - outs.row0) * width + gx) * channels;
+    for (int o = 0; o < outs.n; ++o)
+      for (int ch = 0; ch < channels; ++ch) outs.p[o][doff + ch] = src[ch];
   }
 }
 
@@ -227,15 +229,17 @@ __global__ void k_dilate_copy(int width, int channels, const uint8_t* __restrict
 
 }  // namespace
 
-void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
-                  const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
-                  int radius, uint8_t* map_out, int out_row0, int out_rows) {
-  if (out_rows <= 0 || width <= 0) return;
+void dilate_seams_to(Ctx& ctx, cudaStream_t s, int width, int height, int channels, const uint8_t* map_in,
+                     const uint8_t* valid, int in_row0, int in_rows, int radius, const OutSet& outs, int out_row0,
+                     int out_rows) {
+  if (out_rows <= 0 || width <= 0 || outs.n <= 0) return;
   const int64_t out_bytes = static_cast<int64_t>(width) * out_rows * channels;
+  const int64_t dst_off = static_cast<int64_t>(out_row0 - outs.row0) * width * channels;
   if (radius == 0) {
-    MFB_CUDA_TRY(cudaMemcpyAsync(map_out,
-                                 map_in + static_cast<int64_t>(out_row0 - in_row0) * width * channels,
-                                 out_bytes, cudaMemcpyDeviceToDevice, s));
+    for (int k = 0; k < outs.n; ++k)
+      MFB_CUDA_TRY(cudaMemcpyAsync(outs.p[k] + dst_off,
+                                   map_in + static_cast<int64_t>(out_row0 - in_row0) * width * channels,
+                                   out_bytes, cudaMemcpyDeviceToDevice, s));
     return;
   }
   const size_t smem = static_cast<size_t>(4) * (kTW + 2 * radius) * (kTH + 2 * radius) * sizeof(int16_t);
@@ -251,7 +255,7 @@ void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
     }
     const int tiles = ((width + kTW - 1) / kTW) * ((out_rows + kTH - 1) / kTH);
     k_dilate_fused<<<tiles, 256, smem, s>>>(width, height, channels, map_in, valid, in_row0, in_rows,
-                                            radius, map_out, out_row0, out_rows);
+                                            radius, outs, out_row0, out_rows);
     ctx.count_launch();
     MFB_CUDA_TRY(cudaGetLastError());
     return;
@@ -271,10 +275,22 @@ void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
     std::swap(sy, nsy);
     std::swap(d2, nd2);
   }
-  k_dilate_copy<<<div_up(static_cast<int64_t>(width) * out_rows, T), T, 0, s>>>(
-      width, channels, map_in, valid, in_row0, sx, sy, d2, map_out, out_row0, out_rows);
-  ctx.count_launch(radius + 2);
+  for (int k = 0; k < outs.n; ++k)
+    k_dilate_copy<<<div_up(static_cast<int64_t>(width) * out_rows, T), T, 0, s>>>(
+        width, channels, map_in, valid, in_row0, sx, sy, d2, outs.p[k] + dst_off, out_row0, out_rows);
+  ctx.count_launch(radius + 1 + outs.n);
   MFB_CUDA_TRY(cudaGetLastError());
+}
+
+void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
+                  const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
+                  int radius, uint8_t* map_out, int out_row0, int out_rows) {
+  OutSet one;
+  one.p[0] = map_out;
+  one.n = 1;
+  one.row0 = out_row0;
+  dilate_seams_to(ctx, s, width, height, channels, map_in, valid, in_row0, in_rows, radius, one, out_row0,
+                  out_rows);
 }
 
 }  // namespace mfb

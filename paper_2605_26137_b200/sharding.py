@@ -7,6 +7,12 @@ rows - the library rasterises and transfers `radius` halo rows on each side
 itself, so the dilated slab is exact without any exchange - and one
 all-gather of the RGB8 slabs (padded to the largest slab) assembles the
 row-major atlas on every rank. The BVH is built per rank (replicated).
+
+`PeerAtlas` is the fused alternative: every rank exports its full-atlas
+buffer over CUDA IPC, opens its peers', and the bake's dilation kernel stores
+each output row straight into all of them (`mf_bake_normal_map_dev_publish`),
+so the gather rides on the producing kernel's stores over NVLink instead of
+a separate NCCL collective; one host barrier then marks every atlas complete.
 """
 from __future__ import annotations
 
@@ -80,3 +86,48 @@ def sharded_bake(bake_rows: Callable[[int, int], object], ranges: Sequence[Tuple
     gathered = [torch.empty_like(as_tensor) for _ in ranges]
     dist.all_gather(gathered, as_tensor.contiguous(), group=group)
     return assemble(gathered, ranges)
+
+
+class PeerAtlas:
+    """Full-atlas buffers shared by all ranks of a node through CUDA IPC.
+
+    `atlas` is this rank's (res, res, 3) uint8 CUDA tensor; `dst` holds the
+    device pointers of every rank's atlas as seen from this process (own
+    first), ready for mf_bake_normal_map_dev_publish."""
+
+    def __init__(self, ctx, res: int, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from . import capi
+
+        self.ctx = ctx
+        self.atlas = torch.zeros((res, res, 3), dtype=torch.uint8, device="cuda")
+        handle = (ctypes.c_uint8 * 64)()
+        offset = ctypes.c_uint64(0)
+        capi.check(ctx.lib.mf_ipc_export(ctypes.c_void_p(self.atlas.data_ptr()), handle, ctypes.byref(offset)))
+        mine = (bytes(handle), int(offset.value))
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        every = [None] * world
+        dist.all_gather_object(every, mine, group=group)
+        self.opened = []
+        ptrs = [self.atlas.data_ptr()]
+        for r in range(world):
+            if r == rank:
+                continue
+            h = (ctypes.c_uint8 * 64).from_buffer_copy(every[r][0])
+            p = ctypes.c_void_p()
+            capi.check(ctx.lib.mf_ipc_open(ctx.h, h, ctypes.c_uint64(every[r][1]), ctypes.byref(p)))
+            self.opened.append(p.value)
+            ptrs.append(p.value)
+        self.dst = (ctypes.c_void_p * len(ptrs))(*ptrs)
+        self.n = len(ptrs)
+
+    def close(self):
+        import ctypes
+        for p in self.opened:
+            self.ctx.lib.mf_ipc_close(self.ctx.h, ctypes.c_void_p(p))
+        self.opened = []
