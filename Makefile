@@ -27,7 +27,7 @@ MF_HDRS := $(shell find include/meshforge -name '*.h' 2>/dev/null) include/eigen
 all: lib cpp peaks oracle
 
 lib: $(PKG)/libmfbake.so
-cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200
+cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200 build/test_io_cpu
 peaks: build/libmfpeaks.so
 
 build/cu/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
@@ -43,6 +43,10 @@ $(PKG)/libmeshforge_b200.so: $(PKG)/cpp/meshforge_b200.cpp $(PKG)/cpp/io_b200.cp
 	  -lz -Wl,-rpath,'$$ORIGIN'
 
 build/test_bake_b200: tests/cpp/test_bake_b200.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+build/test_io_cpu: tests/cpp/test_io_cpu.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
