@@ -32,6 +32,8 @@ struct Ctx {
   bool own_stream = false;
   cudaStream_t side = nullptr;      // second stream: dense-mesh work overlaps the lowpoly work
   cudaStream_t aux = nullptr;       // third stream: lowpoly wedge frames overlap its reliability pass
+  cudaStream_t side2 = nullptr;     // LBVH helper: triangle repack alongside the hierarchy emission
+  cudaEvent_t lfork = nullptr, ljoin = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr, join3 = nullptr;
   cudaEvent_t hi_ready = nullptr;   // host entry point: dense mesh uploaded and validated
   cudaEvent_t dfork = nullptr, djoin = nullptr;  // host entry point: dense phase side -> aux -> side

@@ -69,6 +69,7 @@ void Ctx::sync_all() {
   MFB_CUDA_TRY(cudaStreamSynchronize(stream));
   if (side) MFB_CUDA_TRY(cudaStreamSynchronize(side));
   if (aux) MFB_CUDA_TRY(cudaStreamSynchronize(aux));
+  if (side2) MFB_CUDA_TRY(cudaStreamSynchronize(side2));
 }
 void* Ctx::cub_temp(size_t bytes, cudaStream_t s) {
   const int slot = s == side ? 1 : (s == aux ? 2 : 0);
@@ -104,14 +105,16 @@ Ctx::~Ctx() {
   if (stream) cudaStreamSynchronize(stream);
   if (side) cudaStreamSynchronize(side);
   if (aux) cudaStreamSynchronize(aux);
+  if (side2) cudaStreamSynchronize(side2);
   for (auto& kv : scratch) cudaFree(kv.second.ptr);
   for (auto& kv : pinned) cudaFreeHost(kv.second.ptr);
   for (void* p : cub_tmp)
     if (p) cudaFree(p);
-  for (cudaEvent_t e : {fork, join, fork2, join2, join3, hi_ready, dfork, djoin, up_fork, up_join})
+  for (cudaEvent_t e : {fork, join, fork2, join2, join3, hi_ready, dfork, djoin, up_fork, up_join, lfork, ljoin})
     if (e) cudaEventDestroy(e);
   if (side) cudaStreamDestroy(side);
   if (aux) cudaStreamDestroy(aux);
+  if (side2) cudaStreamDestroy(side2);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -923,8 +926,10 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     }
     MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
     MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.aux, cudaStreamNonBlocking));
+    MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.side2, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3, &ctx->c.hi_ready,
-                            &ctx->c.dfork, &ctx->c.djoin, &ctx->c.up_fork, &ctx->c.up_join})
+                            &ctx->c.dfork, &ctx->c.djoin, &ctx->c.up_fork, &ctx->c.up_join, &ctx->c.lfork,
+                            &ctx->c.ljoin})
       MFB_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     *out = ctx.release();
     return MF_OK;

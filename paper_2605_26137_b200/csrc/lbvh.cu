@@ -40,22 +40,21 @@ __host__ __device__ __forceinline__ double from_ordered(unsigned long long b) {
 #endif
 }
 
-// acc[0..2] = min centroid, acc[3..5] = max centroid, acc[6] = max |vertex coord|
-__global__ void k_bounds(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
-                         int nv, unsigned long long* acc) {
+// acc[0..2] = min vertex, acc[3..5] = max vertex (the Morton quantisation
+// domain: it contains every centroid, and one streaming pass over the
+// positions is cheaper than gathering every face's corners), acc[6] = max
+// |vertex coord|
+__global__ void k_bounds(const double* __restrict__ pos, int nv, unsigned long long* acc) {
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
   double amax = 0.0;
-  for (int f = blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += gridDim.x * blockDim.x) {
-    const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const double ck = ((pos[3 * a + k] + pos[3 * b + k]) + pos[3 * c + k]) / 3.0;
-      mn[k] = fmin(mn[k], ck);
-      mx[k] = fmax(mx[k], ck);
+      const double c = pos[3 * v + k];
+      mn[k] = fmin(mn[k], c);
+      mx[k] = fmax(mx[k], c);
+      amax = fmax(amax, fabs(c));
     }
-  }
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
-    amax = fmax(amax, fmax(fabs(pos[3 * v]), fmax(fabs(pos[3 * v + 1]), fabs(pos[3 * v + 2]))));
   }
   // warp reduce, then block reduce in shared memory, one atomic per block
 #pragma unroll
@@ -475,7 +474,7 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
 
   const int T = 256;
   const int grid_b = std::min(div_up(std::max(n, m.nv), T), kNumSMs * 8);
-  k_bounds<<<grid_b, T, 0, s>>>(m.pos, m.faces, n, m.nv, acc);
+  k_bounds<<<grid_b, T, 0, s>>>(m.pos, m.nv, acc);
   // Morton bits per axis: 10 (30-bit keys, 4 radix passes) unless
   // MFB_MORTON_BITS (6..10) overrides it; fewer bits = fewer sort passes.
   static const int axis_bits = [] {
@@ -498,13 +497,22 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
     const int v = e ? std::atoi(e) : kLeafMaxDefault;
     return v >= 1 && v <= 7 ? v : kLeafMaxDefault;
   }();
+  // repack (gathers) and emit (key searches) both need only the sorted
+  // keys / ids: repack runs on the context's helper stream alongside emit
+  cudaStream_t rs = ctx.side2 ? ctx.side2 : s;
+  if (rs != s) {
+    MFB_CUDA_TRY(cudaEventRecord(ctx.lfork, s));
+    MFB_CUDA_TRY(cudaStreamWaitEvent(rs, ctx.lfork, 0));
+  }
+  k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
+  if (rs != s) MFB_CUDA_TRY(cudaEventRecord(ctx.ljoin, rs));
   if (n > 1) {
     MFB_CUDA_TRY(cudaMemsetAsync(starts_n, 0, sizeof(int), s));
     k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent, starts,
                                           starts_n);
     ctx.count_launch();
   }
-  k_repack<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
+  if (rs != s) MFB_CUDA_TRY(cudaStreamWaitEvent(s, ctx.ljoin, 0));
   if (n > 1) {
     // starts <= leaf ranges <= n; threads past the device count exit at once
     k_refit_ranges<<<div_up(n, T), T, 0, s>>>(out.tbox, out.nodes, starts, starts_n, out.nodes,
