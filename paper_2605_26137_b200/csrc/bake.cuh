@@ -33,6 +33,8 @@ struct Ctx {
   cudaStream_t side = nullptr;      // second stream: dense-mesh work overlaps the lowpoly work
   cudaStream_t aux = nullptr;       // third stream: lowpoly wedge frames overlap its reliability pass
   cudaStream_t side2 = nullptr;     // LBVH helper: triangle repack alongside the hierarchy emission
+  cudaStream_t aux2 = nullptr;      // lowpoly reliability pass alongside the raster setup and binning
+  cudaEvent_t setup_done = nullptr, join4 = nullptr;
   cudaEvent_t lfork = nullptr, ljoin = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr, join3 = nullptr;
   cudaEvent_t hi_ready = nullptr;   // host entry point: dense mesh uploaded and validated
@@ -46,10 +48,10 @@ struct Ctx {
   };
   std::unordered_map<std::string, Buf> scratch;
   std::unordered_map<std::string, Buf> pinned;
-  // CUB temp storage, one slot per stream (main, side, aux): concurrent
+  // CUB temp storage, one slot per stream (main, side, aux, aux2, side2): concurrent
   // branches of the bake must not share it
-  void* cub_tmp[3] = {nullptr, nullptr, nullptr};
-  size_t cub_tmp_bytes[3] = {0, 0, 0};
+  void* cub_tmp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // main, side, aux, aux2, side2
+  size_t cub_tmp_bytes[5] = {0, 0, 0, 0, 0};
   int64_t bin_capacity = 0;         // raster tile-bin capacity hint (grows on overflow)
 
   // Grow-only named device scratch (never shrinks; freed with the context).
@@ -195,6 +197,7 @@ struct RasterPlan {
   void* attrs = nullptr;   // AttrFace[nf]
   int nf = 0;
   int res = 0;
+  cudaEvent_t pending[2] = {nullptr, nullptr};  // side branches raster_gbuffer joins before the texel kernel
 };
 void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterPlan& plan);
 // Frames only (for mf_wedge_tangents): F x 3 x {T, B, N} x 3 doubles.

@@ -70,9 +70,10 @@ void Ctx::sync_all() {
   if (side) MFB_CUDA_TRY(cudaStreamSynchronize(side));
   if (aux) MFB_CUDA_TRY(cudaStreamSynchronize(aux));
   if (side2) MFB_CUDA_TRY(cudaStreamSynchronize(side2));
+  if (aux2) MFB_CUDA_TRY(cudaStreamSynchronize(aux2));
 }
 void* Ctx::cub_temp(size_t bytes, cudaStream_t s) {
-  const int slot = s == side ? 1 : (s == aux ? 2 : 0);
+  const int slot = s == side ? 1 : (s == aux ? 2 : (s == aux2 ? 3 : (s == side2 ? 4 : 0)));
   void*& p = cub_tmp[slot];
   size_t& n = cub_tmp_bytes[slot];
   if (n < bytes) {
@@ -106,15 +107,17 @@ Ctx::~Ctx() {
   if (side) cudaStreamSynchronize(side);
   if (aux) cudaStreamSynchronize(aux);
   if (side2) cudaStreamSynchronize(side2);
+  if (aux2) cudaStreamSynchronize(aux2);
   for (auto& kv : scratch) cudaFree(kv.second.ptr);
   for (auto& kv : pinned) cudaFreeHost(kv.second.ptr);
   for (void* p : cub_tmp)
     if (p) cudaFree(p);
-  for (cudaEvent_t e : {fork, join, fork2, join2, join3, hi_ready, dfork, djoin, up_fork, up_join, lfork, ljoin})
+  for (cudaEvent_t e : {fork, join, fork2, join2, join3, hi_ready, dfork, djoin, up_fork, up_join, lfork, ljoin, setup_done, join4})
     if (e) cudaEventDestroy(e);
   if (side) cudaStreamDestroy(side);
   if (aux) cudaStreamDestroy(aux);
   if (side2) cudaStreamDestroy(side2);
+  if (aux2) cudaStreamDestroy(aux2);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -436,7 +439,7 @@ void run_graphed(Ctx& c, Ctx::GraphSlot& slot, cudaStream_t s, const std::vector
     }
     if (slot.exec) cudaGraphExecDestroy(slot.exec);
     slot.exec = nullptr;
-    MFB_CUDA_TRY(cudaGraphInstantiate(&slot.exec, graph, 0));
+    MFB_CUDA_TRY(cudaGraphInstantiateWithFlags(&slot.exec, graph, cudaGraphInstantiateFlagUseNodePriority));
     cudaGraphDestroy(graph);
     slot.key = key;
     slot.gen = c.alloc_gen;
@@ -701,7 +704,7 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
       } else {
         if (c.bake_exec) cudaGraphExecDestroy(c.bake_exec);
         c.bake_exec = nullptr;
-        MFB_CUDA_TRY(cudaGraphInstantiate(&c.bake_exec, graph, 0));
+        MFB_CUDA_TRY(cudaGraphInstantiateWithFlags(&c.bake_exec, graph, cudaGraphInstantiateFlagUseNodePriority));
         cudaGraphDestroy(graph);
         c.bake_key = kb;
         c.bake_gen = c.alloc_gen;
@@ -924,12 +927,22 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
       MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
       ctx->c.own_stream = true;
     }
-    MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.side, cudaStreamNonBlocking));
+    // the dense LBVH branch is the bake's longest pre-transfer chain: its
+    // streams get the higher priority so the lowpoly branches fill in around it
+    // (MFB_LBVH_PRIORITY=0 disables)
+    static const bool prio = [] {
+      const char* e = std::getenv("MFB_LBVH_PRIORITY");
+      return !(e && e[0] == '0');
+    }();
+    int lo_prio = 0, hi_prio = 0;
+    MFB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, prio ? hi_prio : lo_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.aux, cudaStreamNonBlocking));
-    MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.side2, cudaStreamNonBlocking));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, prio ? hi_prio : lo_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.aux2, cudaStreamNonBlocking));
     for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3, &ctx->c.hi_ready,
                             &ctx->c.dfork, &ctx->c.djoin, &ctx->c.up_fork, &ctx->c.up_join, &ctx->c.lfork,
-                            &ctx->c.ljoin})
+                            &ctx->c.ljoin, &ctx->c.setup_done, &ctx->c.join4})
       MFB_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     *out = ctx.release();
     return MF_OK;

@@ -380,13 +380,13 @@ __global__ void __launch_bounds__(256) k_island_select(int nu, const int* __rest
 }
 
 // ------------------------------------------------------------ face setup
-__global__ void k_face_setup(const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
-                             int res, const double* __restrict__ uv_area, const double* __restrict__ ratio,
-                             const int* __restrict__ island, const double* __restrict__ median,
-                             RasterFace* __restrict__ rf, AttrFace* __restrict__ attrs) {
+// reliable (gbuffer.cpp:74-81) into the face's raster record and attributes;
+// runs after k_face_setup, which leaves rel = 0
+__global__ void k_face_rel(int nf, const double* __restrict__ uv_area, const double* __restrict__ ratio,
+                           const int* __restrict__ island, const double* __restrict__ median,
+                           RasterFace* __restrict__ rf, AttrFace* __restrict__ attrs) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
-  // reliable (gbuffer.cpp:74-81)
   int rel = 0;
   if (!(uv_area[f] < 1e-8) && !(ratio[f] < 0.0)) {
     const double m = median[island[f]];
@@ -394,9 +394,17 @@ __global__ void k_face_setup(const double* __restrict__ uvs, const int32_t* __re
   }
   attrs[f].reliable = rel;
   attrs[f].pad = 0;
+  rf[f].rel = rel;
+}
 
+// UV-space raster setup of a face (gbuffer.cpp:114-144): everything the
+// binning and the coverage test need, from the UVs alone
+__global__ void k_face_setup(const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf, int res,
+                             RasterFace* __restrict__ rf) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
   RasterFace s;
-  s.rel = rel;
+  s.rel = 0;
   s.pad[0] = s.pad[1] = s.pad[2] = 0;
   const double R = static_cast<double>(res);
   const int u[3] = {fuv[3 * f], fuv[3 * f + 1], fuv[3 * f + 2]};
@@ -901,16 +909,21 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
   const int nf = lo.nf, nu = lo.nu;
   auto* rf = ctx.buf<RasterFace>("lo.rf", nf);
   auto* attrs = ctx.buf<AttrFace>("lo.attrs", nf);
-  // fork: the wedge frames (computeWedgeTangents) on the aux stream overlap
-  // the reliability pass below; they write disjoint AttrFace fields
-  // (P/N/T vs reliable/pad). Joined before returning.
+  // Three branches: the UV-only raster setup on `s` (the binning follows it
+  // there in raster_gbuffer), the wedge frames (computeWedgeTangents) on aux
+  // and the reliability pass (reliableFaces) on aux2, which ends by setting
+  // the faces' rel flags after the setup; raster_gbuffer joins both side
+  // branches just before the texel kernel. They write disjoint fields.
   cudaStream_t ws = ctx.aux ? ctx.aux : s;
-  if (ws != s) {
-    MFB_CUDA_TRY(cudaEventRecord(ctx.fork2, s));
-    MFB_CUDA_TRY(cudaStreamWaitEvent(ws, ctx.fork2, 0));
-  }
+  cudaStream_t us = ctx.aux2 ? ctx.aux2 : s;
+  if (ws != s || us != s) MFB_CUDA_TRY(cudaEventRecord(ctx.fork2, s));
+  if (ws != s) MFB_CUDA_TRY(cudaStreamWaitEvent(ws, ctx.fork2, 0));
+  if (us != s) MFB_CUDA_TRY(cudaStreamWaitEvent(us, ctx.fork2, 0));
   wedge_pipeline(ctx, ws, lo, nullptr, attrs);
   if (ws != s) MFB_CUDA_TRY(cudaEventRecord(ctx.join2, ws));
+
+  k_face_setup<<<div_up(nf, T), T, 0, s>>>(lo.uvs, lo.fuv, nf, res, rf);
+  if (us != s) MFB_CUDA_TRY(cudaEventRecord(ctx.setup_done, s));
 
   // reliableFaces (gbuffer.cpp:31-83)
   int* parent = ctx.buf<int>("lo.rel.parent", nu);
@@ -922,26 +935,29 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
   int* cursor = ctx.buf<int>("lo.rel.cursor", nu + 1);
   auto* items = ctx.buf<unsigned long long>("lo.rel.items", nf);
   double* median = ctx.buf<double>("lo.rel.median", nu);
-  MFB_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int) * (nu + 1), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (nu + 1), s));
-  k_iota<<<div_up(nu, T), T, 0, s>>>(nu, parent);
-  k_uf_unite<<<div_up(nf, T), T, 0, s>>>(lo.fuv, nf, parent);
-  k_uf_flatten<<<div_up(nu, T), T, 0, s>>>(nu, parent);
-  k_face_ratio<<<div_up(nf, T), T, 0, s>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, parent, uv_area, ratio, island,
-                                           count);
+  MFB_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int) * (nu + 1), us));
+  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (nu + 1), us));
+  k_iota<<<div_up(nu, T), T, 0, us>>>(nu, parent);
+  k_uf_unite<<<div_up(nf, T), T, 0, us>>>(lo.fuv, nf, parent);
+  k_uf_flatten<<<div_up(nu, T), T, 0, us>>>(nu, parent);
+  k_face_ratio<<<div_up(nf, T), T, 0, us>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, parent, uv_area, ratio, island,
+                                            count);
   size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, start, nu + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, count, start, nu + 1, s));
-  k_island_fill<<<div_up(nf, T), T, 0, s>>>(nf, ratio, island, start, cursor, items);
-  k_island_select<<<nu, 256, 0, s>>>(nu, count, start, items, median);
-  k_face_setup<<<div_up(nf, T), T, 0, s>>>(lo.uvs, lo.fuv, nf, res, uv_area, ratio, island, median, rf, attrs);
-  ctx.count_launch(7);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, start, nu + 1, us);
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, us), tmp, count, start, nu + 1, us));
+  k_island_fill<<<div_up(nf, T), T, 0, us>>>(nf, ratio, island, start, cursor, items);
+  k_island_select<<<nu, 256, 0, us>>>(nu, count, start, items, median);
+  if (us != s) MFB_CUDA_TRY(cudaStreamWaitEvent(us, ctx.setup_done, 0));
+  k_face_rel<<<div_up(nf, T), T, 0, us>>>(nf, uv_area, ratio, island, median, rf, attrs);
+  ctx.count_launch(9);
   MFB_CUDA_TRY(cudaGetLastError());
-  if (ws != s) MFB_CUDA_TRY(cudaStreamWaitEvent(s, ctx.join2, 0));
+  if (us != s) MFB_CUDA_TRY(cudaEventRecord(ctx.join4, us));
   plan.faces = rf;
   plan.attrs = attrs;
   plan.nf = nf;
   plan.res = res;
+  plan.pending[0] = ws != s ? ctx.join2 : nullptr;
+  plan.pending[1] = us != s ? ctx.join4 : nullptr;
 }
 
 void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPlan& plan, GBufDev& g,
@@ -973,6 +989,9 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
                                               capacity, flags_dev + 1);
   MFB_CUDA_TRY(cudaMemcpyAsync(flags_dev + 2, start + ntiles, sizeof(int), cudaMemcpyDeviceToDevice, s));
   if (row_counts_dev) MFB_CUDA_TRY(cudaMemsetAsync(row_counts_dev, 0, sizeof(int64_t) * g.rows, s));
+  // the wedge frames and reliability branches of prepare_lowpoly
+  for (cudaEvent_t e : plan.pending)
+    if (e) MFB_CUDA_TRY(cudaStreamWaitEvent(s, e, 0));
   auto* rc = reinterpret_cast<unsigned long long*>(row_counts_dev);
   // Split raster (default): coverage + compaction, then a barrier-free
   // interpolation kernel over the compacted queries. MFB_RASTER_SPLIT=0
