@@ -139,13 +139,16 @@ struct alignas(16) TBox {
   float4 a, b;
 };
 
+// Leaf range reference: ~(first << 4 | count), count <= kLeafCountMax
+// (first < 2^27 triangles).
+constexpr int kLeafCountMax = 15;
 __host__ __device__ __forceinline__ int32_t leaf_ref(int first, int count) {
-  return ~((first << 3) | count);
+  return ~((first << 4) | count);
 }
 __host__ __device__ __forceinline__ void leaf_decode(int32_t ref, int& first, int& count) {
   const int32_t r = ~ref;
-  first = r >> 3;
-  count = r & 7;
+  first = r >> 4;
+  count = r & 15;
 }
 
 // 4-wide node: the grandchildren of binary node i (children of i's internal
@@ -177,7 +180,8 @@ struct Lbvh {
 };
 
 // Build into buffers owned by `owner` scratch names prefixed with `tag`.
-void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag);
+// leaf_hint: leaf-range size cap (0 = kLeafMaxDefault); MFB_LEAF_MAX overrides.
+void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint = 0);
 // The descriptor lbvh_build fills (device buffers by scratch name), without
 // launching anything: used when a captured build is replayed.
 void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag);

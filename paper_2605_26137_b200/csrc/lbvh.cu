@@ -454,7 +454,7 @@ void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag) 
   out.scene_acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
 }
 
-void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag) {
+void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint) {
   const int n = m.nf;
   lbvh_layout(ctx, m, out, tag);
   auto* acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
@@ -490,13 +490,16 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   void* tptr = ctx.cub_temp(tmp, s);
   MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 3 * axis_bits, s));
 
-  // Leaf size: kLeafMaxDefault (the reference uses 4, bvh.cpp:13; the
-  // results are tree-independent) unless MFB_LEAF_MAX (1..7) overrides it.
-  static const int leaf_max = [] {
+  // Leaf size: the caller's hint or kLeafMaxDefault (the reference uses 4,
+  // bvh.cpp:13; results are tree-independent) unless MFB_LEAF_MAX (1..15)
+  // overrides it.
+  static const int leaf_env = [] {
     const char* e = std::getenv("MFB_LEAF_MAX");
-    const int v = e ? std::atoi(e) : kLeafMaxDefault;
-    return v >= 1 && v <= 7 ? v : kLeafMaxDefault;
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 1 && v <= kLeafCountMax ? v : 0;
   }();
+  const int leaf_max = leaf_env ? leaf_env
+                                : (leaf_hint >= 1 && leaf_hint <= kLeafCountMax ? leaf_hint : kLeafMaxDefault);
   // repack (gathers) and emit (key searches) both need only the sorted
   // keys / ids: repack runs on the context's helper stream alongside emit
   cudaStream_t rs = ctx.side2 ? ctx.side2 : s;
