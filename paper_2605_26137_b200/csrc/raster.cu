@@ -620,6 +620,9 @@ __device__ __forceinline__ void interp_texel(const RasterFace& sfc, const AttrFa
 // Split raster, second kernel: one thread per compacted query (texel, face)
 // written by k_raster<2>; interpolates exactly as the fused path and writes
 // the same query record. No barriers, full SIMT width for the f64 chain.
+#ifndef MFB_INTERP_PF
+#define MFB_INTERP_PF 0
+#endif
 #ifndef MFB_INTERP_MINB
 #define MFB_INTERP_MINB 0
 #endif
@@ -633,8 +636,25 @@ __global__ void MFB_INTERP_BOUNDS k_interp(const RasterFace* __restrict__ rf,
                                                 const int2* __restrict__ pend, const int* __restrict__ count,
                                                 int res, int g_row0, QueryList q) {
   const int n = *count;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int2 tf = pend[i];
+  const int stride = gridDim.x * blockDim.x;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  int2 nxt = i < n ? pend[i] : make_int2(0, 0);
+  for (; i < n; i += stride) {
+    const int2 tf = nxt;
+#if MFB_INTERP_PF
+    // software pipelining: the next query's pair now, its face records into L1
+    if (i + stride < n) {
+      nxt = pend[i + stride];
+      const char* a = reinterpret_cast<const char*>(rf + nxt.y);
+      const char* b = reinterpret_cast<const char*>(attrs + nxt.y);
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 128));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(b));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(b + 128));
+    }
+#else
+    if (i + stride < n) nxt = pend[i + stride];
+#endif
     const int yr = tf.x / res, x = tf.x - yr * res;
     const double cx = x + 0.5, cy = (yr + g_row0) + 0.5;
     float P[3], Nf[3], Tf[3], Bf[3];
