@@ -571,7 +571,11 @@ struct BakeEnq {
   }
 
   // main stream, after both dense branches: transfer + dilation + flags
-  void tail(int* hflags_pinned, unsigned long long* hcnt_pinned) {
+  // With host_out (host-buffer entry point) the dilation runs in `bands` row
+  // bands and each band's D2H starts on aux2 as soon as it is dilated, so the
+  // download overlaps the remaining dilation; the main stream then waits for
+  // the last copy.
+  void tail(int* hflags_pinned, unsigned long long* hcnt_pinned, uint8_t* host_out = nullptr, int bands = 1) {
     cudaStream_t s = c.stream;
     MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
     MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join3, 0));
@@ -592,9 +596,29 @@ struct BakeEnq {
     ta.counters = counters;
     transfer_normals(c, s, bvh, ta);
     mk.e4 = tm.mark(s);
-    if (pub) dilate_seams_to(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, *pub, rb, re - rb);
-    else dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out, rb, re - rb);
-    mk.e5 = tm.mark(s);
+    cudaStream_t cp = c.aux2 ? c.aux2 : s;
+    if (host_out && !pub && bands > 1 && cp != s) {
+      for (int b = 0; b < bands; ++b) {
+        const int r0 = rb + static_cast<int>(static_cast<int64_t>(re - rb) * b / bands);
+        const int r1 = rb + static_cast<int>(static_cast<int64_t>(re - rb) * (b + 1) / bands);
+        if (r1 <= r0) continue;
+        const int64_t off = 3ll * (r0 - rb) * res;
+        dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out + off, r0, r1 - r0);
+        cudaEvent_t ev = c.pool_event(40 + b);
+        MFB_CUDA_TRY(cudaEventRecord(ev, s));
+        MFB_CUDA_TRY(cudaStreamWaitEvent(cp, ev, 0));
+        MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off, 3ll * (r1 - r0) * res, cudaMemcpyDeviceToHost, cp));
+      }
+      mk.e5 = tm.mark(s);
+      MFB_CUDA_TRY(cudaEventRecord(c.join4, cp));
+      MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join4, 0));
+    } else {
+      if (pub) dilate_seams_to(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, *pub, rb, re - rb);
+      else dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out, rb, re - rb);
+      mk.e5 = tm.mark(s);
+      if (host_out)
+        MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, 3ll * (re - rb) * res, cudaMemcpyDeviceToHost, s));
+    }
     MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(
         cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -866,9 +890,15 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilation radius must be >= 0");
   }
   q.dense_side(use_graphs);
-  q.tail(hflags, hcnt);
+  // MFB_E2E_DL_BANDS=k: dilate in k row bands, each downloaded as soon as it is
+  // done (measured within noise of one band at config B: 1 stays the default)
+  static const int dl_bands = [] {
+    const char* e = std::getenv("MFB_E2E_DL_BANDS");
+    const int v = e ? std::atoi(e) : 1;
+    return v >= 1 && v <= 16 ? v : 1;
+  }();
   cudaEvent_t t2 = tm.mark(s);
-  MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, s));
+  q.tail(hflags, hcnt, rgb_out, dl_bands);
   cudaEvent_t t3 = tm.mark(s);
   MFB_CUDA_TRY(cudaStreamSynchronize(s));
   if (hflags[1] || hflags[3]) {
