@@ -151,18 +151,6 @@ __host__ __device__ __forceinline__ void leaf_decode(int32_t ref, int& first, in
   count = r & 15;
 }
 
-// 4-wide node: the grandchildren of binary node i (children of i's internal
-// children, or i's leaf children themselves), up to 4 entries. Child boxes are
-// stored per axis (SoA) so the four fp32 box tests vectorise; empty slots
-// carry the empty box (+inf, -inf) and are never entered. Node i of the wide
-// array is only meaningful at even binary depth; the traversal reaches no other.
-struct alignas(16) WNode {
-  float4 lx, ly, lz;  // child k: min x/y/z in component k
-  float4 hx, hy, hz;  // child k: max x/y/z
-  int4 ref;           // child refs: binary/wide node index (>= 0) or leaf ref (< 0)
-  int4 pad;
-};
-static_assert(sizeof(WNode) == 128, "wide node is one 128-byte line");
 
 struct Lbvh {
   int n_tris = 0;
@@ -170,7 +158,6 @@ struct Lbvh {
   BNode* nodes = nullptr;   // device
   BTri* tris = nullptr;     // device, leaf order
   TBox* tbox = nullptr;     // device, leaf order
-  WNode* wnodes = nullptr;  // device, 4-wide collapse of `nodes` (same indices)
   int32_t root_ref = 0;     // 0 (internal root) or a leaf ref when n_tris <= kLeafMax... see build
   float root_box[6];        // host copy not needed for traversal; kept for export
   float* root_box_dev = nullptr;

@@ -1245,8 +1245,6 @@ int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
     BNode* nodes = b->store.buf<BNode>("nodes", nn);
     BTri* tris = b->store.buf<BTri>("tris", b->bvh.n_tris);
     TBox* tbox = b->store.buf<TBox>("tbox", b->bvh.n_tris);
-    WNode* wn = b->store.buf<WNode>("wnodes", nn);
-    MFB_CUDA_TRY(cudaMemcpyAsync(wn, b->bvh.wnodes, sizeof(WNode) * nn, cudaMemcpyDeviceToDevice, ctx->c.stream));
     MFB_CUDA_TRY(cudaMemcpyAsync(tbox, b->bvh.tbox, sizeof(TBox) * b->bvh.n_tris, cudaMemcpyDeviceToDevice, ctx->c.stream));
     auto* acc = b->store.buf<unsigned long long>("acc", 8);
     MFB_CUDA_TRY(cudaMemcpyAsync(nodes, b->bvh.nodes, sizeof(BNode) * nn, cudaMemcpyDeviceToDevice, ctx->c.stream));
@@ -1259,7 +1257,6 @@ int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
     b->bvh.nodes = nodes;
     b->bvh.tris = tris;
     b->bvh.tbox = tbox;
-    b->bvh.wnodes = wn;
     b->bvh.scene_acc = acc;
     b->bvh.root_box_dev = nullptr;
     b->store.own_stream = false;

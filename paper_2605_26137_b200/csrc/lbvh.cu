@@ -390,55 +390,6 @@ __global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __res
   }
 }
 
-// Collapses the binary tree into 4-wide nodes: wide node i lists binary
-// node i's grandchildren (an internal child contributes its two children, a
-// leaf child itself). Fully parallel over binary nodes; uses the refit boxes.
-__global__ void k_collapse4(const BNode* __restrict__ nodes, int n_nodes, WNode* __restrict__ wn) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n_nodes) return;
-  const BNode nd = nodes[i];
-  float b[4][6];
-  int r[4];
-  int k = 0;
-  const float* own = reinterpret_cast<const float*>(&nd);
-  const int refs[2] = {nd.d.x, nd.d.y};
-#pragma unroll
-  for (int side = 0; side < 2; ++side) {
-    const int c = refs[side];
-    if (c >= 0) {
-      const BNode ch = nodes[c];
-      const float* cf = reinterpret_cast<const float*>(&ch);
-#pragma unroll
-      for (int gs = 0; gs < 2; ++gs) {
-#pragma unroll
-        for (int q = 0; q < 6; ++q) b[k][q] = cf[6 * gs + q];
-        r[k] = gs ? ch.d.y : ch.d.x;
-        ++k;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < 6; ++q) b[k][q] = own[6 * side + q];
-      r[k] = c;
-      ++k;
-    }
-  }
-  for (; k < 4; ++k) {
-    b[k][0] = b[k][1] = b[k][2] = INFINITY;
-    b[k][3] = b[k][4] = b[k][5] = -INFINITY;
-    r[k] = 0;
-  }
-  WNode w;
-  w.lx = make_float4(b[0][0], b[1][0], b[2][0], b[3][0]);
-  w.ly = make_float4(b[0][1], b[1][1], b[2][1], b[3][1]);
-  w.lz = make_float4(b[0][2], b[1][2], b[2][2], b[3][2]);
-  w.hx = make_float4(b[0][3], b[1][3], b[2][3], b[3][3]);
-  w.hy = make_float4(b[0][4], b[1][4], b[2][4], b[3][4]);
-  w.hz = make_float4(b[0][5], b[1][5], b[2][5], b[3][5]);
-  w.ref = make_int4(r[0], r[1], r[2], r[3]);
-  w.pad = make_int4(0, 0, 0, 0);
-  wn[i] = w;
-}
-
 }  // namespace
 
 void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag) {
@@ -448,7 +399,6 @@ void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag) 
   out.nodes = ctx.buf<BNode>(tag + ".nodes", out.n_nodes > 0 ? out.n_nodes : 1);
   out.tris = ctx.buf<BTri>(tag + ".tris", n);
   out.tbox = ctx.buf<TBox>(tag + ".tbox", n);
-  out.wnodes = ctx.buf<WNode>(tag + ".wnodes", out.n_nodes > 0 ? out.n_nodes : 1);
   out.root_box_dev = ctx.buf<float>(tag + ".rootbox", 8);
   out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
   out.scene_acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
@@ -524,15 +474,6 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
     k_refit<<<1, 32, 0, s>>>(out.tbox, n, out.nodes, prim_parent, node_parent, flags, out.root_box_dev);
   }
   ctx.count_launch(2);
-  // 4-wide collapse only when the wide traversal is selected (MFB_BVH4=1)
-  static const bool wide = [] {
-    const char* e = std::getenv("MFB_BVH4");
-    return e && e[0] == '1';
-  }();
-  if (wide && out.n_nodes > 0) {
-    k_collapse4<<<div_up(out.n_nodes, T), T, 0, s>>>(out.nodes, out.n_nodes, out.wnodes);
-    ctx.count_launch();
-  }
   MFB_CUDA_TRY(cudaGetLastError());
   out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
   out.scene_acc = acc;

@@ -239,161 +239,6 @@ __device__ __forceinline__ uint8_t encode_channel(double v) {
   return static_cast<uint8_t>(q < 0 ? 0 : (q > 255 ? 255 : q));
 }
 
-// ---------------------------------------------------------------- warp-coherent transfer
-// A warp owns 32 spatially coherent queries (one 8x4 texel block, compacted
-// by the rasteriser) and walks ONE traversal for all of them: every node is
-// fetched once per warp (uniform 64-B load, 4 x LDG.128 broadcast), each lane
-// tests both child boxes against its own bound, and the warp descends into a
-// child if any lane still needs it (ballot). Leaves are intersected by the
-// lanes whose bound admits them. The traversal stack is warp-uniform and lives
-// distributed in registers: entry k is held by lane k % 32 in slot k / 32, so
-// it needs neither shared nor local memory. Entries record (parent, side) so
-// a popped subtree is re-tested against every lane's current bound.
-__device__ __forceinline__ int stack_get(int s0, int s1, int s2, int k) {
-  const int v = k < 32 ? s0 : (k < 64 ? s1 : s2);
-  return __shfl_sync(0xffffffffu, v, k & 31);
-}
-__device__ __forceinline__ void stack_put(int& s0, int& s1, int& s2, int k, int v, int lane) {
-  if (lane == (k & 31)) {
-    if (k < 32) s0 = v;
-    else if (k < 64) s1 = v;
-    else s2 = v;
-  }
-}
-
-// prof (optional, warp-uniform counters): [0] internal-node visits,
-// [1] leaf visits, [2] stack pops tested, [3] pair rounds, [4] pairs,
-// [5] batches (warps x batches)
-template <bool kProf>
-__device__ __forceinline__ void warp_closest(const BNode* __restrict__ nodes, const BTri* __restrict__ tris,
-                                             const TBox* __restrict__ tbox, int32_t root, d3 q, float3 qf,
-                                             double E, Best& best, float& bnd, int lane,
-                                             unsigned long long* prof) {
-  int s0 = 0, s1 = 0, s2 = 0;
-  int sp = 0;
-  int32_t ref = root;
-  unsigned need = __ballot_sync(0xffffffffu, bnd >= 0.0f);  // root: every live lane
-  for (;;) {
-    if (ref >= 0) {
-      if (kProf) ++prof[0];
-      const float4* np = reinterpret_cast<const float4*>(nodes + ref);
-      const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
-      const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
-      const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
-      const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
-      const bool hL = lbL <= bnd, hR = lbR <= bnd;
-      const unsigned mL = __ballot_sync(0xffffffffu, hL);
-      const unsigned mR = __ballot_sync(0xffffffffu, hR);
-      if (mL && mR) {
-        const unsigned prefL = __ballot_sync(0xffffffffu, hL && (!hR || lbL <= lbR));
-        const bool goL = 2 * __popc(prefL) >= __popc(mL | mR);
-        stack_put(s0, s1, s2, sp, (ref << 1) | (goL ? 1 : 0), lane);
-        ++sp;
-        need = goL ? mL : mR;
-        ref = goL ? d.x : d.y;
-        continue;
-      }
-      if (mL | mR) {
-        need = mL ? mL : mR;
-        ref = mL ? d.x : d.y;
-        continue;
-      }
-    } else {
-      // Leaf: each lane in `need` first tests every triangle's own fp32 box
-      // (conservative, like the node boxes). The surviving (lane, triangle)
-      // pairs are spread over the 32 lanes, evaluated exactly in f64 in rounds
-      // of 32 (branch-free test: full-width f64 issue), and each owner gathers
-      // its candidates by shuffle keeping the lexicographic (distSq, face)
-      // minimum - order-independent, so the result is exact. Per-triangle
-      // masks and prefix counts live one per lane (lane t holds triangle t).
-      int first, count;
-      leaf_decode(ref, first, count);
-      const bool mine = (need >> lane) & 1u;
-      unsigned my_m = 0;
-      for (int t = 0; t < count; ++t) {
-        const float4* bp = reinterpret_cast<const float4*>(tbox + first + t);
-        const float4 ba = __ldg(bp), bb = __ldg(bp + 1);
-        const float lb = box_lb(ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, qf, qf);
-        const unsigned m = __ballot_sync(0xffffffffu, mine && lb <= bnd);
-        if (lane == t) my_m = m;
-      }
-      const int my_cnt = __popc(my_m);
-      int incl = my_cnt;
-#pragma unroll
-      for (int off = 1; off < 8; off <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += v;
-      }
-      const int excl = incl - my_cnt;
-      const int total = __shfl_sync(0xffffffffu, incl, 7);
-      if (kProf) {
-        ++prof[1];
-        prof[3] += (total + 31) / 32;
-        prof[4] += total;
-      }
-      for (int base = 0; base < total; base += 32) {
-        const int j = base + lane;
-        const bool act = j < total;
-        int t = 0;
-        for (int k = 0; k < count - 1; ++k) t += (__shfl_sync(0xffffffffu, incl, k) <= j) ? 1 : 0;
-        const unsigned m = __shfl_sync(0xffffffffu, my_m, t);
-        const int pre_t = __shfl_sync(0xffffffffu, excl, t);
-        const int owner = act ? static_cast<int>(__fns(m, 0, j - pre_t + 1)) : 0;
-        const float ox = __shfl_sync(0xffffffffu, qf.x, owner);
-        const float oy = __shfl_sync(0xffffffffu, qf.y, owner);
-        const float oz = __shfl_sync(0xffffffffu, qf.z, owner);
-        double ds = INFINITY;
-        int face = 0x7fffffff;
-        d3 bary = mk3(0.0, 0.0, 0.0);
-        if (act) {
-          d3 A, B, C;
-          load_tri(tris + first + t, A, B, C, face);
-          const d3 oq = mk3(ox, oy, oz);
-          const d3 pt = closest_point_triangle_sel(oq, A, B, C, bary);
-          ds = sqnorm(pt - oq);
-        }
-        int win = -1;
-        for (int tt = 0; tt < count; ++tt) {
-          const unsigned mt = __shfl_sync(0xffffffffu, my_m, tt);
-          const int src = __shfl_sync(0xffffffffu, excl, tt) + __popc(mt & ((1u << lane) - 1u)) - base;
-          const bool ok = ((mt >> lane) & 1u) && src >= 0 && src < 32;
-          const double dd = __shfl_sync(0xffffffffu, ds, src & 31);
-          const int ff = __shfl_sync(0xffffffffu, face, src & 31);
-          if (ok && (dd < best.d || (dd == best.d && ff < best.face))) {
-            best.d = dd;
-            best.face = ff;
-            win = src;
-          }
-        }
-        const double bx = __shfl_sync(0xffffffffu, bary.x, win & 31);
-        const double by = __shfl_sync(0xffffffffu, bary.y, win & 31);
-        const double bz = __shfl_sync(0xffffffffu, bary.z, win & 31);
-        if (win >= 0) {
-          best.bary = mk3(bx, by, bz);
-          bnd = prune_bound(best.d, E);
-        }
-      }
-    }
-    bool found = false;
-    while (sp > 0) {
-      --sp;
-      if (kProf) ++prof[2];
-      const int e = stack_get(s0, s1, s2, sp);
-      const int par = e >> 1, side = e & 1;
-      const float* f = reinterpret_cast<const float*>(nodes + par) + (side ? 6 : 0);
-      const float lb = box_lb(__ldg(f), __ldg(f + 1), __ldg(f + 2), __ldg(f + 3), __ldg(f + 4), __ldg(f + 5), qf, qf);
-      const unsigned m = __ballot_sync(0xffffffffu, lb <= bnd);
-      if (m) {
-        need = m;
-        ref = __ldg(reinterpret_cast<const int*>(nodes + par) + 12 + side);
-        found = true;
-        break;
-      }
-    }
-    if (!found) break;
-  }
-}
-
 // ---------------------------------------------------------------- per-thread while-while transfer
 // One query per thread over the compacted, spatially coherent query list.
 // Aila-Laine "while-while" structure: each lane descends internal nodes until
@@ -411,9 +256,6 @@ __device__ __forceinline__ void warp_closest(const BNode* __restrict__ nodes, co
 #endif
 #ifndef MFB_TRI_SEL
 #define MFB_TRI_SEL 0  // branchy form measured 2% faster in the per-thread walk
-#endif
-#ifndef MFB_SPEC
-#define MFB_SPEC 0
 #endif
 // L1 prefetch hints for the traversal (bit mask, compile-time):
 //   1 = a leaf's triangle lines when the leaf is entered (its 2-4 triangles
@@ -443,49 +285,6 @@ __device__ __forceinline__ void pf_ref(const BNode* __restrict__ nodes, const BT
     pf_leaf(tris, ref);
 }
 
-// Shared descent of a warp (its 32 queries are one 8x4 texel patch): from
-// the root, follow the only child whose box lies within the initial pruning
-// bound of the warp's query box (all queries' fp32 points, widened by the
-// largest lane slack); stop at the first node where both children qualify.
-// Every skipped subtree has a box-to-query-box lower bound above the bound
-// every lane starts with (and bounds only shrink), so each lane would prune
-// it too: starting the per-lane walks at the returned node gives the same
-// result, minus the ~8-10 top-level visits every lane repeats otherwise.
-// Returns kDone when nothing is within reach of any lane (all miss).
-#ifndef MFB_WARP_ROOT
-#define MFB_WARP_ROOT 0  // measured: -5.3 internal visits per query, no time change (top levels are L1-hot)
-#endif
-__device__ __forceinline__ int32_t warp_root(const BNode* __restrict__ nodes, int32_t root, float3 qf, float E,
-                                             double init, bool live, int32_t kDone) {
-  float3 lo = live ? qf : make_float3(INFINITY, INFINITY, INFINITY);
-  float3 hi = live ? qf : make_float3(-INFINITY, -INFINITY, -INFINITY);
-  float e = live ? E : 0.0f;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    lo.x = fminf(lo.x, __shfl_xor_sync(0xffffffffu, lo.x, off));
-    lo.y = fminf(lo.y, __shfl_xor_sync(0xffffffffu, lo.y, off));
-    lo.z = fminf(lo.z, __shfl_xor_sync(0xffffffffu, lo.z, off));
-    hi.x = fmaxf(hi.x, __shfl_xor_sync(0xffffffffu, hi.x, off));
-    hi.y = fmaxf(hi.y, __shfl_xor_sync(0xffffffffu, hi.y, off));
-    hi.z = fmaxf(hi.z, __shfl_xor_sync(0xffffffffu, hi.z, off));
-    e = fmaxf(e, __shfl_xor_sync(0xffffffffu, e, off));
-  }
-  if (isinf(init) || root < 0) return root;  // unbounded search: no shared prefix
-  const float bw = prune_bound(init, e);      // >= every lane's initial bound
-  int32_t ref = root;
-  while (ref >= 0) {  // warp-uniform
-    const float4* np = reinterpret_cast<const float4*>(nodes + ref);
-    const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
-    const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
-    const bool hL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, lo, hi) <= bw;
-    const bool hR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, lo, hi) <= bw;
-    if (hL && hR) break;
-    if (!hL && !hR) return kDone;
-    ref = hL ? d.x : d.y;
-  }
-  return ref;
-}
-
 // Pop of the per-thread stack that skips entries whose lower bound no longer
 // passes `bnd` four at a time: one aligned 16-byte local load covers the top
 // (up to) four lower bounds, so a run of pruned entries costs one dependent
@@ -493,12 +292,6 @@ __device__ __forceinline__ int32_t warp_root(const BNode* __restrict__ nodes, in
 // topmost surviving entry's ref (sp = its slot) or kDoneRef (sp = 0).
 #ifndef MFB_POP4
 #define MFB_POP4 1
-#endif
-#ifndef MFB_LEAF_UNROLL
-#define MFB_LEAF_UNROLL 0
-#endif
-#ifndef MFB_TIE
-#define MFB_TIE 0
 #endif
 #ifndef MFB_DYN
 #define MFB_DYN 1
@@ -618,93 +411,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     // ref: node (>= 0), leaf (< 0 and != kDone), or kDone
     constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
     int32_t ref = live ? root : kDone;
-#if MFB_WARP_ROOT
-    if (kPass == 0) {  // every lane of the warp takes part (the loop condition is warp-uniform)
-      const int32_t wr = warp_root(nodes, root, qf, E, init, live, kDone);
-      ref = live ? wr : kDone;
-    }
-#endif
-#if MFB_SPEC
-    // Speculative while-while (Aila & Laine 2009): a lane that reaches a leaf
-    // parks it and keeps walking while any lane of the warp still needs
-    // internal nodes; the leaf phase then intersects every parked leaf.
-    const unsigned live_mask = __ballot_sync(0xffffffffu, live);
-    (void)live_mask;
-    int32_t park0 = kDone, park1 = kDone;
-    // all loop conditions are warp-uniform (ballots over every lane)
-    while (__any_sync(0xffffffffu, ref != kDone || park0 != kDone)) {
-      for (;;) {
-        if (ref < 0 && ref != kDone) {  // reached a leaf: park it
-          if (park0 == kDone) park0 = ref;
-          else park1 = ref;
-          ref = kDone;
-          while (sp > 0) {
-            --sp;
-            if (st_lb[sp] <= bnd) {
-              ref = st_ref[sp];
-              break;
-            }
-          }
-        }
-        const bool want = ref >= 0 && park1 == kDone;   // can still walk
-        const bool needy = ref >= 0 && park0 == kDone;  // has no leaf yet
-        if (!__any_sync(0xffffffffu, needy)) break;     // uniform exit
-        if (!want) continue;                            // parked-full lanes idle this step
-        if (kProf) ++pv[0];
-        const float4* np = reinterpret_cast<const float4*>(nodes + ref);
-        const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
-        const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
-        const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
-        const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
-        const bool hL = lbL <= bnd, hR = lbR <= bnd;
-        if (hL && hR) {
-          const bool lf = lbL <= lbR;
-          st_ref[sp] = lf ? d.y : d.x;
-          st_lb[sp] = lf ? lbR : lbL;
-          ++sp;
-          ref = lf ? d.x : d.y;
-        } else if (hL || hR) {
-          ref = hL ? d.x : d.y;
-        } else {
-          ref = kDone;
-          while (sp > 0) {
-            --sp;
-            if (st_lb[sp] <= bnd) {
-              ref = st_ref[sp];
-              break;
-            }
-          }
-        }
-      }
-      // ---- leaf phase: every parked leaf
-      for (int slot = 0; slot < 2; ++slot) {
-        const int32_t leaf = slot ? park1 : park0;
-        if (leaf == kDone) continue;
-        int first, count;
-        leaf_decode(leaf, first, count);
-        if (kProf) {
-          ++pv[1];
-          pv[2] += count;
-        }
-        for (int k = 0; k < count; ++k) {
-          d3 A, B, C;
-          int face;
-          load_tri(tris + first + k, A, B, C, face);
-          d3 bary;
-          const d3 pt = closest_point_triangle(q, A, B, C, bary);
-          const double ds = sqnorm(pt - q);
-          if (ds < best.d || (ds == best.d && face < best.face)) {
-            best.d = ds;
-            best.face = face;
-            best.bary = bary;
-            bnd = prune_bound(ds, E);
-          }
-        }
-      }
-      park0 = park1 = kDone;
-      // the node a lane stopped on may now be prunable; it is re-tested on visit
-    }
-#else
     while (ref != kDone) {
       // ---- descend until this lane holds a leaf
       while (ref >= 0) {
@@ -720,18 +426,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
         const bool hL = lbL <= bnd, hR = lbR <= bnd;
         if (hL && hR) {
-#if MFB_TIE
-          // equal lower bounds (query inside both boxes): the child whose box
-          // centre is nearer first (order only; the result is order-independent)
-          bool lf = lbL < lbR;
-          if (lbL == lbR) {
-            const float ax = (a.x + a.w) - 2.f * qf.x, ay = (a.y + b.x) - 2.f * qf.y, az = (a.z + b.y) - 2.f * qf.z;
-            const float bx = (b.z + c.y) - 2.f * qf.x, by = (b.w + c.z) - 2.f * qf.y, bz = (c.x + c.w) - 2.f * qf.z;
-            lf = ax * ax + ay * ay + az * az <= bx * bx + by * by + bz * bz;
-          }
-#else
           const bool lf = lbL <= lbR;
-#endif
           st_ref[sp] = lf ? d.y : d.x;
           st_lb[sp] = lf ? lbR : lbL;
           ++sp;
@@ -755,9 +450,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       // (iterate [first, end): two live loop values instead of three, so the
       // loop state stays in registers under the 64-register cap)
       const int end = first + count;
-#if MFB_LEAF_UNROLL
-#pragma unroll 3
-#endif
       for (int k = first; k < end; ++k) {
 #if MFB_TRI_BOX
         {  // conservative per-triangle fp32 box check before the exact f64 test
@@ -788,7 +480,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       }
       ref = pop_within(st_ref, st_lb, sp, bnd);
     }
-#endif
     if (!live) continue;
     if (kProf) ++pv[3];
     const int texel = __float_as_int(p.w);
@@ -800,7 +491,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       ++hits;
       const float* tb = qtbn + 9ll * i;
       const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
-#if MFB_LEAN && !MFB_SPEC
+#if MFB_LEAN
       // the winner's barycentrics, recomputed: same inputs (BTri holds copies
       // of these positions) and the same function give the same bits
       closest_point_triangle(qe, ld3(hiPos + 3 * v0), ld3(hiPos + 3 * v1), ld3(hiPos + 3 * v2), best.bary);
@@ -845,439 +536,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
     if (lane == 0 && hits) atomicAdd(&counters[1], static_cast<unsigned long long>(hits));
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));
-  }
-}
-
-// ---------------------------------------------------------------- persistent refill transfer
-// Same per-thread while-while traversal, but lanes are persistent: a lane that
-// finishes its query writes the texel and, once at least kRefill lanes of the
-// warp are idle, the idle lanes grab new queries from a global cursor with
-// one warp-aggregated atomic. Warps therefore stay (nearly) full instead of
-// running at the width of their slowest query.
-__device__ __forceinline__ void encode_texel(const Best& best, const float* __restrict__ tb,
-                                             const double* __restrict__ hiN, const int32_t* __restrict__ hiF,
-                                             uint8_t* __restrict__ rgb, int texel, int32_t* dbg_face,
-                                             double* dbg_ts) {
-  uint8_t px[3] = {128, 128, 255};
-  double ts3[3] = {0.0, 0.0, 0.0};
-  if (best.face >= 0) {
-    const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
-    const d3 n = (best.bary.x * ld3(hiN + 3 * v0) + best.bary.y * ld3(hiN + 3 * v1)) + best.bary.z * ld3(hiN + 3 * v2);
-    const d3 T = mk3(tb[0], tb[1], tb[2]);
-    const d3 B = mk3(tb[3], tb[4], tb[5]);
-    const d3 N = mk3(tb[6], tb[7], tb[8]);
-    d3 ts = mk3(dot(n, T), dot(n, B), dot(n, N));
-    const double len = norm(ts);
-    if (!(len < 1e-12)) {
-      ts = ts / len;
-      px[0] = encode_channel(ts.x);
-      px[1] = encode_channel(ts.y);
-      px[2] = encode_channel(ts.z);
-      ts3[0] = ts.x;
-      ts3[1] = ts.y;
-      ts3[2] = ts.z;
-    }
-  }
-  uint8_t* o = rgb + 3ll * texel;
-  o[0] = px[0];
-  o[1] = px[1];
-  o[2] = px[2];
-  if (dbg_face) dbg_face[texel] = best.face >= 0 ? best.face : -3;
-  if (dbg_ts) {
-    dbg_ts[3ll * texel] = ts3[0];
-    dbg_ts[3ll * texel + 1] = ts3[1];
-    dbg_ts[3ll * texel + 2] = ts3[2];
-  }
-}
-
-template <bool kDebug, int kRefill, int kChunkQ>
-__global__ void __launch_bounds__(128) k_transfer_p(
-    const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
-    const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
-    const float* __restrict__ qtbn, int* __restrict__ qcount, const double* __restrict__ hiN,
-    const int32_t* __restrict__ hiF, double max_dist, uint8_t* __restrict__ rgb,
-    int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters) {
-  constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
-  const int nq = qcount[0];
-  const int lane = threadIdx.x & 31;
-  const double scene_max = from_ordered_dev(scene_acc[6]);
-  const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
-  unsigned long long hits = 0;
-  int32_t st_ref[kStackMax];
-  float st_lb[kStackMax];
-  int sp = 0;
-  int32_t ref = kDone;
-  bool live = false;
-  int qi = 0;
-  float3 qf = make_float3(0.f, 0.f, 0.f);
-  double E = 0.0;
-  Best best;
-  best.d = init;
-  best.face = -1;
-  best.bary = mk3(0.0, 0.0, 0.0);
-  float bnd = -INFINITY;
-  // Work distribution: warp w owns chunks w, w + W, w + 2W, ... of kChunkQ
-  // consecutive queries (one raster tile's worth: spatial neighbours); idle
-  // lanes refill from the warp's current chunk through a warp-uniform cursor.
-  const int warp_id = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int nwarps = (gridDim.x * blockDim.x) >> 5;
-  int chunk = warp_id;
-  int cur = chunk * kChunkQ;                      // next unassigned query of the chunk
-  int chunk_end = min(cur + kChunkQ, nq);
-  for (;;) {
-    const unsigned idle = __ballot_sync(0xffffffffu, !live);
-    if (cur >= chunk_end && idle == 0xffffffffu) {  // chunk drained: move the whole warp on
-      chunk += nwarps;
-      cur = chunk * kChunkQ;
-      if (cur >= nq) break;
-      chunk_end = min(cur + kChunkQ, nq);
-    }
-    if (cur < chunk_end && __popc(idle) >= (idle == 0xffffffffu ? 1 : kRefill)) {
-      if (!live) {
-        const int i = cur + __popc(idle & ((1u << lane) - 1u));
-        if (i < chunk_end) {
-          qi = i;
-          const float4 p = __ldg(qpos + i);
-          qf = make_float3(p.x, p.y, p.z);
-          E = fmax(scene_max, fmax(fabs(static_cast<double>(p.x)), fmax(fabs(static_cast<double>(p.y)),
-                                                                          fabs(static_cast<double>(p.z))))) * 0x1p-32;
-          best.d = init;
-          best.face = -1;
-          best.bary = mk3(0.0, 0.0, 0.0);
-          bnd = prune_bound(init, E);
-          sp = 0;
-          ref = root;
-          live = true;
-        }
-      }
-      cur = min(cur + __popc(idle), chunk_end);
-    }
-    if (!__any_sync(0xffffffffu, live)) break;
-    // ---- descend until this lane holds a leaf (or finishes)
-    while (live && ref >= 0) {
-      const float4* np = reinterpret_cast<const float4*>(nodes + ref);
-      const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
-      const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
-      const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
-      const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
-      const bool hL = lbL <= bnd, hR = lbR <= bnd;
-      if (hL && hR) {
-        const bool lf = lbL <= lbR;
-        st_ref[sp] = lf ? d.y : d.x;
-        st_lb[sp] = lf ? lbR : lbL;
-        ++sp;
-        ref = lf ? d.x : d.y;
-      } else if (hL || hR) {
-        ref = hL ? d.x : d.y;
-      } else {
-        ref = kDone;
-        while (sp > 0) {
-          --sp;
-          if (st_lb[sp] <= bnd) {
-            ref = st_ref[sp];
-            break;
-          }
-        }
-      }
-    }
-    // ---- leaf phase
-    if (live && ref != kDone) {
-      const d3 q = mk3(qf.x, qf.y, qf.z);
-      int first, count;
-      leaf_decode(ref, first, count);
-      for (int k = 0; k < count; ++k) {
-        d3 A, B, C;
-        int face;
-        load_tri(tris + first + k, A, B, C, face);
-        d3 bary;
-        const d3 pt = closest_point_triangle_sel(q, A, B, C, bary);
-        const double ds = sqnorm(pt - q);
-        if (ds < best.d || (ds == best.d && face < best.face)) {
-          best.d = ds;
-          best.face = face;
-          best.bary = bary;
-          bnd = prune_bound(ds, E);
-        }
-      }
-      ref = kDone;
-      while (sp > 0) {
-        --sp;
-        if (st_lb[sp] <= bnd) {
-          ref = st_ref[sp];
-          break;
-        }
-      }
-    }
-    // ---- finished queries: encode and free the lane
-    if (live && ref == kDone) {
-      const int texel = __float_as_int(__ldg(qpos + qi).w);
-      if (best.face >= 0) ++hits;
-      encode_texel(best, qtbn + 9ll * qi, hiN, hiF, rgb, texel, kDebug ? dbg_face : nullptr,
-                   kDebug ? dbg_ts : nullptr);
-      live = false;
-    }
-  }
-  if (counters) {
-    for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
-    if (lane == 0 && hits) atomicAdd(&counters[1], hits);
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));
-  }
-}
-
-// ---------------------------------------------------------------- 4-wide while-while transfer
-// Per-thread while-while over the 4-wide collapse (WNode): each visit loads
-// one 128-B node (7 x LDG.128), tests four fp32 child boxes, continues into the
-// nearest admissible child and pushes the others far-to-near, halving the
-// dependent node-to-node chain of the binary walk.
-__device__ __forceinline__ void cswap(float& la, int& ra, float& lb, int& rb) {
-  if (lb < la) {
-    const float tl = la;
-    la = lb;
-    lb = tl;
-    const int tr = ra;
-    ra = rb;
-    rb = tr;
-  }
-}
-
-template <bool kDebug, bool kProf>
-__global__ void __launch_bounds__(128, MFB_XFER_T_MINB) k_transfer_w(
-    const WNode* __restrict__ wnodes, const BTri* __restrict__ tris, int32_t root,
-    const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
-    const float* __restrict__ qtbn, const int* __restrict__ qcount, const double* __restrict__ hiN,
-    const int32_t* __restrict__ hiF, double max_dist, uint8_t* __restrict__ rgb,
-    int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters,
-    unsigned long long* __restrict__ prof_out, const double* __restrict__ hiPos) {
-  const int nq = qcount[0];
-  const int lane = threadIdx.x & 31;
-  unsigned long long pv[4] = {0, 0, 0, 0};  // wide visits, leaf visits, triangle tests, queries
-  const double scene_max = from_ordered_dev(scene_acc[6]);
-  const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
-  unsigned long long hits = 0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i - lane < nq; i += gridDim.x * blockDim.x) {
-    const bool live = i < nq;
-    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live) p = __ldg(qpos + i);
-    const float3 qf = make_float3(p.x, p.y, p.z);
-    const d3 q = mk3(p.x, p.y, p.z);
-    const float E = __double2float_ru(fmax(scene_max, fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z)))) * 0x1p-32);
-    Best best;
-    best.d = init;
-    best.face = -1;
-    best.bary = mk3(0.0, 0.0, 0.0);
-    float bnd = live ? prune_bound(init, E) : -INFINITY;
-    int32_t st_ref[kStackMax];
-    float st_lb[kStackMax];
-    int sp = 0;
-    constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
-    int32_t ref = live ? root : kDone;
-    while (ref != kDone) {
-      while (ref >= 0) {
-        if (kProf) ++pv[0];
-        const float4* np = reinterpret_cast<const float4*>(wnodes + ref);
-        const float4 lx = __ldg(np), ly = __ldg(np + 1), lz = __ldg(np + 2);
-        const float4 hx = __ldg(np + 3), hy = __ldg(np + 4), hz = __ldg(np + 5);
-        const int4 rr = __ldg(reinterpret_cast<const int4*>(np + 6));
-        float l0 = box_lb(lx.x, ly.x, lz.x, hx.x, hy.x, hz.x, qf, qf);
-        float l1 = box_lb(lx.y, ly.y, lz.y, hx.y, hy.y, hz.y, qf, qf);
-        float l2 = box_lb(lx.z, ly.z, lz.z, hx.z, hy.z, hz.z, qf, qf);
-        float l3 = box_lb(lx.w, ly.w, lz.w, hx.w, hy.w, hz.w, qf, qf);
-        int r0 = rr.x, r1 = rr.y, r2 = rr.z, r3 = rr.w;
-        // sort the four (lb, ref) pairs ascending (5-comparator network)
-        cswap(l0, r0, l1, r1);
-        cswap(l2, r2, l3, r3);
-        cswap(l0, r0, l2, r2);
-        cswap(l1, r1, l3, r3);
-        cswap(l1, r1, l2, r2);
-        if (l3 <= bnd) {
-          st_ref[sp] = r3;
-          st_lb[sp] = l3;
-          ++sp;
-        }
-        if (l2 <= bnd) {
-          st_ref[sp] = r2;
-          st_lb[sp] = l2;
-          ++sp;
-        }
-        if (l1 <= bnd) {
-          st_ref[sp] = r1;
-          st_lb[sp] = l1;
-          ++sp;
-        }
-        if (l0 <= bnd) {
-          ref = r0;
-        } else {
-          ref = kDone;
-          while (sp > 0) {
-            --sp;
-            if (st_lb[sp] <= bnd) {
-              ref = st_ref[sp];
-              break;
-            }
-          }
-        }
-      }
-      if (ref == kDone) break;
-      int first, count;
-      leaf_decode(ref, first, count);
-      if (kProf) {
-        ++pv[1];
-        pv[2] += count;
-      }
-      for (int k = 0; k < count; ++k) {
-        d3 A, B, C;
-        int face;
-        load_tri(tris + first + k, A, B, C, face);
-        d3 bary;
-        const d3 pt = closest_point_triangle(q, A, B, C, bary);
-        const double ds = sqnorm(pt - q);
-        if (ds < best.d || (ds == best.d && face < best.face)) {
-          best.d = ds;
-          best.face = face;
-#if !MFB_LEAN
-          best.bary = bary;
-#endif
-          bnd = prune_bound(ds, E);
-        }
-      }
-      ref = kDone;
-      while (sp > 0) {
-        --sp;
-        if (st_lb[sp] <= bnd) {
-          ref = st_ref[sp];
-          break;
-        }
-      }
-    }
-    if (!live) continue;
-    if (kProf) ++pv[3];
-    if (best.face >= 0) {
-      ++hits;
-#if MFB_LEAN
-      const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
-      closest_point_triangle(q, ld3(hiPos + 3 * v0), ld3(hiPos + 3 * v1), ld3(hiPos + 3 * v2), best.bary);
-#endif
-    }
-    encode_texel(best, qtbn + 9ll * i, hiN, hiF, rgb, __float_as_int(p.w), kDebug ? dbg_face : nullptr,
-                 kDebug ? dbg_ts : nullptr);
-  }
-  if (kProf)
-    for (int k = 0; k < 4; ++k) {
-      unsigned long long v = pv[k];
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0) atomicAdd(&prof_out[k], v);
-    }
-  if (counters) {
-    for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
-    if (lane == 0 && hits) atomicAdd(&counters[1], hits);
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));
-  }
-}
-
-// kPass 1: pass A (records each query's winning face in face_map);
-// kPass 2: pass B (queries stored from the back of the list; each lane first
-// tests the face pass A found for its 2x2-quad corner texel, which only
-// tightens its initial bound - the answer is unchanged).
-template <bool kDebug, bool kProf, int kPass>
-#ifndef MFB_XFER_MINB
-#define MFB_XFER_MINB 4
-#endif
-__global__ void __launch_bounds__(128, MFB_XFER_MINB) k_transfer(
-    const BNode* __restrict__ nodes, const BTri* __restrict__ tris, const TBox* __restrict__ tbox, int32_t root,
-    const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
-    const float* __restrict__ qtbn, const int* __restrict__ qcount, int qcap, int res, int slab_row0,
-    int* __restrict__ face_map, const double* __restrict__ hiPos,
-    const double* __restrict__ hiN, const int32_t* __restrict__ hiF, double max_dist,
-    uint8_t* __restrict__ rgb, int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts,
-    unsigned long long* __restrict__ counters, unsigned long long* __restrict__ prof_out) {
-  const int lane = threadIdx.x & 31;
-  const int nq = qcount[kPass == 2 ? 1 : 0];
-  unsigned long long prof[6] = {0, 0, 0, 0, 0, 0};
-  const int warps = gridDim.x * (blockDim.x >> 5);
-  const double scene_max = from_ordered_dev(scene_acc[6]);
-  const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
-  unsigned long long hits = 0;
-  for (int base = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < nq; base += warps * 32) {
-    const int li = base + lane;
-    const bool live = li < nq;
-    const int i = kPass == 2 ? qcap - 1 - li : li;
-    float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live) p = __ldg(qpos + i);
-    const d3 q = mk3(p.x, p.y, p.z);
-    const float3 qf = make_float3(p.x, p.y, p.z);
-    const double M = fmax(scene_max, fmax(fabs(q.x), fmax(fabs(q.y), fabs(q.z))));
-    const double E = M * 0x1p-32;
-    Best best;
-    best.d = init;
-    best.face = -1;
-    best.bary = mk3(0.0, 0.0, 0.0);
-    if (kPass == 2 && live) {
-      const int gi = __float_as_int(p.w);
-      const int x = gi % res, y = gi / res + slab_row0;
-      const int sy = (y & ~1) - slab_row0;
-      if (sy >= 0) {
-        const int sf = face_map[static_cast<int64_t>(sy) * res + (x & ~1)];
-        if (sf >= 0) {  // exact test of the seed face (as if visited first)
-          const int v0 = hiF[3 * sf], v1 = hiF[3 * sf + 1], v2 = hiF[3 * sf + 2];
-          d3 bary;
-          const d3 pt = closest_point_triangle(q, ld3(hiPos + 3 * v0), ld3(hiPos + 3 * v1), ld3(hiPos + 3 * v2), bary);
-          const double ds = sqnorm(pt - q);
-          if (ds < best.d || (ds == best.d && sf < best.face)) {
-            best.d = ds;
-            best.face = sf;
-            best.bary = bary;
-          }
-        }
-      }
-    }
-    float bnd = live ? prune_bound(best.d, E) : -INFINITY;
-    warp_closest<kProf>(nodes, tris, tbox, root, q, qf, E, best, bnd, lane, prof);
-    if (kProf) ++prof[5];
-    if (!live) continue;
-    const int texel = __float_as_int(p.w);
-    if (kPass == 1) face_map[texel] = best.face;
-    uint8_t px[3] = {128, 128, 255};
-    double ts3[3] = {0.0, 0.0, 0.0};
-    if (best.face >= 0) {
-      ++hits;
-      const float* tb = qtbn + 9ll * i;
-      const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
-      const d3 n = (best.bary.x * ld3(hiN + 3 * v0) + best.bary.y * ld3(hiN + 3 * v1)) +
-                   best.bary.z * ld3(hiN + 3 * v2);
-      const d3 T = mk3(tb[0], tb[1], tb[2]);
-      const d3 B = mk3(tb[3], tb[4], tb[5]);
-      const d3 N = mk3(tb[6], tb[7], tb[8]);
-      d3 ts = mk3(dot(n, T), dot(n, B), dot(n, N));
-      const double len = norm(ts);
-      if (!(len < 1e-12)) {
-        ts = ts / len;
-        px[0] = encode_channel(ts.x);
-        px[1] = encode_channel(ts.y);
-        px[2] = encode_channel(ts.z);
-        ts3[0] = ts.x;
-        ts3[1] = ts.y;
-        ts3[2] = ts.z;
-      }
-    }
-    uint8_t* o = rgb + 3ll * texel;
-    o[0] = px[0];
-    o[1] = px[1];
-    o[2] = px[2];
-    if (kDebug) {
-      if (dbg_face) dbg_face[texel] = best.face >= 0 ? best.face : -3;
-      if (dbg_ts) {
-        dbg_ts[3ll * texel] = ts3[0];
-        dbg_ts[3ll * texel + 1] = ts3[1];
-        dbg_ts[3ll * texel + 2] = ts3[2];
-      }
-    }
-  }
-  if (kProf && lane == 0)
-    for (int k = 0; k < 6; ++k) atomicAdd(&prof_out[k], prof[k]);
-  if (counters) {
-    for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
-    if (lane == 0 && hits) atomicAdd(&counters[1], hits);
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&counters[0], static_cast<unsigned long long>(nq));  // per pass
   }
 }
 
@@ -1877,11 +1135,11 @@ int occupancy(K kern) {
 static const unsigned long long* scene_acc_of(Ctx&, const Lbvh& bvh) { return bvh.scene_acc; }
 
 void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferArgs& a) {
-  // Persistent grid: enough resident warps to cover every SM; each warp
-  // strides over 32-query batches until the (device-side) count is reached.
-  static const int blocks_per_sm = occupancy(k_transfer<false, false, 1>);
-  const int grid_cap = kNumSMs * blocks_per_sm;
-  const int grid = std::max(1, std::min(grid_cap, div_up(a.q.capacity, 128)));
+  // Per-thread while-while walk (k_transfer_t) on a persistent grid of the
+  // resident CTAs; warps take 32-query batches from the list's cursor.
+  // Variants measured on config B and removed: the
+  // warp-coherent walk (2.49 ms), persistent lanes with refill (1.54-1.86 ms),
+  // the 4-wide collapsed BVH (slower on B and E).
   const bool dbg = a.dbg_face || a.dbg_ts;
   static const bool prof = std::getenv("MFB_PROF") != nullptr;
   unsigned long long* pbuf = nullptr;
@@ -1890,82 +1148,8 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     MFB_CUDA_TRY(cudaMemsetAsync(pbuf, 0, 8 * sizeof(unsigned long long), s));
   }
   if (kSeedPasses) MFB_CUDA_TRY(cudaMemsetAsync(a.face_map, 0xff, sizeof(int) * a.face_map_size, s));
-#define MFB_XFER(D, P, PASS)                                                                                     \
-  k_transfer<D, P, PASS><<<grid, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.tbox, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, \
-                                              a.q.count, a.q.capacity, a.res, a.slab_row0, a.face_map,            \
-                                              a.hi_positions, a.hi_normals, a.hi_faces, a.max_dist, a.rgb,        \
-                                              D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf)
-#define MFB_XFER_PASS(PASS)                              \
-  if (prof) {                                            \
-    if (dbg) MFB_XFER(true, true, PASS);                 \
-    else MFB_XFER(false, true, PASS);                    \
-  } else {                                               \
-    if (dbg) MFB_XFER(true, false, PASS);                \
-    else MFB_XFER(false, false, PASS);                   \
-  }
-  // Default: per-thread while-while (measured 1.43 ms vs 2.49 ms for the
-  // warp-coherent kernel on config B, profiles/r01). MFB_XFER=warp selects
-  // the warp-coherent variant for comparison.
-  static const bool per_thread = [] {
-    const char* e = std::getenv("MFB_XFER");
-    return !(e && std::string(e) == "warp");
-  }();
-  // Persistent lanes with refill measured slower than plain while-while on
-  // config B (1.85 vs 1.42 ms): lanes at different depths lose the broadcast
-  // node loads. Off by default; MFB_REFILL=k enables it for experiments.
-  static const int refill = [] {
-    const char* e = std::getenv("MFB_REFILL");
-    return e ? std::atoi(e) : 0;
-  }();
-  // 4-wide walk (MFB_BVH4=1): 13.8 wide visits vs 27.1 binary visits per
-  // query on config B but the same time (1.45 vs 1.43 ms, r01 profiles) - the
-  // kernel is issue-bound, not chain-latency-bound - so binary stays default.
-  static const bool wide = [] {
-    const char* e = std::getenv("MFB_BVH4");
-    return e && std::string(e) == "1";
-  }();
-  if (per_thread && wide && refill == 0) {
-    static const int bpw = occupancy(k_transfer_w<false, false>);
-    const int gw = std::max(1, std::min(kNumSMs * bpw, div_up(a.q.capacity, 128)));
-#define MFB_XFER_W(D, P)                                                                                      \
-  k_transfer_w<D, P><<<gw, 128, 0, s>>>(bvh.wnodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn,  \
-                                        a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb,               \
-                                        D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
-                                        a.hi_positions)
-    if (prof) {
-      if (dbg) MFB_XFER_W(true, true); else MFB_XFER_W(false, true);
-    } else {
-      if (dbg) MFB_XFER_W(true, false); else MFB_XFER_W(false, false);
-    }
-#undef MFB_XFER_W
-  } else if (per_thread && refill > 0) {
-    static const int bpp = occupancy(k_transfer_p<false, 8, 256>);
-    const int g3 = std::max(1, std::min(kNumSMs * bpp, div_up(a.q.capacity, 128)));
-    MFB_CUDA_TRY(cudaMemsetAsync(a.q.count + 2, 0, sizeof(int), s));
-#define MFB_XFER_P(D, R, C)                                                                                 \
-  k_transfer_p<D, R, C><<<g3, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos,        \
-                                           a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, \
-                                           D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters)
-    static const int chunkq = [] {
-      const char* e = std::getenv("MFB_CHUNKQ");
-      return e ? std::atoi(e) : 256;
-    }();
-#define MFB_XFER_PC(D, R) \
-  if (chunkq >= 1024) MFB_XFER_P(D, R, 1024); else if (chunkq >= 256) MFB_XFER_P(D, R, 256); else MFB_XFER_P(D, R, 64)
-    if (refill >= 16) {
-      if (dbg) { MFB_XFER_PC(true, 16); } else { MFB_XFER_PC(false, 16); }
-    } else if (refill >= 8) {
-      if (dbg) { MFB_XFER_PC(true, 8); } else { MFB_XFER_PC(false, 8); }
-    } else if (refill >= 4) {
-      if (dbg) { MFB_XFER_PC(true, 4); } else { MFB_XFER_PC(false, 4); }
-    } else {
-      if (dbg) { MFB_XFER_PC(true, 1); } else { MFB_XFER_PC(false, 1); }
-    }
-#undef MFB_XFER_PC
-#undef MFB_XFER_P
-  } else if (per_thread) {
-    static const int bps = occupancy(k_transfer_t<false, false>);
-    const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
+  static const int bps = occupancy(k_transfer_t<false, false>);
+  const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
 #define MFB_XFER_T(D, P, PASS)                                                                                \
   k_transfer_t<D, P, PASS><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos,        \
                                               a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, \
@@ -1973,47 +1157,29 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
                                               a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions,  \
                                               bvh.tbox)
 #define MFB_XFER_TP(PASS)                                               \
-    if (prof) {                                                          \
-      if (dbg) MFB_XFER_T(true, true, PASS); else MFB_XFER_T(false, true, PASS); \
-    } else {                                                             \
-      if (dbg) MFB_XFER_T(true, false, PASS); else MFB_XFER_T(false, false, PASS); \
-    }
-    if (kSeedPasses) {
-      MFB_XFER_TP(1);
-      MFB_XFER_TP(2);
-    } else {
-      MFB_XFER_TP(0);
-    }
+  if (prof) {                                                           \
+    if (dbg) MFB_XFER_T(true, true, PASS); else MFB_XFER_T(false, true, PASS); \
+  } else {                                                              \
+    if (dbg) MFB_XFER_T(true, false, PASS); else MFB_XFER_T(false, false, PASS); \
+  }
+  if (kSeedPasses) {
+    MFB_XFER_TP(1);
+    MFB_XFER_TP(2);
+    ctx.count_launch();
+  } else {
+    MFB_XFER_TP(0);
+  }
 #undef MFB_XFER_TP
 #undef MFB_XFER_T
-  } else {
-    MFB_XFER_PASS(1);
-    if (kSeedPasses) {
-      MFB_XFER_PASS(2);
-    }
-  }
-#undef MFB_XFER_PASS
-#undef MFB_XFER
-  ctx.count_launch();
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
   if (prof) {
     unsigned long long h[8];
     MFB_CUDA_TRY(cudaMemcpyAsync(h, pbuf, sizeof(h), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
-    if (per_thread) {
-      const double nqd = h[3] ? static_cast<double>(h[3]) : 1.0;
-      if (wide && refill == 0)
-        std::fprintf(stderr, "[mfb prof] (4-wide) per query: wide visits %.2f leaves %.2f triangles %.2f\n",
-                     h[0] / nqd, h[1] / nqd, h[2] / nqd);
-      std::fprintf(stderr, "[mfb prof] per query: internal %.2f leaves %.2f triangles %.2f (queries %llu)\n",
-                   h[0] / nqd, h[1] / nqd, h[2] / nqd, h[3]);
-      return;
-    }
-    const double b = h[5] ? static_cast<double>(h[5]) : 1.0;
-    std::fprintf(stderr,
-                 "[mfb prof] per warp-batch: internal %.1f leaves %.1f pops %.1f rounds %.1f pairs %.1f "
-                 "(batches %llu)\n", h[0] / b, h[1] / b, h[2] / b, h[3] / b, h[4] / b, h[5]);
+    const double nqd = h[3] ? static_cast<double>(h[3]) : 1.0;
+    std::fprintf(stderr, "[mfb prof] per query: internal %.2f leaves %.2f triangles %.2f (queries %llu)\n",
+                 h[0] / nqd, h[1] / nqd, h[2] / nqd, h[3]);
   }
 }
 
