@@ -35,6 +35,9 @@ struct Ctx {
   cudaStream_t side2 = nullptr;     // LBVH helper: triangle repack alongside the hierarchy emission
   cudaStream_t aux2 = nullptr;      // lowpoly reliability pass alongside the raster setup and binning
   cudaEvent_t setup_done = nullptr, join4 = nullptr;
+  cudaStream_t lowhi = nullptr;     // the bake's lowpoly branch, high priority (the main stream is the caller's)
+  cudaStream_t dn = nullptr;        // dense vertex normals (needed only by the transfer's encode), low priority
+  cudaEvent_t lowfork = nullptr, lowjoin = nullptr;
   cudaEvent_t lfork = nullptr, ljoin = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr, join3 = nullptr;
   cudaEvent_t hi_ready = nullptr;   // host entry point: dense mesh uploaded and validated
@@ -50,8 +53,8 @@ struct Ctx {
   std::unordered_map<std::string, Buf> pinned;
   // CUB temp storage, one slot per stream (main, side, aux, aux2, side2): concurrent
   // branches of the bake must not share it
-  void* cub_tmp[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // main, side, aux, aux2, side2
-  size_t cub_tmp_bytes[5] = {0, 0, 0, 0, 0};
+  void* cub_tmp[7] = {};  // main, side, aux, aux2, side2, lowhi, dn
+  size_t cub_tmp_bytes[7] = {};
   int64_t bin_capacity = 0;         // raster tile-bin capacity hint (grows on overflow)
 
   // Grow-only named device scratch (never shrinks; freed with the context).
