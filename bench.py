@@ -678,7 +678,7 @@ def run_e2e(args, ctx, pair, world, distributed=False):
     for _ in range(2):
         call()
     torch.cuda.synchronize()
-    steps = max(3, min(args.steps, 10))
+    steps = max(10, min(3 * args.steps, 30))
     times = []
     for _ in range(steps):
         s = torch.cuda.Event(enable_timing=True)

@@ -229,7 +229,18 @@ struct RasterFused {
   double* dbg_ts = nullptr;
   unsigned long long* valid_count = nullptr;  // N_v accumulator (optional)
   int2* pend = nullptr;  // split raster: (slab texel, face) per query, interpolated by k_interp
+  // dilation resolved before the transfer (dilate_links): with qslot set, the
+  // split raster marks query texels with bit 1 of the valid byte, records
+  // their list slot in qslot (slab texel -> slot) and resets dep_head[slot]
+  int* qslot = nullptr;
+  int* dep_head = nullptr;
+  // row-band completion (BandSync): queries per band of band_rows slab rows
+  int* band_tot = nullptr;
+  int band_rows = 0;
 };
+// True when raster_gbuffer fills RasterFused::qslot / dep_head (split raster,
+// single-pass query list).
+bool raster_links_supported();
 
 // Tile-binned rasteriser over rows [g.row0, g.row0 + g.rows). Device flags:
 // flags[0] = 1 when a texel is claimed twice (AtlasOverlap); flags[1] = 1
@@ -245,6 +256,23 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
 void gbuffer_queries(Ctx& ctx, cudaStream_t s, const GBufDev& g, const RasterFused& out);
 
 // ---------------------------------------------------------------- queries
+// Row-band completion of the fused bake's atlas, for a download that overlaps
+// the transfer (host-buffer entry point): the raster counts each band's
+// queries (tot), the transfer's warps count finished ones (done); a band's
+// rows are final once it and its neighbours are done (dilation sources lie
+// within radius <= rows rows), and the warp that completes the last of them
+// sets ready[band] = 1, which a copy stream waits on (cuStreamWaitValue32).
+struct BandSync {
+  int* tot = nullptr;    // [nb] queries per band (raster)
+  int* done = nullptr;   // [nb] finished queries per band (transfer)
+  int* nbr = nullptr;    // [nb] completed bands among {b-1, b, b+1}
+  int* ready = nullptr;  // [nb] 1 once band b's rows are final
+  int rows = 0, nb = 0, res = 0;
+};
+constexpr int kMaxBands = 64;
+// Completes bands with no query (one CTA, after the raster).
+void band_init(Ctx& ctx, cudaStream_t s, const BandSync& bs);
+
 struct TransferArgs {
   QueryList q;
   int res = 0;
@@ -259,6 +287,11 @@ struct TransferArgs {
   int32_t* dbg_face = nullptr;
   double* dbg_ts = nullptr;
   unsigned long long* counters = nullptr;  // [queries, hits]
+  // dilation links (dilate_links): the epilogue also stores each query's
+  // colour into every texel of its list dep_head[slot] -> dep_next[texel]
+  const int* dep_head = nullptr;
+  const int* dep_next = nullptr;
+  BandSync bands;  // optional (bands.done != nullptr)
 };
 void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferArgs& a);
 
@@ -309,6 +342,12 @@ void dilate_seams_to(Ctx& ctx, cudaStream_t s, int width, int height, int channe
 // width x height x channels image with the matching valid slab; outputs rows
 // [out_row0, out_row0 + out_rows) (which must lie `radius` rows inside the
 // input slab unless at the image border).
+// Dilation resolved before the transfer over a full res x res atlas (see
+// k_dilate_links): gutter texels whose source is a valid unreliable texel get
+// their colour in `rgb` now, the others are linked to their source query.
+bool dilate_links_supported(int radius);
+void dilate_links(Ctx& ctx, cudaStream_t s, int res, const uint8_t* valid, int radius, const int* qslot,
+                  int* dep_head, int* dep_next, uint8_t* rgb);
 void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
                   const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
                   int radius, uint8_t* map_out, int out_row0, int out_rows);

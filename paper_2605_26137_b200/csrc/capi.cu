@@ -480,6 +480,26 @@ std::vector<char> key_bytes(const T& k) {
   return std::vector<char>(reinterpret_cast<const char*>(&k), reinterpret_cast<const char*>(&k) + sizeof(k));
 }
 
+// cuStreamWaitValue32 (driver API, resolved at run time: the library does
+// not link libcuda). Null when the driver does not provide it.
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<WaitValueFn>(f);
+  }();
+  return fn;
+}
+void stream_wait_value(cudaStream_t s, int* flag) {
+  if (wait_value_fn()(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), 1,
+                      CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+    throw ApiError(MF_ERR_CUDA, "cuStreamWaitValue32 failed");
+}
+
 // The bake's three phases. enqueue_bake() chains them with a fork/join (the
 // captured graph); the host-buffer entry point interleaves its own upload and
 // validation wait between them (bake_host_overlapped).
@@ -500,10 +520,22 @@ struct BakeEnq {
   Lbvh bvh;
   double* hiN = nullptr;
 
+  // Dilation resolved before the transfer (full atlas, one output): the
+  // raster and transfer write straight into rgb_out, the gutter texels are
+  // filled by dilate_links (constant sources) and by the transfer's epilogue
+  // (query sources), and no dilation pass follows the transfer.
+  // MFB_DILATE_LINKS=0 keeps the post-transfer k_dilate_fused (A/B).
+  bool links = false;
+  int* dep_next = nullptr;
+  // host-buffer path: row bands of the atlas downloaded while the transfer
+  // runs (BandSync); set before low()
+  bool band_sync = false;
+  BandSync bs;
+
   BakeEnq(Ctx& cc, const mf_mesh* l, const mf_mesh* h, int rs, double dg, double fr, int rad, int b0, int b1,
-          uint8_t* out, bool dbg, Timer& t, BakeMarks& m)
+          uint8_t* out, bool dbg, Timer& t, BakeMarks& m, const OutSet* pb = nullptr)
       : c(cc), lo(l), hi(h), res(rs), radius(rad), rb(b0), re(b1), diag(dg), frac(fr), rgb_out(out), debug(dbg),
-        tm(t), mk(m) {
+        pub(pb), tm(t), mk(m) {
     s0 = std::max(0, rb - radius);  // raster/transfer slab with the dilation halo
     s1 = std::min(res, re + radius);
     g.res = res;
@@ -513,8 +545,18 @@ struct BakeEnq {
     // flags: [0] AtlasOverlap, [1] bin overflow, [2] bin total, [3] query overflow
     flags = c.buf<int>("bake.flags", 4);
     counters = c.buf<unsigned long long>("bake.counters", 4);
-    fo.rgb = c.buf<uint8_t>("bake.raw", 3 * g.texels());
+    static const bool links_env = [] {
+      const char* e = std::getenv("MFB_DILATE_LINKS");
+      return !(e && e[0] == '0');
+    }();
+    links = links_env && !pub && rb == 0 && re == res && dilate_links_supported(radius) && raster_links_supported();
+    fo.rgb = links ? rgb_out : c.buf<uint8_t>("bake.raw", 3 * g.texels());
     fo.q = query_list(c, g.texels());
+    if (links) {
+      fo.qslot = c.buf<int>("bake.qslot", g.texels());
+      fo.dep_head = c.buf<int>("bake.dephead", g.texels());
+      dep_next = c.buf<int>("bake.depnext", g.texels());
+    }
     fo.valid_count = counters + 2;
     if (debug) {
       fo.dbg_face = c.buf<int32_t>("bake.dface", g.texels());
@@ -535,11 +577,18 @@ struct BakeEnq {
       MFB_CUDA_TRY(cudaEventRecord(c.lowfork, m));
       MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.lowfork, 0));
     }
+    if (band_sync) {
+      MFB_CUDA_TRY(cudaMemsetAsync(bs.tot, 0, 4 * kMaxBands * sizeof(int), s));
+      fo.band_tot = bs.tot;
+      fo.band_rows = bs.rows;
+    }
     mk.e0 = tm.mark(s);
     RasterPlan plan;
     prepare_lowpoly(c, s, lo->m, res, plan);
     mk.e1 = tm.mark(s);
     raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
+    if (links) dilate_links(c, s, res, g.valid, radius, fo.qslot, fo.dep_head, dep_next, rgb_out);
+    if (band_sync) band_init(c, s, bs);
     mk.e2 = tm.mark(s);
     if (s != m) {
       MFB_CUDA_TRY(cudaEventRecord(c.lowjoin, s));
@@ -617,10 +666,67 @@ struct BakeEnq {
     ta.dbg_face = fo.dbg_face;
     ta.dbg_ts = fo.dbg_ts;
     ta.counters = counters;
+    if (links) {
+      ta.dep_head = fo.dep_head;
+      ta.dep_next = dep_next;
+    }
+    cudaStream_t cp = c.aux2 ? c.aux2 : s;
+    if (links && band_sync && host_out && cp != s) {
+      // each band's download waits (on cp) for its ready flag, set by the
+      // transfer's warps; the memset after the transfer releases every wait
+      // regardless (by then every band is final), so no wait outlives it
+      ta.bands = bs;
+      cudaEvent_t ev = c.pool_event(40);
+      MFB_CUDA_TRY(cudaEventRecord(ev, s));
+      transfer_normals(c, s, bvh, ta);
+      mk.e4 = tm.mark(s);
+      MFB_CUDA_TRY(cudaMemsetAsync(bs.ready, 1, bs.nb * sizeof(int), s));
+      mk.e5 = tm.mark(s);
+      MFB_CUDA_TRY(cudaStreamWaitEvent(cp, ev, 0));
+      // MFB_BAND_TRACE=1 (diagnostic): per-band copy start/end vs the transfer start
+      static const bool trace = std::getenv("MFB_BAND_TRACE") != nullptr;
+      cudaEvent_t tev[2 * kMaxBands + 2];
+      if (trace) {
+        for (int k = 0; k < 2 * bs.nb + 2; ++k) MFB_CUDA_TRY(cudaEventCreate(&tev[k]));
+        MFB_CUDA_TRY(cudaEventRecord(tev[2 * bs.nb], cp));
+      }
+      for (int b = 0; b < bs.nb; ++b) {
+        const int r0 = b * bs.rows, r1 = std::min(res, r0 + bs.rows);
+        stream_wait_value(cp, bs.ready + b);
+        if (trace) MFB_CUDA_TRY(cudaEventRecord(tev[2 * b], cp));
+        const int64_t off = 3ll * r0 * res;
+        MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off, 3ll * (r1 - r0) * res, cudaMemcpyDeviceToHost, cp));
+        if (trace) MFB_CUDA_TRY(cudaEventRecord(tev[2 * b + 1], cp));
+      }
+      if (trace) {
+        MFB_CUDA_TRY(cudaEventRecord(tev[2 * bs.nb + 1], s));
+        MFB_CUDA_TRY(cudaDeviceSynchronize());
+        float t;
+        std::fprintf(stderr, "[mfb bands] nb %d rows %d (ms from transfer start):", bs.nb, bs.rows);
+        for (int b = 0; b < bs.nb; ++b) {
+          cudaEventElapsedTime(&t, tev[2 * bs.nb], tev[2 * b]);
+          float t2;
+          cudaEventElapsedTime(&t2, tev[2 * bs.nb], tev[2 * b + 1]);
+          std::fprintf(stderr, " %d:%.3f-%.3f", b, t, t2);
+        }
+        cudaEventElapsedTime(&t, tev[2 * bs.nb], tev[2 * bs.nb + 1]);
+        std::fprintf(stderr, " transfer end %.3f\n", t);
+        for (int k = 0; k < 2 * bs.nb + 2; ++k) cudaEventDestroy(tev[k]);
+      }
+      MFB_CUDA_TRY(cudaEventRecord(c.join4, cp));
+      MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join4, 0));
+      MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+      MFB_CUDA_TRY(
+          cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+      return;
+    }
     transfer_normals(c, s, bvh, ta);
     mk.e4 = tm.mark(s);
-    cudaStream_t cp = c.aux2 ? c.aux2 : s;
-    if (host_out && !pub && bands > 1 && cp != s) {
+    if (links) {  // the atlas is complete
+      mk.e5 = tm.mark(s);
+      if (host_out)
+        MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, 3ll * (re - rb) * res, cudaMemcpyDeviceToHost, s));
+    } else if (host_out && !pub && bands > 1 && cp != s) {
       for (int b = 0; b < bands; ++b) {
         const int r0 = rb + static_cast<int>(static_cast<int64_t>(re - rb) * b / bands);
         const int r1 = rb + static_cast<int>(static_cast<int64_t>(re - rb) * (b + 1) / bands);
@@ -653,8 +759,7 @@ struct BakeEnq {
 void enqueue_bake(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag, double frac, int radius,
                   int rb, int re, uint8_t* rgb_out, bool debug, Timer& tm, BakeMarks& mk, int* hflags_pinned,
                   unsigned long long* hcnt_pinned, const OutSet* pub = nullptr) {
-  BakeEnq q(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, debug, tm, mk);
-  q.pub = pub;
+  BakeEnq q(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, debug, tm, mk, pub);
   // MFB_DIAG_SKIP=bvh|low|normals: DIAGNOSTIC ONLY (critical-path analysis):
   // reuse that phase's buffers from the previous (eager) call instead of
   // recomputing them. Never set in a measured run.
@@ -885,6 +990,23 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   BakeMarks mk;
   Timer tmb(c, 8);
   BakeEnq q(c, &lo, &hi, res, diag, frac, radius, 0, res, drgb, false, tmb, mk);
+  // MFB_E2E_BANDS=0: download the atlas after the transfer instead of in row
+  // bands while it runs (A/B)
+  static const bool band_env = [] {
+    const char* e = std::getenv("MFB_E2E_BANDS");
+    return !(e && e[0] == '0');
+  }();
+  if (q.links && band_env && wait_value_fn() && c.aux2 && host_pinned(rgb_out)) {
+    q.band_sync = true;
+    int* bb = c.buf<int>("bake.bands", 4 * kMaxBands);
+    q.bs.tot = bb;
+    q.bs.done = bb + kMaxBands;
+    q.bs.nbr = bb + 2 * kMaxBands;
+    q.bs.ready = bb + 3 * kMaxBands;
+    q.bs.res = res;
+    q.bs.rows = std::max((div_up(res, 16) + 15) / 16 * 16, (radius + 15) / 16 * 16);
+    q.bs.nb = div_up(res, q.bs.rows);
+  }
   static const bool graphs = [] {
     const char* e = std::getenv("MFB_GRAPH");
     return !(e && e[0] == '0');
@@ -897,7 +1019,8 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   {
     const int64_t k[] = {reinterpret_cast<int64_t>(lo.m.pos), reinterpret_cast<int64_t>(lo.m.faces),
                          reinterpret_cast<int64_t>(lo.m.nrm), reinterpret_cast<int64_t>(lo.m.uvs),
-                         reinterpret_cast<int64_t>(lo.m.fuv), lo.m.nf, lo.m.nv, lo.m.nu, res, c.bin_capacity};
+                         reinterpret_cast<int64_t>(lo.m.fuv), lo.m.nf, lo.m.nv, lo.m.nu, res, c.bin_capacity,
+                         q.band_sync ? 1 : 0, radius};
     run_graphed(c, c.g_low, s, key_bytes(k), use_graphs, [&] { q.low(); });
   }
   if (!early) upload_hi();

@@ -65,17 +65,16 @@ __device__ __forceinline__ void chamfer_step(const int16_t* __restrict__ ox, con
   }
 }
 
-// One 64x16 output tile per 256-thread CTA over a (64+2r) x (16+2r) halo
-// region in shared memory. Tiles whose output texels are all valid, or whose
-// region holds no valid texel, are plain copies. Pass k (1-based) updates only
-// cells at least k steps inside the region: exactly the cells the output
-// depends on, so the region shrinks by one ring per pass.
-__global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int channels,
-                                                      const uint8_t* __restrict__ map_in,
-                                                      const uint8_t* __restrict__ valid, int in_row0,
-                                                      int in_rows, int radius, OutSet outs,
-                                                      int out_row0, int out_rows) {
-  extern __shared__ int16_t sm[];
+// The chamfer state of one 64x16 output tile over its (64+2r) x (16+2r) halo
+// region in shared memory (sm: 4 planes of rw*rh int16). Returns false for
+// tiles whose output texels are all valid, or whose region holds no valid
+// texel (nothing to propagate); otherwise runs the r passes and leaves the
+// final source offsets in *ox / *oy. Pass k (1-based) updates only cells at
+// least k steps inside the region: exactly the cells the output depends on,
+// so the region shrinks by one ring per pass.
+__device__ __forceinline__ bool chamfer_tile(int width, int height, const uint8_t* __restrict__ valid,
+                                             int in_row0, int in_rows, int radius, int out_row0, int out_rows,
+                                             int16_t* sm, const int16_t** ox, const int16_t** oy) {
   const int rw = kTW + 2 * radius, rh = kTH + 2 * radius, cells = rw * rh;
   int16_t* ox0 = sm;
   int16_t* oy0 = sm + cells;
@@ -105,30 +104,49 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
       any_hole |= out_cell && v != 0;
     }
   const bool work = __syncthreads_or(any_valid) && __syncthreads_or(any_hole);
+  if (!work) return false;
   // the region (and so every neighbour read) lies inside the image
   const bool interior = x0 >= 0 && x0 + rw <= width && y0 >= 0 && y0 + rh <= height;
-  if (work) {
-    for (int pass = 1; pass <= radius; ++pass) {
-      for (int cy = pass + warp; cy < rh - pass; cy += nwarps)
-        for (int cx = pass + lane; cx < rw - pass; cx += 32) {
-          const int i = cy * rw + cx;
-          int16_t a, b;
-          if (interior) chamfer_step<false>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
-          else chamfer_step<true>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
-          ox1[i] = a;
-          oy1[i] = b;
-        }
-      __syncthreads();
-      int16_t* t = ox0;
-      ox0 = ox1;
-      ox1 = t;
-      t = oy0;
-      oy0 = oy1;
-      oy1 = t;
-      // (pass k + 1 reads only cells in [k, rw - k) x [k, rh - k), all
-      // written by pass k, so the stale outer ring is never read)
-    }
+  for (int pass = 1; pass <= radius; ++pass) {
+    for (int cy = pass + warp; cy < rh - pass; cy += nwarps)
+      for (int cx = pass + lane; cx < rw - pass; cx += 32) {
+        const int i = cy * rw + cx;
+        int16_t a, b;
+        if (interior) chamfer_step<false>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
+        else chamfer_step<true>(ox0, oy0, rw, cx, cy, x0 + cx, y0 + cy, width, height, a, b);
+        ox1[i] = a;
+        oy1[i] = b;
+      }
+    __syncthreads();
+    int16_t* t = ox0;
+    ox0 = ox1;
+    ox1 = t;
+    t = oy0;
+    oy0 = oy1;
+    oy1 = t;
+    // (pass k + 1 reads only cells in [k, rw - k) x [k, rh - k), all
+    // written by pass k, so the stale outer ring is never read)
   }
+  *ox = ox0;
+  *oy = oy0;
+  return true;
+}
+
+// One 64x16 output tile per 256-thread CTA: the chamfer state in shared
+// memory (chamfer_tile), then every output texel copies the input map at its
+// source; copy-only tiles move 16-byte words.
+__global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int channels,
+                                                      const uint8_t* __restrict__ map_in,
+                                                      const uint8_t* __restrict__ valid, int in_row0,
+                                                      int in_rows, int radius, OutSet outs,
+                                                      int out_row0, int out_rows) {
+  extern __shared__ int16_t sm[];
+  const int rw = kTW + 2 * radius;
+  const int tiles_x = (width + kTW - 1) / kTW;
+  const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+  const int out_end = out_row0 + out_rows;
+  const int16_t *ox0 = nullptr, *oy0 = nullptr;
+  const bool work = chamfer_tile(width, height, valid, in_row0, in_rows, radius, out_row0, out_rows, sm, &ox0, &oy0);
   // copy-only tile, full width, 16-byte aligned rows: 16-byte moves
   const int gx0 = tx * kTW, gy0 = out_row0 + ty * kTH;
   if (!work && gx0 + kTW <= width && gy0 + kTH <= out_end) {
@@ -165,6 +183,44 @@ __global__ void __launch_bounds__(256) k_dilate_fused(int width, int height, int
     const int64_t doff = (static_cast<int64_t>(gy - outs.row0) * width + gx) * channels;
     for (int o = 0; o < outs.n; ++o)
       for (int ch = 0; ch < channels; ++ch) outs.p[o][doff + ch] = src[ch];
+  }
+}
+
+// Dilation resolved before the transfer (fused bake, full atlas): the sources
+// depend only on the valid mask, so each gutter texel (invalid, with a source
+// after r passes) is either given its final colour now - the source is a
+// valid unreliable texel, whose raw colour is the constant (128,128,255) - or
+// linked into its source query's list (dep_head[slot] -> dep_next[texel] ->
+// ...), which the transfer's epilogue walks to store the query's colour into
+// every texel that copies it. Valid texels carry bit 1 in `valid` when they
+// are queries; qslot maps a query texel to its list slot.
+__global__ void __launch_bounds__(256) k_dilate_links(int width, int height, const uint8_t* __restrict__ valid,
+                                                      int radius, const int* __restrict__ qslot,
+                                                      int* __restrict__ dep_head, int* __restrict__ dep_next,
+                                                      uint8_t* __restrict__ rgb) {
+  extern __shared__ int16_t sm[];
+  const int rw = kTW + 2 * radius;
+  const int tiles_x = (width + kTW - 1) / kTW;
+  const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+  const int16_t *ox0 = nullptr, *oy0 = nullptr;
+  if (!chamfer_tile(width, height, valid, 0, height, radius, 0, height, sm, &ox0, &oy0)) return;
+  for (int c = threadIdx.x; c < kTW * kTH; c += blockDim.x) {
+    const int lx = c % kTW, ly = c / kTW;
+    const int gx = tx * kTW + lx, gy = ty * kTH + ly;
+    if (gx >= width || gy >= height) continue;
+    const int rc = (ly + radius) * rw + (lx + radius);
+    const int16_t sx = ox0[rc], sy = oy0[rc];
+    if (sx == kNone || (sx == 0 && sy == 0)) continue;
+    const int64_t t = static_cast<int64_t>(gy) * width + gx;
+    const int64_t src = static_cast<int64_t>(gy + sy) * width + (gx + sx);
+    if (valid[src] & 2) {
+      const int slot = qslot[src];
+      if (slot >= 0) dep_next[t] = atomicExch(&dep_head[slot], static_cast<int>(t));
+    } else {
+      rgb[3 * t] = 128;
+      rgb[3 * t + 1] = 128;
+      rgb[3 * t + 2] = 255;
+    }
   }
 }
 
@@ -229,6 +285,27 @@ __global__ void k_dilate_copy(int width, int channels, const uint8_t* __restrict
 
 }  // namespace
 
+static size_t dilate_smem(int radius) {
+  return static_cast<size_t>(4) * (kTW + 2 * radius) * (kTH + 2 * radius) * sizeof(int16_t);
+}
+
+bool dilate_links_supported(int radius) { return radius > 0 && radius <= 64 && dilate_smem(radius) <= 200 * 1024; }
+
+void dilate_links(Ctx& ctx, cudaStream_t s, int res, const uint8_t* valid, int radius, const int* qslot,
+                  int* dep_head, int* dep_next, uint8_t* rgb) {
+  static std::atomic<unsigned long long> attr_set{0};
+  int dev = 0;
+  MFB_CUDA_TRY(cudaGetDevice(&dev));
+  if (!((attr_set.load(std::memory_order_acquire) >> (dev & 63)) & 1ull)) {
+    MFB_CUDA_TRY(cudaFuncSetAttribute(k_dilate_links, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr_set.fetch_or(1ull << (dev & 63), std::memory_order_acq_rel);
+  }
+  const int tiles = ((res + kTW - 1) / kTW) * ((res + kTH - 1) / kTH);
+  k_dilate_links<<<tiles, 256, dilate_smem(radius), s>>>(res, res, valid, radius, qslot, dep_head, dep_next, rgb);
+  ctx.count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
 void dilate_seams_to(Ctx& ctx, cudaStream_t s, int width, int height, int channels, const uint8_t* map_in,
                      const uint8_t* valid, int in_row0, int in_rows, int radius, const OutSet& outs, int out_row0,
                      int out_rows) {
@@ -242,7 +319,7 @@ void dilate_seams_to(Ctx& ctx, cudaStream_t s, int width, int height, int channe
                                    out_bytes, cudaMemcpyDeviceToDevice, s));
     return;
   }
-  const size_t smem = static_cast<size_t>(4) * (kTW + 2 * radius) * (kTH + 2 * radius) * sizeof(int16_t);
+  const size_t smem = dilate_smem(radius);
   if (radius <= 64 && smem <= 200 * 1024) {
     // the attribute is per device: one bit per device, set once each
     static std::atomic<unsigned long long> attr_set{0};

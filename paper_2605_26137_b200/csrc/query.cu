@@ -331,6 +331,30 @@ __device__ __forceinline__ int32_t pop_within(const int32_t* st_ref, const float
 #endif
 }
 
+// Row-band completion (BandSync, bake.cuh). Band b is complete once all its
+// queries are done; its rows are final once b-1, b, b+1 (those that exist)
+// are complete. The caller has fenced its stores.
+__device__ __forceinline__ void band_complete(const BandSync& bs, int band) {
+  for (int k = max(0, band - 1); k <= min(bs.nb - 1, band + 1); ++k) {
+    const int need = 1 + (k > 0) + (k < bs.nb - 1);
+    if (atomicAdd(&bs.nbr[k], 1) + 1 == need) {
+      __threadfence_system();
+      atomicExch(&bs.ready[k], 1);
+    }
+  }
+}
+__device__ __forceinline__ void band_arrive(const BandSync& bs, int band, int n) {
+  const int old = atomicAdd(&bs.done[band], n);
+  if (old + n == __ldcg(bs.tot + band)) {
+    __threadfence();
+    band_complete(bs, band);
+  }
+}
+__global__ void k_band_init(BandSync bs) {
+  for (int b = threadIdx.x; b < bs.nb; b += blockDim.x)
+    if (bs.tot[b] == 0) band_complete(bs, b);
+}
+
 // Occupancy over registers: the walk is bound by dependent L1/L2 latency
 // (node record -> box test -> child record), so resident warps matter more
 // than the spills a 64-register cap costs. Measured at config B (transfer
@@ -353,7 +377,8 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters,
     unsigned long long* __restrict__ prof_out, int qcap = 0, int res = 0, int slab_row0 = 0,
     int* __restrict__ face_map = nullptr, const double* __restrict__ hiPos = nullptr,
-    const TBox* __restrict__ tbox = nullptr) {
+    const TBox* __restrict__ tbox = nullptr, const int* __restrict__ dep_head = nullptr,
+    const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}) {
   const int nq = qcount[kPass == 2 ? 1 : 0];
   const int lane = threadIdx.x & 31;
   unsigned long long pv[4] = {0, 0, 0, 0};  // internal visits, leaf visits, triangle tests, queries
@@ -480,6 +505,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       }
       ref = pop_within(st_ref, st_lb, sp, bnd);
     }
+    const unsigned live_mask = __ballot_sync(0xffffffffu, live);
     if (!live) continue;
     if (kProf) ++pv[3];
     const int texel = __float_as_int(p.w);
@@ -517,6 +543,20 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     o[0] = px[0];
     o[1] = px[1];
     o[2] = px[2];
+    if (dep_head) {  // dilation: the gutter texels whose source is this texel
+      for (int t = __ldcs(dep_head + i); t >= 0; t = dep_next[t]) {
+        uint8_t* d = rgb + 3ll * t;
+        d[0] = px[0];
+        d[1] = px[1];
+        d[2] = px[2];
+      }
+    }
+    if (bands.done) {  // this batch's texels (and their gutter texels) are written
+      __threadfence();
+      const int band = texel / bands.res / bands.rows;
+      const unsigned grp = __match_any_sync(live_mask, band);
+      if (lane == __ffs(grp) - 1) band_arrive(bands, band, __popc(grp));
+    }
     if (kDebug) {
       if (dbg_face) dbg_face[texel] = best.face >= 0 ? best.face : -3;
       if (dbg_ts) {
@@ -1134,6 +1174,12 @@ int occupancy(K kern) {
 
 static const unsigned long long* scene_acc_of(Ctx&, const Lbvh& bvh) { return bvh.scene_acc; }
 
+void band_init(Ctx& ctx, cudaStream_t s, const BandSync& bs) {
+  k_band_init<<<1, 64, 0, s>>>(bs);
+  ctx.count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
 void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferArgs& a) {
   // Per-thread while-while walk (k_transfer_t) on a persistent grid of the
   // resident CTAs; warps take 32-query batches from the list's cursor.
@@ -1155,7 +1201,7 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
                                               a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, \
                                               D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf, \
                                               a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions,  \
-                                              bvh.tbox)
+                                              bvh.tbox, a.dep_head, a.dep_next, a.bands)
 #define MFB_XFER_TP(PASS)                                               \
   if (prof) {                                                           \
     if (dbg) MFB_XFER_T(true, true, PASS); else MFB_XFER_T(false, true, PASS); \

@@ -506,7 +506,8 @@ __device__ __forceinline__ void tile_texel(int t, int& lx, int& ly) {
 // Block-wide compaction of this thread's query flag: returns the query slot
 // (or -1). One atomicAdd per block on the global counter.
 __device__ __forceinline__ int compact_slot(bool is_q, int* counter, int capacity, int* overflow,
-                                            bool extra = false, unsigned long long* extra_count = nullptr) {
+                                            bool extra = false, unsigned long long* extra_count = nullptr,
+                                            int* band_add = nullptr) {
   __shared__ int warp_base[8];
   __shared__ int warp_extra[8];
   __shared__ int block_base;
@@ -528,6 +529,10 @@ __device__ __forceinline__ int compact_slot(bool is_q, int* counter, int capacit
     }
     block_base = acc ? atomicAdd(counter, acc) : 0;
     if (acc && block_base + acc > capacity) *overflow = 1;
+    if (band_add && acc) {  // slots actually granted to this block
+      const int got = min(acc, capacity - block_base);
+      if (got > 0) atomicAdd(band_add, got);
+    }
     if (extra_count && ex) atomicAdd(extra_count, static_cast<unsigned long long>(ex));
   }
   __syncthreads();
@@ -763,11 +768,19 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
   }
   if (kMode == 2) {
     const bool is_q = in && valid && rel;
-    const int slot = compact_slot(is_q, fo.q.count, fo.q.capacity, &flags[3], in && valid != 0, fo.valid_count);
+    int* band_add = fo.band_tot ? fo.band_tot + (row_begin + ty * kTile - g_row0) / fo.band_rows : nullptr;
+    const int slot = compact_slot(is_q, fo.q.count, fo.q.capacity, &flags[3], in && valid != 0, fo.valid_count,
+                                  band_add);
     if (!in) return;
-    if (gvalid) gvalid[gi] = valid;
+    if (gvalid) gvalid[gi] = fo.qslot && is_q ? 3 : valid;
     if (is_q) {
-      if (slot >= 0) fo.pend[slot] = make_int2(static_cast<int>(gi), cover);
+      if (slot >= 0) {
+        fo.pend[slot] = make_int2(static_cast<int>(gi), cover);
+        if (fo.qslot) {
+          fo.qslot[gi] = slot;
+          fo.dep_head[slot] = -1;
+        }
+      }
       return;
     }
     uint8_t* o = fo.rgb + 3 * gi;
@@ -1016,10 +1029,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
   // Split raster (default): coverage + compaction, then a barrier-free
   // interpolation kernel over the compacted queries. MFB_RASTER_SPLIT=0
   // selects the single fused kernel (A/B).
-  static const bool split = [] {
-    const char* e = std::getenv("MFB_RASTER_SPLIT");
-    return !(e && e[0] == '0') && !kSeedPasses;
-  }();
+  const bool split = raster_links_supported();
   if (fused && split) {
     MFB_CUDA_TRY(cudaMemsetAsync(fused->q.count, 0, 4 * sizeof(int), s));  // [3]: transfer batch cursor
     RasterFused f2 = *fused;
@@ -1038,6 +1048,14 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
   }
   ctx.count_launch(3);
   MFB_CUDA_TRY(cudaGetLastError());
+}
+
+bool raster_links_supported() {
+  static const bool split = [] {
+    const char* e = std::getenv("MFB_RASTER_SPLIT");
+    return !(e && e[0] == '0') && !kSeedPasses;
+  }();
+  return split;
 }
 
 void gbuffer_queries(Ctx& ctx, cudaStream_t s, const GBufDev& g, const RasterFused& out) {

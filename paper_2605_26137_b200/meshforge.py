@@ -91,13 +91,18 @@ def dilate_seams(image: np.ndarray, gbuffer: GBuffer, radius: int = 4, ctx=None)
 
 def bake_normal_map(lowpoly: TriangleMesh, highpoly: TriangleMesh, resolution: int, bbox_diagonal: float,
                     max_distance_fraction: float = 0.01, radius: int = 4, debug: bool = False,
-                    stats: bool = False, ctx=None):
+                    stats: bool = False, ctx=None, out=None):
     """dilateSeams(transferNormals(rasterizeGBuffer(lo, res), hi, diag, frac), g, radius)
     (test_bake.cpp:205-206) in one device-resident call. With ``debug`` also
-    returns per-texel hit faces and pre-quantisation tangent-space vectors."""
+    returns per-texel hit faces and pre-quantisation tangent-space vectors.
+    ``out`` (optional): a caller-owned (res, res, 3) uint8 C-contiguous array
+    to write into, e.g. a view of pinned host memory."""
     ctx = ctx or default_context()
     res = int(resolution)
-    out = np.zeros((res, res, 3), np.uint8) if res > 0 else np.zeros((0, 0, 3), np.uint8)
+    if out is None:
+        out = np.zeros((res, res, 3), np.uint8) if res > 0 else np.zeros((0, 0, 3), np.uint8)
+    elif out.shape != (res, res, 3) or out.dtype != np.uint8 or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError("out must be a C-contiguous (res, res, 3) uint8 array")
     face = np.zeros(res * res, np.int32) if debug and res > 0 else None
     ts = np.zeros((res * res, 3), np.float64) if debug and res > 0 else None
     st = capi.MfBakeStats()

@@ -220,3 +220,24 @@ def test_host_bake_error_order(gpu_ctx):
     # and the context still bakes afterwards
     out = mf.bake_normal_map(quad, quad, 32, float(np.sqrt(2.0)))
     assert out.shape[:2] == (32, 32) or out.size == 32 * 32 * 3
+
+
+@pytest.mark.parametrize("res,radius", [(None, 4), (None, 1), (None, 20), (300, 4), (100, 0), (64, 17)])
+def test_host_bake_pinned_banded_download(gpu_ctx, port, pair_a, res, radius):
+    """Host-buffer bake into pinned memory: the atlas is downloaded in row bands
+    while the transfer runs (BandSync, cuStreamWaitValue32) and the dilation is
+    resolved before the transfer (dilate_links). Byte-identical to the eager
+    device path, and within the parity bar of the oracle."""
+    torch = pytest.importorskip("torch")
+    p = pair_a
+    res = res or p.res
+    pinned = torch.empty((res, res, 3), dtype=torch.uint8).pin_memory().numpy()
+    pinned[:] = 7  # stale bytes must all be overwritten
+    for _ in range(3):  # eager, captured, replayed graphs
+        got = mf.bake_normal_map(p.lowpoly, p.dense, res, p.bbox_diagonal, p.max_distance_fraction, radius,
+                                 out=pinned)
+        ref = mf.bake_normal_map(p.lowpoly, p.dense, res, p.bbox_diagonal, p.max_distance_fraction, radius,
+                                 debug=True)
+        assert np.array_equal(got, ref["rgb"])
+    o = port.bake(p.lowpoly, p.dense, res, p.bbox_diagonal, p.max_distance_fraction, radius, debug=True)
+    assert_rgb_parity(pinned, o["rgb"], o["ts"])
