@@ -237,6 +237,8 @@ struct RasterFused {
   // row-band completion (BandSync): queries per band of band_rows slab rows
   int* band_tot = nullptr;
   int band_rows = 0;
+  cudaEvent_t cover_done = nullptr;  // recorded after the coverage/compaction kernel (split raster)
+  uint8_t* tile_state = nullptr;  // per 16x16 raster tile: 0 no valid texel, 1 mixed, 2 all valid
 };
 // True when raster_gbuffer fills RasterFused::qslot / dep_head (split raster,
 // single-pass query list).
@@ -347,7 +349,7 @@ void dilate_seams_to(Ctx& ctx, cudaStream_t s, int width, int height, int channe
 // their colour in `rgb` now, the others are linked to their source query.
 bool dilate_links_supported(int radius);
 void dilate_links(Ctx& ctx, cudaStream_t s, int res, const uint8_t* valid, int radius, const int* qslot,
-                  int* dep_head, int* dep_next, uint8_t* rgb);
+                  int* dep_head, int* dep_next, uint8_t* rgb, const uint8_t* tile_state = nullptr);
 void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
                   const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
                   int radius, uint8_t* map_out, int out_row0, int out_rows);

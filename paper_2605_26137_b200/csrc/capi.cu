@@ -556,6 +556,7 @@ struct BakeEnq {
       fo.qslot = c.buf<int>("bake.qslot", g.texels());
       fo.dep_head = c.buf<int>("bake.dephead", g.texels());
       dep_next = c.buf<int>("bake.depnext", g.texels());
+      fo.tile_state = c.buf<uint8_t>("bake.tilestate", static_cast<int64_t>(div_up(res, 16)) * div_up(res, 16));
     }
     fo.valid_count = counters + 2;
     if (debug) {
@@ -586,9 +587,27 @@ struct BakeEnq {
     RasterPlan plan;
     prepare_lowpoly(c, s, lo->m, res, plan);
     mk.e1 = tm.mark(s);
+    // the dilation links run beside the interpolation kernel (both need only
+    // the coverage kernel's outputs); MFB_LINKS_FORK=0 keeps them in line
+    static const bool links_fork = [] {
+      const char* e = std::getenv("MFB_LINKS_FORK");
+      return !(e && e[0] == '0');
+    }();
+    cudaStream_t ls = links && links_fork && c.aux2 ? c.aux2 : nullptr;
+    fo.cover_done = ls ? c.pool_event(60) : nullptr;
     raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
-    if (links) dilate_links(c, s, res, g.valid, radius, fo.qslot, fo.dep_head, dep_next, rgb_out);
-    if (band_sync) band_init(c, s, bs);
+    if (links) {
+      cudaStream_t t = ls ? ls : s;
+      if (ls) MFB_CUDA_TRY(cudaStreamWaitEvent(ls, fo.cover_done, 0));
+      dilate_links(c, t, res, g.valid, radius, fo.qslot, fo.dep_head, dep_next, rgb_out, fo.tile_state);
+      if (band_sync) band_init(c, t, bs);
+      if (ls) {
+        MFB_CUDA_TRY(cudaEventRecord(c.pool_event(61), ls));
+        MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.pool_event(61), 0));
+      }
+    } else if (band_sync) {
+      band_init(c, s, bs);
+    }
     mk.e2 = tm.mark(s);
     if (s != m) {
       MFB_CUDA_TRY(cudaEventRecord(c.lowjoin, s));

@@ -768,6 +768,10 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
   }
   if (kMode == 2) {
     const bool is_q = in && valid && rel;
+    if (fo.tile_state) {  // coverage class of this 16x16 tile (the dilation's tile skip)
+      const int nin = __syncthreads_count(in), nval = __syncthreads_count(in && valid);
+      if (threadIdx.x == 0) fo.tile_state[t] = nval == 0 ? 0 : (nval == nin ? 2 : 1);
+    }
     int* band_add = fo.band_tot ? fo.band_tot + (row_begin + ty * kTile - g_row0) / fo.band_rows : nullptr;
     const int slot = compact_slot(is_q, fo.q.count, fo.q.capacity, &flags[3], in && valid != 0, fo.valid_count,
                                   band_add);
@@ -1036,6 +1040,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
     f2.pend = ctx.buf<int2>("ras.pend", g.texels());
     k_raster<2><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
                                        g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, f2);
+    if (fused->cover_done) MFB_CUDA_TRY(cudaEventRecord(fused->cover_done, s));
     k_interp<<<kNumSMs * 8, 256, 0, s>>>(rf, attrs, f2.pend, fused->q.count, res, g.row0, fused->q);
     ctx.count_launch();
   } else if (fused) {
