@@ -366,7 +366,10 @@ __global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __res
       box.mx[k] = fmaxf(box.mx[k], other.mx[k]);
     }
   }
-  // `node` is complete with `box`: climb
+  // `node` is complete with `box`: climb. The parent's own link is loaded
+  // before the arrival atomic, so the next level does not start with a
+  // dependent load.
+  int link = node != 0 ? __ldg(node_parent + node) : 0;
   for (;;) {
     if (node == 0) {
 #pragma unroll
@@ -376,9 +379,9 @@ __global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __res
       }
       return;
     }
-    const int link = node_parent[node];
     const int par = link >> 1, side = link & 1;
     store_child_box(&nodes[par], side, box);
+    link = par != 0 ? __ldg(node_parent + par) : 0;
     if (arrive(&flags[par]) == 0) return;
     const FBox other = load_child_box_cg(&nodes[par], side ^ 1);
 #pragma unroll
