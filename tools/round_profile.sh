@@ -17,6 +17,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --c
   --log-file $OUT/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-rays \
   > $OUT/${TAG}_ncu_launch.log 2>&1; echo "ncu launches rc=$?"
 timeout 1200 ncu --set full --clock-control none --import-source on \
-  -k 'regex:k_transfer_t|k_raster|k_interp|k_refit_ranges|k_dilate_fused' -c 5 \
+  -k 'regex:k_transfer_t|k_raster|k_interp|k_refit_ranges|k_dilate_links' -c 5 \
   -o $OUT/${TAG}_prof -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-rays \
   > $OUT/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
