@@ -531,6 +531,7 @@ struct BakeEnq {
   // runs (BandSync); set before low()
   bool band_sync = false;
   BandSync bs;
+  int* band_check = nullptr;  // pinned [nb]: ready flags before the release (MFB_BAND_CHECK)
 
   BakeEnq(Ctx& cc, const mf_mesh* l, const mf_mesh* h, int rs, double dg, double fr, int rad, int b0, int b1,
           uint8_t* out, bool dbg, Timer& t, BakeMarks& m, const OutSet* pb = nullptr)
@@ -694,13 +695,26 @@ struct BakeEnq {
       // each band's download waits (on cp) for its ready flag, set by the
       // transfer's warps; the memset after the transfer releases every wait
       // regardless (by then every band is final), so no wait outlives it
-      ta.bands = bs;
+      // MFB_BAND_DIAG (diagnostic only, wrong results for 2): 1 = count in the
+      // transfer but copy after it; 2 = copy the bands without waiting
+      static const int band_diag = [] {
+        const char* e = std::getenv("MFB_BAND_DIAG");
+        return e ? std::atoi(e) : 0;
+      }();
+      if (band_diag != 2) ta.bands = bs;
       cudaEvent_t ev = c.pool_event(40);
       MFB_CUDA_TRY(cudaEventRecord(ev, s));
       transfer_normals(c, s, bvh, ta);
       mk.e4 = tm.mark(s);
+      // MFB_BAND_CHECK=1 (tests): the flags as the transfer left them, checked
+      // by the host after the bake - every band must have been signalled
+      // by the counts, not by the release below
+      if (band_check) {
+        MFB_CUDA_TRY(cudaMemcpyAsync(band_check, bs.ready, bs.nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+      }
       MFB_CUDA_TRY(cudaMemsetAsync(bs.ready, 1, bs.nb * sizeof(int), s));
       mk.e5 = tm.mark(s);
+      if (band_diag == 1) MFB_CUDA_TRY(cudaEventRecord(c.pool_event(41), s));
       MFB_CUDA_TRY(cudaStreamWaitEvent(cp, ev, 0));
       // MFB_BAND_TRACE=1 (diagnostic): per-band copy start/end vs the transfer start
       static const bool trace = std::getenv("MFB_BAND_TRACE") != nullptr;
@@ -709,9 +723,10 @@ struct BakeEnq {
         for (int k = 0; k < 2 * bs.nb + 2; ++k) MFB_CUDA_TRY(cudaEventCreate(&tev[k]));
         MFB_CUDA_TRY(cudaEventRecord(tev[2 * bs.nb], cp));
       }
+      if (band_diag == 1) MFB_CUDA_TRY(cudaStreamWaitEvent(cp, c.pool_event(41), 0));
       for (int b = 0; b < bs.nb; ++b) {
         const int r0 = b * bs.rows, r1 = std::min(res, r0 + bs.rows);
-        stream_wait_value(cp, bs.ready + b);
+        if (band_diag != 2) stream_wait_value(cp, bs.ready + b);
         if (trace) MFB_CUDA_TRY(cudaEventRecord(tev[2 * b], cp));
         const int64_t off = 3ll * r0 * res;
         MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off, 3ll * (r1 - r0) * res, cudaMemcpyDeviceToHost, cp));
@@ -1025,6 +1040,8 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     q.bs.res = res;
     q.bs.rows = std::max((div_up(res, 16) + 15) / 16 * 16, (radius + 15) / 16 * 16);
     q.bs.nb = div_up(res, q.bs.rows);
+    const char* chk = std::getenv("MFB_BAND_CHECK");
+    if (chk && chk[0] == '1') q.band_check = static_cast<int*>(c.host_buf("bake.bandcheck", kMaxBands * sizeof(int)));
   }
   static const bool graphs = [] {
     const char* e = std::getenv("MFB_GRAPH");
@@ -1077,6 +1094,10 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     return;
   }
   if (hflags[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+  if (q.band_check)
+    for (int b = 0; b < q.bs.nb; ++b)
+      if (q.band_check[b] != 1)
+        throw ApiError(MF_ERR_CUDA, "band sync: row band " + std::to_string(b) + " was not signalled by the transfer");
   if (st) {
     st->queries = static_cast<int64_t>(hcnt[0]);
     st->hits = static_cast<int64_t>(hcnt[1]);

@@ -334,19 +334,30 @@ __device__ __forceinline__ int32_t pop_within(const int32_t* st_ref, const float
 // Row-band completion (BandSync, bake.cuh). Band b is complete once all its
 // queries are done; its rows are final once b-1, b, b+1 (those that exist)
 // are complete. The caller has fenced its stores.
+// (rare path: full fences are fine here)
 __device__ __forceinline__ void band_complete(const BandSync& bs, int band) {
   for (int k = max(0, band - 1); k <= min(bs.nb - 1, band + 1); ++k) {
     const int need = 1 + (k > 0) + (k < bs.nb - 1);
+    __threadfence();
     if (atomicAdd(&bs.nbr[k], 1) + 1 == need) {
       __threadfence_system();
       atomicExch(&bs.ready[k], 1);
     }
   }
 }
+// Per-batch publication: a release add (MEMBAR.GPU + atomic). __threadfence
+// here would be MEMBAR.SC + CCTL.IVALL - an L1 invalidation per batch that
+// costs the walk its cached nodes (measured +40 us per transfer). The other
+// lanes' stores are ordered before the leader's release by __syncwarp.
+__device__ __forceinline__ int atom_add_release_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.release.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void band_arrive(const BandSync& bs, int band, int n) {
-  const int old = atomicAdd(&bs.done[band], n);
+  const int old = atom_add_release_gpu(&bs.done[band], n);
   if (old + n == __ldcg(bs.tot + band)) {
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire the other publishers' releases
     band_complete(bs, band);
   }
 }
@@ -552,9 +563,10 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       }
     }
     if (bands.done) {  // this batch's texels (and their gutter texels) are written
-      __threadfence();
       const int band = texel / bands.res / bands.rows;
+      // (a batch can hold several raster tiles' segments: group by band)
       const unsigned grp = __match_any_sync(live_mask, band);
+      __syncwarp(live_mask);
       if (lane == __ffs(grp) - 1) band_arrive(bands, band, __popc(grp));
     }
     if (kDebug) {

@@ -229,6 +229,8 @@ def test_host_bake_pinned_banded_download(gpu_ctx, port, pair_a, res, radius):
     resolved before the transfer (dilate_links). Byte-identical to the eager
     device path, and within the parity bar of the oracle."""
     torch = pytest.importorskip("torch")
+    import os
+    os.environ["MFB_BAND_CHECK"] = "1"  # every band signalled by the transfer's counts
     p = pair_a
     res = res or p.res
     pinned = torch.empty((res, res, 3), dtype=torch.uint8).pin_memory().numpy()
