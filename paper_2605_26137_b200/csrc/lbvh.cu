@@ -256,6 +256,158 @@ __global__ void k_repack(const double* __restrict__ pos, const int32_t* __restri
   tbox[p].b = make_float4(box.mx[1], box.mx[2], 0.f, 0.f);
 }
 
+// ---- node boxes from a segment tree over the leaf-order triangle boxes -----
+// Every Karras node covers a contiguous range of leaf-order triangles, so its
+// children's boxes are range unions: a power-of-two segment tree over the
+// TBox array (leaves at N + i, internal node j = union of 2j and 2j+1, built
+// 10 levels per 1024-thread CTA in shared memory) answers each child box
+// with O(log range) independent loads - no bottom-up climb with one atomic
+// and one dependent L2 round trip per level. The unions are exact (fminf /
+// fmaxf), so the boxes are the ones the climb would produce.
+__device__ __forceinline__ FBox fbox_empty() {
+  FBox b;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    b.mn[k] = INFINITY;
+    b.mx[k] = -INFINITY;
+  }
+  return b;
+}
+__device__ __forceinline__ void fbox_union(FBox& a, const FBox& b) {
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    a.mn[k] = fminf(a.mn[k], b.mn[k]);
+    a.mx[k] = fmaxf(a.mx[k], b.mx[k]);
+  }
+}
+__device__ __forceinline__ FBox fbox_load(const TBox* p) {
+  const float4 a = __ldg(&p->a), b = __ldg(&p->b);
+  FBox r;
+  r.mn[0] = a.x;
+  r.mn[1] = a.y;
+  r.mn[2] = a.z;
+  r.mx[0] = a.w;
+  r.mx[1] = b.x;
+  r.mx[2] = b.y;
+  return r;
+}
+__device__ __forceinline__ void fbox_store(TBox* p, const FBox& r) {
+  p->a = make_float4(r.mn[0], r.mn[1], r.mn[2], r.mx[0]);
+  p->b = make_float4(r.mx[1], r.mx[2], 0.f, 0.f);
+}
+// Thread t holds node base + t of a level [L, 2L); the CTA's `cnt` nodes
+// are consecutive and 1024-aligned (or the whole level when L < 1024).
+// Writes their ancestors up to 10 levels, or to the root (index 1).
+__device__ __forceinline__ void seg_reduce_block(FBox box, unsigned base, int cnt, TBox* seg, FBox* sm) {
+  const int t = threadIdx.x;
+  sm[t] = box;
+  __syncthreads();
+  for (int lv = 1; lv <= 10; ++lv) {
+    if ((base >> lv) == 0) break;  // past the root (uniform across the CTA)
+    const unsigned par = (base + t) >> lv;
+    const int half = 1 << (lv - 1);
+    if ((t & ((1 << lv) - 1)) == 0 && t < cnt) {
+      FBox u = sm[t];
+      if (t + half < cnt) fbox_union(u, sm[t + half]);
+      sm[t] = u;
+      fbox_store(seg + par, u);
+    }
+    __syncthreads();
+  }
+}
+
+// Gathers each primitive's f64 vertices into leaf order and its outward-
+// rounded fp32 box, and builds the segment tree's first 10 levels.
+__global__ void __launch_bounds__(1024) k_repack_seg(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                                     const uint32_t* __restrict__ order, int n, int N,
+                                                     BTri* __restrict__ tris, TBox* __restrict__ tbox,
+                                                     TBox* __restrict__ seg) {
+  __shared__ FBox sm[1024];
+  const int p = blockIdx.x * 1024 + threadIdx.x;
+  FBox box = fbox_empty();
+  if (p < n) {
+    const int f = static_cast<int>(order[p]);
+    const int vi[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
+    BTri t;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const double x = pos[3 * vi[c] + k];
+        t.v[3 * c + k] = x;
+        box.mn[k] = fminf(box.mn[k], __double2float_rd(x));
+        box.mx[k] = fmaxf(box.mx[k], __double2float_ru(x));
+      }
+    }
+    t.face = f;
+    t.pad = 0;
+    const double2* src = reinterpret_cast<const double2*>(&t);
+    double2* dst = reinterpret_cast<double2*>(&tris[p]);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) dst[q] = src[q];
+    fbox_store(tbox + p, box);
+  }
+  seg_reduce_block(box, static_cast<unsigned>(N + blockIdx.x * 1024), min(1024, N), seg, sm);
+}
+
+// The next 10 levels: nodes [L, 2L) -> their ancestors.
+__global__ void __launch_bounds__(1024) k_seg_up(TBox* __restrict__ seg, int L) {
+  __shared__ FBox sm[1024];
+  const int i = blockIdx.x * 1024 + threadIdx.x;
+  const FBox box = i < L ? fbox_load(seg + L + i) : fbox_empty();
+  seg_reduce_block(box, static_cast<unsigned>(L + blockIdx.x * 1024), min(1024, L), seg, sm);
+}
+
+// Union of leaf-order triangles [a, b] (inclusive) from the segment tree.
+__device__ __forceinline__ FBox seg_query(const TBox* __restrict__ seg, const TBox* __restrict__ tbox, unsigned N,
+                                          int a, int b) {
+  FBox r = fbox_empty();
+  unsigned l = static_cast<unsigned>(a) + N, h = static_cast<unsigned>(b) + N + 1;
+  while (l < h) {
+    if (l & 1) {
+      fbox_union(r, l >= N ? fbox_load(tbox + (l - N)) : fbox_load(seg + l));
+      ++l;
+    }
+    if (h & 1) {
+      --h;
+      fbox_union(r, h >= N ? fbox_load(tbox + (h - N)) : fbox_load(seg + h));
+    }
+    l >>= 1;
+    h >>= 1;
+  }
+  return r;
+}
+
+// Both child boxes of every reachable node (root, or range > leaf_max).
+__global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restrict__ tbox, int N, int n, int leaf_max,
+                             BNode* __restrict__ nodes, float* __restrict__ root_box) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  const int4 d = nodes[i].d;
+  if (i != 0 && d.w <= leaf_max) return;  // inside a leaf range: never referenced
+  int gamma;
+  if (d.x >= 0) {
+    gamma = d.x;
+  } else {
+    int f, c;
+    leaf_decode(d.x, f, c);
+    gamma = f + c - 1;
+  }
+  const FBox L = seg_query(seg, tbox, static_cast<unsigned>(N), d.z, gamma);
+  const FBox R = seg_query(seg, tbox, static_cast<unsigned>(N), gamma + 1, d.z + d.w - 1);
+  store_child_box(&nodes[i], 0, L);
+  store_child_box(&nodes[i], 1, R);
+  if (i == 0) {
+    FBox u = L;
+    fbox_union(u, R);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      root_box[k] = u.mn[k];
+      root_box[3 + k] = u.mx[k];
+    }
+  }
+}
+
 // Bottom-up refit: each primitive's thread climbs while it is the second
 // child to arrive (acquire/release counter per node), storing the child box
 // into its parent's slot.
@@ -423,7 +575,13 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
 
   MFB_CUDA_TRY(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
   MFB_CUDA_TRY(cudaMemsetAsync(acc + 3, 0x00, 5 * sizeof(unsigned long long), s));
-  if (out.n_nodes > 0) MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * out.n_nodes, s));
+  // segment-tree node boxes (MFB_SEGTREE=0: the bottom-up refit climb)
+  static const bool segtree = [] {
+    const char* e = std::getenv("MFB_SEGTREE");
+    return !(e && e[0] == '0');
+  }();
+  const bool use_seg = segtree && n > 1;
+  if (out.n_nodes > 0 && !use_seg) MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * out.n_nodes, s));
 
   const int T = 256;
   const int grid_b = std::min(div_up(std::max(n, m.nv), T), kNumSMs * 8);
@@ -460,7 +618,19 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
     MFB_CUDA_TRY(cudaEventRecord(ctx.lfork, s));
     MFB_CUDA_TRY(cudaStreamWaitEvent(rs, ctx.lfork, 0));
   }
-  k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
+  // segment tree over the leaf-order boxes (node boxes without a refit climb)
+  int N = 1;
+  while (N < n) N <<= 1;
+  TBox* seg = nullptr;
+  if (use_seg) {
+    seg = ctx.buf<TBox>(tag + ".seg", N);
+    k_repack_seg<<<div_up(N, 1024), 1024, 0, rs>>>(m.pos, m.faces, vals2, n, N, out.tris, out.tbox, seg);
+    int launches = 1;
+    for (int L = N >> 10; L > 1; L >>= 10, ++launches) k_seg_up<<<div_up(L, 1024), 1024, 0, rs>>>(seg, L);
+    ctx.count_launch(launches - 1);
+  } else {
+    k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
+  }
   if (rs != s) MFB_CUDA_TRY(cudaEventRecord(ctx.ljoin, rs));
   if (n > 1) {
     MFB_CUDA_TRY(cudaMemsetAsync(starts_n, 0, sizeof(int), s));
@@ -469,7 +639,9 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
     ctx.count_launch();
   }
   if (rs != s) MFB_CUDA_TRY(cudaStreamWaitEvent(s, ctx.ljoin, 0));
-  if (n > 1) {
+  if (seg) {
+    k_node_boxes<<<div_up(n - 1, T), T, 0, s>>>(seg, out.tbox, N, n, leaf_max, out.nodes, out.root_box_dev);
+  } else if (n > 1) {
     // starts <= leaf ranges <= n; threads past the device count exit at once
     k_refit_ranges<<<div_up(n, T), T, 0, s>>>(out.tbox, out.nodes, starts, starts_n, out.nodes,
                                                        node_parent, flags, out.root_box_dev);
