@@ -42,13 +42,40 @@ __device__ __forceinline__ float prune_bound(double best, double E) {
   return __double2float_ru(r * r * (1.0 + 0x1p-30));
 }
 
+// One 64-byte node record in two 256-bit read-only loads (LDG.E.256 on
+// sm_100; four LDG.128 otherwise). MFB_LDG256=0 keeps the 128-bit loads.
+#ifndef MFB_LDG256
+#define MFB_LDG256 1
+#endif
+__device__ __forceinline__ void ld_node(const BNode* __restrict__ nd, float4& a, float4& b, float4& c, int4& d) {
+#if MFB_LDG256
+  const float* p = reinterpret_cast<const float*>(nd);
+  float dx, dy, dz, dw;
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+               : "l"(p));
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w), "=f"(dx), "=f"(dy), "=f"(dz), "=f"(dw)
+               : "l"(p + 8));
+  d = make_int4(__float_as_int(dx), __float_as_int(dy), __float_as_int(dz), __float_as_int(dw));
+#else
+  const float4* np = reinterpret_cast<const float4*>(nd);
+  a = __ldg(np);
+  b = __ldg(np + 1);
+  c = __ldg(np + 2);
+  d = __ldg(reinterpret_cast<const int4*>(np + 3));
+#endif
+}
+
 // Lower bound of the squared distance from [qlo, qhi] (per axis) to a box.
 __device__ __forceinline__ float box_lb(float mnx, float mny, float mnz, float mxx, float mxy,
                                         float mxz, float3 qlo, float3 qhi) {
   const float dx = fmaxf(fmaxf(__fsub_rd(mnx, qhi.x), __fsub_rd(qlo.x, mxx)), 0.0f);
   const float dy = fmaxf(fmaxf(__fsub_rd(mny, qhi.y), __fsub_rd(qlo.y, mxy)), 0.0f);
   const float dz = fmaxf(fmaxf(__fsub_rd(mnz, qhi.z), __fsub_rd(qlo.z, mxz)), 0.0f);
-  return __fadd_rd(__fadd_rd(__fmul_rd(dx, dx), __fmul_rd(dy, dy)), __fmul_rd(dz, dz));
+  // fused multiply-adds rounded down: one rounding each, still a lower bound
+  // (2 instructions fewer per box than separate products and sums)
+  return __fmaf_rd(dz, dz, __fmaf_rd(dy, dy, __fmul_rd(dx, dx)));
 }
 
 // spatial/tri_geom.h:37-95 — same branch order, same expression order.
@@ -451,9 +478,9 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       // ---- descend until this lane holds a leaf
       while (ref >= 0) {
         if (kProf) ++pv[0];
-        const float4* np = reinterpret_cast<const float4*>(nodes + ref);
-        const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
-        const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
+        float4 a, b, c;
+        int4 d;
+        ld_node(nodes + ref, a, b, c, d);
         if (MFB_PF & 4) {
           if (d.x >= 0) pf_l1(nodes + d.x);
           if (d.y >= 0) pf_l1(nodes + d.y);
