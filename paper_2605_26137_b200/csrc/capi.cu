@@ -1048,7 +1048,14 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     q.bs.nbr = bb + 2 * kMaxBands;
     q.bs.ready = bb + 3 * kMaxBands;
     q.bs.res = res;
-    q.bs.rows = std::max((div_up(res, 16) + 15) / 16 * 16, (radius + 15) / 16 * 16);
+    // ~32 bands (64 rows at 2048^2): the copy left after the transfer is one
+    // small band. MFB_E2E_BAND_DIV overrides the count (A/B).
+    static const int band_div = [] {
+      const char* e = std::getenv("MFB_E2E_BAND_DIV");
+      const int v = e ? std::atoi(e) : 32;
+      return v >= 1 && v <= kMaxBands ? v : 32;
+    }();
+    q.bs.rows = std::max((div_up(res, band_div) + 15) / 16 * 16, (radius + 15) / 16 * 16);
     q.bs.nb = div_up(res, q.bs.rows);
     const char* chk = std::getenv("MFB_BAND_CHECK");
     if (chk && chk[0] == '1') q.band_check = static_cast<int*>(c.host_buf("bake.bandcheck", kMaxBands * sizeof(int)));
