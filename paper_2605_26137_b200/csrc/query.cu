@@ -419,6 +419,11 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}) {
   const int nq = qcount[kPass == 2 ? 1 : 0];
   const int lane = threadIdx.x & 31;
+  if (kProf && lane == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&prof_out[4], t);
+  }
   unsigned long long pv[4] = {0, 0, 0, 0};  // internal visits, leaf visits, triangle tests, queries
   const double scene_max = from_ordered_dev(scene_acc[6]);
   const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
@@ -605,12 +610,19 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       }
     }
   }
-  if (kProf)
+  if (kProf) {
     for (int k = 0; k < 4; ++k) {
       unsigned long long v = pv[k];
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
       if (lane == 0) atomicAdd(&prof_out[k], v);
     }
+    if (lane == 0) {  // warp exit times (tail spread): [5] first, [6] last, [4] kernel start
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      atomicMin(&prof_out[5], t);
+      atomicMax(&prof_out[6], t);
+    }
+  }
   if (counters) {
     for (int off = 16; off > 0; off >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, off);
     if (lane == 0 && hits) atomicAdd(&counters[1], static_cast<unsigned long long>(hits));
@@ -1231,6 +1243,7 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
   if (prof) {
     pbuf = ctx.buf<unsigned long long>("xfer.prof", 8);
     MFB_CUDA_TRY(cudaMemsetAsync(pbuf, 0, 8 * sizeof(unsigned long long), s));
+    MFB_CUDA_TRY(cudaMemsetAsync(pbuf + 4, 0xff, 2 * sizeof(unsigned long long), s));
   }
   if (kSeedPasses) MFB_CUDA_TRY(cudaMemsetAsync(a.face_map, 0xff, sizeof(int) * a.face_map_size, s));
   static const int bps = occupancy(k_transfer_t<false, false>);
@@ -1263,8 +1276,10 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     MFB_CUDA_TRY(cudaMemcpyAsync(h, pbuf, sizeof(h), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
     const double nqd = h[3] ? static_cast<double>(h[3]) : 1.0;
-    std::fprintf(stderr, "[mfb prof] per query: internal %.2f leaves %.2f triangles %.2f (queries %llu)\n",
-                 h[0] / nqd, h[1] / nqd, h[2] / nqd, h[3]);
+    std::fprintf(stderr,
+                 "[mfb prof] per query: internal %.2f leaves %.2f triangles %.2f (queries %llu); warp exits "
+                 "%.1f..%.1f us after the first start\n",
+                 h[0] / nqd, h[1] / nqd, h[2] / nqd, h[3], (h[5] - h[4]) * 1e-3, (h[6] - h[4]) * 1e-3);
   }
 }
 
