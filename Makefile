@@ -37,9 +37,9 @@ build/cu/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
 $(PKG)/libmfbake.so: $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $^ -Xlinker -soname=libmfbake.so
 
-$(PKG)/libmeshforge_b200.so: $(PKG)/cpp/meshforge_b200.cpp $(PKG)/cpp/io_b200.cpp $(MF_HDRS) include/mfbake.h \
+$(PKG)/libmeshforge_b200.so: $(PKG)/cpp/meshforge_b200.cpp $(PKG)/cpp/io_b200.cpp $(PKG)/cpp/metrics_b200.cpp $(MF_HDRS) include/mfbake.h \
                              $(PKG)/libmfbake.so
-	$(CXX) $(CXXFLAGS) -pthread -shared -o $@ $(PKG)/cpp/meshforge_b200.cpp $(PKG)/cpp/io_b200.cpp -L$(PKG) -lmfbake \
+	$(CXX) $(CXXFLAGS) -pthread -shared -o $@ $(PKG)/cpp/meshforge_b200.cpp $(PKG)/cpp/io_b200.cpp $(PKG)/cpp/metrics_b200.cpp -L$(PKG) -lmfbake \
 	  -lz -Wl,-rpath,'$$ORIGIN'
 
 build/test_bake_b200: tests/cpp/test_bake_b200.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so

@@ -42,6 +42,14 @@ inline Eigen::Vector3d faceNormal(const TriangleMesh& m, int f) {
 
 // Bounding box of the positions.
 Aabb3d bounds(const TriangleMesh& m);
+// Sum of face areas in face order (core/mesh.cpp:18-22).
+double surfaceArea(const TriangleMesh& m);
+// Uniform scale + translation putting the mesh inside the sphere of the given
+// radius centred at the origin; returns the scale (core/mesh.cpp:50-59).
+double normalizeToSphere(TriangleMesh& m, double radius = 0.5);
+// One shared transform mapping the pair's union bounding box into the unit
+// cube (core/mesh.cpp:61-70).
+void normalizePairToUnitCube(TriangleMesh& a, TriangleMesh& b);
 // Area-weighted vertex normals summed in face order, normalised (zero stays
 // zero) - computed on the B200 (mf_vertex_normals).
 std::vector<Eigen::Vector3d> computeVertexNormals(const TriangleMesh& m);

@@ -66,3 +66,14 @@ def test_reference_test_io_against_b200_api(gpu_ctx):
         pytest.skip("built only where /root/reference exists")
     out = run(exe)
     assert "FAIL" not in out and "test cases passed" in out
+
+
+def test_reference_test_metrics_against_b200_api(gpu_ctx):
+    """The reference's own tests/test_metrics.cpp (surface sampling, chamfer /
+    Hausdorff, flipped-normal pixels, geometric and baked normal error) against
+    the B200 C++ API: the closest-point queries run on the device."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_metrics_b200")
+    if not os.path.exists(exe):
+        pytest.skip("built only where /root/reference exists")
+    out = run(exe)
+    assert "FAIL" not in out and "test cases passed" in out
