@@ -406,7 +406,9 @@ __global__ void k_band_init(BandSync bs) {
 #else
 #define MFB_XFER_T_BOUNDS __launch_bounds__(128)
 #endif
-template <bool kDebug, bool kProf, int kPass = 0>
+// kBands: the row-band publication of the host path's overlapped download
+// (compiled only into that instantiation: it costs the walk registers)
+template <bool kDebug, bool kProf, int kPass = 0, bool kBands = false>
 __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
     const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
@@ -594,7 +596,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         d[2] = px[2];
       }
     }
-    if (bands.done) {  // this batch's texels (and their gutter texels) are written
+    if (kBands && bands.done) {  // this batch's texels (and their gutter texels) are written
       const int band = texel / bands.res / bands.rows;
       // (a batch can hold several raster tiles' segments: group by band)
       const unsigned grp = __match_any_sync(live_mask, band);
@@ -1264,6 +1266,11 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     MFB_XFER_TP(1);
     MFB_XFER_TP(2);
     ctx.count_launch();
+  } else if (a.bands.done) {
+    k_transfer_t<false, false, 0, true><<<g2, 128, 0, s>>>(
+        bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
+        a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
+        a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands);
   } else {
     MFB_XFER_TP(0);
   }
