@@ -280,39 +280,49 @@ __device__ __forceinline__ void fbox_union(FBox& a, const FBox& b) {
     a.mx[k] = fmaxf(a.mx[k], b.mx[k]);
   }
 }
-__device__ __forceinline__ FBox fbox_load(const TBox* p) {
-  const float4 a = __ldg(&p->a), b = __ldg(&p->b);
+__device__ __forceinline__ FBox fbox_load(const TBox* p) {  // one 256-bit read-only load
   FBox r;
-  r.mn[0] = a.x;
-  r.mn[1] = a.y;
-  r.mn[2] = a.z;
-  r.mx[0] = a.w;
-  r.mx[1] = b.x;
-  r.mx[2] = b.y;
+  float p0, p1;
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r.mn[0]), "=f"(r.mn[1]), "=f"(r.mn[2]), "=f"(r.mx[0]), "=f"(r.mx[1]), "=f"(r.mx[2]), "=f"(p0), "=f"(p1)
+      : "l"(p));
   return r;
 }
 __device__ __forceinline__ void fbox_store(TBox* p, const FBox& r) {
   p->a = make_float4(r.mn[0], r.mn[1], r.mn[2], r.mx[0]);
   p->b = make_float4(r.mx[1], r.mx[2], 0.f, 0.f);
 }
-// Thread t holds node base + t of a level [L, 2L); the CTA's `cnt` nodes
-// are consecutive and 1024-aligned (or the whole level when L < 1024).
-// Writes their ancestors up to 10 levels, or to the root (index 1).
+// Thread t holds node base + t of a level [L, 2L) (empty box past `cnt`);
+// the CTA's nodes are consecutive and 1024-aligned (or the whole level when
+// L < 1024). Writes their ancestors up to 10 levels, or to the root (index 1):
+// five levels inside each warp with shuffles, five more across the CTA's
+// warps in warp 0 - one barrier.
+__device__ __forceinline__ FBox fbox_shfl_down(const FBox& b, int d) {
+  FBox r;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    r.mn[k] = __shfl_down_sync(0xffffffffu, b.mn[k], d);
+    r.mx[k] = __shfl_down_sync(0xffffffffu, b.mx[k], d);
+  }
+  return r;
+}
 __device__ __forceinline__ void seg_reduce_block(FBox box, unsigned base, int cnt, TBox* seg, FBox* sm) {
-  const int t = threadIdx.x;
-  sm[t] = box;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int lv = 1; lv <= 5; ++lv) {
+    if ((base >> lv) == 0) return;  // past the root (uniform across the CTA)
+    fbox_union(box, fbox_shfl_down(box, 1 << (lv - 1)));  // (lanes past 31 get their own box)
+    if ((lane & ((1 << lv) - 1)) == 0 && t < cnt) fbox_store(seg + ((base + t) >> lv), box);
+  }
+  if ((base >> 6) == 0) return;
+  if (lane == 0) sm[w] = box;
   __syncthreads();
-  for (int lv = 1; lv <= 10; ++lv) {
-    if ((base >> lv) == 0) break;  // past the root (uniform across the CTA)
-    const unsigned par = (base + t) >> lv;
-    const int half = 1 << (lv - 1);
-    if ((t & ((1 << lv) - 1)) == 0 && t < cnt) {
-      FBox u = sm[t];
-      if (t + half < cnt) fbox_union(u, sm[t + half]);
-      sm[t] = u;
-      fbox_store(seg + par, u);
-    }
-    __syncthreads();
+  if (w != 0) return;
+  const int nw = (cnt + 31) >> 5;
+  box = lane < nw ? sm[lane] : fbox_empty();
+  for (int lv = 6; lv <= 10; ++lv) {
+    if ((base >> lv) == 0) return;
+    fbox_union(box, fbox_shfl_down(box, 1 << (lv - 6)));
+    if ((lane & ((1 << (lv - 5)) - 1)) == 0 && lane < nw) fbox_store(seg + ((base + 32u * lane) >> lv), box);
   }
 }
 
@@ -322,7 +332,7 @@ __global__ void __launch_bounds__(1024) k_repack_seg(const double* __restrict__ 
                                                      const uint32_t* __restrict__ order, int n, int N,
                                                      BTri* __restrict__ tris, TBox* __restrict__ tbox,
                                                      TBox* __restrict__ seg) {
-  __shared__ FBox sm[1024];
+  __shared__ FBox sm[32];
   const int p = blockIdx.x * 1024 + threadIdx.x;
   FBox box = fbox_empty();
   if (p < n) {
@@ -350,9 +360,20 @@ __global__ void __launch_bounds__(1024) k_repack_seg(const double* __restrict__ 
   seg_reduce_block(box, static_cast<unsigned>(N + blockIdx.x * 1024), min(1024, N), seg, sm);
 }
 
+// The first 10 levels above the leaf-order boxes written by k_repack (a
+// separate pass: the 256-thread gather runs at full occupancy, and this
+// streaming reduction reads the 32-byte boxes once).
+__global__ void __launch_bounds__(1024) k_seg_leaves(const TBox* __restrict__ tbox, int n, int N,
+                                                     TBox* __restrict__ seg) {
+  __shared__ FBox sm[32];
+  const int p = blockIdx.x * 1024 + threadIdx.x;
+  const FBox box = p < n ? fbox_load(tbox + p) : fbox_empty();
+  seg_reduce_block(box, static_cast<unsigned>(N + blockIdx.x * 1024), min(1024, N), seg, sm);
+}
+
 // The next 10 levels: nodes [L, 2L) -> their ancestors.
 __global__ void __launch_bounds__(1024) k_seg_up(TBox* __restrict__ seg, int L) {
-  __shared__ FBox sm[1024];
+  __shared__ FBox sm[32];
   const int i = blockIdx.x * 1024 + threadIdx.x;
   const FBox box = i < L ? fbox_load(seg + L + i) : fbox_empty();
   seg_reduce_block(box, static_cast<unsigned>(L + blockIdx.x * 1024), min(1024, L), seg, sm);
@@ -624,8 +645,18 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   TBox* seg = nullptr;
   if (use_seg) {
     seg = ctx.buf<TBox>(tag + ".seg", N);
-    k_repack_seg<<<div_up(N, 1024), 1024, 0, rs>>>(m.pos, m.faces, vals2, n, N, out.tris, out.tbox, seg);
+    static const bool fused_seg = [] {
+      const char* e = std::getenv("MFB_SEG_FUSED");
+      return e && e[0] == '1';
+    }();
     int launches = 1;
+    if (fused_seg) {
+      k_repack_seg<<<div_up(N, 1024), 1024, 0, rs>>>(m.pos, m.faces, vals2, n, N, out.tris, out.tbox, seg);
+    } else {
+      k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
+      k_seg_leaves<<<div_up(N, 1024), 1024, 0, rs>>>(out.tbox, n, N, seg);
+      ++launches;
+    }
     for (int L = N >> 10; L > 1; L >>= 10, ++launches) k_seg_up<<<div_up(L, 1024), 1024, 0, rs>>>(seg, L);
     ctx.count_launch(launches - 1);
   } else {
