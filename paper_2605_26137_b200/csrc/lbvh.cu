@@ -414,8 +414,30 @@ __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restric
     leaf_decode(d.x, f, c);
     gamma = f + c - 1;
   }
-  const FBox L = seg_query(seg, tbox, static_cast<unsigned>(N), d.z, gamma);
-  const FBox R = seg_query(seg, tbox, static_cast<unsigned>(N), gamma + 1, d.z + d.w - 1);
+  // both children's ranges walked together: the up-to-four loads of a level
+  // are issued before any of them is used (one L2 round trip per level)
+  FBox L = fbox_empty(), R = fbox_empty();
+  const unsigned uN = static_cast<unsigned>(N);
+  unsigned l1 = static_cast<unsigned>(d.z) + uN, h1 = static_cast<unsigned>(gamma) + uN + 1;
+  unsigned l2 = h1, h2 = static_cast<unsigned>(d.z + d.w) + uN;
+  auto ld = [&](unsigned j) { return j >= uN ? fbox_load(tbox + (j - uN)) : fbox_load(seg + j); };
+  while (l1 < h1 || l2 < h2) {
+    const bool a = l1 < h1 && (l1 & 1), b = l1 < h1 && (h1 & 1);
+    const bool c = l2 < h2 && (l2 & 1), e = l2 < h2 && (h2 & 1);
+    FBox xa = fbox_empty(), xb = fbox_empty(), xc = fbox_empty(), xe = fbox_empty();
+    if (a) xa = ld(l1);
+    if (b) xb = ld(h1 - 1);
+    if (c) xc = ld(l2);
+    if (e) xe = ld(h2 - 1);
+    fbox_union(L, xa);
+    fbox_union(L, xb);
+    fbox_union(R, xc);
+    fbox_union(R, xe);
+    l1 = (l1 + a) >> 1;
+    h1 = (h1 - b) >> 1;
+    l2 = (l2 + c) >> 1;
+    h2 = (h2 - e) >> 1;
+  }
   store_child_box(&nodes[i], 0, L);
   store_child_box(&nodes[i], 1, R);
   if (i == 0) {
