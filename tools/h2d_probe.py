@@ -20,6 +20,14 @@ def two():
     with torch.cuda.stream(s2):
         s2.wait_event(ev); d[N//2:].copy_(h[N//2:], non_blocking=True)
     torch.cuda.current_stream().wait_stream(s1); torch.cuda.current_stream().wait_stream(s2)
+ss = [torch.cuda.Stream() for _ in range(4)]
+def four():
+    ev = torch.cuda.Event(); ev.record()
+    q = N // 4
+    for k, st in enumerate(ss):
+        with torch.cuda.stream(st):
+            st.wait_event(ev); d[k * q:(k + 1) * q].copy_(h[k * q:(k + 1) * q], non_blocking=True)
+    for st in ss: torch.cuda.current_stream().wait_stream(st)
 def down(): h.copy_(d, non_blocking=True)
-for name, fn in (("h2d one", one), ("h2d two streams", two), ("d2h one", down)):
+for name, fn in (("h2d one", one), ("h2d two streams", two), ("h2d four streams", four), ("d2h one", down)):
     ms = t(fn); print(f"{name}: {ms:.3f} ms  {N / ms / 1e6:.1f} GB/s")
