@@ -73,6 +73,7 @@ struct Ctx {
   uint64_t alloc_gen = 0;
   // Persistent timing events (graph-capturable: never destroyed mid-flight).
   std::vector<cudaEvent_t> ev_pool;
+  int wait_value_probe = 0;  // cuStreamWaitValue32 on this device: 0 untested, 1 usable, -1 not
   cudaEvent_t pool_event(int i);
   // Captured fused bake (see capi.cu bake_dev).
   cudaGraphExec_t bake_exec = nullptr;

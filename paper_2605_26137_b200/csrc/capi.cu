@@ -504,6 +504,24 @@ WaitValueFn wait_value_fn() {
   }();
   return fn;
 }
+// One probe per context (first host-buffer bake): a wait on a flag that is
+// already set, on the copy stream, must succeed - otherwise the bake keeps
+// the single download after the transfer.
+bool wait_value_usable(Ctx& c) {
+  if (c.wait_value_probe != 0) return c.wait_value_probe > 0;
+  c.wait_value_probe = -1;
+  if (!wait_value_fn() || !c.aux2) return false;
+  int* f = c.buf<int>("bake.waitprobe", 1);
+  if (cudaMemsetAsync(f, 0x01, sizeof(int), c.aux2) != cudaSuccess) return false;
+  if (wait_value_fn()(reinterpret_cast<CUstream>(c.aux2), reinterpret_cast<CUdeviceptr>(f), 1,
+                      CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+    (void)cudaGetLastError();
+    return false;
+  }
+  if (cudaStreamSynchronize(c.aux2) != cudaSuccess) return false;
+  c.wait_value_probe = 1;
+  return true;
+}
 void stream_wait_value(cudaStream_t s, int* flag) {
   if (wait_value_fn()(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(flag), 1,
                       CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
@@ -1040,7 +1058,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     const char* e = std::getenv("MFB_E2E_BANDS");
     return !(e && e[0] == '0');
   }();
-  if (q.links && band_env && wait_value_fn() && c.aux2 && host_pinned(rgb_out)) {
+  if (q.links && band_env && host_pinned(rgb_out) && wait_value_usable(c)) {
     q.band_sync = true;
     int* bb = c.buf<int>("bake.bands", 4 * kMaxBands);
     q.bs.tot = bb;
