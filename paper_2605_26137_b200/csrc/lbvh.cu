@@ -136,9 +136,11 @@ __device__ __forceinline__ int kdelta(const uint32_t* __restrict__ k, int n, int
 // Also appends every reachable node with a leaf-range child to `starts`
 // (count in starts_n): the refit climbs start there, so it never reads the
 // nodes buried inside leaf ranges.
+// (reach_list: `starts` instead lists every reachable node - the root and
+// every node covering more than leaf_max primitives - for k_node_boxes)
 __global__ void k_emit(const uint32_t* __restrict__ keys, int n, int leaf_max, BNode* __restrict__ nodes,
                        int32_t* __restrict__ prim_parent, int32_t* __restrict__ node_parent,
-                       int32_t* __restrict__ starts, int* __restrict__ starts_n) {
+                       int32_t* __restrict__ starts, int* __restrict__ starts_n, int reach_list = 0) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n - 1;
   bool start = false;
@@ -170,7 +172,7 @@ __global__ void k_emit(const uint32_t* __restrict__ keys, int n, int leaf_max, B
     else node_parent[gamma] = (i << 1) | 0;
     if (last == gamma + 1) prim_parent[gamma + 1] = (i << 1) | 1;
     else node_parent[gamma + 1] = (i << 1) | 1;
-    start = (i == 0 || dd.w > leaf_max) && (dd.x < 0 || dd.y < 0);
+    start = (i == 0 || dd.w > leaf_max) && (reach_list || dd.x < 0 || dd.y < 0);
   }
   // warp-aggregated append
   const unsigned m = __ballot_sync(0xffffffffu, start);
@@ -400,12 +402,15 @@ __device__ __forceinline__ FBox seg_query(const TBox* __restrict__ seg, const TB
 }
 
 // Both child boxes of every reachable node (root, or range > leaf_max).
+// One thread per reachable node, from emit's compacted list (full warps of
+// range queries instead of one active lane in three).
 __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restrict__ tbox, int N, int n, int leaf_max,
-                             BNode* __restrict__ nodes, float* __restrict__ root_box) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n - 1) return;
+                             BNode* __restrict__ nodes, float* __restrict__ root_box,
+                             const int32_t* __restrict__ reach, const int* __restrict__ reach_n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= *reach_n) return;
+  const int i = reach[j];
   const int4 d = nodes[i].d;
-  if (i != 0 && d.w <= leaf_max) return;  // inside a leaf range: never referenced
   int gamma;
   if (d.x >= 0) {
     gamma = d.x;
@@ -421,22 +426,41 @@ __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restric
   unsigned l1 = static_cast<unsigned>(d.z) + uN, h1 = static_cast<unsigned>(gamma) + uN + 1;
   unsigned l2 = h1, h2 = static_cast<unsigned>(d.z + d.w) + uN;
   auto ld = [&](unsigned j) { return j >= uN ? fbox_load(tbox + (j - uN)) : fbox_load(seg + j); };
+  // two levels per iteration: their (up to 8) loads depend only on index
+  // arithmetic, so all are in flight before the first union
   while (l1 < h1 || l2 < h2) {
     const bool a = l1 < h1 && (l1 & 1), b = l1 < h1 && (h1 & 1);
     const bool c = l2 < h2 && (l2 & 1), e = l2 < h2 && (h2 & 1);
-    FBox xa = fbox_empty(), xb = fbox_empty(), xc = fbox_empty(), xe = fbox_empty();
-    if (a) xa = ld(l1);
-    if (b) xb = ld(h1 - 1);
-    if (c) xc = ld(l2);
-    if (e) xe = ld(h2 - 1);
-    fbox_union(L, xa);
-    fbox_union(L, xb);
-    fbox_union(R, xc);
-    fbox_union(R, xe);
+    const unsigned ja = l1, jb = h1 - 1, jc = l2, je = h2 - 1;
     l1 = (l1 + a) >> 1;
     h1 = (h1 - b) >> 1;
     l2 = (l2 + c) >> 1;
     h2 = (h2 - e) >> 1;
+    const bool a2 = l1 < h1 && (l1 & 1), b2 = l1 < h1 && (h1 & 1);
+    const bool c2 = l2 < h2 && (l2 & 1), e2 = l2 < h2 && (h2 & 1);
+    const unsigned ja2 = l1, jb2 = h1 - 1, jc2 = l2, je2 = h2 - 1;
+    l1 = (l1 + a2) >> 1;
+    h1 = (h1 - b2) >> 1;
+    l2 = (l2 + c2) >> 1;
+    h2 = (h2 - e2) >> 1;
+    FBox xa = fbox_empty(), xb = fbox_empty(), xc = fbox_empty(), xe = fbox_empty();
+    FBox ya = fbox_empty(), yb = fbox_empty(), yc = fbox_empty(), ye = fbox_empty();
+    if (a) xa = ld(ja);
+    if (b) xb = ld(jb);
+    if (c) xc = ld(jc);
+    if (e) xe = ld(je);
+    if (a2) ya = ld(ja2);
+    if (b2) yb = ld(jb2);
+    if (c2) yc = ld(jc2);
+    if (e2) ye = ld(je2);
+    fbox_union(L, xa);
+    fbox_union(L, xb);
+    fbox_union(R, xc);
+    fbox_union(R, xe);
+    fbox_union(L, ya);
+    fbox_union(L, yb);
+    fbox_union(R, yc);
+    fbox_union(R, ye);
   }
   store_child_box(&nodes[i], 0, L);
   store_child_box(&nodes[i], 1, R);
@@ -688,12 +712,14 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   if (n > 1) {
     MFB_CUDA_TRY(cudaMemsetAsync(starts_n, 0, sizeof(int), s));
     k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent, starts,
-                                          starts_n);
+                                          starts_n, use_seg ? 1 : 0);
     ctx.count_launch();
   }
   if (rs != s) MFB_CUDA_TRY(cudaStreamWaitEvent(s, ctx.ljoin, 0));
   if (seg) {
-    k_node_boxes<<<div_up(n - 1, T), T, 0, s>>>(seg, out.tbox, N, n, leaf_max, out.nodes, out.root_box_dev);
+    // (grid for every internal node; threads past the device count exit)
+    k_node_boxes<<<div_up(n - 1, T), T, 0, s>>>(seg, out.tbox, N, n, leaf_max, out.nodes, out.root_box_dev,
+                                                    starts, starts_n);
   } else if (n > 1) {
     // starts <= leaf ranges <= n; threads past the device count exit at once
     k_refit_ranges<<<div_up(n, T), T, 0, s>>>(out.tbox, out.nodes, starts, starts_n, out.nodes,
