@@ -288,6 +288,8 @@ __device__ __forceinline__ FBox fbox_load(const TBox* p) {  // one 256-bit read-
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=f"(r.mn[0]), "=f"(r.mn[1]), "=f"(r.mn[2]), "=f"(r.mx[0]), "=f"(r.mx[1]), "=f"(r.mx[2]), "=f"(p0), "=f"(p1)
       : "l"(p));
+  (void)p0;
+  (void)p1;
   return r;
 }
 __device__ __forceinline__ void fbox_store(TBox* p, const FBox& r) {
@@ -381,27 +383,6 @@ __global__ void __launch_bounds__(1024) k_seg_up(TBox* __restrict__ seg, int L) 
   seg_reduce_block(box, static_cast<unsigned>(L + blockIdx.x * 1024), min(1024, L), seg, sm);
 }
 
-// Union of leaf-order triangles [a, b] (inclusive) from the segment tree.
-__device__ __forceinline__ FBox seg_query(const TBox* __restrict__ seg, const TBox* __restrict__ tbox, unsigned N,
-                                          int a, int b) {
-  FBox r = fbox_empty();
-  unsigned l = static_cast<unsigned>(a) + N, h = static_cast<unsigned>(b) + N + 1;
-  while (l < h) {
-    if (l & 1) {
-      fbox_union(r, l >= N ? fbox_load(tbox + (l - N)) : fbox_load(seg + l));
-      ++l;
-    }
-    if (h & 1) {
-      --h;
-      fbox_union(r, h >= N ? fbox_load(tbox + (h - N)) : fbox_load(seg + h));
-    }
-    l >>= 1;
-    h >>= 1;
-  }
-  return r;
-}
-
-// Both child boxes of every reachable node (root, or range > leaf_max).
 // One thread per reachable node, from emit's compacted list (full warps of
 // range queries instead of one active lane in three).
 __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restrict__ tbox, int N, int n, int leaf_max,
