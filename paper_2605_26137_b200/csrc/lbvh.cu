@@ -282,16 +282,16 @@ __device__ __forceinline__ void fbox_union(FBox& a, const FBox& b) {
     a.mx[k] = fmaxf(a.mx[k], b.mx[k]);
   }
 }
+#pragma nv_diag_suppress 550  // the load's two padding lanes are not used
 __device__ __forceinline__ FBox fbox_load(const TBox* p) {  // one 256-bit read-only load
   FBox r;
   float p0, p1;
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=f"(r.mn[0]), "=f"(r.mn[1]), "=f"(r.mn[2]), "=f"(r.mx[0]), "=f"(r.mx[1]), "=f"(r.mx[2]), "=f"(p0), "=f"(p1)
       : "l"(p));
-  (void)p0;
-  (void)p1;
   return r;
 }
+#pragma nv_diag_default 550
 __device__ __forceinline__ void fbox_store(TBox* p, const FBox& r) {
   p->a = make_float4(r.mn[0], r.mn[1], r.mn[2], r.mx[0]);
   p->b = make_float4(r.mx[1], r.mx[2], 0.f, 0.f);
