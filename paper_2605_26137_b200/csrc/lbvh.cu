@@ -383,6 +383,9 @@ __global__ void __launch_bounds__(1024) k_seg_up(TBox* __restrict__ seg, int L) 
   seg_reduce_block(box, static_cast<unsigned>(L + blockIdx.x * 1024), min(1024, L), seg, sm);
 }
 
+#ifndef MFB_NODEBOX_LEVELS
+#define MFB_NODEBOX_LEVELS 2
+#endif
 // One thread per reachable node, from emit's compacted list (full warps of
 // range queries instead of one active lane in three).
 __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restrict__ tbox, int N, int n, int leaf_max,
@@ -407,41 +410,39 @@ __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restric
   unsigned l1 = static_cast<unsigned>(d.z) + uN, h1 = static_cast<unsigned>(gamma) + uN + 1;
   unsigned l2 = h1, h2 = static_cast<unsigned>(d.z + d.w) + uN;
   auto ld = [&](unsigned j) { return j >= uN ? fbox_load(tbox + (j - uN)) : fbox_load(seg + j); };
-  // two levels per iteration: their (up to 8) loads depend only on index
-  // arithmetic, so all are in flight before the first union
+  // MFB_NODEBOX_LEVELS levels per iteration: their (up to 4 per level) loads
+  // depend only on index arithmetic, so all are in flight before the first union
+  constexpr int kLv = MFB_NODEBOX_LEVELS;
   while (l1 < h1 || l2 < h2) {
-    const bool a = l1 < h1 && (l1 & 1), b = l1 < h1 && (h1 & 1);
-    const bool c = l2 < h2 && (l2 & 1), e = l2 < h2 && (h2 & 1);
-    const unsigned ja = l1, jb = h1 - 1, jc = l2, je = h2 - 1;
-    l1 = (l1 + a) >> 1;
-    h1 = (h1 - b) >> 1;
-    l2 = (l2 + c) >> 1;
-    h2 = (h2 - e) >> 1;
-    const bool a2 = l1 < h1 && (l1 & 1), b2 = l1 < h1 && (h1 & 1);
-    const bool c2 = l2 < h2 && (l2 & 1), e2 = l2 < h2 && (h2 & 1);
-    const unsigned ja2 = l1, jb2 = h1 - 1, jc2 = l2, je2 = h2 - 1;
-    l1 = (l1 + a2) >> 1;
-    h1 = (h1 - b2) >> 1;
-    l2 = (l2 + c2) >> 1;
-    h2 = (h2 - e2) >> 1;
-    FBox xa = fbox_empty(), xb = fbox_empty(), xc = fbox_empty(), xe = fbox_empty();
-    FBox ya = fbox_empty(), yb = fbox_empty(), yc = fbox_empty(), ye = fbox_empty();
-    if (a) xa = ld(ja);
-    if (b) xb = ld(jb);
-    if (c) xc = ld(jc);
-    if (e) xe = ld(je);
-    if (a2) ya = ld(ja2);
-    if (b2) yb = ld(jb2);
-    if (c2) yc = ld(jc2);
-    if (e2) ye = ld(je2);
-    fbox_union(L, xa);
-    fbox_union(L, xb);
-    fbox_union(R, xc);
-    fbox_union(R, xe);
-    fbox_union(L, ya);
-    fbox_union(L, yb);
-    fbox_union(R, yc);
-    fbox_union(R, ye);
+    bool take[kLv][4];
+    unsigned at[kLv][4];
+#pragma unroll
+    for (int v = 0; v < kLv; ++v) {
+      take[v][0] = l1 < h1 && (l1 & 1);
+      take[v][1] = l1 < h1 && (h1 & 1);
+      take[v][2] = l2 < h2 && (l2 & 1);
+      take[v][3] = l2 < h2 && (h2 & 1);
+      at[v][0] = l1;
+      at[v][1] = h1 - 1;
+      at[v][2] = l2;
+      at[v][3] = h2 - 1;
+      l1 = (l1 + take[v][0]) >> 1;
+      h1 = (h1 - take[v][1]) >> 1;
+      l2 = (l2 + take[v][2]) >> 1;
+      h2 = (h2 - take[v][3]) >> 1;
+    }
+    FBox x[kLv][4];
+#pragma unroll
+    for (int v = 0; v < kLv; ++v)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[v][k] = take[v][k] ? ld(at[v][k]) : fbox_empty();
+#pragma unroll
+    for (int v = 0; v < kLv; ++v) {
+      fbox_union(L, x[v][0]);
+      fbox_union(L, x[v][1]);
+      fbox_union(R, x[v][2]);
+      fbox_union(R, x[v][3]);
+    }
   }
   store_child_box(&nodes[i], 0, L);
   store_child_box(&nodes[i], 1, R);
