@@ -1221,12 +1221,14 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     int lo_prio = 0, hi_prio = 0;
     MFB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, prio ? hi_prio : lo_prio));
-    // MFB_PRIO_MODE=2: the lowpoly branch streams (wedge frames, reliability,
-    // raster) high as well (measured 1.52 vs 1.505 ms: the LBVH then ends last);
-    // default 1: only the LBVH streams high
+    // Default (2): the lowpoly branch streams (wedge frames, reliability,
+    // raster) high as well as the LBVH's; the dense normals stay low. With
+    // the segment-tree LBVH the lowpoly branch is the longer chain: 1.431 ->
+    // 1.401 ms (with the refit climb it was the reverse: 1.52 vs 1.505 ms).
+    // MFB_PRIO_MODE=1: only the LBVH streams high.
     static const int mode = [] {
       const char* e = std::getenv("MFB_PRIO_MODE");
-      return e ? std::atoi(e) : 1;
+      return e ? std::atoi(e) : 2;
     }();
     const int low_branch = (prio && mode == 2) ? hi_prio : lo_prio;
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux, cudaStreamNonBlocking, low_branch));
