@@ -81,8 +81,8 @@ typedef struct mf_bake_stats {
   int64_t valid_texels;   /* N_v: texels whose centre lies in a UV triangle */
   int64_t queries;        /* N_q: valid and reliable texels (closest-point queries) */
   int64_t hits;           /* queries that found a surface within maxDist */
-  int32_t bvh_nodes;      /* LBVH node count (2F - 1) */
-  int32_t bvh_depth;      /* deepest leaf */
+  int32_t bvh_nodes;      /* internal LBVH nodes of the dense tree (F - 1, binary Karras tree) */
+  int32_t bvh_depth;      /* 0: the bake does not measure it (mf_bvh_info reports a tree's depth) */
   /* device time per stage in milliseconds (CUDA events on the ctx stream);
    * only filled when mf_ctx_set_timing(ctx, 1) was called. */
   float ms_upload;        /* H2D of the meshes (host entry points only) */
@@ -90,7 +90,8 @@ typedef struct mf_bake_stats {
   float ms_bvh;           /* LBVH build (Morton, sort, emit, refit, repack) */
   float ms_raster;        /* G-buffer rasterisation */
   float ms_transfer;      /* closest-point transfer + RGB8 encode */
-  float ms_dilate;        /* seam dilation */
+  float ms_dilate;        /* seam dilation: the dilation-links kernel of the fused full-atlas
+                           * bake (its copies ride on the transfer), else the dilation pass */
   float ms_download;      /* D2H of the result (host entry points only) */
   float ms_total;
 } mf_bake_stats;
@@ -159,9 +160,16 @@ int mf_coverage_rows(mf_ctx* ctx, mf_mesh* lowpoly, int resolution, int64_t* row
 
 /* ---- BVH (spatial/bvh.h:30-69) ----------------------------------------- */
 /* Bvh::Bvh (bvh.cpp:48-61): validates and builds an LBVH on the device.
- * The mesh must outlive the tree, as in the reference (bvh.h:27). */
+ * The mesh must outlive the tree, as in the reference (bvh.h:27). The tree
+ * owns its arrays, query scratch and stream: it may outlive `ctx`, and its
+ * queries are safe from several host threads at once (they serialise on a
+ * per-tree lock), as the reference's const queries are (bvh.h:28). */
 int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out);
 void mf_bvh_destroy(mf_bvh* bvh);
+/* Stream the tree's queries run on (null = the tree's own stream). Default:
+ * the building context's stream if the caller supplied it at mf_ctx_create,
+ * else the tree's own. Device-pointer inputs must be ready on that stream. */
+int mf_bvh_set_stream(mf_bvh* bvh, void* stream);
 /* Node count, leaf count, max depth. */
 int mf_bvh_info(const mf_bvh* bvh, int32_t* nodes, int32_t* leaves, int32_t* depth);
 /* Export in the reference's Node layout (bvh.h:32-39): per node

@@ -81,6 +81,7 @@ SIGNATURES = [
     ("mf_coverage_rows", _I, [_VP, _VP, _I, _VP]),
     ("mf_bvh_build", _I, [_VP, _VP, ctypes.POINTER(_VP)]),
     ("mf_bvh_destroy", None, [_VP]),
+    ("mf_bvh_set_stream", ctypes.c_int, [_VP, _VP]),
     ("mf_bvh_info", _I, [_VP, _VP, _VP, _VP]),
     ("mf_bvh_export", _I, [_VP, _VP, _VP, _VP]),
     ("mf_bvh_closest_within", _I, [_VP, _VP, _I64, _D, _VP, _VP, _VP, _VP]),

@@ -44,6 +44,7 @@ struct Ctx {
   cudaEvent_t dfork = nullptr, djoin = nullptr;  // host entry point: dense phase side -> aux -> side
   cudaEvent_t up_fork = nullptr, up_join = nullptr;  // split H2D of one mesh over two streams
   bool timing = false;
+  bool capturing = false;  // a graph capture of this context's streams is open
   int64_t launches = 0;
   struct Buf {
     void* ptr = nullptr;
@@ -88,6 +89,7 @@ struct Ctx {
     uint64_t gen = 0, prev_gen = ~0ull;
   };
   GraphSlot g_low, g_dense;
+  void invalidate_graphs();  // drop every captured graph and capture key
   ~Ctx();
 };
 
@@ -121,7 +123,14 @@ constexpr int kLeafMax = 4;     // reference leaf size (bvh.cpp:13)
 // LBVH leaf-range cap used by default: results do not depend on the tree, and
 // 3 measured ~3% faster than 4 in the config-B walk (2: -2.5%, 4: 0, BVH4: +3%).
 constexpr int kLeafMaxDefault = 3;
-constexpr int kStackMax = 64;   // >= max Karras depth over 30-bit Morton + 32-bit index keys (62)
+constexpr int kMaxFaces = 1 << 27;  // leaf refs encode first < 2^27 (leaf_ref)
+// Traversal stacks (one entry per level at most). Karras emission over
+// (30-bit Morton, index) keys: along a root-to-leaf path the split deltas
+// strictly increase, and they range over the 30 Morton bits plus the
+// ceil(log2 F) <= 27 index bits, so depth <= 30 + 27 + 1 (lbvh_layout rejects
+// F >= kMaxFaces).
+constexpr int kStackMax = 64;
+static_assert(kStackMax >= 30 + 27 + 1, "traversal stack must cover the deepest Karras tree");
 
 struct alignas(16) BNode {
   float4 a;  // L.min.x L.min.y L.min.z L.max.x

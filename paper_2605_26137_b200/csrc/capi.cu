@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -34,6 +35,7 @@ void set_last_error(const std::string& m) { g_last_error = m; }
 void* Ctx::buf(const std::string& name, size_t bytes) {
   Buf& b = scratch[name];
   if (b.bytes < bytes) {
+    if (capturing) throw CaptureRealloc{};
     if (b.ptr) {
       // the streams may still use the old buffer; free after they drain
       sync_all();
@@ -55,6 +57,7 @@ void* Ctx::buf(const std::string& name, size_t bytes) {
 void* Ctx::host_buf(const std::string& name, size_t bytes) {
   Buf& b = pinned[name];
   if (b.bytes < bytes) {
+    if (capturing) throw CaptureRealloc{};
     if (b.ptr) {
       MFB_CUDA_TRY(cudaStreamSynchronize(stream));
       MFB_CUDA_TRY(cudaFreeHost(b.ptr));
@@ -85,6 +88,7 @@ void* Ctx::cub_temp(size_t bytes, cudaStream_t s) {
   void*& p = cub_tmp[slot];
   size_t& n = cub_tmp_bytes[slot];
   if (n < bytes) {
+    if (capturing) throw CaptureRealloc{};
     if (p) {
       sync_all();
       MFB_CUDA_TRY(cudaFree(p));
@@ -103,6 +107,19 @@ cudaEvent_t Ctx::pool_event(int i) {
     ev_pool.push_back(e);
   }
   return ev_pool[i];
+}
+
+void Ctx::invalidate_graphs() {
+  if (bake_exec) cudaGraphExecDestroy(bake_exec);
+  bake_exec = nullptr;
+  bake_key.clear();
+  bake_prev_key.clear();
+  for (GraphSlot* g : {&g_low, &g_dense}) {
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    g->exec = nullptr;
+    g->key.clear();
+    g->prev_key.clear();
+  }
 }
 
 Ctx::~Ctx() {
@@ -181,7 +198,8 @@ struct mf_ctx {
 };
 
 struct mf_mesh {
-  mf_ctx* ctx = nullptr;
+  mf_ctx* ctx = nullptr;  // the creating context (not used after creation)
+  int device = 0;
   DevMesh m;
   void* mem = nullptr;
   int status = MF_OK;  // validateMesh outcome (reference order)
@@ -193,10 +211,19 @@ struct mf_mesh {
   }
 };
 
+// A built tree owns everything its queries touch: the tree arrays, its own
+// query scratch and stream (`store`), and a mutex, so const queries from
+// several host threads are safe (bvh.h:28) and the tree outlives the context
+// (and host thread) that built it. Queries run on `qstream`: the building
+// context's stream when that one was supplied by the caller (so device-input
+// queries stay ordered with the caller's work), else the tree's own stream;
+// mf_bvh_set_stream overrides it.
 struct mf_bvh {
-  mf_ctx* ctx = nullptr;
+  int device = 0;
   mf_mesh* mesh = nullptr;
-  Ctx store;  // owns the tree's device arrays
+  Ctx store;  // owns the tree's device arrays, query scratch and stream
+  cudaStream_t qstream = nullptr;
+  std::mutex mu;
   Lbvh bvh;
   // host export cache
   bool exported = false;
@@ -234,6 +261,24 @@ template <typename F>
 int guarded(mf_ctx* ctx, F&& fn) {
   try {
     if (ctx) MFB_CUDA_TRY(cudaSetDevice(ctx->c.device));
+    return fn();
+  } catch (const ApiError& e) {
+    return fail(e.code, e.msg);
+  } catch (const CudaFailure& e) {
+    return fail(MF_ERR_CUDA, std::string("cuda: ") + cudaGetErrorString(e.err) + " at " + e.file + ":" +
+                                 std::to_string(e.line) + " (" + e.expr + ")");
+  } catch (const std::bad_alloc&) {
+    return fail(MF_ERR_OUT_OF_MEMORY, "device or host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(MF_ERR_CUDA, e.what());
+  }
+}
+
+// guarded() for handles that outlive their context (meshes, trees)
+template <typename F>
+int guarded_dev(int device, F&& fn) {
+  try {
+    MFB_CUDA_TRY(cudaSetDevice(device));
     return fn();
   } catch (const ApiError& e) {
     return fail(e.code, e.msg);
@@ -439,9 +484,12 @@ QueryList query_list(Ctx& c, int64_t capacity) {
 
 // Everything the fused bake enqueues; no host synchronisation inside, so
 // the same sequence can be captured into a CUDA graph.
+// Recorded in this order (the graph-timing path rebuilds them from the pool
+// indices): side0 side1 e0 e1 d0 d1 e2 e3 e4 e5. d0/d1 bracket the dilation
+// links kernel (empty when the bake dilates after the transfer, e4/e5).
 struct BakeMarks {
-  cudaEvent_t side0 = nullptr, side1 = nullptr, e0 = nullptr, e1 = nullptr, e2 = nullptr, e3 = nullptr,
-              e4 = nullptr, e5 = nullptr;
+  cudaEvent_t side0 = nullptr, side1 = nullptr, e0 = nullptr, e1 = nullptr, d0 = nullptr, d1 = nullptr,
+              e2 = nullptr, e3 = nullptr, e4 = nullptr, e5 = nullptr;
 };
 
 // Runs `body` (work enqueued on `s`, possibly forking/joining other streams)
@@ -457,20 +505,26 @@ void run_graphed(Ctx& c, Ctx::GraphSlot& slot, cudaStream_t s, const std::vector
   if (allow && key == slot.prev_key && c.alloc_gen == slot.prev_gen) {
     cudaGraph_t graph = nullptr;
     MFB_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    c.capturing = true;
     try {
       body();
+    } catch (const CaptureRealloc&) {  // scratch had to grow: discard, run eagerly
+      c.capturing = false;
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      (void)cudaGetLastError();
+      body();
+      slot.prev_key = key;
+      slot.prev_gen = c.alloc_gen;
+      return;
     } catch (...) {
+      c.capturing = false;
       cudaStreamEndCapture(s, &graph);
       if (graph) cudaGraphDestroy(graph);
       throw;
     }
+    c.capturing = false;
     MFB_CUDA_TRY(cudaStreamEndCapture(s, &graph));
-    if (c.alloc_gen != slot.prev_gen) {
-      cudaGraphDestroy(graph);
-      slot.prev_gen = c.alloc_gen;
-      body();
-      return;
-    }
     if (slot.exec) cudaGraphExecDestroy(slot.exec);
     slot.exec = nullptr;
     MFB_CUDA_TRY(cudaGraphInstantiateWithFlags(&slot.exec, graph, cudaGraphInstantiateFlagUseNodePriority));
@@ -552,7 +606,6 @@ struct BakeEnq {
   // raster and transfer write straight into rgb_out, the gutter texels are
   // filled by dilate_links (constant sources) and by the transfer's epilogue
   // (query sources), and no dilation pass follows the transfer.
-  // MFB_DILATE_LINKS=0 keeps the post-transfer k_dilate_fused (A/B).
   bool links = false;
   int* dep_next = nullptr;
   // host-buffer path: row bands of the atlas downloaded while the transfer
@@ -574,11 +627,7 @@ struct BakeEnq {
     // flags: [0] AtlasOverlap, [1] bin overflow, [2] bin total, [3] query overflow
     flags = c.buf<int>("bake.flags", 4);
     counters = c.buf<unsigned long long>("bake.counters", 4);
-    static const bool links_env = [] {
-      const char* e = std::getenv("MFB_DILATE_LINKS");
-      return !(e && e[0] == '0');
-    }();
-    links = links_env && !pub && rb == 0 && re == res && dilate_links_supported(radius) && raster_links_supported();
+    links = !pub && rb == 0 && re == res && dilate_links_supported(radius) && raster_links_supported();
     fo.rgb = links ? rgb_out : c.buf<uint8_t>("bake.raw", 3 * g.texels());
     fo.q = query_list(c, g.texels());
     if (links) {
@@ -617,18 +666,16 @@ struct BakeEnq {
     prepare_lowpoly(c, s, lo->m, res, plan);
     mk.e1 = tm.mark(s);
     // the dilation links run beside the interpolation kernel (both need only
-    // the coverage kernel's outputs); MFB_LINKS_FORK=0 keeps them in line
-    static const bool links_fork = [] {
-      const char* e = std::getenv("MFB_LINKS_FORK");
-      return !(e && e[0] == '0');
-    }();
-    cudaStream_t ls = links && links_fork && c.aux2 ? c.aux2 : nullptr;
+    // the coverage kernel's outputs)
+    cudaStream_t ls = links && c.aux2 ? c.aux2 : nullptr;
     fo.cover_done = ls ? c.pool_event(60) : nullptr;
     raster_gbuffer(c, s, lo->m, plan, g, flags, nullptr, &fo);
+    cudaStream_t t = ls ? ls : s;
+    if (ls) MFB_CUDA_TRY(cudaStreamWaitEvent(ls, fo.cover_done, 0));
+    mk.d0 = tm.mark(t);
+    if (links) dilate_links(c, t, res, g.valid, radius, fo.qslot, fo.dep_head, dep_next, rgb_out, fo.tile_state);
+    mk.d1 = tm.mark(t);
     if (links) {
-      cudaStream_t t = ls ? ls : s;
-      if (ls) MFB_CUDA_TRY(cudaStreamWaitEvent(ls, fo.cover_done, 0));
-      dilate_links(c, t, res, g.valid, radius, fo.qslot, fo.dep_head, dep_next, rgb_out, fo.tile_state);
       if (band_sync) band_init(c, t, bs);
       if (ls) {
         MFB_CUDA_TRY(cudaEventRecord(c.pool_event(61), ls));
@@ -691,11 +738,9 @@ struct BakeEnq {
   }
 
   // main stream, after both dense branches: transfer + dilation + flags
-  // With host_out (host-buffer entry point) the dilation runs in `bands` row
-  // bands and each band's D2H starts on aux2 as soon as it is dilated, so the
-  // download overlaps the remaining dilation; the main stream then waits for
-  // the last copy.
-  void tail(int* hflags_pinned, unsigned long long* hcnt_pinned, uint8_t* host_out = nullptr, int bands = 1) {
+  // With host_out (host-buffer entry point) and the dilation links, the atlas
+  // downloads in row bands on aux2 while the transfer runs (BandSync).
+  void tail(int* hflags_pinned, unsigned long long* hcnt_pinned, uint8_t* host_out = nullptr) {
     cudaStream_t s = c.stream;
     MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join, 0));
     MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join3, 0));
@@ -723,13 +768,7 @@ struct BakeEnq {
       // each band's download waits (on cp) for its ready flag, set by the
       // transfer's warps; the memset after the transfer releases every wait
       // regardless (by then every band is final), so no wait outlives it
-      // MFB_BAND_DIAG (diagnostic only, wrong results for 2): 1 = count in the
-      // transfer but copy after it; 2 = copy the bands without waiting
-      static const int band_diag = [] {
-        const char* e = std::getenv("MFB_BAND_DIAG");
-        return e ? std::atoi(e) : 0;
-      }();
-      if (band_diag != 2) ta.bands = bs;
+      ta.bands = bs;
       cudaEvent_t ev = c.pool_event(40);
       MFB_CUDA_TRY(cudaEventRecord(ev, s));
       transfer_normals(c, s, bvh, ta);
@@ -742,38 +781,12 @@ struct BakeEnq {
       }
       MFB_CUDA_TRY(cudaMemsetAsync(bs.ready, 1, bs.nb * sizeof(int), s));
       mk.e5 = tm.mark(s);
-      if (band_diag == 1) MFB_CUDA_TRY(cudaEventRecord(c.pool_event(41), s));
       MFB_CUDA_TRY(cudaStreamWaitEvent(cp, ev, 0));
-      // MFB_BAND_TRACE=1 (diagnostic): per-band copy start/end vs the transfer start
-      static const bool trace = std::getenv("MFB_BAND_TRACE") != nullptr;
-      cudaEvent_t tev[2 * kMaxBands + 2];
-      if (trace) {
-        for (int k = 0; k < 2 * bs.nb + 2; ++k) MFB_CUDA_TRY(cudaEventCreate(&tev[k]));
-        MFB_CUDA_TRY(cudaEventRecord(tev[2 * bs.nb], cp));
-      }
-      if (band_diag == 1) MFB_CUDA_TRY(cudaStreamWaitEvent(cp, c.pool_event(41), 0));
       for (int b = 0; b < bs.nb; ++b) {
         const int r0 = b * bs.rows, r1 = std::min(res, r0 + bs.rows);
-        if (band_diag != 2) stream_wait_value(cp, bs.ready + b);
-        if (trace) MFB_CUDA_TRY(cudaEventRecord(tev[2 * b], cp));
+        stream_wait_value(cp, bs.ready + b);
         const int64_t off = 3ll * r0 * res;
         MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off, 3ll * (r1 - r0) * res, cudaMemcpyDeviceToHost, cp));
-        if (trace) MFB_CUDA_TRY(cudaEventRecord(tev[2 * b + 1], cp));
-      }
-      if (trace) {
-        MFB_CUDA_TRY(cudaEventRecord(tev[2 * bs.nb + 1], s));
-        MFB_CUDA_TRY(cudaDeviceSynchronize());
-        float t;
-        std::fprintf(stderr, "[mfb bands] nb %d rows %d (ms from transfer start):", bs.nb, bs.rows);
-        for (int b = 0; b < bs.nb; ++b) {
-          cudaEventElapsedTime(&t, tev[2 * bs.nb], tev[2 * b]);
-          float t2;
-          cudaEventElapsedTime(&t2, tev[2 * bs.nb], tev[2 * b + 1]);
-          std::fprintf(stderr, " %d:%.3f-%.3f", b, t, t2);
-        }
-        cudaEventElapsedTime(&t, tev[2 * bs.nb], tev[2 * bs.nb + 1]);
-        std::fprintf(stderr, " transfer end %.3f\n", t);
-        for (int k = 0; k < 2 * bs.nb + 2; ++k) cudaEventDestroy(tev[k]);
       }
       MFB_CUDA_TRY(cudaEventRecord(c.join4, cp));
       MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join4, 0));
@@ -788,21 +801,6 @@ struct BakeEnq {
       mk.e5 = tm.mark(s);
       if (host_out)
         MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, 3ll * (re - rb) * res, cudaMemcpyDeviceToHost, s));
-    } else if (host_out && !pub && bands > 1 && cp != s) {
-      for (int b = 0; b < bands; ++b) {
-        const int r0 = rb + static_cast<int>(static_cast<int64_t>(re - rb) * b / bands);
-        const int r1 = rb + static_cast<int>(static_cast<int64_t>(re - rb) * (b + 1) / bands);
-        if (r1 <= r0) continue;
-        const int64_t off = 3ll * (r0 - rb) * res;
-        dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out + off, r0, r1 - r0);
-        cudaEvent_t ev = c.pool_event(40 + b);
-        MFB_CUDA_TRY(cudaEventRecord(ev, s));
-        MFB_CUDA_TRY(cudaStreamWaitEvent(cp, ev, 0));
-        MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off, 3ll * (r1 - r0) * res, cudaMemcpyDeviceToHost, cp));
-      }
-      mk.e5 = tm.mark(s);
-      MFB_CUDA_TRY(cudaEventRecord(c.join4, cp));
-      MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join4, 0));
     } else {
       if (pub) dilate_seams_to(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, *pub, rb, re - rb);
       else dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out, rb, re - rb);
@@ -822,32 +820,10 @@ void enqueue_bake(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double 
                   int rb, int re, uint8_t* rgb_out, bool debug, Timer& tm, BakeMarks& mk, int* hflags_pinned,
                   unsigned long long* hcnt_pinned, const OutSet* pub = nullptr) {
   BakeEnq q(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, debug, tm, mk, pub);
-  // MFB_DIAG_SKIP=bvh|low|normals: DIAGNOSTIC ONLY (critical-path analysis):
-  // reuse that phase's buffers from the previous (eager) call instead of
-  // recomputing them. Never set in a measured run.
-  static const std::string skip = [] {
-    const char* e = std::getenv("MFB_DIAG_SKIP");
-    return std::string(e ? e : "");
-  }();
-  static int calls = 0;
-  const bool reuse = !debug && ++calls > 2;  // the first calls build every buffer
   MFB_CUDA_TRY(cudaEventRecord(c.fork, c.stream));
-  if (skip == "bvh" && reuse) {
-    lbvh_layout(c, hi->m, q.bvh, "hi.bvh");
-    MFB_CUDA_TRY(cudaEventRecord(c.join, c.stream));
-  } else {
-    q.dense_bvh(c.fork);
-  }
-  if (!(skip == "low" && reuse)) q.low();
-  if (skip == "low" && reuse) {  // the transfer's batch cursor is reset by the raster
-    MFB_CUDA_TRY(cudaMemsetAsync(q.fo.q.count + 3, 0, sizeof(int), c.stream));
-  }
-  if (skip == "normals" && reuse) {
-    q.hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
-    MFB_CUDA_TRY(cudaEventRecord(c.join3, c.stream));
-  } else {
-    q.dense_normals(c.fork);
-  }
+  q.dense_bvh(c.fork);
+  q.low();
+  q.dense_normals(c.fork);
   q.tail(hflags_pinned, hcnt_pinned);
 }
 
@@ -881,23 +857,29 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
   int* hflags = static_cast<int*>(c.host_buf("bake.hflags", 4 * sizeof(int)));
   auto* hcnt = static_cast<unsigned long long*>(c.host_buf("bake.hcnt", 4 * sizeof(unsigned long long)));
   // graph key: everything baked into the captured sequence
+  // (the mesh handles' contents are immutable after upload: the ABI has no
+  // call that modifies an mf_mesh in place)
   struct Key {
     const void *lo, *hi, *out, *lo_mem, *hi_mem;
     int lo_nf, lo_nv, lo_nu, hi_nf, hi_nv, res, radius, rb, re, timing;
+    int64_t bin_capacity;
     double diag, frac;
-  } key{lo, hi, rgb_out, lo->mem, hi->mem, lo->m.nf, lo->m.nv, lo->m.nu, hi->m.nf, hi->m.nv, res, radius, rb, re,
-        c.timing ? 1 : 0, diag, frac};
-  std::vector<char> kb(reinterpret_cast<const char*>(&key), reinterpret_cast<const char*>(&key) + sizeof(key));
-  if (pub) {  // published bakes are keyed on their destination buffers too
-    const char* pb = reinterpret_cast<const char*>(pub);
-    kb.insert(kb.end(), pb, pb + sizeof(OutSet));
-  }
+  };
   const int s0 = std::max(0, rb - radius);
+  bool force_eager = false;
   for (int attempt = 0;; ++attempt) {
+    Key key{};
+    key = Key{lo, hi, rgb_out, lo->mem, hi->mem, lo->m.nf, lo->m.nv, lo->m.nu, hi->m.nf, hi->m.nv, res, radius, rb,
+              re, c.timing ? 1 : 0, c.bin_capacity, diag, frac};
+    std::vector<char> kb(reinterpret_cast<const char*>(&key), reinterpret_cast<const char*>(&key) + sizeof(key));
+    if (pub) {  // published bakes are keyed on their destination buffers too
+      const char* pb = reinterpret_cast<const char*>(pub);
+      kb.insert(kb.end(), pb, pb + sizeof(OutSet));
+    }
     HostTrace ht("bake_dev");
     BakeMarks mk;
     Timer t2(c, tm.next);
-    if (graphs && !debug && c.bake_exec && kb == c.bake_key && c.alloc_gen == c.bake_gen) {
+    if (graphs && !debug && !force_eager && c.bake_exec && kb == c.bake_key && c.alloc_gen == c.bake_gen) {
       MFB_CUDA_TRY(cudaGraphLaunch(c.bake_exec, s));
       // the graph recorded its marks on pool events tm.next .. tm.next + 7 in this order
       if (c.timing) {
@@ -906,27 +888,42 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
         mk.side1 = c.pool_event(i++);
         mk.e0 = c.pool_event(i++);
         mk.e1 = c.pool_event(i++);
+        mk.d0 = c.pool_event(i++);
+        mk.d1 = c.pool_event(i++);
         mk.e2 = c.pool_event(i++);
         mk.e3 = c.pool_event(i++);
         mk.e4 = c.pool_event(i++);
         mk.e5 = c.pool_event(i++);
       }
-    } else if (graphs && !debug && kb == c.bake_prev_key && c.alloc_gen == c.bake_prev_gen) {
+    } else if (graphs && !debug && !force_eager && kb == c.bake_prev_key && c.alloc_gen == c.bake_prev_gen) {
       // same shape as the previous eager run: every buffer exists -> capture
       cudaGraph_t graph = nullptr;
+      bool realloc = false;
       MFB_CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      c.capturing = true;
       try {
         enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, false, t2, mk, hflags, hcnt, pub);
+      } catch (const CaptureRealloc&) {  // scratch had to grow: discard the capture
+        realloc = true;
       } catch (...) {
+        c.capturing = false;
         cudaStreamEndCapture(s, &graph);
         if (graph) cudaGraphDestroy(graph);
         throw;
       }
-      MFB_CUDA_TRY(cudaStreamEndCapture(s, &graph));
-      if (c.alloc_gen != c.bake_prev_gen) {  // something allocated during capture: do not keep it
-        cudaGraphDestroy(graph);
-        c.bake_prev_gen = c.alloc_gen;
+      c.capturing = false;
+      if (realloc) {
+        cudaStreamEndCapture(s, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        graph = nullptr;
+        (void)cudaGetLastError();
+      } else {
+        MFB_CUDA_TRY(cudaStreamEndCapture(s, &graph));
+      }
+      if (realloc || c.alloc_gen != c.bake_prev_gen) {  // scratch changed: do not keep it, run eagerly
+        if (graph) cudaGraphDestroy(graph);
         enqueue_bake(c, lo, hi, res, diag, frac, radius, rb, re, rgb_out, false, t2, mk, hflags, hcnt, pub);
+        c.bake_prev_gen = c.alloc_gen;
       } else {
         if (c.bake_exec) cudaGraphExecDestroy(c.bake_exec);
         c.bake_exec = nullptr;
@@ -956,7 +953,8 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
     ht.mark("synced");
     if (hflags[1] && attempt == 0) {  // tile bins overflowed: rerun eagerly with the exact capacity
       c.bin_capacity = static_cast<int64_t>(hflags[2]) + 1;
-      c.bake_prev_key.clear();
+      c.invalidate_graphs();
+      force_eager = true;
       continue;
     }
     if (hflags[1] || hflags[3]) throw ApiError(MF_ERR_CUDA, "internal capacity overflow");
@@ -979,7 +977,8 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
         st->ms_raster = Timer::ms(mk.e1, mk.e2);
         st->ms_bvh = Timer::ms(mk.side0, mk.side1);
         st->ms_transfer = Timer::ms(mk.e3, mk.e4);
-        st->ms_dilate = Timer::ms(mk.e4, mk.e5);
+        // the dilation links kernel (fused full-atlas bake) or the dilation after the transfer
+        st->ms_dilate = Timer::ms(mk.d0, mk.d1) + Timer::ms(mk.e4, mk.e5);
         st->ms_total = Timer::ms(t_begin ? t_begin : mk.e0, mk.e5);
       }
     }
@@ -1026,11 +1025,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   MFB_CUDA_TRY(cudaEventRecord(c.fork, s));  // the caller's earlier work on the ctx stream
   auto upload_hi = [&] {
     MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.fork, 0));
-    static const bool split_h2d = [] {
-      const char* e = std::getenv("MFB_H2D_SPLIT");
-      return !(e && e[0] == '0');
-    }();
-    upload_mesh_async(c, c.side, hv, &hi, "up.hi", hup + 1, split_h2d && c.aux ? c.aux : nullptr);
+    upload_mesh_async(c, c.side, hv, &hi, "up.hi", hup + 1, c.aux ? c.aux : nullptr);
     MFB_CUDA_TRY(cudaEventRecord(c.hi_ready, c.side));
   };
   auto drain = [&] {
@@ -1052,13 +1047,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   BakeMarks mk;
   Timer tmb(c, 8);
   BakeEnq q(c, &lo, &hi, res, diag, frac, radius, 0, res, drgb, false, tmb, mk);
-  // MFB_E2E_BANDS=0: download the atlas after the transfer instead of in row
-  // bands while it runs (A/B)
-  static const bool band_env = [] {
-    const char* e = std::getenv("MFB_E2E_BANDS");
-    return !(e && e[0] == '0');
-  }();
-  if (q.links && band_env && host_pinned(rgb_out) && wait_value_usable(c)) {
+  if (q.links && host_pinned(rgb_out) && wait_value_usable(c)) {
     q.band_sync = true;
     int* bb = c.buf<int>("bake.bands", 4 * kMaxBands);
     q.bs.tot = bb;
@@ -1067,12 +1056,8 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     q.bs.ready = bb + 3 * kMaxBands;
     q.bs.res = res;
     // ~32 bands (64 rows at 2048^2): the copy left after the transfer is one
-    // small band. MFB_E2E_BAND_DIV overrides the count (A/B).
-    static const int band_div = [] {
-      const char* e = std::getenv("MFB_E2E_BAND_DIV");
-      const int v = e ? std::atoi(e) : 32;
-      return v >= 1 && v <= kMaxBands ? v : 32;
-    }();
+    // small band (16 or 64 bands measured 15-19 us slower end to end)
+    constexpr int band_div = 32;
     q.bs.rows = std::max((div_up(res, band_div) + 15) / 16 * 16, (radius + 15) / 16 * 16);
     q.bs.nb = div_up(res, q.bs.rows);
     const char* chk = std::getenv("MFB_BAND_CHECK");
@@ -1099,12 +1084,8 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   // behind the dense upload and its validation (which zeroes out-of-range
   // indices in the device copy), without a host round trip on the critical
   // path; the validation outcome is read after the bake, in the reference's
-  // error order. MFB_E2E_SPEC=0 waits for it first (A/B).
-  static const bool spec_env = [] {
-    const char* e = std::getenv("MFB_E2E_SPEC");
-    return !(e && e[0] == '0');
-  }();
-  const bool spec = spec_env && hv->n_faces > 0 && hv->n_vertices > 0 && diag > 0.0 && frac > 0.0 && radius >= 0;
+  // error order.
+  const bool spec = hv->n_faces > 0 && hv->n_vertices > 0 && diag > 0.0 && frac > 0.0 && radius >= 0;
   if (spec) {
     hi.status = MF_OK;  // provisional until the flags are read
   } else {
@@ -1121,15 +1102,8 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilation radius must be >= 0");
   }
   q.dense_side(use_graphs);
-  // MFB_E2E_DL_BANDS=k: dilate in k row bands, each downloaded as soon as it is
-  // done (measured within noise of one band at config B: 1 stays the default)
-  static const int dl_bands = [] {
-    const char* e = std::getenv("MFB_E2E_DL_BANDS");
-    const int v = e ? std::atoi(e) : 1;
-    return v >= 1 && v <= 16 ? v : 1;
-  }();
   cudaEvent_t t2 = tm.mark(s);
-  q.tail(hflags, hcnt, rgb_out, dl_bands);
+  q.tail(hflags, hcnt, rgb_out);
   cudaEvent_t t3 = tm.mark(s);
   MFB_CUDA_TRY(cudaStreamSynchronize(s));
   if (spec) {
@@ -1143,6 +1117,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     // tile bins overflowed on this shape: the device-mesh path re-runs with
     // the exact capacity (and keeps it for later calls)
     if (hflags[1]) c.bin_capacity = static_cast<int64_t>(hflags[2]) + 1;
+    c.invalidate_graphs();
     Timer tr(c, 8);
     bake_dev(c, &lo, &hi, res, diag, frac, radius, 0, res, drgb, nullptr, nullptr, st, tr, nullptr);
     MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, s));
@@ -1174,7 +1149,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
       st->ms_raster = Timer::ms(mk.e1, mk.e2);
       st->ms_bvh = Timer::ms(mk.side0, mk.side1);
       st->ms_transfer = Timer::ms(mk.e3, mk.e4);
-      st->ms_dilate = Timer::ms(mk.e4, mk.e5);
+      st->ms_dilate = Timer::ms(mk.d0, mk.d1) + Timer::ms(mk.e4, mk.e5);
       st->ms_download = Timer::ms(t2, t3);
       st->ms_total = Timer::ms(t0, t3);
     }
@@ -1213,28 +1188,17 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     }
     // the dense LBVH branch is the bake's longest pre-transfer chain: its
     // streams get the higher priority so the lowpoly branches fill in around it
-    // (MFB_LBVH_PRIORITY=0 disables)
-    static const bool prio = [] {
-      const char* e = std::getenv("MFB_LBVH_PRIORITY");
-      return !(e && e[0] == '0');
-    }();
     int lo_prio = 0, hi_prio = 0;
     MFB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, prio ? hi_prio : lo_prio));
-    // Default (2): the lowpoly branch streams (wedge frames, reliability,
-    // raster) high as well as the LBVH's; the dense normals stay low. With
-    // the segment-tree LBVH the lowpoly branch is the longer chain: 1.431 ->
+    // The lowpoly branch streams (wedge frames, reliability, raster) are high
+    // priority as well as the LBVH's; the dense normals stay low. With the
+    // segment-tree LBVH the lowpoly branch is the longer chain: 1.431 ->
     // 1.401 ms (with the refit climb it was the reverse: 1.52 vs 1.505 ms).
-    // MFB_PRIO_MODE=1: only the LBVH streams high.
-    static const int mode = [] {
-      const char* e = std::getenv("MFB_PRIO_MODE");
-      return e ? std::atoi(e) : 2;
-    }();
-    const int low_branch = (prio && mode == 2) ? hi_prio : lo_prio;
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux, cudaStreamNonBlocking, low_branch));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, prio ? hi_prio : lo_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, low_branch));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, low_branch));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, hi_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux, cudaStreamNonBlocking, hi_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, hi_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, hi_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, lo_prio));
     for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3, &ctx->c.hi_ready,
                             &ctx->c.dfork, &ctx->c.djoin, &ctx->c.up_fork, &ctx->c.up_join, &ctx->c.lfork,
@@ -1270,6 +1234,7 @@ int mf_mesh_upload(mf_ctx* ctx, const mf_mesh_view* view, mf_mesh** out) {
   return guarded(ctx, [&]() -> int {
     auto mesh = std::make_unique<mf_mesh>();
     mesh->ctx = ctx;
+    mesh->device = ctx->c.device;
     upload_mesh(ctx->c, ctx->c.stream, view, mesh.get());
     *out = mesh.release();
     return MF_OK;
@@ -1277,7 +1242,7 @@ int mf_mesh_upload(mf_ctx* ctx, const mf_mesh_view* view, mf_mesh** out) {
 }
 
 void mf_mesh_destroy(mf_mesh* mesh) {
-  if (mesh && mesh->ctx) cudaSetDevice(mesh->ctx->c.device);
+  if (mesh) cudaSetDevice(mesh->device);
   delete mesh;
 }
 
@@ -1402,12 +1367,8 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
   if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
   return guarded(ctx, [&]() -> int {
     Ctx& c = ctx->c;
-    // MFB_E2E_OVERLAP=0: the sequential upload -> bake -> download path (A/B)
-    static const bool overlap = [] {
-      const char* e = std::getenv("MFB_E2E_OVERLAP");
-      return !(e && e[0] == '0');
-    }();
-    if (overlap && !dbg_face && !dbg_ts) {
+    // debug outputs take the sequential upload -> bake -> download path
+    if (!dbg_face && !dbg_ts) {
       mf_bake_stats local{};
       bake_host_overlapped(c, ctx, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius, rgb_out,
                            &local);
@@ -1490,10 +1451,12 @@ int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
   return guarded(ctx, [&]() -> int {
     check_mesh(mesh);  // Bvh::Bvh calls validateMesh (bvh.cpp:49)
     auto b = std::make_unique<mf_bvh>();
-    b->ctx = ctx;
+    b->device = ctx->c.device;
     b->mesh = mesh;
     b->store.device = ctx->c.device;
-    b->store.stream = ctx->c.stream;  // only used to order frees
+    MFB_CUDA_TRY(cudaStreamCreateWithFlags(&b->store.stream, cudaStreamNonBlocking));
+    b->store.own_stream = true;
+    b->qstream = ctx->c.own_stream ? b->store.stream : ctx->c.stream;
     lbvh_build(ctx->c, ctx->c.stream, mesh->m, b->bvh, "bvh");
     // move the persistent arrays out of the context scratch into the handle
     const int nn = std::max(b->bvh.n_nodes, 1);
@@ -1514,16 +1477,24 @@ int mf_bvh_build(mf_ctx* ctx, mf_mesh* mesh, mf_bvh** out) {
     b->bvh.tbox = tbox;
     b->bvh.scene_acc = acc;
     b->bvh.root_box_dev = nullptr;
-    b->store.own_stream = false;
     *out = b.release();
     return MF_OK;
   });
 }
 
 void mf_bvh_destroy(mf_bvh* bvh) {
-  if (bvh && bvh->ctx) cudaSetDevice(bvh->ctx->c.device);
-  if (bvh) bvh->store.stream = nullptr;
+  if (bvh) cudaSetDevice(bvh->device);
   delete bvh;
+}
+
+int mf_bvh_set_stream(mf_bvh* bvh, void* stream) {
+  if (!bvh) return fail(MF_ERR_BAD_ARGUMENT, "bvh is null");
+  return guarded_dev(bvh->device, [&]() -> int {
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    MFB_CUDA_TRY(cudaStreamSynchronize(bvh->qstream));
+    bvh->qstream = stream ? static_cast<cudaStream_t>(stream) : bvh->store.stream;
+    return MF_OK;
+  });
 }
 
 namespace {
@@ -1581,7 +1552,8 @@ void export_bvh(mf_bvh* b) {
 int mf_bvh_info(const mf_bvh* bvh, int32_t* nodes, int32_t* leaves, int32_t* depth) {
   if (!bvh) return fail(MF_ERR_BAD_ARGUMENT, "bvh is null");
   mf_bvh* b = const_cast<mf_bvh*>(bvh);
-  return guarded(b->ctx, [&]() -> int {
+  return guarded_dev(b->device, [&]() -> int {
+    std::lock_guard<std::mutex> lk(b->mu);
     export_bvh(b);
     if (nodes) *nodes = static_cast<int32_t>(b->links.size() / 4);
     if (leaves) *leaves = b->leaves;
@@ -1592,7 +1564,8 @@ int mf_bvh_info(const mf_bvh* bvh, int32_t* nodes, int32_t* leaves, int32_t* dep
 
 int mf_bvh_export(mf_bvh* bvh, double* boxes, int32_t* links, int32_t* face_order) {
   if (!bvh) return fail(MF_ERR_BAD_ARGUMENT, "bvh is null");
-  return guarded(bvh->ctx, [&]() -> int {
+  return guarded_dev(bvh->device, [&]() -> int {
+    std::lock_guard<std::mutex> lk(bvh->mu);
     export_bvh(bvh);
     if (boxes) std::memcpy(boxes, bvh->boxes.data(), sizeof(double) * bvh->boxes.size());
     if (links) std::memcpy(links, bvh->links.data(), sizeof(int32_t) * bvh->links.size());
@@ -1604,10 +1577,12 @@ int mf_bvh_export(mf_bvh* bvh, double* boxes, int32_t* links, int32_t* face_orde
 int mf_bvh_closest_within_dev(mf_bvh* bvh, const double* q, int64_t n, double max_distance, int32_t* face,
                               double* dist_sq, double* point, double* bary) {
   if (!bvh || (n > 0 && (!q || !face || !dist_sq))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
-  return guarded(bvh->ctx, [&]() -> int {
-    Ctx& c = bvh->ctx->c;
-    closest_within(c, c.stream, bvh->bvh, q, n, max_distance, face, dist_sq, point, bary);
-    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  return guarded_dev(bvh->device, [&]() -> int {
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    Ctx& c = bvh->store;
+    const cudaStream_t qs = bvh->qstream;
+    closest_within(c, qs, bvh->bvh, q, n, max_distance, face, dist_sq, point, bary);
+    MFB_CUDA_TRY(cudaStreamSynchronize(qs));
     return MF_OK;
   });
 }
@@ -1615,21 +1590,23 @@ int mf_bvh_closest_within_dev(mf_bvh* bvh, const double* q, int64_t n, double ma
 int mf_bvh_closest_within(mf_bvh* bvh, const double* q, int64_t n, double max_distance, int32_t* face,
                           double* dist_sq, double* point, double* bary) {
   if (!bvh || (n > 0 && (!q || !face || !dist_sq))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
-  return guarded(bvh->ctx, [&]() -> int {
+  return guarded_dev(bvh->device, [&]() -> int {
     if (n <= 0) return MF_OK;
-    Ctx& c = bvh->ctx->c;
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    Ctx& c = bvh->store;
+    const cudaStream_t qs = bvh->qstream;
     double* dq = c.buf<double>("cp.q", 3 * n);
     int32_t* df = c.buf<int32_t>("cp.f", n);
     double* dd = c.buf<double>("cp.d", n);
     double* dp = c.buf<double>("cp.p", 3 * n);
     double* db = c.buf<double>("cp.b", 3 * n);
-    MFB_CUDA_TRY(cudaMemcpyAsync(dq, q, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
-    closest_within(c, c.stream, bvh->bvh, dq, n, max_distance, df, dd, dp, db);
-    MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaMemcpyAsync(dist_sq, dd, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
-    if (point) MFB_CUDA_TRY(cudaMemcpyAsync(point, dp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
-    if (bary) MFB_CUDA_TRY(cudaMemcpyAsync(bary, db, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dq, q, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, qs));
+    closest_within(c, qs, bvh->bvh, dq, n, max_distance, df, dd, dp, db);
+    MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dist_sq, dd, sizeof(double) * n, cudaMemcpyDeviceToHost, qs));
+    if (point) MFB_CUDA_TRY(cudaMemcpyAsync(point, dp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, qs));
+    if (bary) MFB_CUDA_TRY(cudaMemcpyAsync(bary, db, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaStreamSynchronize(qs));
     return MF_OK;
   });
 }
@@ -1637,10 +1614,12 @@ int mf_bvh_closest_within(mf_bvh* bvh, const double* q, int64_t n, double max_di
 int mf_bvh_raycast_first_dev(mf_bvh* bvh, const double* o, const double* d, int64_t n, double tmin, double tmax,
                              int32_t* face, double* t, double* u, double* v) {
   if (!bvh || (n > 0 && (!o || !d || !face || !t || !u || !v))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
-  return guarded(bvh->ctx, [&]() -> int {
-    Ctx& c = bvh->ctx->c;
-    raycast_first(c, c.stream, bvh->bvh, o, d, n, tmin, tmax, face, t, u, v);
-    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  return guarded_dev(bvh->device, [&]() -> int {
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    Ctx& c = bvh->store;
+    const cudaStream_t qs = bvh->qstream;
+    raycast_first(c, qs, bvh->bvh, o, d, n, tmin, tmax, face, t, u, v);
+    MFB_CUDA_TRY(cudaStreamSynchronize(qs));
     return MF_OK;
   });
 }
@@ -1648,23 +1627,25 @@ int mf_bvh_raycast_first_dev(mf_bvh* bvh, const double* o, const double* d, int6
 int mf_bvh_raycast_first(mf_bvh* bvh, const double* o, const double* d, int64_t n, double tmin, double tmax,
                          int32_t* face, double* t, double* u, double* v) {
   if (!bvh || (n > 0 && (!o || !d || !face || !t || !u || !v))) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
-  return guarded(bvh->ctx, [&]() -> int {
+  return guarded_dev(bvh->device, [&]() -> int {
     if (n <= 0) return MF_OK;
-    Ctx& c = bvh->ctx->c;
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    Ctx& c = bvh->store;
+    const cudaStream_t qs = bvh->qstream;
     double* dO = c.buf<double>("rc.o", 3 * n);
     double* dD = c.buf<double>("rc.d", 3 * n);
     int32_t* df = c.buf<int32_t>("rc.f", n);
     double* dt = c.buf<double>("rc.t", n);
     double* du = c.buf<double>("rc.u", n);
     double* dv = c.buf<double>("rc.v", n);
-    MFB_CUDA_TRY(cudaMemcpyAsync(dO, o, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
-    MFB_CUDA_TRY(cudaMemcpyAsync(dD, d, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, c.stream));
-    raycast_first(c, c.stream, bvh->bvh, dO, dD, n, tmin, tmax, df, dt, du, dv);
-    MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaMemcpyAsync(t, dt, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaMemcpyAsync(u, du, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaMemcpyAsync(v, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dO, o, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, qs));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dD, d, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, qs));
+    raycast_first(c, qs, bvh->bvh, dO, dD, n, tmin, tmax, df, dt, du, dv);
+    MFB_CUDA_TRY(cudaMemcpyAsync(face, df, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaMemcpyAsync(t, dt, sizeof(double) * n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaMemcpyAsync(u, du, sizeof(double) * n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaMemcpyAsync(v, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaStreamSynchronize(qs));
     return MF_OK;
   });
 }
@@ -1796,7 +1777,7 @@ BandGrid band_grid(Ctx& c, const mf_bvh* bvh, int res, double band_voxels, int d
   if (res < 8) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: grid resolution must be >= 8");
   if (dilate < 0) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilate radius must be >= 0");
   double box[6];
-  vertex_bounds(c, c.stream, bvh->mesh->m, box);  // bounds(mesh), mesh.cpp:12-16
+  vertex_bounds(c, bvh->qstream, bvh->mesh->m, box);  // bounds(mesh), mesh.cpp:12-16
   const int margin = dilate + 3;
   if (res - 2 * margin < 4)
     throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: grid resolution too small for the dilation margin");
@@ -1838,12 +1819,14 @@ extern "C" {
 int mf_surface_band_dev(mf_bvh* bvh, int resolution, double band_voxels, int dilate_radius, const double* domain,
                         uint8_t* labels_dev, float* distance_dev, double* grid_out) {
   if (!bvh || !labels_dev || !distance_dev) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
-  return guarded(bvh->ctx, [&]() -> int {
-    Ctx& c = bvh->ctx->c;
+  return guarded_dev(bvh->device, [&]() -> int {
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    Ctx& c = bvh->store;
+    const cudaStream_t qs = bvh->qstream;
     const BandGrid g = band_grid(c, bvh, resolution, band_voxels, dilate_radius, domain);
-    surface_band(c, c.stream, bvh->bvh, resolution, g.origin, g.h, g.truncation, g.band_world, labels_dev,
+    surface_band(c, qs, bvh->bvh, resolution, g.origin, g.h, g.truncation, g.band_world, labels_dev,
                  distance_dev);
-    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(qs));
     if (grid_out) {
       grid_out[0] = g.origin[0];
       grid_out[1] = g.origin[1];
@@ -1858,16 +1841,18 @@ int mf_surface_band_dev(mf_bvh* bvh, int resolution, double band_voxels, int dil
 int mf_surface_band(mf_bvh* bvh, int resolution, double band_voxels, int dilate_radius, const double* domain,
                     uint8_t* labels, float* distance, double* grid_out) {
   if (!bvh || !labels || !distance) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
-  return guarded(bvh->ctx, [&]() -> int {
-    Ctx& c = bvh->ctx->c;
+  return guarded_dev(bvh->device, [&]() -> int {
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    Ctx& c = bvh->store;
+    const cudaStream_t qs = bvh->qstream;
     const BandGrid g = band_grid(c, bvh, resolution, band_voxels, dilate_radius, domain);
     const int64_t n = static_cast<int64_t>(resolution) * resolution * resolution;
     uint8_t* dl = c.buf<uint8_t>("band.labels", n);
     float* dd = c.buf<float>("band.dist", n);
-    surface_band(c, c.stream, bvh->bvh, resolution, g.origin, g.h, g.truncation, g.band_world, dl, dd);
-    MFB_CUDA_TRY(cudaMemcpyAsync(labels, dl, n, cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaMemcpyAsync(distance, dd, sizeof(float) * n, cudaMemcpyDeviceToHost, c.stream));
-    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    surface_band(c, qs, bvh->bvh, resolution, g.origin, g.h, g.truncation, g.band_world, dl, dd);
+    MFB_CUDA_TRY(cudaMemcpyAsync(labels, dl, n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaMemcpyAsync(distance, dd, sizeof(float) * n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaStreamSynchronize(qs));
     if (grid_out) {
       grid_out[0] = g.origin[0];
       grid_out[1] = g.origin[1];
@@ -1949,20 +1934,10 @@ int mf_cast_visibility(mf_ctx* ctx, const mf_mesh_view* mesh, int viewpoints, in
     fibonacci_cameras(viewpoints, radius * 1.04, cams.data());
     auto* dh = c.buf<unsigned long long>("vis.hits", nf);
     MFB_CUDA_TRY(cudaMemsetAsync(dh, 0, sizeof(unsigned long long) * nf, c.stream));
-    // default: the reference's face-order rasteriser on the device (z-buffer
-    // of atomicMax keys); MFB_VIS_RAY=1: one pixel ray per thread through the LBVH
-    static const bool by_ray = [] {
-      const char* e = std::getenv("MFB_VIS_RAY");
-      return e && e[0] == '1';
-    }();
-    if (by_ray) {
-      Lbvh bvh;
-      lbvh_build(c, c.stream, cm, bvh, "vis.bvh");
-      render_views(c, c.stream, bvh, cams.data(), viewpoints, resolution, 0, dh, nullptr, nullptr, nullptr, nullptr,
-                   nullptr, nullptr);
-    } else {
-      raster_visibility(c, c.stream, cm, cams.data(), viewpoints, resolution, dh);
-    }
+    // the reference's face-order rasteriser on the device (z-buffer of
+    // atomicMax keys; 57 ms vs 431 ms for one pixel ray per thread through the
+    // LBVH at 512 views x 1024^2)
+    raster_visibility(c, c.stream, cm, cams.data(), viewpoints, resolution, dh);
     MFB_CUDA_TRY(cudaMemcpyAsync(hits, dh, sizeof(int64_t) * nf, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
     if (state)

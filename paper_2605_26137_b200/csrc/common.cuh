@@ -41,6 +41,11 @@ struct CudaFailure {
 };
 
 // A reference-code error (maps to 1 + ErrorCode across the ABI).
+// Thrown by Ctx::buf / cub_temp when a buffer must grow while a stream
+// capture is open (the old buffer cannot be freed without a sync): the
+// capturing code discards the capture and runs the sequence eagerly.
+struct CaptureRealloc {};
+
 struct ApiError {
   int code;
   std::string msg;

@@ -598,6 +598,11 @@ __global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __res
 
 void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag) {
   const int n = m.nf;
+  // leaf refs hold first < 2^27 (bake.cuh), which also bounds the traversal
+  // stacks: a root-to-leaf path's Karras deltas strictly increase over the 30
+  // Morton bits and the 27 index bits, so depth <= 58 < kStackMax
+  if (n >= kMaxFaces)
+    throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: the device LBVH supports fewer than 2^27 faces");
   out.n_tris = n;
   out.n_nodes = n > 1 ? n - 1 : 0;
   out.nodes = ctx.buf<BNode>(tag + ".nodes", out.n_nodes > 0 ? out.n_nodes : 1);

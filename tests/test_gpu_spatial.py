@@ -185,3 +185,59 @@ def test_surface_band_errors(gpu_ctx):
         with pytest.raises(MeshforgeError) as e:
             bvh.surface_band(*args)
         assert e.value.status == code
+
+
+def _deep_tree_mesh():
+    """Karras worst case: 20k copies of one triangle (identical Morton keys:
+    the hierarchy splits on index bits only) plus triangles whose centroids
+    halve their distance to the origin along every axis (Morton keys sharing
+    ever longer prefixes), so root-to-leaf paths run through both key parts."""
+    tris = []
+    base = np.array([[0.0, 0.0, 0.0], [1e-3, 0.0, 0.0], [0.0, 1e-3, 0.0]])
+    tris += [base] * 20000
+    for k in range(40):
+        s = 2.0 ** -k
+        tris.append(base * s + s)
+        tris.append(base * s - s)
+    pos = np.concatenate(tris, 0)
+    faces = np.arange(pos.shape[0], dtype=np.int32).reshape(-1, 3)
+    return TriangleMesh(pos, faces)
+
+
+def test_deep_degenerate_tree_matches_brute_force(gpu_ctx):
+    m = _deep_tree_mesh()
+    bvh = mf.Bvh(m)
+    _, _, depth = bvh.info()
+    assert 16 <= depth <= 58
+    rng = np.random.default_rng(5)
+    q = np.concatenate([rng.uniform(-1, 1, (3000, 3)), rng.uniform(-1e-3, 2e-3, (3000, 3))])
+    f, ds, pt, bary = bvh.closest_points(q)
+    bf, bd, bp, bb = brute_closest(gpu_ctx, m, q)
+    assert np.array_equal(f, bf) and np.array_equal(ds, bd)
+    assert np.array_equal(pt, bp) and np.array_equal(bary, bb)
+    d = rng.normal(size=(3000, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    rf, rt, _, _ = bvh.raycasts(q[:3000], d)
+    xf, xt, _, _ = brute_ray(gpu_ctx, m, q[:3000], d)
+    assert np.array_equal(rf, xf) and np.array_equal(rt[rf >= 0], xt[rf >= 0])
+
+
+def test_bvh_outlives_its_context_and_serves_threads(gpu_ctx):
+    """A tree built on a context stays usable after that context is destroyed
+    (it owns its arrays, scratch and stream), and concurrent const queries
+    from several host threads give the serial answers (bvh.h:28)."""
+    import concurrent.futures as cf
+
+    from paper_2605_26137_b200 import capi
+    m = fx.icosphere(5)
+    ctx = capi.Context(0)
+    bvh = mf.Bvh(m, ctx=ctx)
+    ctx.close()
+    rng = np.random.default_rng(9)
+    qs = [rng.uniform(-0.7, 0.7, (20000 + 1000 * i, 3)) for i in range(8)]
+    serial = [bvh.closest_points(q, 0.05) for q in qs]
+    with cf.ThreadPoolExecutor(max_workers=8) as pool:
+        par = list(pool.map(lambda q: bvh.closest_points(q, 0.05), qs))
+    for a, b in zip(serial, par):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
