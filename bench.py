@@ -1,31 +1,41 @@
 #!/usr/bin/env python
 """Benchmark: baked texels/s (+ BVH rays/s) of the fused B200 normal bake.
 
-Workload (BASELINE.json configs[1], "config B"): synthetic geodesic pair,
-dense G(224) = 1,003,520 faces -> lowpoly G(32) = 20,480 faces with a 20-chart
-UV atlas, 2048^2 atlas, maxDistanceFraction 0.01, dilation radius 4.
+Workloads (BASELINE.json configs, synthetic Appendix-B pairs):
+  N = 1 (default): config B - dense G(224) = 1,003,520 faces -> lowpoly G(32)
+        = 20,480 faces, 20-chart atlas, 2048^2, maxDistanceFraction 0.01,
+        dilation radius 4, one asset on one B200.
+  N > 1 (default): config C - the same meshes at 4096^2, ONE atlas row-sharded
+        across the N GPUs (valid-balanced row slabs + dilation halo, the BVH
+        replicated per rank), gathered by the producing dilation kernel's
+        stores into every rank's atlas over CUDA IPC peer memory (NVLink /
+        NVSwitch; `--gather nccl` = NCCL all-gather + assembly) -> "scaling":
+        "strong"; plus config D as 8 independent assets per GPU (the 64-asset
+        batch at N = 8, no collective), reported under "batch_d".
 One step = one whole bake: dense vertex normals + LBVH build + lowpoly wedge
 frames/reliability + raster + closest-point transfer + dilation, i.e.
 dilateSeams(transferNormals(rasterizeGBuffer(lo), hi, diag), g, 4) of the
 reference (test_bake.cpp:205-206), with the meshes already resident in HBM.
 
-`value`  = N_v / t_step   (baked texels/s, device time, CUDA events)
-`e2e`    = the same bake through the host-buffer C ABI call
-           (mf_bake_normal_map) from pinned host memory: H2D of both meshes,
-           device validation, bake, D2H of the RGB8 atlas inside the timing.
-Multi-GPU (torchrun, N ranks): each rank bakes its own asset (seed 7 + rank),
-no data-path collective (batches of independent assets, SURVEY §8e config D
-style) -> "scaling": "weak"; value = sum_r N_v(r) / max_r t.
+`value`  = N_v / t_step   (baked texels/s, device time, CUDA events, max over ranks)
+`e2e`    = the same bake through the host-buffer C ABI (N = 1: mf_bake_normal_map
+           from pinned host memory; N > 1: per rank, mesh upload + validation,
+           the sharded bake and its gather, D2H of the atlas), copies inside
+           the timed region.
+`--gpus N` without torchrun re-launches itself under torch.distributed.run
+(one rank per GPU, 127.0.0.1 rendezvous).
 
 `--impl reference` times the reference's own CPU implementation (the
 reference TUs compiled in place, oracle/_ref/libmfref.so; the C restatement
-oracle/build/liboracle.so if that is absent) on the host cores, rank 0 only.
+oracle/build/liboracle.so if that is absent) on the host cores, rank 0 only,
+on the same workload and config dict as `--impl ours`.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -52,29 +62,72 @@ PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 PEAKS_LIB = os.path.join(ROOT, "build", "libmfpeaks.so")  # tools/peaks.cu
 N_RAYS = 1_000_000  # SURVEY §8(d) secondary metric: raycastFirst on 10^6 random rays
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+L2_FLUSH = "flushed between timed steps (256 MiB write, outside the per-step events)"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="B")
+    ap.add_argument("--config", default=None, help="A..E (default: B at N = 1, C at N > 1)")
+    ap.add_argument("--mode", choices=["auto", "single", "shard", "replicas", "batch"], default="auto",
+                    help="auto: single at N = 1, shard at N > 1; replicas: one asset per rank (seed 7 + rank); "
+                         "batch: --assets independent assets per GPU")
+    ap.add_argument("--shard", action="store_true", help="same as --mode shard")
+    ap.add_argument("--gather", choices=["nccl", "peer"], default="peer",
+                    help="shard: atlas gather by the dilation kernel storing its rows into every rank's atlas "
+                         "over CUDA IPC peer memory (mf_bake_normal_map_dev_publish), or NCCL all-gather")
+    ap.add_argument("--assets", type=int, default=8, help="batch: independent assets per GPU (config D: 8)")
+    ap.add_argument("--no-batch", action="store_true", help="N > 1: skip the config-D batch line")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-rays", action="store_true", help="skip the secondary BVH rays/s metrics")
     ap.add_argument("--json-out", default=None)
-    ap.add_argument("--assets", type=int, default=1,
-                    help="independent assets baked concurrently per GPU (config D: 8), one context + stream + "
-                         "host thread each")
-    ap.add_argument("--gather", choices=["nccl", "peer"], default="peer",
-                    help="--shard: atlas gather by NCCL all-gather, or by the dilation kernel storing its rows "
-                         "into every rank's atlas over CUDA IPC peer memory (mf_bake_normal_map_dev_publish)")
-    ap.add_argument("--shard", action="store_true",
-                    help="N>1: row-shard ONE atlas across ranks + NCCL all-gather (strong scaling) "
-                         "instead of one asset per rank")
-    return ap.parse_args()
+    ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)
+    return ap.parse_args(argv)
+
+
+def resolve(args, world):
+    """(mode, config) of this run."""
+    mode = "shard" if args.shard else args.mode
+    if mode == "auto":
+        mode = "shard" if world > 1 else "single"
+    if mode == "shard" and world == 1:
+        mode = "single"
+    name = args.config or {"shard": "C", "batch": "D"}.get(mode, "B")
+    return mode, name
+
+
+def config_dict(name, pair, mode, world, assets=1, seed=None):
+    """The workload description both arms print (identical dicts)."""
+    par = {"single": "single asset, one GPU",
+           "shard": f"rows x{world}: one atlas in valid-balanced row slabs, BVH replicated, atlas gathered",
+           "replicas": f"assets x{world}: one asset per GPU, no collective",
+           "batch": f"assets x{assets * world}: {assets} per GPU, no collective"}[mode]
+    batch = {"shard": 1, "replicas": world, "batch": assets * world}.get(mode, 1)
+    return {"workload": workload_desc(name, pair), "global_batch": batch, "seq_len": None, "parallelism": par,
+            "l2": L2_FLUSH, "seed": seed}
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch(argv, n):
+    """`bench.py --gpus N` outside torchrun: re-run under torch.distributed.run
+    with one rank per GPU (NCCL init lines on, so the rank count is visible)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.run(cmd, env=env).returncode
 
 
 def dist_env():
@@ -212,7 +265,7 @@ def live_peaks(device):
     return out
 
 
-def stage_rooflines(pair, stage, n_queries, counters, hbm, peaks):
+def stage_rooflines(pair, stage, n_queries, counters, hbm, peaks, n_valid=None):
     """SURVEY §8(d) per-stage roofline fractions: streaming stages against HBM,
     the traversal against the measured L2 read bandwidth and the FP64 pipe.
     Times are the eager per-stage CUDA-event times (all kernels of the stage)."""
@@ -234,11 +287,16 @@ def stage_rooflines(pair, stage, n_queries, counters, hbm, peaks):
                       note="50 B x res^2 (G-buffer as the API output); fused path writes only query records"),
         "lbvh": row(148 * f + 24 * v, stage["ms_bvh"], hbm,
                     note="148 F + 24 V; stage also builds the dense vertex normals, side stream, overlapped"),
-        "dilate": row(7 * res * res, stage["ms_dilate"], hbm, note="7 B x res^2"),
+        # the fused bake resolves the dilation before the transfer: its time is
+        # the dilation-links kernel (the copies ride on the transfer epilogue)
+        "dilate": row(7 * res * res, stage["ms_dilate"], hbm,
+                      note="7 B x res^2 over the dilation-links kernel's time (fused bake: the source choice; "
+                           "the copies are stored by the transfer epilogue)"),
     }
     if counters:
         out["transfer_l2"] = row(counters["bytes_per_query"] * n_queries, stage["ms_transfer"],
-                                 peaks.get("l2_read_gbs"), note="W_q x N_q against the measured L2 read bandwidth")
+                                 peaks.get("l2_read_gbs"),
+                                 note="W_q x N_q visit bytes against the measured L2 read bandwidth")
         flops = (22 * counters["n_node"] + 80 * counters["n_tri"]) * n_queries
         out["transfer_fp64"] = row(flops, stage["ms_transfer"], peaks.get("fp64_tflops"), unit="TFLOP/s",
                                    scale=1e12, note="(22 N_node + 80 N_tri) x N_q")
@@ -338,14 +396,15 @@ def bvh_rays(ctx, hi, pair, steps):
 
 def transfer_traffic():
     """dram__bytes_read + dram__bytes_write of the transfer kernel from the
-    committed `ncu --set full` capture summary (profiles/k_transfer_ncu.json)."""
+    committed `ncu --set full` capture summary (profiles/k_transfer_ncu.json),
+    with that launch's whole record."""
     try:
         with open(TRAFFIC) as f:
             d = json.load(f)
         launch = next(x for x in d["launches"] if "k_transfer" in x["kernel"])
-        return float(launch["dram_bytes"]), d.get("source")
+        return float(launch["dram_bytes"]), d.get("source"), launch
     except (OSError, KeyError, StopIteration, ValueError):
-        return None, None
+        return None, None, None
 
 
 def transfer_algorithmic_bytes(name, n_queries, n_valid, res):
@@ -365,22 +424,111 @@ def transfer_algorithmic_bytes(name, n_queries, n_valid, res):
 
 
 # ----------------------------------------------------------------------------- ours
-def run_ours(args):
+class Dist:
+    """torch.distributed plumbing of one bench rank: NCCL when every rank has
+    its own GPU, gloo when ranks share one (a single-GPU test of the N > 1
+    path); small host-side reductions either way."""
+
+    def __init__(self):
+        import torch
+        self.rank, self.local_rank, self.world = dist_env()
+        self.on = "RANK" in os.environ
+        ndev = torch.cuda.device_count()
+        self.device = self.local_rank % max(ndev, 1)
+        self.shared_gpu = self.on and ndev < self.world
+        torch.cuda.set_device(self.device)
+        self.backend = None
+        if self.on:
+            import torch.distributed as dist
+            self.backend = "gloo" if self.shared_gpu else "nccl"
+            if self.backend == "nccl":
+                os.environ.setdefault("NCCL_DEBUG", "INFO")
+                os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+            else:
+                dist.init_process_group("gloo")
+
+    def _reduce(self, vals, op):
+        if not self.on:
+            return list(vals)
+        import torch
+        import torch.distributed as dist
+        dev = "cuda" if self.backend == "nccl" else "cpu"
+        t = torch.tensor(list(vals), dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=op)
+        return t.tolist()
+
+    def max(self, *vals):
+        import torch.distributed as dist
+        return self._reduce(vals, dist.ReduceOp.MAX if self.on else None)
+
+    def min(self, *vals):
+        import torch.distributed as dist
+        return self._reduce(vals, dist.ReduceOp.MIN if self.on else None)
+
+    def sum(self, *vals):
+        import torch.distributed as dist
+        return self._reduce(vals, dist.ReduceOp.SUM if self.on else None)
+
+    def barrier(self):
+        if self.on:
+            import torch.distributed as dist
+            if self.backend == "nccl":
+                dist.barrier(device_ids=[self.device])
+            else:
+                dist.barrier()
+
+    def close(self):
+        if self.on:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+def timed_steps(d, step, steps, warmup, stream, flush, clk_device):
+    """W untimed warm-up steps, then K timed steps bracketed by a barrier and a
+    device synchronize on both sides; per-step CUDA events on the launching
+    stream with the L2 flushed (untimed) in between. Returns (mean ms over
+    the K steps, clock summary)."""
+    import torch
+    for _ in range(max(warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    d.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(clk_device) as clk:
+        for i in range(steps):
+            flush.zero_()
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    d.barrier()
+    return sum(s.elapsed_time(e) for s, e in zip(starts, ends)) / steps, clk.summary()
+
+
+def run_ours(args, argv_mode, name):
+    import ctypes
+
     import torch
 
-    rank, local_rank, world = dist_env()
-    torch.cuda.set_device(local_rank)
-    distributed = "RANK" in os.environ  # launched by torchrun (any world size)
-    if distributed:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    d = Dist()
+    rank, world = d.rank, d.world
+    mode = argv_mode
     from paper_2605_26137_b200 import capi, fixtures as fx
+    from paper_2605_26137_b200 import meshforge as mf
 
-    name = args.config
-    pair = fx.config_pair(name, seed=fx.CONFIGS[name]["seed"] + (0 if args.shard else rank))
+    if mode == "batch":
+        line = run_batch(args, d, name)
+        d.close()
+        return line
+
+    seed = fx.CONFIGS[name]["seed"] + (rank if mode == "replicas" else 0)
+    pair = fx.config_pair(name, seed=seed)
     res = pair.res
     stream = torch.cuda.current_stream()
-    ctx = capi.Context(local_rank, stream.cuda_stream)
+    ctx = capi.Context(d.device, stream.cuda_stream)
     lib = ctx.lib
     lo = capi.DeviceMesh(ctx, pair.lowpoly)
     hi = capi.DeviceMesh(ctx, pair.dense)
@@ -393,9 +541,9 @@ def run_ours(args):
     row_b, row_e = 0, res
     shard_ranges = None
     peer = None
-    if args.shard and distributed:
-        # one atlas, rows balanced by valid texels, all-gathered
-        import ctypes
+    gather = None
+    if mode == "shard":
+        # one atlas, rows balanced by valid texels, gathered on every rank
         from paper_2605_26137_b200 import sharding
         counts = np.zeros(res, np.int64)
         capi.check(lib.mf_coverage_rows(ctx.h, lo.h, res, ctypes.c_void_p(counts.ctypes.data)))
@@ -403,8 +551,21 @@ def run_ours(args):
         row_b, row_e = shard_ranges[rank]
         rows_max = max(e - b for b, e in shard_ranges)
         slab = torch.empty((rows_max, res, 3), dtype=torch.uint8, device="cuda")
-        gathered = [torch.empty_like(slab) for _ in range(world)]
-        peer = sharding.PeerAtlas(ctx, res) if args.gather == "peer" else None
+        gather = args.gather
+        if gather == "peer":
+            ok = 1.0
+            try:
+                peer = sharding.PeerAtlas(ctx, res)
+            except Exception as e:  # noqa: BLE001 - fall back to NCCL for every rank
+                print(f"[bench rank {rank}] peer-memory atlas unavailable ({e}); NCCL all-gather", file=sys.stderr)
+                ok = 0.0
+            if d.min(ok)[0] < 1.0:
+                if peer is not None:
+                    peer.close()
+                peer = None
+                gather = "nccl"
+        if gather == "nccl":
+            gathered = [torch.empty_like(slab) for _ in range(world)]
 
     def step(stats=None):
         if shard_ranges is None:
@@ -414,121 +575,139 @@ def run_ours(args):
         if peer is not None:  # rows stored into every rank's atlas by the dilation kernel
             capi.check(lib.mf_bake_normal_map_dev_publish(ctx.h, lo.h, hi.h, res, diag, frac, 4, row_b, row_e,
                                                           peer.dst, peer.n, stats))
-            torch.distributed.barrier()
+            d.barrier()
             return
         capi.check(lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, diag, frac, 4, row_b, row_e,
                                               slab.data_ptr(), stats))
-        torch.distributed.all_gather(gathered, slab)
-        rgb.copy_(sharding.assemble(gathered, shard_ranges))
+        if d.backend == "nccl":
+            torch.distributed.all_gather(gathered, slab)
+            rgb.copy_(sharding.assemble(gathered, shard_ranges))
+        else:  # ranks sharing one GPU (test mode): gather through the host
+            host = [torch.empty_like(slab, device="cpu") for _ in range(world)]
+            torch.distributed.all_gather(host, slab.cpu())
+            rgb.copy_(sharding.assemble(host, shard_ranges).to("cuda"))
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-
-    # timed region: per-step CUDA events on the launching stream, L2 flushed
-    # (untimed) between steps. The library replays its captured CUDA graph of
-    # the whole bake here (stage events are not meaningful inside a graph).
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    launches0 = ctx.launches
-    n_valid = n_queries = hits = 0
-    if distributed:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local_rank) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            starts[i].record(stream)
-            step(st)
-            ends[i].record(stream)
-            n_valid, n_queries, hits = st.valid_texels, st.queries, st.hits
-        torch.cuda.synchronize()
-    if distributed:
-        torch.distributed.barrier()
-    launches = ctx.launches - launches0
-    if launches == 0:  # graph replays do not pass through the host launch counter
-        launches = args.steps * launches_per_bake(ctx, step)
+    ms_step, clocks = timed_steps(d, lambda: step(st), args.steps, args.warmup, stream, flush, d.device)
+    n_valid, n_queries, hits = st.valid_texels, st.queries, st.hits
+    # graph replays bypass the host launch counter: count one eager bake's
+    launches = launches_per_bake(ctx, step) * args.steps
     # stage breakdown + the transfer kernel's own duration: the same bake run
     # eagerly with CUDA events around each stage on the launching stream
     ctx.set_timing(True)
     stage = {k: [] for k in ("ms_prepare", "ms_bvh", "ms_raster", "ms_transfer", "ms_dilate", "ms_total")}
-    for i in range(max(3, min(args.steps, 10))):
+    for _ in range(max(3, min(args.steps, 10))):
         flush.zero_()
         step(st)
-        d = st.as_dict()
+        dd = st.as_dict()
         for k in stage:
-            stage[k].append(d[k])
+            stage[k].append(dd[k])
     ctx.set_timing(False)
-    t_ms = sum(s.elapsed_time(e) for s, e in zip(starts, ends))
-    ms_step = t_ms / args.steps
     ms_transfer = statistics.mean(stage["ms_transfer"])
 
-    # aggregate over ranks: max time, summed work
-    agg_nv = n_valid
-    agg_nq = n_queries
-    t_max = ms_step
-    t_xfer_max = ms_transfer
-    if distributed:
-        import torch.distributed as dist
-        tt = torch.tensor([ms_step, ms_transfer], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        nn = torch.tensor([n_valid, n_queries], dtype=torch.float64, device="cuda")
-        dist.all_reduce(nn, op=dist.ReduceOp.SUM)
-        t_max, t_xfer_max = tt.tolist()
-        agg_nv, agg_nq = nn.tolist()
-        if shard_ranges is not None:  # slabs overlap by the dilation halo: count each texel once
-            agg_nv, agg_nq = float(_n_valid(pair)), float(n_queries_full(name, pair))
+    # aggregate over ranks: max time, summed work (slabs overlap by the
+    # dilation halo: a sharded atlas counts each texel once)
+    t_max, t_xfer_max = d.max(ms_step, ms_transfer)
+    agg_nv, agg_nq = d.sum(n_valid, n_queries)
+    extra = {}
+    if shard_ranges is not None:
+        agg_nv, agg_nq = float(_n_valid(pair)), float(n_queries_full(name, pair))
+        extra["shards"] = {"ranges": shard_ranges, "gather": gather,
+                           "gather_method": ("dilation kernel stores into every rank's atlas over CUDA IPC "
+                                             "peer memory" if gather == "peer" else
+                                             ("NCCL all-gather + assembly" if d.backend == "nccl"
+                                              else "gloo host all-gather (ranks share one GPU: test mode)")),
+                           "backend": d.backend, "shared_gpu": d.shared_gpu}
+        # the gathered atlas equals a single-GPU bake of the whole atlas
+        full = torch.empty((res, res, 3), dtype=torch.uint8, device="cuda")
+        capi.check(lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, diag, frac, 4, 0, res, full.data_ptr(),
+                                              None))
+        torch.cuda.synchronize()
+        atlas = peer.atlas if peer is not None else rgb
+        eq = float(torch.equal(atlas, full))
+        extra["shards"]["gather_check"] = bool(d.max(1.0 - eq)[0] == 0.0)
+        # the same config on one GPU (rank 0), for the strong-scaling comparison
+        if rank == 0:
+            one = lambda: capi.check(lib.mf_bake_normal_map_dev(  # noqa: E731
+                ctx.h, lo.h, hi.h, res, diag, frac, 4, 0, res, full.data_ptr(), None))
+            for _ in range(3):
+                one()
+            torch.cuda.synchronize()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps)]
+            for i in range(args.steps):
+                flush.zero_()
+                ev[2 * i].record(stream)
+                one()
+                ev[2 * i + 1].record(stream)
+            torch.cuda.synchronize()
+            ms1 = sum(ev[2 * i].elapsed_time(ev[2 * i + 1]) for i in range(args.steps)) / args.steps
+            extra["single_gpu_same_config"] = {"ms_per_step": ms1, "value": agg_nv / (ms1 * 1e-3), "unit": UNIT,
+                                               "note": "whole atlas on rank 0's GPU alone, same timing rules"}
+        del full
 
-    # secondary BVH metrics and the live L2 / FP64 peaks (rank 0)
-    rays = bvh_rays(ctx, hi, pair, args.steps) if rank == 0 and not args.no_rays else None
-    peaks = live_peaks(local_rank) if rank == 0 else {}
+    # secondary BVH metrics and the live L2 / FP64 peaks (rank 0, N = 1 only:
+    # they are single-GPU numbers)
+    rays = bvh_rays(ctx, hi, pair, args.steps) if rank == 0 and world == 1 and not args.no_rays else None
+    peaks = live_peaks(d.device) if rank == 0 else {}
 
-    # end-to-end through the host-buffer C ABI call (pinned host inputs/outputs)
+    # end-to-end through the public host-buffer API
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, ctx, pair, world, distributed)
+        if shard_ranges is not None:
+            e2e = run_e2e_shard(args, d, ctx, pair, shard_ranges, peer, gather)
+        else:
+            e2e = run_e2e(args, d, ctx, pair)
+
+    batch_d = None
+    if world > 1 and mode == "shard" and not args.no_batch:
+        batch_d = run_batch(args, d, "D", assets=8, as_line=False)
 
     if rank != 0:
-        if distributed:
-            torch.distributed.destroy_process_group()
+        d.close()
         return None
 
     peak, peak_src = hbm_peak()
     alg_bytes, counters = transfer_algorithmic_bytes(name, n_queries, n_valid, res)
     stage_mean = {k: statistics.mean(v) for k, v in stage.items()}
-    stages_rl = stage_rooflines(pair, stage_mean, n_queries, counters, peak, peaks)
+    stages_rl = stage_rooflines(pair, stage_mean, n_queries, counters, peak, peaks, n_valid)
     roofline = None
     if alg_bytes is not None:
         # the traversal's node/triangle bytes are served from L2
         # (its DRAM traffic, `traffic`, is ~5% of them), so its roofline is the
-        # measured L2 read bandwidth; the HBM-relative figure is kept beside it.
+        # measured L2 read bandwidth. The §8(d) bytes are node/triangle VISITS
+        # (the reference's best-first loop's), not DRAM or L2 transactions;
+        # `l2_actual` is the kernel's measured L2 traffic from the committed
+        # ncu capture of the same kernel.
         achieved = alg_bytes / (ms_transfer * 1e-3) / 1e9
-        traffic, traffic_src = transfer_traffic()
+        traffic, traffic_src, ncu = transfer_traffic()
         l2 = peaks.get("l2_read_gbs")
         roofline = {"bound": "l2" if l2 else "hbm", "kernel": "k_transfer_t (closest-point traversal + encode)",
                     "achieved": round(achieved, 1), "peak": l2 or peak, "unit": "GB/s",
                     "frac": round(achieved / (l2 or peak), 4), "traffic": traffic, "traffic_source": traffic_src,
                     "peak_source": ("measured live: L2 read bandwidth, tools/peaks.cu" if l2 else peak_src),
-                    "hbm_peak": peak, "hbm_peak_source": peak_src, "frac_of_hbm": round(achieved / peak, 4),
+                    "hbm_peak": peak, "hbm_peak_source": peak_src,
+                    "bytes_model": "SURVEY 8(d) visit bytes W_q x N_q (node/triangle visits of the reference's "
+                                   "best-first loop), served from L1/L2",
                     "algorithmic_bytes_per_launch": alg_bytes, "ms_per_launch": round(ms_transfer, 4),
                     "per_query": counters}
+        if ncu and l2:
+            l2b = ncu.get("l2_sectors", 0) * 32.0
+            dur = ncu.get("duration_ns")
+            if l2b and dur:
+                roofline["l2_actual"] = {
+                    "bytes_per_launch": l2b, "gbs": round(l2b / dur, 1), "frac": round(l2b / dur / l2, 4),
+                    "issue_active_pct": ncu.get("issue_active_pct"),
+                    "threads_per_instruction": ncu.get("threads_per_instruction"),
+                    "source": traffic_src}
     cpu = None
-    if not args.no_cpu_baseline:
-        cpu = cpu_baseline(pair, name)
-    clocks = clk.summary()
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(pair, name, ctx=ctx, gpu_rgb=rgb.cpu().numpy())
     line = {
         "metric": METRICS.get(name, METRIC), "value": agg_nv / (t_max * 1e-3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": t_max,
         "higher_is_better": True, "scaling": "strong" if shard_ranges else "weak", "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (deterministic geodesic blob pair, Appendix B of SURVEY.md)",
-        "config": {"workload": workload_desc(name, pair), "global_batch": 1 if shard_ranges else world,
-                   "seq_len": None,
-                   "parallelism": (f"rows x{world} (one atlas, valid-balanced row slabs, "
-                                   f"{'peer-memory gather in the dilation kernel' if args.gather == 'peer' else 'NCCL all-gather'})"
-                                   if shard_ranges else f"assets x{world} (one asset per GPU, no collective)"),
-                   "l2": "flushed between timed steps (256 MiB write, outside the per-step events)",
-                   "seed": fx.CONFIGS[name]["seed"]},
+        "config": config_dict(name, pair, mode, world, seed=seed if mode != "replicas" else fx.CONFIGS[name]["seed"]),
         "rays_per_s": agg_nq / (t_xfer_max * 1e-3),
         "n_valid_texels": n_valid, "n_queries": n_queries, "hits": hits,
         "stage_ms": {k: round(statistics.mean(v), 4) for k, v in stage.items()},
@@ -536,14 +715,16 @@ def run_ours(args):
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks,
     }
-    if distributed:
-        torch.distributed.destroy_process_group()
+    line.update(extra)
+    if batch_d is not None:
+        line["batch_d"] = batch_d
+    d.close()
     return line
 
 
-def run_batch(args):
+def run_batch(args, d, name, assets=None, as_line=True):
     """K independent assets per GPU, each on its own
-    context (own stream + side stream, own captured graph), driven by K host
+    context (own stream + side streams, own captured graph), driven by K host
     threads (ctypes drops the GIL in the call). One step = all K bakes;
     value = sum of valid texels over all assets of all ranks / max-rank time.
     Device time: one event on the launch stream that every asset stream waits
@@ -552,19 +733,14 @@ def run_batch(args):
 
     import torch
 
-    rank, local_rank, world = dist_env()
-    torch.cuda.set_device(local_rank)
-    distributed = "RANK" in os.environ
-    if distributed:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     from paper_2605_26137_b200 import capi, fixtures as fx
 
-    name, k = args.config, args.assets
+    k = assets or args.assets
+    rank, world = d.rank, d.world
     base = fx.CONFIGS[name]["seed"] + rank * k
     pairs = [fx.config_pair(name, seed=base + i) for i in range(k)]
     streams = [torch.cuda.Stream() for _ in range(k)]
-    ctxs = [capi.Context(local_rank, st.cuda_stream) for st in streams]
+    ctxs = [capi.Context(d.device, s.cuda_stream) for s in streams]
     meshes = [(capi.DeviceMesh(c, p.lowpoly), capi.DeviceMesh(c, p.dense)) for c, p in zip(ctxs, pairs)]
     outs = [torch.empty((p.res, p.res, 3), dtype=torch.uint8, device="cuda") for p in pairs]
     stats = [capi.MfBakeStats() for _ in range(k)]
@@ -580,63 +756,33 @@ def run_batch(args):
     def batch():
         ev = torch.cuda.Event()
         ev.record(main)
-        for st in streams:
-            st.wait_event(ev)
+        for s in streams:
+            s.wait_event(ev)
         list(pool.map(one, range(k)))
-        for st in streams:
-            main.wait_stream(st)
+        for s in streams:
+            main.wait_stream(s)
 
-    for _ in range(max(args.warmup, 3)):
-        batch()
-    torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if distributed:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    launches0 = sum(c.launches for c in ctxs)
-    with ClockSampler(local_rank) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            starts[i].record(main)
-            batch()
-            ends[i].record(main)
-        torch.cuda.synchronize()
-    if distributed:
-        torch.distributed.barrier()
-    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends)) / args.steps
+    ms, clocks = timed_steps(d, batch, args.steps, args.warmup, main, flush, d.device)
     nv = sum(s.valid_texels for s in stats)
-    launches = sum(c.launches for c in ctxs) - launches0
-    if launches == 0:
-        launches = args.steps * k * launches_per_bake(ctxs[0], lambda: one(0))
-    if distributed:
-        import torch.distributed as dist
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        nn = torch.tensor([nv], dtype=torch.float64, device="cuda")
-        dist.all_reduce(nn, op=dist.ReduceOp.SUM)
-        ms, nv = tt.item(), nn.item()
+    launches = args.steps * k * launches_per_bake(ctxs[0], lambda: one(0))
+    ms, = d.max(ms)
+    nv, = d.sum(nv)
     pool.shutdown()
-    if rank != 0:
-        if distributed:
-            torch.distributed.destroy_process_group()
+    for c in ctxs:
+        c.synchronize()
+    if d.rank != 0:
         return None
-    line = {
-        "metric": METRICS.get(name, METRIC), "value": nv / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (deterministic geodesic blob pairs, one seed per asset)",
-        "config": {"workload": workload_desc(name, pairs[0]) + f"; {k} assets per GPU (seeds {base}..{base + k - 1} "
-                                                               f"on rank {rank})",
-                   "global_batch": k * world, "seq_len": None,
-                   "parallelism": f"assets x{k * world} ({k} per GPU on {k} streams, no collective)",
-                   "l2": "flushed between timed steps (256 MiB write, outside the per-step events)"},
-        "assets_per_gpu": k, "ms_per_asset": ms / k,
-        "gpu_launches": launches, "clocks": clk.summary(),
-    }
-    if distributed:
-        torch.distributed.destroy_process_group()
-    return line
+    out = {"metric": METRICS.get(name, METRIC), "value": nv / (ms * 1e-3), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (deterministic geodesic blob pairs, one seed per asset)",
+           "config": config_dict(name, pairs[0], "batch", world, k, seed=fx.CONFIGS[name]["seed"]),
+           "assets_per_gpu": k, "assets_total": k * world, "ms_per_asset": ms / k,
+           "ms_per_64_assets": ms * 64.0 / (k * world),
+           "gpu_launches": launches, "clocks": clocks}
+    if not as_line:
+        out = {k_: v for k_, v in out.items() if k_ not in ("higher_is_better", "vs_baseline", "dtype", "data")}
+    return out
 
 
 def launches_per_bake(ctx, step):
@@ -648,37 +794,23 @@ def launches_per_bake(ctx, step):
     return ctx.launches - before
 
 
-def run_e2e(args, ctx, pair, world, distributed=False):
-    import ctypes
+def _pinned_pair(pair):
     import torch
 
-    from paper_2605_26137_b200 import capi
     from paper_2605_26137_b200.mesh import TriangleMesh
 
     def pinned(a):
-        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        return t.numpy()
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
 
     lo, hi = pair.lowpoly, pair.dense
     lo_p = TriangleMesh(pinned(lo.positions), pinned(lo.faces), uvs=pinned(lo.uvs), face_uvs=pinned(lo.face_uvs))
     hi_p = TriangleMesh(pinned(hi.positions), pinned(hi.faces))
-    res = pair.res
-    out = torch.empty((res, res, 3), dtype=torch.uint8).pin_memory().numpy()
-    lv, hv = lo_p.view(), hi_p.view()
     h2d = sum(a.nbytes for a in (lo_p.positions, lo_p.faces, lo_p.uvs, lo_p.face_uvs, hi_p.positions, hi_p.faces))
-    d2h = out.nbytes
-    st = capi.MfBakeStats()
-    stream = torch.cuda.current_stream()
+    return lo_p, hi_p, h2d
 
-    def call():
-        capi.check(ctx.lib.mf_bake_normal_map(ctx.h, ctypes.byref(lv), ctypes.byref(hv), res, pair.bbox_diagonal,
-                                              pair.max_distance_fraction, 4, ctypes.c_void_p(out.ctypes.data),
-                                              None, None, ctypes.byref(st)))
 
-    for _ in range(5):  # eager, graph capture, replays
-        call()
-    torch.cuda.synchronize()
-    steps = max(10, min(3 * args.steps, 30))
+def _time_calls(call, stream, steps):
+    import torch
     times = []
     for _ in range(steps):
         s = torch.cuda.Event(enable_timing=True)
@@ -688,20 +820,110 @@ def run_e2e(args, ctx, pair, world, distributed=False):
         e.record(stream)
         e.synchronize()
         times.append(s.elapsed_time(e))
-    ms = statistics.mean(times)
-    nv = st.valid_texels
-    if distributed:
-        import torch.distributed as dist
-        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        nn = torch.tensor([nv], dtype=torch.float64, device="cuda")
-        dist.all_reduce(nn, op=dist.ReduceOp.SUM)
-        ms = tt.item()
-        nv = nn.item()
-    return {"value": nv / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "ms_median": statistics.median(times),
-            "ms_min": min(times), "h2d_bytes_per_step": int(h2d),
-            "d2h_bytes_per_step": int(d2h), "steps": steps,
-            "call": "mf_bake_normal_map (host buffers, pinned) via ctypes"}
+    return times
+
+
+def run_e2e(args, d, ctx, pair):
+    """mf_bake_normal_map from host buffers: pinned (the headline e2e) and
+    pageable numpy arrays (what a drop-in caller's std::vectors are)."""
+    import ctypes
+
+    import torch
+
+    from paper_2605_26137_b200 import capi
+
+    lo_p, hi_p, h2d = _pinned_pair(pair)
+    res = pair.res
+    out = torch.empty((res, res, 3), dtype=torch.uint8).pin_memory().numpy()
+    out_pg = np.empty((res, res, 3), np.uint8)
+    st = capi.MfBakeStats()
+    stream = torch.cuda.current_stream()
+
+    def call_with(lv, hv, o):
+        def call():
+            capi.check(ctx.lib.mf_bake_normal_map(ctx.h, ctypes.byref(lv), ctypes.byref(hv), res,
+                                                  pair.bbox_diagonal, pair.max_distance_fraction, 4,
+                                                  ctypes.c_void_p(o.ctypes.data), None, None, ctypes.byref(st)))
+        return call
+
+    steps = max(10, min(3 * args.steps, 30))
+    res_out = {}
+    for tag, (lm, hm, o) in {"pinned": (lo_p, hi_p, out), "pageable": (pair.lowpoly, pair.dense, out_pg)}.items():
+        lv, hv = lm.view(), hm.view()
+        call = call_with(lv, hv, o)
+        for _ in range(5):  # eager, graph capture, replays
+            call()
+        torch.cuda.synchronize()
+        times = _time_calls(call, stream, steps)
+        ms, = d.max(statistics.mean(times))
+        nv, = d.sum(st.valid_texels)
+        res_out[tag] = {"value": nv / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+                        "ms_median": statistics.median(times), "ms_min": min(times), "steps": steps}
+    assert np.array_equal(out, out_pg)
+    e2e = dict(res_out["pinned"])
+    e2e.update({"h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out.nbytes),
+                "call": "mf_bake_normal_map (host buffers, pinned) via ctypes",
+                "pageable": dict(res_out["pageable"], call="mf_bake_normal_map from pageable numpy arrays "
+                                                           "(a drop-in caller's std::vector data)")})
+    return e2e
+
+
+def run_e2e_shard(args, d, ctx, pair, ranges, peer, gather):
+    """Sharded bake end to end through the public ABI, per rank and step: the
+    H2D upload + device validation of both meshes from pinned host memory
+    (mf_mesh_upload), the rank's row slab with its gather into every rank's
+    atlas, a barrier, and the D2H of the assembled atlas into pinned memory."""
+    import ctypes
+
+    import torch
+
+    from paper_2605_26137_b200 import capi, sharding
+
+    lo_p, hi_p, h2d = _pinned_pair(pair)
+    res = pair.res
+    b, e = ranges[d.rank]
+    out = torch.empty((res, res, 3), dtype=torch.uint8).pin_memory()
+    rows_max = max(hi_ - lo_ for lo_, hi_ in ranges)
+    slab = torch.empty((rows_max, res, 3), dtype=torch.uint8, device="cuda")
+    rgb = torch.empty((res, res, 3), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def call():
+        lo = capi.DeviceMesh(ctx, lo_p)
+        hi = capi.DeviceMesh(ctx, hi_p)
+        if peer is not None:
+            capi.check(ctx.lib.mf_bake_normal_map_dev_publish(ctx.h, lo.h, hi.h, res, pair.bbox_diagonal,
+                                                              pair.max_distance_fraction, 4, b, e, peer.dst,
+                                                              peer.n, None))
+            d.barrier()
+            out.copy_(peer.atlas, non_blocking=True)
+        else:
+            capi.check(ctx.lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, pair.bbox_diagonal,
+                                                      pair.max_distance_fraction, 4, b, e, slab.data_ptr(), None))
+            if d.backend == "nccl":
+                g = [torch.empty_like(slab) for _ in ranges]
+                torch.distributed.all_gather(g, slab)
+                rgb.copy_(sharding.assemble(g, ranges))
+            else:
+                g = [torch.empty_like(slab, device="cpu") for _ in ranges]
+                torch.distributed.all_gather(g, slab.cpu())
+                rgb.copy_(sharding.assemble(g, ranges).to("cuda"))
+            out.copy_(rgb, non_blocking=True)
+        lo.close()
+        hi.close()
+
+    for _ in range(4):
+        call()
+    torch.cuda.synchronize()
+    d.barrier()
+    steps = max(5, min(args.steps, 20))
+    times = _time_calls(call, stream, steps)
+    ms, = d.max(statistics.mean(times))
+    return {"value": float(_n_valid(pair)) / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "ms_median": statistics.median(times), "steps": steps, "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(out.numel()),
+            "call": "per rank: mf_mesh_upload x2 (pinned host meshes) + sharded bake + gather + barrier + "
+                    "D2H of the whole atlas; bytes are per rank"}
 
 
 # ----------------------------------------------------------------------------- CPU reference
@@ -712,11 +934,15 @@ def _reference_lib():
     return bindings.port(), "port"
 
 
-def cpu_reference_bake(pair, time_bvh=False):
+def cpu_reference_bake(pair, time_bvh=False, debug=False):
     lib, kind = _reference_lib()
     t0 = time.perf_counter()
-    r = lib.bake(pair.lowpoly, pair.dense, pair.res, pair.bbox_diagonal, pair.max_distance_fraction, 4,
-                 time_bvh=time_bvh)
+    if kind == "reference":
+        r = lib.bake(pair.lowpoly, pair.dense, pair.res, pair.bbox_diagonal, pair.max_distance_fraction, 4,
+                     time_bvh=time_bvh, debug=debug)
+    else:
+        r = lib.bake(pair.lowpoly, pair.dense, pair.res, pair.bbox_diagonal, pair.max_distance_fraction, 4,
+                     debug=debug)
     wall = time.perf_counter() - t0
     return r, wall, kind, r.get("n_valid")
 
@@ -728,18 +954,57 @@ def cores():
     return os.cpu_count() or 1
 
 
-def cpu_baseline(pair, name, runs=5):
+def atlas_parity(pair, ctx, r, gpu_rgb):
+    """The GPU atlas of the timed run against the reference's (same inputs):
+    RGB8 mismatches (count, max LSB, and how many are NOT explained by the
+    .5-boundary rule of SURVEY §8c), plus hit faces of a GPU debug bake
+    against the reference replica's (Appendix D)."""
+    from paper_2605_26137_b200 import meshforge as mf
+    ref_rgb = r["rgb"].reshape(-1, 3).astype(np.int32)
+    g = gpu_rgb.reshape(-1, 3).astype(np.int32)
+    diff = np.abs(g - ref_rgb)
+    bad = np.argwhere(diff > 0)
+    out = {"texels": int(ref_rgb.shape[0]), "rgb_mismatch_texels": int((diff.max(1) > 0).sum()),
+           "rgb_max_lsb": int(diff.max()) if diff.size else 0}
+    ts = r.get("ts")
+    if ts is not None:
+        v = (ts.reshape(-1, 3)[bad[:, 0], bad[:, 1]] + 1.0) * 127.5
+        near = np.abs(v - np.floor(v) - 0.5) <= 1e-3 * 127.5
+        out["rgb_outside_rule"] = int(((diff[bad[:, 0], bad[:, 1]] > 1) | ~near).sum())
+    if r.get("face") is not None and ctx is not None:
+        dbg = mf.bake_normal_map(pair.lowpoly, pair.dense, pair.res, pair.bbox_diagonal,
+                                 pair.max_distance_fraction, 4, debug=True, ctx=ctx)
+        out["face_mismatch"] = int((dbg["face"] != r["face"]).sum())
+        out["queries"] = int((r["face"] != -1).sum())
+        out["debug_rgb_equals_timed"] = bool(np.array_equal(dbg["rgb"].reshape(-1, 3), gpu_rgb.reshape(-1, 3)))
+        if ts is not None:
+            out["ts_max_abs_diff"] = float(np.abs(dbg["ts"] - ts).max())
+    out["ok"] = (out["rgb_max_lsb"] <= 1 and out.get("rgb_outside_rule", 0) == 0
+                 and out.get("face_mismatch", 0) == 0)
+    return out
+
+
+def cpu_baseline(pair, name, runs=5, ctx=None, gpu_rgb=None):
     """The reference's CPU bake (rasterizeGBuffer + transferNormals + dilateSeams,
     as test_bake.cpp:205-206 composes it) on the box's host cores, median of
     `runs` full bakes (~8 s at B), with a standalone Bvh(hi) build
-    timed beside it (not part of the total: transferNormals builds its own)."""
+    timed beside it (not part of the total: transferNormals builds its own).
+    The first run also returns per-texel hit faces and ts (the reference
+    replica, run after the timed stock chain) and its atlas is diffed against
+    the GPU's (`parity`)."""
     runs_t = []
+    parity = None
+    bvh_s = 0.0
     for i in range(runs):
-        r, wall, kind, _ = cpu_reference_bake(pair, time_bvh=(i == 0))
+        dbg = i == 0 and gpu_rgb is not None
+        r, wall, kind, _ = cpu_reference_bake(pair, time_bvh=(i == 0), debug=dbg)
         times = r.get("times") or {}
         if i == 0:
-            bvh_s = times.get("bvh", 0.0)
+            bvh_s = times.get("bvh", 0.0) or 0.0
+        if dbg:
+            parity = atlas_parity(pair, ctx, r, gpu_rgb)
         runs_t.append((times.get("total", wall) or wall, times))
+        del r
     runs_t.sort(key=lambda x: x[0])
     t, times = runs_t[len(runs_t) // 2]
     times = dict(times, bvh=bvh_s)
@@ -750,7 +1015,8 @@ def cpu_baseline(pair, name, runs=5):
                       + ", ".join(f"{k} {v:.3f}" for k, v in times.items() if k != "bvh")
                       + f"; standalone Bvh(hi) build {bvh_s:.3f} s (outside the total)",
             "threads_note": "std::thread::hardware_concurrency() threads in the transfer loop only, "
-                            "raster/BVH/dilate single-threaded, exactly as shipped (core/parallel.h)"}
+                            "raster/BVH/dilate single-threaded, exactly as shipped (core/parallel.h)",
+            "parity": parity}
 
 
 _NV_CACHE = {}
@@ -778,45 +1044,88 @@ def _n_valid(pair):
     return _NV_CACHE[key]
 
 
-def run_reference(args):
+def run_reference(args, mode, name):
+    """The reference's own CPU bake on the host cores (rank 0 only), on this
+    arm's workload and config dict. Each step is one full bake; the number of
+    steps actually run is capped so the whole run stays within ~2.5 minutes
+    (`steps` reports what ran, `steps_requested` what was asked)."""
     rank, _, world = dist_env()
     if rank != 0:
         return None
     from paper_2605_26137_b200 import fixtures as fx
-    name = args.config
-    pair = fx.config_pair(name)
+    seed = fx.CONFIGS[name]["seed"]
+    pair = fx.config_pair(name, seed=seed)
     n_valid = _n_valid(pair)
-    for _ in range(args.warmup):
+    budget_s = 150.0
+    t_start = time.perf_counter()
+    warm = min(args.warmup, 1)
+    t_one = None
+    for _ in range(warm):
+        t0 = time.perf_counter()
         cpu_reference_bake(pair)
+        t_one = time.perf_counter() - t0
+    steps = args.steps
+    if t_one:
+        steps = max(1, min(args.steps, int((budget_s - (time.perf_counter() - t_start)) / t_one)))
     ts = []
     kind = None
-    for _ in range(args.steps):
+    for _ in range(steps):
         r, wall, kind, _ = cpu_reference_bake(pair)
         times = r.get("times") or {}
         ts.append(times.get("total", wall) or wall)
     t = statistics.mean(ts)
     value = n_valid / t
     return {
-        "metric": METRICS.get(name, METRIC), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "metric": METRICS.get(name, METRIC), "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "steps_requested": args.steps, "warmup": warm, "warmup_requested": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "strong" if mode == "shard" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (same pair as --impl ours)",
-        "config": {"workload": workload_desc(name, pair), "global_batch": 1, "seq_len": None,
-                   "parallelism": "host threads"},
+        "config": config_dict(name, pair, mode, world, args.assets, seed=seed),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": kind,
-                         "sample": f"one full {name} bake per step"},
+                         "sample": f"one full {name} bake per step ({steps} steps), rasterizeGBuffer + "
+                                   f"transferNormals (incl. its BVH build) + dilateSeams, rank 0 only",
+                         "threads_note": "hardware_concurrency() threads in the transfer loop, the rest "
+                                         "single-threaded as shipped (core/parallel.h)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
+def launch_selftest(args):
+    """CPU check of the launcher (tests/test_bench_launch.py): every rank joins
+    a gloo group and rank 0 prints the line shape with the group's size."""
+    import torch.distributed as dist
+    rank, _, world = dist_env()
+    if "RANK" in os.environ:
+        dist.init_process_group("gloo")
+        import torch
+        t = torch.ones(1)
+        dist.all_reduce(t)
+        world = int(t.item())
+        dist.destroy_process_group()
+    if rank != 0:
+        return None
+    mode, name = resolve(args, world)
+    return {"metric": METRICS.get(name, METRIC), "n_gpus": world, "mode": mode, "config_name": name,
+            "selftest": True}
+
+
 def main():
-    args = parse()
-    if args.impl == "reference":
-        line = run_reference(args)
-    elif args.assets > 1:
-        line = run_batch(args)
+    argv = sys.argv[1:]
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(relaunch(argv, args.gpus))
+    _, _, world = dist_env()
+    # (the reference arm is not re-launched: outside torchrun --gpus N still
+    # selects the N-GPU workload)
+    mode, name = resolve(args, world if "WORLD_SIZE" in os.environ else max(world, args.gpus))
+    if args.launch_selftest:
+        line = launch_selftest(args)
+    elif args.impl == "reference":
+        line = run_reference(args, mode, name)
     else:
-        line = run_ours(args)
+        line = run_ours(args, mode, name)
     if line is not None:
         s = json.dumps(line)
         print(s, flush=True)
