@@ -27,7 +27,7 @@ MF_HDRS := $(shell find include/meshforge -name '*.h' 2>/dev/null) include/eigen
 all: lib cpp peaks oracle
 
 lib: $(PKG)/libmfbake.so
-cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200 build/test_io_cpu
+cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200 build/test_io_cpu build/bench_api
 peaks: build/libmfpeaks.so
 
 build/cu/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
@@ -49,6 +49,11 @@ build/test_bake_b200: tests/cpp/test_bake_b200.cpp tests/cpp/doctest.h $(PKG)/li
 build/test_io_cpu: tests/cpp/test_io_cpu.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+# end-to-end timing of the reference-facing C++ API (bench.py e2e_api)
+build/bench_api: tools/bench_api.cpp $(PKG)/libmeshforge_b200.so
+	@mkdir -p build
+	$(CXX) $(CXXFLAGS) -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 # L2 / FP64 microbenchmarks (tools/peaks.cu) used by bench.py for the roofline peaks
 build/libmfpeaks.so: tools/peaks.cu

@@ -861,11 +861,42 @@ def run_e2e(args, d, ctx, pair):
                         "ms_median": statistics.median(times), "ms_min": min(times), "steps": steps}
     assert np.array_equal(out, out_pg)
     e2e = dict(res_out["pinned"])
+    api = run_e2e_api(pair, steps) if d.world == 1 else None
     e2e.update({"h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out.nbytes),
                 "call": "mf_bake_normal_map (host buffers, pinned) via ctypes",
                 "pageable": dict(res_out["pageable"], call="mf_bake_normal_map from pageable numpy arrays "
                                                            "(a drop-in caller's std::vector data)")})
+    if api is not None:
+        e2e["api"] = api
     return e2e
+
+
+def run_e2e_api(pair, steps):
+    """The reference-facing C++ API end to end (tools/bench_api.cpp through
+    libmeshforge_b200): TriangleMesh std::vectors in, ImageU8 out, wall clock,
+    the fused meshforge::bakeNormalMap and the reference's three-call
+    composition (each call round-trips its G-buffer / image through the host)."""
+    import tempfile
+    exe = os.path.join(ROOT, "build", "bench_api")
+    if not os.path.exists(exe):
+        return {"unavailable": f"{exe} not built"}
+    with tempfile.TemporaryDirectory() as tmp:
+        lo, hi = pair.lowpoly, pair.dense
+        for name, a, dt in (("lo_pos.f64", lo.positions, np.float64), ("lo_faces.i32", lo.faces, np.int32),
+                            ("lo_uvs.f64", lo.uvs, np.float64), ("lo_fuv.i32", lo.face_uvs, np.int32),
+                            ("hi_pos.f64", hi.positions, np.float64), ("hi_faces.i32", hi.faces, np.int32)):
+            np.ascontiguousarray(a, dtype=dt).tofile(os.path.join(tmp, name))
+        p = subprocess.run([exe, tmp, str(pair.res), repr(pair.bbox_diagonal), repr(pair.max_distance_fraction),
+                            "4", "3", str(steps)], capture_output=True, text=True, timeout=600)
+    if p.returncode != 0:
+        return {"unavailable": (p.stderr or p.stdout)[-300:]}
+    r = json.loads(p.stdout.strip().splitlines()[-1])
+    nv = _n_valid(pair)
+    r.update({"value": nv / (r["fused_ms_mean"] * 1e-3), "unit": UNIT,
+              "three_call_value": nv / (r["three_call_ms_mean"] * 1e-3),
+              "call": "meshforge::bakeNormalMap (C++ API, pageable std::vector meshes, ImageU8 out; wall clock) "
+                      "and dilateSeams(transferNormals(rasterizeGBuffer(lo, res), hi, diag, frac), g, 4)"})
+    return r
 
 
 def run_e2e_shard(args, d, ctx, pair, ranges, peer, gather):

@@ -26,6 +26,8 @@ struct mf_ctx;
 namespace mfb {
 
 // ---------------------------------------------------------------- context
+class HostPool;  // host_pool.h
+
 struct Ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -90,6 +92,9 @@ struct Ctx {
   };
   GraphSlot g_low, g_dense;
   void invalidate_graphs();  // drop every captured graph and capture key
+  // host worker threads staging pageable caller buffers (created on first use)
+  HostPool* pool = nullptr;
+  HostPool& host_pool();
   ~Ctx();
 };
 

@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "bake.cuh"
+#include "host_pool.h"
 
 namespace mfb {
 
@@ -109,6 +110,14 @@ cudaEvent_t Ctx::pool_event(int i) {
   return ev_pool[i];
 }
 
+HostPool& Ctx::host_pool() {
+  if (!pool) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    pool = new HostPool(static_cast<int>(std::min(8u, std::max(2u, hw / 2))));
+  }
+  return *pool;
+}
+
 void Ctx::invalidate_graphs() {
   if (bake_exec) cudaGraphExecDestroy(bake_exec);
   bake_exec = nullptr;
@@ -124,6 +133,7 @@ void Ctx::invalidate_graphs() {
 
 Ctx::~Ctx() {
   cudaSetDevice(device);
+  delete pool;  // idle: every entry point waits for its pool job
   if (bake_exec) cudaGraphExecDestroy(bake_exec);
   for (GraphSlot* g : {&g_low, &g_dense})
     if (g->exec) cudaGraphExecDestroy(g->exec);
@@ -296,12 +306,17 @@ size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 bool view_has_uvs(const mf_mesh_view* v) { return v->face_uvs && v->uvs && v->n_uvs > 0; }
 
-// Enqueues the H2D copies and the device validation of `v` on `s`; the
-// validation flags land in `*hflag` (pinned host memory) when `s` reaches
-// them. finish_upload() turns them into the mesh status after the caller has
-// synchronised.
-void upload_mesh_async(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* mesh, const char* scratch_tag,
-                       int* hflag, cudaStream_t s2 = nullptr) {
+// Device layout of an uploaded mesh: validates the view's sizes, allocates
+// (scratch or owned) and points mesh->m at the device arrays.
+struct MeshLayout {
+  double* pos = nullptr;
+  int32_t* faces = nullptr;
+  double* nrm = nullptr;
+  double* uvs = nullptr;
+  int32_t* fuv = nullptr;
+  int* flags = nullptr;
+};
+MeshLayout layout_mesh(Ctx& c, const mf_mesh_view* v, mf_mesh* mesh, const char* scratch_tag) {
   if (!v) throw ApiError(MF_ERR_BAD_ARGUMENT, "mesh view is null");
   if (v->n_vertices < 0 || v->n_faces < 0 || v->n_uvs < 0) throw ApiError(MF_ERR_BAD_ARGUMENT, "negative size");
   if ((v->n_vertices > 0 && !v->positions) || (v->n_faces > 0 && !v->faces))
@@ -329,49 +344,122 @@ void upload_mesh_async(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* m
     mesh->owns_mem = true;
   }
   char* p = static_cast<char*>(mesh->mem);
+  MeshLayout L;
+  L.pos = reinterpret_cast<double*>(p);
+  L.faces = reinterpret_cast<int32_t*>(p + bp);
+  L.nrm = has_n ? reinterpret_cast<double*>(p + bp + bf) : nullptr;
+  L.uvs = has_uv ? reinterpret_cast<double*>(p + bp + bf + bn) : nullptr;
+  L.fuv = has_uv ? reinterpret_cast<int32_t*>(p + bp + bf + bn + bu) : nullptr;
+  L.flags = reinterpret_cast<int*>(p + total - 256);
   DevMesh m;
   m.nv = v->n_vertices;
   m.nf = v->n_faces;
   m.nu = has_uv ? v->n_uvs : 0;
-  double* dpos = reinterpret_cast<double*>(p);
-  int32_t* dfac = reinterpret_cast<int32_t*>(p + bp);
-  double* dnrm = has_n ? reinterpret_cast<double*>(p + bp + bf) : nullptr;
-  double* duv = has_uv ? reinterpret_cast<double*>(p + bp + bf + bn) : nullptr;
-  int32_t* dfuv = has_uv ? reinterpret_cast<int32_t*>(p + bp + bf + bn + bu) : nullptr;
-  int* flags = reinterpret_cast<int*>(p + total - 256);
+  m.pos = L.pos;
+  m.faces = L.faces;
+  m.nrm = L.nrm;
+  m.uvs = L.uvs;
+  m.fuv = L.fuv;
+  mesh->m = m;
+  return L;
+}
+
+// Enqueues the H2D copies (positions and faces unless `staged`: a staged
+// upload already enqueued them) and the device validation of `v` on `s`;
+// the validation flags land in `*hflag` (pinned host memory) when `s`
+// reaches them. finish_upload() turns them into the mesh status after the
+// caller has synchronised.
+void copy_validate_async(Ctx& c, cudaStream_t s, const mf_mesh_view* v, const MeshLayout& L, DevMesh& m,
+                         int* hflag, cudaStream_t s2 = nullptr, bool staged = false) {
   // with s2, the face indices travel on a second stream concurrently with
   // the positions (two H2D streams measured 25 -> 32 GB/s on the box)
-  if (s2) {
-    MFB_CUDA_TRY(cudaEventRecord(c.up_fork, s));
-    MFB_CUDA_TRY(cudaStreamWaitEvent(s2, c.up_fork, 0));
+  if (!staged) {
+    if (s2) {
+      MFB_CUDA_TRY(cudaEventRecord(c.up_fork, s));
+      MFB_CUDA_TRY(cudaStreamWaitEvent(s2, c.up_fork, 0));
+    }
+    if (m.nv) MFB_CUDA_TRY(cudaMemcpyAsync(L.pos, v->positions, sizeof(double) * 3 * m.nv, cudaMemcpyHostToDevice, s));
+    if (m.nf)
+      MFB_CUDA_TRY(cudaMemcpyAsync(L.faces, v->faces, sizeof(int32_t) * 3 * m.nf, cudaMemcpyHostToDevice, s2 ? s2 : s));
   }
-  if (m.nv) MFB_CUDA_TRY(cudaMemcpyAsync(dpos, v->positions, sizeof(double) * 3 * m.nv, cudaMemcpyHostToDevice, s));
-  if (m.nf)
-    MFB_CUDA_TRY(cudaMemcpyAsync(dfac, v->faces, sizeof(int32_t) * 3 * m.nf, cudaMemcpyHostToDevice, s2 ? s2 : s));
   if (s2) {
     MFB_CUDA_TRY(cudaEventRecord(c.up_join, s2));
     MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.up_join, 0));
   }
-  if (has_n) MFB_CUDA_TRY(cudaMemcpyAsync(dnrm, v->normals, sizeof(double) * 3 * m.nv, cudaMemcpyHostToDevice, s));
-  if (has_uv) {
-    MFB_CUDA_TRY(cudaMemcpyAsync(duv, v->uvs, sizeof(double) * 2 * m.nu, cudaMemcpyHostToDevice, s));
-    MFB_CUDA_TRY(cudaMemcpyAsync(dfuv, v->face_uvs, sizeof(int32_t) * 3 * m.nf, cudaMemcpyHostToDevice, s));
+  if (L.nrm) MFB_CUDA_TRY(cudaMemcpyAsync(L.nrm, v->normals, sizeof(double) * 3 * m.nv, cudaMemcpyHostToDevice, s));
+  if (L.uvs) {
+    MFB_CUDA_TRY(cudaMemcpyAsync(L.uvs, v->uvs, sizeof(double) * 2 * m.nu, cudaMemcpyHostToDevice, s));
+    MFB_CUDA_TRY(cudaMemcpyAsync(L.fuv, v->face_uvs, sizeof(int32_t) * 3 * m.nf, cudaMemcpyHostToDevice, s));
   }
-  MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int), s));
+  MFB_CUDA_TRY(cudaMemsetAsync(L.flags, 0, sizeof(int), s));
   const int64_t work = std::max<int64_t>(3ll * m.nv, 3ll * m.nf);
   if (work > 0) {
     const int grid = static_cast<int>(std::min<int64_t>(div_up(work, 256), kNumSMs * 16));
-    k_validate<<<grid, 256, 0, s>>>(dpos, m.nv, dfac, m.nf, dfuv, m.nu, flags);
+    k_validate<<<grid, 256, 0, s>>>(L.pos, m.nv, L.faces, m.nf, L.fuv, m.nu, L.flags);
     c.count_launch();
     MFB_CUDA_TRY(cudaGetLastError());
   }
-  MFB_CUDA_TRY(cudaMemcpyAsync(hflag, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
-  m.pos = dpos;
-  m.faces = dfac;
-  m.nrm = dnrm;
-  m.uvs = duv;
-  m.fuv = dfuv;
-  mesh->m = m;
+  MFB_CUDA_TRY(cudaMemcpyAsync(hflag, L.flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+}
+
+void upload_mesh_async(Ctx& c, cudaStream_t s, const mf_mesh_view* v, mf_mesh* mesh, const char* scratch_tag,
+                       int* hflag, cudaStream_t s2 = nullptr) {
+  const MeshLayout L = layout_mesh(c, v, mesh, scratch_tag);
+  copy_validate_async(c, s, v, L, mesh->m, hflag, s2);
+}
+
+// Pageable host -> device through the context's pinned staging buffer: the
+// context's host pool copies 1 MiB chunks into it and enqueues each chunk's
+// DMA on the piece's stream right behind the copy, so host copies overlap
+// the DMAs (a pageable cudaMemcpyAsync runs both serially on the calling
+// thread). Returns once the job is started; c.host_pool().wait() ends it,
+// after which every chunk's DMA is enqueued.
+struct H2DPiece {
+  void* dst;
+  const void* src;
+  size_t bytes;
+  cudaStream_t s;
+};
+void staged_h2d_start(Ctx& c, const std::vector<H2DPiece>& pieces, const char* tag) {
+  struct Chunk {
+    char* dst;
+    const char* src;
+    size_t len, soff;
+    cudaStream_t s;
+  };
+  constexpr size_t kChunk = 1 << 20;
+  auto chunks = std::make_shared<std::vector<Chunk>>();
+  size_t total = 0;
+  for (const H2DPiece& p : pieces) {
+    for (size_t off = 0; off < p.bytes; off += kChunk) {
+      const size_t len = std::min(kChunk, p.bytes - off);
+      chunks->push_back({static_cast<char*>(p.dst) + off, static_cast<const char*>(p.src) + off, len, total, p.s});
+      total += len;
+    }
+    total = align_up(total, 256);
+  }
+  char* stage = static_cast<char*>(c.host_buf(tag, std::max<size_t>(total, 1)));
+  // interleave the pieces so both streams' DMAs start early
+  std::stable_sort(chunks->begin(), chunks->end(), [&](const Chunk& a, const Chunk& b) {
+    auto rank = [&](const Chunk& k) {
+      for (const H2DPiece& p : pieces)
+        if (k.src >= static_cast<const char*>(p.src) && k.src < static_cast<const char*>(p.src) + p.bytes)
+          return static_cast<size_t>(k.src - static_cast<const char*>(p.src));
+      return size_t(0);
+    };
+    return rank(a) < rank(b);
+  });
+  const int dev = c.device;
+  c.host_pool().start(static_cast<int>(chunks->size()), [chunks, stage, dev](int i) {
+    thread_local int cur = -1;
+    if (cur != dev) {
+      MFB_CUDA_TRY(cudaSetDevice(dev));
+      cur = dev;
+    }
+    const Chunk& k = (*chunks)[i];
+    std::memcpy(stage + k.soff, k.src, k.len);
+    MFB_CUDA_TRY(cudaMemcpyAsync(k.dst, stage + k.soff, k.len, cudaMemcpyHostToDevice, k.s));
+  });
 }
 
 // validateMesh (core/mesh.cpp:37-48) outcome from the device flags.
@@ -481,6 +569,8 @@ QueryList query_list(Ctx& c, int64_t capacity) {
   q.count = c.buf<int>("q.count", 4);  // [0] pass A, [1] pass B
   return q;
 }
+
+constexpr int kBandEventBase = 80;  // pool events 80 .. 80 + kMaxBands - 1: band downloads
 
 // Everything the fused bake enqueues; no host synchronisation inside, so
 // the same sequence can be captured into a CUDA graph.
@@ -613,6 +703,7 @@ struct BakeEnq {
   bool band_sync = false;
   BandSync bs;
   int* band_check = nullptr;  // pinned [nb]: ready flags before the release (MFB_BAND_CHECK)
+  int band_ev_base = -1;      // >= 0: record pool event base + b after band b's download
 
   BakeEnq(Ctx& cc, const mf_mesh* l, const mf_mesh* h, int rs, double dg, double fr, int rad, int b0, int b1,
           uint8_t* out, bool dbg, Timer& t, BakeMarks& m, const OutSet* pb = nullptr)
@@ -787,6 +878,7 @@ struct BakeEnq {
         stream_wait_value(cp, bs.ready + b);
         const int64_t off = 3ll * r0 * res;
         MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off, 3ll * (r1 - r0) * res, cudaMemcpyDeviceToHost, cp));
+        if (band_ev_base >= 0) MFB_CUDA_TRY(cudaEventRecord(c.pool_event(band_ev_base + b), cp));
       }
       MFB_CUDA_TRY(cudaEventRecord(c.join4, cp));
       MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join4, 0));
@@ -1023,14 +1115,54 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   // after the lowpoly work is queued.
   const bool early = host_pinned(hv->positions) && host_pinned(hv->faces) && host_pinned(hv->normals);
   MFB_CUDA_TRY(cudaEventRecord(c.fork, s));  // the caller's earlier work on the ctx stream
+  // Pageable dense arrays (a drop-in caller's std::vectors) are staged
+  // through the context's pinned buffer by its host pool, starting now: the
+  // chunk copies and their DMAs run while this thread uploads and checks the
+  // lowpoly and queues its work.
+  const bool staged = !early && hv->n_vertices > 0 && hv->n_faces > 0 && c.aux;
+  struct PoolGuard {
+    Ctx& c;
+    bool on = false;
+    void wait() {
+      if (on) {
+        on = false;
+        c.host_pool().wait();
+      }
+    }
+    ~PoolGuard() {
+      try {
+        wait();
+      } catch (...) {
+      }
+    }
+  } pool_job{c};
+  MeshLayout hiL;
+  if (staged) {
+    MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.fork, 0));
+    MFB_CUDA_TRY(cudaStreamWaitEvent(c.aux, c.fork, 0));
+    hiL = layout_mesh(c, hv, &hi, "up.hi");
+    staged_h2d_start(c,
+                     {{hiL.pos, hv->positions, sizeof(double) * 3 * static_cast<size_t>(hv->n_vertices), c.side},
+                      {hiL.faces, hv->faces, sizeof(int32_t) * 3 * static_cast<size_t>(hv->n_faces), c.aux}},
+                     "stage.hi");
+    pool_job.on = true;
+  }
   auto upload_hi = [&] {
     MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.fork, 0));
-    upload_mesh_async(c, c.side, hv, &hi, "up.hi", hup + 1, c.aux ? c.aux : nullptr);
+    if (staged) {
+      pool_job.wait();  // every chunk's DMA is enqueued
+      copy_validate_async(c, c.side, hv, hiL, hi.m, hup + 1, c.aux, true);
+    } else {
+      upload_mesh_async(c, c.side, hv, &hi, "up.hi", hup + 1, c.aux ? c.aux : nullptr);
+    }
     MFB_CUDA_TRY(cudaEventRecord(c.hi_ready, c.side));
   };
   auto drain = [&] {
-    cudaStreamSynchronize(c.side);
-    cudaStreamSynchronize(s);
+    try {
+      pool_job.wait();
+    } catch (...) {
+    }
+    c.sync_all();
   };
   try {
     upload_mesh_async(c, s, lv, &lo, "up.lo", hup);
@@ -1047,7 +1179,12 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   BakeMarks mk;
   Timer tmb(c, 8);
   BakeEnq q(c, &lo, &hi, res, diag, frac, radius, 0, res, drgb, false, tmb, mk);
-  if (q.links && host_pinned(rgb_out) && wait_value_usable(c)) {
+  // A pageable rgb_out gets the atlas through pinned staging: its row bands
+  // are copied out by the host pool as their DMAs land.
+  const bool stage_out = !host_pinned(rgb_out);
+  uint8_t* host_dst = stage_out ? static_cast<uint8_t*>(c.host_buf("stage.rgb", 3 * static_cast<size_t>(res) * res))
+                                : rgb_out;
+  if (q.links && wait_value_usable(c)) {
     q.band_sync = true;
     int* bb = c.buf<int>("bake.bands", 4 * kMaxBands);
     q.bs.tot = bb;
@@ -1062,6 +1199,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     q.bs.nb = div_up(res, q.bs.rows);
     const char* chk = std::getenv("MFB_BAND_CHECK");
     if (chk && chk[0] == '1') q.band_check = static_cast<int*>(c.host_buf("bake.bandcheck", kMaxBands * sizeof(int)));
+    if (stage_out) q.band_ev_base = kBandEventBase;
   }
   static const bool graphs = [] {
     const char* e = std::getenv("MFB_GRAPH");
@@ -1103,9 +1241,37 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   }
   q.dense_side(use_graphs);
   cudaEvent_t t2 = tm.mark(s);
-  q.tail(hflags, hcnt, rgb_out);
+  q.tail(hflags, hcnt, host_dst);
+  const int64_t row_bytes = 3ll * res;
+  if (stage_out && q.band_sync) {
+    const int dev = c.device, nb = q.bs.nb, rows = q.bs.rows;
+    std::vector<cudaEvent_t> ev(nb);
+    for (int b = 0; b < nb; ++b) ev[b] = c.pool_event(kBandEventBase + b);
+    c.host_pool().start(nb, [=](int b) {
+      thread_local int cur = -1;
+      if (cur != dev) {
+        MFB_CUDA_TRY(cudaSetDevice(dev));
+        cur = dev;
+      }
+      MFB_CUDA_TRY(cudaEventSynchronize(ev[b]));
+      const int r0 = b * rows, r1 = std::min(res, r0 + rows);
+      std::memcpy(rgb_out + r0 * row_bytes, host_dst + r0 * row_bytes, (r1 - r0) * row_bytes);
+    });
+    pool_job.on = true;
+  }
   cudaEvent_t t3 = tm.mark(s);
   MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  if (stage_out) {
+    if (q.band_sync) {
+      pool_job.wait();
+    } else {
+      constexpr int kRows = 64;
+      c.host_pool().run(static_cast<int>(div_up(res, kRows)), [=](int b) {
+        const int r0 = b * kRows, r1 = std::min(res, r0 + kRows);
+        std::memcpy(rgb_out + r0 * row_bytes, host_dst + r0 * row_bytes, (r1 - r0) * row_bytes);
+      });
+    }
+  }
   if (spec) {
     finish_upload(&hi, hup[1]);
     if (hi.status != MF_OK) {
