@@ -45,6 +45,11 @@ struct Ctx {
   cudaEvent_t hi_ready = nullptr;   // host entry point: dense mesh uploaded and validated
   cudaEvent_t dfork = nullptr, djoin = nullptr;  // host entry point: dense phase side -> aux -> side
   cudaEvent_t up_fork = nullptr, up_join = nullptr;  // split H2D of one mesh over two streams
+  // staged (pageable) dense upload: the host pool's chunk DMAs go to these two
+  // streams, which no captured bake graph touches (a capture of the lowpoly
+  // branch runs while the pool is still enqueueing)
+  cudaStream_t up1 = nullptr, up2 = nullptr;
+  cudaEvent_t up1_done = nullptr, up2_done = nullptr;
   bool timing = false;
   bool capturing = false;  // a graph capture of this context's streams is open
   int64_t launches = 0;

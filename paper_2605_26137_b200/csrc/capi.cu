@@ -77,6 +77,8 @@ void Ctx::sync_all() {
   if (aux2) MFB_CUDA_TRY(cudaStreamSynchronize(aux2));
   if (lowhi) MFB_CUDA_TRY(cudaStreamSynchronize(lowhi));
   if (dn) MFB_CUDA_TRY(cudaStreamSynchronize(dn));
+  if (up1) MFB_CUDA_TRY(cudaStreamSynchronize(up1));
+  if (up2) MFB_CUDA_TRY(cudaStreamSynchronize(up2));
 }
 void* Ctx::cub_temp(size_t bytes, cudaStream_t s) {
   const int slot = s == side    ? 1
@@ -145,12 +147,16 @@ Ctx::~Ctx() {
   if (aux2) cudaStreamSynchronize(aux2);
   if (lowhi) cudaStreamSynchronize(lowhi);
   if (dn) cudaStreamSynchronize(dn);
+  if (up1) cudaStreamSynchronize(up1);
+  if (up2) cudaStreamSynchronize(up2);
   for (auto& kv : scratch) cudaFree(kv.second.ptr);
   for (auto& kv : pinned) cudaFreeHost(kv.second.ptr);
   for (void* p : cub_tmp)
     if (p) cudaFree(p);
-  for (cudaEvent_t e : {fork, join, fork2, join2, join3, hi_ready, dfork, djoin, up_fork, up_join, lfork, ljoin, setup_done, join4, lowfork, lowjoin})
+  for (cudaEvent_t e : {fork, join, fork2, join2, join3, hi_ready, dfork, djoin, up_fork, up_join, lfork, ljoin, setup_done, join4, lowfork, lowjoin, up1_done, up2_done})
     if (e) cudaEventDestroy(e);
+  if (up1) cudaStreamDestroy(up1);
+  if (up2) cudaStreamDestroy(up2);
   if (side) cudaStreamDestroy(side);
   if (aux) cudaStreamDestroy(aux);
   if (side2) cudaStreamDestroy(side2);
@@ -1119,7 +1125,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   // through the context's pinned buffer by its host pool, starting now: the
   // chunk copies and their DMAs run while this thread uploads and checks the
   // lowpoly and queues its work.
-  const bool staged = !early && hv->n_vertices > 0 && hv->n_faces > 0 && c.aux;
+  const bool staged = !early && hv->n_vertices > 0 && hv->n_faces > 0 && c.up1;
   struct PoolGuard {
     Ctx& c;
     bool on = false;
@@ -1138,12 +1144,12 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   } pool_job{c};
   MeshLayout hiL;
   if (staged) {
-    MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.fork, 0));
-    MFB_CUDA_TRY(cudaStreamWaitEvent(c.aux, c.fork, 0));
+    MFB_CUDA_TRY(cudaStreamWaitEvent(c.up1, c.fork, 0));
+    MFB_CUDA_TRY(cudaStreamWaitEvent(c.up2, c.fork, 0));
     hiL = layout_mesh(c, hv, &hi, "up.hi");
     staged_h2d_start(c,
-                     {{hiL.pos, hv->positions, sizeof(double) * 3 * static_cast<size_t>(hv->n_vertices), c.side},
-                      {hiL.faces, hv->faces, sizeof(int32_t) * 3 * static_cast<size_t>(hv->n_faces), c.aux}},
+                     {{hiL.pos, hv->positions, sizeof(double) * 3 * static_cast<size_t>(hv->n_vertices), c.up1},
+                      {hiL.faces, hv->faces, sizeof(int32_t) * 3 * static_cast<size_t>(hv->n_faces), c.up2}},
                      "stage.hi");
     pool_job.on = true;
   }
@@ -1151,7 +1157,11 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.fork, 0));
     if (staged) {
       pool_job.wait();  // every chunk's DMA is enqueued
-      copy_validate_async(c, c.side, hv, hiL, hi.m, hup + 1, c.aux, true);
+      MFB_CUDA_TRY(cudaEventRecord(c.up1_done, c.up1));
+      MFB_CUDA_TRY(cudaEventRecord(c.up2_done, c.up2));
+      MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.up1_done, 0));
+      MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.up2_done, 0));
+      copy_validate_async(c, c.side, hv, hiL, hi.m, hup + 1, nullptr, true);
     } else {
       upload_mesh_async(c, c.side, hv, &hi, "up.hi", hup + 1, c.aux ? c.aux : nullptr);
     }
@@ -1366,10 +1376,12 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, lo_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up1, cudaStreamNonBlocking, hi_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up2, cudaStreamNonBlocking, hi_prio));
     for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3, &ctx->c.hi_ready,
                             &ctx->c.dfork, &ctx->c.djoin, &ctx->c.up_fork, &ctx->c.up_join, &ctx->c.lfork,
                             &ctx->c.ljoin, &ctx->c.setup_done, &ctx->c.join4, &ctx->c.lowfork,
-                            &ctx->c.lowjoin})
+                            &ctx->c.lowjoin, &ctx->c.up1_done, &ctx->c.up2_done})
       MFB_CUDA_TRY(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     *out = ctx.release();
     return MF_OK;

@@ -1197,8 +1197,10 @@ __global__ void __launch_bounds__(128) k_zbuf_faces(const double* __restrict__ p
       const double bv = dot(dir, qv) * inv;
       if (bv < 0.0 || bu + bv > 1.0) continue;
       const double t = dot(e2, qv) * inv;
+      // + 0.0f maps -0 to +0: the reference's `depth > stored` treats the two
+      // as equal (ties go to the lower face), so they must share one key
       const unsigned long long key =
-          (static_cast<unsigned long long>(ordered_f32(__double2float_rn(-t))) << 32) | fkey;
+          (static_cast<unsigned long long>(ordered_f32(__fadd_rn(__double2float_rn(-t), 0.0f))) << 32) | fkey;
       unsigned long long* z = zb + static_cast<int64_t>(py) * res + px;
       if (key > *z) atomicMax(z, key);
     }
