@@ -75,6 +75,11 @@ struct Ctx {
   void* cub_temp(size_t bytes, cudaStream_t s);
   void sync_all();  // drain every stream of the context
   void count_launch(int n = 1) { launches += n; }
+  // Byte fill as a kernel (capi.cu). Inside the bake's captured graphs
+  // memset nodes run on the copy engine one after another, each a few us
+  // apart, and delayed the lowpoly branch's start by ~35 us (r02 CUPTI
+  // timeline); a fill kernel runs beside the other branches' kernels.
+  void fill(void* p, int value, size_t bytes, cudaStream_t s);
 
   // Every scratch (re)allocation bumps the generation: a captured CUDA graph
   // is replayed only while the buffers it references are unchanged.

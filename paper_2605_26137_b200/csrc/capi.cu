@@ -28,6 +28,13 @@
 #include "bake.cuh"
 #include "host_pool.h"
 
+#ifndef MFB_LOWPOLY_PRIO_DELTA
+#define MFB_LOWPOLY_PRIO_DELTA 1  // lowpoly branch streams: this many levels below the LBVH's
+#endif
+#ifndef MFB_DN_PRIO_MID
+#define MFB_DN_PRIO_MID 0  // dense vertex normals at the lowpoly branch's level (else the lowest)
+#endif
+
 namespace mfb {
 
 thread_local std::string g_last_error;
@@ -110,6 +117,31 @@ cudaEvent_t Ctx::pool_event(int i) {
     ev_pool.push_back(e);
   }
   return ev_pool[i];
+}
+
+namespace {
+__global__ void k_fill(uint32_t* __restrict__ w, size_t nw, uint32_t v, uint8_t* __restrict__ tail, int ntail) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nw; i += stride) w[i] = v;
+  if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < ntail) tail[threadIdx.x] = static_cast<uint8_t>(v);
+}
+}  // namespace
+
+void Ctx::fill(void* p, int value, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  // scratch buffers are 256-byte aligned: whole words, then the byte tail
+  if (reinterpret_cast<uintptr_t>(p) & 3) {
+    MFB_CUDA_TRY(cudaMemsetAsync(p, value, bytes, s));
+    return;
+  }
+  const uint32_t b = static_cast<uint8_t>(value);
+  const uint32_t v = b | (b << 8) | (b << 16) | (b << 24);
+  const size_t nw = bytes / 4;
+  const int ntail = static_cast<int>(bytes - 4 * nw);
+  const int grid = static_cast<int>(std::min<size_t>(std::max<size_t>(1, (nw + 255) / 256), kNumSMs * 4));
+  k_fill<<<grid, 256, 0, s>>>(static_cast<uint32_t*>(p), nw, v, static_cast<uint8_t*>(p) + 4 * nw, ntail);
+  count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
 }
 
 HostPool& Ctx::host_pool() {
@@ -397,7 +429,7 @@ void copy_validate_async(Ctx& c, cudaStream_t s, const mf_mesh_view* v, const Me
     MFB_CUDA_TRY(cudaMemcpyAsync(L.uvs, v->uvs, sizeof(double) * 2 * m.nu, cudaMemcpyHostToDevice, s));
     MFB_CUDA_TRY(cudaMemcpyAsync(L.fuv, v->face_uvs, sizeof(int32_t) * 3 * m.nf, cudaMemcpyHostToDevice, s));
   }
-  MFB_CUDA_TRY(cudaMemsetAsync(L.flags, 0, sizeof(int), s));
+  c.fill(L.flags, 0, sizeof(int), s);
   const int64_t work = std::max<int64_t>(3ll * m.nv, 3ll * m.nf);
   if (work > 0) {
     const int grid = static_cast<int>(std::min<int64_t>(div_up(work, 256), kNumSMs * 16));
@@ -744,8 +776,8 @@ struct BakeEnq {
   // raster (valid mask, raw map, query list)
   void low() {
     cudaStream_t m = c.stream;
-    MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), m));
-    MFB_CUDA_TRY(cudaMemsetAsync(counters, 0, 4 * sizeof(unsigned long long), m));
+    c.fill(flags, 0, 4 * sizeof(int), m);
+    c.fill(counters, 0, 4 * sizeof(unsigned long long), m);
     // the lowpoly branch on the context's high-priority stream (the caller's
     // stream has whatever priority the caller gave it), joined back to main
     cudaStream_t s = c.lowhi ? c.lowhi : m;
@@ -754,7 +786,7 @@ struct BakeEnq {
       MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.lowfork, 0));
     }
     if (band_sync) {
-      MFB_CUDA_TRY(cudaMemsetAsync(bs.tot, 0, 4 * kMaxBands * sizeof(int), s));
+      c.fill(bs.tot, 0, 4 * kMaxBands * sizeof(int), s);
       fo.band_tot = bs.tot;
       fo.band_rows = bs.rows;
     }
@@ -876,7 +908,7 @@ struct BakeEnq {
       if (band_check) {
         MFB_CUDA_TRY(cudaMemcpyAsync(band_check, bs.ready, bs.nb * sizeof(int), cudaMemcpyDeviceToHost, s));
       }
-      MFB_CUDA_TRY(cudaMemsetAsync(bs.ready, 1, bs.nb * sizeof(int), s));
+      c.fill(bs.ready, 1, bs.nb * sizeof(int), s);
       mk.e5 = tm.mark(s);
       MFB_CUDA_TRY(cudaStreamWaitEvent(cp, ev, 0));
       for (int b = 0; b < bs.nb; ++b) {
@@ -1370,12 +1402,18 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     // priority as well as the LBVH's; the dense normals stay low. With the
     // segment-tree LBVH the lowpoly branch is the longer chain: 1.431 ->
     // 1.401 ms (with the refit climb it was the reverse: 1.52 vs 1.505 ms).
+    // r02: three levels. With equal priorities the coverage kernel's 16k
+    // CTAs (queued first) held the SMs while the LBVH's repack and emission
+    // waited ~70-100 us behind them (CUPTI timeline, tools/timeline.py): the
+    // LBVH chain (the long pole) now outranks the lowpoly branch, which
+    // fills in around it.
+    const int mid_prio = std::min(lo_prio, hi_prio + MFB_LOWPOLY_PRIO_DELTA);
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, hi_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux, cudaStreamNonBlocking, hi_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux, cudaStreamNonBlocking, mid_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, hi_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, hi_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, hi_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, lo_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, mid_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, mid_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, MFB_DN_PRIO_MID ? mid_prio : lo_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up1, cudaStreamNonBlocking, hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up2, cudaStreamNonBlocking, hi_prio));
     for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3, &ctx->c.hi_ready,

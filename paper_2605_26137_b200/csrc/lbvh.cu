@@ -86,6 +86,11 @@ __global__ void k_bounds(const double* __restrict__ pos, int nv, unsigned long l
   }
 }
 
+// min slots (0..2) to all-ones, max / |max| slots (3..7) to zero
+__global__ void k_acc_init(unsigned long long* acc) {
+  if (threadIdx.x < 8) acc[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
+}
+
 __device__ __forceinline__ uint32_t spread10(uint32_t v) {
   v &= 0x3ffu;
   v = (v | (v << 16)) & 0x030000ffu;
@@ -627,15 +632,15 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   auto* starts = ctx.buf<int32_t>(tag + ".starts", n);
   auto* starts_n = ctx.buf<int>(tag + ".starts_n", 1);
 
-  MFB_CUDA_TRY(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(acc + 3, 0x00, 5 * sizeof(unsigned long long), s));
+  k_acc_init<<<1, 32, 0, s>>>(acc);
+  ctx.count_launch();
   // segment-tree node boxes (MFB_SEGTREE=0: the bottom-up refit climb)
   static const bool segtree = [] {
     const char* e = std::getenv("MFB_SEGTREE");
     return !(e && e[0] == '0');
   }();
   const bool use_seg = segtree && n > 1;
-  if (out.n_nodes > 0 && !use_seg) MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, sizeof(int) * out.n_nodes, s));
+  if (out.n_nodes > 0 && !use_seg) ctx.fill(flags, 0, sizeof(int) * out.n_nodes, s);
 
   const int T = 256;
   const int grid_b = std::min(div_up(std::max(n, m.nv), T), kNumSMs * 8);
@@ -697,7 +702,7 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   }
   if (rs != s) MFB_CUDA_TRY(cudaEventRecord(ctx.ljoin, rs));
   if (n > 1) {
-    MFB_CUDA_TRY(cudaMemsetAsync(starts_n, 0, sizeof(int), s));
+    ctx.fill(starts_n, 0, sizeof(int), s);
     k_emit<<<div_up(n - 1, T), T, 0, s>>>(keys2, n, leaf_max, out.nodes, prim_parent, node_parent, starts,
                                           starts_n, use_seg ? 1 : 0);
     ctx.count_launch();

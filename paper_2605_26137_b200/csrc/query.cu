@@ -1246,10 +1246,10 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
   unsigned long long* pbuf = nullptr;
   if (prof) {
     pbuf = ctx.buf<unsigned long long>("xfer.prof", 8);
-    MFB_CUDA_TRY(cudaMemsetAsync(pbuf, 0, 8 * sizeof(unsigned long long), s));
-    MFB_CUDA_TRY(cudaMemsetAsync(pbuf + 4, 0xff, 2 * sizeof(unsigned long long), s));
+    ctx.fill(pbuf, 0, 8 * sizeof(unsigned long long), s);
+    ctx.fill(pbuf + 4, 0xff, 2 * sizeof(unsigned long long), s);
   }
-  if (kSeedPasses) MFB_CUDA_TRY(cudaMemsetAsync(a.face_map, 0xff, sizeof(int) * a.face_map_size, s));
+  if (kSeedPasses) ctx.fill(a.face_map, 0xff, sizeof(int) * a.face_map_size, s);
   static const int bps = occupancy(k_transfer_t<false, false>);
   const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
 #define MFB_XFER_T(D, P, PASS)                                                                                \
@@ -1320,8 +1320,8 @@ void raycast_brute(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double* o, 
 
 void vertex_bounds(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out6) {
   auto* acc = ctx.buf<unsigned long long>("vb.acc", 6);
-  MFB_CUDA_TRY(cudaMemsetAsync(acc, 0xff, 3 * sizeof(unsigned long long), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(acc + 3, 0x00, 3 * sizeof(unsigned long long), s));
+  ctx.fill(acc, 0xff, 3 * sizeof(unsigned long long), s);
+  ctx.fill(acc + 3, 0x00, 3 * sizeof(unsigned long long), s);
   if (m.nv > 0) {
     k_vertex_bounds<<<std::min(div_up(m.nv, 256), kNumSMs * 4), 256, 0, s>>>(m.pos, m.nv, acc);
     ctx.count_launch();
@@ -1428,7 +1428,7 @@ void raster_visibility(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double*
   auto* zb = ctx.buf<unsigned long long>("view.zbuf", static_cast<size_t>(std::min(group, nviews)) * px);
   for (int v0 = 0; v0 < nviews; v0 += group) {
     const int nv = std::min(group, nviews - v0);
-    MFB_CUDA_TRY(cudaMemsetAsync(zb, 0, sizeof(unsigned long long) * nv * px, s));
+    ctx.fill(zb, 0, sizeof(unsigned long long) * nv * px, s);
     k_zbuf_faces<<<dim3(div_up(m.nf, 128), nv), 128, 0, s>>>(m.pos, m.faces, m.nf, dc + v0, res, 0, zb);
     k_zbuf_hits<<<kNumSMs * 8, 256, 0, s>>>(zb, nv * px, hits);
     ctx.count_launch(2);
@@ -1438,7 +1438,7 @@ void raster_visibility(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double*
 
 double center_mesh(Ctx& ctx, cudaStream_t s, const DevMesh& m, const double center[3], double* out) {
   auto* acc = ctx.buf<unsigned long long>("ctr.acc", 1);
-  MFB_CUDA_TRY(cudaMemsetAsync(acc, 0, sizeof(unsigned long long), s));
+  ctx.fill(acc, 0, sizeof(unsigned long long), s);
   if (m.nv > 0) {
     k_center_mesh<<<std::min(div_up(m.nv, 256), kNumSMs * 4), 256, 0, s>>>(m.pos, m.nv, center[0], center[1],
                                                                             center[2], out, acc);

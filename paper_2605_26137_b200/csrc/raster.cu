@@ -473,8 +473,9 @@ __global__ void k_bin_count(const RasterFace* __restrict__ rf, int nf, int row_b
 }
 __global__ void k_bin_fill(const RasterFace* __restrict__ rf, int nf, int row_begin, int row_end,
                            int tiles_x, const int* __restrict__ tile_start, int* __restrict__ cursor,
-                           int* __restrict__ bins, int capacity, int* __restrict__ overflow) {
+                           int* __restrict__ bins, int capacity, int* __restrict__ overflow, int ntiles) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f == 0) overflow[1] = tile_start[ntiles];  // the bins' exact total (flags[2])
   if (f >= nf) return;
   int tx0, tx1, ty0, ty1;
   if (!face_tiles(rf[f], row_begin, row_end, tx0, tx1, ty0, ty1)) return;
@@ -853,12 +854,11 @@ void corner_csr(Ctx& ctx, cudaStream_t s, const DevMesh& m, const std::string& t
                 int** list_out) {
   const int T = 256;
   const int nc = 3 * m.nf;
-  int* cnt = ctx.buf<int>(tag + ".csr.cnt", m.nv + 1);
+  int* cnt = ctx.buf<int>(tag + ".csr.cc", 2 * (m.nv + 1));  // counts, then fill cursors: one fill
+  int* cursor = cnt + m.nv + 1;
   int* start = ctx.buf<int>(tag + ".csr.start", m.nv + 1);
-  int* cursor = ctx.buf<int>(tag + ".csr.cursor", m.nv + 1);
   int* list = ctx.buf<int>(tag + ".csr.list", nc);
-  MFB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (m.nv + 1), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (m.nv + 1), s));
+  ctx.fill(cnt, 0, sizeof(int) * 2 * (m.nv + 1), s);
   k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
@@ -894,13 +894,12 @@ void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, boo
   }
   // unsorted CSR + in-register ordering inside the summation kernel
   const int nc = 3 * m.nf;
-  int* cnt = ctx.buf<int>(tag + ".csr.cnt", m.nv + 1);
+  int* cnt = ctx.buf<int>(tag + ".csr.cc", 2 * (m.nv + 1));  // counts, then fill cursors: one fill
+  int* cursor = cnt + m.nv + 1;
   int* start = ctx.buf<int>(tag + ".csr.start", m.nv + 1);
-  int* cursor = ctx.buf<int>(tag + ".csr.cursor", m.nv + 1);
   int* list = ctx.buf<int>(tag + ".csr.list", nc);
   double* av = ctx.buf<double>(tag + ".vn.av", 3 * static_cast<size_t>(m.nf));
-  MFB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (m.nv + 1), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (m.nv + 1), s));
+  ctx.fill(cnt, 0, sizeof(int) * 2 * (m.nv + 1), s);
   k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
@@ -967,13 +966,12 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
   double* uv_area = ctx.buf<double>("lo.rel.uvarea", nf);
   double* ratio = ctx.buf<double>("lo.rel.ratio", nf);
   int* island = ctx.buf<int>("lo.rel.island", nf);
-  int* count = ctx.buf<int>("lo.rel.count", nu + 1);
+  int* count = ctx.buf<int>("lo.rel.cc", 2 * (nu + 1));  // counts, then fill cursors: one fill
+  int* cursor = count + nu + 1;
   int* start = ctx.buf<int>("lo.rel.start", nu + 1);
-  int* cursor = ctx.buf<int>("lo.rel.cursor", nu + 1);
   auto* items = ctx.buf<unsigned long long>("lo.rel.items", nf);
   double* median = ctx.buf<double>("lo.rel.median", nu);
-  MFB_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int) * (nu + 1), us));
-  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (nu + 1), us));
+  ctx.fill(count, 0, sizeof(int) * 2 * (nu + 1), us);
   k_iota<<<div_up(nu, T), T, 0, us>>>(nu, parent);
   k_uf_unite<<<div_up(nf, T), T, 0, us>>>(lo.fuv, nf, parent);
   k_uf_flatten<<<div_up(nu, T), T, 0, us>>>(nu, parent);
@@ -1008,24 +1006,22 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
   const int ntiles = tiles_x * tiles_y;
   auto* rf = static_cast<const RasterFace*>(plan.faces);
   auto* attrs = static_cast<const AttrFace*>(plan.attrs);
-  int* cnt = ctx.buf<int>("ras.cnt", ntiles + 1);
+  int* cnt = ctx.buf<int>("ras.cc", 2 * (ntiles + 1));  // counts, then fill cursors: one fill
+  int* cursor = cnt + ntiles + 1;
   int* start = ctx.buf<int>("ras.start", ntiles + 1);
-  int* cursor = ctx.buf<int>("ras.cursor", ntiles + 1);
   // Bin capacity: a bound that holds for ordinary atlases; the bake driver
   // re-runs with the exact total (flags[1] set, total in flags[2]) otherwise.
   const int64_t cap64 = std::max<int64_t>(ctx.bin_capacity, 8ll * plan.nf + 4ll * ntiles + 1024);
   const int capacity = static_cast<int>(std::min<int64_t>(cap64, 0x7fffffff));
   int* bins = ctx.buf<int>("ras.bins", capacity);
-  MFB_CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(int) * (ntiles + 1), s));
-  MFB_CUDA_TRY(cudaMemsetAsync(cursor, 0, sizeof(int) * (ntiles + 1), s));
+  ctx.fill(cnt, 0, sizeof(int) * 2 * (ntiles + 1), s);
   k_bin_count<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, cnt);
   size_t tmp = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, ntiles + 1, s);
   MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, start, ntiles + 1, s));
   k_bin_fill<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, start, cursor, bins,
-                                              capacity, flags_dev + 1);
-  MFB_CUDA_TRY(cudaMemcpyAsync(flags_dev + 2, start + ntiles, sizeof(int), cudaMemcpyDeviceToDevice, s));
-  if (row_counts_dev) MFB_CUDA_TRY(cudaMemsetAsync(row_counts_dev, 0, sizeof(int64_t) * g.rows, s));
+                                              capacity, flags_dev + 1, ntiles);
+  if (row_counts_dev) ctx.fill(row_counts_dev, 0, sizeof(int64_t) * g.rows, s);
   // the wedge frames and reliability branches of prepare_lowpoly
   for (cudaEvent_t e : plan.pending)
     if (e) MFB_CUDA_TRY(cudaStreamWaitEvent(s, e, 0));
@@ -1035,7 +1031,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
   // selects the single fused kernel (A/B).
   const bool split = raster_links_supported();
   if (fused && split) {
-    MFB_CUDA_TRY(cudaMemsetAsync(fused->q.count, 0, 4 * sizeof(int), s));  // [3]: transfer batch cursor
+    ctx.fill(fused->q.count, 0, 4 * sizeof(int), s);  // [3]: transfer batch cursor
     RasterFused f2 = *fused;
     f2.pend = ctx.buf<int2>("ras.pend", g.texels());
     k_raster<2><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
@@ -1044,7 +1040,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
     k_interp<<<kNumSMs * 8, 256, 0, s>>>(rf, attrs, f2.pend, fused->q.count, res, g.row0, fused->q);
     ctx.count_launch();
   } else if (fused) {
-    MFB_CUDA_TRY(cudaMemsetAsync(fused->q.count, 0, 4 * sizeof(int), s));  // [3]: transfer batch cursor
+    ctx.fill(fused->q.count, 0, 4 * sizeof(int), s);  // [3]: transfer batch cursor
     k_raster<1><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
                                        g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, *fused);
   } else {
@@ -1066,7 +1062,7 @@ bool raster_links_supported() {
 void gbuffer_queries(Ctx& ctx, cudaStream_t s, const GBufDev& g, const RasterFused& out) {
   const int tiles = ((g.res + kTile - 1) / kTile) * ((g.rows + kTile - 1) / kTile);
   int* overflow = ctx.buf<int>("gq.overflow", 1);
-  MFB_CUDA_TRY(cudaMemsetAsync(out.q.count, 0, 4 * sizeof(int), s));  // [3]: transfer batch cursor
+  ctx.fill(out.q.count, 0, 4 * sizeof(int), s);  // [3]: transfer batch cursor
   k_gbuffer_queries<<<tiles, 256, 0, s>>>(g.res, g.rows, g.pos, g.nrm, g.tan, g.bit, g.valid, g.rel, out,
                                           overflow);
   ctx.count_launch();
