@@ -217,8 +217,29 @@ struct RasterPlan {
   int nf = 0;
   int res = 0;
   cudaEvent_t pending[2] = {nullptr, nullptr};  // side branches raster_gbuffer joins before the texel kernel
+  // set by the cooperative prep, which also bins the faces into tiles
+  bool binned = false;
+  const int* tile_start = nullptr;
+  const int* bins = nullptr;
+  int capacity = 0;
 };
-void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterPlan& plan);
+// Wedge frames + reliable flags run as ONE cooperative kernel
+// (k_lowpoly_prep) on the aux stream (MFB_COOP_PREP=0: separate kernels on
+// aux / aux2); the UV setup and, with `bin` (the rows raster_gbuffer will
+// cover, its flags and the counters it would reset), the tile binning run
+// on `s`. raster_gbuffer joins the side branch before the interpolation
+// (split raster) or before the texel kernel.
+#ifndef MFB_COOP_PREP
+#define MFB_COOP_PREP 1
+#endif
+struct PrepBinning {
+  int row0 = 0, rows = 0;
+  int* flags = nullptr;           // raster flags: [1] bin overflow, [2] bin total
+  int* zero4 = nullptr;           // fused query-list counters to reset, or null
+  int64_t* row_counts = nullptr;  // per-row valid counts to reset (mf_coverage_rows), or null
+};
+void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterPlan& plan,
+                     const PrepBinning* bin = nullptr);
 // Frames only (for mf_wedge_tangents): F x 3 x {T, B, N} x 3 doubles.
 void wedge_frames(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames_out);
 

@@ -792,7 +792,12 @@ struct BakeEnq {
     }
     mk.e0 = tm.mark(s);
     RasterPlan plan;
-    prepare_lowpoly(c, s, lo->m, res, plan);
+    PrepBinning pb;
+    pb.row0 = g.row0;
+    pb.rows = g.rows;
+    pb.flags = flags;
+    pb.zero4 = raster_links_supported() ? fo.q.count : nullptr;
+    prepare_lowpoly(c, s, lo->m, res, plan, &pb);
     mk.e1 = tm.mark(s);
     // the dilation links run beside the interpolation kernel (both need only
     // the coverage kernel's outputs)
@@ -1090,7 +1095,7 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
     if (hflags[1] || hflags[3]) throw ApiError(MF_ERR_CUDA, "internal capacity overflow");
     if (hflags[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
     if (st) {
-      st->queries = static_cast<int64_t>(hcnt[0]);
+      st->queries = static_cast<int64_t>(hcnt[0] - hcnt[3]);  // less the dead records (unreliable texels)
       st->hits = static_cast<int64_t>(hcnt[1]);
       st->valid_texels = static_cast<int64_t>(hcnt[2]);
       st->bvh_nodes = hi->m.nf > 1 ? hi->m.nf - 1 : 0;
@@ -1338,7 +1343,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
       if (q.band_check[b] != 1)
         throw ApiError(MF_ERR_CUDA, "band sync: row band " + std::to_string(b) + " was not signalled by the transfer");
   if (st) {
-    st->queries = static_cast<int64_t>(hcnt[0]);
+    st->queries = static_cast<int64_t>(hcnt[0] - hcnt[3]);  // less the dead records (unreliable texels)
     st->hits = static_cast<int64_t>(hcnt[1]);
     st->valid_texels = static_cast<int64_t>(hcnt[2]);
     st->bvh_nodes = hi.m.nf > 1 ? hi.m.nf - 1 : 0;
@@ -1478,7 +1483,11 @@ int mf_raster_gbuffer(mf_ctx* ctx, const mf_mesh_view* lowpoly, int res, float* 
     for (int attempt = 0;; ++attempt) {
       MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), c.stream));
       RasterPlan plan;
-      prepare_lowpoly(c, c.stream, lo.m, res, plan);
+      PrepBinning pb;
+      pb.row0 = g.row0;
+      pb.rows = g.rows;
+      pb.flags = flags;
+      prepare_lowpoly(c, c.stream, lo.m, res, plan, &pb);
       raster_gbuffer(c, c.stream, lo.m, plan, g, flags, nullptr);
       int hf[4] = {0, 0, 0, 0};
       MFB_CUDA_TRY(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, c.stream));
@@ -1652,7 +1661,12 @@ int mf_coverage_rows(mf_ctx* ctx, mf_mesh* lowpoly, int res, int64_t* row_counts
     int64_t* rows = c.buf<int64_t>("cov.rows", res);
     MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), c.stream));
     RasterPlan plan;
-    prepare_lowpoly(c, c.stream, lowpoly->m, res, plan);
+    PrepBinning pb;
+    pb.row0 = g.row0;
+    pb.rows = g.rows;
+    pb.flags = flags;
+    pb.row_counts = rows;
+    prepare_lowpoly(c, c.stream, lowpoly->m, res, plan, &pb);
     raster_gbuffer(c, c.stream, lowpoly->m, plan, g, flags, rows);
     MFB_CUDA_TRY(cudaMemcpyAsync(row_counts, rows, sizeof(int64_t) * res, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));

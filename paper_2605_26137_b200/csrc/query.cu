@@ -447,6 +447,10 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     const int i = kPass == 2 ? qcap - 1 - li : li;
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
     if (live) p = MFB_STREAM_LD(qpos + i);
+    // a dead record (texel id stored as ~texel by k_interp: the texel's face
+    // is unreliable) is not walked; its epilogue stores the (128, 128, 255)
+    // of gbuffer.cpp:218-227 into the texel and the gutter texels linked to it
+    const bool dead = live && __float_as_int(p.w) < 0;
     const float3 qf = make_float3(p.x, p.y, p.z);
     const d3 q = mk3(p.x, p.y, p.z);
     // pruning slack, rounded up to fp32 (conservative; one register)
@@ -474,13 +478,13 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         }
       }
     }
-    float bnd = live ? prune_bound(best.d, E) : -INFINITY;
+    float bnd = live && !dead ? prune_bound(best.d, E) : -INFINITY;
     int32_t st_ref[kStackMax];
     alignas(16) float st_lb[kStackMax];
     int sp = 0;
     // ref: node (>= 0), leaf (< 0 and != kDone), or kDone
     constexpr int32_t kDone = static_cast<int32_t>(0x80000000);
-    int32_t ref = live ? root : kDone;
+    int32_t ref = live && !dead ? root : kDone;
     while (ref != kDone) {
       // ---- descend until this lane holds a leaf
       while (ref >= 0) {
@@ -551,9 +555,12 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       ref = pop_within(st_ref, st_lb, sp, bnd);
     }
     const unsigned live_mask = __ballot_sync(0xffffffffu, live);
+    const unsigned dead_mask = __ballot_sync(0xffffffffu, dead);
+    if (counters && dead_mask && lane == __ffs(dead_mask) - 1)
+      atomicAdd(&counters[3], static_cast<unsigned long long>(__popc(dead_mask)));
     if (!live) continue;
     if (kProf) ++pv[3];
-    const int texel = __float_as_int(p.w);
+    const int texel = dead ? ~__float_as_int(p.w) : __float_as_int(p.w);
     const d3 qe = q;
     if (kPass == 1) face_map[texel] = best.face;
     uint8_t px[3] = {128, 128, 255};
@@ -604,7 +611,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       if (lane == __ffs(grp) - 1) band_arrive(bands, band, __popc(grp));
     }
     if (kDebug) {
-      if (dbg_face) dbg_face[texel] = best.face >= 0 ? best.face : -3;
+      if (dbg_face) dbg_face[texel] = dead ? -2 : (best.face >= 0 ? best.face : -3);
       if (dbg_ts) {
         dbg_ts[3ll * texel] = ts3[0];
         dbg_ts[3ll * texel + 1] = ts3[1];

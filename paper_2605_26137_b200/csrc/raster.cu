@@ -16,8 +16,10 @@
 //                   reference coverage predicate (tie rule ownsBoundary,
 //                   gbuffer.cpp:21-27,146-154), AtlasOverlap detection,
 //                   f64 attribute interpolation, coalesced G-buffer stores.
+#include <cooperative_groups.h>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "bake.cuh"
@@ -45,29 +47,25 @@ struct alignas(16) AttrFace {
 };
 
 // ------------------------------------------------------------ vertex normals
-__global__ void k_corner_count(const int32_t* __restrict__ faces, int nc, int* __restrict__ cnt) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c < nc) atomicAdd(&cnt[faces[c]], 1);
+// Each pre-pass is a __device__ body over one item index, called by its own
+// kernel (the dense mesh, mf_wedge_tangents, ...) and by the cooperative
+// lowpoly kernel (k_lowpoly_prep), which runs them as grid-synchronised
+// phases. No __restrict__ / read-only loads on buffers the cooperative kernel
+// produces itself: the non-coherent path could return stale lines.
+__device__ __forceinline__ void d_corner_count(const int32_t* faces, int c, int* cnt) {
+  atomicAdd(&cnt[faces[c]], 1);
 }
-__global__ void k_corner_fill(const int32_t* __restrict__ faces, int nc, const int* __restrict__ start,
-                              int* __restrict__ cursor, int* __restrict__ list) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nc) return;
+__device__ __forceinline__ void d_corner_fill(const int32_t* faces, int c, const int* start, int* cursor, int* list) {
   const int v = faces[c];
   list[start[v] + atomicAdd(&cursor[v], 1)] = c;
 }
-__global__ void k_face_area_vec(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
-                                double* __restrict__ av) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
+__device__ __forceinline__ void d_face_area_vec(const double* pos, const int32_t* faces, int f, double* av) {
   const d3 p0 = ld3(pos + 3 * faces[3 * f]), p1 = ld3(pos + 3 * faces[3 * f + 1]),
            p2 = ld3(pos + 3 * faces[3 * f + 2]);
   st3(av + 3 * f, 0.5 * cross(p1 - p0, p2 - p0));  // faceAreaVector, mesh.h:28-31
 }
-// Sorts each vertex's incident-corner list into face order (valence is small).
-__global__ void k_csr_sort(int nv, const int* __restrict__ start, int* __restrict__ list) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nv) return;
+// Sorts vertex v's incident-corner list into face order (valence is small).
+__device__ __forceinline__ void d_csr_sort(int v, const int* start, int* list) {
   const int b = start[v], e = start[v + 1];
   for (int i = b + 1; i < e; ++i) {
     const int key = list[i];
@@ -80,10 +78,8 @@ __global__ void k_csr_sort(int nv, const int* __restrict__ start, int* __restric
   }
 }
 // computeVertexNormals (mesh.cpp:24-35): area vectors summed in face order.
-__global__ void k_vertex_sum(int nv, const int* __restrict__ start, const int* __restrict__ list,
-                             const double* __restrict__ av, double* __restrict__ out, int renorm) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nv) return;
+__device__ __forceinline__ void d_vertex_sum(int v, const int* start, const int* list, const double* av,
+                                             double* out, int renorm) {
   const int b = start[v], e = start[v + 1];
   d3 n = mk3(0.0, 0.0, 0.0);
   for (int i = b; i < e; ++i) n = n + ld3(av + 3 * (list[i] / 3));
@@ -94,6 +90,35 @@ __global__ void k_vertex_sum(int nv, const int* __restrict__ start, const int* _
     if (l2 > 1e-20) n = n / l2;
   }
   st3(out + 3 * v, n);
+}
+__device__ __forceinline__ void d_renorm(int v, const double* in, double* out) {
+  d3 n = ld3(in + 3 * v);
+  const double len = norm(n);
+  if (len > 1e-20) n = n / len;
+  st3(out + 3 * v, n);
+}
+__global__ void k_corner_count(const int32_t* __restrict__ faces, int nc, int* __restrict__ cnt) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nc) d_corner_count(faces, c, cnt);
+}
+__global__ void k_corner_fill(const int32_t* __restrict__ faces, int nc, const int* __restrict__ start,
+                              int* __restrict__ cursor, int* __restrict__ list) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nc) d_corner_fill(faces, c, start, cursor, list);
+}
+__global__ void k_face_area_vec(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
+                                double* __restrict__ av) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) d_face_area_vec(pos, faces, f, av);
+}
+__global__ void k_csr_sort(int nv, const int* __restrict__ start, int* __restrict__ list) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nv) d_csr_sort(v, start, list);
+}
+__global__ void k_vertex_sum(int nv, const int* __restrict__ start, const int* __restrict__ list,
+                             const double* __restrict__ av, double* __restrict__ out, int renorm) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nv) d_vertex_sum(v, start, list, av, out, renorm);
 }
 // Same sum for an UNSORTED incident-corner list: lists of up to 16 corners
 // (any regular mesh) are ordered in registers, longer ones in place; the sum
@@ -142,19 +167,12 @@ __global__ void k_vertex_sum_unsorted(int nv, const int* __restrict__ start, int
 }
 __global__ void k_renorm(int nv, const double* __restrict__ in, double* __restrict__ out) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nv) return;
-  d3 n = ld3(in + 3 * v);
-  const double len = norm(n);
-  if (len > 1e-20) n = n / len;
-  st3(out + 3 * v, n);
+  if (v < nv) d_renorm(v, in, out);
 }
 
 // ------------------------------------------------------------ wedge frames
-__global__ void k_wedge_contrib(const double* __restrict__ pos, const int32_t* __restrict__ faces,
-                                const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
-                                double* __restrict__ contrib, uint8_t* __restrict__ present) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
+__device__ __forceinline__ void d_wedge_contrib(const double* pos, const int32_t* faces, const double* uvs,
+                                                const int32_t* fuv, int f, double* contrib, uint8_t* present) {
   const int t[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
   const int u[3] = {fuv[3 * f], fuv[3 * f + 1], fuv[3 * f + 2]};
   const d3 p0 = ld3(pos + 3 * t[0]), p1 = ld3(pos + 3 * t[1]), p2 = ld3(pos + 3 * t[2]);
@@ -190,11 +208,8 @@ __global__ void k_wedge_contrib(const double* __restrict__ pos, const int32_t* _
 // in face order (the vertex's corner list is sorted by corner id) - exactly
 // the unordered_map accumulation of tangent.cpp:40-63 - and every corner
 // receives its wedge's sum.
-__global__ void k_wedge_acc(int nv, const int* __restrict__ start, const int* __restrict__ list,
-                            const int32_t* __restrict__ fuv, const double* __restrict__ contrib,
-                            const uint8_t* __restrict__ present, double* __restrict__ acc) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nv) return;
+__device__ __forceinline__ void d_wedge_acc(int v, const int* start, const int* list, const int32_t* fuv,
+                                            const double* contrib, const uint8_t* present, double* acc) {
   const int b = start[v], e = start[v + 1];
   for (int i = b; i < e; ++i) {
     const int ui = fuv[list[i]];
@@ -213,11 +228,8 @@ __global__ void k_wedge_acc(int nv, const int* __restrict__ start, const int* __
   }
 }
 // frames[c] = {T, B, N}; also fills the raster attribute block when attrs != null.
-__global__ void k_wedge_frames(const int32_t* __restrict__ faces, int nf, const double* __restrict__ unitN,
-                               const double* __restrict__ acc, double* __restrict__ frames,
-                               AttrFace* __restrict__ attrs, const double* __restrict__ pos) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 3 * nf) return;
+__device__ __forceinline__ void d_wedge_frames(const int32_t* faces, int c, const double* unitN, const double* acc,
+                                               double* frames, AttrFace* attrs, const double* pos) {
   const int v = faces[c];
   d3 N = ld3(unitN + 3 * v);
   if (norm(N) < 1e-20) N = mk3(0.0, 0.0, 1.0);
@@ -237,12 +249,26 @@ __global__ void k_wedge_frames(const int32_t* __restrict__ faces, int nf, const 
     st3(attrs[f].T + 3 * k, T);
   }
 }
+__global__ void k_wedge_contrib(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                                const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
+                                double* __restrict__ contrib, uint8_t* __restrict__ present) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) d_wedge_contrib(pos, faces, uvs, fuv, f, contrib, present);
+}
+__global__ void k_wedge_acc(int nv, const int* __restrict__ start, const int* __restrict__ list,
+                            const int32_t* __restrict__ fuv, const double* __restrict__ contrib,
+                            const uint8_t* __restrict__ present, double* __restrict__ acc) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nv) d_wedge_acc(v, start, list, fuv, contrib, present, acc);
+}
+__global__ void k_wedge_frames(const int32_t* __restrict__ faces, int nf, const double* __restrict__ unitN,
+                               const double* __restrict__ acc, double* __restrict__ frames,
+                               AttrFace* __restrict__ attrs, const double* __restrict__ pos) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < 3 * nf) d_wedge_frames(faces, c, unitN, acc, frames, attrs, pos);
+}
 
 // ------------------------------------------------------------ reliable faces
-__global__ void k_iota(int n, int* __restrict__ a) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) a[i] = i;
-}
 // find with path halving: parent[x] <- parent[parent[x]] (a benign race:
 // any ancestor is a valid parent, and roots never change except by the CAS).
 __device__ __forceinline__ int uf_find(int* parent, int x) {
@@ -257,9 +283,7 @@ __device__ __forceinline__ int uf_find(int* parent, int x) {
 }
 // Hook the larger root under the smaller one, so every root is its island's
 // minimum UV index — exactly the reference's parent[max] = min (gbuffer.cpp:41-45).
-__global__ void k_uf_unite(const int32_t* __restrict__ fuv, int nf, int* parent) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
+__device__ __forceinline__ void d_uf_unite(const int32_t* fuv, int f, int* parent) {
   for (int e = 1; e <= 2; ++e) {
     int a = fuv[3 * f], b = fuv[3 * f + e];
     for (;;) {
@@ -273,23 +297,16 @@ __global__ void k_uf_unite(const int32_t* __restrict__ fuv, int nf, int* parent)
     }
   }
 }
-__global__ void k_uf_flatten(int n, int* parent) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) parent[i] = uf_find(parent, i);
-}
-__global__ void k_face_ratio(const double* __restrict__ pos, const int32_t* __restrict__ faces,
-                             const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
-                             const int* __restrict__ parent, double* __restrict__ uv_area,
-                             double* __restrict__ ratio, int* __restrict__ island, int* __restrict__ count) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
+__device__ __forceinline__ void d_face_ratio(const double* pos, const int32_t* faces, const double* uvs,
+                                             const int32_t* fuv, int f, const int* parent, double* uv_area,
+                                             double* ratio, int* island, int* count) {
   const int u0 = fuv[3 * f], u1 = fuv[3 * f + 1], u2 = fuv[3 * f + 2];
   const double a = 0.5 * fabs(cross2(uvs[2 * u1] - uvs[2 * u0], uvs[2 * u1 + 1] - uvs[2 * u0 + 1],
                                      uvs[2 * u2] - uvs[2 * u0], uvs[2 * u2 + 1] - uvs[2 * u0 + 1]));
   const d3 p0 = ld3(pos + 3 * faces[3 * f]), p1 = ld3(pos + 3 * faces[3 * f + 1]),
            p2 = ld3(pos + 3 * faces[3 * f + 2]);
   const double surf = norm(0.5 * cross(p1 - p0, p2 - p0));  // faceArea, mesh.h:33
-  const int isl = parent[u0];
+  const int isl = uf_find(const_cast<int*>(parent), u0);  // = parent[u0] once flattened
   double r = -1.0;
   if (surf > 1e-20) {
     r = a / surf;
@@ -301,46 +318,42 @@ __global__ void k_face_ratio(const double* __restrict__ pos, const int32_t* __re
 }
 // Groups the sampled ratios by island (order within an island is irrelevant
 // to its median).
-__global__ void k_island_fill(int nf, const double* __restrict__ ratio, const int* __restrict__ island,
-                              const int* __restrict__ start, int* __restrict__ cursor,
-                              unsigned long long* __restrict__ items) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf || ratio[f] < 0.0) return;
+__device__ __forceinline__ void d_island_fill(int f, const double* ratio, const int* island, const int* start,
+                                              int* cursor, unsigned long long* items) {
+  if (ratio[f] < 0.0) return;
   const int isl = island[f];
   // ratio >= 0, so its IEEE bit pattern orders like its value
   items[start[isl] + atomicAdd(&cursor[isl], 1)] = static_cast<unsigned long long>(__double_as_longlong(ratio[f]));
 }
 // Island median = element size/2 of the island's sorted ratios (the
 // std::nth_element of gbuffer.cpp:69-71), by an exact 8-pass radix select
-// over the 64-bit patterns; one CTA per island.
-__global__ void __launch_bounds__(256) k_island_select(int nu, const int* __restrict__ count,
-                                                       const int* __restrict__ start,
-                                                       const unsigned long long* __restrict__ items,
-                                                       double* __restrict__ median) {
-  const int isl = blockIdx.x;
-  if (isl >= nu) return;
+// over the 64-bit patterns; one CTA per island (any blockDim >= 32).
+struct SelectSmem {
+  int hist[256];
+  unsigned long long prefix;
+  int k;
+};
+__device__ void d_island_select(int isl, const int* count, const int* start, const unsigned long long* items,
+                                double* median, SelectSmem& sm) {
   const int n = count[isl];
   if (n == 0) {
     if (threadIdx.x == 0) median[isl] = 0.0;
     return;
   }
   const unsigned long long* it = items + start[isl];
-  __shared__ int hist[256];
-  __shared__ unsigned long long s_prefix;
-  __shared__ int s_k;
   if (threadIdx.x == 0) {
-    s_prefix = 0;
-    s_k = n / 2;
+    sm.prefix = 0;
+    sm.k = n / 2;
   }
   for (int pass = 7; pass >= 0; --pass) {
     const int shift = pass * 8;
     const unsigned long long hi_mask = pass == 7 ? 0ull : (~0ull << (shift + 8));
-    for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0;
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) sm.hist[i] = 0;
     __syncthreads();
-    const unsigned long long prefix = s_prefix;
+    const unsigned long long prefix = sm.prefix;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       const unsigned long long v = it[i];
-      if ((v & hi_mask) == prefix) atomicAdd(&hist[(v >> shift) & 0xff], 1);
+      if ((v & hi_mask) == prefix) atomicAdd(&sm.hist[(v >> shift) & 0xff], 1);
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -350,7 +363,7 @@ __global__ void __launch_bounds__(256) k_island_select(int nu, const int* __rest
       int c[8], sum = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        c[j] = hist[8 * lane + j];
+        c[j] = sm.hist[8 * lane + j];
         sum += c[j];
       }
       int incl = sum;
@@ -359,7 +372,7 @@ __global__ void __launch_bounds__(256) k_island_select(int nu, const int* __rest
         const int y = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= off) incl += y;
       }
-      const int k = s_k;
+      const int k = sm.k;
       const unsigned owner = __ballot_sync(0xffffffffu, incl > k);  // k < n: some lane holds it
       const int ol = __ffs(owner) - 1;
       if (lane == ol) {
@@ -370,23 +383,53 @@ __global__ void __launch_bounds__(256) k_island_select(int nu, const int* __rest
           kk -= c[j];
           ++b;
         }
-        s_k = kk;
-        s_prefix = prefix | (static_cast<unsigned long long>(b) << shift);
+        sm.k = kk;
+        sm.prefix = prefix | (static_cast<unsigned long long>(b) << shift);
       }
     }
     __syncthreads();
   }
-  if (threadIdx.x == 0) median[isl] = __longlong_as_double(static_cast<long long>(s_prefix));
+  if (threadIdx.x == 0) median[isl] = __longlong_as_double(static_cast<long long>(sm.prefix));
+  __syncthreads();  // sm is reused by the caller's next island
+}
+__global__ void k_iota(int n, int* __restrict__ a) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+__global__ void k_uf_unite(const int32_t* __restrict__ fuv, int nf, int* parent) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) d_uf_unite(fuv, f, parent);
+}
+__global__ void k_uf_flatten(int n, int* parent) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) parent[i] = uf_find(parent, i);
+}
+__global__ void k_face_ratio(const double* __restrict__ pos, const int32_t* __restrict__ faces,
+                             const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf,
+                             const int* __restrict__ parent, double* __restrict__ uv_area,
+                             double* __restrict__ ratio, int* __restrict__ island, int* __restrict__ count) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) d_face_ratio(pos, faces, uvs, fuv, f, parent, uv_area, ratio, island, count);
+}
+__global__ void k_island_fill(int nf, const double* __restrict__ ratio, const int* __restrict__ island,
+                              const int* __restrict__ start, int* __restrict__ cursor,
+                              unsigned long long* __restrict__ items) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) d_island_fill(f, ratio, island, start, cursor, items);
+}
+__global__ void __launch_bounds__(256) k_island_select(int nu, const int* __restrict__ count,
+                                                       const int* __restrict__ start,
+                                                       const unsigned long long* __restrict__ items,
+                                                       double* __restrict__ median) {
+  __shared__ SelectSmem sm;
+  if (blockIdx.x < nu) d_island_select(blockIdx.x, count, start, items, median, sm);
 }
 
 // ------------------------------------------------------------ face setup
 // reliable (gbuffer.cpp:74-81) into the face's raster record and attributes;
-// runs after k_face_setup, which leaves rel = 0
-__global__ void k_face_rel(int nf, const double* __restrict__ uv_area, const double* __restrict__ ratio,
-                           const int* __restrict__ island, const double* __restrict__ median,
-                           RasterFace* __restrict__ rf, AttrFace* __restrict__ attrs) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
+// runs after the face setup, which leaves rel = 0
+__device__ __forceinline__ void d_face_rel(int f, const double* uv_area, const double* ratio, const int* island,
+                                           const double* median, RasterFace* rf, AttrFace* attrs) {
   int rel = 0;
   if (!(uv_area[f] < 1e-8) && !(ratio[f] < 0.0)) {
     const double m = median[island[f]];
@@ -394,15 +437,18 @@ __global__ void k_face_rel(int nf, const double* __restrict__ uv_area, const dou
   }
   attrs[f].reliable = rel;
   attrs[f].pad = 0;
-  rf[f].rel = rel;
+  if (rf) rf[f].rel = rel;
+}
+__global__ void k_face_rel(int nf, const double* __restrict__ uv_area, const double* __restrict__ ratio,
+                           const int* __restrict__ island, const double* __restrict__ median,
+                           RasterFace* __restrict__ rf, AttrFace* __restrict__ attrs) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) d_face_rel(f, uv_area, ratio, island, median, rf, attrs);
 }
 
 // UV-space raster setup of a face (gbuffer.cpp:114-144): everything the
 // binning and the coverage test need, from the UVs alone
-__global__ void k_face_setup(const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf, int res,
-                             RasterFace* __restrict__ rf) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
+__device__ __forceinline__ void d_face_setup(const double* uvs, const int32_t* fuv, int f, int res, RasterFace* rf) {
   RasterFace s;
   s.rel = 0;
   s.pad[0] = s.pad[1] = s.pad[2] = 0;
@@ -450,6 +496,11 @@ __global__ void k_face_setup(const double* __restrict__ uvs, const int32_t* __re
   }
   rf[f] = s;
 }
+__global__ void k_face_setup(const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf, int res,
+                             RasterFace* __restrict__ rf) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) d_face_setup(uvs, fuv, f, res, rf);
+}
 
 // ------------------------------------------------------------ binning
 __device__ __forceinline__ bool face_tiles(const RasterFace& s, int row_begin, int row_end, int& tx0,
@@ -462,21 +513,16 @@ __device__ __forceinline__ bool face_tiles(const RasterFace& s, int row_begin, i
   ty1 = (y1 - row_begin) / kTile;
   return true;
 }
-__global__ void k_bin_count(const RasterFace* __restrict__ rf, int nf, int row_begin, int row_end,
-                            int tiles_x, int* __restrict__ tile_cnt) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
+__device__ __forceinline__ void d_bin_count(const RasterFace* rf, int f, int row_begin, int row_end, int tiles_x,
+                                            int* tile_cnt) {
   int tx0, tx1, ty0, ty1;
   if (!face_tiles(rf[f], row_begin, row_end, tx0, tx1, ty0, ty1)) return;
   for (int ty = ty0; ty <= ty1; ++ty)
     for (int tx = tx0; tx <= tx1; ++tx) atomicAdd(&tile_cnt[ty * tiles_x + tx], 1);
 }
-__global__ void k_bin_fill(const RasterFace* __restrict__ rf, int nf, int row_begin, int row_end,
-                           int tiles_x, const int* __restrict__ tile_start, int* __restrict__ cursor,
-                           int* __restrict__ bins, int capacity, int* __restrict__ overflow, int ntiles) {
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f == 0) overflow[1] = tile_start[ntiles];  // the bins' exact total (flags[2])
-  if (f >= nf) return;
+__device__ __forceinline__ void d_bin_fill(const RasterFace* rf, int f, int row_begin, int row_end, int tiles_x,
+                                           const int* tile_start, int* cursor, int* bins, int capacity,
+                                           int* overflow) {
   int tx0, tx1, ty0, ty1;
   if (!face_tiles(rf[f], row_begin, row_end, tx0, tx1, ty0, ty1)) return;
   for (int ty = ty0; ty <= ty1; ++ty)
@@ -487,6 +533,291 @@ __global__ void k_bin_fill(const RasterFace* __restrict__ rf, int nf, int row_be
       else *overflow = 1;
     }
 }
+__global__ void k_bin_count(const RasterFace* __restrict__ rf, int nf, int row_begin, int row_end,
+                            int tiles_x, int* __restrict__ tile_cnt) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f < nf) d_bin_count(rf, f, row_begin, row_end, tiles_x, tile_cnt);
+}
+__global__ void k_bin_fill(const RasterFace* __restrict__ rf, int nf, int row_begin, int row_end,
+                           int tiles_x, const int* __restrict__ tile_start, int* __restrict__ cursor,
+                           int* __restrict__ bins, int capacity, int* __restrict__ overflow, int ntiles,
+                           int* __restrict__ zero4 = nullptr) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f == 0) overflow[1] = tile_start[ntiles];  // the bins' exact total (flags[2])
+  if (zero4 && f < 4) zero4[f] = 0;              // query-list counters of the raster that follows
+  if (f < nf) d_bin_fill(rf, f, row_begin, row_end, tiles_x, tile_start, cursor, bins, capacity, overflow);
+}
+
+// ------------------------------------------------------------ cooperative lowpoly prep
+// Everything per corner c of the lowpoly once the incident-corner lists are
+// filled (unordered): the corner's vertex list sorted into face order in
+// registers (up to 16 corners; longer lists are walked in order by repeated
+// minimum selection), the unit vertex
+// normal (computeVertexNormals + the tangent.cpp:26-31 re-normalisation, or
+// the mesh's own normal), the corner's wedge sum (tangent.cpp:40-63: the
+// same-uv corners of the vertex in face order) and its frame
+// (tangent.cpp:65-80) into the raster attributes - the work of k_csr_sort,
+// k_vertex_sum, k_wedge_acc and k_wedge_frames with one thread per corner
+// and independent loads instead of per-vertex dependent chains (each of a
+// vertex's corners repeats the vertex's sums: same operands, same order,
+// same bits).
+__device__ __forceinline__ void d_corner_pass(int c, const int32_t* faces, const int* start, const int* list,
+                                              const double* av, const double* nrm, const int32_t* fuv,
+                                              const double* contrib, const uint8_t* present, const double* pos,
+                                              double* unitN, AttrFace* attrs) {
+  constexpr int K = 16;
+  const int v = faces[c];
+  const int b = start[v], e = start[v + 1], k = e - b;
+  const int ui = fuv[c];
+  d3 N, sum = mk3(0.0, 0.0, 0.0);
+  bool first = false;
+  if (k <= K) {
+    int cs[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) cs[i] = i < k ? list[b + i] : 0x7fffffff;
+#pragma unroll
+    for (int i = 1; i < K; ++i) {
+#pragma unroll
+      for (int j = i; j > 0; --j) {
+        const int lo = min(cs[j - 1], cs[j]), hi = max(cs[j - 1], cs[j]);
+        cs[j - 1] = lo;
+        cs[j] = hi;
+      }
+    }
+    first = cs[0] == c;
+    d3 n = mk3(0.0, 0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (i < k) {
+        const int cj = cs[i];
+        if (!nrm) n = n + ld3(av + 3 * (cj / 3));
+        if (fuv[cj] == ui && present[cj]) sum = sum + ld3(contrib + 3 * cj);
+      }
+    }
+    N = n;
+  } else {  // rare high valence: visit the unsorted list in face order by selection, O(k^2)
+    d3 n = mk3(0.0, 0.0, 0.0);
+    int prev = -1;
+    for (int step = 0; step < k; ++step) {
+      int cj = 0x7fffffff;
+      for (int i = b; i < e; ++i) {
+        const int x = list[i];
+        if (x > prev && x < cj) cj = x;
+      }
+      if (step == 0) first = cj == c;
+      if (!nrm) n = n + ld3(av + 3 * (cj / 3));
+      if (fuv[cj] == ui && present[cj]) sum = sum + ld3(contrib + 3 * cj);
+      prev = cj;
+    }
+    N = n;
+  }
+  if (nrm) {
+    N = ld3(nrm + 3 * v);
+    const double len = norm(N);
+    if (len > 1e-20) N = N / len;
+  } else {
+    const double len = norm(N);
+    if (len > 0) N = N / len;
+    const double l2 = norm(N);
+    if (l2 > 1e-20) N = N / l2;
+  }
+  if (first) st3(unitN + 3 * v, N);
+  if (norm(N) < 1e-20) N = mk3(0.0, 0.0, 1.0);
+  const d3 t = sum - N * dot(N, sum);
+  const double len = norm(t);
+  const d3 T = len > 1e-12 ? t / len : any_perpendicular(N);
+  const int f = c / 3, q = c % 3;
+  st3(attrs[f].P + 3 * q, ld3(pos + 3 * v));
+  st3(attrs[f].N + 3 * q, N);
+  st3(attrs[f].T + 3 * q, T);
+}
+
+// Block-wide exclusive scan of in[0, n) into out[0, n) by one CTA (the
+// callers' last element is a zero pad, so out[n - 1] is the total, as the
+// DeviceScan::ExclusiveSum it replaces).
+__device__ void block_exclusive_scan(const int* in, int* out, int n) {
+  // tiles of 8 x blockDim elements: coalesced independent loads into shared
+  // memory, each thread scans 8 consecutive elements, one block scan of the
+  // thread sums, coalesced stores; a running carry links the tiles
+  constexpr int kPer = 8, kMaxT = 512;
+  __shared__ int tile[kPer * kMaxT];
+  __shared__ int wsum[32];
+  __shared__ int carry_s;
+  const int T = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+  int carry = 0;
+  for (int base = 0; base < n; base += kPer * T) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = base + k * T + t;
+      tile[k * T + t] = i < n ? in[i] : 0;
+    }
+    __syncthreads();
+    int v[kPer], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      v[k] = tile[kPer * t + k];
+      sum += v[k];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const int nw = T >> 5;
+      int x = lane < nw ? wsum[lane] : 0;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, off);
+        if (lane >= off) x += y;
+      }
+      if (lane < nw) wsum[lane] = x;  // inclusive warp totals
+      if (lane == nw - 1) carry_s = x;
+    }
+    __syncthreads();
+    int run = carry + (w ? wsum[w - 1] : 0) + incl - sum;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      tile[kPer * t + k] = run;
+      run += v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = base + k * T + t;
+      if (i < n) out[i] = tile[k * T + t];
+    }
+    carry += carry_s;
+    __syncthreads();  // tile / wsum / carry_s reused
+  }
+}
+
+struct PrepArgs {
+  // lowpoly
+  const double* pos;
+  const int32_t* faces;
+  const double* nrm;  // mesh normals (re-normalised) or null: computed from the corner CSR
+  const double* uvs;
+  const int32_t* fuv;
+  int nv, nf, nu, res;
+  // corner CSR + normals + wedges
+  int* ccnt;  // 2 (nv + 1): counts, cursors
+  int* cstart;
+  int* clist;
+  double* av;
+  double* unitN;
+  double* contrib;
+  uint8_t* present;
+  double* wacc;
+  // reliability
+  int* parent;
+  double* uv_area;
+  double* ratio;
+  int* island;
+  int* icnt;  // 2 (nu + 1)
+  int* istart;
+  unsigned long long* items;
+  double* median;
+  int* roots;   // islands with sampled faces
+  int* nroots;
+  // face records
+  AttrFace* attrs;
+};
+
+// The lowpoly pre-pass the interpolation needs - vertex normals
+// (mesh.cpp:24-35), computeWedgeTangents (tangent.cpp:22-82) and
+// reliableFaces (gbuffer.cpp:31-83) - as one cooperative kernel: seven
+// phases separated by grid-wide barriers, each phase the same per-item bodies
+// the separate kernels run. It replaces ~20 dependent launches (each a few
+// us of work on a 20k-face mesh) on two streams, and runs beside the UV
+// setup, binning and coverage kernel: only k_interp waits for it (r02 CUPTI
+// timeline: the separate kernels took 0.17 ms before the coverage kernel
+// could start).
+#ifndef MFB_PREP_PROF
+#define MFB_PREP_PROF 0  // variant builds: block 0 prints its per-phase times
+#endif
+__global__ void __launch_bounds__(512) k_lowpoly_prep(PrepArgs a) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+#if MFB_PREP_PROF
+  unsigned long long ts[8];
+  int nts = 0;
+  auto stamp = [&] { asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts[nts])); ++nts; };
+  stamp();
+#define PREP_SYNC() \
+  do {              \
+    grid.sync();    \
+    stamp();        \
+  } while (0)
+#else
+#define PREP_SYNC() grid.sync()
+#endif
+  __shared__ SelectSmem sel;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, gs = gridDim.x * blockDim.x;
+  const int nc = 3 * a.nf;
+  const bool own_n = a.nrm == nullptr;
+  // P0: resets, UV setup, wedge contributions, area vectors, parent = iota
+  for (int i = gt; i < 2 * (a.nv + 1); i += gs) a.ccnt[i] = 0;
+  for (int i = gt; i < 2 * (a.nu + 1); i += gs) a.icnt[i] = 0;
+  for (int i = gt; i < a.nu; i += gs) a.parent[i] = i;
+  if (gt == 0) *a.nroots = 0;
+  for (int f = gt; f < a.nf; f += gs) {
+    d_wedge_contrib(a.pos, a.faces, a.uvs, a.fuv, f, a.contrib, a.present);
+    if (own_n) d_face_area_vec(a.pos, a.faces, f, a.av);
+  }
+  PREP_SYNC();
+  // P1: corner counts, union-find
+  for (int c = gt; c < nc; c += gs) d_corner_count(a.faces, c, a.ccnt);
+  for (int f = gt; f < a.nf; f += gs) d_uf_unite(a.fuv, f, a.parent);
+  PREP_SYNC();
+  // P2: corner scan (one CTA); per-face ratios and island counts (the
+  // roots are final: find without flattening)
+  if (blockIdx.x == 0) block_exclusive_scan(a.ccnt, a.cstart, a.nv + 1);
+  for (int f = gt; f < a.nf; f += gs)
+    d_face_ratio(a.pos, a.faces, a.uvs, a.fuv, f, a.parent, a.uv_area, a.ratio, a.island, a.icnt);
+  PREP_SYNC();
+  // P3: corner lists, island scan
+  for (int c = gt; c < nc; c += gs) d_corner_fill(a.faces, c, a.cstart, a.ccnt + a.nv + 1, a.clist);
+  if (blockIdx.x == (gridDim.x > 1 ? 1 : 0)) block_exclusive_scan(a.icnt, a.istart, a.nu + 1);
+  PREP_SYNC();
+  // P4: per vertex normals, wedges and corner frames; island ratio lists
+  for (int c = gt; c < nc; c += gs)
+    d_corner_pass(c, a.faces, a.cstart, a.clist, a.av, a.nrm, a.fuv, a.contrib, a.present, a.pos, a.unitN,
+                  a.attrs);
+  for (int f = gt; f < a.nf; f += gs) d_island_fill(f, a.ratio, a.island, a.istart, a.icnt + a.nu + 1, a.items);
+  // the islands with sampled faces (a handful of roots among nu UV indices)
+  for (int isl = gt; isl < a.nu; isl += gs) {
+    const bool has = a.icnt[isl] > 0;
+    if (!has) a.median[isl] = 0.0;
+    const unsigned m = __ballot_sync(__activemask(), has);
+    if (!m) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(a.nroots, __popc(m));
+    base = __shfl_sync(__activemask(), base, leader);
+    if (has) a.roots[base + __popc(m & ((1u << lane) - 1u))] = isl;
+  }
+  PREP_SYNC();
+  // P5: island medians (one CTA per island with samples)
+  const int nroots = __ldcg(a.nroots);
+  for (int r = blockIdx.x; r < nroots; r += gridDim.x)
+    d_island_select(__ldcg(&a.roots[r]), a.icnt, a.istart, a.items, a.median, sel);
+  PREP_SYNC();
+  // P6: reliable flags
+  for (int f = gt; f < a.nf; f += gs) d_face_rel(f, a.uv_area, a.ratio, a.island, a.median, nullptr, a.attrs);
+#if MFB_PREP_PROF
+  stamp();
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("[prep] %d CTAs  phases us: %.1f %.1f %.1f %.1f %.1f %.1f %.1f  total %.1f\n", gridDim.x,
+           (ts[1] - ts[0]) * 1e-3, (ts[2] - ts[1]) * 1e-3, (ts[3] - ts[2]) * 1e-3, (ts[4] - ts[3]) * 1e-3,
+           (ts[5] - ts[4]) * 1e-3, (ts[6] - ts[5]) * 1e-3, (ts[7] - ts[6]) * 1e-3, (ts[7] - ts[0]) * 1e-3);
+#endif
+#undef PREP_SYNC
+}
+
 
 // ------------------------------------------------------------ raster
 __device__ __forceinline__ bool owns_boundary(double dx, double dy) {
@@ -663,6 +994,10 @@ __global__ void MFB_INTERP_BOUNDS k_interp(const RasterFace* __restrict__ rf,
 #endif
     const int yr = tf.x / res, x = tf.x - yr * res;
     const double cx = x + 0.5, cy = (yr + g_row0) + 0.5;
+    if (!attrs[tf.y].reliable) {  // gbuffer.cpp:218-227: not a query; texel id stored as ~gi
+      q.qpos[i] = make_float4(0.f, 0.f, 0.f, __int_as_float(~tf.x));
+      continue;
+    }
     float P[3], Nf[3], Tf[3], Bf[3];
     interp_texel(rf[tf.y], attrs[tf.y], cx, cy, P, Nf, Tf, Bf);
     store_query(q, i, false, tf.x, P, Nf, Tf, Bf);
@@ -703,7 +1038,7 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
   const bool in = x < res && y < row_end;
   const double cx = x + 0.5, cy = y + 0.5;
   const int b = tile_start[t], e = min(tile_start[t + 1], capacity);
-  int cover = -1, hits = 0, crel = 0;
+  int cover = -1, hits = 0;
   for (int base = b; base < e; base += kChunk) {
     const int n = min(kChunk, e - base);
     __syncthreads();
@@ -733,10 +1068,7 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
         }
         if (!inside) continue;
         ++hits;
-        if (cover < 0 || sfid[i] < cover) {
-          cover = sfid[i];
-          crel = sfc.rel;
-        }
+        if (cover < 0 || sfid[i] < cover) cover = sfid[i];
       }
     }
   }
@@ -750,8 +1082,11 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
     rel = static_cast<uint8_t>(attrs[cover].reliable);
   }
   if (kMode == 2 && in && cover >= 0) {
+    // late reliability: every valid texel is compacted as a query; k_interp
+    // (which runs after the reliability pass) turns the texels of unreliable
+    // faces into dead records the transfer encodes as (128, 128, 255)
     valid = 1;
-    rel = static_cast<uint8_t>(crel);
+    rel = 1;
   }
   if (row_counts) {
     // warp = 8 columns x 4 rows: lanes 8r..8r+7 share row r
@@ -940,17 +1275,144 @@ void wedge_frames(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames_ou
   wedge_pipeline(ctx, s, lo, frames_out, nullptr);
 }
 
-void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterPlan& plan) {
+#ifndef MFB_PREP_CTAS
+#define MFB_PREP_CTAS 32  // the cooperative prep holds its SMs through every barrier: few CTAs
+#endif
+namespace {
+int bin_capacity_for(const Ctx& ctx, int nf, int ntiles) {
+  // a bound that holds for ordinary atlases; the bake driver re-runs with
+  // the exact total (flags[1] set, total in flags[2]) otherwise
+  const int64_t cap64 = std::max<int64_t>(ctx.bin_capacity, 8ll * nf + 4ll * ntiles + 1024);
+  return static_cast<int>(std::min<int64_t>(cap64, 0x7fffffff));
+}
+
+// One cooperative launch of k_lowpoly_prep: wedge frames and reliable
+// flags into the faces' raster attributes.
+void prepare_lowpoly_coop(Ctx& ctx, cudaStream_t s, const DevMesh& lo, AttrFace* attrs) {
+  const int nf = lo.nf, nu = lo.nu, nv = lo.nv, nc = 3 * nf;
+  PrepArgs a{};
+  a.pos = lo.pos;
+  a.faces = lo.faces;
+  a.uvs = lo.uvs;
+  a.fuv = lo.fuv;
+  a.nv = nv;
+  a.nf = nf;
+  a.nu = nu;
+  a.nrm = lo.has_normals() ? lo.nrm : nullptr;
+  a.ccnt = ctx.buf<int>("lo.csr.cc", 2 * (nv + 1));
+  a.cstart = ctx.buf<int>("lo.csr.start", nv + 1);
+  a.clist = ctx.buf<int>("lo.csr.list", nc);
+  a.av = ctx.buf<double>("lo.vn.av", 3 * static_cast<size_t>(nf));
+  a.unitN = ctx.buf<double>("lo.unitN", 3 * static_cast<size_t>(nv));
+  a.contrib = ctx.buf<double>("lo.wt.contrib", 3 * static_cast<size_t>(nc));
+  a.present = ctx.buf<uint8_t>("lo.wt.present", nc);
+  a.parent = ctx.buf<int>("lo.rel.parent", nu);
+  a.uv_area = ctx.buf<double>("lo.rel.uvarea", nf);
+  a.ratio = ctx.buf<double>("lo.rel.ratio", nf);
+  a.island = ctx.buf<int>("lo.rel.island", nf);
+  a.icnt = ctx.buf<int>("lo.rel.cc", 2 * (nu + 1));
+  a.istart = ctx.buf<int>("lo.rel.start", nu + 1);
+  a.items = ctx.buf<unsigned long long>("lo.rel.items", nf);
+  a.median = ctx.buf<double>("lo.rel.median", nu);
+  a.roots = ctx.buf<int>("lo.rel.roots", nu + 1);
+  a.nroots = a.roots + nu;
+  a.attrs = attrs;
+  // grid: every CTA co-resident (cooperative launch); the kernel holds its
+  // SMs through every barrier, so it stays small beside the LBVH
+  static int max_blocks = [] {
+    int per_sm = 0;
+    MFB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lowpoly_prep, 512, 0));
+    return std::max(1, per_sm) * kNumSMs;
+  }();
+  const int want = div_up(std::max(nc, nu), 512);
+  const int grid = std::max(1, std::min(std::min(MFB_PREP_CTAS, max_blocks), want));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(512);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MFB_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_lowpoly_prep, a));
+  ctx.count_launch();
+}
+
+// UV setup fused with the tile counts (the face's record is in registers)
+__global__ void k_face_setup_count(const double* __restrict__ uvs, const int32_t* __restrict__ fuv, int nf, int res,
+                                   RasterFace* __restrict__ rf, int row_begin, int row_end, int tiles_x,
+                                   int* __restrict__ tile_cnt) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  d_face_setup(uvs, fuv, f, res, rf);
+  d_bin_count(rf, f, row_begin, row_end, tiles_x, tile_cnt);
+}
+
+// Tile binning of the faces over slab rows [b.row0, b.row0 + b.rows) on `s`:
+// setup + counts, scan, fill (which also stores the exact total in flags[2]
+// and resets the query-list counters).
+void bin_faces(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterFace* rf, const PrepBinning& b,
+               RasterPlan& plan) {
+  const int T = 256, nf = lo.nf;
+  const int row_begin = b.row0, row_end = b.row0 + b.rows;
+  const int tiles_x = (res + kTile - 1) / kTile;
+  const int ntiles = tiles_x * ((b.rows + kTile - 1) / kTile);
+  int* cnt = ctx.buf<int>("ras.cc", 2 * (ntiles + 1));  // counts, then fill cursors: one fill
+  int* cursor = cnt + ntiles + 1;
+  int* tstart = ctx.buf<int>("ras.start", ntiles + 1);
+  const int capacity = bin_capacity_for(ctx, nf, ntiles);
+  int* bins = ctx.buf<int>("ras.bins", capacity);
+  ctx.fill(cnt, 0, sizeof(int) * 2 * (ntiles + 1), s);
+  k_face_setup_count<<<div_up(nf, T), T, 0, s>>>(lo.uvs, lo.fuv, nf, res, rf, row_begin, row_end, tiles_x, cnt);
+  size_t tmp = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, tstart, ntiles + 1, s);
+  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, tstart, ntiles + 1, s));
+  k_bin_fill<<<div_up(nf, T), T, 0, s>>>(rf, nf, row_begin, row_end, tiles_x, tstart, cursor, bins, capacity,
+                                         b.flags + 1, ntiles, b.zero4);
+  ctx.count_launch(2);
+  if (b.row_counts) ctx.fill(b.row_counts, 0, sizeof(int64_t) * b.rows, s);
+  MFB_CUDA_TRY(cudaGetLastError());
+  plan.binned = true;
+  plan.tile_start = tstart;
+  plan.bins = bins;
+  plan.capacity = capacity;
+}
+}  // namespace
+
+void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterPlan& plan,
+                     const PrepBinning* bin) {
+  auto* rf = ctx.buf<RasterFace>("lo.rf", lo.nf);
+  auto* attrs = ctx.buf<AttrFace>("lo.attrs", lo.nf);
+  cudaStream_t ws = ctx.aux ? ctx.aux : s;
+  if (MFB_COOP_PREP && ws != s) {
+    // frames + reliability: one cooperative kernel on aux, beside the
+    // setup and binning on s
+    MFB_CUDA_TRY(cudaEventRecord(ctx.fork2, s));
+    MFB_CUDA_TRY(cudaStreamWaitEvent(ws, ctx.fork2, 0));
+    prepare_lowpoly_coop(ctx, ws, lo, attrs);
+    MFB_CUDA_TRY(cudaEventRecord(ctx.join2, ws));
+    if (bin) {
+      bin_faces(ctx, s, lo, res, rf, *bin, plan);
+    } else {
+      k_face_setup<<<div_up(lo.nf, 256), 256, 0, s>>>(lo.uvs, lo.fuv, lo.nf, res, rf);
+      ctx.count_launch();
+    }
+    plan.faces = rf;
+    plan.attrs = attrs;
+    plan.nf = lo.nf;
+    plan.res = res;
+    plan.pending[0] = ctx.join2;
+    plan.pending[1] = nullptr;
+    return;
+  }
   const int T = 256;
   const int nf = lo.nf, nu = lo.nu;
-  auto* rf = ctx.buf<RasterFace>("lo.rf", nf);
-  auto* attrs = ctx.buf<AttrFace>("lo.attrs", nf);
   // Three branches: the UV-only raster setup on `s` (the binning follows it
   // there in raster_gbuffer), the wedge frames (computeWedgeTangents) on aux
   // and the reliability pass (reliableFaces) on aux2, which ends by setting
   // the faces' rel flags after the setup; raster_gbuffer joins both side
   // branches just before the texel kernel. They write disjoint fields.
-  cudaStream_t ws = ctx.aux ? ctx.aux : s;
   cudaStream_t us = ctx.aux2 ? ctx.aux2 : s;
   if (ws != s || us != s) MFB_CUDA_TRY(cudaEventRecord(ctx.fork2, s));
   if (ws != s) MFB_CUDA_TRY(cudaStreamWaitEvent(ws, ctx.fork2, 0));
@@ -1006,48 +1468,59 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
   const int ntiles = tiles_x * tiles_y;
   auto* rf = static_cast<const RasterFace*>(plan.faces);
   auto* attrs = static_cast<const AttrFace*>(plan.attrs);
-  int* cnt = ctx.buf<int>("ras.cc", 2 * (ntiles + 1));  // counts, then fill cursors: one fill
-  int* cursor = cnt + ntiles + 1;
-  int* start = ctx.buf<int>("ras.start", ntiles + 1);
-  // Bin capacity: a bound that holds for ordinary atlases; the bake driver
-  // re-runs with the exact total (flags[1] set, total in flags[2]) otherwise.
-  const int64_t cap64 = std::max<int64_t>(ctx.bin_capacity, 8ll * plan.nf + 4ll * ntiles + 1024);
-  const int capacity = static_cast<int>(std::min<int64_t>(cap64, 0x7fffffff));
-  int* bins = ctx.buf<int>("ras.bins", capacity);
-  ctx.fill(cnt, 0, sizeof(int) * 2 * (ntiles + 1), s);
-  k_bin_count<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, cnt);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, ntiles + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, start, ntiles + 1, s));
-  k_bin_fill<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, start, cursor, bins,
-                                              capacity, flags_dev + 1, ntiles);
-  if (row_counts_dev) ctx.fill(row_counts_dev, 0, sizeof(int64_t) * g.rows, s);
-  // the wedge frames and reliability branches of prepare_lowpoly
-  for (cudaEvent_t e : plan.pending)
-    if (e) MFB_CUDA_TRY(cudaStreamWaitEvent(s, e, 0));
+  const int* start = plan.tile_start;
+  const int* bins = plan.bins;
+  int capacity = plan.capacity;
+  if (!plan.binned) {  // (the cooperative prep bins, resets the counters and the row counts itself)
+    int* cnt = ctx.buf<int>("ras.cc", 2 * (ntiles + 1));  // counts, then fill cursors: one fill
+    int* cursor = cnt + ntiles + 1;
+    int* tstart = ctx.buf<int>("ras.start", ntiles + 1);
+    capacity = bin_capacity_for(ctx, plan.nf, ntiles);
+    int* tbins = ctx.buf<int>("ras.bins", capacity);
+    ctx.fill(cnt, 0, sizeof(int) * 2 * (ntiles + 1), s);
+    k_bin_count<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, cnt);
+    size_t tmp = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, tstart, ntiles + 1, s);
+    MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, tstart, ntiles + 1, s));
+    k_bin_fill<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, tstart, cursor, tbins,
+                                                capacity, flags_dev + 1, ntiles);
+    ctx.count_launch(3);
+    if (row_counts_dev) ctx.fill(row_counts_dev, 0, sizeof(int64_t) * g.rows, s);
+    start = tstart;
+    bins = tbins;
+  }
+  // the wedge frames and reliability branches of prepare_lowpoly: joined
+  // before the texel kernel, or (split raster) before the interpolation
+  auto join_prep = [&] {
+    for (cudaEvent_t e : plan.pending)
+      if (e) MFB_CUDA_TRY(cudaStreamWaitEvent(s, e, 0));
+  };
   auto* rc = reinterpret_cast<unsigned long long*>(row_counts_dev);
   // Split raster (default): coverage + compaction, then a barrier-free
   // interpolation kernel over the compacted queries. MFB_RASTER_SPLIT=0
   // selects the single fused kernel (A/B).
   const bool split = raster_links_supported();
   if (fused && split) {
-    ctx.fill(fused->q.count, 0, 4 * sizeof(int), s);  // [3]: transfer batch cursor
+    if (!plan.binned) ctx.fill(fused->q.count, 0, 4 * sizeof(int), s);  // [3]: transfer batch cursor
     RasterFused f2 = *fused;
     f2.pend = ctx.buf<int2>("ras.pend", g.texels());
     k_raster<2><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
                                        g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, f2);
     if (fused->cover_done) MFB_CUDA_TRY(cudaEventRecord(fused->cover_done, s));
+    join_prep();
     k_interp<<<kNumSMs * 8, 256, 0, s>>>(rf, attrs, f2.pend, fused->q.count, res, g.row0, fused->q);
     ctx.count_launch();
   } else if (fused) {
-    ctx.fill(fused->q.count, 0, 4 * sizeof(int), s);  // [3]: transfer batch cursor
+    if (!plan.binned) ctx.fill(fused->q.count, 0, 4 * sizeof(int), s);  // [3]: transfer batch cursor
+    join_prep();
     k_raster<1><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0, g.pos,
                                        g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, *fused);
   } else {
+    join_prep();
     k_raster<0><<<ntiles, 256, 0, s>>>(rf, attrs, start, bins, capacity, res, row_begin, row_end, g.row0,
                                        g.pos, g.nrm, g.tan, g.bit, g.valid, g.rel, flags_dev, rc, RasterFused{});
   }
-  ctx.count_launch(3);
+  ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
 }
 

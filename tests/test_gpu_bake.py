@@ -243,3 +243,33 @@ def test_host_bake_pinned_banded_download(gpu_ctx, port, pair_a, res, radius):
         assert np.array_equal(got, ref["rgb"])
     o = port.bake(p.lowpoly, p.dense, res, p.bbox_diagonal, p.max_distance_fraction, radius, debug=True)
     assert_rgb_parity(pinned, o["rgb"], o["ts"])
+
+
+def test_fused_bake_unreliable_faces(gpu_ctx, port):
+    """Late reliability in the fused bake: the coverage kernel compacts every
+    valid texel and the texels of unreliable faces (the stretched face of the
+    test_bake.cpp:77-100 KAT) become dead records encoded as (128,128,255) by
+    the transfer, dilated like any other source - equal to the port, through
+    the device-mesh and the host-buffer (pinned and pageable) entry points."""
+    torch = pytest.importorskip("torch")
+    m = TriangleMesh([[0, 0, 0], [1, 0, 0], [1, 1, 0], [0, 1, 0], [1, 0, 200]], [[0, 1, 2], [0, 2, 3], [1, 4, 2]],
+                     uvs=[[0.05, 0.05], [0.35, 0.05], [0.35, 0.35], [0.05, 0.35], [0.65, 0.05]],
+                     face_uvs=[[0, 1, 2], [0, 2, 3], [1, 4, 2]])
+    dense = fx.bake_pair(24, 4, 64, name="unrel").dense
+    dense.positions[:] = dense.positions * 250.0 + np.array([0.5, 0.5, 100.0])
+    for radius in (0, 4, 9):
+        o = port.bake(m, dense, 128, float(dense.bbox_diagonal()), 0.5, radius, debug=True)
+        assert (o["face"] == -2).sum() > 0  # unreliable texels present
+        out = mf.bake_normal_map(m, dense, 128, float(dense.bbox_diagonal()), 0.5, radius, debug=True, stats=True)
+        assert np.array_equal(out["face"], o["face"])
+        assert_rgb_parity(out["rgb"], o["rgb"], o["ts"])
+        assert out["stats"]["queries"] == o["n_queries"]
+        assert out["stats"]["valid_texels"] == o["n_valid"]
+        for pinned in (True, False):
+            buf = torch.empty((128, 128, 3), dtype=torch.uint8)
+            if pinned:
+                buf = buf.pin_memory()
+            host = buf.numpy()
+            for _ in range(3):  # eager, captured, replayed
+                got = mf.bake_normal_map(m, dense, 128, float(dense.bbox_diagonal()), 0.5, radius, out=host)
+                assert np.array_equal(got.reshape(-1, 3), out["rgb"].reshape(-1, 3))
