@@ -43,4 +43,13 @@ ImageU8 dilateSeams(const ImageU8& map, const GBuffer& gbuffer, int radius = 4);
 ImageU8 bakeNormalMap(const TriangleMesh& lowpoly, const TriangleMesh& highpoly, int resolution,
                       double bboxDiagonal, double maxDistanceFraction = 0.01, int radius = 4);
 
+// B200 extensions (no reference equivalent; north_star item 4): the same
+// fused bake written as RGBA8 (the RGB8 bytes plus alpha 255, 4 bytes per
+// texel) or as RG16 (tangent-space x, y as unorm16 round((v + 1) / 2 * 65535);
+// z = sqrt(1 - x^2 - y^2) on decode; background and neutral texels (0, 0)).
+ImageU8 bakeNormalMapRGBA8(const TriangleMesh& lowpoly, const TriangleMesh& highpoly, int resolution,
+                           double bboxDiagonal, double maxDistanceFraction = 0.01, int radius = 4);
+Image<std::uint16_t> bakeNormalMapRG16(const TriangleMesh& lowpoly, const TriangleMesh& highpoly, int resolution,
+                                       double bboxDiagonal, double maxDistanceFraction = 0.01, int radius = 4);
+
 }  // namespace meshforge

@@ -146,6 +146,21 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
                        int radius, uint8_t* rgb_out, int32_t* dbg_face, double* dbg_ts,
                        mf_bake_stats* stats);
 
+/* Atlas encodings of the fused bake (north_star item 4). RGB8 is the
+ * reference's ImageU8(res, res, 3) (gbuffer.cpp:212, encodeChannel :85-88).
+ * RGBA8: the same three bytes plus alpha 255, 4 bytes per texel. RG16: the
+ * normalised tangent-space x, y as unorm16 round((v + 1) / 2 * 65535),
+ * clamped, little-endian x then y (z = sqrt(1 - x^2 - y^2) on decode);
+ * background and neutral texels both store (32768, 32768). Dilation copies
+ * whole pixels, as dilateSeams does (gbuffer.cpp:311-318). */
+enum { MF_ATLAS_RGB8 = 0, MF_ATLAS_RGBA8 = 1, MF_ATLAS_RG16 = 2 };
+
+/* mf_bake_normal_map with an atlas encoding: out holds res*res*bpp bytes,
+ * bpp = 3 (RGB8) or 4 (RGBA8, RG16). format RGB8 is mf_bake_normal_map. */
+int mf_bake_normal_map_ex(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_view* highpoly,
+                          int resolution, double bbox_diagonal, double max_distance_fraction,
+                          int radius, int format, void* out, mf_bake_stats* stats);
+
 /* Same bake over device-resident meshes into a device buffer, for rows
  * [row_begin, row_end) of the atlas (0, res for the whole map). rgb_dev holds
  * (row_end - row_begin) * res * 3 bytes. Rows outside the range are still
@@ -153,6 +168,11 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
 int mf_bake_normal_map_dev(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int resolution,
                            double bbox_diagonal, double max_distance_fraction, int radius,
                            int row_begin, int row_end, uint8_t* rgb_dev, mf_bake_stats* stats);
+/* mf_bake_normal_map_dev with an atlas encoding (MF_ATLAS_*): out_dev holds
+ * (row_end - row_begin) * res * bpp bytes (4-byte aligned for bpp 4). */
+int mf_bake_normal_map_dev_ex(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int resolution,
+                              double bbox_diagonal, double max_distance_fraction, int radius,
+                              int row_begin, int row_end, int format, void* out_dev, mf_bake_stats* stats);
 
 /* Per-row valid-texel counts (res int64 on the host) from a coverage
  * pre-pass; used to balance row shards by N_v. */

@@ -77,7 +77,10 @@ SIGNATURES = [
     ("mf_transfer_normals", _I, [_VP, _I, _VP, _VP, _VP, _VP, _VP, _VP, _MV, _D, _D, _VP]),
     ("mf_dilate_seams", _I, [_VP, _I, _I, _I, _VP, _I, _VP, _I, _VP]),
     ("mf_bake_normal_map", _I, [_VP, _MV, _MV, _I, _D, _D, _I, _VP, _VP, _VP, ctypes.POINTER(MfBakeStats)]),
+    ("mf_bake_normal_map_ex", _I, [_VP, _MV, _MV, _I, _D, _D, _I, _I, _VP, ctypes.POINTER(MfBakeStats)]),
     ("mf_bake_normal_map_dev", _I, [_VP, _VP, _VP, _I, _D, _D, _I, _I, _I, _VP, ctypes.POINTER(MfBakeStats)]),
+    ("mf_bake_normal_map_dev_ex", _I, [_VP, _VP, _VP, _I, _D, _D, _I, _I, _I, _I, _VP,
+                                       ctypes.POINTER(MfBakeStats)]),
     ("mf_coverage_rows", _I, [_VP, _VP, _I, _VP]),
     ("mf_bvh_build", _I, [_VP, _VP, ctypes.POINTER(_VP)]),
     ("mf_bvh_destroy", None, [_VP]),

@@ -176,6 +176,24 @@ ImageU8 bakeNormalMap(const TriangleMesh& lowpoly, const TriangleMesh& highpoly,
   return map;
 }
 
+ImageU8 bakeNormalMapRGBA8(const TriangleMesh& lowpoly, const TriangleMesh& highpoly, int resolution,
+                           double bboxDiagonal, double maxDistanceFraction, int radius) {
+  ImageU8 map(resolution > 0 ? resolution : 0, resolution > 0 ? resolution : 0, 4);
+  const mf_mesh_view lv = viewOf(lowpoly), hv = viewOf(highpoly);
+  check(mf_bake_normal_map_ex(context(), &lv, &hv, resolution, bboxDiagonal, maxDistanceFraction, radius,
+                              MF_ATLAS_RGBA8, map.data.empty() ? nullptr : map.data.data(), nullptr));
+  return map;
+}
+
+Image<std::uint16_t> bakeNormalMapRG16(const TriangleMesh& lowpoly, const TriangleMesh& highpoly, int resolution,
+                                       double bboxDiagonal, double maxDistanceFraction, int radius) {
+  Image<std::uint16_t> map(resolution > 0 ? resolution : 0, resolution > 0 ? resolution : 0, 2);
+  const mf_mesh_view lv = viewOf(lowpoly), hv = viewOf(highpoly);
+  check(mf_bake_normal_map_ex(context(), &lv, &hv, resolution, bboxDiagonal, maxDistanceFraction, radius,
+                              MF_ATLAS_RG16, map.data.empty() ? nullptr : map.data.data(), nullptr));
+  return map;
+}
+
 // ------------------------------------------------------------------ Bvh
 struct Bvh::Handle {
   mf_mesh* mesh = nullptr;

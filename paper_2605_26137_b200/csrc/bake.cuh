@@ -64,6 +64,7 @@ struct Ctx {
   void* cub_tmp[7] = {};  // main, side, aux, aux2, side2, lowhi, dn
   size_t cub_tmp_bytes[7] = {};
   int64_t bin_capacity = 0;         // raster tile-bin capacity hint (grows on overflow)
+  int fmt = MF_ATLAS_RGB8;          // atlas encoding of the fused bake in progress (MF_ATLAS_*)
 
   // Grow-only named device scratch (never shrinks; freed with the context).
   void* buf(const std::string& name, size_t bytes);
@@ -270,6 +271,7 @@ struct QueryList {
 // and the query records; debug planes get -1/-2 for invalid/unreliable.
 struct RasterFused {
   uint8_t* rgb = nullptr;
+  int fmt = MF_ATLAS_RGB8;  // atlas encoding of rgb (MF_ATLAS_*)
   QueryList q;
   int32_t* dbg_face = nullptr;
   double* dbg_ts = nullptr;
@@ -332,6 +334,7 @@ struct TransferArgs {
   const int32_t* hi_faces = nullptr;
   double max_dist = 0.0;
   uint8_t* rgb = nullptr;           // raw map slab (indexed by the query's slab texel)
+  int fmt = MF_ATLAS_RGB8;          // its encoding (MF_ATLAS_*)
   int32_t* dbg_face = nullptr;
   double* dbg_ts = nullptr;
   unsigned long long* counters = nullptr;  // [queries, hits]
@@ -395,7 +398,8 @@ void dilate_seams_to(Ctx& ctx, cudaStream_t s, int width, int height, int channe
 // their colour in `rgb` now, the others are linked to their source query.
 bool dilate_links_supported(int radius);
 void dilate_links(Ctx& ctx, cudaStream_t s, int res, const uint8_t* valid, int radius, const int* qslot,
-                  int* dep_head, int* dep_next, uint8_t* rgb, const uint8_t* tile_state = nullptr);
+                  int* dep_head, int* dep_next, uint8_t* rgb, const uint8_t* tile_state = nullptr,
+                  int fmt = MF_ATLAS_RGB8);
 void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
                   const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
                   int radius, uint8_t* map_out, int out_row0, int out_rows);

@@ -719,6 +719,7 @@ struct BakeEnq {
   int res, radius, rb, re, s0, s1;
   double diag, frac;
   uint8_t* rgb_out;
+  int bpp = 3;  // bytes per atlas texel (c.fmt)
   bool debug;
   const OutSet* pub = nullptr;  // set: the dilation stores every output row into each buffer
   Timer& tm;
@@ -757,7 +758,9 @@ struct BakeEnq {
     flags = c.buf<int>("bake.flags", 4);
     counters = c.buf<unsigned long long>("bake.counters", 4);
     links = !pub && rb == 0 && re == res && dilate_links_supported(radius) && raster_links_supported();
-    fo.rgb = links ? rgb_out : c.buf<uint8_t>("bake.raw", 3 * g.texels());
+    fo.fmt = c.fmt;
+    bpp = atlas_bpp(c.fmt);
+    fo.rgb = links ? rgb_out : c.buf<uint8_t>("bake.raw", bpp * g.texels());
     fo.q = query_list(c, g.texels());
     if (links) {
       fo.qslot = c.buf<int>("bake.qslot", g.texels());
@@ -807,7 +810,8 @@ struct BakeEnq {
     cudaStream_t t = ls ? ls : s;
     if (ls) MFB_CUDA_TRY(cudaStreamWaitEvent(ls, fo.cover_done, 0));
     mk.d0 = tm.mark(t);
-    if (links) dilate_links(c, t, res, g.valid, radius, fo.qslot, fo.dep_head, dep_next, rgb_out, fo.tile_state);
+    if (links) dilate_links(c, t, res, g.valid, radius, fo.qslot, fo.dep_head, dep_next, rgb_out, fo.tile_state,
+                             fo.fmt);
     mk.d1 = tm.mark(t);
     if (links) {
       if (band_sync) band_init(c, t, bs);
@@ -890,6 +894,7 @@ struct BakeEnq {
     ta.hi_faces = hi->m.faces;
     ta.max_dist = frac * diag;
     ta.rgb = fo.rgb;
+    ta.fmt = fo.fmt;
     ta.dbg_face = fo.dbg_face;
     ta.dbg_ts = fo.dbg_ts;
     ta.counters = counters;
@@ -919,8 +924,9 @@ struct BakeEnq {
       for (int b = 0; b < bs.nb; ++b) {
         const int r0 = b * bs.rows, r1 = std::min(res, r0 + bs.rows);
         stream_wait_value(cp, bs.ready + b);
-        const int64_t off = 3ll * r0 * res;
-        MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off, 3ll * (r1 - r0) * res, cudaMemcpyDeviceToHost, cp));
+        const int64_t off = static_cast<int64_t>(bpp) * r0 * res;
+        MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off, static_cast<int64_t>(bpp) * (r1 - r0) * res,
+                                     cudaMemcpyDeviceToHost, cp));
         if (band_ev_base >= 0) MFB_CUDA_TRY(cudaEventRecord(c.pool_event(band_ev_base + b), cp));
       }
       MFB_CUDA_TRY(cudaEventRecord(c.join4, cp));
@@ -935,13 +941,15 @@ struct BakeEnq {
     if (links) {  // the atlas is complete
       mk.e5 = tm.mark(s);
       if (host_out)
-        MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, 3ll * (re - rb) * res, cudaMemcpyDeviceToHost, s));
+        MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, static_cast<int64_t>(bpp) * (re - rb) * res,
+                                     cudaMemcpyDeviceToHost, s));
     } else {
-      if (pub) dilate_seams_to(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, *pub, rb, re - rb);
-      else dilate_seams(c, s, res, res, 3, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out, rb, re - rb);
+      if (pub) dilate_seams_to(c, s, res, res, bpp, fo.rgb, g.valid, s0, s1 - s0, radius, *pub, rb, re - rb);
+      else dilate_seams(c, s, res, res, bpp, fo.rgb, g.valid, s0, s1 - s0, radius, rgb_out, rb, re - rb);
       mk.e5 = tm.mark(s);
       if (host_out)
-        MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, 3ll * (re - rb) * res, cudaMemcpyDeviceToHost, s));
+        MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, static_cast<int64_t>(bpp) * (re - rb) * res,
+                                     cudaMemcpyDeviceToHost, s));
     }
     MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(
@@ -996,7 +1004,7 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
   // call that modifies an mf_mesh in place)
   struct Key {
     const void *lo, *hi, *out, *lo_mem, *hi_mem;
-    int lo_nf, lo_nv, lo_nu, hi_nf, hi_nv, res, radius, rb, re, timing;
+    int lo_nf, lo_nv, lo_nu, hi_nf, hi_nv, res, radius, rb, re, timing, fmt;
     int64_t bin_capacity;
     double diag, frac;
   };
@@ -1005,7 +1013,7 @@ void bake_dev(Ctx& c, const mf_mesh* lo, const mf_mesh* hi, int res, double diag
   for (int attempt = 0;; ++attempt) {
     Key key{};
     key = Key{lo, hi, rgb_out, lo->mem, hi->mem, lo->m.nf, lo->m.nv, lo->m.nu, hi->m.nf, hi->m.nv, res, radius, rb,
-              re, c.timing ? 1 : 0, c.bin_capacity, diag, frac};
+              re, c.timing ? 1 : 0, c.fmt, c.bin_capacity, diag, frac};
     std::vector<char> kb(reinterpret_cast<const char*>(&key), reinterpret_cast<const char*>(&key) + sizeof(key));
     if (pub) {  // published bakes are keyed on their destination buffers too
       const char* pb = reinterpret_cast<const char*>(pub);
@@ -1222,14 +1230,15 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     drain();
     throw;
   }
-  uint8_t* drgb = c.buf<uint8_t>("bake.rgb", 3 * static_cast<int64_t>(res) * res);
+  const int bpp = atlas_bpp(c.fmt);
+  uint8_t* drgb = c.buf<uint8_t>("bake.rgb", bpp * static_cast<int64_t>(res) * res);
   BakeMarks mk;
   Timer tmb(c, 8);
   BakeEnq q(c, &lo, &hi, res, diag, frac, radius, 0, res, drgb, false, tmb, mk);
   // A pageable rgb_out gets the atlas through pinned staging: its row bands
   // are copied out by the host pool as their DMAs land.
   const bool stage_out = !host_pinned(rgb_out);
-  uint8_t* host_dst = stage_out ? static_cast<uint8_t*>(c.host_buf("stage.rgb", 3 * static_cast<size_t>(res) * res))
+  uint8_t* host_dst = stage_out ? static_cast<uint8_t*>(c.host_buf("stage.rgb", bpp * static_cast<size_t>(res) * res))
                                 : rgb_out;
   if (q.links && wait_value_usable(c)) {
     q.band_sync = true;
@@ -1261,7 +1270,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     const int64_t k[] = {reinterpret_cast<int64_t>(lo.m.pos), reinterpret_cast<int64_t>(lo.m.faces),
                          reinterpret_cast<int64_t>(lo.m.nrm), reinterpret_cast<int64_t>(lo.m.uvs),
                          reinterpret_cast<int64_t>(lo.m.fuv), lo.m.nf, lo.m.nv, lo.m.nu, res, c.bin_capacity,
-                         q.band_sync ? 1 : 0, radius};
+                         q.band_sync ? 1 : 0, radius, c.fmt};
     run_graphed(c, c.g_low, s, key_bytes(k), use_graphs, [&] { q.low(); });
   }
   if (!early) upload_hi();
@@ -1289,7 +1298,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   q.dense_side(use_graphs);
   cudaEvent_t t2 = tm.mark(s);
   q.tail(hflags, hcnt, host_dst);
-  const int64_t row_bytes = 3ll * res;
+  const int64_t row_bytes = static_cast<int64_t>(bpp) * res;
   if (stage_out && q.band_sync) {
     const int dev = c.device, nb = q.bs.nb, rows = q.bs.rows;
     std::vector<cudaEvent_t> ev(nb);
@@ -1333,7 +1342,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     c.invalidate_graphs();
     Timer tr(c, 8);
     bake_dev(c, &lo, &hi, res, diag, frac, radius, 0, res, drgb, nullptr, nullptr, st, tr, nullptr);
-    MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, s));
+    MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, bpp * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
     return;
   }
@@ -1586,12 +1595,26 @@ int mf_dilate_seams(mf_ctx* ctx, int width, int height, int channels, const uint
   });
 }
 
-int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_view* highpoly, int res,
-                       double bbox_diagonal, double max_distance_fraction, int radius, uint8_t* rgb_out,
-                       int32_t* dbg_face, double* dbg_ts, mf_bake_stats* stats) {
+// The atlas encoding of one bake call (Ctx::fmt), restored when the call ends.
+struct FmtScope {
+  Ctx& c;
+  int saved;
+  FmtScope(Ctx& cc, int fmt) : c(cc), saved(cc.fmt) {
+    if (fmt != MF_ATLAS_RGB8 && fmt != MF_ATLAS_RGBA8 && fmt != MF_ATLAS_RG16)
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "unknown atlas format");
+    c.fmt = fmt;
+  }
+  ~FmtScope() { c.fmt = saved; }
+};
+
+static int bake_host_call(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_view* highpoly, int res,
+                          double bbox_diagonal, double max_distance_fraction, int radius, int fmt, uint8_t* rgb_out,
+                          int32_t* dbg_face, double* dbg_ts, mf_bake_stats* stats) {
   if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
   return guarded(ctx, [&]() -> int {
     Ctx& c = ctx->c;
+    FmtScope fs(c, fmt);
+    const int bpp = atlas_bpp(fmt);
     // debug outputs take the sequential upload -> bake -> download path
     if (!dbg_face && !dbg_ts) {
       mf_bake_stats local{};
@@ -1614,13 +1637,14 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
     ht.mark("upload hi");
     cudaEvent_t t1 = tm.mark(c.stream);
     if (!rgb_out) throw ApiError(MF_ERR_BAD_ARGUMENT, "rgb_out is null");
-    uint8_t* drgb = c.buf<uint8_t>("bake.rgb", 3 * static_cast<int64_t>(res) * res);
+    uint8_t* drgb = c.buf<uint8_t>("bake.rgb", bpp * static_cast<int64_t>(res) * res);
     mf_bake_stats local{};
     bake_dev(c, &lo, &hi, res, bbox_diagonal, max_distance_fraction, radius, 0, res, drgb, dbg_face, dbg_ts,
              &local, tmb, t1);
     ht.mark("bake_dev");
     cudaEvent_t t2 = tm.mark(c.stream);
-    MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, 3 * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaMemcpyAsync(rgb_out, drgb, bpp * static_cast<int64_t>(res) * res, cudaMemcpyDeviceToHost,
+                                 c.stream));
     cudaEvent_t t3 = tm.mark(c.stream);
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
     ht.mark("download+sync");
@@ -1637,11 +1661,36 @@ int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_v
   });
 }
 
+int mf_bake_normal_map(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_view* highpoly, int res,
+                       double bbox_diagonal, double max_distance_fraction, int radius, uint8_t* rgb_out,
+                       int32_t* dbg_face, double* dbg_ts, mf_bake_stats* stats) {
+  return bake_host_call(ctx, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius, MF_ATLAS_RGB8,
+                        rgb_out, dbg_face, dbg_ts, stats);
+}
+
+int mf_bake_normal_map_ex(mf_ctx* ctx, const mf_mesh_view* lowpoly, const mf_mesh_view* highpoly, int res,
+                          double bbox_diagonal, double max_distance_fraction, int radius, int format, void* out,
+                          mf_bake_stats* stats) {
+  return bake_host_call(ctx, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius, format,
+                        static_cast<uint8_t*>(out), nullptr, nullptr, stats);
+}
+
 int mf_bake_normal_map_dev(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int res, double bbox_diagonal,
                            double max_distance_fraction, int radius, int row_begin, int row_end, uint8_t* rgb_dev,
                            mf_bake_stats* stats) {
+  return mf_bake_normal_map_dev_ex(ctx, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius,
+                                   row_begin, row_end, MF_ATLAS_RGB8, rgb_dev, stats);
+}
+
+int mf_bake_normal_map_dev_ex(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highpoly, int res, double bbox_diagonal,
+                              double max_distance_fraction, int radius, int row_begin, int row_end, int format,
+                              void* out_dev, mf_bake_stats* stats) {
+  uint8_t* rgb_dev = static_cast<uint8_t*>(out_dev);
   if (!ctx || !lowpoly || !highpoly || !rgb_dev) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
   return guarded(ctx, [&]() -> int {
+    FmtScope fs(ctx->c, format);
+    if (format != MF_ATLAS_RGB8 && (reinterpret_cast<uintptr_t>(rgb_dev) & 3))
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "4-byte atlas formats need a 4-byte aligned buffer");
     Timer tm(ctx->c, 8);
     mf_bake_stats local{};
     bake_dev(ctx->c, lowpoly, highpoly, res, bbox_diagonal, max_distance_fraction, radius, row_begin, row_end,

@@ -91,6 +91,49 @@ __host__ __device__ __forceinline__ d3 any_perpendicular(d3 n) {
   return len > 1e-20 ? p / len : mk3(1.0, 0.0, 0.0);
 }
 
+// ---------------------------------------------------------------- atlas pixel formats
+// (north_star item 4; MF_ATLAS_* in mfbake.h). RGB8 is the reference's
+// ImageU8(res, res, 3) (gbuffer.cpp:212) with encodeChannel (gbuffer.cpp:85-88);
+// RGBA8 is the same bytes plus alpha 255 as one aligned 32-bit store; RG16 is
+// the tangent-space x, y as unorm16 (z = sqrt(1 - x^2 - y^2) on decode), one
+// 32-bit store: the background and the neutral texel both encode (0, 0).
+__host__ __device__ __forceinline__ int atlas_bpp(int fmt) { return fmt == MF_ATLAS_RGB8 ? 3 : 4; }
+__device__ __forceinline__ uint32_t enc8(double v) {
+  const long long q = llround((v + 1.0) * 0.5 * 255.0);
+  return static_cast<uint32_t>(q < 0 ? 0 : (q > 255 ? 255 : q));
+}
+__device__ __forceinline__ uint32_t enc16(double v) {
+  const long long q = llround((v + 1.0) * 0.5 * 65535.0);
+  return static_cast<uint32_t>(q < 0 ? 0 : (q > 65535 ? 65535 : q));
+}
+// packed pixel: RGB8/RGBA8 little-endian r | g << 8 | b << 16 | a << 24, RG16 x | y << 16
+__device__ __forceinline__ uint32_t px_rgb(int fmt, uint32_t r, uint32_t g, uint32_t b) {
+  return r | (g << 8) | (b << 16) | (fmt == MF_ATLAS_RGBA8 ? 0xff000000u : 0u);
+}
+__device__ __forceinline__ uint32_t px_encode(int fmt, double x, double y, double z) {
+  if (fmt == MF_ATLAS_RG16) return enc16(x) | (enc16(y) << 16);
+  return px_rgb(fmt, enc8(x), enc8(y), enc8(z));
+}
+constexpr uint32_t kRG16Zero = 32768u | (32768u << 16);  // enc16(0), enc16(0)
+// tangent-space (0, 0, 1): (128, 128, 255) (gbuffer.cpp:212-227)
+__device__ __forceinline__ uint32_t px_neutral(int fmt) {
+  return fmt == MF_ATLAS_RG16 ? kRG16Zero : px_rgb(fmt, 128, 128, 255);
+}
+// invalid texel: ImageU8(res, res, 3, 128) (gbuffer.cpp:212)
+__device__ __forceinline__ uint32_t px_background(int fmt) {
+  return fmt == MF_ATLAS_RG16 ? kRG16Zero : px_rgb(fmt, 128, 128, 128);
+}
+__device__ __forceinline__ void px_store(uint8_t* base, int64_t t, int fmt, uint32_t v) {
+  if (fmt == MF_ATLAS_RGB8) {
+    uint8_t* o = base + 3 * t;
+    o[0] = static_cast<uint8_t>(v);
+    o[1] = static_cast<uint8_t>(v >> 8);
+    o[2] = static_cast<uint8_t>(v >> 16);
+  } else {
+    reinterpret_cast<uint32_t*>(base)[t] = v;
+  }
+}
+
 // ---------------------------------------------------------------- launch geometry
 constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
 

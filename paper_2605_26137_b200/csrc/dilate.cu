@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(256) k_dilate_links(int width, int height, con
                                                       int radius, const int* __restrict__ qslot,
                                                       int* __restrict__ dep_head, int* __restrict__ dep_next,
                                                       uint8_t* __restrict__ rgb,
-                                                      const uint8_t* __restrict__ tile_state) {
+                                                      const uint8_t* __restrict__ tile_state, int fmt) {
   extern __shared__ int smi[];
   const int rw = kTW + 2 * radius;
   const int tiles_x = (width + kTW - 1) / kTW;
@@ -535,9 +535,7 @@ __global__ void __launch_bounds__(256) k_dilate_links(int width, int height, con
       const int slot = qslot[src];
       if (slot >= 0) dep_next[t] = atomicExch(&dep_head[slot], static_cast<int>(t));
     } else {
-      rgb[3 * t] = 128;
-      rgb[3 * t + 1] = 128;
-      rgb[3 * t + 2] = 255;
+      px_store(rgb, t, fmt, px_neutral(fmt));
     }
   }
 }
@@ -610,7 +608,7 @@ static size_t dilate_smem(int radius) {
 bool dilate_links_supported(int radius) { return radius > 0 && radius <= kSparseMaxR; }
 
 void dilate_links(Ctx& ctx, cudaStream_t s, int res, const uint8_t* valid, int radius, const int* qslot,
-                  int* dep_head, int* dep_next, uint8_t* rgb, const uint8_t* tile_state) {
+                  int* dep_head, int* dep_next, uint8_t* rgb, const uint8_t* tile_state, int fmt) {
   static std::atomic<unsigned long long> attr_set{0};
   int dev = 0;
   MFB_CUDA_TRY(cudaGetDevice(&dev));
@@ -621,7 +619,7 @@ void dilate_links(Ctx& ctx, cudaStream_t s, int res, const uint8_t* valid, int r
   }
   const int tiles = ((res + kTW - 1) / kTW) * ((res + kTH - 1) / kTH);
   k_dilate_links<<<tiles, 256, sparse_smem(radius), s>>>(res, res, valid, radius, qslot, dep_head, dep_next, rgb,
-                                                            tile_state);
+                                                            tile_state, fmt);
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
 }

@@ -261,10 +261,6 @@ __device__ __forceinline__ void traverse_closest(const BNode* __restrict__ nodes
   }
 }
 
-__device__ __forceinline__ uint8_t encode_channel(double v) {
-  const long long q = llround((v + 1.0) * 0.5 * 255.0);
-  return static_cast<uint8_t>(q < 0 ? 0 : (q > 255 ? 255 : q));
-}
 
 // ---------------------------------------------------------------- per-thread while-while transfer
 // One query per thread over the compacted, spatially coherent query list.
@@ -418,7 +414,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     unsigned long long* __restrict__ prof_out, int qcap = 0, int res = 0, int slab_row0 = 0,
     int* __restrict__ face_map = nullptr, const double* __restrict__ hiPos = nullptr,
     const TBox* __restrict__ tbox = nullptr, const int* __restrict__ dep_head = nullptr,
-    const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}) {
+    const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}, int fmt = MF_ATLAS_RGB8) {
   const int nq = qcount[kPass == 2 ? 1 : 0];
   const int lane = threadIdx.x & 31;
   if (kProf && lane == 0) {
@@ -563,7 +559,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     const int texel = dead ? ~__float_as_int(p.w) : __float_as_int(p.w);
     const d3 qe = q;
     if (kPass == 1) face_map[texel] = best.face;
-    uint8_t px[3] = {128, 128, 255};
+    uint32_t px = px_neutral(fmt);
     double ts3[3] = {0.0, 0.0, 0.0};
     if (best.face >= 0) {
       ++hits;
@@ -583,25 +579,15 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       const double len = norm(ts);
       if (!(len < 1e-12)) {
         ts = ts / len;
-        px[0] = encode_channel(ts.x);
-        px[1] = encode_channel(ts.y);
-        px[2] = encode_channel(ts.z);
+        px = px_encode(fmt, ts.x, ts.y, ts.z);  // encodeChannel (gbuffer.cpp:85-88) per channel
         ts3[0] = ts.x;
         ts3[1] = ts.y;
         ts3[2] = ts.z;
       }
     }
-    uint8_t* o = rgb + 3ll * texel;
-    o[0] = px[0];
-    o[1] = px[1];
-    o[2] = px[2];
+    px_store(rgb, texel, fmt, px);
     if (dep_head) {  // dilation: the gutter texels whose source is this texel
-      for (int t = __ldcs(dep_head + i); t >= 0; t = dep_next[t]) {
-        uint8_t* d = rgb + 3ll * t;
-        d[0] = px[0];
-        d[1] = px[1];
-        d[2] = px[2];
-      }
+      for (int t = __ldcs(dep_head + i); t >= 0; t = dep_next[t]) px_store(rgb, t, fmt, px);
     }
     if (kBands && bands.done) {  // this batch's texels (and their gutter texels) are written
       const int band = texel / bands.res / bands.rows;
@@ -1264,7 +1250,7 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
                                               a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, \
                                               D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf, \
                                               a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions,  \
-                                              bvh.tbox, a.dep_head, a.dep_next, a.bands)
+                                              bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt)
 #define MFB_XFER_TP(PASS)                                               \
   if (prof) {                                                           \
     if (dbg) MFB_XFER_T(true, true, PASS); else MFB_XFER_T(false, true, PASS); \
@@ -1279,7 +1265,7 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     k_transfer_t<false, false, 0, true><<<g2, 128, 0, s>>>(
         bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
         a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
-        a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands);
+        a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt);
   } else {
     MFB_XFER_TP(0);
   }

@@ -906,10 +906,7 @@ __device__ __forceinline__ void emit_fused(int64_t gi, int x, int y, bool in, ui
   if (!in) return;
   if (gvalid) gvalid[gi] = valid;
   if (!is_q) {
-    uint8_t* o = fo.rgb + 3 * gi;
-    o[0] = 128;
-    o[1] = 128;
-    o[2] = valid ? 255 : 128;  // gbuffer.cpp:212-213 background / neutral
+    px_store(fo.rgb, gi, fo.fmt, valid ? px_neutral(fo.fmt) : px_background(fo.fmt));  // gbuffer.cpp:212-227
     if (fo.dbg_face) fo.dbg_face[gi] = valid ? -2 : -1;
     if (fo.dbg_ts) {
       fo.dbg_ts[3 * gi] = 0.0;
@@ -1123,10 +1120,7 @@ __global__ void MFB_RASTER_BOUNDS k_raster(const RasterFace* __restrict__ rf,
       }
       return;
     }
-    uint8_t* o = fo.rgb + 3 * gi;
-    o[0] = 128;
-    o[1] = 128;
-    o[2] = valid ? 255 : 128;  // gbuffer.cpp:212-213 background / neutral
+    px_store(fo.rgb, gi, fo.fmt, valid ? px_neutral(fo.fmt) : px_background(fo.fmt));  // gbuffer.cpp:212-227
     if (fo.dbg_face) fo.dbg_face[gi] = valid ? -2 : -1;
     if (fo.dbg_ts) {
       fo.dbg_ts[3 * gi] = 0.0;

@@ -19,6 +19,7 @@ from .capi import MeshforgeError, check, default_context
 from .mesh import TriangleMesh
 
 __all__ = ["GBuffer", "rasterize_gbuffer", "transfer_normals", "dilate_seams", "bake_normal_map",
+           "bake_normal_map_ex", "decode_rg16",
            "Bvh", "compute_wedge_tangents", "compute_vertex_normals", "MeshforgeError", "TriangleMesh"]
 
 
@@ -118,6 +119,40 @@ def bake_normal_map(lowpoly: TriangleMesh, highpoly: TriangleMesh, resolution: i
     if stats:
         result["stats"] = st.as_dict()
     return result
+
+
+ATLAS_RGB8, ATLAS_RGBA8, ATLAS_RG16 = 0, 1, 2  # MF_ATLAS_* (include/mfbake.h)
+_ATLAS_SHAPE = {ATLAS_RGB8: (3, np.uint8), ATLAS_RGBA8: (4, np.uint8), ATLAS_RG16: (2, np.uint16)}
+
+
+def bake_normal_map_ex(lowpoly: TriangleMesh, highpoly: TriangleMesh, resolution: int, bbox_diagonal: float,
+                       max_distance_fraction: float = 0.01, radius: int = 4, fmt: int = ATLAS_RGBA8,
+                       stats: bool = False, ctx=None, out=None):
+    """bake_normal_map with an atlas encoding (mf_bake_normal_map_ex): RGB8
+    -> (res, res, 3) uint8, RGBA8 -> (res, res, 4) uint8 (alpha 255), RG16
+    -> (res, res, 2) uint16 (tangent-space x, y as unorm16)."""
+    ctx = ctx or default_context()
+    res = int(resolution)
+    ch, dt = _ATLAS_SHAPE.get(fmt, (4, np.uint8))
+    if out is None:
+        out = np.zeros((max(res, 0), max(res, 0), ch), dt)
+    elif out.shape != (res, res, ch) or out.dtype != dt or not out.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"out must be a C-contiguous (res, res, {ch}) {np.dtype(dt).name} array")
+    st = capi.MfBakeStats()
+    lv, hv = lowpoly.view(), highpoly.view()
+    check(ctx.lib.mf_bake_normal_map_ex(ctx.h, ctypes.byref(lv), ctypes.byref(hv), res, float(bbox_diagonal),
+                                        float(max_distance_fraction), int(radius), int(fmt), _p(out),
+                                        ctypes.byref(st)))
+    if not stats:
+        return out
+    return {"atlas": out, "stats": st.as_dict()}
+
+
+def decode_rg16(atlas: np.ndarray) -> np.ndarray:
+    """RG16 atlas -> (res, res, 3) f64 tangent-space vectors (z reconstructed)."""
+    xy = atlas.astype(np.float64) / 65535.0 * 2.0 - 1.0
+    z = np.sqrt(np.clip(1.0 - (xy ** 2).sum(-1), 0.0, None))
+    return np.concatenate([xy, z[..., None]], -1)
 
 
 def compute_wedge_tangents(mesh: TriangleMesh, ctx=None) -> np.ndarray:
