@@ -282,6 +282,69 @@ int mf_raycast_first_brute(mf_ctx* ctx, const mf_mesh_view* mesh, const double* 
                            const double* dirs, int64_t n, double tmin, double tmax, int32_t* face,
                            double* t, double* u, double* v);
 
+/* ---- texfuse: device-resident G-buffer consumers -------- */
+/* The texture-fusion steps of proj/src/texfuse (fuse.h:15-138, mips.h:17-18).
+ * Images are ImageF: row-major interleaved f32. A camera is 7 f64 (direction
+ * xyz, up xyz, halfExtent; OrthoCamera, render/camera.h:12-38) plus the view
+ * resolution passed beside it. The G-buffer planes are the reference layout
+ * (mf_raster_gbuffer). Errors follow the reference's checks: InvalidConfig /
+ * ShapeMismatch as 1 + ErrorCode. */
+typedef struct mf_fuse_options {  /* FuseOptions + BlendOptions (fuse.h:83-86, 122-130) */
+  double edge_threshold;   /* 0.02 */
+  double depth_tolerance;  /* 0.005 */
+  int32_t mip_levels;      /* 6 */
+  float sharpen_strength;  /* 0.2 */
+  double alpha;            /* 4.0 */
+  double epsilon;          /* 1e-8 */
+} mf_fuse_options;
+void mf_fuse_options_default(mf_fuse_options* options);
+/* buildMips' chain length and total f32 count (levels concatenated, each
+ * halving rounding up, stopping at 1x1; mips.cpp:96-112). */
+int64_t mf_mip_chain_floats(int width, int height, int channels, int levels, int* n_levels);
+/* edgeMask (fuse.cpp:66-101) of a rendered view: position w*h*3 f32, face w*h i32. */
+int mf_edge_mask(mf_ctx* ctx, int width, int height, const float* position, const int32_t* face,
+                 double bbox_diagonal, double threshold, uint8_t* mask);
+/* buildMips (mips.cpp:96-112): chain = mf_mip_chain_floats(...) f32, level 0 = base. */
+int mf_build_mips(mf_ctx* ctx, int width, int height, int channels, const float* base, int levels, float sharpen,
+                  float* chain, int* n_levels);
+/* backprojectView (fuse.cpp:103-186): mips = the view's chain (n_mips levels,
+ * level 0 view_res^2 x channels), mask view_res^2; outputs gres^2 x channels
+ * f32 colour and gres^2 sampled flags. */
+int mf_backproject_view(mf_ctx* ctx, int gres, const float* position, const uint8_t* valid, const double* camera,
+                        int view_res, int channels, int n_mips, const float* mips, const uint8_t* mask, float* color,
+                        uint8_t* sampled);
+/* incidenceMap (fuse.cpp:188-221): depth view_res^2 f32; out gres^2 f32. */
+int mf_incidence_map(mf_ctx* ctx, int gres, const float* position, const float* normal, const uint8_t* valid,
+                     const double* camera, int view_res, const float* depth, double bbox_diagonal,
+                     double depth_tolerance, float* out);
+/* blendViews (fuse.cpp:223-280): n_views partial atlases (colors n x w*h*ch,
+ * sampled n x w*h), incidence n x w*h, priors n; out w*h*ch f32 + filled. */
+int mf_blend_views(mf_ctx* ctx, int n_views, int width, int height, int channels, const float* colors,
+                   const uint8_t* sampled, const float* incidence, const double* priors, double alpha, double epsilon,
+                   float* color, uint8_t* filled);
+/* fuseViews (fuse.cpp:292-326) up to the blend (the reference's inpainting
+ * step, fuse.h:110, is declared but never defined by it): per view edgeMask,
+ * buildMips, backprojectView, incidenceMap, then blendViews. cameras n x 7
+ * (host); view_position n x vres^2 x 3, view_face n x vres^2, view_depth n x
+ * vres^2, colors n x vres^2 x channels; priors n (host). options NULL =
+ * defaults. Host-buffer form: */
+int mf_fuse_views(mf_ctx* ctx, int gres, const float* position, const float* normal, const uint8_t* valid,
+                  int n_views, const double* cameras, int view_res, const float* view_position,
+                  const int32_t* view_face, const float* view_depth, int channels, const float* colors,
+                  const double* priors, double bbox_diagonal, const mf_fuse_options* options, float* color,
+                  uint8_t* filled);
+/* Same with every image a device pointer (G-buffer, views, colours and
+ * outputs resident in HBM; cameras and priors stay host arrays). */
+int mf_fuse_views_dev(mf_ctx* ctx, int gres, const float* position, const float* normal, const uint8_t* valid,
+                      int n_views, const double* cameras, int view_res, const float* view_position,
+                      const int32_t* view_face, const float* view_depth, int channels, const float* colors,
+                      const double* priors, double bbox_diagonal, const mf_fuse_options* options, float* color,
+                      uint8_t* filled);
+/* rasterizeGBuffer into device buffers (the G-buffer the texfuse calls
+ * consume without leaving HBM): planes res*res*3 f32, masks res*res u8. */
+int mf_raster_gbuffer_dev(mf_ctx* ctx, mf_mesh* lowpoly, int resolution, float* position, float* normal,
+                          float* tangent, float* bitangent, uint8_t* valid, uint8_t* reliable);
+
 /* ---- lowpoly helpers ----------------------------------------------------- */
 /* computeWedgeTangents (bake/tangent.cpp:22-82): frames n_faces x 3 corners x
  * {tangent, bitangent, normal} x 3 f64 (= std::array<TangentFrame,3>). */

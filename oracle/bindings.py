@@ -321,6 +321,80 @@ class Ref(_Lib):
                                             ctypes.c_int(dilate), _ptr(dom), _ptr(labels), _ptr(dist), _ptr(grid)))
         return labels, dist, grid
 
+    # ---- texfuse (src/texfuse/fuse.cpp, mips.cpp; ref_harness.cpp) ----
+    def footprint(self, jac):
+        """footprintFromJacobian: jac = [[j00, j01], [j10, j11]] -> dict."""
+        j = np.asarray(jac, np.float64).reshape(2, 2)
+        jc = np.ascontiguousarray(j.T).reshape(4)  # column-major
+        out = np.zeros(7)
+        self.fn("footprint")(_ptr(jc), _ptr(out))
+        return dict(axis=out[0:2].copy(), major=out[2], minor=out[3], mip=out[4], taps=int(out[5]))
+
+    def edge_mask(self, pos, face, diag: float, threshold: float = 0.02):
+        face = np.ascontiguousarray(face, np.int32)
+        h, w = face.shape
+        pos = np.ascontiguousarray(pos, np.float32)
+        mask = np.zeros((h, w), np.uint8)
+        self._check(self.fn("edge_mask")(ctypes.c_int(w), ctypes.c_int(h), _ptr(pos), _ptr(face),
+                                         ctypes.c_double(diag), ctypes.c_double(threshold), _ptr(mask)))
+        return mask
+
+    def build_mips(self, base, levels: int = 6, sharpen: float = 0.2):
+        base = np.ascontiguousarray(base, np.float32)
+        h, w, c = base.shape
+        total, dims, ww, hh = 0, [], w, h
+        for l in range(levels):
+            if l and dims[-1] == (1, 1):
+                break
+            if l:
+                ww, hh = max(1, (ww + 1) // 2), max(1, (hh + 1) // 2)
+            dims.append((ww, hh))
+            total += ww * hh * c
+        out = np.zeros(total, np.float32)
+        n = ctypes.c_int(0)
+        self._check(self.fn("build_mips")(ctypes.c_int(w), ctypes.c_int(h), ctypes.c_int(c), _ptr(base),
+                                          ctypes.c_int(levels), ctypes.c_float(sharpen), _ptr(out), ctypes.byref(n)))
+        return out, n.value
+
+    def backproject_view(self, gpos, gvalid, gres: int, cam7, view_res: int, channels: int, n_mips: int, mips, mask):
+        color = np.zeros((gres * gres, channels), np.float32)
+        sampled = np.zeros(gres * gres, np.uint8)
+        self._check(self.fn("backproject_view")(
+            ctypes.c_int(gres), _ptr(np.ascontiguousarray(gpos, np.float32)),
+            _ptr(np.ascontiguousarray(gvalid, np.uint8)), _ptr(np.ascontiguousarray(cam7, np.float64)),
+            ctypes.c_int(view_res), ctypes.c_int(channels), ctypes.c_int(n_mips),
+            _ptr(np.ascontiguousarray(mips, np.float32)), _ptr(np.ascontiguousarray(mask, np.uint8)),
+            _ptr(color), _ptr(sampled)))
+        return color, sampled
+
+    def incidence_map(self, gpos, gnrm, gvalid, gres: int, cam7, view_res: int, depth, diag: float,
+                      tol: float = 0.005):
+        out = np.zeros(gres * gres, np.float32)
+        self._check(self.fn("incidence_map")(
+            ctypes.c_int(gres), _ptr(np.ascontiguousarray(gpos, np.float32)),
+            _ptr(np.ascontiguousarray(gnrm, np.float32)), _ptr(np.ascontiguousarray(gvalid, np.uint8)),
+            _ptr(np.ascontiguousarray(cam7, np.float64)), ctypes.c_int(view_res),
+            _ptr(np.ascontiguousarray(depth, np.float32)), ctypes.c_double(diag), ctypes.c_double(tol), _ptr(out)))
+        return out
+
+    def blend_views(self, colors, sampled, inc, priors, alpha: float = 4.0, eps: float = 1e-8):
+        colors = np.ascontiguousarray(colors, np.float32)
+        k, n, c = colors.shape
+        w = int(round(np.sqrt(n)))
+        out = np.zeros((n, c), np.float32)
+        filled = np.zeros(n, np.uint8)
+        self._check(self.fn("blend_views")(
+            ctypes.c_int(k), ctypes.c_int(w), ctypes.c_int(n // w), ctypes.c_int(c), _ptr(colors),
+            _ptr(np.ascontiguousarray(sampled, np.uint8)), _ptr(np.ascontiguousarray(inc, np.float32)),
+            _ptr(np.ascontiguousarray(priors, np.float64)), ctypes.c_double(alpha), ctypes.c_double(eps),
+            _ptr(out), _ptr(filled)))
+        return out, filled
+
+    def standard_cameras(self, half_extent: float = 0.52) -> np.ndarray:
+        cams = np.zeros((10, 7))
+        self.fn("standard_cameras")(ctypes.c_double(half_extent), _ptr(cams))
+        return cams
+
     def raycast_first(self, m: TriangleMesh, o, d, tmin=0.0, tmax=float("inf"), brute=False):
         o = np.ascontiguousarray(o, dtype=np.float64).reshape(-1, 3)
         d = np.ascontiguousarray(d, dtype=np.float64).reshape(-1, 3)

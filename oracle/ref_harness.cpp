@@ -13,6 +13,8 @@
 //                                                       src/core/mesh.cpp:24-35)
 //   fixtures::icosphere / uvSphere / starBlob / random* (tests/support/fixtures.cpp)
 //   bakedMeanErrorDeg                                  (src/metrics/metrics.cpp:213-290)
+//   texfuse: footprintFromJacobian / edgeMask / backprojectView / incidenceMap /
+//   blendViews (src/texfuse/fuse.cpp:39-280), buildMips (src/texfuse/mips.cpp:96-112)
 // plus the Appendix-D instrumented replica of the per-texel transfer body
 // (gbuffer.cpp:218-248) that reports hit faces, pre-quantisation ts, and the
 // N_node / N_tri counters of the reference best-first loop (bvh.cpp:151-176).
@@ -36,6 +38,8 @@
 #include "meshforge/visibility/visibility.h"
 #include "meshforge/spatial/bvh.h"
 #include "meshforge/spatial/tri_geom.h"
+#include "meshforge/texfuse/fuse.h"
+#include "meshforge/texfuse/mips.h"
 #include "mfbake.h"
 #include "support/fixtures.h"
 
@@ -557,6 +561,147 @@ void ref_random_units(int n, uint64_t seed, double* out) {
 
 double ref_star_blob_radius(uint64_t seed, const double* dir, double base) {
   return fixtures::starBlobRadius(seed, Eigen::Vector3d(dir[0], dir[1], dir[2]), base);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- texfuse
+// The reference declares inpaintAtlas (texfuse/fuse.h:110) and calls it from
+// fuseViews (fuse.cpp:321) but never defines it; this stub
+// only lets fuse.cpp link. Nothing here calls fuseViews.
+namespace meshforge {
+TextureAtlas inpaintAtlas(const TextureAtlas&, const GBuffer&, double, const InpaintOptions&) {
+  throw Error(ErrorCode::InvalidConfig, "inpaintAtlas is not defined by the reference");
+}
+}  // namespace meshforge
+
+namespace {
+OrthoCamera toCamera(const double* cam7, int res) {
+  OrthoCamera cam;
+  cam.direction = {cam7[0], cam7[1], cam7[2]};
+  cam.up = {cam7[3], cam7[4], cam7[5]};
+  cam.halfExtent = cam7[6];
+  cam.resolution = res;
+  return cam;
+}
+ImageF toImage(int w, int h, int c, const float* p) {
+  ImageF im(w, h, c);
+  std::memcpy(im.data.data(), p, sizeof(float) * static_cast<size_t>(w) * h * c);
+  return im;
+}
+std::vector<ImageF> toChain(int w, int h, int c, int levels, const float* p) {
+  std::vector<ImageF> chain;
+  for (int l = 0; l < levels; ++l) {
+    chain.push_back(toImage(w, h, c, p));
+    p += static_cast<size_t>(w) * h * c;
+    w = std::max(1, (w + 1) / 2);
+    h = std::max(1, (h + 1) / 2);
+  }
+  return chain;
+}
+}  // namespace
+
+extern "C" {
+
+// footprintFromJacobian (fuse.cpp:39-64): jac4 column-major; out7 = major axis
+// xy, major length, minor length, mip, taps.
+void ref_footprint(const double* jac4, double* out7) {
+  Eigen::Matrix2d j;
+  j(0, 0) = jac4[0];
+  j(1, 0) = jac4[1];
+  j(0, 1) = jac4[2];
+  j(1, 1) = jac4[3];
+  const TexelFootprint fp = footprintFromJacobian(j);
+  out7[0] = fp.majorAxis.x();
+  out7[1] = fp.majorAxis.y();
+  out7[2] = fp.majorLength;
+  out7[3] = fp.minorLength;
+  out7[4] = fp.mip;
+  out7[5] = fp.taps;
+  out7[6] = 0.0;
+}
+
+// edgeMask (fuse.cpp:66-101) of a rendered view (position f32x3, face i32).
+int ref_edge_mask(int w, int h, const float* pos, const int32_t* face, double diag, double threshold,
+                  uint8_t* mask) {
+  return guarded([&] {
+    RenderedView v;
+    v.position = toImage(w, h, 3, pos);
+    v.face = Image<std::int32_t>(w, h, 1);
+    std::memcpy(v.face.data.data(), face, sizeof(int32_t) * static_cast<size_t>(w) * h);
+    const auto m = edgeMask(v, diag, threshold);
+    std::memcpy(mask, m.data(), m.size());
+  });
+}
+
+// buildMips (mips.cpp:96-112): the chain concatenated level after level into
+// out; *n_levels = its length.
+int ref_build_mips(int w, int h, int c, const float* base, int levels, float sharpen, float* out, int* n_levels) {
+  return guarded([&] {
+    const auto chain = buildMips(toImage(w, h, c, base), levels, sharpen);
+    for (const ImageF& im : chain) {
+      std::memcpy(out, im.data.data(), im.data.size() * sizeof(float));
+      out += im.data.size();
+    }
+    *n_levels = static_cast<int>(chain.size());
+  });
+}
+
+// backprojectView (fuse.cpp:103-186) over a G-buffer (position + valid).
+int ref_backproject_view(int gres, const float* pos, const uint8_t* valid, const double* cam7, int view_res,
+                         int channels, int n_mips, const float* mips, const uint8_t* mask, float* color,
+                         uint8_t* sampled) {
+  return guarded([&] {
+    const GBuffer g = toGBuffer(gres, pos, nullptr, nullptr, nullptr, valid, nullptr);
+    const auto chain = toChain(view_res, view_res, channels, n_mips, mips);
+    std::vector<std::uint8_t> m(mask, mask + static_cast<size_t>(view_res) * view_res);
+    const PartialAtlas pa = backprojectView(g, toCamera(cam7, view_res), chain, m);
+    std::memcpy(color, pa.color.data.data(), pa.color.data.size() * sizeof(float));
+    std::memcpy(sampled, pa.sampled.data(), pa.sampled.size());
+  });
+}
+
+// incidenceMap (fuse.cpp:188-221).
+int ref_incidence_map(int gres, const float* pos, const float* nrm, const uint8_t* valid, const double* cam7,
+                      int view_res, const float* depth, double diag, double tol, float* out) {
+  return guarded([&] {
+    const GBuffer g = toGBuffer(gres, pos, nrm, nullptr, nullptr, valid, nullptr);
+    const ImageF r = incidenceMap(g, toCamera(cam7, view_res), toImage(view_res, view_res, 1, depth), diag, tol);
+    std::memcpy(out, r.data.data(), r.data.size() * sizeof(float));
+  });
+}
+
+// blendViews (fuse.cpp:223-280): k partial atlases (w x h x c colours + sampled
+// flags), k incidence maps, k priors.
+int ref_blend_views(int k, int w, int h, int c, const float* colors, const uint8_t* sampled, const float* inc,
+                    const double* priors, double alpha, double eps, float* out, uint8_t* filled) {
+  return guarded([&] {
+    const size_t n = static_cast<size_t>(w) * h;
+    std::vector<PartialAtlas> parts(k);
+    std::vector<ImageF> incs;
+    for (int i = 0; i < k; ++i) {
+      parts[i].color = toImage(w, h, c, colors + i * n * c);
+      parts[i].sampled.assign(sampled + i * n, sampled + (i + 1) * n);
+      incs.push_back(toImage(w, h, 1, inc + i * n));
+    }
+    BlendOptions opt;
+    opt.alpha = alpha;
+    opt.epsilon = eps;
+    const TextureAtlas a = blendViews(parts, incs, std::vector<double>(priors, priors + k), opt);
+    std::memcpy(out, a.color.data.data(), a.color.data.size() * sizeof(float));
+    std::memcpy(filled, a.filled.data(), a.filled.size());
+  });
+}
+
+void ref_standard_cameras(double half_extent, double* cams7) {
+  const auto cams = standardCameras(64, half_extent);
+  for (size_t i = 0; i < cams.size(); ++i) {
+    for (int k = 0; k < 3; ++k) {
+      cams7[7 * i + k] = cams[i].direction[k];
+      cams7[7 * i + 3 + k] = cams[i].up[k];
+    }
+    cams7[7 * i + 6] = cams[i].halfExtent;
+  }
 }
 
 }  // extern "C"

@@ -103,6 +103,17 @@ SIGNATURES = [
     ("mf_cast_visibility", _I, [_VP, _MV, _I, _I, _VP, _VP]),
     ("mf_closest_point_brute", _I, [_VP, _MV, _VP, _I64, _VP, _VP, _VP, _VP]),
     ("mf_raycast_first_brute", _I, [_VP, _MV, _VP, _VP, _I64, _D, _D, _VP, _VP, _VP, _VP]),
+    ("mf_fuse_options_default", None, [_VP]),
+    ("mf_mip_chain_floats", _I64, [_I, _I, _I, _I, _VP]),
+    ("mf_edge_mask", _I, [_VP, _I, _I, _VP, _VP, _D, _D, _VP]),
+    ("mf_build_mips", _I, [_VP, _I, _I, _I, _VP, _I, ctypes.c_float, _VP, _VP]),
+    ("mf_backproject_view", _I, [_VP, _I, _VP, _VP, _VP, _I, _I, _I, _VP, _VP, _VP, _VP]),
+    ("mf_incidence_map", _I, [_VP, _I, _VP, _VP, _VP, _VP, _I, _VP, _D, _D, _VP]),
+    ("mf_blend_views", _I, [_VP, _I, _I, _I, _I, _VP, _VP, _VP, _VP, _D, _D, _VP, _VP]),
+    ("mf_fuse_views", _I, [_VP, _I, _VP, _VP, _VP, _I, _VP, _I, _VP, _VP, _VP, _I, _VP, _VP, _D, _VP, _VP, _VP]),
+    ("mf_fuse_views_dev", _I, [_VP, _I, _VP, _VP, _VP, _I, _VP, _I, _VP, _VP, _VP, _I, _VP, _VP, _D, _VP, _VP,
+                               _VP]),
+    ("mf_raster_gbuffer_dev", _I, [_VP, _VP, _I, _VP, _VP, _VP, _VP, _VP, _VP]),
     ("mf_wedge_tangents", _I, [_VP, _MV, _VP]),
     ("mf_vertex_normals", _I, [_VP, _MV, _VP]),
 ]

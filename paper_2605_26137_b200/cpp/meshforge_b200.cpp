@@ -23,6 +23,8 @@
 #include "meshforge/signfield/sign_grid.h"
 #include "meshforge/visibility/visibility.h"
 #include "meshforge/spatial/bvh.h"
+#include "meshforge/texfuse/fuse.h"
+#include "meshforge/texfuse/mips.h"
 #include "mfbake.h"
 
 namespace meshforge {
@@ -541,6 +543,247 @@ TriangleMesh removeHidden(const TriangleMesh& mesh, const VisibilityMask& mask) 
 
 TriangleMesh cullHiddenFaces(const TriangleMesh& mesh, int viewpoints, int resolution, double cosThreshold) {
   return removeHidden(mesh, promoteExterior(mesh, castVisibility(mesh, viewpoints, resolution), cosThreshold));
+}
+
+}  // namespace meshforge
+
+// ------------------------------------------------------------------ texfuse
+// fuse.h / mips.h over the texfuse entry points of include/mfbake.h. Argument
+// checks are the reference's, in its order (fuse.cpp:66-326, mips.cpp:96-102);
+// the images go to the device in one call each.
+namespace meshforge {
+namespace {
+
+void camera7(const OrthoCamera& c, double* out) {
+  for (int k = 0; k < 3; ++k) {
+    out[k] = c.direction[k];
+    out[3 + k] = c.up[k];
+  }
+  out[6] = c.halfExtent;
+}
+
+void checkEdgeMask(const RenderedView& view, double bboxDiagonal, double threshold) {
+  const int w = view.position.width, h = view.position.height;
+  if (w < 1 || h < 1 || view.face.width != w || view.face.height != h)
+    throw Error(ErrorCode::InvalidConfig, "edge mask needs a rendered view");
+  if (!(bboxDiagonal > 0.0) || !(threshold > 0.0))
+    throw Error(ErrorCode::InvalidConfig, "edge mask scale must be positive");
+}
+void checkMips(const ImageF& base, int levels, float sharpen) {
+  if (base.width < 1 || base.height < 1 || base.channels < 1)
+    throw Error(ErrorCode::InvalidConfig, "mip base image is empty");
+  if (levels < 1) throw Error(ErrorCode::InvalidConfig, "mip chain needs >= 1 level");
+  if (!(sharpen >= 0.0f)) throw Error(ErrorCode::InvalidConfig, "sharpen strength must be >= 0");
+}
+void checkBackproject(const GBuffer& geom, int res, int w0, int h0, std::size_t maskSize) {
+  if (geom.empty()) throw Error(ErrorCode::InvalidConfig, "geometry image is empty");
+  if (w0 < 1) throw Error(ErrorCode::InvalidConfig, "view mip chain is empty");
+  if (w0 != res || h0 != res) throw Error(ErrorCode::ShapeMismatch, "view image does not match the camera");
+  if (maskSize != static_cast<std::size_t>(res) * res)
+    throw Error(ErrorCode::ShapeMismatch, "edge mask does not match the view");
+}
+void checkIncidence(const GBuffer& geom, const OrthoCamera& camera, const ImageF& depth, double diag, double tol) {
+  if (geom.empty()) throw Error(ErrorCode::InvalidConfig, "geometry image is empty");
+  if (!(diag > 0.0) || !(tol > 0.0)) throw Error(ErrorCode::InvalidConfig, "incidence scale must be positive");
+  const int res = camera.resolution;
+  if (depth.width != res || depth.height != res || depth.channels != 1)
+    throw Error(ErrorCode::ShapeMismatch, "depth buffer does not match the camera");
+}
+// buildMips' halving layout (the device chain format)
+bool standardChain(const std::vector<ImageF>& mips) {
+  for (std::size_t l = 1; l < mips.size(); ++l)
+    if (mips[l].width != std::max(1, (mips[l - 1].width + 1) / 2) ||
+        mips[l].height != std::max(1, (mips[l - 1].height + 1) / 2) || mips[l].channels != mips[0].channels ||
+        (mips[l - 1].width == 1 && mips[l - 1].height == 1))
+      return false;
+  return true;
+}
+
+}  // namespace
+
+TexelFootprint footprintFromJacobian(const Eigen::Matrix2d& jacobian) {
+  TexelFootprint fp;
+  fp.jacobian = jacobian;
+  const Eigen::Matrix2d m = jacobian * jacobian.transpose();
+  const double mean = 0.5 * (m(0, 0) + m(1, 1));
+  const double disc = std::hypot(0.5 * (m(0, 0) - m(1, 1)), m(0, 1));
+  const double s1 = std::sqrt(std::max(0.0, mean + disc));
+  const double s2 = std::sqrt(std::max(0.0, mean - disc));
+  constexpr double kTiny = 1e-12;
+  if (!(s1 > kTiny)) return fp;
+  Eigen::Vector2d axis(m(0, 1), mean + disc - m(0, 0));
+  const Eigen::Vector2d alt(mean + disc - m(1, 1), m(0, 1));
+  if (alt.squaredNorm() > axis.squaredNorm()) axis = alt;
+  fp.majorAxis = axis.squaredNorm() > 0.0 ? axis.normalized() : Eigen::Vector2d::UnitX();
+  fp.majorLength = s1;
+  fp.minorLength = s2;
+  const double ratio = s1 / std::max(s2, kTiny);
+  fp.taps = static_cast<int>(std::clamp(std::ceil(ratio), 1.0, 8.0));
+  fp.mip = std::max(0.0, std::log2(std::max(s2, kTiny)) - 0.5 + 0.5 * std::log2(std::min(ratio, 8.0)));
+  return fp;
+}
+
+std::vector<std::uint8_t> edgeMask(const RenderedView& view, double bboxDiagonal, double threshold) {
+  checkEdgeMask(view, bboxDiagonal, threshold);
+  const int w = view.position.width, h = view.position.height;
+  std::vector<std::uint8_t> mask(static_cast<std::size_t>(w) * h, 0);
+  check(mf_edge_mask(context(), w, h, view.position.data.data(), view.face.data.data(), bboxDiagonal, threshold,
+                     mask.data()));
+  return mask;
+}
+
+std::vector<ImageF> buildMips(const ImageF& base, int levels, float sharpenStrength) {
+  checkMips(base, levels, sharpenStrength);
+  int n = 0;
+  const int64_t total = mf_mip_chain_floats(base.width, base.height, base.channels, levels, &n);
+  std::vector<float> flat(static_cast<std::size_t>(total));
+  check(mf_build_mips(context(), base.width, base.height, base.channels, base.data.data(), levels, sharpenStrength,
+                      flat.data(), &n));
+  std::vector<ImageF> chain;
+  int w = base.width, h = base.height;
+  std::size_t o = 0;
+  for (int l = 0; l < n; ++l) {
+    ImageF im(w, h, base.channels);
+    std::copy(flat.begin() + o, flat.begin() + o + im.data.size(), im.data.begin());
+    o += im.data.size();
+    chain.push_back(std::move(im));
+    w = std::max(1, (w + 1) / 2);
+    h = std::max(1, (h + 1) / 2);
+  }
+  return chain;
+}
+
+PartialAtlas backprojectView(const GBuffer& geom, const OrthoCamera& camera, const std::vector<ImageF>& viewMips,
+                             const std::vector<std::uint8_t>& mask) {
+  if (geom.empty()) throw Error(ErrorCode::InvalidConfig, "geometry image is empty");
+  if (viewMips.empty() || viewMips[0].width < 1) throw Error(ErrorCode::InvalidConfig, "view mip chain is empty");
+  checkBackproject(geom, camera.resolution, viewMips[0].width, viewMips[0].height, mask.size());
+  if (!standardChain(viewMips))
+    throw Error(ErrorCode::InvalidConfig, "mip chain levels must follow buildMips' halving");
+  std::vector<float> flat;
+  for (const ImageF& im : viewMips) flat.insert(flat.end(), im.data.begin(), im.data.end());
+  const int n = geom.resolution, ch = viewMips[0].channels;
+  PartialAtlas out;
+  out.color = ImageF(n, n, ch, 0.0f);
+  out.sampled.assign(static_cast<std::size_t>(n) * n, 0);
+  double cam[7];
+  camera7(camera, cam);
+  check(mf_backproject_view(context(), n, f3(geom.position), geom.valid.data(), cam, camera.resolution, ch,
+                            static_cast<int>(viewMips.size()), flat.data(), mask.data(), out.color.data.data(),
+                            out.sampled.data()));
+  return out;
+}
+
+ImageF incidenceMap(const GBuffer& geom, const OrthoCamera& camera, const ImageF& depthBuffer, double bboxDiagonal,
+                    double depthTolerance) {
+  checkIncidence(geom, camera, depthBuffer, bboxDiagonal, depthTolerance);
+  const int n = geom.resolution;
+  ImageF out(n, n, 1, 0.0f);
+  double cam[7];
+  camera7(camera, cam);
+  check(mf_incidence_map(context(), n, f3(geom.position), f3(geom.normal), geom.valid.data(), cam, camera.resolution,
+                         depthBuffer.data.data(), bboxDiagonal, depthTolerance, out.data.data()));
+  return out;
+}
+
+TextureAtlas blendViews(const std::vector<PartialAtlas>& partials, const std::vector<ImageF>& incidence,
+                        const std::vector<double>& priors, const BlendOptions& options) {
+  const std::size_t k = partials.size();
+  if (k == 0) throw Error(ErrorCode::InvalidConfig, "no views to blend");
+  if (incidence.size() != k || priors.size() != k)
+    throw Error(ErrorCode::InvalidConfig, "views, incidence maps and priors must pair up");
+  if (!(options.epsilon > 0.0) || !(options.alpha >= 0.0))
+    throw Error(ErrorCode::InvalidConfig, "blend needs epsilon > 0 and alpha >= 0");
+  for (double p : priors)
+    if (!(p >= 0.0)) throw Error(ErrorCode::InvalidConfig, "priors must be >= 0");
+  const int w = partials[0].color.width, h = partials[0].color.height, ch = partials[0].color.channels;
+  const std::size_t n = static_cast<std::size_t>(w) * h;
+  std::vector<float> colors, inc;
+  std::vector<std::uint8_t> sampled;
+  colors.reserve(k * n * ch);
+  inc.reserve(k * n);
+  sampled.reserve(k * n);
+  for (std::size_t i = 0; i < k; ++i) {
+    const PartialAtlas& p = partials[i];
+    if (p.color.width != w || p.color.height != h || p.color.channels != ch || p.sampled.size() != n)
+      throw Error(ErrorCode::ShapeMismatch, "partial atlases disagree on resolution");
+    if (incidence[i].width != w || incidence[i].height != h || incidence[i].channels != 1)
+      throw Error(ErrorCode::ShapeMismatch, "incidence maps disagree on resolution");
+    colors.insert(colors.end(), p.color.data.begin(), p.color.data.end());
+    sampled.insert(sampled.end(), p.sampled.begin(), p.sampled.end());
+    inc.insert(inc.end(), incidence[i].data.begin(), incidence[i].data.end());
+  }
+  TextureAtlas atlas;
+  atlas.color = ImageF(w, h, ch, 0.0f);
+  atlas.filled.assign(n, 0);
+  check(mf_blend_views(context(), static_cast<int>(k), w, h, ch, colors.data(), sampled.data(), inc.data(),
+                       priors.data(), options.alpha, options.epsilon, atlas.color.data.data(), atlas.filled.data()));
+  return atlas;
+}
+
+std::vector<double> standardViewPriors() { return {1.0, 0.1, 0.01, 0.001, 1.0, 0.001, 0.01, 0.1, 0.3, 0.3}; }
+
+TextureAtlas inpaintAtlas(const TextureAtlas&, const GBuffer&, double, const InpaintOptions&) {
+  throw Error(ErrorCode::InvalidConfig, "inpaintAtlas is declared but never defined by the reference (fuse.h:110)");
+}
+
+TextureAtlas fuseViews(const GBuffer& geom, const std::vector<OrthoCamera>& cameras,
+                       const std::vector<RenderedView>& views, const std::vector<ImageF>& colors,
+                       const std::vector<double>& priors, double bboxDiagonal, const FuseOptions& options) {
+  const std::size_t k = cameras.size();
+  if (k == 0 || views.size() != k || colors.size() != k || priors.size() != k)
+    throw Error(ErrorCode::InvalidConfig, "cameras, views, colors and priors must pair up");
+  // the reference's per-view checks, in its order (fuse.cpp:305-312)
+  for (std::size_t i = 0; i < k; ++i) {
+    checkEdgeMask(views[i], bboxDiagonal, options.edgeThreshold);
+    checkMips(colors[i], options.mipLevels, options.sharpenStrength);
+    const std::size_t maskSize = static_cast<std::size_t>(views[i].position.width) * views[i].position.height;
+    checkBackproject(geom, cameras[i].resolution, colors[i].width, colors[i].height, maskSize);
+    checkIncidence(geom, cameras[i], views[i].depth, bboxDiagonal, options.depthTolerance);
+  }
+  if (!(options.blend.epsilon > 0.0) || !(options.blend.alpha >= 0.0))
+    throw Error(ErrorCode::InvalidConfig, "blend needs epsilon > 0 and alpha >= 0");
+  for (double p : priors)
+    if (!(p >= 0.0)) throw Error(ErrorCode::InvalidConfig, "priors must be >= 0");
+  const int vres = cameras[0].resolution, ch = colors[0].channels;
+  for (std::size_t i = 1; i < k; ++i)
+    if (cameras[i].resolution != vres || colors[i].channels != ch)
+      throw Error(ErrorCode::InvalidConfig, "fused views must share one resolution and channel count");
+  const std::size_t vn = static_cast<std::size_t>(vres) * vres;
+  std::vector<double> cams(7 * k);
+  std::vector<float> vpos, vdepth, cols;
+  std::vector<std::int32_t> vface;
+  vpos.reserve(3 * vn * k);
+  vdepth.reserve(vn * k);
+  vface.reserve(vn * k);
+  cols.reserve(vn * k * ch);
+  for (std::size_t i = 0; i < k; ++i) {
+    camera7(cameras[i], cams.data() + 7 * i);
+    vpos.insert(vpos.end(), views[i].position.data.begin(), views[i].position.data.end());
+    vdepth.insert(vdepth.end(), views[i].depth.data.begin(), views[i].depth.data.end());
+    vface.insert(vface.end(), views[i].face.data.begin(), views[i].face.data.end());
+    cols.insert(cols.end(), colors[i].data.begin(), colors[i].data.end());
+  }
+  mf_fuse_options o;
+  mf_fuse_options_default(&o);
+  o.edge_threshold = options.edgeThreshold;
+  o.depth_tolerance = options.depthTolerance;
+  o.mip_levels = options.mipLevels;
+  o.sharpen_strength = options.sharpenStrength;
+  o.alpha = options.blend.alpha;
+  o.epsilon = options.blend.epsilon;
+  const int n = geom.resolution;
+  TextureAtlas atlas;
+  atlas.color = ImageF(n, n, ch, 0.0f);
+  atlas.filled.assign(static_cast<std::size_t>(n) * n, 0);
+  check(mf_fuse_views(context(), n, f3(geom.position), f3(geom.normal), geom.valid.data(), static_cast<int>(k),
+                      cams.data(), vres, vpos.data(), vface.data(), vdepth.data(), ch, cols.data(), priors.data(),
+                      bboxDiagonal, &o, atlas.color.data.data(), atlas.filled.data()));
+  if (options.runInpaint) {
+    for (std::size_t t = 0; t < atlas.filled.size(); ++t)
+      if (geom.valid[t] && !atlas.filled[t]) return inpaintAtlas(atlas, geom, bboxDiagonal, options.inpaint);
+  }
+  return atlas;
 }
 
 }  // namespace meshforge

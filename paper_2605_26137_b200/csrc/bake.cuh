@@ -404,4 +404,30 @@ void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
                   const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
                   int radius, uint8_t* map_out, int out_row0, int out_rows);
 
+// ---------------------------------------------------------------- texfuse
+// Device-resident consumers of the G-buffer: proj/src/texfuse/fuse.cpp and
+// mips.cpp (texfuse.cu). Images are row-major interleaved f32 (ImageF).
+constexpr int kTfMaxMips = 24;
+struct TfCamera {  // OrthoCamera (render/camera.h:12-38) with right() precomputed
+  double dir[3], up[3], right[3], he;
+  int res;
+};
+TfCamera tf_camera(const double* cam7, int res);
+// buildMips' level sizes (mips.cpp:104-110): returns the chain length;
+// lw/lh/off need kTfMaxMips + 1 entries; off[n] = total floats.
+int tf_mip_layout(int w, int h, int c, int levels, int* lw, int* lh, int64_t* off);
+void tf_edge_mask(Ctx& ctx, cudaStream_t s, int w, int h, const float* pos, const int32_t* face, double limit2,
+                  uint8_t* mask);
+int tf_build_mips(Ctx& ctx, cudaStream_t s, int w, int h, int c, const float* base, int levels, float sharpen,
+                  float* chain, const std::string& tag);
+void tf_valid_bounds(Ctx& ctx, cudaStream_t s, int64_t n, const float* pos, const uint8_t* valid, unsigned* b6);
+void tf_backproject(Ctx& ctx, cudaStream_t s, int gres, const float* pos, const uint8_t* valid, const unsigned* b6,
+                    const TfCamera& cam, int channels, int n_mips, const float* chain, const uint8_t* mask,
+                    float* color, uint8_t* sampled);
+void tf_incidence(Ctx& ctx, cudaStream_t s, int gres, const float* pos, const float* nrm, const uint8_t* valid,
+                  const TfCamera& cam, const float* depth, double tolerance, float* out);
+void tf_blend(Ctx& ctx, cudaStream_t s, int k, int64_t n, int c, const float* colors, const uint8_t* sampled,
+              const float* inc, const double* priors_host, double alpha, double epsilon, float* out,
+              uint8_t* filled);
+
 }  // namespace mfb

@@ -1476,6 +1476,32 @@ void mf_mesh_destroy(mf_mesh* mesh) {
   delete mesh;
 }
 
+// rasterizeGBuffer into the slab buffers of g (full atlas); retries once
+// with the exact tile-bin capacity when the bins overflowed.
+static void raster_full(Ctx& c, const mf_mesh& lo, GBufDev& g) {
+  int* flags = c.buf<int>("bake.flags", 4);
+  for (int attempt = 0;; ++attempt) {
+    MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), c.stream));
+    RasterPlan plan;
+    PrepBinning pb;
+    pb.row0 = g.row0;
+    pb.rows = g.rows;
+    pb.flags = flags;
+    prepare_lowpoly(c, c.stream, lo.m, g.res, plan, &pb);
+    raster_gbuffer(c, c.stream, lo.m, plan, g, flags, nullptr);
+    int hf[4] = {0, 0, 0, 0};
+    MFB_CUDA_TRY(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, c.stream));
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (hf[1] && attempt == 0) {
+      c.bin_capacity = static_cast<int64_t>(hf[2]) + 1;
+      continue;
+    }
+    if (hf[1]) throw ApiError(MF_ERR_CUDA, "internal capacity overflow");
+    if (hf[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
+    break;
+  }
+}
+
 int mf_raster_gbuffer(mf_ctx* ctx, const mf_mesh_view* lowpoly, int res, float* position, float* normal,
                       float* tangent, float* bitangent, uint8_t* valid, uint8_t* reliable) {
   if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
@@ -1488,27 +1514,7 @@ int mf_raster_gbuffer(mf_ctx* ctx, const mf_mesh_view* lowpoly, int res, float* 
     if (!position || !normal || !tangent || !bitangent || !valid || !reliable)
       throw ApiError(MF_ERR_BAD_ARGUMENT, "null G-buffer output");
     GBufDev g = gbuf_slab(c, res, 0, res);
-    int* flags = c.buf<int>("bake.flags", 4);
-    for (int attempt = 0;; ++attempt) {
-      MFB_CUDA_TRY(cudaMemsetAsync(flags, 0, 4 * sizeof(int), c.stream));
-      RasterPlan plan;
-      PrepBinning pb;
-      pb.row0 = g.row0;
-      pb.rows = g.rows;
-      pb.flags = flags;
-      prepare_lowpoly(c, c.stream, lo.m, res, plan, &pb);
-      raster_gbuffer(c, c.stream, lo.m, plan, g, flags, nullptr);
-      int hf[4] = {0, 0, 0, 0};
-      MFB_CUDA_TRY(cudaMemcpyAsync(hf, flags, sizeof(hf), cudaMemcpyDeviceToHost, c.stream));
-      MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
-      if (hf[1] && attempt == 0) {
-        c.bin_capacity = static_cast<int64_t>(hf[2]) + 1;
-        continue;
-      }
-      if (hf[1]) throw ApiError(MF_ERR_CUDA, "internal capacity overflow");
-      if (hf[0]) throw ApiError(MF_ERR_ATLAS_OVERLAP, "AtlasOverlap: texel claimed by two UV triangles");
-      break;
-    }
+    raster_full(c, lo, g);
     const int64_t n = g.texels();
     MFB_CUDA_TRY(cudaMemcpyAsync(position, g.pos, 12 * n, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaMemcpyAsync(normal, g.nrm, 12 * n, cudaMemcpyDeviceToHost, c.stream));
@@ -1517,6 +1523,29 @@ int mf_raster_gbuffer(mf_ctx* ctx, const mf_mesh_view* lowpoly, int res, float* 
     MFB_CUDA_TRY(cudaMemcpyAsync(valid, g.valid, n, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaMemcpyAsync(reliable, g.rel, n, cudaMemcpyDeviceToHost, c.stream));
     MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_raster_gbuffer_dev(mf_ctx* ctx, mf_mesh* lowpoly, int res, float* position, float* normal, float* tangent,
+                          float* bitangent, uint8_t* valid, uint8_t* reliable) {
+  if (!ctx || !lowpoly) return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    check_lowpoly(lowpoly, res);
+    if (!position || !normal || !tangent || !bitangent || !valid || !reliable)
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "null G-buffer output");
+    GBufDev g;
+    g.res = res;
+    g.row0 = 0;
+    g.rows = res;
+    g.pos = position;
+    g.nrm = normal;
+    g.tan = tangent;
+    g.bit = bitangent;
+    g.valid = valid;
+    g.rel = reliable;
+    raster_full(c, *lowpoly, g);
     return MF_OK;
   });
 }
@@ -2308,3 +2337,278 @@ int mf_bake_normal_map_dev_publish(mf_ctx* ctx, mf_mesh* lowpoly, mf_mesh* highp
   });
 }
 }  // extern "C"
+
+// ---------------------------------------------------------------- texfuse
+// The G-buffer consumers of proj/src/texfuse (texfuse.cu). Host entry points
+// copy their inputs into context scratch, run the device kernels and copy the
+// results back; mf_fuse_views_dev keeps everything in HBM.
+namespace {
+
+template <typename T>
+T* up(Ctx& c, const std::string& name, const T* host, size_t count) {
+  T* d = c.buf<T>(name, count);
+  if (count) MFB_CUDA_TRY(cudaMemcpyAsync(d, host, sizeof(T) * count, cudaMemcpyHostToDevice, c.stream));
+  return d;
+}
+template <typename T>
+void down(Ctx& c, T* host, const T* dev, size_t count) {
+  if (count) MFB_CUDA_TRY(cudaMemcpyAsync(host, dev, sizeof(T) * count, cudaMemcpyDeviceToHost, c.stream));
+}
+
+// edgeMask's argument checks (fuse.cpp:68-71)
+void check_edge_args(int w, int h, double diag, double threshold) {
+  if (w < 1 || h < 1) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: edge mask needs a rendered view");
+  if (!(diag > 0.0) || !(threshold > 0.0))
+    throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: edge mask scale must be positive");
+}
+// buildMips (mips.cpp:98-102)
+void check_mip_args(int w, int h, int c, int levels, float sharpen) {
+  if (w < 1 || h < 1 || c < 1) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: mip base image is empty");
+  if (levels < 1) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: mip chain needs >= 1 level");
+  if (!(sharpen >= 0.0f)) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: sharpen strength must be >= 0");
+}
+// backprojectView (fuse.cpp:106-113): the chain's level 0 is view_res^2 by construction here
+void check_backproject_args(int gres, const uint8_t* valid, int view_res, int channels, int n_mips) {
+  if (gres < 1 || !valid) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: geometry image is empty");
+  if (n_mips < 1 || channels < 1 || view_res < 1)
+    throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: view mip chain is empty");
+}
+// incidenceMap (fuse.cpp:191-196)
+void check_incidence_args(int gres, const uint8_t* valid, double diag, double tol, int view_res) {
+  if (gres < 1 || !valid) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: geometry image is empty");
+  if (!(diag > 0.0) || !(tol > 0.0))
+    throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: incidence scale must be positive");
+  if (view_res < 1) throw ApiError(MF_ERR_SHAPE_MISMATCH, "ShapeMismatch: depth buffer does not match the camera");
+}
+// blendViews (fuse.cpp:226-233)
+void check_blend_args(int k, const double* priors, double alpha, double eps) {
+  if (k <= 0) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: no views to blend");
+  if (!priors) throw ApiError(MF_ERR_BAD_ARGUMENT, "priors is null");
+  if (!(eps > 0.0) || !(alpha >= 0.0))
+    throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: blend needs epsilon > 0 and alpha >= 0");
+  for (int i = 0; i < k; ++i)
+    if (!(priors[i] >= 0.0)) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: priors must be >= 0");
+}
+
+int64_t mip_floats(int w, int h, int c, int levels, int* n_levels) {
+  int lw[kTfMaxMips + 1], lh[kTfMaxMips + 1];
+  int64_t off[kTfMaxMips + 1];
+  const int n = tf_mip_layout(w, h, c, levels, lw, lh, off);
+  if (n_levels) *n_levels = n;
+  return off[n];
+}
+
+// fuseViews (fuse.cpp:292-326) without the inpainting step, every buffer
+// device-resident: per view the edge mask, the mip chain, the backprojected
+// partial atlas and the incidence map, then the blend. Partial atlases and
+// incidence maps stay in context scratch (k x gres^2 x (channels + 1) f32).
+void fuse_dev(Ctx& c, int gres, const float* pos, const float* nrm, const uint8_t* valid, int k,
+              const double* cams, int vres, const float* vpos, const int32_t* vface, const float* vdepth, int ch,
+              const float* colors, const double* priors, double diag, const mf_fuse_options& o, float* color,
+              uint8_t* filled) {
+  if (k <= 0 || !cams || !priors) throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: cameras, views, colors and priors must pair up");
+  check_edge_args(vres, vres, diag, o.edge_threshold);
+  check_mip_args(vres, vres, ch, o.mip_levels, o.sharpen_strength);
+  int n_mips = 0;
+  const int64_t chain_floats = mip_floats(vres, vres, ch, o.mip_levels, &n_mips);
+  check_backproject_args(gres, valid, vres, ch, n_mips);
+  check_incidence_args(gres, valid, diag, o.depth_tolerance, vres);
+  check_blend_args(k, priors, o.alpha, o.epsilon);
+  cudaStream_t s = c.stream;
+  const int64_t n = static_cast<int64_t>(gres) * gres, vn = static_cast<int64_t>(vres) * vres;
+  auto* b6 = c.buf<unsigned>("tf.bounds", 6);
+  tf_valid_bounds(c, s, n, pos, valid, b6);
+  float* part = c.buf<float>("tf.part", static_cast<size_t>(k) * n * ch);
+  uint8_t* samp = c.buf<uint8_t>("tf.samp", static_cast<size_t>(k) * n);
+  float* inc = c.buf<float>("tf.inc", static_cast<size_t>(k) * n);
+  uint8_t* mask = c.buf<uint8_t>("tf.mask", vn);
+  float* chain = c.buf<float>("tf.chain", chain_floats);
+  double limit2 = o.edge_threshold * diag;
+  limit2 *= limit2;
+  for (int i = 0; i < k; ++i) {
+    const TfCamera cam = tf_camera(cams + 7 * i, vres);
+    tf_edge_mask(c, s, vres, vres, vpos + 3 * vn * i, vface + vn * i, limit2, mask);
+    tf_build_mips(c, s, vres, vres, ch, colors + vn * ch * i, o.mip_levels, o.sharpen_strength, chain, "tf.mips");
+    tf_backproject(c, s, gres, pos, valid, b6, cam, ch, n_mips, chain, mask, part + n * ch * i, samp + n * i);
+    tf_incidence(c, s, gres, pos, nrm, valid, cam, vdepth + vn * i, o.depth_tolerance * diag, inc + n * i);
+  }
+  tf_blend(c, s, k, n, ch, part, samp, inc, priors, o.alpha, o.epsilon, color, filled);
+}
+
+}  // namespace
+
+void mf_fuse_options_default(mf_fuse_options* o) {
+  if (!o) return;
+  o->edge_threshold = 0.02;  // FuseOptions (fuse.h:122-130)
+  o->depth_tolerance = 0.005;
+  o->mip_levels = 6;
+  o->sharpen_strength = 0.2f;
+  o->alpha = 4.0;  // BlendOptions (fuse.h:83-86)
+  o->epsilon = 1e-8;
+}
+
+int64_t mf_mip_chain_floats(int width, int height, int channels, int levels, int* n_levels) {
+  if (width < 1 || height < 1 || channels < 1 || levels < 1) {
+    if (n_levels) *n_levels = 0;
+    return 0;
+  }
+  return mip_floats(width, height, channels, levels, n_levels);
+}
+
+int mf_edge_mask(mf_ctx* ctx, int width, int height, const float* position, const int32_t* face,
+                 double bbox_diagonal, double threshold, uint8_t* mask) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    check_edge_args(width, height, bbox_diagonal, threshold);
+    if (!position || !face || !mask) throw ApiError(MF_ERR_BAD_ARGUMENT, "null argument");
+    const size_t n = static_cast<size_t>(width) * height;
+    double limit2 = threshold * bbox_diagonal;
+    limit2 *= limit2;
+    uint8_t* dm = c.buf<uint8_t>("tf.mask", n);
+    tf_edge_mask(c, c.stream, width, height, up(c, "tf.vpos", position, 3 * n), up(c, "tf.vface", face, n), limit2,
+                 dm);
+    down(c, mask, dm, n);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_build_mips(mf_ctx* ctx, int width, int height, int channels, const float* base, int levels, float sharpen,
+                  float* chain, int* n_levels) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    check_mip_args(width, height, channels, levels, sharpen);
+    if (!base || !chain) throw ApiError(MF_ERR_BAD_ARGUMENT, "null argument");
+    int n = 0;
+    const int64_t total = mip_floats(width, height, channels, levels, &n);
+    float* d = c.buf<float>("tf.chain", total);
+    MFB_CUDA_TRY(cudaMemcpyAsync(d, base, sizeof(float) * width * static_cast<size_t>(height) * channels,
+                                 cudaMemcpyHostToDevice, c.stream));
+    tf_build_mips(c, c.stream, width, height, channels, d, levels, sharpen, d, "tf.mips");
+    down(c, chain, d, total);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (n_levels) *n_levels = n;
+    return MF_OK;
+  });
+}
+
+int mf_backproject_view(mf_ctx* ctx, int gres, const float* position, const uint8_t* valid, const double* camera,
+                        int view_res, int channels, int n_mips, const float* mips, const uint8_t* mask, float* color,
+                        uint8_t* sampled) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    check_backproject_args(gres, valid, view_res, channels, n_mips);
+    if (!position || !camera || !mips || !mask || !color || !sampled)
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "null argument");
+    int expect = 0;
+    const int64_t chain_floats = mip_floats(view_res, view_res, channels, n_mips, &expect);
+    if (expect != n_mips) throw ApiError(MF_ERR_SHAPE_MISMATCH, "ShapeMismatch: mip chain does not match the view");
+    const size_t n = static_cast<size_t>(gres) * gres, vn = static_cast<size_t>(view_res) * view_res;
+    const float* dpos = up(c, "tf.gpos", position, 3 * n);
+    const uint8_t* dval = up(c, "tf.gval", valid, n);
+    auto* b6 = c.buf<unsigned>("tf.bounds", 6);
+    tf_valid_bounds(c, c.stream, n, dpos, dval, b6);
+    float* dcol = c.buf<float>("tf.part", n * channels);
+    uint8_t* dsam = c.buf<uint8_t>("tf.samp", n);
+    tf_backproject(c, c.stream, gres, dpos, dval, b6, tf_camera(camera, view_res), channels, n_mips,
+                   up(c, "tf.chain", mips, chain_floats), up(c, "tf.mask", mask, vn), dcol, dsam);
+    down(c, color, dcol, n * channels);
+    down(c, sampled, dsam, n);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_incidence_map(mf_ctx* ctx, int gres, const float* position, const float* normal, const uint8_t* valid,
+                     const double* camera, int view_res, const float* depth, double bbox_diagonal,
+                     double depth_tolerance, float* out) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    check_incidence_args(gres, valid, bbox_diagonal, depth_tolerance, view_res);
+    if (!position || !normal || !camera || !depth || !out) throw ApiError(MF_ERR_BAD_ARGUMENT, "null argument");
+    const size_t n = static_cast<size_t>(gres) * gres, vn = static_cast<size_t>(view_res) * view_res;
+    float* dout = c.buf<float>("tf.inc", n);
+    tf_incidence(c, c.stream, gres, up(c, "tf.gpos", position, 3 * n), up(c, "tf.gnrm", normal, 3 * n),
+                 up(c, "tf.gval", valid, n), tf_camera(camera, view_res), up(c, "tf.depth", depth, vn),
+                 depth_tolerance * bbox_diagonal, dout);
+    down(c, out, dout, n);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_blend_views(mf_ctx* ctx, int n_views, int width, int height, int channels, const float* colors,
+                   const uint8_t* sampled, const float* incidence, const double* priors, double alpha, double epsilon,
+                   float* color, uint8_t* filled) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    check_blend_args(n_views, priors, alpha, epsilon);
+    if (width < 0 || height < 0 || channels < 0) throw ApiError(MF_ERR_SHAPE_MISMATCH, "ShapeMismatch: bad atlas shape");
+    if (!colors || !sampled || !incidence || !color || !filled) throw ApiError(MF_ERR_BAD_ARGUMENT, "null argument");
+    const size_t n = static_cast<size_t>(width) * height, k = static_cast<size_t>(n_views);
+    float* dout = c.buf<float>("tf.out", n * channels);
+    uint8_t* dfill = c.buf<uint8_t>("tf.fill", n);
+    tf_blend(c, c.stream, n_views, static_cast<int64_t>(n), channels, up(c, "tf.part", colors, k * n * channels),
+             up(c, "tf.samp", sampled, k * n), up(c, "tf.inc", incidence, k * n), priors, alpha, epsilon, dout,
+             dfill);
+    down(c, color, dout, n * channels);
+    down(c, filled, dfill, n);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}
+
+int mf_fuse_views_dev(mf_ctx* ctx, int gres, const float* position, const float* normal, const uint8_t* valid,
+                      int n_views, const double* cameras, int view_res, const float* view_position,
+                      const int32_t* view_face, const float* view_depth, int channels, const float* colors,
+                      const double* priors, double bbox_diagonal, const mf_fuse_options* options, float* color,
+                      uint8_t* filled) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    mf_fuse_options o;
+    mf_fuse_options_default(&o);
+    if (options) o = *options;
+    if (!position || !normal || !view_position || !view_face || !view_depth || !colors || !color || !filled)
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "null argument");
+    fuse_dev(ctx->c, gres, position, normal, valid, n_views, cameras, view_res, view_position, view_face, view_depth,
+             channels, colors, priors, bbox_diagonal, o, color, filled);
+    return MF_OK;
+  });
+}
+
+int mf_fuse_views(mf_ctx* ctx, int gres, const float* position, const float* normal, const uint8_t* valid,
+                  int n_views, const double* cameras, int view_res, const float* view_position,
+                  const int32_t* view_face, const float* view_depth, int channels, const float* colors,
+                  const double* priors, double bbox_diagonal, const mf_fuse_options* options, float* color,
+                  uint8_t* filled) {
+  if (!ctx) return fail(MF_ERR_BAD_ARGUMENT, "ctx is null");
+  return guarded(ctx, [&]() -> int {
+    Ctx& c = ctx->c;
+    mf_fuse_options o;
+    mf_fuse_options_default(&o);
+    if (options) o = *options;
+    if (n_views <= 0 || gres < 1 || !valid || view_res < 1 || channels < 1) {  // argument errors first
+      fuse_dev(c, gres, nullptr, nullptr, valid, n_views, cameras, view_res, nullptr, nullptr, nullptr, channels,
+               nullptr, priors, bbox_diagonal, o, nullptr, nullptr);
+    }
+    if (!position || !normal || !view_position || !view_face || !view_depth || !colors || !color || !filled)
+      throw ApiError(MF_ERR_BAD_ARGUMENT, "null argument");
+    const size_t n = static_cast<size_t>(gres) * gres, vn = static_cast<size_t>(view_res) * view_res,
+                 k = static_cast<size_t>(n_views);
+    float* dout = c.buf<float>("tf.out", n * channels);
+    uint8_t* dfill = c.buf<uint8_t>("tf.fill", n);
+    fuse_dev(c, gres, up(c, "tf.gpos", position, 3 * n), up(c, "tf.gnrm", normal, 3 * n), up(c, "tf.gval", valid, n),
+             n_views, cameras, view_res, up(c, "tf.vpos", view_position, 3 * vn * k), up(c, "tf.vface", view_face, vn * k),
+             up(c, "tf.vdepth", view_depth, vn * k), channels, up(c, "tf.colors", colors, vn * k * channels), priors,
+             bbox_diagonal, o, dout, dfill);
+    down(c, color, dout, n * channels);
+    down(c, filled, dfill, n);
+    MFB_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return MF_OK;
+  });
+}

@@ -150,8 +150,44 @@ def views_case(ref):
     return out
 
 
+def texfuse_case(ref):
+    """texfuse over a small G-buffer (fuse.cpp:66-280, mips.cpp:96-112): three
+    standard views of a dense blob, synthetic colours; the reference's edge
+    masks, mip chains, partial atlases, incidence maps and blend."""
+    p = fx.bake_pair(24, 4, 64, name="texfuse")
+    g = ref.raster_gbuffer(p.lowpoly, 64)
+    cams = ref.standard_cameras(0.8)[[0, 4, 8]]
+    vres = 96
+    face, depth, pos, _ = ref.render_views(p.dense, cams, vres)
+    col = (0.5 + 0.5 * np.sin(np.concatenate([5.0 * pos[..., :1], 3.0 * pos[..., 1:2] + 1.0,
+                                              7.0 * pos[..., 2:3]], -1))) * (face >= 0)[..., None]
+    col = col.astype(np.float32)
+    diag = p.bbox_diagonal
+    masks, chains, parts, samps, incs = [], [], [], [], []
+    for i in range(3):
+        m = ref.edge_mask(pos[i], face[i], diag, 0.02)
+        chain, nm = ref.build_mips(col[i], 6, 0.2)
+        c, sp = ref.backproject_view(g.position, g.valid, 64, cams[i], vres, 3, nm, chain, m)
+        inc = ref.incidence_map(g.position, g.normal, g.valid, 64, cams[i], vres, depth[i], diag, 0.005)
+        masks.append(m)
+        chains.append(chain)
+        parts.append(c)
+        samps.append(sp)
+        incs.append(inc)
+    priors = np.array([1.0, 1.0, 0.3])
+    out, filled = ref.blend_views(np.stack(parts), np.stack(samps), np.stack(incs), priors)
+    return dict(g_position=g.position, g_normal=g.normal, g_valid=g.valid, cams=cams, vres=vres, diag=diag,
+                v_face=face, v_depth=depth, v_pos=pos, colors=col, masks=np.stack(masks), chains=np.stack(chains),
+                parts=np.stack(parts), sampled=np.stack(samps), incidence=np.stack(incs), priors=priors,
+                blend=out, filled=filled)
+
+
 def main():
     ref = bindings.ref()
+    if sys.argv[1:] == ["texfuse"]:  # regenerate only this file
+        np.savez_compressed(os.path.join(HERE, "texfuse.npz"), **texfuse_case(ref))
+        return
+    np.savez_compressed(os.path.join(HERE, "texfuse.npz"), **texfuse_case(ref))
     np.savez_compressed(os.path.join(HERE, "views.npz"), **views_case(ref))
     np.savez_compressed(os.path.join(HERE, "band.npz"), **band_case(ref))
     np.savez_compressed(os.path.join(HERE, "kats.npz"), **kat_case(ref))

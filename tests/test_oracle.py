@@ -237,3 +237,24 @@ def test_port_matches_reference_golden_views(port, case):
         assert np.array_equal(cf, d["blob_cull_face"])
         assert np.array_equal(f32bits(cd), f32bits(d["blob_cull_depth"]))
     assert np.array_equal(port.cast_visibility(m, 32, 96), d[f"{case}_hits"])
+
+
+def test_reference_texfuse_reproduces_golden(ref):
+    """The texfuse golden (tests/golden/texfuse.npz, make_golden.py) is
+    reproducible from the reference build: fuse.cpp / mips.cpp are
+    deterministic given the committed inputs."""
+    d = np.load(os.path.join(GOLDEN, "texfuse.npz"))
+    vres, diag = int(d["vres"]), float(d["diag"])
+    for i in range(d["cams"].shape[0]):
+        m = ref.edge_mask(d["v_pos"][i], d["v_face"][i], diag, 0.02)
+        assert np.array_equal(m, d["masks"][i])
+        chain, nm = ref.build_mips(d["colors"][i], 6, 0.2)
+        assert np.array_equal(chain, d["chains"][i])
+        c, s = ref.backproject_view(d["g_position"], d["g_valid"], 64, d["cams"][i], vres, 3, nm, chain, m)
+        assert np.array_equal(c, d["parts"][i]) and np.array_equal(s, d["sampled"][i])
+        inc = ref.incidence_map(d["g_position"], d["g_normal"], d["g_valid"], 64, d["cams"][i], vres, d["v_depth"][i],
+                                diag, 0.005)
+        assert np.array_equal(inc, d["incidence"][i])
+    out, filled = ref.blend_views(d["parts"], d["sampled"], d["incidence"], d["priors"])
+    assert np.array_equal(out, d["blend"]) and np.array_equal(filled, d["filled"])
+    assert int(filled.sum()) > 0
