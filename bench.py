@@ -394,6 +394,88 @@ def bvh_rays(ctx, hi, pair, steps):
                       "closest-point radius = maxDistFrac x diag"}
 
 
+def texfuse_bench(ctx, lo, pair, steps):
+    """fuseViews up to the blend (fuse.cpp:292-318) on the
+    device over the config-B lowpoly's 2048^2 G-buffer (mf_raster_gbuffer_dev,
+    resident in HBM) and the 10 standard views at 1024^2 of the dense mesh
+    (mf_render_views), 3-channel synthetic colours: one mf_fuse_views_dev call
+    = per view edge mask + 6-level mip chain + backprojection + incidence, then
+    the blend. The reference's own fuse.cpp runs one of the views on the host
+    cores beside it (its backprojectView / incidenceMap are single-threaded)."""
+    import ctypes
+
+    import torch
+
+    from paper_2605_26137_b200 import capi
+    from paper_2605_26137_b200 import texfuse as tf
+    lib = ctx.lib
+    res, vres, k = pair.res, 1024, 10
+    n = res * res
+    gp, gn, gt, gb = (torch.empty((n, 3), dtype=torch.float32, device="cuda") for _ in range(4))
+    gv, gr = (torch.empty(n, dtype=torch.uint8, device="cuda") for _ in range(2))
+    capi.check(lib.mf_raster_gbuffer_dev(ctx.h, lo.h, res, gp.data_ptr(), gn.data_ptr(), gt.data_ptr(),
+                                         gb.data_ptr(), gv.data_ptr(), gr.data_ptr()))
+    cams = tf.standard_cameras(0.8)
+    face = np.zeros((k, vres, vres), np.int32)
+    depth = np.zeros((k, vres, vres), np.float32)
+    pos = np.zeros((k, vres, vres, 3), np.float32)
+    mv = pair.dense.view()
+    capi.check(lib.mf_render_views(ctx.h, ctypes.byref(mv), cams.ctypes.data_as(ctypes.c_void_p), k, vres, None, 0,
+                                   face.ctypes.data_as(ctypes.c_void_p), depth.ctypes.data_as(ctypes.c_void_p),
+                                   pos.ctypes.data_as(ctypes.c_void_p), None))
+    fg = (face >= 0)[..., None]
+    col = ((0.5 + 0.5 * np.sin(np.concatenate([7.0 * pos[..., :1], 5.0 * pos[..., 1:2] + 1.0,
+                                                3.0 * pos[..., 2:3]], -1))) * fg).astype(np.float32)
+    dface, ddepth, dpos, dcol = (torch.from_numpy(a).cuda() for a in (face, depth, pos, col))
+    out = torch.empty((n, 3), dtype=torch.float32, device="cuda")
+    filled = torch.empty(n, dtype=torch.uint8, device="cuda")
+    priors = np.array(tf.standard_view_priors())
+    diag = pair.bbox_diagonal
+
+    def call():
+        capi.check(lib.mf_fuse_views_dev(ctx.h, res, gp.data_ptr(), gn.data_ptr(), gv.data_ptr(), k,
+                                          cams.ctypes.data_as(ctypes.c_void_p), vres, dpos.data_ptr(),
+                                          dface.data_ptr(), ddepth.data_ptr(), 3, dcol.data_ptr(),
+                                          priors.ctypes.data_as(ctypes.c_void_p), diag, None, out.data_ptr(),
+                                          filled.data_ptr()))
+    call()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ts = []
+    for _ in range(max(3, min(steps, 10))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        call()
+        b.record(stream)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    ms = statistics.median(ts)
+    n_valid = int(gv.sum())
+    n_filled = int(filled.sum())
+    line = {"ms": round(ms, 3), "views": k, "view_res": vres, "atlas_res": res, "valid_texels": n_valid,
+            "filled_texels": n_filled, "texel_views_per_s": n_valid * k / (ms * 1e-3),
+            "call": "mf_fuse_views_dev: every image resident in HBM (G-buffer from mf_raster_gbuffer_dev)"}
+    # the reference's fuse.cpp on the host cores: edgeMask + buildMips +
+    # backprojectView + incidenceMap of view 0 (single-threaded as shipped)
+    try:
+        from oracle import bindings
+        if bindings.ref_available():
+            r = bindings.ref()
+            gpos, gnrm, gval = gp.cpu().numpy(), gn.cpu().numpy(), gv.cpu().numpy()
+            t0 = time.perf_counter()
+            m = r.edge_mask(pos[0], face[0], diag, 0.02)
+            chain, nm = r.build_mips(col[0], 6, 0.2)
+            r.backproject_view(gpos, gval, res, cams[0], vres, 3, nm, chain, m)
+            r.incidence_map(gpos, gnrm, gval, res, cams[0], vres, depth[0], diag, 0.005)
+            dt = time.perf_counter() - t0
+            line["cpu_reference"] = {"s_per_view": round(dt, 3), "texel_views_per_s": n_valid / dt, "cores": 1,
+                                     "kind": "reference", "sample": "view 0 of 10 (edgeMask, buildMips, "
+                                     "backprojectView, incidenceMap; the blend excluded)"}
+    except Exception as e:  # noqa: BLE001 - informative only
+        line["cpu_reference"] = {"unavailable": str(e)[:120]}
+    return line
+
+
 def transfer_traffic():
     """dram__bytes_read + dram__bytes_write of the transfer kernel from the
     committed `ncu --set full` capture summary (profiles/k_transfer_ncu.json),
@@ -647,6 +729,7 @@ def run_ours(args, argv_mode, name):
     # secondary BVH metrics and the live L2 / FP64 peaks (rank 0, N = 1 only:
     # they are single-GPU numbers)
     rays = bvh_rays(ctx, hi, pair, args.steps) if rank == 0 and world == 1 and not args.no_rays else None
+    texfuse = texfuse_bench(ctx, lo, pair, args.steps) if rank == 0 and world == 1 and not args.no_rays else None
     peaks = live_peaks(d.device) if rank == 0 else {}
 
     # end-to-end through the public host-buffer API
@@ -711,7 +794,7 @@ def run_ours(args, argv_mode, name):
         "rays_per_s": agg_nq / (t_xfer_max * 1e-3),
         "n_valid_texels": n_valid, "n_queries": n_queries, "hits": hits,
         "stage_ms": {k: round(statistics.mean(v), 4) for k, v in stage.items()},
-        "roofline": roofline, "stage_rooflines": stages_rl, "peaks": peaks, "bvh": rays,
+        "roofline": roofline, "stage_rooflines": stages_rl, "peaks": peaks, "bvh": rays, "texfuse": texfuse,
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks,
     }
