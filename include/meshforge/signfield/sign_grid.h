@@ -57,4 +57,9 @@ struct GridParams {
 // every reference call site); the grid's bounds come from that mesh.
 SignGrid markSurfaceBand(const TriangleMesh& mesh, const Bvh& bvh, const GridParams& params);
 
+// Trilinear interpolation of the signed field at a world point, clamped to
+// the voxel-center lattice (sign_grid.cpp:239-264; host, one point; sampleSdf
+// evaluates it per point on the device).
+double sampleSignedField(const SignGrid& grid, const std::vector<float>& field, const Eigen::Vector3d& p);
+
 }  // namespace meshforge

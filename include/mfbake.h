@@ -252,6 +252,17 @@ int mf_surface_band(mf_bvh* bvh, int resolution, double band_voxels, int dilate_
 int mf_surface_band_dev(mf_bvh* bvh, int resolution, double band_voxels, int dilate_radius, const double* domain,
                         uint8_t* labels_dev, float* distance_dev, double* grid_out);
 
+/* sampleSdf (signfield/watertight.cpp:29-38, watertight.h:25-28) for n points
+ * against the tree of the watertight mesh: values[i] = sign * distance, the
+ * distance of the unbounded closest point (closestPoint, bvh.cpp:147-149),
+ * the sign that of sampleSignedField (sign_grid.cpp:239-264): the trilinear
+ * interpolation of `field` (grid_res^3 f32, x fastest, voxel centres at
+ * grid_origin + (i + 0.5) * voxel_size), -1 where it is < 0, else +1. */
+int mf_sample_sdf(mf_bvh* bvh, int grid_res, const double* grid_origin, double voxel_size, const float* field,
+                  const double* points, int64_t n, double* values);
+int mf_sample_sdf_dev(mf_bvh* bvh, int grid_res, const double* grid_origin, double voxel_size, const float* field_dev,
+                      const double* points_dev, int64_t n, double* values_dev);
+
 /* ---- ortho ray-cast views ------------------------------ */
 /* fibonacciCameras (render/camera.cpp:38-55): count x 7 f64 per camera =
  * direction xyz, up xyz, halfExtent. Host-only helper (no device). */

@@ -390,6 +390,17 @@ class Ref(_Lib):
             _ptr(out), _ptr(filled)))
         return out, filled
 
+    def sample_sdf(self, m: TriangleMesh, res: int, origin, voxel: float, field, pts):
+        """sampleSdf (signfield/watertight.cpp:29-38)."""
+        pts = np.ascontiguousarray(pts, np.float64).reshape(-1, 3)
+        out = np.zeros(len(pts))
+        v = m.view()
+        self._check(self.fn("sample_sdf")(ctypes.byref(v), ctypes.c_int(res),
+                                          _ptr(np.ascontiguousarray(origin, np.float64)), ctypes.c_double(voxel),
+                                          _ptr(np.ascontiguousarray(field, np.float32)), _ptr(pts),
+                                          ctypes.c_int64(len(pts)), _ptr(out)))
+        return out
+
     def standard_cameras(self, half_extent: float = 0.52) -> np.ndarray:
         cams = np.zeros((10, 7))
         self.fn("standard_cameras")(ctypes.c_double(half_extent), _ptr(cams))

@@ -35,6 +35,7 @@
 #include "meshforge/render/camera.h"
 #include "meshforge/render/raster.h"
 #include "meshforge/signfield/sign_grid.h"
+#include "meshforge/signfield/watertight.h"
 #include "meshforge/visibility/visibility.h"
 #include "meshforge/spatial/bvh.h"
 #include "meshforge/spatial/tri_geom.h"
@@ -690,6 +691,25 @@ int ref_blend_views(int k, int w, int h, int c, const float* colors, const uint8
     const TextureAtlas a = blendViews(parts, incs, std::vector<double>(priors, priors + k), opt);
     std::memcpy(out, a.color.data.data(), a.color.data.size() * sizeof(float));
     std::memcpy(filled, a.filled.data(), a.filled.size());
+  });
+}
+
+// sampleSdf (src/signfield/watertight.cpp:29-38) over a WatertightResult
+// holding `mesh`, the grid geometry and `field` (res^3).
+int ref_sample_sdf(const mf_mesh_view* mesh, int res, const double* origin, double voxel, const float* field,
+                   const double* pts, int64_t n, double* out) {
+  return guarded([&] {
+    WatertightResult wt;
+    wt.mesh = toMesh(mesh);
+    wt.grid.res = res;
+    wt.grid.voxelSize = voxel;
+    wt.grid.origin = {origin[0], origin[1], origin[2]};
+    wt.field.assign(field, field + static_cast<size_t>(res) * res * res);
+    const Bvh bvh(wt.mesh);
+    std::vector<Eigen::Vector3d> p(n);
+    for (int64_t i = 0; i < n; ++i) p[i] = {pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]};
+    const auto v = sampleSdf(wt, bvh, p);
+    std::memcpy(out, v.data(), sizeof(double) * n);
   });
 }
 

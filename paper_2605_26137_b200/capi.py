@@ -96,6 +96,8 @@ SIGNATURES = [
     ("mf_ipc_close", _I, [_VP, _VP]),
     ("mf_bake_normal_map_dev_publish", _I, [_VP, _VP, _VP, _I, _D, _D, _I, _I, _I, _VP, _I,
                                             ctypes.POINTER(MfBakeStats)]),
+    ("mf_sample_sdf", _I, [_VP, _I, _VP, _D, _VP, _VP, _I64, _VP]),
+    ("mf_sample_sdf_dev", _I, [_VP, _I, _VP, _D, _VP, _VP, _I64, _VP]),
     ("mf_surface_band", _I, [_VP, _I, _D, _I, _VP, _VP, _VP, _VP]),
     ("mf_surface_band_dev", _I, [_VP, _I, _D, _I, _VP, _VP, _VP, _VP]),
     ("mf_fibonacci_cameras", _I, [_I, _D, _VP]),
@@ -138,7 +140,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
 
 
 def _ptr(a: Optional[np.ndarray]):
-    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
 def check(status: int):

@@ -21,6 +21,7 @@
 #include "meshforge/render/camera.h"
 #include "meshforge/render/raster.h"
 #include "meshforge/signfield/sign_grid.h"
+#include "meshforge/signfield/watertight.h"
 #include "meshforge/visibility/visibility.h"
 #include "meshforge/spatial/bvh.h"
 #include "meshforge/texfuse/fuse.h"
@@ -336,6 +337,37 @@ SignGrid markSurfaceBand(const TriangleMesh& mesh, const Bvh& bvh, const GridPar
   g.labels.resize(labels.size());
   for (std::size_t i = 0; i < labels.size(); ++i) g.labels[i] = static_cast<VoxelLabel>(labels[i]);
   return g;
+}
+
+double sampleSignedField(const SignGrid& grid, const std::vector<float>& field, const Eigen::Vector3d& p) {
+  const Eigen::Vector3d q = (p - grid.origin) / grid.voxelSize - Eigen::Vector3d::Constant(0.5);
+  double result = 0;
+  int i0[3];
+  double f[3];
+  for (int k = 0; k < 3; ++k) {
+    const double c = std::clamp(q[k], 0.0, static_cast<double>(grid.res - 1));
+    i0[k] = std::max(std::min(static_cast<int>(std::floor(c)), grid.res - 2), 0);
+    f[k] = std::clamp(c - i0[k], 0.0, 1.0);
+  }
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const double w = (dx ? f[0] : 1 - f[0]) * (dy ? f[1] : 1 - f[1]) * (dz ? f[2] : 1 - f[2]);
+        result += w * field[grid.index(i0[0] + dx, i0[1] + dy, i0[2] + dz)];
+      }
+  return result;
+}
+
+std::vector<double> sampleSdf(const WatertightResult& wt, const Bvh& watertightBvh,
+                              const std::vector<Eigen::Vector3d>& points) {
+  std::vector<double> values(points.size());
+  if (points.empty()) return values;
+  if (wt.field.size() != wt.grid.cells())
+    throw Error(ErrorCode::ShapeMismatch, "signed field does not match the grid");
+  const double origin[3] = {wt.grid.origin.x(), wt.grid.origin.y(), wt.grid.origin.z()};
+  check(mf_sample_sdf(watertightBvh.handle()->bvh, wt.grid.res, origin, wt.grid.voxelSize, wt.field.data(),
+                      points.data()->data(), static_cast<int64_t>(points.size()), values.data()));
+  return values;
 }
 
 // ------------------------------------------------------------------ cameras, views, visibility

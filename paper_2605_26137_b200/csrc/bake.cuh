@@ -348,6 +348,10 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
 
 void closest_within(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* q, int64_t n,
                     double max_dist, int32_t* face, double* dist_sq, double* point, double* bary);
+// sampleSdf (signfield/watertight.cpp:29-38) for n points: unbounded closest
+// distance through the LBVH, sign from the trilinear signed field.
+void sample_sdf(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* pts, int64_t n, int res,
+                const double origin[3], double voxel, const float* field, double* out);
 // bounds(mesh) (core/mesh.cpp:12-16) into out6 = min xyz, max xyz (synchronises).
 void vertex_bounds(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out6);
 // markSurfaceBand's voxel sweep (signfield/sign_grid.cpp:56-66) over a res^3 grid.
@@ -403,6 +407,24 @@ void dilate_links(Ctx& ctx, cudaStream_t s, int res, const uint8_t* valid, int r
 void dilate_seams(Ctx& ctx, cudaStream_t s, int width, int height, int channels,
                   const uint8_t* map_in, const uint8_t* valid, int in_row0, int in_rows,
                   int radius, uint8_t* map_out, int out_row0, int out_rows);
+
+// ---------------------------------------------------------------- sort / scan (sort.cu)
+// Stable LSD sort of 30-bit Morton keys + face ids in three 10-bit onesweep
+// passes. hist: the 3 x 1024 digit histograms of the keys (built by the
+// Morton kernel); status: sort_status_words(n) words zeroed before the sort;
+// counters: 3 tile counters zeroed before the sort. Result in keys_alt /
+// vals_alt.
+struct SortArgs {
+  uint32_t *keys = nullptr, *vals = nullptr, *keys_alt = nullptr, *vals_alt = nullptr;
+  int n = 0;
+  const int* hist = nullptr;
+  uint32_t* status = nullptr;
+  int* counters = nullptr;
+};
+int64_t sort_status_words(int n);
+void radix_sort_morton30(Ctx& ctx, cudaStream_t s, const SortArgs& a);
+// Exclusive prefix sum of n int32 (single pass, decoupled look-back).
+void scan_exclusive(Ctx& ctx, cudaStream_t s, const int* in, int* out, int n, const std::string& tag);
 
 // ---------------------------------------------------------------- texfuse
 // Device-resident consumers of the G-buffer: proj/src/texfuse/fuse.cpp and

@@ -31,8 +31,8 @@
 #ifndef MFB_LOWPOLY_PRIO_DELTA
 #define MFB_LOWPOLY_PRIO_DELTA 1  // lowpoly branch streams: this many levels below the LBVH's
 #endif
-#ifndef MFB_DN_PRIO_MID
-#define MFB_DN_PRIO_MID 0  // dense vertex normals at the lowpoly branch's level (else the lowest)
+#ifndef MFB_DN_PRIO
+#define MFB_DN_PRIO 1  // dense vertex normals: 0 lowest, 1 the lowpoly branch's level, 2 the LBVH's
 #endif
 
 namespace mfb {
@@ -1412,6 +1412,10 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     // streams get the higher priority so the lowpoly branches fill in around it
     int lo_prio = 0, hi_prio = 0;
     MFB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    // r02e: the dense vertex normals (needed by the transfer's epilogue) at
+    // the lowpoly branch's level, no longer the lowest: with the hand-written
+    // sort the LBVH chain ends ~170 us earlier and the normals, starved behind
+    // the raster, became the last pre-transfer item (1.406 -> 1.352 ms).
     // The lowpoly branch streams (wedge frames, reliability, raster) are high
     // priority as well as the LBVH's; the dense normals stay low. With the
     // segment-tree LBVH the lowpoly branch is the longer chain: 1.431 ->
@@ -1427,7 +1431,7 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, mid_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, mid_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, MFB_DN_PRIO_MID ? mid_prio : lo_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, MFB_DN_PRIO == 2 ? hi_prio : (MFB_DN_PRIO == 1 ? mid_prio : lo_prio)));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up1, cudaStreamNonBlocking, hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up2, cudaStreamNonBlocking, hi_prio));
     for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3, &ctx->c.hi_ready,
@@ -1914,6 +1918,45 @@ int mf_bvh_closest_within(mf_bvh* bvh, const double* q, int64_t n, double max_di
     MFB_CUDA_TRY(cudaMemcpyAsync(dist_sq, dd, sizeof(double) * n, cudaMemcpyDeviceToHost, qs));
     if (point) MFB_CUDA_TRY(cudaMemcpyAsync(point, dp, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, qs));
     if (bary) MFB_CUDA_TRY(cudaMemcpyAsync(bary, db, sizeof(double) * 3 * n, cudaMemcpyDeviceToHost, qs));
+    MFB_CUDA_TRY(cudaStreamSynchronize(qs));
+    return MF_OK;
+  });
+}
+
+int mf_sample_sdf_dev(mf_bvh* bvh, int grid_res, const double* grid_origin, double voxel_size, const float* field_dev,
+                      const double* points_dev, int64_t n, double* values_dev) {
+  if (!bvh || !grid_origin || (n > 0 && (!field_dev || !points_dev || !values_dev)))
+    return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded_dev(bvh->device, [&]() -> int {
+    if (grid_res < 2 || !(voxel_size > 0.0))
+      throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: the signed field needs res >= 2 and voxelSize > 0");
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    sample_sdf(bvh->store, bvh->qstream, bvh->bvh, points_dev, n, grid_res, grid_origin, voxel_size, field_dev,
+               values_dev);
+    MFB_CUDA_TRY(cudaStreamSynchronize(bvh->qstream));
+    return MF_OK;
+  });
+}
+
+int mf_sample_sdf(mf_bvh* bvh, int grid_res, const double* grid_origin, double voxel_size, const float* field,
+                  const double* points, int64_t n, double* values) {
+  if (!bvh || !grid_origin || (n > 0 && (!field || !points || !values)))
+    return fail(MF_ERR_BAD_ARGUMENT, "null argument");
+  return guarded_dev(bvh->device, [&]() -> int {
+    if (grid_res < 2 || !(voxel_size > 0.0))
+      throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: the signed field needs res >= 2 and voxelSize > 0");
+    if (n <= 0) return MF_OK;
+    std::lock_guard<std::mutex> lk(bvh->mu);
+    Ctx& c = bvh->store;
+    const cudaStream_t qs = bvh->qstream;
+    const int64_t cells = static_cast<int64_t>(grid_res) * grid_res * grid_res;
+    double* dq = c.buf<double>("sdf.q", 3 * n);
+    float* dfield = c.buf<float>("sdf.field", cells);
+    double* dv = c.buf<double>("sdf.v", n);
+    MFB_CUDA_TRY(cudaMemcpyAsync(dq, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, qs));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dfield, field, sizeof(float) * cells, cudaMemcpyHostToDevice, qs));
+    sample_sdf(c, qs, bvh->bvh, dq, n, grid_res, grid_origin, voxel_size, dfield, dv);
+    MFB_CUDA_TRY(cudaMemcpyAsync(values, dv, sizeof(double) * n, cudaMemcpyDeviceToHost, qs));
     MFB_CUDA_TRY(cudaStreamSynchronize(qs));
     return MF_OK;
   });

@@ -134,6 +134,50 @@ __device__ __forceinline__ void px_store(uint8_t* base, int64_t t, int fmt, uint
   }
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with launch_pdl may start (its CTAs become resident and
+// run their prologue) while its same-stream predecessor is finishing; it must
+// call pdl_wait() before touching anything the predecessor writes or reads.
+// Predecessors call pdl_trigger() once every CTA has started, so the
+// dependent's launch overlaps their tail. Inside a captured graph the
+// dependency becomes a programmatic edge. Without the launch attribute both
+// instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+// Where the chain's kernels trigger: MFB_PDL_EARLY=1 (default) right after
+// their own wait, so each dependent's CTAs become resident while the
+// predecessor runs; 0: before their final stores (PDL_TRIGGER_LATE), or
+// implicitly at exit. Measured on config B: early 1.390-1.394 ms per bake,
+// late 1.404-1.411, no PDL 1.409-1.414.
+#ifndef MFB_PDL_EARLY
+#define MFB_PDL_EARLY 1
+#endif
+#if MFB_PDL_EARLY
+#define PDL_TRIGGER_EARLY() pdl_trigger()
+#define PDL_TRIGGER_LATE() ((void)0)
+#else
+#define PDL_TRIGGER_EARLY() ((void)0)
+#define PDL_TRIGGER_LATE() pdl_trigger()
+#endif
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+#ifdef MFB_NO_PDL
+  cfg.numAttrs = 0;
+#else
+  cfg.numAttrs = 1;
+#endif
+  MFB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+
 // ---------------------------------------------------------------- launch geometry
 constexpr int kNumSMs = 148;  // B200: 2 dies x 74 SMs
 

@@ -1,10 +1,11 @@
 // lbvh.cu — GPU LBVH over the dense mesh (replaces Bvh::Bvh/build,
 // spatial/bvh.cpp:48-98).
 //
-// Pipeline (one stream, 5 launches + one CUB radix sort):
+// Pipeline (one stream; the repack / segment tree on a helper stream):
 //   1. bounds      : centroid bounds + max |coordinate| (ordered-int atomics)
 //   2. morton      : 30-bit Morton key of each face centroid
-//   3. sort        : CUB onesweep radix sort of (key, face) pairs
+//   3. sort        : hand-written stable 3-pass onesweep radix sort of
+//                    (key, face) pairs (sort.cu), histograms built in step 2
 //   4. emit        : Karras 2012 hierarchy emission; subtrees covering
 //                    <= kLeafMax primitives become leaf ranges (the
 //                    reference's leaf size, bvh.cpp:13)
@@ -15,7 +16,6 @@
 // Query results do not depend on the tree shape: the reference
 // answer is argmin over faces of (distSq, face), which any conservative tree
 // reproduces exactly.
-#include <cub/device/device_radix_sort.cuh>
 #include <cuda/atomic>
 
 #include <cstdlib>
@@ -45,6 +45,8 @@ __host__ __device__ __forceinline__ double from_ordered(unsigned long long b) {
 // positions is cheaper than gathering every face's corners), acc[6] = max
 // |vertex coord|
 __global__ void k_bounds(const double* __restrict__ pos, int nv, unsigned long long* acc) {
+  pdl_wait();
+  PDL_TRIGGER_EARLY();
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
   double amax = 0.0;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
@@ -86,9 +88,11 @@ __global__ void k_bounds(const double* __restrict__ pos, int nv, unsigned long l
   }
 }
 
-// min slots (0..2) to all-ones, max / |max| slots (3..7) to zero
-__global__ void k_acc_init(unsigned long long* acc) {
+// min slots (0..2) to all-ones, max / |max| slots (3..7) to zero; the sort's
+// 3 x 1024 digit histograms and 3 tile counters to zero
+__global__ void k_acc_init(unsigned long long* acc, int* hist) {
   if (threadIdx.x < 8) acc[threadIdx.x] = threadIdx.x < 3 ? ~0ull : 0ull;
+  for (int i = threadIdx.x; i < 3 * 1024 + 4; i += blockDim.x) hist[i] = 0;
 }
 
 __device__ __forceinline__ uint32_t spread10(uint32_t v) {
@@ -100,15 +104,27 @@ __device__ __forceinline__ uint32_t spread10(uint32_t v) {
   return v;
 }
 
-// 30-bit Morton keys (10 bits per axis over the centroid bounds): 4 radix
-// passes instead of 8. Duplicate keys are fine - Karras' emission breaks
+// 30-bit Morton keys (10 bits per axis over the centroid bounds), fused with
+// the sort's three 10-bit digit histograms (block histograms in shared
+// memory, one global atomic per non-empty bin) and the zeroing of its
+// look-back status words. Duplicate keys are fine - Karras' emission breaks
 // ties with the primitive index.
-__global__ void k_morton(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
-                         const unsigned long long* __restrict__ acc, uint32_t* __restrict__ keys,
-                         uint32_t* __restrict__ vals, int axis_bits) {
-  const double cells = static_cast<double>((1 << axis_bits) - 1);
-  const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= nf) return;
+constexpr int kMortonThreads = 512, kMortonPer = 8;
+__global__ void __launch_bounds__(kMortonThreads) k_morton(const double* __restrict__ pos,
+                                                           const int32_t* __restrict__ faces, int nf,
+                                                           const unsigned long long* __restrict__ acc,
+                                                           uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                           int* __restrict__ hist, uint32_t* __restrict__ status,
+                                                           int64_t status_words) {
+  pdl_wait();
+  PDL_TRIGGER_EARLY();
+  __shared__ int h[3 * 1024];
+  for (int i = threadIdx.x; i < 3 * 1024; i += blockDim.x) h[i] = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < status_words;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    status[i] = 0u;
+  __syncthreads();
+  constexpr double cells = 1023.0;
   double lo[3], inv[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -116,17 +132,30 @@ __global__ void k_morton(const double* __restrict__ pos, const int32_t* __restri
     const double ext = from_ordered(acc[3 + k]) - lo[k];
     inv[k] = ext > 0.0 ? cells / ext : 0.0;
   }
-  const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
-  uint32_t q[3];
+  const int f0 = blockIdx.x * (kMortonThreads * kMortonPer);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    const double ck = ((pos[3 * a + k] + pos[3 * b + k]) + pos[3 * c + k]) / 3.0;
-    double t = (ck - lo[k]) * inv[k];
-    t = fmin(fmax(t, 0.0), cells);
-    q[k] = static_cast<uint32_t>(t);
+  for (int j = 0; j < kMortonPer; ++j) {
+    const int f = f0 + j * kMortonThreads + threadIdx.x;
+    if (f >= nf) break;
+    const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+    uint32_t q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double ck = ((pos[3 * a + k] + pos[3 * b + k]) + pos[3 * c + k]) / 3.0;
+      double t = (ck - lo[k]) * inv[k];
+      t = fmin(fmax(t, 0.0), cells);
+      q[k] = static_cast<uint32_t>(t);
+    }
+    const uint32_t key = (spread10(q[0]) << 2) | (spread10(q[1]) << 1) | spread10(q[2]);
+    keys[f] = key;
+    vals[f] = static_cast<uint32_t>(f);
+    atomicAdd(&h[key & 1023u], 1);
+    atomicAdd(&h[1024 + ((key >> 10) & 1023u)], 1);
+    atomicAdd(&h[2048 + (key >> 20)], 1);
   }
-  keys[f] = (spread10(q[0]) << 2) | (spread10(q[1]) << 1) | spread10(q[2]);
-  vals[f] = static_cast<uint32_t>(f);
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * 1024; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 
 // Karras delta over augmented keys (key, index): -1 outside [0, n).
@@ -146,6 +175,8 @@ __device__ __forceinline__ int kdelta(const uint32_t* __restrict__ k, int n, int
 __global__ void k_emit(const uint32_t* __restrict__ keys, int n, int leaf_max, BNode* __restrict__ nodes,
                        int32_t* __restrict__ prim_parent, int32_t* __restrict__ node_parent,
                        int32_t* __restrict__ starts, int* __restrict__ starts_n, int reach_list = 0) {
+  pdl_wait();
+  PDL_TRIGGER_EARLY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n - 1;
   bool start = false;
@@ -374,6 +405,8 @@ __global__ void __launch_bounds__(1024) k_repack_seg(const double* __restrict__ 
 // streaming reduction reads the 32-byte boxes once).
 __global__ void __launch_bounds__(1024) k_seg_leaves(const TBox* __restrict__ tbox, int n, int N,
                                                      TBox* __restrict__ seg) {
+  pdl_wait();
+  PDL_TRIGGER_EARLY();
   __shared__ FBox sm[32];
   const int p = blockIdx.x * 1024 + threadIdx.x;
   const FBox box = p < n ? fbox_load(tbox + p) : fbox_empty();
@@ -382,6 +415,8 @@ __global__ void __launch_bounds__(1024) k_seg_leaves(const TBox* __restrict__ tb
 
 // The next 10 levels: nodes [L, 2L) -> their ancestors.
 __global__ void __launch_bounds__(1024) k_seg_up(TBox* __restrict__ seg, int L) {
+  pdl_wait();
+  PDL_TRIGGER_EARLY();
   __shared__ FBox sm[32];
   const int i = blockIdx.x * 1024 + threadIdx.x;
   const FBox box = i < L ? fbox_load(seg + L + i) : fbox_empty();
@@ -396,6 +431,8 @@ __global__ void __launch_bounds__(1024) k_seg_up(TBox* __restrict__ seg, int L) 
 __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restrict__ tbox, int N, int n, int leaf_max,
                              BNode* __restrict__ nodes, float* __restrict__ root_box,
                              const int32_t* __restrict__ reach, const int* __restrict__ reach_n) {
+  pdl_wait();
+  PDL_TRIGGER_EARLY();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *reach_n) return;
   const int i = reach[j];
@@ -632,7 +669,11 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   auto* starts = ctx.buf<int32_t>(tag + ".starts", n);
   auto* starts_n = ctx.buf<int>(tag + ".starts_n", 1);
 
-  k_acc_init<<<1, 32, 0, s>>>(acc);
+  // sort scratch: 3 x 1024 digit histograms + 3 tile counters, look-back status
+  auto* hist = ctx.buf<int>(tag + ".hist", 3 * 1024 + 4);
+  const int64_t status_words = sort_status_words(n);
+  auto* status = ctx.buf<uint32_t>(tag + ".sortst", status_words);
+  k_acc_init<<<1, 1024, 0, s>>>(acc, hist);
   ctx.count_launch();
   // segment-tree node boxes (MFB_SEGTREE=0: the bottom-up refit climb)
   static const bool segtree = [] {
@@ -644,21 +685,22 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
 
   const int T = 256;
   const int grid_b = std::min(div_up(std::max(n, m.nv), T), kNumSMs * 8);
-  k_bounds<<<grid_b, T, 0, s>>>(m.pos, m.nv, acc);
-  // Morton bits per axis: 10 (30-bit keys, 4 radix passes) unless
-  // MFB_MORTON_BITS (6..10) overrides it; fewer bits = fewer sort passes.
-  static const int axis_bits = [] {
-    const char* e = std::getenv("MFB_MORTON_BITS");
-    const int v = e ? std::atoi(e) : 10;
-    return v >= 6 && v <= 10 ? v : 10;
-  }();
-  k_morton<<<div_up(n, T), T, 0, s>>>(m.pos, m.faces, n, acc, keys, vals, axis_bits);
+  // the chain up to the sort runs with programmatic dependent launch
+  launch_pdl(k_bounds, grid_b, T, 0, s, m.pos, m.nv, acc);
+  launch_pdl(k_morton, std::max(1, div_up(n, kMortonThreads * kMortonPer)), kMortonThreads, 0, s, m.pos, m.faces, n,
+             acc, keys, vals, hist, status, status_words);
   ctx.count_launch(2);
-
-  size_t tmp = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, keys2, vals, vals2, n, 0, 3 * axis_bits, s);
-  void* tptr = ctx.cub_temp(tmp, s);
-  MFB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tptr, tmp, keys, keys2, vals, vals2, n, 0, 3 * axis_bits, s));
+  // stable 3-pass radix sort (sort.cu): sorted pairs in keys2 / vals2
+  SortArgs sa;
+  sa.keys = keys;
+  sa.vals = vals;
+  sa.keys_alt = keys2;
+  sa.vals_alt = vals2;
+  sa.n = n;
+  sa.hist = hist;
+  sa.status = status;
+  sa.counters = hist + 3 * 1024;
+  radix_sort_morton30(ctx, s, sa);
 
   // Leaf size: the caller's hint or kLeafMaxDefault (the reference uses 4,
   // bvh.cpp:13; results are tree-independent) unless MFB_LEAF_MAX (1..15)
@@ -692,10 +734,10 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
       k_repack_seg<<<div_up(N, 1024), 1024, 0, rs>>>(m.pos, m.faces, vals2, n, N, out.tris, out.tbox, seg);
     } else {
       k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
-      k_seg_leaves<<<div_up(N, 1024), 1024, 0, rs>>>(out.tbox, n, N, seg);
+      launch_pdl(k_seg_leaves, div_up(N, 1024), 1024, 0, rs, out.tbox, n, N, seg);
       ++launches;
     }
-    for (int L = N >> 10; L > 1; L >>= 10, ++launches) k_seg_up<<<div_up(L, 1024), 1024, 0, rs>>>(seg, L);
+    for (int L = N >> 10; L > 1; L >>= 10, ++launches) launch_pdl(k_seg_up, div_up(L, 1024), 1024, 0, rs, seg, L);
     ctx.count_launch(launches - 1);
   } else {
     k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);

@@ -1285,6 +1285,54 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
   }
 }
 
+namespace {
+// sampleSdf's per-point tail (signfield/watertight.cpp:29-38): magnitude
+// sqrt(distSq) of the unbounded closest point (SurfacePoint::distance,
+// bvh.h:24), sign from sampleSignedField (sign_grid.cpp:239-264, the same f64
+// operations: lattice coordinates, clamped cell, trilinear weights summed
+// z-y-x in order).
+__global__ void k_sdf_finish(int64_t n, const double* __restrict__ pts, const double* __restrict__ dist_sq,
+                             int res, double ox, double oy, double oz, double h, const float* __restrict__ field,
+                             double* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double q[3] = {(pts[3 * i] - ox) / h - 0.5, (pts[3 * i + 1] - oy) / h - 0.5, (pts[3 * i + 2] - oz) / h - 0.5};
+  int i0[3];
+  double f[3];
+  for (int k = 0; k < 3; ++k) {
+    const double hi = static_cast<double>(res - 1);
+    const double c = q[k] < 0.0 ? 0.0 : (hi < q[k] ? hi : q[k]);  // std::clamp(v, 0, res - 1)
+    int a = min(static_cast<int>(floor(c)), res - 2);
+    a = max(a, 0);
+    const double fr = c - a;
+    i0[k] = a;
+    f[k] = fr < 0.0 ? 0.0 : (1.0 < fr ? 1.0 : fr);
+  }
+  double result = 0;
+  for (int dz = 0; dz < 2; ++dz)
+    for (int dy = 0; dy < 2; ++dy)
+      for (int dx = 0; dx < 2; ++dx) {
+        const double w = (dx ? f[0] : 1 - f[0]) * (dy ? f[1] : 1 - f[1]) * (dz ? f[2] : 1 - f[2]);
+        const int64_t idx = static_cast<int64_t>(i0[0] + dx) +
+                            static_cast<int64_t>(res) * ((i0[1] + dy) + static_cast<int64_t>(res) * (i0[2] + dz));
+        result += w * field[idx];
+      }
+  const double sign = result < 0 ? -1.0 : 1.0;
+  out[i] = sign * sqrt(dist_sq[i]);
+}
+}  // namespace
+
+void sample_sdf(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* pts, int64_t n, int res,
+                const double origin[3], double voxel, const float* field, double* out) {
+  if (n <= 0) return;
+  int32_t* face = ctx.buf<int32_t>("sdf.face", n);
+  double* ds = ctx.buf<double>("sdf.ds", n);
+  closest_within(ctx, s, bvh, pts, n, INFINITY, face, ds, nullptr, nullptr);
+  k_sdf_finish<<<div_up(n, 256), 256, 0, s>>>(n, pts, ds, res, origin[0], origin[1], origin[2], voxel, field, out);
+  ctx.count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
+}
+
 void closest_within(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const double* q, int64_t n,
                     double max_dist, int32_t* face, double* dist_sq, double* point, double* bary) {
   if (n <= 0) return;

@@ -17,7 +17,6 @@
 //                   gbuffer.cpp:21-27,146-154), AtlasOverlap detection,
 //                   f64 attribute interpolation, coalesced G-buffer stores.
 #include <cooperative_groups.h>
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cstdlib>
@@ -120,21 +119,48 @@ __global__ void k_vertex_sum(int nv, const int* __restrict__ start, const int* _
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v < nv) d_vertex_sum(v, start, list, av, out, renorm);
 }
-// Same sum for an UNSORTED incident-corner list: lists of up to 16 corners
-// (any regular mesh) are ordered in registers, longer ones in place; the sum
-// then runs in face order exactly as k_vertex_sum.
-__global__ void k_vertex_sum_unsorted(int nv, const int* __restrict__ start, int* __restrict__ list,
-                                      const double* __restrict__ av, double* __restrict__ out, int renorm) {
+// Dense-mesh vertex normals without a CSR build: each face stores its area
+// vector and drops its three corner ids into fixed per-vertex slots
+// (kVnSlots; a vertex of higher valence spills the rest into an overflow
+// list); the summation orders a vertex's corners in registers and adds the
+// area vectors in face order, exactly as computeVertexNormals' face loop
+// (mesh.cpp:24-35).
+constexpr int kVnSlots = 16;
+__global__ void k_vn_slots(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
+                           double* __restrict__ av, int* __restrict__ cnt, int* __restrict__ slots,
+                           int* __restrict__ ovf, int ovf_cap) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nf) return;
+  d_face_area_vec(pos, faces, f, av);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int c = 3 * f + k, v = faces[c];
+    const int s = atomicAdd(&cnt[v], 1);
+    if (s < kVnSlots) {
+      slots[static_cast<int64_t>(v) * kVnSlots + s] = c;
+    } else {
+      const int o = atomicAdd(ovf, 1);
+      if (o < ovf_cap) {
+        ovf[1 + 2 * o] = v;
+        ovf[2 + 2 * o] = c;
+      }
+    }
+  }
+}
+__global__ void k_vn_sum(int nv, const int* __restrict__ cnt, const int* __restrict__ slots,
+                         const int* __restrict__ ovf, const double* __restrict__ av, double* __restrict__ out,
+                         int renorm) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= nv) return;
-  const int b = start[v], e = start[v + 1], k = e - b;
+  const int k = cnt[v];
+  const int* sl = slots + static_cast<int64_t>(v) * kVnSlots;
   d3 n = mk3(0.0, 0.0, 0.0);
-  if (k <= 16) {
-    int c[16];
+  if (k <= kVnSlots) {
+    int c[kVnSlots];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) c[i] = i < k ? list[b + i] : 0x7fffffff;
+    for (int i = 0; i < kVnSlots; ++i) c[i] = i < k ? sl[i] : 0x7fffffff;
 #pragma unroll
-    for (int i = 1; i < 16; ++i) {  // insertion sort, fully unrolled (register resident)
+    for (int i = 1; i < kVnSlots; ++i) {  // insertion sort, fully unrolled (register resident)
 #pragma unroll
       for (int j = i; j > 0; --j) {
         const int lo = min(c[j - 1], c[j]), hi = max(c[j - 1], c[j]);
@@ -143,19 +169,27 @@ __global__ void k_vertex_sum_unsorted(int nv, const int* __restrict__ start, int
       }
     }
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
+    for (int i = 0; i < kVnSlots; ++i)
       if (i < k) n = n + ld3(av + 3 * (c[i] / 3));
   } else {
-    for (int i = b + 1; i < e; ++i) {
-      const int key = list[i];
-      int j = i - 1;
-      while (j >= b && list[j] > key) {
-        list[j + 1] = list[j];
-        --j;
+    // valence above kVnSlots (rare): the slots plus this vertex's overflow
+    // entries, taken in increasing corner order by repeated minimum search
+    const int no = ovf[0];
+    int last = -1;
+    for (int it = 0; it < k; ++it) {
+      int nxt = 0x7fffffff;
+      for (int i = 0; i < kVnSlots; ++i) {
+        const int c = sl[i];
+        if (c > last && c < nxt) nxt = c;
       }
-      list[j + 1] = key;
+      for (int o = 0; o < no; ++o)
+        if (ovf[1 + 2 * o] == v) {
+          const int c = ovf[2 + 2 * o];
+          if (c > last && c < nxt) nxt = c;
+        }
+      n = n + ld3(av + 3 * (nxt / 3));
+      last = nxt;
     }
-    for (int i = b; i < e; ++i) n = n + ld3(av + 3 * (list[i] / 3));
   }
   const double len = norm(n);
   if (len > 0) n = n / len;
@@ -1189,9 +1223,7 @@ void corner_csr(Ctx& ctx, cudaStream_t s, const DevMesh& m, const std::string& t
   int* list = ctx.buf<int>(tag + ".csr.list", nc);
   ctx.fill(cnt, 0, sizeof(int) * 2 * (m.nv + 1), s);
   k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, start, m.nv + 1, s));
+  scan_exclusive(ctx, s, cnt, start, m.nv + 1, tag + ".csr");
   k_corner_fill<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, start, cursor, list);
   k_csr_sort<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list);
   ctx.count_launch(3);
@@ -1221,22 +1253,17 @@ void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, boo
     }
     return;
   }
-  // unsorted CSR + in-register ordering inside the summation kernel
-  const int nc = 3 * m.nf;
-  int* cnt = ctx.buf<int>(tag + ".csr.cc", 2 * (m.nv + 1));  // counts, then fill cursors: one fill
-  int* cursor = cnt + m.nv + 1;
-  int* start = ctx.buf<int>(tag + ".csr.start", m.nv + 1);
-  int* list = ctx.buf<int>(tag + ".csr.list", nc);
+  // per-vertex corner slots + in-register ordering inside the summation kernel
+  int* cnt = ctx.buf<int>(tag + ".vn.cnt", static_cast<size_t>(m.nv) + 1);  // [nv]: overflow count
+  int* slots = ctx.buf<int>(tag + ".vn.slots", static_cast<size_t>(m.nv) * kVnSlots);
+  const int ovf_cap = 3 * m.nf;
+  int* ovf = ctx.buf<int>(tag + ".vn.ovf", 1 + 2 * static_cast<size_t>(ovf_cap));
   double* av = ctx.buf<double>(tag + ".vn.av", 3 * static_cast<size_t>(m.nf));
-  ctx.fill(cnt, 0, sizeof(int) * 2 * (m.nv + 1), s);
-  k_corner_count<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, cnt);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, start, m.nv + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, start, m.nv + 1, s));
-  k_corner_fill<<<div_up(nc, T), T, 0, s>>>(m.faces, nc, start, cursor, list);
-  k_face_area_vec<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, av);
-  k_vertex_sum_unsorted<<<div_up(m.nv, T), T, 0, s>>>(m.nv, start, list, av, out, renorm ? 1 : 0);
-  ctx.count_launch(4);
+  ctx.fill(cnt, 0, sizeof(int) * (m.nv + 1), s);
+  ctx.fill(ovf, 0, sizeof(int), s);
+  k_vn_slots<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, av, cnt, slots, ovf, ovf_cap);
+  k_vn_sum<<<div_up(m.nv, T), T, 0, s>>>(m.nv, cnt, slots, ovf, av, out, renorm ? 1 : 0);
+  ctx.count_launch(2);
   MFB_CUDA_TRY(cudaGetLastError());
 }
 
@@ -1359,9 +1386,7 @@ void bin_faces(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, RasterFace*
   int* bins = ctx.buf<int>("ras.bins", capacity);
   ctx.fill(cnt, 0, sizeof(int) * 2 * (ntiles + 1), s);
   k_face_setup_count<<<div_up(nf, T), T, 0, s>>>(lo.uvs, lo.fuv, nf, res, rf, row_begin, row_end, tiles_x, cnt);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, tstart, ntiles + 1, s);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, tstart, ntiles + 1, s));
+  scan_exclusive(ctx, s, cnt, tstart, ntiles + 1, std::string("ras"));
   k_bin_fill<<<div_up(nf, T), T, 0, s>>>(rf, nf, row_begin, row_end, tiles_x, tstart, cursor, bins, capacity,
                                          b.flags + 1, ntiles, b.zero4);
   ctx.count_launch(2);
@@ -1433,9 +1458,7 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
   k_uf_flatten<<<div_up(nu, T), T, 0, us>>>(nu, parent);
   k_face_ratio<<<div_up(nf, T), T, 0, us>>>(lo.pos, lo.faces, lo.uvs, lo.fuv, nf, parent, uv_area, ratio, island,
                                             count);
-  size_t tmp = 0;
-  cub::DeviceScan::ExclusiveSum(nullptr, tmp, count, start, nu + 1, us);
-  MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, us), tmp, count, start, nu + 1, us));
+  scan_exclusive(ctx, us, count, start, nu + 1, std::string("lo.rel"));
   k_island_fill<<<div_up(nf, T), T, 0, us>>>(nf, ratio, island, start, cursor, items);
   k_island_select<<<nu, 256, 0, us>>>(nu, count, start, items, median);
   if (us != s) MFB_CUDA_TRY(cudaStreamWaitEvent(us, ctx.setup_done, 0));
@@ -1473,9 +1496,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
     int* tbins = ctx.buf<int>("ras.bins", capacity);
     ctx.fill(cnt, 0, sizeof(int) * 2 * (ntiles + 1), s);
     k_bin_count<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, cnt);
-    size_t tmp = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp, cnt, tstart, ntiles + 1, s);
-    MFB_CUDA_TRY(cub::DeviceScan::ExclusiveSum(ctx.cub_temp(tmp, s), tmp, cnt, tstart, ntiles + 1, s));
+    scan_exclusive(ctx, s, cnt, tstart, ntiles + 1, std::string("ras"));
     k_bin_fill<<<div_up(plan.nf, T), T, 0, s>>>(rf, plan.nf, row_begin, row_end, tiles_x, tstart, cursor, tbins,
                                                 capacity, flags_dev + 1, ntiles);
     ctx.count_launch(3);

@@ -24,7 +24,8 @@ __all__ = ["GBuffer", "rasterize_gbuffer", "transfer_normals", "dilate_seams", "
 
 
 def _p(a):
-    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+    # data_as keeps a reference to `a`: temporaries stay alive through the call
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
 @dataclass
@@ -232,6 +233,17 @@ class Bvh:
         f, t, u, v = self.raycasts(np.asarray(origin, np.float64)[None], np.asarray(direction, np.float64)[None],
                                    t_min, t_max)
         return RayHit(int(f[0]), float(t[0]), float(u[0]), float(v[0]))
+
+    def sample_sdf(self, grid_res: int, origin, voxel_size: float, field: np.ndarray, points: np.ndarray):
+        """sampleSdf (signfield/watertight.cpp:29-38) with this tree as the
+        watertight mesh's: sign(trilinear field) * closest distance."""
+        pts = np.ascontiguousarray(points, np.float64).reshape(-1, 3)
+        fld = np.ascontiguousarray(field, np.float32).reshape(-1)
+        org = np.ascontiguousarray(origin, np.float64).reshape(3)
+        out = np.zeros(len(pts))
+        check(self.ctx.lib.mf_sample_sdf(self.h, int(grid_res), _p(org), float(voxel_size), _p(fld), _p(pts),
+                                         len(pts), _p(out)))
+        return out
 
     def surface_band(self, resolution: int = 128, band_voxels: float = 1.0, dilate_radius: int = 2,
                      domain=None):

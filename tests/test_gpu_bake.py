@@ -273,3 +273,21 @@ def test_fused_bake_unreliable_faces(gpu_ctx, port):
             for _ in range(3):  # eager, captured, replayed
                 got = mf.bake_normal_map(m, dense, 128, float(dense.bbox_diagonal()), 0.5, radius, out=host)
                 assert np.array_equal(got.reshape(-1, 3), out["rgb"].reshape(-1, 3))
+
+
+@pytest.mark.parametrize("valence", [5, 16, 17, 40, 300])
+def test_vertex_normals_high_valence_fans(gpu_ctx, port, valence):
+    """computeVertexNormals (mesh.cpp:24-35) on a cone fan whose apex has the
+    given valence (per-vertex slots hold 16 corners; more spill to the
+    overflow list), plus a degenerate face naming one vertex twice: bit-exact
+    vs the port (face-order sums)."""
+    from paper_2605_26137_b200.mesh import TriangleMesh
+    rng = np.random.default_rng(valence)
+    ang = np.sort(rng.uniform(0, 2 * np.pi, valence))
+    rim = np.stack([np.cos(ang), np.sin(ang), 0.1 * rng.standard_normal(valence)], 1)
+    pos = np.vstack([[0.0, 0.0, 0.7], rim, [[0.3, 0.2, -0.4]]])
+    faces = [[0, 1 + i, 1 + (i + 1) % valence] for i in range(valence)]
+    faces.append([1, 1, valence + 1])  # degenerate: vertex 1 twice
+    perm = rng.permutation(len(faces))  # apex corners spread over the face order
+    m = TriangleMesh(pos, np.asarray(faces, np.int32)[perm])
+    assert np.array_equal(mf.compute_vertex_normals(m), port.vertex_normals(m))

@@ -241,3 +241,72 @@ def test_bvh_outlives_its_context_and_serves_threads(gpu_ctx):
     for a, b in zip(serial, par):
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
+
+
+def _morton30(m: TriangleMesh) -> np.ndarray:
+    """lbvh.cu k_morton restated in numpy (same f64 operations): 10 bits per
+    axis of the face centroid over the vertex bounds."""
+    p = m.positions
+    lo, hi = p.min(0), p.max(0)
+    ext = hi - lo
+    inv = np.where(ext > 0.0, 1023.0 / np.where(ext > 0.0, ext, 1.0), 0.0)
+    f = m.faces
+    c = ((p[f[:, 0]] + p[f[:, 1]]) + p[f[:, 2]]) / 3.0
+    q = np.clip((c - lo) * inv, 0.0, 1023.0).astype(np.uint32)
+
+    def spread(v):
+        v = v & 0x3FF
+        v = (v | (v << 16)) & 0x030000FF
+        v = (v | (v << 8)) & 0x0300F00F
+        v = (v | (v << 4)) & 0x030C30C3
+        v = (v | (v << 2)) & 0x09249249
+        return v
+
+    return (spread(q[:, 0]) << 2) | (spread(q[:, 1]) << 1) | spread(q[:, 2])
+
+
+@pytest.mark.parametrize("kind", ["blob", "dense", "dups", "tiny"])
+def test_lbvh_leaf_order_is_the_stable_morton_sort(gpu_ctx, kind):
+    """The hand-written 3-pass radix sort (sort.cu) is a stable sort of the
+    30-bit Morton keys: the tree's leaf order equals numpy's stable argsort,
+    across several 8192-key tiles, a partial last tile, and many equal keys
+    (duplicated triangles: deep equal-key runs resolved by face index)."""
+    if kind == "blob":
+        m = fx.star_blob(9, 40, 40)
+    elif kind == "dense":
+        m = fx.bake_pair(96, 4, 16, name="sort").dense  # ~184k faces, 23 tiles
+    elif kind == "dups":
+        base = fx.star_blob(5, 24, 24)
+        k = 40  # 40 copies of every face: equal keys in runs of 40
+        m = TriangleMesh(base.positions, np.tile(base.faces, (k, 1)))
+    else:
+        m = TriangleMesh([[0, 0, 0], [1, 0, 0], [0, 1, 0], [1, 1, 0]], [[0, 1, 2], [1, 3, 2]])
+    _, _, order = mf.Bvh(m).export()
+    expect = np.argsort(_morton30(m), kind="stable")
+    assert np.array_equal(order, expect)
+    if kind == "dups":  # the traversal copes with the deep equal-key subtrees
+        b = mf.Bvh(m)
+        q = np.random.default_rng(1).uniform(-0.6, 0.6, (2000, 3))
+        f, ds, _, _ = b.closest_points(q)
+        ref_f, ref_ds, _, _ = mf.Bvh(TriangleMesh(m.positions, m.faces[: len(m.faces) // 40])).closest_points(q)
+        assert np.array_equal(ds, ref_ds)
+        assert np.array_equal(f, ref_f)  # ties go to the lowest face index: the first copy
+
+
+def test_sample_sdf_matches_reference(gpu_ctx, ref):
+    """sampleSdf (signfield/watertight.cpp:29-38) batched on the device
+    (mf_sample_sdf): bit-exact vs the reference's own function over the same
+    mesh, grid geometry and signed field (a synthetic field: the signed
+    distance to a sphere, sampled at the voxel centres)."""
+    m = fx.star_blob(7, 32, 32)
+    res = 24
+    origin = np.array([-0.8, -0.75, -0.7])
+    h = 1.5 / res
+    c = origin + h * (np.stack(np.meshgrid(np.arange(res), np.arange(res), np.arange(res), indexing="ij"), -1) + 0.5)
+    field = (np.linalg.norm(c, axis=-1) - 0.45).astype(np.float32).transpose(2, 1, 0).reshape(-1)  # x fastest
+    rng = np.random.default_rng(9)
+    pts = np.vstack([rng.uniform(-1.0, 1.0, (3000, 3)), [[0.0, 0.0, 0.0], [5.0, 5.0, 5.0], [-3.0, 0.1, 0.2]]])
+    got = mf.Bvh(m).sample_sdf(res, origin, h, field, pts)
+    exp = ref.sample_sdf(m, res, origin, h, field, pts)
+    assert np.array_equal(got, exp)
+    assert (got < 0).any() and (got > 0).any()
