@@ -394,7 +394,7 @@ def bvh_rays(ctx, hi, pair, steps):
                       "closest-point radius = maxDistFrac x diag"}
 
 
-def texfuse_bench(ctx, lo, pair, steps):
+def texfuse_bench(ctx, lo, pair, steps, once=False):
     """fuseViews up to the blend (fuse.cpp:292-318) on the
     device over the config-B lowpoly's 2048^2 G-buffer (mf_raster_gbuffer_dev,
     resident in HBM) and the 10 standard views at 1024^2 of the dense mesh
@@ -440,6 +440,8 @@ def texfuse_bench(ctx, lo, pair, steps):
                                           filled.data_ptr()))
     call()
     torch.cuda.synchronize()
+    if once:  # (profiling: one call)
+        return None
     stream = torch.cuda.current_stream()
     ts = []
     for _ in range(max(3, min(steps, 10))):

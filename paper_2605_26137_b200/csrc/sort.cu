@@ -7,8 +7,10 @@
 //   onesweep style: a CTA takes the next 8192-key tile (dynamic tile order, so
 //   look-back only ever waits on running CTAs), ranks its keys per warp with
 //   __match_any_sync (stable: element order within the warp, warps in tile
-//   order), publishes its per-digit tile counts, resolves the tile's exclusive
-//   digit prefix by decoupled look-back over earlier tiles, shuffles the tile
+//   order), publishes its per-digit tile counts, sums the earlier tiles'
+//   published counts (8 independent loads in flight per digit) back to the
+//   first inclusive prefix for its exclusive digit prefix, publishes its own
+//   inclusive prefix, shuffles the tile
 //   into digit order in shared memory and writes it out in per-digit runs.
 //   Config B (1,003,520 keys): 123 tiles, one wave at 2 CTAs/SM.
 // scan_exclusive: single-pass decoupled look-back exclusive sum of int32.
@@ -142,8 +144,8 @@ __global__ void __launch_bounds__(kSortThreads, 2)
       acc += c;
     }
     tot[k] = acc;
-    // publish the tile's aggregate (the first tile's is already inclusive)
-    const uint32_t v = (tile == 0 ? kFlagInc : kFlagAgg) | static_cast<uint32_t>(acc);
+    // publish the tile's aggregate
+    const uint32_t v = kFlagAgg | static_cast<uint32_t>(acc);
     st_status(status + static_cast<int64_t>(tile) * kBins + d, v);
   }
   // tile-local digit starts (exclusive scan over the 1024 digits)
@@ -158,33 +160,31 @@ __global__ void __launch_bounds__(kSortThreads, 2)
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const int d = 2 * threadIdx.x + k;
+    // look back over the earlier tiles 8 at a time (independent loads): sum
+    // their published counts down to the first inclusive prefix; every tile
+    // publishes its aggregate right after ranking, so no tile waits on a
+    // serial chain of inclusive prefixes
     int excl = 0;
-    if (tile > 0) {
-#ifdef MFB_SORT_DEBUG
-      int iters = 0;
-      uint32_t first = 0;
-#endif
-      for (int t = tile - 1; t >= 0; --t) {
-        uint32_t v;
-        do {
-          v = ld_status(status + static_cast<int64_t>(t) * kBins + d);
-        } while ((v & (kFlagAgg | kFlagInc)) == 0u);
-#ifdef MFB_SORT_DEBUG
-        if (iters++ == 0) first = v;
-#endif
-        excl += static_cast<int>(v & kCountMask);
-        if (v & kFlagInc) break;
+    for (int t1 = tile - 1; t1 >= 0; t1 -= 8) {
+      uint32_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = t1 - u >= 0 ? ld_status(status + static_cast<int64_t>(t1 - u) * kBins + d) : kFlagInc;
+      bool done = false;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (done) break;
+        if (t1 - u < 0) {
+          done = true;
+          break;
+        }
+        while ((v[u] & (kFlagAgg | kFlagInc)) == 0u) v[u] = ld_status(status + static_cast<int64_t>(t1 - u) * kBins + d);
+        excl += static_cast<int>(v[u] & kCountMask);
+        done = (v[u] & kFlagInc) != 0u;
       }
-#ifdef MFB_SORT_DEBUG
-      if (d == 0 && blockIdx.x < 16) {
-        g_sort_dbg[4 * blockIdx.x] = tile;
-        g_sort_dbg[4 * blockIdx.x + 1] = excl;
-        g_sort_dbg[4 * blockIdx.x + 2] = static_cast<int>(first);
-        g_sort_dbg[4 * blockIdx.x + 3] = iters;
-      }
-#endif
-      st_status(status + static_cast<int64_t>(tile) * kBins + d, kFlagInc | static_cast<uint32_t>(excl + tot[k]));
+      if (done) break;
     }
+    st_status(status + static_cast<int64_t>(tile) * kBins + d, kFlagInc | static_cast<uint32_t>(excl + tot[k]));
     sm.out_off[d] = (k == 0 ? gb0 : gb1) + excl - sm.tile_start[d];
   }
   __syncthreads();

@@ -83,8 +83,12 @@ def launches(path: str) -> str:
 
 
 def full(path: str) -> dict:
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
-                         check=True).stdout
+    if path.endswith(".csv"):  # `ncu --metrics ... --csv --page raw --log-file` output
+        raw = open(path).read()
+        raw = raw[raw.index('"ID"'):] if '"ID"' in raw else raw
+    else:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True,
+                             check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     header, units = rows[0], rows[1]
     results = []

@@ -30,11 +30,15 @@ bvh.closest_points(q, p.max_distance_fraction * p.bbox_diagonal)
 bvh.surface_band(256, 1.0, 2)
 hits = np.zeros(p.dense.face_count(), np.int64)
 mv = p.dense.view()
-capi.check(ctx.lib.mf_cast_visibility(ctx.h, ctypes.byref(mv), 64, 1024, hits.ctypes.data_as(ctypes.c_void_p), None))
+capi.check(ctx.lib.mf_cast_visibility(ctx.h, ctypes.byref(mv), 8, 1024, hits.ctypes.data_as(ctypes.c_void_p), None))
+res = 24
+field = np.linspace(-1.0, 1.0, res ** 3, dtype=np.float32)
+bvh.sample_sdf(res, p.dense.positions.min(0) - 0.05, 1.3 / res, field, q[: 1 << 18])
 g = mf.rasterize_gbuffer(p.lowpoly, p.res)
 img = rng.integers(0, 255, (p.res, p.res, 3), dtype=np.uint8)
 mf.dilate_seams(img, g, 4)
 mf.dilate_seams(img, g, 40)
-bench.texfuse_bench(ctx, lo, p, 3)
+# texfuse: one fuseViews call (10 views at 1024^2 onto the 2048^2 G-buffer)
+bench.texfuse_bench(ctx, lo, p, 1, once=True)
 torch.cuda.synchronize()
 print("secondary kernels done")
