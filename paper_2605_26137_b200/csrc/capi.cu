@@ -465,7 +465,10 @@ void staged_h2d_start(Ctx& c, const std::vector<H2DPiece>& pieces, const char* t
     size_t len, soff;
     cudaStream_t s;
   };
-  constexpr size_t kChunk = 1 << 20;
+#ifndef MFB_STAGE_CHUNK_KB
+#define MFB_STAGE_CHUNK_KB 1024
+#endif
+  constexpr size_t kChunk = static_cast<size_t>(MFB_STAGE_CHUNK_KB) << 10;
   auto chunks = std::make_shared<std::vector<Chunk>>();
   size_t total = 0;
   for (const H2DPiece& p : pieces) {

@@ -30,7 +30,10 @@ constexpr int kDigitBits = 10;
 constexpr int kBins = 1 << kDigitBits;
 constexpr int kSortThreads = 512;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kPerLane = 16;                           // keys per thread
+#ifndef MFB_SORT_PER_LANE
+#define MFB_SORT_PER_LANE 16
+#endif
+constexpr int kPerLane = MFB_SORT_PER_LANE;            // keys per thread
 constexpr int kTile = kSortThreads * kPerLane;         // 8192 keys per tile
 constexpr int kWarpKeys = 32 * kPerLane;               // 512 keys per warp
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1u;
@@ -89,7 +92,7 @@ __device__ __forceinline__ void block_scan_pairs(int& lo, int& hi, int* carry) {
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kSortThreads, 2)
+__global__ void __launch_bounds__(kSortThreads, kPerLane <= 8 ? 3 : 2)
     k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                uint32_t* __restrict__ vout, int n, int shift, const int* __restrict__ ghist,
                uint32_t* __restrict__ status, int* __restrict__ tile_counter) {

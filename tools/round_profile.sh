@@ -20,3 +20,9 @@ timeout 1200 ncu --set full --clock-control none --import-source on \
   -k 'regex:k_transfer_t|k_raster|k_interp|k_refit_ranges|k_dilate_links' -c 5 \
   -o $OUT/${TAG}_prof -f python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-rays \
   > $OUT/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
+# per-kernel counters of every bake / secondary kernel (raw CSV) and the
+# CUPTI timelines of the device bake and of the host-buffer entry point
+TAG=$TAG bash tools/ncu_all.sh
+timeout 300 python tools/timeline.py B 7 2>/dev/null | grep -v Warn > $OUT/${TAG}_timeline_B.txt
+TL_E2E=1 timeout 300 python tools/timeline.py B 7 2>/dev/null | grep -v Warn > $OUT/${TAG}_timeline_e2e.txt
+TAG=$TAG bash tools/configs_run.sh

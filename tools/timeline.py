@@ -30,7 +30,25 @@ rgb = torch.empty((res, res, 3), dtype=torch.uint8, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 
+E2E = os.environ.get("TL_E2E") == "1"  # the host-buffer entry point (pinned inputs / output) instead
+if E2E:
+    import numpy as np
+
+    from paper_2605_26137_b200 import meshforge as mf
+
+    def _pin(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    hlo = mf.TriangleMesh(_pin(p.lowpoly.positions), _pin(p.lowpoly.faces), uvs=_pin(p.lowpoly.uvs),
+                          face_uvs=_pin(p.lowpoly.face_uvs))
+    hhi = mf.TriangleMesh(_pin(p.dense.positions), _pin(p.dense.faces))
+    hout = torch.empty((res, res, 3), dtype=torch.uint8).pin_memory().numpy()
+
+
 def bake():
+    if E2E:
+        mf.bake_normal_map(hlo, hhi, res, p.bbox_diagonal, p.max_distance_fraction, 4, out=hout, ctx=ctx)
+        return
     capi.check(ctx.lib.mf_bake_normal_map_dev(ctx.h, lo.h, hi.h, res, p.bbox_diagonal, p.max_distance_fraction, 4,
                                               0, res, rgb.data_ptr(), None))
 
