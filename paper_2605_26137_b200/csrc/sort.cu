@@ -26,6 +26,13 @@
 namespace mfb {
 namespace {
 
+#ifndef MFB_SORT_BALLOT
+#define MFB_SORT_BALLOT 1  // 10-ballot warp multi-split instead of __match_any_sync: 75.7 -> 65.5 us per 1M-key sort
+#endif
+#ifndef MFB_SORT_WIN
+#define MFB_SORT_WIN 8
+#endif
+constexpr int kWin = MFB_SORT_WIN;  // look-back status loads in flight per digit
 constexpr int kDigitBits = 10;
 constexpr int kBins = 1 << kDigitBits;
 constexpr int kSortThreads = 512;
@@ -122,7 +129,19 @@ __global__ void __launch_bounds__(kSortThreads, kPerLane <= 8 ? 3 : 2)
   for (int j = 0; j < kPerLane; ++j) {
     const bool live = key[j] != 0xffffffffu;
     const int d = live ? static_cast<int>((key[j] >> shift) & (kBins - 1)) : kBins;
+#if MFB_SORT_BALLOT
+    // warp multi-split: lanes with the same 10-bit digit by 10 ballots
+    unsigned peers = __ballot_sync(0xffffffffu, live);
+#pragma unroll
+    for (int b = 0; b < kDigitBits; ++b) {
+      const bool bit = (d >> b) & 1;
+      const unsigned m = __ballot_sync(0xffffffffu, bit);
+      peers &= bit ? m : ~m;
+    }
+    if (!live) peers = 1u << lane;
+#else
     const unsigned peers = __match_any_sync(0xffffffffu, d);
+#endif
     const int leader = __ffs(peers) - 1;
     int old = 0;
     if (live && lane == leader) {
@@ -168,14 +187,14 @@ __global__ void __launch_bounds__(kSortThreads, kPerLane <= 8 ? 3 : 2)
     // publishes its aggregate right after ranking, so no tile waits on a
     // serial chain of inclusive prefixes
     int excl = 0;
-    for (int t1 = tile - 1; t1 >= 0; t1 -= 8) {
-      uint32_t v[8];
+    for (int t1 = tile - 1; t1 >= 0; t1 -= kWin) {
+      uint32_t v[kWin];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int u = 0; u < kWin; ++u)
         v[u] = t1 - u >= 0 ? ld_status(status + static_cast<int64_t>(t1 - u) * kBins + d) : kFlagInc;
       bool done = false;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < kWin; ++u) {
         if (done) break;
         if (t1 - u < 0) {
           done = true;
