@@ -27,7 +27,7 @@ MF_HDRS := $(shell find include/meshforge -name '*.h' 2>/dev/null) include/eigen
 all: lib cpp peaks oracle
 
 lib: $(PKG)/libmfbake.so
-cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200 build/test_io_cpu build/bench_api
+cpp: $(PKG)/libmeshforge_b200.so build/test_bake_b200 build/test_io_cpu build/bench_api build/sort_check
 peaks: build/libmfpeaks.so
 
 build/cu/%.o: $(PKG)/csrc/%.cu $(CU_HDRS)
@@ -54,6 +54,11 @@ build/test_io_cpu: tests/cpp/test_io_cpu.cpp tests/cpp/doctest.h $(PKG)/libmeshf
 build/bench_api: tools/bench_api.cpp $(PKG)/libmeshforge_b200.so
 	@mkdir -p build
 	$(CXX) $(CXXFLAGS) -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
+# the LBVH radix sort against std::stable_sort (+ its timing); run by tests/test_gpu_sort.py
+build/sort_check: tools/sort_check.cu $(PKG)/libmfbake.so $(CU_HDRS)
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O2 -std=c++17 -Iinclude -Iinclude/eigen_shim $< -L$(PKG) -lmfbake -Xlinker -rpath,'$$ORIGIN/../$(PKG)' -o $@
 
 # L2 / FP64 microbenchmarks (tools/peaks.cu) used by bench.py for the roofline peaks
 build/libmfpeaks.so: tools/peaks.cu
