@@ -148,12 +148,17 @@ constexpr int kMaxFaces = 1 << 27;  // leaf refs encode first < 2^27 (leaf_ref)
 constexpr int kStackMax = 64;
 static_assert(kStackMax >= 30 + 27 + 1, "traversal stack must cover the deepest Karras tree");
 
+// Child boxes interleaved per coordinate, (left, right) pairs: each pair is
+// one f32x2 register pair after the node load, so the transfer walk bounds
+// both children with packed FADD2.RM / FFMA2.RM (query.cu box_lb2).
 struct alignas(16) BNode {
-  float4 a;  // L.min.x L.min.y L.min.z L.max.x
-  float4 b;  // L.max.y L.max.z R.min.x R.min.y
-  float4 c;  // R.min.z R.max.x R.max.y R.max.z
+  float4 a;  // L.min.x R.min.x L.min.y R.min.y
+  float4 b;  // L.min.z R.min.z L.max.x R.max.x
+  float4 c;  // L.max.y R.max.y L.max.z R.max.z
   int4 d;    // left ref, right ref, range first, range count
 };
+// float index of coordinate k (0..2 min xyz, 3..5 max xyz) of child `side`
+__host__ __device__ __forceinline__ int bnode_coord(int side, int k) { return 2 * k + side; }
 static_assert(sizeof(BNode) == 64, "node must be one 64-byte line segment");
 
 struct alignas(16) BTri {

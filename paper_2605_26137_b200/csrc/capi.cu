@@ -1855,8 +1855,8 @@ void export_bvh(mf_bvh* b) {
     }
     const BNode& n = nodes[it.ref];
     const float* f = reinterpret_cast<const float*>(&n);
-    Item l{n.d.x, {f[0], f[1], f[2], f[3], f[4], f[5]}, idx, 0, it.depth + 1};
-    Item r{n.d.y, {f[6], f[7], f[8], f[9], f[10], f[11]}, idx, 1, it.depth + 1};
+    Item l{n.d.x, {f[0], f[2], f[4], f[6], f[8], f[10]}, idx, 0, it.depth + 1};  // bnode_coord(0, k)
+    Item r{n.d.y, {f[1], f[3], f[5], f[7], f[9], f[11]}, idx, 1, it.depth + 1};  // bnode_coord(1, k)
     stack.push_back(r);  // left is visited (and numbered) first
     stack.push_back(l);
   }

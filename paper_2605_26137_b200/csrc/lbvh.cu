@@ -238,22 +238,19 @@ struct FBox {
 
 __device__ __forceinline__ void store_child_box(BNode* nd, int side, const FBox& b) {
   float* f = reinterpret_cast<float*>(nd);
-  const int o = side ? 6 : 0;
-  f[o + 0] = b.mn[0];
-  f[o + 1] = b.mn[1];
-  f[o + 2] = b.mn[2];
-  f[o + 3] = b.mx[0];
-  f[o + 4] = b.mx[1];
-  f[o + 5] = b.mx[2];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    f[bnode_coord(side, k)] = b.mn[k];
+    f[bnode_coord(side, 3 + k)] = b.mx[k];
+  }
 }
 __device__ __forceinline__ FBox load_child_box_cg(const BNode* nd, int side) {
   const float* f = reinterpret_cast<const float*>(nd);
-  const int o = side ? 6 : 0;
   FBox b;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    b.mn[k] = __ldcg(f + o + k);
-    b.mx[k] = __ldcg(f + o + 3 + k);
+    b.mn[k] = __ldcg(f + bnode_coord(side, k));
+    b.mx[k] = __ldcg(f + bnode_coord(side, 3 + k));
   }
   return b;
 }

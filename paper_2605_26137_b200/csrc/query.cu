@@ -78,6 +78,52 @@ __device__ __forceinline__ float box_lb(float mnx, float mny, float mnz, float m
   return __fmaf_rd(dz, dz, __fmaf_rd(dy, dy, __fmul_rd(dx, dx)));
 }
 
+// Both children's box lower bounds from one node (BNode's interleaved
+// (left, right) coordinate pairs) with packed f32x2 arithmetic: per axis two
+// FADD2.RM against the broadcast query coordinate, one FMNMX3 per child, then
+// FMUL2.RM + 2 FFMA2.RM - 15 instructions instead of box_lb's 24, the same
+// round-down operations in the same order (bit-identical bounds).
+typedef unsigned long long u64x;
+__device__ __forceinline__ u64x pk2(float lo, float hi) {
+  u64x r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk2(u64x v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ u64x sub_rd2(u64x a, u64x b) {
+  u64x r;
+  asm("sub.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64x mul_rd2(u64x a, u64x b) {
+  u64x r;
+  asm("mul.rm.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ u64x fma_rd2(u64x a, u64x b, u64x c) {
+  u64x r;
+  asm("fma.rm.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ void box_lb2(const float4& a, const float4& b, const float4& c, float3 q, float& lbL,
+                                        float& lbR) {
+  const u64x qx = pk2(q.x, q.x), qy = pk2(q.y, q.y), qz = pk2(q.z, q.z);
+  float l0, l1, h0, h1;
+  upk2(sub_rd2(pk2(a.x, a.y), qx), l0, l1);  // min - q
+  upk2(sub_rd2(qx, pk2(b.z, b.w)), h0, h1);  // q - max
+  const float dxL = fmaxf(fmaxf(l0, h0), 0.0f), dxR = fmaxf(fmaxf(l1, h1), 0.0f);
+  upk2(sub_rd2(pk2(a.z, a.w), qy), l0, l1);
+  upk2(sub_rd2(qy, pk2(c.x, c.y)), h0, h1);
+  const float dyL = fmaxf(fmaxf(l0, h0), 0.0f), dyR = fmaxf(fmaxf(l1, h1), 0.0f);
+  upk2(sub_rd2(pk2(b.x, b.y), qz), l0, l1);
+  upk2(sub_rd2(qz, pk2(c.z, c.w)), h0, h1);
+  const float dzL = fmaxf(fmaxf(l0, h0), 0.0f), dzR = fmaxf(fmaxf(l1, h1), 0.0f);
+  const u64x dx = pk2(dxL, dxR), dy = pk2(dyL, dyR), dz = pk2(dzL, dzR);
+  upk2(fma_rd2(dz, dz, fma_rd2(dy, dy, mul_rd2(dx, dx))), lbL, lbR);
+}
+
 // spatial/tri_geom.h:37-95 — same branch order, same expression order.
 __device__ __forceinline__ d3 closest_point_triangle(d3 p, d3 a, d3 b, d3 c, d3& bary) {
   const d3 ab = b - a, ac = c - a, ap = p - a;
@@ -210,8 +256,8 @@ __device__ __forceinline__ void traverse_closest(const BNode* __restrict__ nodes
       const float4* np = reinterpret_cast<const float4*>(nodes + ref);
       const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
       const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
-      const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qlo, qhi);
-      const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qlo, qhi);
+      const float lbL = box_lb(a.x, a.z, b.x, b.z, c.x, c.z, qlo, qhi);
+      const float lbR = box_lb(a.y, a.w, b.y, b.w, c.y, c.w, qlo, qhi);
       const bool hL = lbL <= bnd, hR = lbR <= bnd;
       if (hL && hR) {
         const bool lf = lbL <= lbR;
@@ -278,7 +324,7 @@ __device__ __forceinline__ void traverse_closest(const BNode* __restrict__ nodes
 #define MFB_TRI_BOX 0
 #endif
 #ifndef MFB_TRI_SEL
-#define MFB_TRI_SEL 0  // branchy form measured 2% faster in the per-thread walk
+#define MFB_TRI_SEL 1  // r02: branch-free form 0.994 vs 1.005 ms transfer (round 1 measured the branchy form 2% faster before the walk changes)
 #endif
 // L1 prefetch hints for the traversal (bit mask, compile-time):
 //   1 = a leaf's triangle lines when the leaf is entered (its 2-4 triangles
@@ -492,8 +538,8 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
           if (d.x >= 0) pf_l1(nodes + d.x);
           if (d.y >= 0) pf_l1(nodes + d.y);
         }
-        const float lbL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qf, qf);
-        const float lbR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qf, qf);
+        float lbL, lbR;
+        box_lb2(a, b, c, qf, lbL, lbR);
         const bool hL = lbL <= bnd, hR = lbR <= bnd;
         if (hL && hR) {
           const bool lf = lbL <= lbR;
@@ -722,8 +768,8 @@ __global__ void __launch_bounds__(128) k_raycast(const BNode* __restrict__ nodes
       const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
       const int4 dd = __ldg(reinterpret_cast<const int4*>(np + 3));
       double tl = 0.0, tr = 0.0;
-      const bool hl = slab(a.x, a.y, a.z, a.w, b.x, b.y, o, inv, tmin, limit, slack, tl);
-      const bool hr = slab(b.z, b.w, c.x, c.y, c.z, c.w, o, inv, tmin, limit, slack, tr);
+      const bool hl = slab(a.x, a.z, b.x, b.z, c.x, c.z, o, inv, tmin, limit, slack, tl);
+      const bool hr = slab(a.y, a.w, b.y, b.w, c.y, c.w, o, inv, tmin, limit, slack, tr);
       if (hl && hr) {
         const bool lf = tl <= tr;
         st[sp++] = lf ? dd.y : dd.x;
@@ -888,8 +934,8 @@ __device__ __forceinline__ bool any_leaf_within(const BNode* __restrict__ nodes,
     const float4* np = reinterpret_cast<const float4*>(nodes + ref);
     const float4 a = __ldg(np), b = __ldg(np + 1), c = __ldg(np + 2);
     const int4 d = __ldg(reinterpret_cast<const int4*>(np + 3));
-    const bool hL = box_lb(a.x, a.y, a.z, a.w, b.x, b.y, qlo, qhi) <= bnd;
-    const bool hR = box_lb(b.z, b.w, c.x, c.y, c.z, c.w, qlo, qhi) <= bnd;
+    const bool hL = box_lb(a.x, a.z, b.x, b.z, c.x, c.z, qlo, qhi) <= bnd;
+    const bool hR = box_lb(a.y, a.w, b.y, b.w, c.y, c.w, qlo, qhi) <= bnd;
     if ((hL && d.x < 0) || (hR && d.y < 0)) return true;
     if (hL && hR) {
       st[sp++] = d.y;
@@ -1047,8 +1093,8 @@ __global__ void __launch_bounds__(128) k_render_views(
       const float4 a = __ldg(np), b = __ldg(np + 1), cc = __ldg(np + 2);
       const int4 dd = __ldg(reinterpret_cast<const int4*>(np + 3));
       double tl = 0.0, tr = 0.0;
-      const bool hl = slab(a.x, a.y, a.z, a.w, b.x, b.y, o, inv, -INFINITY, limit, slack, tl);
-      const bool hr = slab(b.z, b.w, cc.x, cc.y, cc.z, cc.w, o, inv, -INFINITY, limit, slack, tr);
+      const bool hl = slab(a.x, a.z, b.x, b.z, cc.x, cc.z, o, inv, -INFINITY, limit, slack, tl);
+      const bool hr = slab(a.y, a.w, b.y, b.w, cc.y, cc.w, o, inv, -INFINITY, limit, slack, tr);
       if (hl && hr) {
         const bool lf = tl <= tr;
         st[sp++] = lf ? dd.y : dd.x;
