@@ -451,6 +451,8 @@ def texfuse_bench(ctx, lo, pair, steps, once=False):
         b.record(stream)
         b.synchronize()
         ts.append(a.elapsed_time(b))
+    if os.environ.get("MFB_TF_TRACE"):
+        print("texfuse call ms:", " ".join(f"{t:.3f}" for t in ts), file=sys.stderr)
     ms = statistics.median(ts)
     n_valid = int(gv.sum())
     n_filled = int(filled.sum())

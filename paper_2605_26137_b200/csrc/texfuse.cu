@@ -242,6 +242,48 @@ __device__ double trilinear(const MipChain& mc, double px, double py, double mip
   return (1.0 - f) * v0 + f * bilinear(mc, l1, (px + 0.5) * s1 - 0.5, (py + 0.5) * s1 - 0.5, ch);
 }
 
+// trilinear for all channels (up to kTfFastChannels) at once: the same
+// per-channel expressions as trilinear / bilinear, shared weights and offsets
+constexpr int kTfFastChannels = 4;
+__device__ void bilinear_all(const MipChain& mc, int l, double x, double y, double* out) {
+  const int w = mc.w[l], h = mc.h[l];
+  const float* im = mc.base + mc.off[l];
+  const double cx = clampd(x, 0.0, static_cast<double>(w - 1));
+  const double cy = clampd(y, 0.0, static_cast<double>(h - 1));
+  const int x0 = static_cast<int>(floor(cx));
+  const int y0 = static_cast<int>(floor(cy));
+  const int x1 = min(x0 + 1, w - 1);
+  const int y1 = min(y0 + 1, h - 1);
+  const double fx = cx - x0, fy = cy - y0;
+  const double gx = 1 - fx, gy = 1 - fy;
+  const float* p00 = im + (static_cast<int64_t>(y0) * w + x0) * mc.c;
+  const float* p10 = im + (static_cast<int64_t>(y0) * w + x1) * mc.c;
+  const float* p01 = im + (static_cast<int64_t>(y1) * w + x0) * mc.c;
+  const float* p11 = im + (static_cast<int64_t>(y1) * w + x1) * mc.c;
+#pragma unroll
+  for (int ch = 0; ch < kTfFastChannels; ++ch) {
+    if (ch >= mc.c) break;
+    const double v00 = p00[ch], v10 = p10[ch], v01 = p01[ch], v11 = p11[ch];
+    out[ch] = (v00 * gx + v10 * fx) * gy + (v01 * gx + v11 * fx) * fy;
+  }
+}
+__device__ void trilinear_all(const MipChain& mc, double px, double py, double mip, double* out) {
+  const int last = mc.n - 1;
+  const double m = clampd(mip, 0.0, static_cast<double>(last));
+  const int l0 = static_cast<int>(floor(m));
+  const int l1 = min(l0 + 1, last);
+  const double f = m - l0;
+  const double s0 = ldexp(1.0, -l0);
+  bilinear_all(mc, l0, (px + 0.5) * s0 - 0.5, (py + 0.5) * s0 - 0.5, out);
+  if (f == 0.0) return;
+  double v1[kTfFastChannels];
+  const double s1 = ldexp(1.0, -l1);
+  bilinear_all(mc, l1, (px + 0.5) * s1 - 0.5, (py + 0.5) * s1 - 0.5, v1);
+#pragma unroll
+  for (int ch = 0; ch < kTfFastChannels; ++ch)
+    if (ch < mc.c) out[ch] = (1.0 - f) * out[ch] + f * v1[ch];
+}
+
 struct Footprint {
   double ax = 1.0, ay = 0.0;  // major axis (unit)
   double major = 1.0;
@@ -335,14 +377,34 @@ __global__ void __launch_bounds__(128) k_backproject(int n, const float* __restr
   double jx0, jx1, jy0, jy1;
   if (diff(t + 1, t - 1, x + 1 < n, x > 0, jx0, jx1) && diff(t + n, t - n, y + 1 < n, y > 0, jy0, jy1))
     fp = footprint(jx0, jx1, jy0, jy1);
-  for (int ch = 0; ch < mc.c; ++ch) {
-    double acc = 0.0;
+  if (mc.c <= kTfFastChannels) {
+    // taps outer, channels inner: each tap's level pick, bilinear weights and
+    // addresses once for all channels (adjacent floats of one texel); every
+    // channel still accumulates its taps in order (bit-identical)
+    double acc[kTfFastChannels];
+#pragma unroll
+    for (int ch = 0; ch < kTfFastChannels; ++ch) acc[ch] = 0.0;
     for (int i = 0; i < fp.taps; ++i) {
       const double s = (i + 0.5) / fp.taps - 0.5;
       const double k = fp.major * s;
-      acc += trilinear(mc, px + fp.ax * k, py + fp.ay * k, fp.mip, ch);
+      double v[kTfFastChannels];
+      trilinear_all(mc, px + fp.ax * k, py + fp.ay * k, fp.mip, v);
+#pragma unroll
+      for (int ch = 0; ch < kTfFastChannels; ++ch) acc[ch] += v[ch];
     }
-    color[t * mc.c + ch] = static_cast<float>(acc / fp.taps);
+#pragma unroll
+    for (int ch = 0; ch < kTfFastChannels; ++ch)
+      if (ch < mc.c) color[t * mc.c + ch] = static_cast<float>(acc[ch] / fp.taps);
+  } else {
+    for (int ch = 0; ch < mc.c; ++ch) {
+      double acc = 0.0;
+      for (int i = 0; i < fp.taps; ++i) {
+        const double s = (i + 0.5) / fp.taps - 0.5;
+        const double k = fp.major * s;
+        acc += trilinear(mc, px + fp.ax * k, py + fp.ay * k, fp.mip, ch);
+      }
+      color[t * mc.c + ch] = static_cast<float>(acc / fp.taps);
+    }
   }
   sampled[t] = 1;
 }
@@ -375,19 +437,25 @@ __global__ void k_incidence(int n, const float* __restrict__ pos, const float* _
 // Per texel: the contributor terms l_k = log(prior_k) + alpha log(I_k) are
 // recomputed in each of the three passes (peak, denominator, colours) instead
 // of being stored, so any view count fits; the values are the same bits.
+constexpr int kParamViews = 64;
+struct BlendParams {
+  double lp[kParamViews];
+  uint8_t pos[kParamViews];
+};
 __global__ void k_blend(int k, int64_t n, int c, const float* __restrict__ colors, const uint8_t* __restrict__ sampled,
-                        const float* __restrict__ inc, const double* __restrict__ logp,
-                        const uint8_t* __restrict__ prior_pos, double alpha, double log_eps, float* __restrict__ out,
+                        const float* __restrict__ inc, const BlendParams bp, const double* __restrict__ logp_big,
+                        const uint8_t* __restrict__ pos_big, double alpha, double log_eps, float* __restrict__ out,
                         uint8_t* __restrict__ filled) {
   const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (t >= n) return;
   for (int ch = 0; ch < c; ++ch) out[t * c + ch] = 0.0f;
   filled[t] = 0;
   auto term = [&](int i, double& l) {
-    if (!sampled[i * n + t] || !prior_pos[i]) return false;
+    const bool ppos = i < kParamViews ? bp.pos[i] != 0 : pos_big[i] != 0;
+    if (!sampled[i * n + t] || !ppos) return false;
     const double iv = inc[i * n + t];
     if (iv <= 0.0) return false;
-    l = logp[i] + alpha * log(iv);
+    l = (i < kParamViews ? bp.lp[i] : logp_big[i]) + alpha * log(iv);
     return true;
   };
   int m = 0;
@@ -550,19 +618,30 @@ void tf_blend(Ctx& ctx, cudaStream_t s, int k, int64_t n, int c, const float* co
               const float* inc, const double* priors_host, double alpha, double epsilon, float* out,
               uint8_t* filled) {
   // log(prior) and log(epsilon) with the reference's own libm (fuse.cpp:246, :255)
-  std::vector<double> lp(k);
-  std::vector<uint8_t> pos(k);
-  for (int i = 0; i < k; ++i) {
-    pos[i] = priors_host[i] > 0.0 ? 1 : 0;
-    lp[i] = pos[i] ? std::log(priors_host[i]) : 0.0;
+  // log(prior) per view as a kernel parameter (no host -> device copy on the
+  // stream) for up to kParamViews views; more views go through device scratch
+  BlendParams bp{};
+  const int kp = std::min(k, kParamViews);
+  for (int i = 0; i < kp; ++i) {
+    bp.pos[i] = priors_host[i] > 0.0 ? 1 : 0;
+    bp.lp[i] = bp.pos[i] ? std::log(priors_host[i]) : 0.0;
   }
-  double* dlp = ctx.buf<double>("tf.logp", k);
-  uint8_t* dpos = ctx.buf<uint8_t>("tf.ppos", k);
-  // (pageable sources: staged before cudaMemcpyAsync returns)
-  MFB_CUDA_TRY(cudaMemcpyAsync(dlp, lp.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
-  MFB_CUDA_TRY(cudaMemcpyAsync(dpos, pos.data(), k, cudaMemcpyHostToDevice, s));
-  k_blend<<<blocks(n), kThreads, 0, s>>>(k, n, c, colors, sampled, inc, dlp, dpos, alpha, std::log(epsilon), out,
-                                         filled);
+  double* dlp = nullptr;
+  uint8_t* dpos = nullptr;
+  if (k > kParamViews) {
+    std::vector<double> lp(k);
+    std::vector<uint8_t> pos(k);
+    for (int i = 0; i < k; ++i) {
+      pos[i] = priors_host[i] > 0.0 ? 1 : 0;
+      lp[i] = pos[i] ? std::log(priors_host[i]) : 0.0;
+    }
+    dlp = ctx.buf<double>("tf.logp", k);
+    dpos = ctx.buf<uint8_t>("tf.ppos", k);
+    MFB_CUDA_TRY(cudaMemcpyAsync(dlp, lp.data(), sizeof(double) * k, cudaMemcpyHostToDevice, s));
+    MFB_CUDA_TRY(cudaMemcpyAsync(dpos, pos.data(), k, cudaMemcpyHostToDevice, s));
+  }
+  k_blend<<<blocks(n), kThreads, 0, s>>>(k, n, c, colors, sampled, inc, bp, dlp, dpos, alpha, std::log(epsilon),
+                                         out, filled);
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());
 }
