@@ -613,7 +613,13 @@ def run_ours(args, argv_mode, name):
     seed = fx.CONFIGS[name]["seed"] + (rank if mode == "replicas" else 0)
     pair = fx.config_pair(name, seed=seed)
     res = pair.res
-    stream = torch.cuda.current_stream()
+    # one non-default stream for everything timed here: the context launches
+    # on it, and the L2 flush, the CUDA events and torch's own work are issued
+    # on it too (torch's default stream would be handed to the library as
+    # NULL, and the context would then launch on a stream of its own that
+    # the events do not bracket)
+    stream = torch.cuda.Stream(device=d.device)
+    torch.cuda.set_stream(stream)
     ctx = capi.Context(d.device, stream.cuda_stream)
     lib = ctx.lib
     lo = capi.DeviceMesh(ctx, pair.lowpoly)

@@ -16,7 +16,8 @@ from paper_2605_26137_b200 import capi, fixtures as fx, meshforge as mf  # noqa:
 import bench  # noqa: E402
 
 p = fx.config_pair("B")
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)  # the context launches on it (the default stream would be NULL)
 ctx = capi.Context(0, stream.cuda_stream)
 lo = capi.DeviceMesh(ctx, p.lowpoly)
 hi = capi.DeviceMesh(ctx, p.dense)

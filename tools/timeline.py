@@ -22,7 +22,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "B"
 bakes = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 p = fx.config_pair(name)
 res = p.res
-stream = torch.cuda.current_stream()
+stream = torch.cuda.Stream()
+torch.cuda.set_stream(stream)  # the context launches on it (the default stream would be NULL)
 ctx = capi.Context(0, stream.cuda_stream)
 lo = capi.DeviceMesh(ctx, p.lowpoly)
 hi = capi.DeviceMesh(ctx, p.dense)
