@@ -32,7 +32,7 @@
 #define MFB_LOWPOLY_PRIO_DELTA 1  // lowpoly branch streams: this many levels below the LBVH's
 #endif
 #ifndef MFB_DN_PRIO
-#define MFB_DN_PRIO 1  // dense vertex normals: 0 lowest, 1 the lowpoly branch's level, 2 the LBVH's
+#define MFB_DN_PRIO 0  // dense vertex normals: 0 lowest, 1 the lowpoly branch's level, 2 the top level
 #endif
 
 namespace mfb {
@@ -1415,10 +1415,6 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     // streams get the higher priority so the lowpoly branches fill in around it
     int lo_prio = 0, hi_prio = 0;
     MFB_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-    // r02e: the dense vertex normals (needed by the transfer's epilogue) at
-    // the lowpoly branch's level, no longer the lowest: with the hand-written
-    // sort the LBVH chain ends ~170 us earlier and the normals, starved behind
-    // the raster, became the last pre-transfer item (1.406 -> 1.352 ms).
     // The lowpoly branch streams (wedge frames, reliability, raster) are high
     // priority as well as the LBVH's; the dense normals stay low. With the
     // segment-tree LBVH the lowpoly branch is the longer chain: 1.431 ->
@@ -1429,11 +1425,21 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     // LBVH chain (the long pole) now outranks the lowpoly branch, which
     // fills in around it.
     const int mid_prio = std::min(lo_prio, hi_prio + MFB_LOWPOLY_PRIO_DELTA);
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, hi_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux, cudaStreamNonBlocking, mid_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, hi_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, mid_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, mid_prio));
+    // r02 (per-step events on the context's stream): the lowpoly branch above
+    // the LBVH, the dense normals lowest: 1.428 ms per bake vs 1.437 (LBVH
+    // above) and 1.455-1.465 with the normals at the lowpoly branch's level;
+    // the pre-transfer phase is bound by the branches' total work, so the
+    // priorities move it by ~2% at most
+#ifndef MFB_PRIO_SWAP
+#define MFB_PRIO_SWAP 1
+#endif
+    const int lbvh_prio = MFB_PRIO_SWAP ? mid_prio : hi_prio;
+    const int low_prio = MFB_PRIO_SWAP ? hi_prio : mid_prio;
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, lbvh_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux, cudaStreamNonBlocking, low_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, lbvh_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, low_prio));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, low_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, MFB_DN_PRIO == 2 ? hi_prio : (MFB_DN_PRIO == 1 ? mid_prio : lo_prio)));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up1, cudaStreamNonBlocking, hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up2, cudaStreamNonBlocking, hi_prio));

@@ -150,7 +150,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // implicitly at exit. Measured on config B: early 1.390-1.394 ms per bake,
 // late 1.404-1.411, no PDL 1.409-1.414.
 #ifndef MFB_PDL_EARLY
-#define MFB_PDL_EARLY 1
+#define MFB_PDL_EARLY 0
 #endif
 #if MFB_PDL_EARLY
 #define PDL_TRIGGER_EARLY() pdl_trigger()
