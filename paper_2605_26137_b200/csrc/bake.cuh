@@ -202,7 +202,11 @@ struct Lbvh {
 
 // Build into buffers owned by `owner` scratch names prefixed with `tag`.
 // leaf_hint: leaf-range size cap (0 = kLeafMaxDefault); MFB_LEAF_MAX overrides.
-void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint = 0);
+// vflags (nullable, device): the mesh was uploaded without its validation
+// pass; the build checks validateMesh's conditions itself (bit 0 non-finite
+// coordinate, bit 1 face index out of range; bad indices zeroed in place).
+void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint = 0,
+                int* vflags = nullptr);
 // The descriptor lbvh_build fills (device buffers by scratch name), without
 // launching anything: used when a captured build is replayed.
 void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag);

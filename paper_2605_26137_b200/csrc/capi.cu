@@ -407,8 +407,11 @@ MeshLayout layout_mesh(Ctx& c, const mf_mesh_view* v, mf_mesh* mesh, const char*
 // the validation flags land in `*hflag` (pinned host memory) when `s`
 // reaches them. finish_upload() turns them into the mesh status after the
 // caller has synchronised.
+// defer: no validation pass and no flag read-back here: the caller's LBVH
+// build checks the mesh itself (lbvh_build's vflags = L.flags, zeroed here)
+// and reads the flags back after it.
 void copy_validate_async(Ctx& c, cudaStream_t s, const mf_mesh_view* v, const MeshLayout& L, DevMesh& m,
-                         int* hflag, cudaStream_t s2 = nullptr, bool staged = false) {
+                         int* hflag, cudaStream_t s2 = nullptr, bool staged = false, bool defer = false) {
   // with s2, the face indices travel on a second stream concurrently with
   // the positions (two H2D streams measured 25 -> 32 GB/s on the box)
   if (!staged) {
@@ -430,6 +433,7 @@ void copy_validate_async(Ctx& c, cudaStream_t s, const mf_mesh_view* v, const Me
     MFB_CUDA_TRY(cudaMemcpyAsync(L.fuv, v->face_uvs, sizeof(int32_t) * 3 * m.nf, cudaMemcpyHostToDevice, s));
   }
   c.fill(L.flags, 0, sizeof(int), s);
+  if (defer) return;
   const int64_t work = std::max<int64_t>(3ll * m.nv, 3ll * m.nf);
   if (work > 0) {
     const int grid = static_cast<int>(std::min<int64_t>(div_up(work, 256), kNumSMs * 16));
@@ -733,6 +737,10 @@ struct BakeEnq {
   RasterFused fo;
   Lbvh bvh;
   double* hiN = nullptr;
+  // host path: the dense mesh's validation runs inside its LBVH build
+  // (lbvh_build vflags); its flags are read back into dense_hflag after it
+  int* dense_vflags = nullptr;
+  int* dense_hflag = nullptr;
 
   // Dilation resolved before the transfer (full atlas, one output): the
   // raster and transfer write straight into rgb_out, the gutter texels are
@@ -859,11 +867,12 @@ struct BakeEnq {
     lbvh_layout(c, hi->m, bvh, "hi.bvh");
     hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
     const int64_t k[] = {reinterpret_cast<int64_t>(hi->m.pos), reinterpret_cast<int64_t>(hi->m.faces),
-                         reinterpret_cast<int64_t>(hi->m.nrm), hi->m.nf, hi->m.nv};
+                         reinterpret_cast<int64_t>(hi->m.nrm), hi->m.nf, hi->m.nv,
+                         reinterpret_cast<int64_t>(dense_vflags), reinterpret_cast<int64_t>(dense_hflag)};
     run_graphed(c, c.g_dense, side, key_bytes(k), graphs, [&] {
       MFB_CUDA_TRY(cudaEventRecord(c.dfork, side));
       mk.side0 = tm.mark(side);
-      lbvh_build(c, side, hi->m, bvh, "hi.bvh", bake_leaf_hint(frac, hi->m.nf));
+      lbvh_build(c, side, hi->m, bvh, "hi.bvh", bake_leaf_hint(frac, hi->m.nf), dense_vflags);
       mk.side1 = tm.mark(side);
       if (ns != side) {
         MFB_CUDA_TRY(cudaStreamWaitEvent(ns, c.dfork, 0));
@@ -934,6 +943,8 @@ struct BakeEnq {
       }
       MFB_CUDA_TRY(cudaEventRecord(c.join4, cp));
       MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join4, 0));
+      if (dense_vflags)  // (after the transfer: off the critical path)
+        MFB_CUDA_TRY(cudaMemcpyAsync(dense_hflag, dense_vflags, sizeof(int), cudaMemcpyDeviceToHost, s));
       MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
       MFB_CUDA_TRY(
           cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -954,6 +965,8 @@ struct BakeEnq {
         MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, static_cast<int64_t>(bpp) * (re - rb) * res,
                                      cudaMemcpyDeviceToHost, s));
     }
+    if (dense_vflags)
+      MFB_CUDA_TRY(cudaMemcpyAsync(dense_hflag, dense_vflags, sizeof(int), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
     MFB_CUDA_TRY(
         cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
@@ -1201,6 +1214,10 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
                      "stage.hi");
     pool_job.on = true;
   }
+  // Speculative dense phase (below): its validation is folded into the LBVH
+  // build (k_bounds / k_morton), so no validation pass and no flag read-back
+  // sit between the dense upload and the build
+  const bool spec = hv->n_faces > 0 && hv->n_vertices > 0 && diag > 0.0 && frac > 0.0 && radius >= 0;
   auto upload_hi = [&] {
     MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.fork, 0));
     if (staged) {
@@ -1209,9 +1226,10 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
       MFB_CUDA_TRY(cudaEventRecord(c.up2_done, c.up2));
       MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.up1_done, 0));
       MFB_CUDA_TRY(cudaStreamWaitEvent(c.side, c.up2_done, 0));
-      copy_validate_async(c, c.side, hv, hiL, hi.m, hup + 1, nullptr, true);
+      copy_validate_async(c, c.side, hv, hiL, hi.m, hup + 1, nullptr, true, spec);
     } else {
-      upload_mesh_async(c, c.side, hv, &hi, "up.hi", hup + 1, c.aux ? c.aux : nullptr);
+      hiL = layout_mesh(c, hv, &hi, "up.hi");
+      copy_validate_async(c, c.side, hv, hiL, hi.m, hup + 1, c.aux ? c.aux : nullptr, false, spec);
     }
     MFB_CUDA_TRY(cudaEventRecord(c.hi_ready, c.side));
   };
@@ -1282,9 +1300,10 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   // indices in the device copy), without a host round trip on the critical
   // path; the validation outcome is read after the bake, in the reference's
   // error order.
-  const bool spec = hv->n_faces > 0 && hv->n_vertices > 0 && diag > 0.0 && frac > 0.0 && radius >= 0;
   if (spec) {
     hi.status = MF_OK;  // provisional until the flags are read
+    q.dense_vflags = hiL.flags;
+    q.dense_hflag = hup + 1;
   } else {
     MFB_CUDA_TRY(cudaEventSynchronize(c.hi_ready));
     finish_upload(&hi, hup[1]);

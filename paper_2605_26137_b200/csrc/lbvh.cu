@@ -44,20 +44,26 @@ __host__ __device__ __forceinline__ double from_ordered(unsigned long long b) {
 // domain: it contains every centroid, and one streaming pass over the
 // positions is cheaper than gathering every face's corners), acc[6] = max
 // |vertex coord|
-__global__ void k_bounds(const double* __restrict__ pos, int nv, unsigned long long* acc) {
+// vflags (optional): validateMesh's non-finite-coordinate check
+// (mesh.cpp:37-48) on the way, bit 0 (the host path defers the mesh's
+// validation pass into the LBVH build)
+__global__ void k_bounds(const double* __restrict__ pos, int nv, unsigned long long* acc, int* vflags) {
   pdl_wait();
   PDL_TRIGGER_EARLY();
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
   double amax = 0.0;
+  bool bad = false;
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       const double c = pos[3 * v + k];
+      bad |= !isfinite(c);
       mn[k] = fmin(mn[k], c);
       mx[k] = fmax(mx[k], c);
       amax = fmax(amax, fabs(c));
     }
   }
+  if (vflags && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(vflags, 1);
   // warp reduce, then block reduce in shared memory, one atomic per block
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
@@ -115,7 +121,7 @@ __global__ void __launch_bounds__(kMortonThreads) k_morton(const double* __restr
                                                            const unsigned long long* __restrict__ acc,
                                                            uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
                                                            int* __restrict__ hist, uint32_t* __restrict__ status,
-                                                           int64_t status_words) {
+                                                           int64_t status_words, int nv, int* vflags) {
   pdl_wait();
   PDL_TRIGGER_EARLY();
   __shared__ int h[3 * 1024];
@@ -137,7 +143,19 @@ __global__ void __launch_bounds__(kMortonThreads) k_morton(const double* __restr
   for (int j = 0; j < kMortonPer; ++j) {
     const int f = f0 + j * kMortonThreads + threadIdx.x;
     if (f >= nf) break;
-    const int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+    int a = faces[3 * f], b = faces[3 * f + 1], c = faces[3 * f + 2];
+    if (vflags && (static_cast<unsigned>(a) >= static_cast<unsigned>(nv) ||
+                   static_cast<unsigned>(b) >= static_cast<unsigned>(nv) ||
+                   static_cast<unsigned>(c) >= static_cast<unsigned>(nv))) {
+      // validateMesh's face-index check (bit 1); the index is zeroed in the
+      // device copy so every later kernel stays in bounds (the bake's result
+      // is discarded: the host reports InvalidGeometry)
+      int32_t* fw = const_cast<int32_t*>(faces);
+      if (static_cast<unsigned>(a) >= static_cast<unsigned>(nv)) fw[3 * f] = a = 0;
+      if (static_cast<unsigned>(b) >= static_cast<unsigned>(nv)) fw[3 * f + 1] = b = 0;
+      if (static_cast<unsigned>(c) >= static_cast<unsigned>(nv)) fw[3 * f + 2] = c = 0;
+      atomicOr(vflags, 2);
+    }
     uint32_t q[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -652,7 +670,8 @@ void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag) 
   out.scene_acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
 }
 
-void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint) {
+void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint,
+                int* vflags) {
   const int n = m.nf;
   lbvh_layout(ctx, m, out, tag);
   auto* acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
@@ -683,9 +702,9 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   const int T = 256;
   const int grid_b = std::min(div_up(std::max(n, m.nv), T), kNumSMs * 8);
   // the chain up to the sort runs with programmatic dependent launch
-  launch_pdl(k_bounds, grid_b, T, 0, s, m.pos, m.nv, acc);
+  launch_pdl(k_bounds, grid_b, T, 0, s, m.pos, m.nv, acc, vflags);
   launch_pdl(k_morton, std::max(1, div_up(n, kMortonThreads * kMortonPer)), kMortonThreads, 0, s, m.pos, m.faces, n,
-             acc, keys, vals, hist, status, status_words);
+             acc, keys, vals, hist, status, status_words, m.nv, vflags);
   ctx.count_launch(2);
   // stable 3-pass radix sort (sort.cu): sorted pairs in keys2 / vals2
   SortArgs sa;

@@ -126,15 +126,25 @@ __global__ void k_vertex_sum(int nv, const int* __restrict__ start, const int* _
 // area vectors in face order, exactly as computeVertexNormals' face loop
 // (mesh.cpp:24-35).
 constexpr int kVnSlots = 16;
-__global__ void k_vn_slots(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf,
+__global__ void k_vn_slots(const double* __restrict__ pos, const int32_t* __restrict__ faces, int nf, int nv,
                            double* __restrict__ av, int* __restrict__ cnt, int* __restrict__ slots,
                            int* __restrict__ ovf, int ovf_cap) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nf) return;
-  d_face_area_vec(pos, faces, f, av);
+  // (indices clamped: on the host path this kernel runs beside the LBVH's
+  // Morton kernel, which validates and zeroes bad indices; the bake is then
+  // discarded with InvalidGeometry)
+  int t[3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
-    const int c = 3 * f + k, v = faces[c];
+    t[k] = faces[3 * f + k];
+    if (static_cast<unsigned>(t[k]) >= static_cast<unsigned>(nv)) t[k] = 0;
+  }
+  const d3 p0 = ld3(pos + 3 * t[0]), p1 = ld3(pos + 3 * t[1]), p2 = ld3(pos + 3 * t[2]);
+  st3(av + 3 * f, 0.5 * cross(p1 - p0, p2 - p0));  // faceAreaVector, mesh.h:28-31
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int c = 3 * f + k, v = t[k];
     const int s = atomicAdd(&cnt[v], 1);
     if (s < kVnSlots) {
       slots[static_cast<int64_t>(v) * kVnSlots + s] = c;
@@ -1261,7 +1271,7 @@ void vertex_normals(Ctx& ctx, cudaStream_t s, const DevMesh& m, double* out, boo
   double* av = ctx.buf<double>(tag + ".vn.av", 3 * static_cast<size_t>(m.nf));
   ctx.fill(cnt, 0, sizeof(int) * (m.nv + 1), s);
   ctx.fill(ovf, 0, sizeof(int), s);
-  k_vn_slots<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, av, cnt, slots, ovf, ovf_cap);
+  k_vn_slots<<<div_up(m.nf, T), T, 0, s>>>(m.pos, m.faces, m.nf, m.nv, av, cnt, slots, ovf, ovf_cap);
   k_vn_sum<<<div_up(m.nv, T), T, 0, s>>>(m.nv, cnt, slots, ovf, av, out, renorm ? 1 : 0);
   ctx.count_launch(2);
   MFB_CUDA_TRY(cudaGetLastError());
