@@ -193,6 +193,7 @@ struct Lbvh {
   BTri* tris = nullptr;     // device, leaf order
   TBox* tbox = nullptr;     // device, leaf order
   int32_t root_ref = 0;     // 0 (internal root) or a leaf ref when n_tris <= kLeafMax... see build
+  int leaf_max = kLeafMaxDefault;  // leaf-range cap the build used
   float root_box[6];        // host copy not needed for traversal; kept for export
   float* root_box_dev = nullptr;
   // [min c, max c, max |coord|] as ordered-int doubles (device); the
@@ -209,7 +210,8 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
                 int* vflags = nullptr);
 // The descriptor lbvh_build fills (device buffers by scratch name), without
 // launching anything: used when a captured build is replayed.
-void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag);
+void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint = 0);
+int lbvh_leaf_max(int leaf_hint);
 
 // ---------------------------------------------------------------- lowpoly prep + raster
 // computeVertexNormals (mesh.cpp:24-35) followed, when `renorm`, by the

@@ -864,7 +864,7 @@ struct BakeEnq {
   // then c.join / c.join3 mark its end for tail().
   void dense_side(bool graphs) {
     cudaStream_t side = c.side, ns = c.dn ? c.dn : (c.aux ? c.aux : c.side);
-    lbvh_layout(c, hi->m, bvh, "hi.bvh");
+    lbvh_layout(c, hi->m, bvh, "hi.bvh", bake_leaf_hint(frac, hi->m.nf));
     hiN = c.buf<double>("hi.unitN", 3 * static_cast<size_t>(hi->m.nv));
     const int64_t k[] = {reinterpret_cast<int64_t>(hi->m.pos), reinterpret_cast<int64_t>(hi->m.faces),
                          reinterpret_cast<int64_t>(hi->m.nrm), hi->m.nf, hi->m.nv,

@@ -653,7 +653,20 @@ __global__ void k_refit_ranges(const TBox* __restrict__ tbox, const BNode* __res
 
 }  // namespace
 
-void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag) {
+// Leaf-range cap of a build: the caller's hint or kLeafMaxDefault (the
+// reference uses 4, bvh.cpp:13; results are tree-independent) unless
+// MFB_LEAF_MAX (1..15) overrides it.
+int lbvh_leaf_max(int leaf_hint) {
+  static const int leaf_env = [] {
+    const char* e = std::getenv("MFB_LEAF_MAX");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 1 && v <= kLeafCountMax ? v : 0;
+  }();
+  return leaf_env ? leaf_env : (leaf_hint >= 1 && leaf_hint <= kLeafCountMax ? leaf_hint : kLeafMaxDefault);
+}
+
+void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint) {
+  out.leaf_max = lbvh_leaf_max(leaf_hint);
   const int n = m.nf;
   // leaf refs hold first < 2^27 (bake.cuh), which also bounds the traversal
   // stacks: a root-to-leaf path's Karras deltas strictly increase over the 30
@@ -673,7 +686,7 @@ void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag) 
 void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint,
                 int* vflags) {
   const int n = m.nf;
-  lbvh_layout(ctx, m, out, tag);
+  lbvh_layout(ctx, m, out, tag, leaf_hint);
   auto* acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
   auto* keys = ctx.buf<uint32_t>(tag + ".keys", n);
   auto* keys2 = ctx.buf<uint32_t>(tag + ".keys2", n);
@@ -718,16 +731,7 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   sa.counters = hist + 3 * 1024;
   radix_sort_morton30(ctx, s, sa);
 
-  // Leaf size: the caller's hint or kLeafMaxDefault (the reference uses 4,
-  // bvh.cpp:13; results are tree-independent) unless MFB_LEAF_MAX (1..15)
-  // overrides it.
-  static const int leaf_env = [] {
-    const char* e = std::getenv("MFB_LEAF_MAX");
-    const int v = e ? std::atoi(e) : 0;
-    return v >= 1 && v <= kLeafCountMax ? v : 0;
-  }();
-  const int leaf_max = leaf_env ? leaf_env
-                                : (leaf_hint >= 1 && leaf_hint <= kLeafCountMax ? leaf_hint : kLeafMaxDefault);
+  const int leaf_max = out.leaf_max = lbvh_leaf_max(leaf_hint);
   // repack (gathers) and emit (key searches) both need only the sorted
   // keys / ids: repack runs on the context's helper stream alongside emit
   cudaStream_t rs = ctx.side2 ? ctx.side2 : s;

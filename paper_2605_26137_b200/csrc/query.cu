@@ -324,7 +324,11 @@ __device__ __forceinline__ void traverse_closest(const BNode* __restrict__ nodes
 #define MFB_TRI_BOX 0
 #endif
 #ifndef MFB_TRI_SEL
-#define MFB_TRI_SEL 1  // r02: branch-free form 0.994 vs 1.005 ms transfer (round 1 measured the branchy form 2% faster before the walk changes)
+// The triangle test's form per bake (template kSel of k_transfer_t): the
+// branch-free one for leaves of <= 3 triangles (config B transfer 0.994 vs
+// 1.005 ms), the branchy one for the larger leaves of a wide search
+// (config E, leaves up to 11: 49.2 vs 54.6 ms). MFB_TRI_SEL=0/1 forces one.
+#define MFB_TRI_SEL 2
 #endif
 // L1 prefetch hints for the traversal (bit mask, compile-time):
 //   1 = a leaf's triangle lines when the leaf is entered (its 2-4 triangles
@@ -450,7 +454,7 @@ __global__ void k_band_init(BandSync bs) {
 #endif
 // kBands: the row-band publication of the host path's overlapped download
 // (compiled only into that instantiation: it costs the walk registers)
-template <bool kDebug, bool kProf, int kPass = 0, bool kBands = false>
+template <bool kDebug, bool kProf, int kPass = 0, bool kBands = false, bool kSel = true>
 __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
     const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
@@ -579,11 +583,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         load_tri(tris + k, A, B, C, face);
         d3 bary;
         const d3 ql = q;
-#if MFB_TRI_SEL
-        const d3 pt = closest_point_triangle_sel(ql, A, B, C, bary);
-#else
-        const d3 pt = closest_point_triangle(ql, A, B, C, bary);
-#endif
+        const d3 pt = kSel ? closest_point_triangle_sel(ql, A, B, C, bary) : closest_point_triangle(ql, A, B, C, bary);
         const double ds = sqnorm(pt - ql);
         if (ds < best.d || (ds == best.d && face < best.face)) {
           best.d = ds;
@@ -1291,12 +1291,22 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
   if (kSeedPasses) ctx.fill(a.face_map, 0xff, sizeof(int) * a.face_map_size, s);
   static const int bps = occupancy(k_transfer_t<false, false>);
   const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
+  const bool sel = MFB_TRI_SEL == 2 ? bvh.leaf_max <= 3 : MFB_TRI_SEL != 0;
 #define MFB_XFER_T(D, P, PASS)                                                                                \
-  k_transfer_t<D, P, PASS><<<g2, 128, 0, s>>>(bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos,        \
-                                              a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces, a.max_dist, a.rgb, \
-                                              D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf, \
-                                              a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions,  \
-                                              bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt)
+  do {                                                                                                        \
+    if (sel)                                                                                                  \
+      k_transfer_t<D, P, PASS, false, true><<<g2, 128, 0, s>>>(                                               \
+          bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
+          a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
+          a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions, bvh.tbox, a.dep_head, a.dep_next,     \
+          a.bands, a.fmt);                                                                                    \
+    else                                                                                                      \
+      k_transfer_t<D, P, PASS, false, false><<<g2, 128, 0, s>>>(                                              \
+          bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
+          a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
+          a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions, bvh.tbox, a.dep_head, a.dep_next,     \
+          a.bands, a.fmt);                                                                                    \
+  } while (0)
 #define MFB_XFER_TP(PASS)                                               \
   if (prof) {                                                           \
     if (dbg) MFB_XFER_T(true, true, PASS); else MFB_XFER_T(false, true, PASS); \
@@ -1308,10 +1318,16 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     MFB_XFER_TP(2);
     ctx.count_launch();
   } else if (a.bands.done) {
-    k_transfer_t<false, false, 0, true><<<g2, 128, 0, s>>>(
-        bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
-        a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
-        a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt);
+    if (sel)
+      k_transfer_t<false, false, 0, true, true><<<g2, 128, 0, s>>>(
+          bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
+          a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
+          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt);
+    else
+      k_transfer_t<false, false, 0, true, false><<<g2, 128, 0, s>>>(
+          bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
+          a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
+          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt);
   } else {
     MFB_XFER_TP(0);
   }
