@@ -7,5 +7,5 @@ for c in A C E; do
   timeout 900 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_cfg_$c.json 2> gpurun_out/${TAG}_cfg_$c.err
   echo "config $c rc=$?"
 done
-timeout 900 python bench.py --config D --assets 8 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_cfg_D8.json 2> gpurun_out/${TAG}_cfg_D8.err
+timeout 900 python bench.py --config D --mode batch --assets 8 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_cfg_D8.json 2> gpurun_out/${TAG}_cfg_D8.err
 echo "config D rc=$?"
