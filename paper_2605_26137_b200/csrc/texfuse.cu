@@ -438,6 +438,7 @@ __global__ void k_incidence(int n, const float* __restrict__ pos, const float* _
 // recomputed in each of the three passes (peak, denominator, colours) instead
 // of being stored, so any view count fits; the values are the same bits.
 constexpr int kParamViews = 64;
+constexpr int kBlendCache = 16;  // views whose blend terms stay in registers
 struct BlendParams {
   double lp[kParamViews];
   uint8_t pos[kParamViews];
@@ -458,6 +459,38 @@ __global__ void k_blend(int k, int64_t n, int c, const float* __restrict__ color
     l = (i < kParamViews ? bp.lp[i] : logp_big[i]) + alpha * log(iv);
     return true;
   };
+  if (k <= kBlendCache) {
+    // up to kBlendCache views: the contributor terms and weights computed once
+    // and kept in registers (the same values as the recomputing path below)
+    double lt[kBlendCache], wt[kBlendCache];
+    int who[kBlendCache];
+    int m = 0;
+    double peak = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kBlendCache; ++i) {
+      if (i >= k) break;
+      double l;
+      if (!term(i, l)) continue;
+      lt[m] = l;
+      who[m] = i;
+      peak = peak < l ? l : peak;  // std::max(peak, l)
+      ++m;
+    }
+    if (m == 0) return;
+    double sum = 0.0;
+    for (int j = 0; j < m; ++j) sum += exp(lt[j] - peak);
+    const double log_denom = peak + log(sum);
+    if (!(log_denom > log_eps)) return;
+    const double shrink = 1.0 / (1.0 + exp(log_eps - log_denom));
+    for (int j = 0; j < m; ++j) wt[j] = exp(lt[j] - log_denom);
+    for (int ch = 0; ch < c; ++ch) {
+      double acc = 0.0;
+      for (int j = 0; j < m; ++j) acc += wt[j] * static_cast<double>(colors[(who[j] * n + t) * c + ch]);
+      out[t * c + ch] = static_cast<float>(acc * shrink);
+    }
+    filled[t] = 1;
+    return;
+  }
   int m = 0;
   double peak = -INFINITY;
   for (int i = 0; i < k; ++i) {

@@ -40,10 +40,13 @@ if E2E:
     def _pin(a):
         return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
 
-    hlo = mf.TriangleMesh(_pin(p.lowpoly.positions), _pin(p.lowpoly.faces), uvs=_pin(p.lowpoly.uvs),
-                          face_uvs=_pin(p.lowpoly.face_uvs))
-    hhi = mf.TriangleMesh(_pin(p.dense.positions), _pin(p.dense.faces))
-    hout = torch.empty((res, res, 3), dtype=torch.uint8).pin_memory().numpy()
+    if os.environ.get("TL_PAGEABLE") == "1":  # numpy (pageable) inputs and output
+        hlo, hhi, hout = p.lowpoly, p.dense, np.zeros((res, res, 3), np.uint8)
+    else:
+        hlo = mf.TriangleMesh(_pin(p.lowpoly.positions), _pin(p.lowpoly.faces), uvs=_pin(p.lowpoly.uvs),
+                              face_uvs=_pin(p.lowpoly.face_uvs))
+        hhi = mf.TriangleMesh(_pin(p.dense.positions), _pin(p.dense.faces))
+        hout = torch.empty((res, res, 3), dtype=torch.uint8).pin_memory().numpy()
 
 
 def bake():
