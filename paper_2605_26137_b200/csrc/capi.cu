@@ -125,7 +125,29 @@ __global__ void k_fill(uint32_t* __restrict__ w, size_t nw, uint32_t v, uint8_t*
   for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nw; i += stride) w[i] = v;
   if (blockIdx.x == 0 && static_cast<int>(threadIdx.x) < ntail) tail[threadIdx.x] = static_cast<uint8_t>(v);
 }
+// After the transfer: the bake's flags and counters and the dense mesh's
+// validation flag stored straight into the pinned host words (UVA: a
+// cudaMallocHost pointer is a device pointer), and every band's ready flag
+// released - one launch in place of a fill and three small copies, each of
+// which costs a copy-engine round trip on the tail of the bake.
+__global__ void k_finish(const int* __restrict__ flags, const unsigned long long* __restrict__ counters,
+                         const int* __restrict__ dense_vflags, int* hflags, unsigned long long* hcnt,
+                         int* dense_hflag, int* ready, int nb) {
+  const int t = threadIdx.x;
+  if (t < 4) hflags[t] = flags[t];
+  else if (t < 8) hcnt[t - 4] = counters[t - 4];
+  else if (t == 8 && dense_vflags) *dense_hflag = *dense_vflags;
+  for (int b = t; b < nb; b += blockDim.x) ready[b] = 1;
+}
 }  // namespace
+
+void finish_flags(Ctx& c, cudaStream_t s, const int* flags, const unsigned long long* counters,
+                  const int* dense_vflags, int* hflags, unsigned long long* hcnt, int* dense_hflag, int* ready,
+                  int nb) {
+  k_finish<<<1, 64, 0, s>>>(flags, counters, dense_vflags, hflags, hcnt, dense_hflag, ready, nb);
+  c.count_launch();
+  MFB_CUDA_TRY(cudaGetLastError());
+}
 
 void Ctx::fill(void* p, int value, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return;
@@ -717,6 +739,16 @@ void stream_wait_value(cudaStream_t s, int* flag) {
     throw ApiError(MF_ERR_CUDA, "cuStreamWaitValue32 failed");
 }
 
+// Bands downloaded in one copy behind the transfer instead of on the band
+// stream (MFB_TAIL_BANDS, default 2; never all of them).
+int tail_bands(int nb) {
+  static const int k = [] {
+    const char* e = std::getenv("MFB_TAIL_BANDS");
+    return e ? std::max(0, std::atoi(e)) : 2;
+  }();
+  return std::min(k, nb - 1);
+}
+
 // The bake's three phases. enqueue_bake() chains them with a fork/join (the
 // captured graph); the host-buffer entry point interleaves its own upload and
 // validation wait between them (bake_host_overlapped).
@@ -917,7 +949,7 @@ struct BakeEnq {
     cudaStream_t cp = c.aux2 ? c.aux2 : s;
     if (links && band_sync && host_out && cp != s) {
       // each band's download waits (on cp) for its ready flag, set by the
-      // transfer's warps; the memset after the transfer releases every wait
+      // transfer's warps; k_finish after the transfer releases every wait
       // regardless (by then every band is final), so no wait outlives it
       ta.bands = bs;
       cudaEvent_t ev = c.pool_event(40);
@@ -930,10 +962,24 @@ struct BakeEnq {
       if (band_check) {
         MFB_CUDA_TRY(cudaMemcpyAsync(band_check, bs.ready, bs.nb * sizeof(int), cudaMemcpyDeviceToHost, s));
       }
-      c.fill(bs.ready, 1, bs.nb * sizeof(int), s);
+      // the last bands complete with the transfer itself: one copy on s right
+      // behind it (each wait-value node on cp costs ~7 us even when already
+      // satisfied, which is what the copies after the transfer paid)
       mk.e5 = tm.mark(s);
+      // (k_finish first: it runs while the band stream's last copy still
+      // holds the copy engine)
+      finish_flags(c, s, flags, counters, dense_vflags, hflags_pinned, hcnt_pinned, dense_hflag, bs.ready, bs.nb);
+      const int nstream = bs.nb - tail_bands(bs.nb);
+      if (nstream < bs.nb) {
+        const int64_t off = static_cast<int64_t>(bpp) * nstream * bs.rows * res;
+        MFB_CUDA_TRY(cudaMemcpyAsync(host_out + off, rgb_out + off,
+                                     static_cast<int64_t>(bpp) * (res - nstream * bs.rows) * res,
+                                     cudaMemcpyDeviceToHost, s));
+        if (band_ev_base >= 0)
+          for (int b = nstream; b < bs.nb; ++b) MFB_CUDA_TRY(cudaEventRecord(c.pool_event(band_ev_base + b), s));
+      }
       MFB_CUDA_TRY(cudaStreamWaitEvent(cp, ev, 0));
-      for (int b = 0; b < bs.nb; ++b) {
+      for (int b = 0; b < nstream; ++b) {
         const int r0 = b * bs.rows, r1 = std::min(res, r0 + bs.rows);
         stream_wait_value(cp, bs.ready + b);
         const int64_t off = static_cast<int64_t>(bpp) * r0 * res;
@@ -943,11 +989,6 @@ struct BakeEnq {
       }
       MFB_CUDA_TRY(cudaEventRecord(c.join4, cp));
       MFB_CUDA_TRY(cudaStreamWaitEvent(s, c.join4, 0));
-      if (dense_vflags)  // (after the transfer: off the critical path)
-        MFB_CUDA_TRY(cudaMemcpyAsync(dense_hflag, dense_vflags, sizeof(int), cudaMemcpyDeviceToHost, s));
-      MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-      MFB_CUDA_TRY(
-          cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
       return;
     }
     transfer_normals(c, s, bvh, ta);
@@ -965,11 +1006,7 @@ struct BakeEnq {
         MFB_CUDA_TRY(cudaMemcpyAsync(host_out, rgb_out, static_cast<int64_t>(bpp) * (re - rb) * res,
                                      cudaMemcpyDeviceToHost, s));
     }
-    if (dense_vflags)
-      MFB_CUDA_TRY(cudaMemcpyAsync(dense_hflag, dense_vflags, sizeof(int), cudaMemcpyDeviceToHost, s));
-    MFB_CUDA_TRY(cudaMemcpyAsync(hflags_pinned, flags, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
-    MFB_CUDA_TRY(
-        cudaMemcpyAsync(hcnt_pinned, counters, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    finish_flags(c, s, flags, counters, dense_vflags, hflags_pinned, hcnt_pinned, dense_hflag, nullptr, 0);
   }
 };
 
