@@ -186,7 +186,23 @@ __host__ __device__ __forceinline__ void leaf_decode(int32_t ref, int& first, in
 }
 
 
+// Per-triangle fp32 containment planes, leaf order (built only for wide
+// leaves, Lbvh::tplane): a unit normal n with the slab lo <= n.x <= hi and,
+// per edge, an in-plane outward unit vector m with the half-space m.x <= o,
+// every one holding all three vertices (bounds evaluated in f64 from the
+// rounded fp32 n / m, then rounded outward). Hence for any point q
+// dist(q, T)^2 >= max(0, lo - n.q, n.q - hi)^2 + max(0, max_e m_e.q - o_e)^2
+// up to the fp32 evaluation error and the rounded vectors' 1e-7 departure from
+// unit length / orthogonality, both covered by the caller's slack.
+constexpr int kPlaneLeafMin = 4;  // leaf caps from which the pre-test is built
+struct alignas(16) TPlane {
+  float4 m0, m1, m2;  // (m_e, o_e)
+  float4 n;           // (n, lo)
+  float4 hi;          // (hi, -, -, -)
+};
+
 struct Lbvh {
+  TPlane* tplane = nullptr;  // device, leaf order, or null (see TPlane)
   int n_tris = 0;
   int n_nodes = 0;          // internal nodes (n_tris - 1), root = node 0 when n_tris > 1
   BNode* nodes = nullptr;   // device

@@ -275,9 +275,65 @@ __device__ __forceinline__ FBox load_child_box_cg(const BNode* nd, int side) {
 
 // Gathers each primitive's f64 vertices into leaf order and its outward-
 // rounded fp32 box (fully parallel; random reads, coalesced writes).
+// The containment planes of one triangle (TPlane): directions in f64,
+// rounded to fp32, and the vertex bounds evaluated in f64 with those fp32
+// directions, rounded outward. Degenerate triangles get zero vectors (their
+// lower bound is 0: never skipped).
+__device__ __forceinline__ double dot_f(const float4& m, const double* v) {
+  return (static_cast<double>(m.x) * v[0] + static_cast<double>(m.y) * v[1]) + static_cast<double>(m.z) * v[2];
+}
+__device__ void tri_planes(const double* v, TPlane& tp) {
+  const double e1[3] = {v[3] - v[0], v[4] - v[1], v[5] - v[2]};
+  const double e2[3] = {v[6] - v[0], v[7] - v[1], v[8] - v[2]};
+  double nn[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+  const double len = sqrt(nn[0] * nn[0] + nn[1] * nn[1] + nn[2] * nn[2]);
+  const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (!(len > 0.0) || !isfinite(len)) {
+    tp.m0 = tp.m1 = tp.m2 = tp.n = tp.hi = zero;
+    return;
+  }
+  float4 n4 = make_float4(static_cast<float>(nn[0] / len), static_cast<float>(nn[1] / len),
+                          static_cast<float>(nn[2] / len), 0.f);
+  const double nf[3] = {n4.x, n4.y, n4.z};
+  double lo = INFINITY, hi = -INFINITY;
+  for (int c = 0; c < 3; ++c) {
+    const double t = dot_f(n4, v + 3 * c);
+    lo = fmin(lo, t);
+    hi = fmax(hi, t);
+  }
+  n4.w = __double2float_rd(lo);
+  tp.n = n4;
+  tp.hi = make_float4(__double2float_ru(hi), 0.f, 0.f, 0.f);
+  float4* ms[3] = {&tp.m0, &tp.m1, &tp.m2};
+  for (int e = 0; e < 3; ++e) {
+    const double* a = v + 3 * e;
+    const double* b = v + 3 * ((e + 1) % 3);
+    const double d[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+    // in-plane direction perpendicular to the edge: d x n (f64, from the fp32 n)
+    double m[3] = {d[1] * nf[2] - d[2] * nf[1], d[2] * nf[0] - d[0] * nf[2], d[0] * nf[1] - d[1] * nf[0]};
+    const double ml = sqrt(m[0] * m[0] + m[1] * m[1] + m[2] * m[2]);
+    if (!(ml > 0.0) || !isfinite(ml)) {
+      *ms[e] = zero;
+      continue;
+    }
+    float4 m4 = make_float4(static_cast<float>(m[0] / ml), static_cast<float>(m[1] / ml),
+                            static_cast<float>(m[2] / ml), 0.f);
+    const double* opp = v + 3 * ((e + 2) % 3);
+    if (dot_f(m4, opp) > dot_f(m4, a)) {  // outward: away from the opposite vertex
+      m4.x = -m4.x;
+      m4.y = -m4.y;
+      m4.z = -m4.z;
+    }
+    double o = -INFINITY;
+    for (int c = 0; c < 3; ++c) o = fmax(o, dot_f(m4, v + 3 * c));
+    m4.w = __double2float_ru(o);
+    *ms[e] = m4;
+  }
+}
+
 __global__ void k_repack(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                          const uint32_t* __restrict__ order, int n, BTri* __restrict__ tris,
-                         TBox* __restrict__ tbox) {
+                         TBox* __restrict__ tbox, TPlane* __restrict__ tplane) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const int f = static_cast<int>(order[p]);
@@ -307,6 +363,11 @@ __global__ void k_repack(const double* __restrict__ pos, const int32_t* __restri
   for (int q = 0; q < 5; ++q) dst[q] = src[q];
   tbox[p].a = make_float4(box.mn[0], box.mn[1], box.mn[2], box.mx[0]);
   tbox[p].b = make_float4(box.mx[1], box.mx[2], 0.f, 0.f);
+  if (tplane) {
+    TPlane tp;
+    tri_planes(t.v, tp);
+    tplane[p] = tp;
+  }
 }
 
 // ---- node boxes from a segment tree over the leaf-order triangle boxes -----
@@ -379,40 +440,6 @@ __device__ __forceinline__ void seg_reduce_block(FBox box, unsigned base, int cn
     fbox_union(box, fbox_shfl_down(box, 1 << (lv - 6)));
     if ((lane & ((1 << (lv - 5)) - 1)) == 0 && lane < nw) fbox_store(seg + ((base + 32u * lane) >> lv), box);
   }
-}
-
-// Gathers each primitive's f64 vertices into leaf order and its outward-
-// rounded fp32 box, and builds the segment tree's first 10 levels.
-__global__ void __launch_bounds__(1024) k_repack_seg(const double* __restrict__ pos, const int32_t* __restrict__ faces,
-                                                     const uint32_t* __restrict__ order, int n, int N,
-                                                     BTri* __restrict__ tris, TBox* __restrict__ tbox,
-                                                     TBox* __restrict__ seg) {
-  __shared__ FBox sm[32];
-  const int p = blockIdx.x * 1024 + threadIdx.x;
-  FBox box = fbox_empty();
-  if (p < n) {
-    const int f = static_cast<int>(order[p]);
-    const int vi[3] = {faces[3 * f], faces[3 * f + 1], faces[3 * f + 2]};
-    BTri t;
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const double x = pos[3 * vi[c] + k];
-        t.v[3 * c + k] = x;
-        box.mn[k] = fminf(box.mn[k], __double2float_rd(x));
-        box.mx[k] = fmaxf(box.mx[k], __double2float_ru(x));
-      }
-    }
-    t.face = f;
-    t.pad = 0;
-    const double2* src = reinterpret_cast<const double2*>(&t);
-    double2* dst = reinterpret_cast<double2*>(&tris[p]);
-#pragma unroll
-    for (int q = 0; q < 5; ++q) dst[q] = src[q];
-    fbox_store(tbox + p, box);
-  }
-  seg_reduce_block(box, static_cast<unsigned>(N + blockIdx.x * 1024), min(1024, N), seg, sm);
 }
 
 // The first 10 levels above the leaf-order boxes written by k_repack (a
@@ -678,6 +705,12 @@ void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag, 
   out.nodes = ctx.buf<BNode>(tag + ".nodes", out.n_nodes > 0 ? out.n_nodes : 1);
   out.tris = ctx.buf<BTri>(tag + ".tris", n);
   out.tbox = ctx.buf<TBox>(tag + ".tbox", n);
+  static const int plane_env = [] {  // MFB_TPLANE=0 / 1: never / always build the triangle planes
+    const char* e = std::getenv("MFB_TPLANE");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool planes = plane_env < 0 ? out.leaf_max >= kPlaneLeafMin : plane_env != 0;
+  out.tplane = planes ? ctx.buf<TPlane>(tag + ".tplane", n) : nullptr;
   out.root_box_dev = ctx.buf<float>(tag + ".rootbox", 8);
   out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
   out.scene_acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
@@ -745,22 +778,15 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   TBox* seg = nullptr;
   if (use_seg) {
     seg = ctx.buf<TBox>(tag + ".seg", N);
-    static const bool fused_seg = [] {
-      const char* e = std::getenv("MFB_SEG_FUSED");
-      return e && e[0] == '1';
-    }();
-    int launches = 1;
-    if (fused_seg) {
-      k_repack_seg<<<div_up(N, 1024), 1024, 0, rs>>>(m.pos, m.faces, vals2, n, N, out.tris, out.tbox, seg);
-    } else {
-      k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
-      launch_pdl(k_seg_leaves, div_up(N, 1024), 1024, 0, rs, out.tbox, n, N, seg);
-      ++launches;
-    }
+    // (the repack fused with the first seg levels in 1024-thread CTAs measured
+    // slower: the 256-thread gather runs at full occupancy)
+    int launches = 2;
+    k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox, out.tplane);
+    launch_pdl(k_seg_leaves, div_up(N, 1024), 1024, 0, rs, out.tbox, n, N, seg);
     for (int L = N >> 10; L > 1; L >>= 10, ++launches) launch_pdl(k_seg_up, div_up(L, 1024), 1024, 0, rs, seg, L);
     ctx.count_launch(launches - 1);
   } else {
-    k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox);
+    k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox, out.tplane);
   }
   if (rs != s) MFB_CUDA_TRY(cudaEventRecord(ctx.ljoin, rs));
   if (n > 1) {

@@ -404,6 +404,30 @@ __device__ __forceinline__ int32_t pop_within(const int32_t* st_ref, const float
 #endif
 }
 
+// Triangle pre-test of the wide searches (Lbvh::tplane, built for leaf caps
+// >= kPlaneLeafMin): a lower bound of the distance from q to the triangle from
+// its containment slab and edge half-spaces in fp32; the exact f64 test is
+// skipped when that bound, less the slack 2^-16 M (M = the scene/query
+// magnitude behind E = M 2^-32; it covers the fp32 evaluation and the rounded
+// vectors' departure from unit length and orthogonality, a few 2^-23 M),
+// already exceeds the pruning bound. Result-neutral like node pruning: a
+// skipped face is farther than any face that can still win.
+__device__ __forceinline__ bool tri_plane_skip(const TPlane* tp, float3 q, float bnd, float E) {
+  // (80-byte records: 16-byte aligned, five 128-bit loads)
+  const float4 a = __ldg(&tp->m0), b = __ldg(&tp->m1), c = __ldg(&tp->m2), nn = __ldg(&tp->n);
+  const float hi = __ldg(&tp->hi.x);
+  const float m0x = a.x, m0y = a.y, m0z = a.z, o0 = a.w, m1x = b.x, m1y = b.y, m1z = b.z, o1 = b.w;
+  const float m2x = c.x, m2y = c.y, m2z = c.z, o2 = c.w, nx = nn.x, ny = nn.y, nz = nn.z, lo = nn.w;
+  const float s0 = fmaf(m0z, q.z, fmaf(m0y, q.y, m0x * q.x)) - o0;
+  const float s1 = fmaf(m1z, q.z, fmaf(m1y, q.y, m1x * q.x)) - o1;
+  const float s2 = fmaf(m2z, q.z, fmaf(m2y, q.y, m2x * q.x)) - o2;
+  const float nq = fmaf(nz, q.z, fmaf(ny, q.y, nx * q.x));
+  const float delta = E * 65536.0f;
+  const float hh = fmaxf(__fsub_rd(fmaxf(lo - nq, nq - hi), delta), 0.0f);
+  const float ss = fmaxf(__fsub_rd(fmaxf(s0, fmaxf(s1, s2)), delta), 0.0f);
+  return __fmaf_rd(ss, ss, __fmul_rd(hh, hh)) > bnd;
+}
+
 // Row-band completion (BandSync, bake.cuh). Band b is complete once all its
 // queries are done; its rows are final once b-1, b, b+1 (those that exist)
 // are complete. The caller has fenced its stores.
@@ -464,7 +488,8 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     unsigned long long* __restrict__ prof_out, int qcap = 0, int res = 0, int slab_row0 = 0,
     int* __restrict__ face_map = nullptr, const double* __restrict__ hiPos = nullptr,
     const TBox* __restrict__ tbox = nullptr, const int* __restrict__ dep_head = nullptr,
-    const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}, int fmt = MF_ATLAS_RGB8) {
+    const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}, int fmt = MF_ATLAS_RGB8,
+    const TPlane* __restrict__ tplane = nullptr) {
   const int nq = qcount[kPass == 2 ? 1 : 0];
   const int lane = threadIdx.x & 31;
   if (kProf && lane == 0) {
@@ -571,6 +596,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       // loop state stays in registers under the 64-register cap)
       const int end = first + count;
       for (int k = first; k < end; ++k) {
+        if (!kSel && tplane && tri_plane_skip(tplane + k, qf, bnd, E)) continue;
 #if MFB_TRI_BOX
         {  // conservative per-triangle fp32 box check before the exact f64 test
           const float4* bp = reinterpret_cast<const float4*>(tbox + k);
@@ -1299,13 +1325,13 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
           a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
           a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions, bvh.tbox, a.dep_head, a.dep_next,     \
-          a.bands, a.fmt);                                                                                    \
+          a.bands, a.fmt, bvh.tplane);                                                                        \
     else                                                                                                      \
       k_transfer_t<D, P, PASS, false, false><<<g2, 128, 0, s>>>(                                              \
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
           a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
           a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions, bvh.tbox, a.dep_head, a.dep_next,     \
-          a.bands, a.fmt);                                                                                    \
+          a.bands, a.fmt, bvh.tplane);                                                                        \
   } while (0)
 #define MFB_XFER_TP(PASS)                                               \
   if (prof) {                                                           \
@@ -1322,12 +1348,12 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
       k_transfer_t<false, false, 0, true, true><<<g2, 128, 0, s>>>(
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
           a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
-          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt);
+          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane);
     else
       k_transfer_t<false, false, 0, true, false><<<g2, 128, 0, s>>>(
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
           a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
-          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt);
+          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane);
   } else {
     MFB_XFER_TP(0);
   }
