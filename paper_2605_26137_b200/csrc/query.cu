@@ -471,8 +471,11 @@ __global__ void k_band_init(BandSync bs) {
 #ifndef MFB_XFER_T_MINB
 #define MFB_XFER_T_MINB 8
 #endif
+// The wide-leaf instantiations (kSel false: f64 triangle tests dominate)
+// run best at 7 (config E per bake: 6 / 7 / 8 / 9 CTAs 46.4 / 43.0 / 44.3 /
+// 46.7 ms).
 #if MFB_XFER_T_MINB > 0
-#define MFB_XFER_T_BOUNDS __launch_bounds__(128, MFB_XFER_T_MINB)
+#define MFB_XFER_T_BOUNDS __launch_bounds__(128, kSel ? MFB_XFER_T_MINB : 7)
 #else
 #define MFB_XFER_T_BOUNDS __launch_bounds__(128)
 #endif
@@ -1315,9 +1318,10 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     ctx.fill(pbuf + 4, 0xff, 2 * sizeof(unsigned long long), s);
   }
   if (kSeedPasses) ctx.fill(a.face_map, 0xff, sizeof(int) * a.face_map_size, s);
-  static const int bps = occupancy(k_transfer_t<false, false>);
-  const int g2 = std::max(1, std::min(kNumSMs * bps, div_up(a.q.capacity, 128)));
   const bool sel = MFB_TRI_SEL == 2 ? bvh.leaf_max <= 3 : MFB_TRI_SEL != 0;
+  static const int bps_sel = occupancy(k_transfer_t<false, false, 0, false, true>);
+  static const int bps_wide = occupancy(k_transfer_t<false, false, 0, false, false>);
+  const int g2 = std::max(1, std::min(kNumSMs * (sel ? bps_sel : bps_wide), div_up(a.q.capacity, 128)));
 #define MFB_XFER_T(D, P, PASS)                                                                                \
   do {                                                                                                        \
     if (sel)                                                                                                  \
