@@ -201,8 +201,22 @@ struct alignas(16) TPlane {
   float4 hi;          // (hi, -, -, -)
 };
 
+// Per-leaf oriented box (built with TPlane): an orthonormal fp32 frame (n the
+// leaf's area-weighted normal, u in its plane, v = n x u) with the ranges
+// [lo, hi], [umin, umax], [vmin, vmax] that hold every vertex of the leaf's
+// triangles (f64 from the rounded directions, rounded outward). Indexed by
+// the leaf's first triangle. dist(q, leaf)^2 >= the sum of the three squared
+// range excesses, less the same slack as TPlane: a leaf whose bound already
+// fails is skipped without touching its triangles.
+struct alignas(32) LPlane {
+  float n[3], lo, hi, u[3];
+  float umin, umax, v[3], vmin, vmax, pad;
+};
+static_assert(sizeof(LPlane) == 64, "leaf record is two 32-byte loads");
+
 struct Lbvh {
   TPlane* tplane = nullptr;  // device, leaf order, or null (see TPlane)
+  LPlane* lplane = nullptr;  // device, by leaf first triangle, or null (see LPlane)
   int n_tris = 0;
   int n_nodes = 0;          // internal nodes (n_tris - 1), root = node 0 when n_tris > 1
   BNode* nodes = nullptr;   // device

@@ -331,6 +331,83 @@ __device__ void tri_planes(const double* v, TPlane& tp) {
   }
 }
 
+// LPlane of the leaf [first, first + count) of leaf-order triangles.
+__device__ void leaf_plane(const BTri* __restrict__ tris, int first, int count, LPlane& lp) {
+  double s[3] = {0.0, 0.0, 0.0}, sa = 0.0, e0[3] = {0.0, 0.0, 0.0};
+  for (int t = 0; t < count; ++t) {
+    const double* v = tris[first + t].v;
+    const double a[3] = {v[3] - v[0], v[4] - v[1], v[5] - v[2]};
+    const double b[3] = {v[6] - v[0], v[7] - v[1], v[8] - v[2]};
+    const double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+    s[0] += c[0];
+    s[1] += c[1];
+    s[2] += c[2];
+    sa += sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    if (t == 0) {
+      e0[0] = a[0];
+      e0[1] = a[1];
+      e0[2] = a[2];
+    }
+  }
+  const double sl = sqrt(s[0] * s[0] + s[1] * s[1] + s[2] * s[2]);
+  lp = LPlane{};
+  // a folded or degenerate patch: no usable frame (a zero record never skips)
+  if (!(sl > 1e-3 * sa) || !isfinite(sl)) return;
+  const double n[3] = {s[0] / sl, s[1] / sl, s[2] / sl};
+  const double en = e0[0] * n[0] + e0[1] * n[1] + e0[2] * n[2];
+  double u[3] = {e0[0] - en * n[0], e0[1] - en * n[1], e0[2] - en * n[2]};
+  const double ul = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
+  if (!(ul > 0.0) || !isfinite(ul)) return;
+  for (int k = 0; k < 3; ++k) u[k] /= ul;
+  const double v[3] = {n[1] * u[2] - n[2] * u[1], n[2] * u[0] - n[0] * u[2], n[0] * u[1] - n[1] * u[0]};
+  for (int k = 0; k < 3; ++k) {
+    lp.n[k] = static_cast<float>(n[k]);
+    lp.u[k] = static_cast<float>(u[k]);
+    lp.v[k] = static_cast<float>(v[k]);
+  }
+  double r[3][2] = {{INFINITY, -INFINITY}, {INFINITY, -INFINITY}, {INFINITY, -INFINITY}};
+  const float* dir[3] = {lp.n, lp.u, lp.v};
+  for (int t = 0; t < count; ++t) {
+    const double* x = tris[first + t].v;
+    for (int c = 0; c < 3; ++c)
+      for (int d = 0; d < 3; ++d) {
+        const double p = (static_cast<double>(dir[d][0]) * x[3 * c] + static_cast<double>(dir[d][1]) * x[3 * c + 1]) +
+                         static_cast<double>(dir[d][2]) * x[3 * c + 2];
+        r[d][0] = fmin(r[d][0], p);
+        r[d][1] = fmax(r[d][1], p);
+      }
+  }
+  lp.lo = __double2float_rd(r[0][0]);
+  lp.hi = __double2float_ru(r[0][1]);
+  lp.umin = __double2float_rd(r[1][0]);
+  lp.umax = __double2float_ru(r[1][1]);
+  lp.vmin = __double2float_rd(r[2][0]);
+  lp.vmax = __double2float_ru(r[2][1]);
+}
+
+// One thread per listed node (every reachable node with a leaf child is in
+// the list); each leaf has one parent, so each record is written once.
+__global__ void k_leaf_planes(const BNode* __restrict__ nodes, const BTri* __restrict__ tris,
+                              const int32_t* __restrict__ list, const int* __restrict__ list_n, int n,
+                              LPlane* __restrict__ lplane) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n == 1) {
+    if (j == 0) leaf_plane(tris, 0, 1, lplane[0]);
+    return;
+  }
+  if (j >= *list_n) return;
+  const int4 d = nodes[list[j]].d;
+  const int refs[2] = {d.x, d.y};
+  for (int c = 0; c < 2; ++c) {
+    if (refs[c] >= 0) continue;
+    int first, count;
+    leaf_decode(refs[c], first, count);
+    LPlane lp;
+    leaf_plane(tris, first, count, lp);
+    lplane[first] = lp;
+  }
+}
+
 __global__ void k_repack(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                          const uint32_t* __restrict__ order, int n, BTri* __restrict__ tris,
                          TBox* __restrict__ tbox, TPlane* __restrict__ tplane) {
@@ -711,6 +788,7 @@ void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag, 
   }();
   const bool planes = plane_env < 0 ? out.leaf_max >= kPlaneLeafMin : plane_env != 0;
   out.tplane = planes ? ctx.buf<TPlane>(tag + ".tplane", n) : nullptr;
+  out.lplane = planes ? ctx.buf<LPlane>(tag + ".lplane", n) : nullptr;
   out.root_box_dev = ctx.buf<float>(tag + ".rootbox", 8);
   out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
   out.scene_acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
@@ -808,6 +886,10 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
     k_refit<<<1, 32, 0, s>>>(out.tbox, n, out.nodes, prim_parent, node_parent, flags, out.root_box_dev);
   }
   ctx.count_launch(2);
+  if (out.lplane) {  // after the boxes: the list and the child refs are final
+    k_leaf_planes<<<div_up(std::max(n - 1, 1), T), T, 0, s>>>(out.nodes, out.tris, starts, starts_n, n, out.lplane);
+    ctx.count_launch();
+  }
   MFB_CUDA_TRY(cudaGetLastError());
   out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
   out.scene_acc = acc;

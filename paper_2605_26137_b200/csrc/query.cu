@@ -428,6 +428,28 @@ __device__ __forceinline__ bool tri_plane_skip(const TPlane* tp, float3 q, float
   return __fmaf_rd(ss, ss, __fmul_rd(hh, hh)) > bnd;
 }
 
+// Leaf pre-test (Lbvh::lplane): the leaf's oriented box, same slack as
+// tri_plane_skip; skips every triangle of a leaf that cannot hold a winner.
+__device__ __forceinline__ bool leaf_skip(const LPlane* lp, float3 q, float bnd, float E) {
+  const float* p = reinterpret_cast<const float*>(lp);
+  float nx, ny, nz, lo, hi, ux, uy, uz, umin, umax, vx, vy, vz, vmin, vmax, pad;
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(nx), "=f"(ny), "=f"(nz), "=f"(lo), "=f"(hi), "=f"(ux), "=f"(uy), "=f"(uz)
+      : "l"(p));
+  asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(umin), "=f"(umax), "=f"(vx), "=f"(vy), "=f"(vz), "=f"(vmin), "=f"(vmax), "=f"(pad)
+      : "l"(p + 8));
+  (void)pad;
+  const float nq = fmaf(nz, q.z, fmaf(ny, q.y, nx * q.x));
+  const float uq = fmaf(uz, q.z, fmaf(uy, q.y, ux * q.x));
+  const float vq = fmaf(vz, q.z, fmaf(vy, q.y, vx * q.x));
+  const float delta = E * 65536.0f;
+  const float a = fmaxf(__fsub_rd(fmaxf(lo - nq, nq - hi), delta), 0.0f);
+  const float b = fmaxf(__fsub_rd(fmaxf(umin - uq, uq - umax), delta), 0.0f);
+  const float c = fmaxf(__fsub_rd(fmaxf(vmin - vq, vq - vmax), delta), 0.0f);
+  return __fmaf_rd(c, c, __fmaf_rd(b, b, __fmul_rd(a, a))) > bnd;
+}
+
 // Row-band completion (BandSync, bake.cuh). Band b is complete once all its
 // queries are done; its rows are final once b-1, b, b+1 (those that exist)
 // are complete. The caller has fenced its stores.
@@ -492,7 +514,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     int* __restrict__ face_map = nullptr, const double* __restrict__ hiPos = nullptr,
     const TBox* __restrict__ tbox = nullptr, const int* __restrict__ dep_head = nullptr,
     const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}, int fmt = MF_ATLAS_RGB8,
-    const TPlane* __restrict__ tplane = nullptr) {
+    const TPlane* __restrict__ tplane = nullptr, const LPlane* __restrict__ lplane = nullptr) {
   const int nq = qcount[kPass == 2 ? 1 : 0];
   const int lane = threadIdx.x & 31;
   if (kProf && lane == 0) {
@@ -500,7 +522,7 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     atomicMin(&prof_out[4], t);
   }
-  unsigned long long pv[4] = {0, 0, 0, 0};  // internal visits, leaf visits, triangle tests, queries
+  unsigned long long pv[5] = {0, 0, 0, 0, 0};  // internal visits, leaf visits, leaf triangles, queries, exact tests
   const double scene_max = from_ordered_dev(scene_acc[6]);
   const double init = isinf(max_dist) ? max_dist : max_dist * max_dist;  // bvh.cpp:153-154
   unsigned hits = 0;
@@ -597,9 +619,10 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       }
       // (iterate [first, end): two live loop values instead of three, so the
       // loop state stays in registers under the 64-register cap)
-      const int end = first + count;
+      const int end = (!kSel && lplane && leaf_skip(lplane + first, qf, bnd, E)) ? first : first + count;
       for (int k = first; k < end; ++k) {
         if (!kSel && tplane && tri_plane_skip(tplane + k, qf, bnd, E)) continue;
+        if (kProf) ++pv[4];
 #if MFB_TRI_BOX
         {  // conservative per-triangle fp32 box check before the exact f64 test
           const float4* bp = reinterpret_cast<const float4*>(tbox + k);
@@ -681,10 +704,10 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     }
   }
   if (kProf) {
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 5; ++k) {
       unsigned long long v = pv[k];
       for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0) atomicAdd(&prof_out[k], v);
+      if (lane == 0) atomicAdd(&prof_out[k < 4 ? k : 7], v);
     }
     if (lane == 0) {  // warp exit times (tail spread): [5] first, [6] last, [4] kernel start
       unsigned long long t;
@@ -1329,13 +1352,13 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
           a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
           a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions, bvh.tbox, a.dep_head, a.dep_next,     \
-          a.bands, a.fmt, bvh.tplane);                                                                        \
+          a.bands, a.fmt, bvh.tplane, bvh.lplane);                                                                        \
     else                                                                                                      \
       k_transfer_t<D, P, PASS, false, false><<<g2, 128, 0, s>>>(                                              \
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
           a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
           a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions, bvh.tbox, a.dep_head, a.dep_next,     \
-          a.bands, a.fmt, bvh.tplane);                                                                        \
+          a.bands, a.fmt, bvh.tplane, bvh.lplane);                                                                        \
   } while (0)
 #define MFB_XFER_TP(PASS)                                               \
   if (prof) {                                                           \
@@ -1352,12 +1375,12 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
       k_transfer_t<false, false, 0, true, true><<<g2, 128, 0, s>>>(
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
           a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
-          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane);
+          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane);
     else
       k_transfer_t<false, false, 0, true, false><<<g2, 128, 0, s>>>(
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
           a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
-          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane);
+          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane);
   } else {
     MFB_XFER_TP(0);
   }
@@ -1371,9 +1394,9 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
     const double nqd = h[3] ? static_cast<double>(h[3]) : 1.0;
     std::fprintf(stderr,
-                 "[mfb prof] per query: internal %.2f leaves %.2f triangles %.2f (queries %llu); warp exits "
-                 "%.1f..%.1f us after the first start\n",
-                 h[0] / nqd, h[1] / nqd, h[2] / nqd, h[3], (h[5] - h[4]) * 1e-3, (h[6] - h[4]) * 1e-3);
+                 "[mfb prof] per query: internal %.2f leaves %.2f triangles %.2f exact tests %.2f (queries %llu); "
+                 "warp exits %.1f..%.1f us after the first start\n",
+                 h[0] / nqd, h[1] / nqd, h[2] / nqd, h[7] / nqd, h[3], (h[5] - h[4]) * 1e-3, (h[6] - h[4]) * 1e-3);
   }
 }
 
