@@ -286,23 +286,11 @@ void prepare_lowpoly(Ctx& ctx, cudaStream_t s, const DevMesh& lo, int res, Raste
 void wedge_frames(Ctx& ctx, cudaStream_t s, const DevMesh& lo, double* frames_out);
 
 // Compacted closest-point queries (valid and reliable texels), in 8x4 texel
-// blocks so each warp's 32 queries are spatial neighbours. Two passes share
-// one buffer: pass A (texels with even x and even y, one per 2x2 quad) fills
-// slots from the front, pass B (the other three texels of each quad) from the
-// back, so pass B can seed its bound with the face pass A found for the quad
-// corner (result-neutral: it only tests that face first).
-// Measured on config B (r01 profiles): the quad split lowers per-warp
-// coherence more than the seeded bound saves, so it is off; every query is
-// in pass A and pass B is empty.
-#ifndef MFB_SEED_PASSES
-#define MFB_SEED_PASSES 0
-#endif
-constexpr bool kSeedPasses = MFB_SEED_PASSES != 0;
-
+// blocks so each warp's 32 queries are spatial neighbours.
 struct QueryList {
   float4* qpos = nullptr;  // x, y, z (the G-buffer's f32 position), w = slab texel index (int bits)
   float* qtbn = nullptr;   // 9 floats per query: tangent, bitangent, normal (f32, as stored)
-  int* count = nullptr;    // device counters: [0] pass A, [1] pass B (reset by the producer)
+  int* count = nullptr;    // device counters: [0] queries, [3] the transfer's batch cursor (reset by the producer)
   int capacity = 0;
 };
 
@@ -368,8 +356,6 @@ struct TransferArgs {
   QueryList q;
   int res = 0;
   int slab_row0 = 0;                // absolute atlas row of slab row 0
-  int* face_map = nullptr;          // slab-sized: pass-A winning face per texel (-1 elsewhere)
-  int64_t face_map_size = 0;
   const double* hi_positions = nullptr;
   const double* hi_normals = nullptr;
   const int32_t* hi_faces = nullptr;

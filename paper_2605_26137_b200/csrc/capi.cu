@@ -28,12 +28,6 @@
 #include "bake.cuh"
 #include "host_pool.h"
 
-#ifndef MFB_LOWPOLY_PRIO_DELTA
-#define MFB_LOWPOLY_PRIO_DELTA 1  // lowpoly branch streams: this many levels below the LBVH's
-#endif
-#ifndef MFB_DN_PRIO
-#define MFB_DN_PRIO 0  // dense vertex normals: 0 lowest, 1 the lowpoly branch's level, 2 the top level
-#endif
 
 namespace mfb {
 
@@ -933,8 +927,6 @@ struct BakeEnq {
     ta.q = fo.q;
     ta.res = res;
     ta.slab_row0 = s0;
-    ta.face_map = c.buf<int>("bake.facemap", g.texels());
-    ta.face_map_size = g.texels();
     ta.hi_positions = hi->m.pos;
     ta.hi_normals = hiN;
     ta.hi_faces = hi->m.faces;
@@ -1477,28 +1469,22 @@ int mf_ctx_create(int device, void* stream, mf_ctx** out) {
     // priority as well as the LBVH's; the dense normals stay low. With the
     // segment-tree LBVH the lowpoly branch is the longer chain: 1.431 ->
     // 1.401 ms (with the refit climb it was the reverse: 1.52 vs 1.505 ms).
-    // r02: three levels. With equal priorities the coverage kernel's 16k
-    // CTAs (queued first) held the SMs while the LBVH's repack and emission
-    // waited ~70-100 us behind them (CUPTI timeline, tools/timeline.py): the
-    // LBVH chain (the long pole) now outranks the lowpoly branch, which
-    // fills in around it.
-    const int mid_prio = std::min(lo_prio, hi_prio + MFB_LOWPOLY_PRIO_DELTA);
-    // r02 (per-step events on the context's stream): the lowpoly branch above
-    // the LBVH, the dense normals lowest: 1.428 ms per bake vs 1.437 (LBVH
-    // above) and 1.455-1.465 with the normals at the lowpoly branch's level;
-    // the pre-transfer phase is bound by the branches' total work, so the
-    // priorities move it by ~2% at most
-#ifndef MFB_PRIO_SWAP
-#define MFB_PRIO_SWAP 1
-#endif
-    const int lbvh_prio = MFB_PRIO_SWAP ? mid_prio : hi_prio;
-    const int low_prio = MFB_PRIO_SWAP ? hi_prio : mid_prio;
+    // Three levels: the lowpoly branch on top, the LBVH one below, the dense
+    // vertex normals (needed only by the transfer's encode) lowest. Measured
+    // with per-step events: 1.428 ms per bake vs 1.437 (LBVH above the
+    // lowpoly branch; r02s: 1.433 vs 1.430) and 1.455-1.465 with the normals
+    // at the lowpoly level. With equal priorities the coverage kernel's 16k
+    // CTAs (queued first) held the SMs while the LBVH waited ~70-100 us. The
+    // pre-transfer phase is bound by the branches' total work, so priorities
+    // move it by ~2% at most.
+    const int mid_prio = std::min(lo_prio, hi_prio + 1);
+    const int lbvh_prio = mid_prio, low_prio = hi_prio;
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side, cudaStreamNonBlocking, lbvh_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux, cudaStreamNonBlocking, low_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.side2, cudaStreamNonBlocking, lbvh_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.aux2, cudaStreamNonBlocking, low_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.lowhi, cudaStreamNonBlocking, low_prio));
-    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, MFB_DN_PRIO == 2 ? hi_prio : (MFB_DN_PRIO == 1 ? mid_prio : lo_prio)));
+    MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.dn, cudaStreamNonBlocking, lo_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up1, cudaStreamNonBlocking, hi_prio));
     MFB_CUDA_TRY(cudaStreamCreateWithPriority(&ctx->c.up2, cudaStreamNonBlocking, hi_prio));
     for (cudaEvent_t* e : {&ctx->c.fork, &ctx->c.join, &ctx->c.fork2, &ctx->c.join2, &ctx->c.join3, &ctx->c.hi_ready,
@@ -1656,8 +1642,6 @@ int mf_transfer_normals(mf_ctx* ctx, int res, const float* position, const float
     ta.q = fo.q;
     ta.res = res;
     ta.slab_row0 = 0;
-    ta.face_map = c.buf<int>("bake.facemap", n);
-    ta.face_map_size = n;
     ta.hi_positions = hi.m.pos;
     ta.hi_normals = hiN;
     ta.hi_faces = hi.m.faces;

@@ -144,21 +144,11 @@ __device__ __forceinline__ void px_store(uint8_t* base, int64_t t, int fmt, uint
 // instructions are no-ops.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
-// Where the chain's kernels trigger: MFB_PDL_EARLY=1 (default) right after
-// their own wait, so each dependent's CTAs become resident while the
-// predecessor runs; 0: before their final stores (PDL_TRIGGER_LATE), or
-// implicitly at exit. Measured on config B: early 1.390-1.394 ms per bake,
-// late 1.404-1.411, no PDL 1.409-1.414.
-#ifndef MFB_PDL_EARLY
-#define MFB_PDL_EARLY 0
-#endif
-#if MFB_PDL_EARLY
-#define PDL_TRIGGER_EARLY() pdl_trigger()
-#define PDL_TRIGGER_LATE() ((void)0)
-#else
-#define PDL_TRIGGER_EARLY() ((void)0)
-#define PDL_TRIGGER_LATE() pdl_trigger()
-#endif
+// Where the chain's kernels trigger: the sort passes before their write-out
+// (the next pass's CTAs become resident meanwhile), the others implicitly at
+// exit. Measured on config B: triggering right after each kernel's own wait
+// 1.390-1.394 ms per bake (r01 timing), late 1.404-1.411, no PDL 1.409-1.414;
+// with the bracketed per-step events of r02 the late form won.
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg{};

@@ -49,7 +49,6 @@ __host__ __device__ __forceinline__ double from_ordered(unsigned long long b) {
 // validation pass into the LBVH build)
 __global__ void k_bounds(const double* __restrict__ pos, int nv, unsigned long long* acc, int* vflags) {
   pdl_wait();
-  PDL_TRIGGER_EARLY();
   double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
   double amax = 0.0;
   bool bad = false;
@@ -123,7 +122,6 @@ __global__ void __launch_bounds__(kMortonThreads) k_morton(const double* __restr
                                                            int* __restrict__ hist, uint32_t* __restrict__ status,
                                                            int64_t status_words, int nv, int* vflags) {
   pdl_wait();
-  PDL_TRIGGER_EARLY();
   __shared__ int h[3 * 1024];
   for (int i = threadIdx.x; i < 3 * 1024; i += blockDim.x) h[i] = 0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < status_words;
@@ -194,7 +192,6 @@ __global__ void k_emit(const uint32_t* __restrict__ keys, int n, int leaf_max, B
                        int32_t* __restrict__ prim_parent, int32_t* __restrict__ node_parent,
                        int32_t* __restrict__ starts, int* __restrict__ starts_n, int reach_list = 0) {
   pdl_wait();
-  PDL_TRIGGER_EARLY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool active = i < n - 1;
   bool start = false;
@@ -525,7 +522,6 @@ __device__ __forceinline__ void seg_reduce_block(FBox box, unsigned base, int cn
 __global__ void __launch_bounds__(1024) k_seg_leaves(const TBox* __restrict__ tbox, int n, int N,
                                                      TBox* __restrict__ seg) {
   pdl_wait();
-  PDL_TRIGGER_EARLY();
   __shared__ FBox sm[32];
   const int p = blockIdx.x * 1024 + threadIdx.x;
   const FBox box = p < n ? fbox_load(tbox + p) : fbox_empty();
@@ -535,7 +531,6 @@ __global__ void __launch_bounds__(1024) k_seg_leaves(const TBox* __restrict__ tb
 // The next 10 levels: nodes [L, 2L) -> their ancestors.
 __global__ void __launch_bounds__(1024) k_seg_up(TBox* __restrict__ seg, int L) {
   pdl_wait();
-  PDL_TRIGGER_EARLY();
   __shared__ FBox sm[32];
   const int i = blockIdx.x * 1024 + threadIdx.x;
   const FBox box = i < L ? fbox_load(seg + L + i) : fbox_empty();
@@ -551,7 +546,6 @@ __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restric
                              BNode* __restrict__ nodes, float* __restrict__ root_box,
                              const int32_t* __restrict__ reach, const int* __restrict__ reach_n) {
   pdl_wait();
-  PDL_TRIGGER_EARLY();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= *reach_n) return;
   const int i = reach[j];

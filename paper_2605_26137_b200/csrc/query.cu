@@ -43,12 +43,8 @@ __device__ __forceinline__ float prune_bound(double best, double E) {
 }
 
 // One 64-byte node record in two 256-bit read-only loads (LDG.E.256 on
-// sm_100; four LDG.128 otherwise). MFB_LDG256=0 keeps the 128-bit loads.
-#ifndef MFB_LDG256
-#define MFB_LDG256 1
-#endif
+// sm_100).
 __device__ __forceinline__ void ld_node(const BNode* __restrict__ nd, float4& a, float4& b, float4& c, int4& d) {
-#if MFB_LDG256
   const float* p = reinterpret_cast<const float*>(nd);
   float dx, dy, dz, dw;
   asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -58,13 +54,6 @@ __device__ __forceinline__ void ld_node(const BNode* __restrict__ nd, float4& a,
                : "=f"(c.x), "=f"(c.y), "=f"(c.z), "=f"(c.w), "=f"(dx), "=f"(dy), "=f"(dz), "=f"(dw)
                : "l"(p + 8));
   d = make_int4(__float_as_int(dx), __float_as_int(dy), __float_as_int(dz), __float_as_int(dw));
-#else
-  const float4* np = reinterpret_cast<const float4*>(nd);
-  a = __ldg(np);
-  b = __ldg(np + 1);
-  c = __ldg(np + 2);
-  d = __ldg(reinterpret_cast<const int4*>(np + 3));
-#endif
 }
 
 // Lower bound of the squared distance from [qlo, qhi] (per axis) to a box.
@@ -315,73 +304,22 @@ __device__ __forceinline__ void traverse_closest(const BNode* __restrict__ nodes
 // holds one, so the expensive exact f64 test executes at high SIMT width.
 // Depth-first nearest-child-first with conservative fp32 pruning (see
 // traverse_closest) - result-neutral vs the reference's best-first heap.
-// kPass 0: single pass over all queries. kPass 1/2: the quad-seeded passes
-// (kSeedPasses): pass 1 (one texel per 2x2 quad, list front) records its
-// winning faces in face_map; pass 2 (the other texels, list back) first tests
-// the face its quad corner won - result-neutral, it only tightens the
-// initial bound.
-#ifndef MFB_TRI_BOX
-#define MFB_TRI_BOX 0
-#endif
-#ifndef MFB_TRI_SEL
 // The triangle test's form per bake (template kSel of k_transfer_t): the
 // branch-free one for leaves of <= 3 triangles (config B transfer 0.994 vs
 // 1.005 ms), the branchy one for the larger leaves of a wide search
-// (config E, leaves up to 11: 49.2 vs 54.6 ms). MFB_TRI_SEL=0/1 forces one.
-#define MFB_TRI_SEL 2
-#endif
-// L1 prefetch hints for the traversal (bit mask, compile-time):
-//   1 = a leaf's triangle lines when the leaf is entered (its 2-4 triangles
-//       are otherwise fetched one dependent L2 round trip after another),
-//   2 = the far child when it is pushed (node record or leaf triangle lines),
-//   4 = both internal children's node records as soon as a node is loaded.
-#ifndef MFB_PF
-#define MFB_PF 0
-#endif
-// Lean traversal state: the incumbent's barycentrics are not carried through
-// the walk (recomputed for the winner at the end), the slack E is one fp32.
-#ifndef MFB_LEAN
-#define MFB_LEAN 1
-#endif
-__device__ __forceinline__ void pf_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-__device__ __forceinline__ void pf_leaf(const BTri* __restrict__ tris, int32_t ref) {
-  int first, count;
-  leaf_decode(ref, first, count);
-  const uintptr_t b = reinterpret_cast<uintptr_t>(tris + first) & ~static_cast<uintptr_t>(127);
-  const uintptr_t e = reinterpret_cast<uintptr_t>(tris + first + count);
-  for (uintptr_t a = b; a < e; a += 128) pf_l1(reinterpret_cast<const void*>(a));
-}
-__device__ __forceinline__ void pf_ref(const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t ref) {
-  if (ref >= 0)
-    pf_l1(nodes + ref);  // 64-B record inside one 128-B line (256-B aligned array)
-  else
-    pf_leaf(tris, ref);
-}
+// (config E, leaves up to 11: 49.2 vs 54.6 ms). Measured and removed (numbers
+// in DESIGN.md): L1 prefetch hints, per-triangle fp32 box pre-test, quad-seeded
+// two-pass lists, carrying the incumbent's barycentrics through the walk.
 
 // Pop of the per-thread stack that skips entries whose lower bound no longer
 // passes `bnd` four at a time: one aligned 16-byte local load covers the top
 // (up to) four lower bounds, so a run of pruned entries costs one dependent
 // L1 round trip per four entries instead of one per entry. Returns the
 // topmost surviving entry's ref (sp = its slot) or kDoneRef (sp = 0).
-#ifndef MFB_POP4
-#define MFB_POP4 1
-#endif
-#ifndef MFB_DYN
-#define MFB_DYN 1
-#endif
-// Query records are read once: MFB_STREAM=1 loads them evict-first so they do
-// not displace node / triangle lines from L1.
-#ifndef MFB_STREAM
-#define MFB_STREAM 1  // measured 1.008 -> 1.005 ms transfer at config B
-#endif
-#if MFB_STREAM
-#define MFB_STREAM_LD(p) __ldcs(p)
-#else
-#define MFB_STREAM_LD(p) __ldg(p)
-#endif
+// Query records are read once: loaded evict-first (__ldcs) so they do not
+// displace node / triangle lines from L1 (1.008 -> 1.005 ms transfer at B).
 constexpr int32_t kDoneRef = static_cast<int32_t>(0x80000000);
 __device__ __forceinline__ int32_t pop_within(const int32_t* st_ref, const float* st_lb, int& sp, float bnd) {
-#if MFB_POP4
   while (sp > 0) {
     const int base = (sp - 1) & ~3;
     const float4 v = *reinterpret_cast<const float4*>(st_lb + base);
@@ -395,13 +333,6 @@ __device__ __forceinline__ int32_t pop_within(const int32_t* st_ref, const float
     sp = base;
   }
   return kDoneRef;
-#else
-  while (sp > 0) {
-    --sp;
-    if (st_lb[sp] <= bnd) return st_ref[sp];
-  }
-  return kDoneRef;
-#endif
 }
 
 // Triangle pre-test of the wide searches (Lbvh::tplane, built for leaf caps
@@ -503,19 +434,18 @@ __global__ void k_band_init(BandSync bs) {
 #endif
 // kBands: the row-band publication of the host path's overlapped download
 // (compiled only into that instantiation: it costs the walk registers)
-template <bool kDebug, bool kProf, int kPass = 0, bool kBands = false, bool kSel = true>
+template <bool kDebug, bool kProf, bool kBands = false, bool kSel = true>
 __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int32_t root,
     const unsigned long long* __restrict__ scene_acc, const float4* __restrict__ qpos,
     const float* __restrict__ qtbn, const int* __restrict__ qcount, const double* __restrict__ hiN,
     const int32_t* __restrict__ hiF, double max_dist, uint8_t* __restrict__ rgb,
     int32_t* __restrict__ dbg_face, double* __restrict__ dbg_ts, unsigned long long* __restrict__ counters,
-    unsigned long long* __restrict__ prof_out, int qcap = 0, int res = 0, int slab_row0 = 0,
-    int* __restrict__ face_map = nullptr, const double* __restrict__ hiPos = nullptr,
-    const TBox* __restrict__ tbox = nullptr, const int* __restrict__ dep_head = nullptr,
+    unsigned long long* __restrict__ prof_out, const double* __restrict__ hiPos = nullptr,
+    const int* __restrict__ dep_head = nullptr,
     const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}, int fmt = MF_ATLAS_RGB8,
     const TPlane* __restrict__ tplane = nullptr, const LPlane* __restrict__ lplane = nullptr) {
-  const int nq = qcount[kPass == 2 ? 1 : 0];
+  const int nq = qcount[0];
   const int lane = threadIdx.x & 31;
   if (kProf && lane == 0) {
     unsigned long long t;
@@ -530,19 +460,17 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
   // next batch from the list's cursor (qcount[3], zeroed by the producer), so
   // warps that drew cheap batches keep working instead of idling in the tail.
   // Measured at config B: transfer 1.055 -> 1.003 ms; config E 69.7 -> 62.1 ms.
-  constexpr bool kDynamic = MFB_DYN && kPass == 0;
   int* cursor = const_cast<int*>(qcount) + 3;
   auto next_batch = [&]() {
     int b = 0;
     if (lane == 0) b = atomicAdd(cursor, 1);
     return __shfl_sync(0xffffffffu, b, 0) * 32 + lane;
   };
-  for (int li = kDynamic ? next_batch() : static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x); li - lane < nq;
-       li = kDynamic ? next_batch() : li + static_cast<int>(gridDim.x * blockDim.x)) {
+  for (int li = next_batch(); li - lane < nq; li = next_batch()) {
     const bool live = li < nq;
-    const int i = kPass == 2 ? qcap - 1 - li : li;
+    const int i = li;
     float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live) p = MFB_STREAM_LD(qpos + i);
+    if (live) p = __ldcs(qpos + i);
     // a dead record (texel id stored as ~texel by k_interp: the texel's face
     // is unreliable) is not walked; its epilogue stores the (128, 128, 255)
     // of gbuffer.cpp:218-227 into the texel and the gutter texels linked to it
@@ -555,25 +483,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     best.d = init;
     best.face = -1;
     best.bary = mk3(0.0, 0.0, 0.0);
-    if (kPass == 2 && live) {
-      const int gi = __float_as_int(p.w);
-      const int x = gi % res, y = gi / res + slab_row0;
-      const int sy = (y & ~1) - slab_row0;
-      if (sy >= 0) {
-        const int sf = face_map[static_cast<int64_t>(sy) * res + (x & ~1)];
-        if (sf >= 0) {  // exact test of the seed face (as if visited first)
-          d3 bary;
-          const d3 pt = closest_point_triangle_sel(q, ld3(hiPos + 3 * hiF[3 * sf]), ld3(hiPos + 3 * hiF[3 * sf + 1]),
-                                                   ld3(hiPos + 3 * hiF[3 * sf + 2]), bary);
-          const double ds = sqnorm(pt - q);
-          if (ds < best.d || (ds == best.d && sf < best.face)) {
-            best.d = ds;
-            best.face = sf;
-            best.bary = bary;
-          }
-        }
-      }
-    }
     float bnd = live && !dead ? prune_bound(best.d, E) : -INFINITY;
     int32_t st_ref[kStackMax];
     alignas(16) float st_lb[kStackMax];
@@ -588,10 +497,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         float4 a, b, c;
         int4 d;
         ld_node(nodes + ref, a, b, c, d);
-        if (MFB_PF & 4) {
-          if (d.x >= 0) pf_l1(nodes + d.x);
-          if (d.y >= 0) pf_l1(nodes + d.y);
-        }
         float lbL, lbR;
         box_lb2(a, b, c, qf, lbL, lbR);
         const bool hL = lbL <= bnd, hR = lbR <= bnd;
@@ -601,7 +506,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
           st_lb[sp] = lf ? lbR : lbL;
           ++sp;
           ref = lf ? d.x : d.y;
-          if (MFB_PF & 2) pf_ref(nodes, tris, lf ? d.y : d.x);
         } else if (hL || hR) {
           ref = hL ? d.x : d.y;
         } else {
@@ -612,7 +516,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       // ---- leaf: exact f64 tests (branch-free, reference arithmetic)
       int first, count;
       leaf_decode(ref, first, count);
-      if (MFB_PF & 1) pf_leaf(tris, ref);
       if (kProf) {
         ++pv[1];
         pv[2] += count;
@@ -623,13 +526,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
       for (int k = first; k < end; ++k) {
         if (!kSel && tplane && tri_plane_skip(tplane + k, qf, bnd, E)) continue;
         if (kProf) ++pv[4];
-#if MFB_TRI_BOX
-        {  // conservative per-triangle fp32 box check before the exact f64 test
-          const float4* bp = reinterpret_cast<const float4*>(tbox + k);
-          const float4 ba = __ldg(bp), bb = __ldg(bp + 1);
-          if (box_lb(ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, qf, qf) > bnd) continue;
-        }
-#endif
         d3 A, B, C;
         int face;
         load_tri(tris + k, A, B, C, face);
@@ -640,9 +536,6 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         if (ds < best.d || (ds == best.d && face < best.face)) {
           best.d = ds;
           best.face = face;
-#if !MFB_LEAN
-          best.bary = bary;
-#endif
           bnd = prune_bound(ds, E);
         }
       }
@@ -656,23 +549,20 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     if (kProf) ++pv[3];
     const int texel = dead ? ~__float_as_int(p.w) : __float_as_int(p.w);
     const d3 qe = q;
-    if (kPass == 1) face_map[texel] = best.face;
     uint32_t px = px_neutral(fmt);
     double ts3[3] = {0.0, 0.0, 0.0};
     if (best.face >= 0) {
       ++hits;
       const float* tb = qtbn + 9ll * i;
       const int v0 = hiF[3 * best.face], v1 = hiF[3 * best.face + 1], v2 = hiF[3 * best.face + 2];
-#if MFB_LEAN
-      // the winner's barycentrics, recomputed: same inputs (BTri holds copies
-      // of these positions) and the same function give the same bits
+      // the winner's barycentrics, recomputed (lean walk state): same inputs
+      // (BTri holds copies of these positions), same function, same bits
       closest_point_triangle(qe, ld3(hiPos + 3 * v0), ld3(hiPos + 3 * v1), ld3(hiPos + 3 * v2), best.bary);
-#endif
       const d3 n = (best.bary.x * ld3(hiN + 3 * v0) + best.bary.y * ld3(hiN + 3 * v1)) +
                    best.bary.z * ld3(hiN + 3 * v2);
-      const d3 T = mk3(MFB_STREAM_LD(tb), MFB_STREAM_LD(tb + 1), MFB_STREAM_LD(tb + 2));
-      const d3 B = mk3(MFB_STREAM_LD(tb + 3), MFB_STREAM_LD(tb + 4), MFB_STREAM_LD(tb + 5));
-      const d3 N = mk3(MFB_STREAM_LD(tb + 6), MFB_STREAM_LD(tb + 7), MFB_STREAM_LD(tb + 8));
+      const d3 T = mk3(__ldcs(tb), __ldcs(tb + 1), __ldcs(tb + 2));
+      const d3 B = mk3(__ldcs(tb + 3), __ldcs(tb + 4), __ldcs(tb + 5));
+      const d3 N = mk3(__ldcs(tb + 6), __ldcs(tb + 7), __ldcs(tb + 8));
       d3 ts = mk3(dot(n, T), dot(n, B), dot(n, N));
       const double len = norm(ts);
       if (!(len < 1e-12)) {
@@ -1340,51 +1230,32 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
     ctx.fill(pbuf, 0, 8 * sizeof(unsigned long long), s);
     ctx.fill(pbuf + 4, 0xff, 2 * sizeof(unsigned long long), s);
   }
-  if (kSeedPasses) ctx.fill(a.face_map, 0xff, sizeof(int) * a.face_map_size, s);
-  const bool sel = MFB_TRI_SEL == 2 ? bvh.leaf_max <= 3 : MFB_TRI_SEL != 0;
-  static const int bps_sel = occupancy(k_transfer_t<false, false, 0, false, true>);
-  static const int bps_wide = occupancy(k_transfer_t<false, false, 0, false, false>);
+  const bool sel = bvh.leaf_max <= 3;
+  static const int bps_sel = occupancy(k_transfer_t<false, false, false, true>);
+  static const int bps_wide = occupancy(k_transfer_t<false, false, false, false>);
   const int g2 = std::max(1, std::min(kNumSMs * (sel ? bps_sel : bps_wide), div_up(a.q.capacity, 128)));
-#define MFB_XFER_T(D, P, PASS)                                                                                \
+#define MFB_XFER_T(D, P, BANDS)                                                                               \
   do {                                                                                                        \
     if (sel)                                                                                                  \
-      k_transfer_t<D, P, PASS, false, true><<<g2, 128, 0, s>>>(                                               \
+      k_transfer_t<D, P, BANDS, true><<<g2, 128, 0, s>>>(                                                     \
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
           a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
-          a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions, bvh.tbox, a.dep_head, a.dep_next,     \
-          a.bands, a.fmt, bvh.tplane, bvh.lplane);                                                                        \
+          a.hi_positions, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane);                    \
     else                                                                                                      \
-      k_transfer_t<D, P, PASS, false, false><<<g2, 128, 0, s>>>(                                              \
+      k_transfer_t<D, P, BANDS, false><<<g2, 128, 0, s>>>(                                                    \
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
           a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
-          a.q.capacity, a.res, a.slab_row0, a.face_map, a.hi_positions, bvh.tbox, a.dep_head, a.dep_next,     \
-          a.bands, a.fmt, bvh.tplane, bvh.lplane);                                                                        \
+          a.hi_positions, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane);                    \
   } while (0)
-#define MFB_XFER_TP(PASS)                                               \
-  if (prof) {                                                           \
-    if (dbg) MFB_XFER_T(true, true, PASS); else MFB_XFER_T(false, true, PASS); \
-  } else {                                                              \
-    if (dbg) MFB_XFER_T(true, false, PASS); else MFB_XFER_T(false, false, PASS); \
-  }
-  if (kSeedPasses) {
-    MFB_XFER_TP(1);
-    MFB_XFER_TP(2);
-    ctx.count_launch();
-  } else if (a.bands.done) {
-    if (sel)
-      k_transfer_t<false, false, 0, true, true><<<g2, 128, 0, s>>>(
-          bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
-          a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
-          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane);
-    else
-      k_transfer_t<false, false, 0, true, false><<<g2, 128, 0, s>>>(
-          bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals, a.hi_faces,
-          a.max_dist, a.rgb, nullptr, nullptr, a.counters, pbuf, a.q.capacity, a.res, a.slab_row0, a.face_map,
-          a.hi_positions, bvh.tbox, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane);
+  // the row-band publication is compiled only into the host path's
+  // instantiation (it costs the walk registers)
+  if (a.bands.done) {
+    MFB_XFER_T(false, false, true);
+  } else if (prof) {
+    if (dbg) MFB_XFER_T(true, true, false); else MFB_XFER_T(false, true, false);
   } else {
-    MFB_XFER_TP(0);
+    if (dbg) MFB_XFER_T(true, false, false); else MFB_XFER_T(false, false, false);
   }
-#undef MFB_XFER_TP
 #undef MFB_XFER_T
   ctx.count_launch();
   MFB_CUDA_TRY(cudaGetLastError());

@@ -917,11 +917,11 @@ __device__ __forceinline__ int compact_slot(bool is_q, int* counter, int capacit
   return slot < capacity ? slot : -1;
 }
 
-// Writes one query record into pass A (front) or pass B (back) of the list.
-__device__ __forceinline__ void store_query(const QueryList& q, int slot, bool pass_b, int64_t gi, const float* P,
+// Writes one query record into the list.
+__device__ __forceinline__ void store_query(const QueryList& q, int slot, int64_t gi, const float* P,
                                             const float* Nf, const float* Tf, const float* Bf) {
   if (slot < 0) return;
-  const int idx = pass_b ? q.capacity - 1 - slot : slot;
+  const int idx = slot;
   q.qpos[idx] = make_float4(P[0], P[1], P[2], __int_as_float(static_cast<int>(gi)));
   float* t = q.qtbn + 9ll * idx;
   t[0] = Tf[0];
@@ -942,11 +942,8 @@ __device__ __forceinline__ void emit_fused(int64_t gi, int x, int y, bool in, ui
                                            const float* P, const float* Nf, const float* Tf, const float* Bf,
                                            uint8_t* gvalid, const RasterFused& fo, int* overflow) {
   const bool is_q = in && valid && rel;
-  const bool pass_a = kSeedPasses ? ((x | y) & 1) == 0 : true;
-  // one block-level compaction per pass; the valid-texel count rides along
-  const int slot_a = compact_slot(is_q && pass_a, fo.q.count, fo.q.capacity, overflow, in && valid != 0,
-                                  fo.valid_count);
-  const int slot_b = kSeedPasses ? compact_slot(is_q && !pass_a, fo.q.count + 1, fo.q.capacity, overflow) : -1;
+  // one block-level compaction; the valid-texel count rides along
+  const int slot = compact_slot(is_q, fo.q.count, fo.q.capacity, overflow, in && valid != 0, fo.valid_count);
   if (!in) return;
   if (gvalid) gvalid[gi] = valid;
   if (!is_q) {
@@ -959,7 +956,7 @@ __device__ __forceinline__ void emit_fused(int64_t gi, int x, int y, bool in, ui
     }
     return;
   }
-  store_query(fo.q, pass_a ? slot_a : slot_b, !pass_a, gi, P, Nf, Tf, Bf);
+  store_query(fo.q, slot, gi, P, Nf, Tf, Bf);
 }
 
 // gbuffer.cpp:162-186 for texel centre (cx, cy) inside face `sfc`: f64
@@ -998,18 +995,7 @@ __device__ __forceinline__ void interp_texel(const RasterFace& sfc, const AttrFa
 // Split raster, second kernel: one thread per compacted query (texel, face)
 // written by k_raster<2>; interpolates exactly as the fused path and writes
 // the same query record. No barriers, full SIMT width for the f64 chain.
-#ifndef MFB_INTERP_PF
-#define MFB_INTERP_PF 0
-#endif
-#ifndef MFB_INTERP_MINB
-#define MFB_INTERP_MINB 0
-#endif
-#if MFB_INTERP_MINB > 0
-#define MFB_INTERP_BOUNDS __launch_bounds__(256, MFB_INTERP_MINB)
-#else
-#define MFB_INTERP_BOUNDS __launch_bounds__(256)
-#endif
-__global__ void MFB_INTERP_BOUNDS k_interp(const RasterFace* __restrict__ rf,
+__global__ void __launch_bounds__(256) k_interp(const RasterFace* __restrict__ rf,
                                                 const AttrFace* __restrict__ attrs,
                                                 const int2* __restrict__ pend, const int* __restrict__ count,
                                                 int res, int g_row0, QueryList q) {
@@ -1019,20 +1005,7 @@ __global__ void MFB_INTERP_BOUNDS k_interp(const RasterFace* __restrict__ rf,
   int2 nxt = i < n ? pend[i] : make_int2(0, 0);
   for (; i < n; i += stride) {
     const int2 tf = nxt;
-#if MFB_INTERP_PF
-    // software pipelining: the next query's pair now, its face records into L1
-    if (i + stride < n) {
-      nxt = pend[i + stride];
-      const char* a = reinterpret_cast<const char*>(rf + nxt.y);
-      const char* b = reinterpret_cast<const char*>(attrs + nxt.y);
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(a));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(a + 128));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(b));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(b + 128));
-    }
-#else
     if (i + stride < n) nxt = pend[i + stride];
-#endif
     const int yr = tf.x / res, x = tf.x - yr * res;
     const double cx = x + 0.5, cy = (yr + g_row0) + 0.5;
     if (!attrs[tf.y].reliable) {  // gbuffer.cpp:218-227: not a query; texel id stored as ~gi
@@ -1041,7 +1014,7 @@ __global__ void MFB_INTERP_BOUNDS k_interp(const RasterFace* __restrict__ rf,
     }
     float P[3], Nf[3], Tf[3], Bf[3];
     interp_texel(rf[tf.y], attrs[tf.y], cx, cy, P, Nf, Tf, Bf);
-    store_query(q, i, false, tf.x, P, Nf, Tf, Bf);
+    store_query(q, i, tf.x, P, Nf, Tf, Bf);
   }
 }
 
@@ -1552,7 +1525,7 @@ void raster_gbuffer(Ctx& ctx, cudaStream_t s, const DevMesh& lo, const RasterPla
 bool raster_links_supported() {
   static const bool split = [] {
     const char* e = std::getenv("MFB_RASTER_SPLIT");
-    return !(e && e[0] == '0') && !kSeedPasses;
+    return !(e && e[0] == '0');
   }();
   return split;
 }

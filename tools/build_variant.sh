@@ -1,7 +1,7 @@
 #!/bin/bash
 # Build libmfbake.so with extra compile flags into build/var/<name>/ for A/B
 # timing through MFB_LIB (e.g. MFB_LIB=build/var/pf1/libmfbake.so python bench.py).
-#   tools/build_variant.sh pf1 -DMFB_PF=1
+#   tools/build_variant.sh minb7 -DMFB_XFER_T_MINB=7
 set -e
 cd "$(dirname "$0")/.."
 name=$1; shift
