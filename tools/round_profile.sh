@@ -26,3 +26,8 @@ TAG=$TAG bash tools/ncu_all.sh
 timeout 300 python tools/timeline.py B 7 2>/dev/null | grep -v Warn > $OUT/${TAG}_timeline_B.txt
 TL_E2E=1 timeout 300 python tools/timeline.py B 7 2>/dev/null | grep -v Warn > $OUT/${TAG}_timeline_e2e.txt
 TAG=$TAG bash tools/configs_run.sh
+# config E's wide-leaf kernels (triangle planes in the repack, leaf planes, the wide transfer)
+M=$(python -c "import sys; sys.path.insert(0, 'tools'); import ncu_summary as n; print(','.join(n.METRICS))")
+timeout 900 ncu --metrics $M --clock-control none --csv --page raw -k 'regex:k_repack|k_leaf_planes|k_transfer_t' -c 3 \
+  --log-file $OUT/${TAG}_E_metrics.csv python bench.py --config E --steps 1 --warmup 1 --no-e2e --no-cpu-baseline \
+  --no-rays > $OUT/${TAG}_ncu_E.log 2>&1; echo "E metrics rc=$?"
