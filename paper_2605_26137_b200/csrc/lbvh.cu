@@ -328,33 +328,28 @@ __device__ void tri_planes(const double* v, TPlane& tp) {
   }
 }
 
-// LPlane of the leaf [first, first + count) of leaf-order triangles.
-__device__ void leaf_plane(const BTri* __restrict__ tris, int first, int count, LPlane& lp) {
-  double s[3] = {0.0, 0.0, 0.0}, sa = 0.0, e0[3] = {0.0, 0.0, 0.0};
-  for (int t = 0; t < count; ++t) {
-    const double* v = tris[first + t].v;
-    const double a[3] = {v[3] - v[0], v[4] - v[1], v[5] - v[2]};
-    const double b[3] = {v[6] - v[0], v[7] - v[1], v[8] - v[2]};
-    const double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
-    s[0] += c[0];
-    s[1] += c[1];
-    s[2] += c[2];
-    sa += sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
-    if (t == 0) {
-      e0[0] = a[0];
-      e0[1] = a[1];
-      e0[2] = a[2];
-    }
-  }
-  const double sl = sqrt(s[0] * s[0] + s[1] * s[1] + s[2] * s[2]);
+// Area vector (b - a) x (c - a) of one leaf-order triangle, and its first edge.
+__device__ __forceinline__ void tri_area(const double* v, double c[3], double e[3]) {
+  e[0] = v[3] - v[0];
+  e[1] = v[4] - v[1];
+  e[2] = v[5] - v[2];
+  const double b[3] = {v[6] - v[0], v[7] - v[1], v[8] - v[2]};
+  c[0] = e[1] * b[2] - e[2] * b[1];
+  c[1] = e[2] * b[0] - e[0] * b[2];
+  c[2] = e[0] * b[1] - e[1] * b[0];
+}
+// The LPlane frame from a patch's summed area vector s, its summed area
+// magnitudes sa and one edge e0: false (zero record) for a folded or
+// degenerate patch.
+__device__ bool plane_frame(const double s[3], double sa, const double e0[3], LPlane& lp) {
   lp = LPlane{};
-  // a folded or degenerate patch: no usable frame (a zero record never skips)
-  if (!(sl > 1e-3 * sa) || !isfinite(sl)) return;
+  const double sl = sqrt(s[0] * s[0] + s[1] * s[1] + s[2] * s[2]);
+  if (!(sl > 1e-3 * sa) || !isfinite(sl)) return false;
   const double n[3] = {s[0] / sl, s[1] / sl, s[2] / sl};
   const double en = e0[0] * n[0] + e0[1] * n[1] + e0[2] * n[2];
   double u[3] = {e0[0] - en * n[0], e0[1] - en * n[1], e0[2] - en * n[2]};
   const double ul = sqrt(u[0] * u[0] + u[1] * u[1] + u[2] * u[2]);
-  if (!(ul > 0.0) || !isfinite(ul)) return;
+  if (!(ul > 0.0) || !isfinite(ul)) return false;
   for (int k = 0; k < 3; ++k) u[k] /= ul;
   const double v[3] = {n[1] * u[2] - n[2] * u[1], n[2] * u[0] - n[0] * u[2], n[0] * u[1] - n[1] * u[0]};
   for (int k = 0; k < 3; ++k) {
@@ -362,24 +357,100 @@ __device__ void leaf_plane(const BTri* __restrict__ tris, int first, int count, 
     lp.u[k] = static_cast<float>(u[k]);
     lp.v[k] = static_cast<float>(v[k]);
   }
-  double r[3][2] = {{INFINITY, -INFINITY}, {INFINITY, -INFINITY}, {INFINITY, -INFINITY}};
+  return true;
+}
+// Extends r[d] = [min, max] of the three rounded directions' projections by
+// one triangle's vertices (f64 products of the fp32 directions).
+__device__ __forceinline__ void plane_ranges(const LPlane& lp, const double* x, double r[3][2]) {
   const float* dir[3] = {lp.n, lp.u, lp.v};
-  for (int t = 0; t < count; ++t) {
-    const double* x = tris[first + t].v;
-    for (int c = 0; c < 3; ++c)
-      for (int d = 0; d < 3; ++d) {
-        const double p = (static_cast<double>(dir[d][0]) * x[3 * c] + static_cast<double>(dir[d][1]) * x[3 * c + 1]) +
-                         static_cast<double>(dir[d][2]) * x[3 * c + 2];
-        r[d][0] = fmin(r[d][0], p);
-        r[d][1] = fmax(r[d][1], p);
-      }
-  }
+  for (int c = 0; c < 3; ++c)
+    for (int d = 0; d < 3; ++d) {
+      const double p = (static_cast<double>(dir[d][0]) * x[3 * c] + static_cast<double>(dir[d][1]) * x[3 * c + 1]) +
+                       static_cast<double>(dir[d][2]) * x[3 * c + 2];
+      r[d][0] = fmin(r[d][0], p);
+      r[d][1] = fmax(r[d][1], p);
+    }
+}
+__device__ __forceinline__ void plane_store_ranges(LPlane& lp, const double r[3][2]) {
   lp.lo = __double2float_rd(r[0][0]);
   lp.hi = __double2float_ru(r[0][1]);
   lp.umin = __double2float_rd(r[1][0]);
   lp.umax = __double2float_ru(r[1][1]);
   lp.vmin = __double2float_rd(r[2][0]);
   lp.vmax = __double2float_ru(r[2][1]);
+}
+
+// LPlane of the leaf [first, first + count) of leaf-order triangles.
+__device__ void leaf_plane(const BTri* __restrict__ tris, int first, int count, LPlane& lp) {
+  double s[3] = {0.0, 0.0, 0.0}, sa = 0.0, e0[3] = {0.0, 0.0, 0.0};
+  for (int t = 0; t < count; ++t) {
+    double c[3], e[3];
+    tri_area(tris[first + t].v, c, e);
+    s[0] += c[0];
+    s[1] += c[1];
+    s[2] += c[2];
+    sa += sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    if (t == 0) {
+      e0[0] = e[0];
+      e0[1] = e[1];
+      e0[2] = e[2];
+    }
+  }
+  if (!plane_frame(s, sa, e0, lp)) return;
+  double r[3][2] = {{INFINITY, -INFINITY}, {INFINITY, -INFINITY}, {INFINITY, -INFINITY}};
+  for (int t = 0; t < count; ++t) plane_ranges(lp, tris[first + t].v, r);
+  plane_store_ranges(lp, r);
+}
+
+// One warp per reachable internal node (the segment-tree build lists them
+// all): its own oriented box when its range holds <= kNodePlaneMax
+// triangles. Lanes stride over the range; the frame comes from lane 0's
+// reduced sums (every lane then uses the same rounded directions), the
+// ranges reduce exactly (min / max).
+__device__ void node_plane(const BNode* __restrict__ nodes, const BTri* __restrict__ tris, int i, int lane,
+                           LPlane* __restrict__ nplane) {
+  const int4 d = nodes[i].d;
+  LPlane lp{};
+  if (d.w <= kNodePlaneMax) {
+    double s[3] = {0.0, 0.0, 0.0}, sa = 0.0;
+    for (int t = lane; t < d.w; t += 32) {
+      double c[3], e[3];
+      tri_area(tris[d.z + t].v, c, e);
+      s[0] += c[0];
+      s[1] += c[1];
+      s[2] += c[2];
+      sa += sqrt(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      s[0] += __shfl_xor_sync(0xffffffffu, s[0], off);
+      s[1] += __shfl_xor_sync(0xffffffffu, s[1], off);
+      s[2] += __shfl_xor_sync(0xffffffffu, s[2], off);
+      sa += __shfl_xor_sync(0xffffffffu, sa, off);
+    }
+    for (int k = 0; k < 3; ++k) s[k] = __shfl_sync(0xffffffffu, s[k], 0);
+    sa = __shfl_sync(0xffffffffu, sa, 0);
+    double c[3], e0[3];
+    tri_area(tris[d.z].v, c, e0);
+    if (plane_frame(s, sa, e0, lp)) {
+      double r[3][2] = {{INFINITY, -INFINITY}, {INFINITY, -INFINITY}, {INFINITY, -INFINITY}};
+      for (int t = lane; t < d.w; t += 32) plane_ranges(lp, tris[d.z + t].v, r);
+      for (int off = 16; off > 0; off >>= 1)
+        for (int k = 0; k < 3; ++k) {
+          r[k][0] = fmin(r[k][0], __shfl_xor_sync(0xffffffffu, r[k][0], off));
+          r[k][1] = fmax(r[k][1], __shfl_xor_sync(0xffffffffu, r[k][1], off));
+        }
+      plane_store_ranges(lp, r);
+    }
+  }
+  if (lane == 0) nplane[i] = lp;
+}
+__global__ void k_node_planes(const BNode* __restrict__ nodes, const BTri* __restrict__ tris,
+                              const int32_t* __restrict__ list, const int* __restrict__ list_n,
+                              LPlane* __restrict__ nplane) {
+  const int lane = threadIdx.x & 31, nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+  const int cnt = *list_n;
+  for (int w = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5); w < cnt; w += nw)  // warp-uniform
+    node_plane(nodes, tris, list[w], lane, nplane);
 }
 
 // One thread per listed node (every reachable node with a leaf child is in
@@ -763,6 +834,15 @@ int lbvh_leaf_max(int leaf_hint) {
   return leaf_env ? leaf_env : (leaf_hint >= 1 && leaf_hint <= kLeafCountMax ? leaf_hint : kLeafMaxDefault);
 }
 
+// segment-tree node boxes (MFB_SEGTREE=0: the bottom-up refit climb)
+static bool lbvh_segtree() {
+  static const bool on = [] {
+    const char* e = std::getenv("MFB_SEGTREE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag, int leaf_hint) {
   out.leaf_max = lbvh_leaf_max(leaf_hint);
   const int n = m.nf;
@@ -783,6 +863,8 @@ void lbvh_layout(Ctx& ctx, const DevMesh& m, Lbvh& out, const std::string& tag, 
   const bool planes = plane_env < 0 ? out.leaf_max >= kPlaneLeafMin : plane_env != 0;
   out.tplane = planes ? ctx.buf<TPlane>(tag + ".tplane", n) : nullptr;
   out.lplane = planes ? ctx.buf<LPlane>(tag + ".lplane", n) : nullptr;
+  // node boxes need every reachable node listed (the segment-tree build's list)
+  out.nplane = planes && n > 1 && lbvh_segtree() ? ctx.buf<LPlane>(tag + ".nplane", n - 1) : nullptr;
   out.root_box_dev = ctx.buf<float>(tag + ".rootbox", 8);
   out.root_ref = n > 1 ? 0 : leaf_ref(0, 1);
   out.scene_acc = ctx.buf<unsigned long long>(tag + ".acc", 8);
@@ -810,11 +892,7 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   k_acc_init<<<1, 1024, 0, s>>>(acc, hist);
   ctx.count_launch();
   // segment-tree node boxes (MFB_SEGTREE=0: the bottom-up refit climb)
-  static const bool segtree = [] {
-    const char* e = std::getenv("MFB_SEGTREE");
-    return !(e && e[0] == '0');
-  }();
-  const bool use_seg = segtree && n > 1;
+  const bool use_seg = lbvh_segtree() && n > 1;
   if (out.n_nodes > 0 && !use_seg) ctx.fill(flags, 0, sizeof(int) * out.n_nodes, s);
 
   const int T = 256;
@@ -882,6 +960,10 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   ctx.count_launch(2);
   if (out.lplane) {  // after the boxes: the list and the child refs are final
     k_leaf_planes<<<div_up(std::max(n - 1, 1), T), T, 0, s>>>(out.nodes, out.tris, starts, starts_n, n, out.lplane);
+    ctx.count_launch();
+  }
+  if (out.nplane) {
+    k_node_planes<<<kNumSMs * 8, T, 0, s>>>(out.nodes, out.tris, starts, starts_n, out.nplane);
     ctx.count_launch();
   }
   MFB_CUDA_TRY(cudaGetLastError());

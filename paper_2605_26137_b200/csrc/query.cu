@@ -444,7 +444,8 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
     unsigned long long* __restrict__ prof_out, const double* __restrict__ hiPos = nullptr,
     const int* __restrict__ dep_head = nullptr,
     const int* __restrict__ dep_next = nullptr, BandSync bands = BandSync{}, int fmt = MF_ATLAS_RGB8,
-    const TPlane* __restrict__ tplane = nullptr, const LPlane* __restrict__ lplane = nullptr) {
+    const TPlane* __restrict__ tplane = nullptr, const LPlane* __restrict__ lplane = nullptr,
+    const LPlane* __restrict__ nplane = nullptr) {
   const int nq = qcount[0];
   const int lane = threadIdx.x & 31;
   if (kProf && lane == 0) {
@@ -497,6 +498,11 @@ __global__ void MFB_XFER_T_BOUNDS k_transfer_t(
         float4 a, b, c;
         int4 d;
         ld_node(nodes + ref, a, b, c, d);
+        // wide searches: the node's own oriented box (loaded beside the node)
+        if (!kSel && nplane && leaf_skip(nplane + ref, qf, bnd, E)) {
+          ref = pop_within(st_ref, st_lb, sp, bnd);
+          continue;
+        }
         float lbL, lbR;
         box_lb2(a, b, c, qf, lbL, lbR);
         const bool hL = lbL <= bnd, hR = lbR <= bnd;
@@ -1240,12 +1246,12 @@ void transfer_normals(Ctx& ctx, cudaStream_t s, const Lbvh& bvh, const TransferA
       k_transfer_t<D, P, BANDS, true><<<g2, 128, 0, s>>>(                                                     \
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
           a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
-          a.hi_positions, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane);                    \
+          a.hi_positions, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane, bvh.nplane);                    \
     else                                                                                                      \
       k_transfer_t<D, P, BANDS, false><<<g2, 128, 0, s>>>(                                                    \
           bvh.nodes, bvh.tris, bvh.root_ref, bvh.scene_acc, a.q.qpos, a.q.qtbn, a.q.count, a.hi_normals,      \
           a.hi_faces, a.max_dist, a.rgb, D ? a.dbg_face : nullptr, D ? a.dbg_ts : nullptr, a.counters, pbuf,  \
-          a.hi_positions, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane);                    \
+          a.hi_positions, a.dep_head, a.dep_next, a.bands, a.fmt, bvh.tplane, bvh.lplane, bvh.nplane);                    \
   } while (0)
   // the row-band publication is compiled only into the host path's
   // instantiation (it costs the walk registers)
