@@ -163,7 +163,12 @@ void Ctx::fill(void* p, int value, size_t bytes, cudaStream_t s) {
 HostPool& Ctx::host_pool() {
   if (!pool) {
     const unsigned hw = std::thread::hardware_concurrency();
-    pool = new HostPool(static_cast<int>(std::min(8u, std::max(2u, hw / 2))));
+    const char* e = std::getenv("MFB_HOST_THREADS");
+    const int want = e ? std::atoi(e) : 0;
+    // (MFB_HOST_THREADS overrides) 5 on the 16-core box: pageable e2e at config
+    // B 2.08 ms with 5 threads, 2.09-2.17 with 4, 2.12-2.25 with 8, 2.43-2.50
+    // with 12-16 (the staging copies contend for host memory bandwidth)
+    pool = new HostPool(want > 0 ? want : static_cast<int>(std::min(5u, std::max(2u, hw / 3))));
   }
   return *pool;
 }
