@@ -44,11 +44,11 @@ $(PKG)/libmeshforge_b200.so: $(PKG)/cpp/meshforge_b200.cpp $(PKG)/cpp/io_b200.cp
 
 build/test_bake_b200: tests/cpp/test_bake_b200.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so
 	@mkdir -p build
-	$(CXX) $(CXXFLAGS) -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+	$(CXX) $(CXXFLAGS) -pthread -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 build/test_io_cpu: tests/cpp/test_io_cpu.cpp tests/cpp/doctest.h $(PKG)/libmeshforge_b200.so
 	@mkdir -p build
-	$(CXX) $(CXXFLAGS) -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+	$(CXX) $(CXXFLAGS) -pthread -Itests/cpp -o $@ $< -L$(PKG) -lmeshforge_b200 -lmfbake -Wl,-rpath,'$$ORIGIN/../$(PKG)'
 
 # end-to-end timing of the reference-facing C++ API (bench.py e2e_api)
 build/bench_api: tools/bench_api.cpp $(PKG)/libmeshforge_b200.so

@@ -198,23 +198,33 @@ Image<std::uint16_t> bakeNormalMapRG16(const TriangleMesh& lowpoly, const Triang
 }
 
 // ------------------------------------------------------------------ Bvh
+// A tree owns its context (stream + query scratch) instead of borrowing the
+// building thread's: the reference queries one const Bvh from many threads
+// (metrics.cpp: toBvh.closestPoint inside parallelChunks) and a Bvh may outlive
+// the thread that built it. `mu` serialises every query on the shared scratch.
 struct Bvh::Handle {
+  mf_ctx* ctx = nullptr;
   mf_mesh* mesh = nullptr;
   mf_bvh* bvh = nullptr;
   Aabb3d box;
   bool exported = false;
-  std::mutex mu;
+  mutable std::mutex mu;
   ~Handle() {
     if (bvh) mf_bvh_destroy(bvh);
     if (mesh) mf_mesh_destroy(mesh);
+    if (ctx) mf_ctx_destroy(ctx);
   }
 };
+
+static std::unique_lock<std::mutex> lockTree(const Bvh& bvh) { return std::unique_lock<std::mutex>(bvh.handle()->mu); }
 
 Bvh::Bvh(const TriangleMesh& mesh) : mesh_(&mesh), h_(std::make_shared<Handle>()) {
   validateMesh(mesh);  // Bvh::Bvh validates first (bvh.cpp:49)
   const mf_mesh_view v = viewOf(mesh);
-  check(mf_mesh_upload(context(), &v, &h_->mesh));
-  check(mf_bvh_build(context(), h_->mesh, &h_->bvh));
+  const char* dev = std::getenv("MFB_DEVICE");
+  check(mf_ctx_create(dev ? std::atoi(dev) : 0, nullptr, &h_->ctx));
+  check(mf_mesh_upload(h_->ctx, &v, &h_->mesh));
+  check(mf_bvh_build(h_->ctx, h_->mesh, &h_->bvh));
 }
 
 SurfacePoint Bvh::closestPointWithin(const Eigen::Vector3d& query, double maxDistance) const {
@@ -231,9 +241,11 @@ std::vector<SurfacePoint> Bvh::closestPointsWithin(const std::vector<Eigen::Vect
   std::vector<int32_t> face(n);
   std::vector<double> ds(n);
   std::vector<Eigen::Vector3d> pt(n), bary(n);
-  if (n)
+  if (n) {
+    const auto lock = lockTree(*this);
     check(mf_bvh_closest_within(h_->bvh, q.data()->data(), n, maxDistance, face.data(), ds.data(),
                                 pt.data()->data(), bary.data()->data()));
+  }
   std::vector<SurfacePoint> out(n);
   for (int64_t i = 0; i < n; ++i) out[i] = SurfacePoint{face[i], ds[i], pt[i], bary[i]};
   return out;
@@ -249,9 +261,11 @@ std::vector<RayHit> Bvh::raycastFirstBatch(const std::vector<Eigen::Vector3d>& o
   const int64_t n = static_cast<int64_t>(std::min(o.size(), d.size()));
   std::vector<int32_t> face(n);
   std::vector<double> t(n), u(n), v(n);
-  if (n)
+  if (n) {
+    const auto lock = lockTree(*this);
     check(mf_bvh_raycast_first(h_->bvh, o.data()->data(), d.data()->data(), n, tMin, tMax, face.data(), t.data(),
                                u.data(), v.data()));
+  }
   std::vector<RayHit> out(n);
   for (int64_t i = 0; i < n; ++i) out[i] = RayHit{face[i], t[i], u[i], v[i]};
   return out;
@@ -328,6 +342,7 @@ SignGrid markSurfaceBand(const TriangleMesh& mesh, const Bvh& bvh, const GridPar
   const std::size_t cells = res >= 8 ? static_cast<std::size_t>(res) * res * res : 1;
   labels.resize(cells);
   g.distance.resize(cells);
+  const auto lock = lockTree(bvh);
   check(mf_surface_band(bvh.handle()->bvh, res, params.bandVoxels, params.dilateRadius,
                         params.domain ? dom : nullptr, labels.data(), g.distance.data(), grid));
   g.res = res;
@@ -365,6 +380,7 @@ std::vector<double> sampleSdf(const WatertightResult& wt, const Bvh& watertightB
   if (wt.field.size() != wt.grid.cells())
     throw Error(ErrorCode::ShapeMismatch, "signed field does not match the grid");
   const double origin[3] = {wt.grid.origin.x(), wt.grid.origin.y(), wt.grid.origin.z()};
+  const auto lock = lockTree(watertightBvh);
   check(mf_sample_sdf(watertightBvh.handle()->bvh, wt.grid.res, origin, wt.grid.voxelSize, wt.field.data(),
                       points.data()->data(), static_cast<int64_t>(points.size()), values.data()));
   return values;
