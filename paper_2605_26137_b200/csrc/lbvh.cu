@@ -476,6 +476,10 @@ __global__ void k_leaf_planes(const BNode* __restrict__ nodes, const BTri* __res
   }
 }
 
+// (kPlanes: the wide-leaf instantiation; the plane arithmetic costs the
+// gather its occupancy, 72 vs 32 registers, so the leaf-<=3 trees
+// of configs A-D run the plain one)
+template <bool kPlanes>
 __global__ void k_repack(const double* __restrict__ pos, const int32_t* __restrict__ faces,
                          const uint32_t* __restrict__ order, int n, BTri* __restrict__ tris,
                          TBox* __restrict__ tbox, TPlane* __restrict__ tplane) {
@@ -508,7 +512,7 @@ __global__ void k_repack(const double* __restrict__ pos, const int32_t* __restri
   for (int q = 0; q < 5; ++q) dst[q] = src[q];
   tbox[p].a = make_float4(box.mn[0], box.mn[1], box.mn[2], box.mx[0]);
   tbox[p].b = make_float4(box.mx[1], box.mx[2], 0.f, 0.f);
-  if (tplane) {
+  if (kPlanes) {
     TPlane tp;
     tri_planes(t.v, tp);
     tplane[p] = tp;
@@ -613,6 +617,7 @@ __global__ void __launch_bounds__(1024) k_seg_up(TBox* __restrict__ seg, int L) 
 #endif
 // One thread per reachable node, from emit's compacted list (full warps of
 // range queries instead of one active lane in three).
+// (72 registers, 3 CTAs of 256 per SM; capped at 64 / 48 registers: 1.437 / 1.474 vs 1.425 ms per bake)
 __global__ void k_node_boxes(const TBox* __restrict__ seg, const TBox* __restrict__ tbox, int N, int n, int leaf_max,
                              BNode* __restrict__ nodes, float* __restrict__ root_box,
                              const int32_t* __restrict__ reach, const int* __restrict__ reach_n) {
@@ -918,6 +923,12 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
   // repack (gathers) and emit (key searches) both need only the sorted
   // keys / ids: repack runs on the context's helper stream alongside emit
   cudaStream_t rs = ctx.side2 ? ctx.side2 : s;
+  auto repack = [&](cudaStream_t st) {
+    if (out.tplane)
+      k_repack<true><<<div_up(n, T), T, 0, st>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox, out.tplane);
+    else
+      k_repack<false><<<div_up(n, T), T, 0, st>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox, nullptr);
+  };
   if (rs != s) {
     MFB_CUDA_TRY(cudaEventRecord(ctx.lfork, s));
     MFB_CUDA_TRY(cudaStreamWaitEvent(rs, ctx.lfork, 0));
@@ -931,12 +942,12 @@ void lbvh_build(Ctx& ctx, cudaStream_t s, const DevMesh& m, Lbvh& out, const std
     // (the repack fused with the first seg levels in 1024-thread CTAs measured
     // slower: the 256-thread gather runs at full occupancy)
     int launches = 2;
-    k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox, out.tplane);
+    repack(rs);
     launch_pdl(k_seg_leaves, div_up(N, 1024), 1024, 0, rs, out.tbox, n, N, seg);
     for (int L = N >> 10; L > 1; L >>= 10, ++launches) launch_pdl(k_seg_up, div_up(L, 1024), 1024, 0, rs, seg, L);
     ctx.count_launch(launches - 1);
   } else {
-    k_repack<<<div_up(n, T), T, 0, rs>>>(m.pos, m.faces, vals2, n, out.tris, out.tbox, out.tplane);
+    repack(rs);
   }
   if (rs != s) MFB_CUDA_TRY(cudaEventRecord(ctx.ljoin, rs));
   if (n > 1) {

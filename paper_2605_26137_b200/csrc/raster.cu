@@ -995,6 +995,7 @@ __device__ __forceinline__ void interp_texel(const RasterFace& sfc, const AttrFa
 // Split raster, second kernel: one thread per compacted query (texel, face)
 // written by k_raster<2>; interpolates exactly as the fused path and writes
 // the same query record. No barriers, full SIMT width for the f64 chain.
+// (__launch_bounds__(256, 5 | 6): 48 / 40 registers, 1.425 / 1.439 vs 1.425 ms per bake at B)
 __global__ void __launch_bounds__(256) k_interp(const RasterFace* __restrict__ rf,
                                                 const AttrFace* __restrict__ attrs,
                                                 const int2* __restrict__ pend, const int* __restrict__ count,
