@@ -1202,6 +1202,7 @@ bool host_pinned(const void* p) {
 // (:157-159), then transferNormals' checks (:195-199), then dilateSeams' (:255).
 void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const mf_mesh_view* hv, int res,
                           double diag, double frac, int radius, uint8_t* rgb_out, mf_bake_stats* st) {
+  HostTrace ht("bake_host");
   cudaStream_t s = c.stream;
   mf_mesh lo, hi;
   lo.ctx = hi.ctx = owner;
@@ -1277,11 +1278,16 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     c.sync_all();
   };
   try {
+    ht.mark("entry");
     upload_mesh_async(c, s, lv, &lo, "up.lo", hup);
+    ht.mark("lowpoly queued");
     if (early) upload_hi();
+    ht.mark("dense upload q");
     MFB_CUDA_TRY(cudaStreamSynchronize(s));
+    ht.mark("lowpoly synced");
     finish_upload(&lo, hup[0]);
     check_lowpoly(&lo, res);
+    ht.mark("lowpoly checked");
     if (!rgb_out) throw ApiError(MF_ERR_BAD_ARGUMENT, "rgb_out is null");
   } catch (...) {
     drain();
@@ -1306,9 +1312,16 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     q.bs.ready = bb + 3 * kMaxBands;
     q.bs.res = res;
     // ~32 bands (64 rows at 2048^2): the copy left after the transfer is one
-    // small band (16 or 64 bands measured 15-19 us slower end to end)
+    // small band (16 or 64 bands measured 15-19 us slower end to end). Each
+    // band's wait + copy costs the band stream ~11 us whatever its size, so
+    // small atlases (a short transfer) get bands of >= kMinBandBytes: at
+    // 512^2, 32 bands of 24 KB queued ~320 us of band copies behind a 96 us
+    // transfer (config A end to end 0.69 ms)
     constexpr int band_div = 32;
-    q.bs.rows = std::max((div_up(res, band_div) + 15) / 16 * 16, (radius + 15) / 16 * 16);
+    constexpr int64_t kMinBandBytes = 256 << 10;
+    const int64_t row_bytes = static_cast<int64_t>(atlas_bpp(c.fmt)) * res;
+    const int min_rows = static_cast<int>(std::min<int64_t>(res, div_up(kMinBandBytes, row_bytes)));
+    q.bs.rows = std::max({(div_up(res, band_div) + 15) / 16 * 16, (min_rows + 15) / 16 * 16, (radius + 15) / 16 * 16});
     q.bs.nb = div_up(res, q.bs.rows);
     const char* chk = std::getenv("MFB_BAND_CHECK");
     if (chk && chk[0] == '1') q.band_check = static_cast<int*>(c.host_buf("bake.bandcheck", kMaxBands * sizeof(int)));
@@ -1330,6 +1343,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
                          q.band_sync ? 1 : 0, radius, c.fmt};
     run_graphed(c, c.g_low, s, key_bytes(k), use_graphs, [&] { q.low(); });
   }
+  ht.mark("low queued");
   if (!early) upload_hi();
   // Speculative dense phase: the LBVH / normals / transfer are queued right
   // behind the dense upload and its validation (which zeroes out-of-range
@@ -1354,8 +1368,10 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
     throw ApiError(MF_ERR_INVALID_CONFIG, "InvalidConfig: dilation radius must be >= 0");
   }
   q.dense_side(use_graphs);
+  ht.mark("dense queued");
   cudaEvent_t t2 = tm.mark(s);
   q.tail(hflags, hcnt, host_dst);
+  ht.mark("tail queued");
   const int64_t row_bytes = static_cast<int64_t>(bpp) * res;
   if (stage_out && q.band_sync) {
     const int dev = c.device, nb = q.bs.nb, rows = q.bs.rows;
@@ -1375,6 +1391,7 @@ void bake_host_overlapped(Ctx& c, mf_ctx* owner, const mf_mesh_view* lv, const m
   }
   cudaEvent_t t3 = tm.mark(s);
   MFB_CUDA_TRY(cudaStreamSynchronize(s));
+  ht.mark("synced");
   if (stage_out) {
     if (q.band_sync) {
       pool_job.wait();
