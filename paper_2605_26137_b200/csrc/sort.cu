@@ -31,9 +31,14 @@ constexpr int kDigitBits = 10;
 constexpr int kBins = 1 << kDigitBits;
 constexpr int kSortThreads = 512;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kPerLane = 16;                          // keys per thread (8 measured equal)
-constexpr int kTile = kSortThreads * kPerLane;         // 8192 keys per tile
-constexpr int kWarpKeys = 32 * kPerLane;               // 512 keys per warp
+// Keys per thread: 16 (8192-key tiles) for large sorts; 4 (2048-key tiles)
+// up to kSmallSortKeys, where a pass is one short wave of few tiles and the
+// per-CTA latency is the pass time. Measured per bake (ms): config B (1M keys)
+// 16 / 8 / 4: 1.424 / 1.434 / 1.439; config D (500k) 0.481 / 0.485 / 0.480;
+// config A (200k) 0.237 / 0.234 / 0.218.
+constexpr int kPerLaneLarge = 16;
+constexpr int kPerLaneSmall = 4;
+constexpr int kSmallSortKeys = 1 << 18;
 constexpr uint32_t kFlagAgg = 1u << 30, kFlagInc = 2u << 30, kCountMask = (1u << 30) - 1u;
 
 // Look-back status words: relaxed GPU-scope loads / stores as volatile asm.
@@ -48,7 +53,9 @@ __device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+template <int kPerLane>
 struct SortSmem {
+  static constexpr int kTile = kSortThreads * kPerLane;
   uint16_t warp_hist[kSortWarps][kBins];  // per-warp digit counts -> per-warp exclusive prefix
   int tile_start[kBins];                  // exclusive scan of the tile's digit counts
   int out_off[kBins];                     // global destination of the digit's first tile element
@@ -87,12 +94,15 @@ __device__ __forceinline__ void block_scan_pairs(int& lo, int& hi, int* carry) {
   __syncthreads();
 }
 
+template <int kPerLane>
 __global__ void __launch_bounds__(kSortThreads, kPerLane <= 8 ? 3 : 2)
     k_onesweep(const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, uint32_t* __restrict__ kout,
                uint32_t* __restrict__ vout, int n, int shift, const int* __restrict__ ghist,
                uint32_t* __restrict__ status, int* __restrict__ tile_counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+  constexpr int kTile = kSortThreads * kPerLane;  // keys per tile
+  constexpr int kWarpKeys = 32 * kPerLane;        // keys per warp
+  SortSmem<kPerLane>& sm = *reinterpret_cast<SortSmem<kPerLane>*>(smem_raw);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   pdl_wait();
   if (threadIdx.x == 0) sm.tile_id = atomicAdd(tile_counter, 1);
@@ -292,29 +302,41 @@ __global__ void k_zero_u32(uint32_t* __restrict__ p, int64_t n) {
 
 }  // namespace
 
-int64_t sort_status_words(int n) { return static_cast<int64_t>(3) * div_up(std::max(n, 1), kTile) * kBins + 8; }
+static int sort_tile_keys(int n) { return kSortThreads * (n <= kSmallSortKeys ? kPerLaneSmall : kPerLaneLarge); }
 
-void radix_sort_morton30(Ctx& ctx, cudaStream_t s, const SortArgs& a) {
+int64_t sort_status_words(int n) {
+  return static_cast<int64_t>(3) * div_up(std::max(n, 1), sort_tile_keys(n)) * kBins + 8;
+}
+
+template <int kPerLane>
+static void onesweep_passes(cudaStream_t s, const SortArgs& a) {
   const int n = a.n;
-  if (n <= 0) return;
-  static const size_t smem = sizeof(SortSmem);
+  static const size_t smem = sizeof(SortSmem<kPerLane>);
   static bool attr = [] {
-    MFB_CUDA_TRY(cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MFB_CUDA_TRY(cudaFuncSetAttribute(k_onesweep<kPerLane>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     return true;
   }();
   (void)attr;
-  const int tiles = div_up(n, kTile);
+  const int tiles = div_up(n, kSortThreads * kPerLane);
   uint32_t* kin = a.keys;
   uint32_t* vin = a.vals;
   uint32_t* kout = a.keys_alt;
   uint32_t* vout = a.vals_alt;
   for (int pass = 0; pass < 3; ++pass) {
     uint32_t* status = a.status + static_cast<int64_t>(pass) * tiles * kBins;
-    launch_pdl(k_onesweep, tiles, kSortThreads, smem, s, kin, vin, kout, vout, n, pass * kDigitBits,
+    launch_pdl(k_onesweep<kPerLane>, tiles, kSortThreads, smem, s, kin, vin, kout, vout, n, pass * kDigitBits,
                a.hist + pass * kBins, status, a.counters + pass);
     std::swap(kin, kout);
     std::swap(vin, vout);
   }
+}
+
+void radix_sort_morton30(Ctx& ctx, cudaStream_t s, const SortArgs& a) {
+  if (a.n <= 0) return;
+  if (a.n <= kSmallSortKeys)
+    onesweep_passes<kPerLaneSmall>(s, a);
+  else
+    onesweep_passes<kPerLaneLarge>(s, a);
   ctx.count_launch(3);
   MFB_CUDA_TRY(cudaGetLastError());
   // three passes: the sorted pairs end in keys_alt / vals_alt

@@ -1,6 +1,7 @@
 """GPU: the LBVH's hand-written radix sort (csrc/sort.cu) equals
-std::stable_sort on random 30-bit and 12-bit keys (single tile, tile
-boundaries, 1,003,520 keys), through tools/sort_check.cu."""
+std::stable_sort on random 30-bit and 12-bit keys (single tile, 2048- and
+8192-key tile boundaries, both sides of the small-sort threshold 2^18,
+1,003,520 keys), through tools/sort_check.cu."""
 import os
 import subprocess
 

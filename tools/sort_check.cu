@@ -81,7 +81,7 @@ static int run(int n, unsigned seed, int key_bits) {
 
 int main() {
   int fails = 0;
-  for (int n : {1, 2, 100, 8191, 8192, 8193, 20000, 100000, 1003520})
+  for (int n : {1, 2, 100, 2047, 2048, 2049, 8191, 8192, 8193, 20000, 100000, 200000, 262144, 262145, 1003520})
     for (int bits : {30, 12}) fails += run(n, 7u + n, bits);
   std::printf("%s\n", fails ? "FAILED" : "all ok");
   {  // timing: 1,003,520 random 30-bit keys, 20 sorts
