@@ -361,6 +361,7 @@ __device__ __forceinline__ bool tri_plane_skip(const TPlane* tp, float3 q, float
 
 // Leaf pre-test (Lbvh::lplane): the leaf's oriented box, same slack as
 // tri_plane_skip; skips every triangle of a leaf that cannot hold a winner.
+#pragma nv_diag_suppress 550  // the second load's padding lane is not used
 __device__ __forceinline__ bool leaf_skip(const LPlane* lp, float3 q, float bnd, float E) {
   const float* p = reinterpret_cast<const float*>(lp);
   float nx, ny, nz, lo, hi, ux, uy, uz, umin, umax, vx, vy, vz, vmin, vmax, pad;
@@ -380,6 +381,7 @@ __device__ __forceinline__ bool leaf_skip(const LPlane* lp, float3 q, float bnd,
   const float c = fmaxf(__fsub_rd(fmaxf(vmin - vq, vq - vmax), delta), 0.0f);
   return __fmaf_rd(c, c, __fmaf_rd(b, b, __fmul_rd(a, a))) > bnd;
 }
+#pragma nv_diag_default 550
 
 // Row-band completion (BandSync, bake.cuh). Band b is complete once all its
 // queries are done; its rows are final once b-1, b, b+1 (those that exist)
